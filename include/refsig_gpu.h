@@ -1,0 +1,161 @@
+/*
+ * refsig_gpu.h — C ABI of the B200-native MRC batch-similarity path.
+ *
+ * Drop-in boundary. The reference's API surface is the
+ * header-only C++ in proj/include/refsig/ (pure functions over value types,
+ * no batch API). This ABI adds the batch entry points the reference's callers
+ * (SPEC eval/cli, absent in the reference) would bind, one per reference
+ * operation it replaces:
+ *
+ *   refsig_gpu_count            NgramVector::from_entries / extract_3grams'
+ *                               sort+RLE (ngram.hpp:62-75, :170-178) per doc,
+ *                               + doc_freq + IDF (A3)
+ *   refsig_gpu_set_reference_*  Reference.partition_vectors (SPEC.md:261-267,
+ *                               :306-314) or K sampled reference docs
+ *   refsig_gpu_sign             sign using cosine
+ *                               (ngram.hpp:184-202)
+ *   refsig_gpu_mrc_pairs        compare over all i<j
+ *                               (sample_pairs "all")
+ *   refsig_gpu_simhash          simhash (simhash.hpp:35-45) with word_hash64
+ *                               (simhash.hpp:23-29) -> splitmix64 or a table
+ *   refsig_gpu_hamming_pairs    hamming (simhash.hpp:47) over all i<j
+ *   refsig_gpu_exact_pairs      cosine (ngram.hpp:184-202) over all i<j
+ *   refsig_gpu_pair_cosines     cosine for a caller-given pair list
+ *
+ * Conventions
+ *   - Status: 0 ok; 1 runtime failure (CUDA error, out of memory) — the
+ *     reference's std::runtime_error, CLI exit 1; 2 validation failure (bad
+ *     sizes, K = 0, id >= vocab, NULL pointers, call order) — the reference's
+ *     refsig::validation_error (error.hpp:8-14), CLI exit 2; 3 candidate
+ *     buffer overflow (runtime class): *out_count still holds the exact count
+ *     and the first `capacity` pairs were written.
+ *     refsig_gpu_last_error(ctx) describes the last non-zero status.
+ *   - Ownership: the caller owns every host buffer; the ABI copies in and out.
+ *     The context owns device memory; results stay device-resident between
+ *     calls (corpus -> counts -> signatures -> pairs).
+ *   - Threading: one context per host thread (no internal locking).
+ *   - Ordering: calls that only produce device-resident state are enqueued on
+ *     the context's stream and return without waiting; calls that write host
+ *     buffers or return counts synchronise. Errors from enqueued work are
+ *     reported by the next synchronising call.
+ *   - Determinism: pair outputs are sorted keys (i << 32 | j), identical for
+ *     any launch configuration.
+ *   - No CPU fallback: every compute entry point runs CUDA kernels built for
+ *     sm_100a; without a usable device refsig_gpu_create fails with 1.
+ */
+#ifndef REFSIG_GPU_H
+#define REFSIG_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define REFSIG_OK 0
+#define REFSIG_E_RUNTIME 1
+#define REFSIG_E_VALIDATION 2
+#define REFSIG_E_OVERFLOW 3
+
+/* Term weighting for documents and reference docs. */
+#define REFSIG_WEIGHT_TF 0    /* raw counts: the reference's GramCount.count (ngram.hpp:48-53) */
+#define REFSIG_WEIGHT_TFIDF 1 /* count * fl32(ln((1+N)/(1+df))+1) */
+
+typedef struct refsig_gpu_ctx refsig_gpu_ctx;
+
+/* ---- lifetime ------------------------------------------------------------ */
+int refsig_gpu_create(int device, refsig_gpu_ctx** out);
+void refsig_gpu_destroy(refsig_gpu_ctx* ctx);
+const char* refsig_gpu_last_error(const refsig_gpu_ctx* ctx);
+const char* refsig_gpu_version(void);
+/* Use an external cudaStream_t (e.g. the framework's current stream); NULL
+ * restores the context-owned stream. */
+int refsig_gpu_set_stream(refsig_gpu_ctx* ctx, void* cuda_stream);
+void* refsig_gpu_get_stream(const refsig_gpu_ctx* ctx);
+int refsig_gpu_synchronize(refsig_gpu_ctx* ctx);
+
+/* ---- corpus (A14 input) ---------------------------------------------------
+ * tokens[doc_off[n_docs]] term ids (< vocab) and doc_off[n_docs+1] (doc_off[0]
+ * = 0, non-decreasing), both HOST pointers; copied to HBM (async when the
+ * tokens are pinned). Resets counts, reference, signatures and fingerprints. */
+int refsig_gpu_load_corpus(refsig_gpu_ctx* ctx, const uint32_t* tokens, const uint64_t* doc_off, uint32_t n_docs,
+                           uint32_t vocab);
+/* Same, with tokens already resident in device memory (borrowed, must stay
+ * alive until the next load); doc_off is a host array (length metadata). */
+int refsig_gpu_load_corpus_device(refsig_gpu_ctx* ctx, const uint32_t* d_tokens, const uint64_t* doc_off,
+                                  uint32_t n_docs, uint32_t vocab);
+
+/* ---- K1: counts, df, idf (A2-A4) ------------------------------------------ */
+int refsig_gpu_count(refsig_gpu_ctx* ctx, int weight_mode);
+/* Compact CSR of the per-doc sorted (id,count) rows, exactly the reference's
+ * NgramVector::entries() per doc. rowptr[n_docs+1]; ids/counts hold `cap`
+ * entries; *nnz receives the total (REFSIG_E_OVERFLOW if nnz > cap). */
+int refsig_gpu_get_counts(refsig_gpu_ctx* ctx, uint64_t* rowptr, uint32_t* ids, uint32_t* counts, uint64_t cap,
+                          uint64_t* nnz);
+/* df[vocab] and idf32[vocab] (either may be NULL). */
+int refsig_gpu_get_df(refsig_gpu_ctx* ctx, uint32_t* df, float* idf32);
+/* 1/||w_d|| per doc (0 for an empty doc). */
+int refsig_gpu_get_inv_norm(refsig_gpu_ctx* ctx, float* inv_norm);
+
+/* ---- A5: reference vectors ------------------------------------------------- */
+/* K corpus docs (indices < n_docs) as references, weighted like the corpus. */
+int refsig_gpu_set_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_ids, uint32_t K);
+/* K explicit reference vectors (host CSR): vector k = term_ids[rowptr[k] ..
+ * rowptr[k+1]) with weights (NULL: all 1.0, the reference's count-1 partition
+ * vectors). Ids must be unique within a vector and < vocab. */
+int refsig_gpu_set_reference_vectors(refsig_gpu_ctx* ctx, uint32_t K, const uint64_t* rowptr, const uint32_t* term_ids,
+                                     const float* weights);
+/* Size of the compact reference table (terms in the union U). */
+int refsig_gpu_reference_union(refsig_gpu_ctx* ctx, uint32_t* out_u);
+
+/* ---- K2: signatures (A6) ---------------------------------------------------- */
+int refsig_gpu_sign(refsig_gpu_ctx* ctx);
+/* S[n_docs*K] row-major: S[d*K+k] = cosine(doc d, reference k). */
+int refsig_gpu_get_signatures(refsig_gpu_ctx* ctx, float* S);
+
+/* ---- K3: MRC all-pairs (A7) -------------------------------------------------
+ * All i<j with compare(S_i,S_j) >= tau. out_pairs: host buffer of `capacity`
+ * keys or NULL (keys stay on the device; count only). */
+int refsig_gpu_mrc_pairs(refsig_gpu_ctx* ctx, float tau, uint64_t* out_pairs, uint64_t capacity,
+                         uint64_t* out_count);
+
+/* ---- K4: Simhash + Hamming (A8-A10) -----------------------------------------
+ * weight_mode as above (TF reproduces the reference's per-occurrence rule).
+ * term_hash: optional HOST table of vocab 64-bit hashes (e.g. word_hash64 of
+ * each term's word); NULL uses splitmix64(seed, id) (Appendix A6). */
+int refsig_gpu_simhash(refsig_gpu_ctx* ctx, uint64_t seed, int weight_mode, const uint64_t* term_hash);
+int refsig_gpu_get_fingerprints(refsig_gpu_ctx* ctx, uint64_t* fp);
+int refsig_gpu_hamming_pairs(refsig_gpu_ctx* ctx, int max_dist, uint64_t* out_pairs, uint64_t capacity,
+                             uint64_t* out_count);
+
+/* ---- K5: exact cosine verifier (A12) ---------------------------------------- */
+int refsig_gpu_exact_pairs(refsig_gpu_ctx* ctx, float tau_cos, uint64_t* out_pairs, uint64_t capacity,
+                           uint64_t* out_count);
+/* Exact cosine (fp32) of the corpus' weighted vectors for n pair keys. */
+int refsig_gpu_pair_cosines(refsig_gpu_ctx* ctx, const uint64_t* keys, uint64_t n, float* out);
+
+/* ---- query-vs-database mode (configs[4]) -------------------------------------
+ * `db` holds the signed/fingerprinted database; `q` holds the query corpus,
+ * counted with the database's IDF and signed against its reference. */
+int refsig_gpu_attach_database(refsig_gpu_ctx* q, refsig_gpu_ctx* db);
+int refsig_gpu_mrc_query_pairs(refsig_gpu_ctx* q, float tau, uint64_t* out_pairs, uint64_t capacity,
+                               uint64_t* out_count);
+int refsig_gpu_hamming_query_pairs(refsig_gpu_ctx* q, int max_dist, uint64_t* out_pairs, uint64_t capacity,
+                                   uint64_t* out_count);
+
+/* Copy the first min(capacity, count) keys of the last pair call (any of the
+ * *_pairs functions) to a host buffer. */
+int refsig_gpu_get_pairs(refsig_gpu_ctx* ctx, uint64_t* out_pairs, uint64_t capacity);
+
+/* ---- device views (for frameworks / collectives; read-only) ------------------ */
+#define REFSIG_BUF_PAIRS 0      /* uint64 keys of the last pair call */
+#define REFSIG_BUF_SIGNATURES 1 /* float S[n_docs*K] */
+#define REFSIG_BUF_DF 2         /* uint32 df[vocab] */
+#define REFSIG_BUF_FINGERPRINTS 3
+int refsig_gpu_device_buffer(refsig_gpu_ctx* ctx, int which, void** ptr, uint64_t* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

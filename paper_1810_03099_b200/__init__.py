@@ -1,0 +1,333 @@
+"""refsig-b200: B200-native MRC batch-similarity path (Python host binding).
+
+Thin ctypes binding of the C ABI in include/refsig_gpu.h (librefsig_gpu.so,
+CUDA kernels for sm_100a). It mirrors the reference's operations
+(reference proj/include/refsig/*.hpp and SPEC.md signature/eval modules) as
+batch calls over a whole corpus:
+
+    count()              NgramVector::from_entries per doc (ngram.hpp:62-75)
+    set_reference_*()    Reference.partition_vectors / K reference docs
+    sign()               sign
+    mrc_pairs(tau)       compare over all i<j
+    simhash()            simhash (simhash.hpp:35-45)
+    hamming_pairs(d)     hamming (simhash.hpp:47) over all i<j
+    exact_pairs(tau)     cosine (ngram.hpp:184-202) over all i<j
+
+Errors keep the reference's split (error.hpp:8-14): ValidationError for
+caller-fixable input (exit code 2 in the reference CLI), RefsigRuntimeError
+otherwise (exit 1). There is no CPU fallback: if the CUDA library or a device
+is missing, construction fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = ["Context", "ValidationError", "RefsigRuntimeError", "PairOverflowError", "WEIGHT_TF", "WEIGHT_TFIDF",
+           "library_path", "load_library", "split_keys"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+WEIGHT_TF = 0
+WEIGHT_TFIDF = 1
+
+OK, E_RUNTIME, E_VALIDATION, E_OVERFLOW = 0, 1, 2, 3
+BUF_PAIRS, BUF_SIGNATURES, BUF_DF, BUF_FINGERPRINTS = 0, 1, 2, 3
+
+
+class ValidationError(ValueError):
+    """refsig::validation_error (reference error.hpp:11-14)."""
+
+
+class RefsigRuntimeError(RuntimeError):
+    """std::runtime_error class failures (CUDA errors, out of memory)."""
+
+
+class PairOverflowError(RefsigRuntimeError):
+    def __init__(self, msg, count):
+        super().__init__(msg)
+        self.count = count
+
+
+def library_path() -> str:
+    return os.path.join(_HERE, "lib", "librefsig_gpu.so")
+
+
+# Exported symbols and their ctypes signatures (tests check this list against
+# include/refsig_gpu.h).
+_P = ctypes.POINTER
+_c = ctypes
+SIGNATURES = {
+    "refsig_gpu_create": ([_c.c_int, _P(_c.c_void_p)], _c.c_int),
+    "refsig_gpu_destroy": ([_c.c_void_p], None),
+    "refsig_gpu_last_error": ([_c.c_void_p], _c.c_char_p),
+    "refsig_gpu_version": ([], _c.c_char_p),
+    "refsig_gpu_set_stream": ([_c.c_void_p, _c.c_void_p], _c.c_int),
+    "refsig_gpu_get_stream": ([_c.c_void_p], _c.c_void_p),
+    "refsig_gpu_synchronize": ([_c.c_void_p], _c.c_int),
+    "refsig_gpu_load_corpus": ([_c.c_void_p, _P(_c.c_uint32), _P(_c.c_uint64), _c.c_uint32, _c.c_uint32], _c.c_int),
+    "refsig_gpu_load_corpus_device": ([_c.c_void_p, _c.c_void_p, _P(_c.c_uint64), _c.c_uint32, _c.c_uint32],
+                                      _c.c_int),
+    "refsig_gpu_count": ([_c.c_void_p, _c.c_int], _c.c_int),
+    "refsig_gpu_get_counts": ([_c.c_void_p, _P(_c.c_uint64), _P(_c.c_uint32), _P(_c.c_uint32), _c.c_uint64,
+                               _P(_c.c_uint64)], _c.c_int),
+    "refsig_gpu_get_df": ([_c.c_void_p, _P(_c.c_uint32), _P(_c.c_float)], _c.c_int),
+    "refsig_gpu_get_inv_norm": ([_c.c_void_p, _P(_c.c_float)], _c.c_int),
+    "refsig_gpu_set_reference_docs": ([_c.c_void_p, _P(_c.c_uint32), _c.c_uint32], _c.c_int),
+    "refsig_gpu_set_reference_vectors": ([_c.c_void_p, _c.c_uint32, _P(_c.c_uint64), _P(_c.c_uint32),
+                                          _P(_c.c_float)], _c.c_int),
+    "refsig_gpu_reference_union": ([_c.c_void_p, _P(_c.c_uint32)], _c.c_int),
+    "refsig_gpu_sign": ([_c.c_void_p], _c.c_int),
+    "refsig_gpu_get_signatures": ([_c.c_void_p, _P(_c.c_float)], _c.c_int),
+    "refsig_gpu_mrc_pairs": ([_c.c_void_p, _c.c_float, _P(_c.c_uint64), _c.c_uint64, _P(_c.c_uint64)], _c.c_int),
+    "refsig_gpu_simhash": ([_c.c_void_p, _c.c_uint64, _c.c_int, _P(_c.c_uint64)], _c.c_int),
+    "refsig_gpu_get_fingerprints": ([_c.c_void_p, _P(_c.c_uint64)], _c.c_int),
+    "refsig_gpu_hamming_pairs": ([_c.c_void_p, _c.c_int, _P(_c.c_uint64), _c.c_uint64, _P(_c.c_uint64)], _c.c_int),
+    "refsig_gpu_exact_pairs": ([_c.c_void_p, _c.c_float, _P(_c.c_uint64), _c.c_uint64, _P(_c.c_uint64)], _c.c_int),
+    "refsig_gpu_pair_cosines": ([_c.c_void_p, _P(_c.c_uint64), _c.c_uint64, _P(_c.c_float)], _c.c_int),
+    "refsig_gpu_attach_database": ([_c.c_void_p, _c.c_void_p], _c.c_int),
+    "refsig_gpu_mrc_query_pairs": ([_c.c_void_p, _c.c_float, _P(_c.c_uint64), _c.c_uint64, _P(_c.c_uint64)],
+                                   _c.c_int),
+    "refsig_gpu_hamming_query_pairs": ([_c.c_void_p, _c.c_int, _P(_c.c_uint64), _c.c_uint64, _P(_c.c_uint64)],
+                                       _c.c_int),
+    "refsig_gpu_get_pairs": ([_c.c_void_p, _P(_c.c_uint64), _c.c_uint64], _c.c_int),
+    "refsig_gpu_device_buffer": ([_c.c_void_p, _c.c_int, _P(_c.c_void_p), _P(_c.c_uint64)], _c.c_int),
+}
+
+_lib = None
+
+
+def load_library():
+    """Load librefsig_gpu.so (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is None:
+        path = library_path()
+        if not os.path.exists(path):
+            raise RefsigRuntimeError(f"{path} not built: run __graft_entry__.build() / make")
+        L = ctypes.CDLL(path)
+        for name, (args, res) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _ptr(a, ct):
+    return None if a is None else a.ctypes.data_as(ctypes.POINTER(ct))
+
+
+def split_keys(keys: np.ndarray):
+    keys = np.asarray(keys, np.uint64)
+    return (keys >> np.uint64(32)).astype(np.uint32), (keys & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+
+
+class Context:
+    """One CUDA stream + device-resident corpus state (refsig_gpu_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self._L = load_library()
+        h = ctypes.c_void_p()
+        rc = self._L.refsig_gpu_create(device, ctypes.byref(h))
+        if rc != OK:
+            raise RefsigRuntimeError(f"refsig_gpu_create(device={device}) failed with status {rc} "
+                                     "(no usable sm_100a device)")
+        self._h = h
+        self.n_docs = 0
+        self.vocab = 0
+        self.K = 0
+
+    # -- plumbing -------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.refsig_gpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _check(self, rc, count=None):
+        if rc == OK:
+            return
+        msg = self._L.refsig_gpu_last_error(self._h).decode()
+        if rc == E_VALIDATION:
+            raise ValidationError(msg)
+        if rc == E_OVERFLOW:
+            raise PairOverflowError(msg, count)
+        raise RefsigRuntimeError(msg)
+
+    def set_stream(self, stream_handle: int | None):
+        self._check(self._L.refsig_gpu_set_stream(self._h, ctypes.c_void_p(stream_handle or 0)))
+
+    @property
+    def stream(self) -> int:
+        return self._L.refsig_gpu_get_stream(self._h) or 0
+
+    def synchronize(self):
+        self._check(self._L.refsig_gpu_synchronize(self._h))
+
+    # -- corpus / K1 ----------------------------------------------------------
+    def load_corpus(self, tokens: np.ndarray, doc_off: np.ndarray, vocab: int):
+        tokens = np.ascontiguousarray(tokens, np.uint32)
+        doc_off = np.ascontiguousarray(doc_off, np.uint64)
+        if doc_off.ndim != 1 or len(doc_off) < 1:
+            raise ValidationError("doc_off must hold n_docs+1 offsets")
+        n = len(doc_off) - 1
+        if n >= 1 and int(doc_off[-1]) > len(tokens):
+            raise ValidationError("doc_off[-1] exceeds the token count")
+        self._check(self._L.refsig_gpu_load_corpus(self._h, _ptr(tokens, ctypes.c_uint32),
+                                                   _ptr(doc_off, ctypes.c_uint64), n, vocab))
+        self._keep = tokens  # pinned/pageable source must outlive async copies
+        self.n_docs, self.vocab = n, vocab
+
+    def load_corpus_device(self, dev_ptr: int, doc_off: np.ndarray, vocab: int):
+        """Tokens already in HBM (e.g. a torch uint32/int32 tensor's data_ptr())."""
+        doc_off = np.ascontiguousarray(doc_off, np.uint64)
+        n = len(doc_off) - 1
+        self._check(self._L.refsig_gpu_load_corpus_device(self._h, ctypes.c_void_p(dev_ptr),
+                                                          _ptr(doc_off, ctypes.c_uint64), n, vocab))
+        self.n_docs, self.vocab = n, vocab
+
+    def count(self, weighting: int = WEIGHT_TFIDF):
+        self._check(self._L.refsig_gpu_count(self._h, weighting))
+
+    def counts(self):
+        """(rowptr, ids, counts): per doc the reference's NgramVector entries."""
+        rowptr = np.zeros(self.n_docs + 1, np.uint64)
+        nnz = ctypes.c_uint64()
+        rc = self._L.refsig_gpu_get_counts(self._h, _ptr(rowptr, ctypes.c_uint64), None, None, 0, ctypes.byref(nnz))
+        if rc not in (OK, E_OVERFLOW):
+            self._check(rc)
+        n = nnz.value
+        ids = np.empty(max(n, 1), np.uint32)
+        cnt = np.empty(max(n, 1), np.uint32)
+        self._check(self._L.refsig_gpu_get_counts(self._h, _ptr(rowptr, ctypes.c_uint64), _ptr(ids, ctypes.c_uint32),
+                                                  _ptr(cnt, ctypes.c_uint32), n, ctypes.byref(nnz)))
+        return rowptr, ids[:n], cnt[:n]
+
+    def df(self):
+        d = np.empty(self.vocab, np.uint32)
+        idf = np.empty(self.vocab, np.float32)
+        self._check(self._L.refsig_gpu_get_df(self._h, _ptr(d, ctypes.c_uint32), _ptr(idf, ctypes.c_float)))
+        return d, idf
+
+    def inv_norm(self):
+        out = np.empty(self.n_docs, np.float32)
+        self._check(self._L.refsig_gpu_get_inv_norm(self._h, _ptr(out, ctypes.c_float)))
+        return out
+
+    # -- reference / K2 -------------------------------------------------------
+    def set_reference_docs(self, doc_ids):
+        ids = np.ascontiguousarray(doc_ids, np.uint32)
+        self._check(self._L.refsig_gpu_set_reference_docs(self._h, _ptr(ids, ctypes.c_uint32), len(ids)))
+        self.K = len(ids)
+
+    def set_reference_vectors(self, rowptr, term_ids, weights=None):
+        rowptr = np.ascontiguousarray(rowptr, np.uint64)
+        term_ids = np.ascontiguousarray(term_ids, np.uint32)
+        w = None if weights is None else np.ascontiguousarray(weights, np.float32)
+        K = len(rowptr) - 1
+        self._check(self._L.refsig_gpu_set_reference_vectors(self._h, K, _ptr(rowptr, ctypes.c_uint64),
+                                                             _ptr(term_ids, ctypes.c_uint32), _ptr(w, ctypes.c_float)))
+        self.K = K
+
+    def set_reference_partitions(self, parts):
+        """Count-1 partition vectors (reference SPEC.md:306-314)."""
+        rowptr = np.zeros(len(parts) + 1, np.uint64)
+        rowptr[1:] = np.cumsum([len(p) for p in parts])
+        ids = np.concatenate([np.asarray(p, np.uint32) for p in parts]) if parts else np.zeros(0, np.uint32)
+        self.set_reference_vectors(rowptr, ids, None)
+
+    def reference_union(self) -> int:
+        u = ctypes.c_uint32()
+        self._check(self._L.refsig_gpu_reference_union(self._h, ctypes.byref(u)))
+        return u.value
+
+    def sign(self, fetch: bool = True):
+        self._check(self._L.refsig_gpu_sign(self._h))
+        if not fetch:
+            return None
+        return self.signatures()
+
+    def signatures(self):
+        S = np.empty((self.n_docs, self.K), np.float32)
+        self._check(self._L.refsig_gpu_get_signatures(self._h, _ptr(S, ctypes.c_float)))
+        return S
+
+    # -- pairs ----------------------------------------------------------------
+    def _pairs(self, fn, arg, out, fetch):
+        n = ctypes.c_uint64()
+        if out is not None:
+            rc = fn(self._h, arg, _ptr(out, ctypes.c_uint64), len(out), ctypes.byref(n))
+            self._check(rc, n.value)
+            return out[: n.value]
+        rc = fn(self._h, arg, None, 0, ctypes.byref(n))
+        self._check(rc, n.value)
+        if not fetch:
+            return n.value
+        keys = np.empty(n.value, np.uint64)
+        if n.value:
+            self._check(self._L.refsig_gpu_get_pairs(self._h, _ptr(keys, ctypes.c_uint64), n.value))
+        return keys
+
+    def mrc_pairs(self, tau: float, out: np.ndarray | None = None, fetch: bool = True):
+        """Sorted keys (i<<32|j) of all i<j with compare(S_i,S_j) >= tau."""
+        return self._pairs(self._L.refsig_gpu_mrc_pairs, ctypes.c_float(tau), out, fetch)
+
+    def simhash(self, seed: int = 0, weighting: int = WEIGHT_TFIDF, term_hash: np.ndarray | None = None,
+                fetch: bool = True):
+        th = None if term_hash is None else np.ascontiguousarray(term_hash, np.uint64)
+        self._check(self._L.refsig_gpu_simhash(self._h, seed, weighting, _ptr(th, ctypes.c_uint64)))
+        if not fetch:
+            return None
+        return self.fingerprints()
+
+    def fingerprints(self):
+        fp = np.empty(self.n_docs, np.uint64)
+        self._check(self._L.refsig_gpu_get_fingerprints(self._h, _ptr(fp, ctypes.c_uint64)))
+        return fp
+
+    def hamming_pairs(self, max_dist: int = 3, out=None, fetch: bool = True):
+        return self._pairs(self._L.refsig_gpu_hamming_pairs, max_dist, out, fetch)
+
+    def exact_pairs(self, tau_cos: float, out=None, fetch: bool = True):
+        return self._pairs(self._L.refsig_gpu_exact_pairs, ctypes.c_float(tau_cos), out, fetch)
+
+    def pair_cosines(self, keys: np.ndarray) -> np.ndarray:
+        keys = np.ascontiguousarray(keys, np.uint64)
+        out = np.empty(len(keys), np.float32)
+        self._check(self._L.refsig_gpu_pair_cosines(self._h, _ptr(keys, ctypes.c_uint64), len(keys),
+                                                    _ptr(out, ctypes.c_float)))
+        return out
+
+    # -- query-vs-database ----------------------------------------------------
+    def attach_database(self, db: "Context"):
+        self._check(self._L.refsig_gpu_attach_database(self._h, db.handle))
+        self.K = db.K
+        self._db = db
+
+    def mrc_query_pairs(self, tau: float, out=None, fetch: bool = True):
+        return self._pairs(self._L.refsig_gpu_mrc_query_pairs, ctypes.c_float(tau), out, fetch)
+
+    def hamming_query_pairs(self, max_dist: int = 3, out=None, fetch: bool = True):
+        return self._pairs(self._L.refsig_gpu_hamming_query_pairs, max_dist, out, fetch)
+
+    def device_buffer(self, which: int):
+        p = ctypes.c_void_p()
+        n = ctypes.c_uint64()
+        self._check(self._L.refsig_gpu_device_buffer(self._h, which, ctypes.byref(p), ctypes.byref(n)))
+        return p.value or 0, n.value

@@ -1,0 +1,820 @@
+// capi.cu — the C ABI (include/refsig_gpu.h): context, device buffers,
+// validation and the status <-> refsig::validation_error / runtime_error
+// mapping (reference error.hpp:8-14). Every compute entry point enqueues CUDA
+// kernels (kernels.cuh); there is no host compute path.
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "refsig_gpu.h"
+
+using namespace refsig_gpu;
+
+namespace {
+
+struct Status {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Status{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(REFSIG_E_RUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void require(bool ok, const std::string& msg) {
+  if (!ok) fail(REFSIG_E_VALIDATION, msg);
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  // Grow-only; contents are not preserved. Returns true if (re)allocated.
+  bool ensure(size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (bytes <= cap) return false;
+    if (p) {
+      cudaFree(p);
+      p = nullptr;
+      cap = 0;
+    }
+    ck(cudaMalloc(&p, bytes), "cudaMalloc");
+    cap = bytes;
+    return true;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+struct refsig_gpu_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  uint64_t* h_pin = nullptr;  // pinned scratch for small D2H reads
+
+  // corpus
+  bool loaded = false;
+  uint32_t n_docs = 0, vocab = 0;
+  uint64_t n_tokens = 0;
+  std::vector<uint64_t> h_off;
+  DevBuf tokens, doc_off;
+  const uint32_t* tok = nullptr;
+  DevBuf bin_docs[4];
+  uint32_t n_bin[4] = {0, 0, 0, 0};
+  DevBuf long_docs, long_off, long_scratch;
+  uint32_t n_long = 0;
+
+  // K1
+  bool counted = false;
+  int weight_mode = REFSIG_WEIGHT_TFIDF;
+  DevBuf ent, nnz, df, info, flags;
+  DevBuf rowptr, c_ids, c_counts, inv_norm;
+  bool have_inv_norm = false;
+
+  // reference
+  bool have_ref = false;
+  uint32_t K = 0;
+  DevBuf ref_docs, ref_start, ref_n, ref_ent, ref_mark, ref_prefix, R;
+
+  // sign
+  bool signed_ = false;
+  DevBuf S, Sn;
+
+  // pairs
+  DevBuf bitmap, rowcnt, rowstart, cand, scan_tmp;
+  uint64_t cand_count = 0;
+
+  // simhash
+  bool have_fp = false;
+  DevBuf fp, term_hash;
+
+  // exact
+  bool have_x = false;
+  DevBuf x, post_off, post_fill, posts, acc_pool;
+  uint64_t acc_pool_docs = 0;
+
+  // query mode
+  refsig_gpu_ctx* db = nullptr;
+};
+
+namespace {
+
+template <class F>
+int guard(refsig_gpu_ctx* ctx, F&& f) {
+  if (!ctx) return REFSIG_E_VALIDATION;
+  try {
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    f();
+    ctx->err.clear();
+    return REFSIG_OK;
+  } catch (const Status& s) {
+    ctx->err = s.msg;
+    return s.code;
+  } catch (const std::bad_alloc&) {
+    ctx->err = "host out of memory";
+    return REFSIG_E_RUNTIME;
+  }
+}
+
+// Synchronise the stream and surface errors of enqueued work (CUDA faults,
+// token ids >= vocab flagged by K1).
+void sync(refsig_gpu_ctx* c) {
+  if (c->flags.p) ck(cudaMemcpyAsync(c->h_pin + 7, c->flags.p, 4, cudaMemcpyDeviceToHost, c->stream), "D2H flags");
+  ck(cudaStreamSynchronize(c->stream), "kernel execution");
+  ck(cudaGetLastError(), "kernel launch");
+  if (c->flags.p) {
+    uint32_t f = static_cast<uint32_t>(c->h_pin[7]);
+    if (f & 1u) {
+      ck(cudaMemsetAsync(c->flags.p, 0, 4, c->stream), "memset");
+      c->counted = false;
+      fail(REFSIG_E_VALIDATION, "token id >= vocab in corpus");
+    }
+  }
+}
+
+void launched(const char* what) { ck(cudaGetLastError(), what); }
+
+void reset_downstream(refsig_gpu_ctx* c) {
+  c->have_ref = c->signed_ = c->have_fp = c->have_x = c->have_inv_norm = false;
+  c->cand_count = 0;
+}
+
+uint32_t words_per_row(uint32_t n_cols) { return static_cast<uint32_t>(ceil_div(n_cols, kTile) * 4); }
+
+// Scan rowcnt, emit sorted keys into ctx->cand (growing it if needed), and
+// optionally copy them to the caller's host buffer.
+int run_emit(refsig_gpu_ctx* c, const PairGrid& g, uint64_t* out, uint64_t capacity, uint64_t* out_count) {
+  const uint64_t n = g.n_rows;
+  c->rowstart.ensure(sizeof(uint64_t) * (n + 1));
+  c->scan_tmp.ensure(scan_tmp_bytes(n));
+  launch_exclusive_scan_u32_to_u64(c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(), n, c->scan_tmp.p,
+                                   c->stream);
+  c->cand.ensure(sizeof(uint64_t) * (1u << 20));
+  uint64_t cap_keys = c->cand.cap / sizeof(uint64_t);
+  launch_emit_pairs(c->bitmap.as<uint32_t>(), g, c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(),
+                    c->cand.as<uint64_t>(), cap_keys, c->stream);
+  launched("emit");
+  ck(cudaMemcpyAsync(c->h_pin, c->rowstart.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, c->stream), "D2H count");
+  sync(c);
+  const uint64_t total = c->h_pin[0];
+  if (total > cap_keys) {
+    c->cand.ensure(sizeof(uint64_t) * (total + total / 4 + 1024));
+    launch_emit_pairs(c->bitmap.as<uint32_t>(), g, c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(),
+                      c->cand.as<uint64_t>(), c->cand.cap / sizeof(uint64_t), c->stream);
+    launched("emit");
+  }
+  c->cand_count = total;
+  *out_count = total;
+  if (out && capacity) {
+    const uint64_t m = std::min(total, capacity);
+    if (m) ck(cudaMemcpyAsync(out, c->cand.p, m * 8, cudaMemcpyDeviceToHost, c->stream), "D2H pairs");
+  }
+  sync(c);
+  if (total > capacity && out) {
+    c->err = "candidate buffer overflow: " + std::to_string(total) + " pairs > capacity " + std::to_string(capacity);
+    return REFSIG_E_OVERFLOW;
+  }
+  return REFSIG_OK;
+}
+
+void prepare_bitmap(refsig_gpu_ctx* c, const PairGrid& g, bool zero) {
+  c->bitmap.ensure(sizeof(uint32_t) * static_cast<size_t>(g.n_rows) * g.words_per_row);
+  c->rowcnt.ensure(sizeof(uint32_t) * (g.n_rows ? g.n_rows : 1));
+  ck(cudaMemsetAsync(c->rowcnt.p, 0, sizeof(uint32_t) * g.n_rows, c->stream), "memset rowcnt");
+  if (zero)
+    ck(cudaMemsetAsync(c->bitmap.p, 0, sizeof(uint32_t) * static_cast<size_t>(g.n_rows) * g.words_per_row,
+                       c->stream),
+       "memset bitmap");
+}
+
+// A5: union, remap and the compact table from c->ref_{start,n} and `ent`.
+void build_reference(refsig_gpu_ctx* c, const RefArgs& r, uint64_t u_cap) {
+  const uint32_t V = c->vocab;
+  c->ref_mark.ensure(sizeof(uint32_t) * V);
+  c->ref_prefix.ensure(sizeof(uint64_t) * (V + 1));
+  c->scan_tmp.ensure(scan_tmp_bytes(V));
+  ck(cudaMemsetAsync(c->ref_mark.p, 0, sizeof(uint32_t) * V, c->stream), "memset");
+  launch_ref_mark(r, c->ref_mark.as<uint32_t>(), c->stream);
+  launch_exclusive_scan_u32_to_u64(c->ref_mark.as<uint32_t>(), c->ref_prefix.as<uint64_t>(), V, c->scan_tmp.p,
+                                   c->stream);
+  launch_ref_remap(c->ref_mark.as<uint32_t>(), c->ref_prefix.as<uint64_t>(), V, c->info.as<TermInfo>(), c->stream);
+  if (u_cap > V) u_cap = V;
+  const size_t rbytes = sizeof(float) * std::max<uint64_t>(u_cap, 1) * r.K;
+  c->R.ensure(rbytes);
+  ck(cudaMemsetAsync(c->R.p, 0, rbytes, c->stream), "memset R");
+  launch_ref_fill(r, c->info.as<TermInfo>(), c->R.as<float>(), c->stream);
+  launched("reference");
+  c->K = r.K;
+  c->have_ref = true;
+  c->signed_ = false;
+}
+
+void ensure_unit_weights(refsig_gpu_ctx* c) {
+  if (c->have_x) return;
+  c->inv_norm.ensure(sizeof(float) * c->n_docs);
+  launch_inv_norm(c->ent.as<uint2>(), c->doc_off.as<uint64_t>(), c->nnz.as<uint32_t>(), c->info.as<TermInfo>(),
+                  c->n_docs, c->inv_norm.as<float>(), c->stream);
+  c->x.ensure(sizeof(float) * std::max<uint64_t>(c->n_tokens, 1));
+  launch_unit_weights(c->ent.as<uint2>(), c->doc_off.as<uint64_t>(), c->nnz.as<uint32_t>(), c->info.as<TermInfo>(),
+                      c->inv_norm.as<float>(), c->n_docs, c->x.as<float>(), c->stream);
+  launched("unit weights");
+  c->have_x = true;
+  c->have_inv_norm = true;
+}
+
+void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, uint32_t vocab) {
+  require(doc_off != nullptr, "doc_off is NULL");
+  require(n_docs >= 1, "empty corpus");
+  require(vocab >= 1 && vocab < 0x7fffffffu, "vocab out of range");
+  require(doc_off[0] == 0, "doc_off[0] must be 0");
+  for (uint32_t d = 0; d < n_docs; ++d) require(doc_off[d + 1] >= doc_off[d], "doc_off must be non-decreasing");
+  c->h_off.assign(doc_off, doc_off + n_docs + 1);
+  c->n_docs = n_docs;
+  c->vocab = vocab;
+  c->n_tokens = doc_off[n_docs];
+  c->doc_off.ensure(sizeof(uint64_t) * (n_docs + 1));
+  ck(cudaMemcpyAsync(c->doc_off.p, doc_off, sizeof(uint64_t) * (n_docs + 1), cudaMemcpyHostToDevice, c->stream),
+     "H2D doc_off");
+  // Length bins for K1 (host metadata only).
+  std::vector<uint32_t> bins[4], longs;
+  std::vector<uint64_t> loff;
+  uint64_t scratch = 0;
+  for (uint32_t d = 0; d < n_docs; ++d) {
+    const uint64_t len = doc_off[d + 1] - doc_off[d];
+    require(len < (1ull << 31), "document longer than 2^31 tokens");
+    int b = 0;
+    while (b < 4 && len > kBinCap[b]) ++b;
+    if (b < 4) {
+      bins[b].push_back(d);
+    } else {
+      longs.push_back(d);
+      loff.push_back(scratch);
+      uint64_t p = 1;
+      while (p < len) p <<= 1;
+      scratch += p;
+    }
+  }
+  for (int b = 0; b < 4; ++b) {
+    c->n_bin[b] = static_cast<uint32_t>(bins[b].size());
+    if (!bins[b].empty()) {
+      c->bin_docs[b].ensure(sizeof(uint32_t) * bins[b].size());
+      ck(cudaMemcpyAsync(c->bin_docs[b].p, bins[b].data(), sizeof(uint32_t) * bins[b].size(), cudaMemcpyHostToDevice,
+                         c->stream),
+         "H2D bins");
+    }
+  }
+  c->n_long = static_cast<uint32_t>(longs.size());
+  if (!longs.empty()) {
+    c->long_docs.ensure(sizeof(uint32_t) * longs.size());
+    c->long_off.ensure(sizeof(uint64_t) * loff.size());
+    c->long_scratch.ensure(sizeof(uint32_t) * scratch);
+    ck(cudaMemcpyAsync(c->long_docs.p, longs.data(), sizeof(uint32_t) * longs.size(), cudaMemcpyHostToDevice,
+                       c->stream),
+       "H2D long docs");
+    ck(cudaMemcpyAsync(c->long_off.p, loff.data(), sizeof(uint64_t) * loff.size(), cudaMemcpyHostToDevice, c->stream),
+       "H2D long offsets");
+  }
+  // bin lists are host-local vectors: make sure the copies finished
+  ck(cudaStreamSynchronize(c->stream), "H2D metadata");
+  c->loaded = true;
+  c->counted = false;
+  reset_downstream(c);
+}
+
+PairGrid self_grid(const refsig_gpu_ctx* c) { return PairGrid{c->n_docs, c->n_docs, words_per_row(c->n_docs), true}; }
+
+}  // namespace
+
+extern "C" {
+
+const char* refsig_gpu_version(void) { return "refsig-b200 0.1 (sm_100a)"; }
+
+int refsig_gpu_create(int device, refsig_gpu_ctx** out) {
+  if (!out) return REFSIG_E_VALIDATION;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return REFSIG_E_RUNTIME;
+  }
+  if (device < 0 || device >= n) return REFSIG_E_VALIDATION;
+  refsig_gpu_ctx* c = new (std::nothrow) refsig_gpu_ctx();
+  if (!c) return REFSIG_E_RUNTIME;
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMallocHost(&c->h_pin, 64) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return REFSIG_E_RUNTIME;
+  }
+  c->stream = c->own_stream;
+  *out = c;
+  return REFSIG_OK;
+}
+
+void refsig_gpu_destroy(refsig_gpu_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
+  delete ctx;
+}
+
+const char* refsig_gpu_last_error(const refsig_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int refsig_gpu_set_stream(refsig_gpu_ctx* ctx, void* s) {
+  return guard(ctx, [&] {
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+  });
+}
+
+void* refsig_gpu_get_stream(const refsig_gpu_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int refsig_gpu_synchronize(refsig_gpu_ctx* ctx) {
+  return guard(ctx, [&] { sync(ctx); });
+}
+
+int refsig_gpu_load_corpus(refsig_gpu_ctx* ctx, const uint32_t* tokens, const uint64_t* doc_off, uint32_t n_docs,
+                           uint32_t vocab) {
+  return guard(ctx, [&] {
+    require(doc_off != nullptr, "doc_off is NULL");
+    require(n_docs >= 1, "empty corpus");
+    require(tokens != nullptr || doc_off[n_docs] == 0, "tokens is NULL");
+    const uint64_t T = doc_off[n_docs];
+    ctx->tokens.ensure(sizeof(uint32_t) * std::max<uint64_t>(T, 1));
+    if (T)
+      ck(cudaMemcpyAsync(ctx->tokens.p, tokens, sizeof(uint32_t) * T, cudaMemcpyHostToDevice, ctx->stream),
+         "H2D tokens");
+    ctx->tok = ctx->tokens.as<uint32_t>();
+    load_common(ctx, doc_off, n_docs, vocab);
+  });
+}
+
+int refsig_gpu_load_corpus_device(refsig_gpu_ctx* ctx, const uint32_t* d_tokens, const uint64_t* doc_off,
+                                  uint32_t n_docs, uint32_t vocab) {
+  return guard(ctx, [&] {
+    require(doc_off != nullptr, "doc_off is NULL");
+    require(n_docs >= 1, "empty corpus");
+    require(d_tokens != nullptr || doc_off[n_docs] == 0, "tokens is NULL");
+    ctx->tok = d_tokens;
+    load_common(ctx, doc_off, n_docs, vocab);
+  });
+}
+
+int refsig_gpu_count(refsig_gpu_ctx* ctx, int weight_mode) {
+  return guard(ctx, [&] {
+    require(ctx->loaded, "no corpus loaded");
+    require(weight_mode == REFSIG_WEIGHT_TF || weight_mode == REFSIG_WEIGHT_TFIDF, "bad weight mode");
+    refsig_gpu_ctx* db = ctx->db;
+    if (db) {
+      require(db->counted, "attached database not counted");
+      require(db->vocab == ctx->vocab, "query vocab differs from database vocab");
+    }
+    const uint32_t N = ctx->n_docs, V = ctx->vocab;
+    ctx->ent.ensure(sizeof(uint2) * std::max<uint64_t>(ctx->n_tokens, 1));
+    ctx->nnz.ensure(sizeof(uint32_t) * N);
+    ctx->df.ensure(sizeof(uint32_t) * V);
+    ctx->info.ensure(sizeof(TermInfo) * V);
+    if (ctx->flags.ensure(16)) ck(cudaMemsetAsync(ctx->flags.p, 0, 16, ctx->stream), "memset");
+    ck(cudaMemsetAsync(ctx->df.p, 0, sizeof(uint32_t) * V, ctx->stream), "memset df");
+    CountArgs a{ctx->tok, ctx->doc_off.as<uint64_t>(), V, ctx->ent.as<uint2>(), ctx->nnz.as<uint32_t>(),
+                ctx->df.as<uint32_t>(), ctx->flags.as<uint32_t>()};
+    for (int b = 0; b < 4; ++b) launch_count_bin(b, a, ctx->bin_docs[b].as<uint32_t>(), ctx->n_bin[b], ctx->stream);
+    launch_count_large(a, ctx->long_docs.as<uint32_t>(), ctx->long_off.as<uint64_t>(), ctx->n_long,
+                       ctx->long_scratch.as<uint32_t>(), ctx->stream);
+    if (db) {
+      // Query mode: the database's IDF and reference rows (configs[4]).
+      ck(cudaStreamSynchronize(db->stream), "sync database");
+      ck(cudaMemcpyAsync(ctx->info.p, db->info.p, sizeof(TermInfo) * V, cudaMemcpyDeviceToDevice, ctx->stream),
+         "copy database idf");
+      ctx->weight_mode = db->weight_mode;
+    } else {
+      launch_idf(ctx->df.as<uint32_t>(), V, N, weight_mode, ctx->info.as<TermInfo>(), ctx->stream);
+      ctx->weight_mode = weight_mode;
+    }
+    launched("count");
+    ctx->counted = true;
+    reset_downstream(ctx);
+  });
+}
+
+int refsig_gpu_get_counts(refsig_gpu_ctx* ctx, uint64_t* rowptr, uint32_t* ids, uint32_t* counts, uint64_t cap,
+                          uint64_t* nnz_out) {
+  int overflow = 0;
+  int rc = guard(ctx, [&] {
+    require(ctx->counted, "count() not called");
+    require(rowptr && nnz_out, "NULL output");
+    require(cap == 0 || (ids && counts), "NULL output");
+    const uint32_t N = ctx->n_docs;
+    ctx->rowptr.ensure(sizeof(uint64_t) * (N + 1));
+    ctx->scan_tmp.ensure(scan_tmp_bytes(N));
+    launch_exclusive_scan_u32_to_u64(ctx->nnz.as<uint32_t>(), ctx->rowptr.as<uint64_t>(), N, ctx->scan_tmp.p,
+                                     ctx->stream);
+    ck(cudaMemcpyAsync(rowptr, ctx->rowptr.p, sizeof(uint64_t) * (N + 1), cudaMemcpyDeviceToHost, ctx->stream),
+       "D2H rowptr");
+    sync(ctx);
+    const uint64_t total = rowptr[N];
+    *nnz_out = total;
+    if (total > cap) {
+      overflow = 1;
+      return;
+    }
+    ctx->c_ids.ensure(sizeof(uint32_t) * std::max<uint64_t>(total, 1));
+    ctx->c_counts.ensure(sizeof(uint32_t) * std::max<uint64_t>(total, 1));
+    launch_compact_csr(ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(),
+                       ctx->rowptr.as<uint64_t>(), N, ctx->c_ids.as<uint32_t>(), ctx->c_counts.as<uint32_t>(),
+                       ctx->stream);
+    launched("compact");
+    if (total) {
+      ck(cudaMemcpyAsync(ids, ctx->c_ids.p, 4 * total, cudaMemcpyDeviceToHost, ctx->stream), "D2H ids");
+      ck(cudaMemcpyAsync(counts, ctx->c_counts.p, 4 * total, cudaMemcpyDeviceToHost, ctx->stream), "D2H counts");
+    }
+    sync(ctx);
+  });
+  if (rc == REFSIG_OK && overflow) {
+    ctx->err = "counts buffer overflow";
+    return REFSIG_E_OVERFLOW;
+  }
+  return rc;
+}
+
+int refsig_gpu_get_df(refsig_gpu_ctx* ctx, uint32_t* df, float* idf32) {
+  return guard(ctx, [&] {
+    require(ctx->counted, "count() not called");
+    const uint32_t V = ctx->vocab;
+    std::vector<TermInfo> info;
+    if (df) ck(cudaMemcpyAsync(df, ctx->df.p, 4ull * V, cudaMemcpyDeviceToHost, ctx->stream), "D2H df");
+    if (idf32) {
+      info.resize(V);
+      ck(cudaMemcpyAsync(info.data(), ctx->info.p, sizeof(TermInfo) * V, cudaMemcpyDeviceToHost, ctx->stream),
+         "D2H idf");
+    }
+    sync(ctx);
+    if (idf32)
+      for (uint32_t t = 0; t < V; ++t) idf32[t] = info[t].idf;
+  });
+}
+
+int refsig_gpu_get_inv_norm(refsig_gpu_ctx* ctx, float* inv_norm) {
+  return guard(ctx, [&] {
+    require(ctx->counted, "count() not called");
+    require(inv_norm != nullptr, "NULL output");
+    ctx->inv_norm.ensure(sizeof(float) * ctx->n_docs);
+    launch_inv_norm(ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(),
+                    ctx->info.as<TermInfo>(), ctx->n_docs, ctx->inv_norm.as<float>(), ctx->stream);
+    launched("inv_norm");
+    ck(cudaMemcpyAsync(inv_norm, ctx->inv_norm.p, 4ull * ctx->n_docs, cudaMemcpyDeviceToHost, ctx->stream),
+       "D2H inv_norm");
+    sync(ctx);
+  });
+}
+
+int refsig_gpu_set_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_ids, uint32_t K) {
+  return guard(ctx, [&] {
+    require(ctx->counted, "count() not called");
+    require(!ctx->db, "query context uses the attached database's reference");
+    require(ref_doc_ids != nullptr, "ref_doc_ids is NULL");
+    require(K >= 1, "K must be >= 1");
+    uint64_t u_cap = 0;
+    for (uint32_t k = 0; k < K; ++k) {
+      require(ref_doc_ids[k] < ctx->n_docs, "reference doc id >= n_docs");
+      u_cap += ctx->h_off[ref_doc_ids[k] + 1] - ctx->h_off[ref_doc_ids[k]];
+    }
+    ctx->ref_docs.ensure(4ull * K);
+    ctx->ref_start.ensure(8ull * K);
+    ctx->ref_n.ensure(4ull * K);
+    ck(cudaMemcpyAsync(ctx->ref_docs.p, ref_doc_ids, 4ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D refs");
+    launch_ref_doc_ranges(ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->ref_docs.as<uint32_t>(), K,
+                          ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->stream);
+    RefArgs r{K, ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->ent.as<uint2>(), false};
+    build_reference(ctx, r, u_cap);
+    // the H2D source is a caller buffer: finish before returning
+    ck(cudaStreamSynchronize(ctx->stream), "reference");
+  });
+}
+
+int refsig_gpu_set_reference_vectors(refsig_gpu_ctx* ctx, uint32_t K, const uint64_t* rowptr, const uint32_t* term_ids,
+                                     const float* weights) {
+  return guard(ctx, [&] {
+    require(ctx->counted, "count() not called");
+    require(!ctx->db, "query context uses the attached database's reference");
+    require(K >= 1, "K must be >= 1");
+    require(rowptr != nullptr, "rowptr is NULL");
+    require(rowptr[0] == 0, "rowptr[0] must be 0");
+    for (uint32_t k = 0; k < K; ++k) require(rowptr[k + 1] >= rowptr[k], "rowptr must be non-decreasing");
+    const uint64_t n = rowptr[K];
+    require(n == 0 || term_ids != nullptr, "term_ids is NULL");
+    std::vector<uint2> h(n);
+    std::vector<uint64_t> start(K);
+    std::vector<uint32_t> cnt(K);
+    for (uint32_t k = 0; k < K; ++k) {
+      start[k] = rowptr[k];
+      cnt[k] = static_cast<uint32_t>(rowptr[k + 1] - rowptr[k]);
+      std::vector<uint32_t> ids(term_ids + rowptr[k], term_ids + rowptr[k + 1]);
+      std::sort(ids.begin(), ids.end());
+      for (size_t i = 0; i < ids.size(); ++i) {
+        require(ids[i] < ctx->vocab, "reference term id >= vocab");
+        require(i == 0 || ids[i] != ids[i - 1], "duplicate term in a reference vector");
+      }
+      for (uint64_t p = rowptr[k]; p < rowptr[k + 1]; ++p) {
+        const float w = weights ? weights[p] : 1.0f;
+        require(std::isfinite(w) && w >= 0.0f, "reference weights must be finite and >= 0");
+        uint32_t bits;
+        std::memcpy(&bits, &w, 4);
+        h[p] = make_uint2(term_ids[p], bits);
+      }
+    }
+    ctx->ref_ent.ensure(sizeof(uint2) * std::max<uint64_t>(n, 1));
+    ctx->ref_start.ensure(8ull * K);
+    ctx->ref_n.ensure(4ull * K);
+    if (n) ck(cudaMemcpyAsync(ctx->ref_ent.p, h.data(), sizeof(uint2) * n, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ck(cudaMemcpyAsync(ctx->ref_start.p, start.data(), 8ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    ck(cudaMemcpyAsync(ctx->ref_n.p, cnt.data(), 4ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    RefArgs r{K, ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->ref_ent.as<uint2>(), true};
+    build_reference(ctx, r, n);
+    ck(cudaStreamSynchronize(ctx->stream), "reference");
+  });
+}
+
+int refsig_gpu_reference_union(refsig_gpu_ctx* ctx, uint32_t* out_u) {
+  return guard(ctx, [&] {
+    require(ctx->have_ref, "no reference set");
+    require(out_u != nullptr, "NULL output");
+    ck(cudaMemcpyAsync(ctx->h_pin, ctx->ref_prefix.as<uint64_t>() + ctx->vocab, 8, cudaMemcpyDeviceToHost,
+                       ctx->stream),
+       "D2H");
+    sync(ctx);
+    *out_u = static_cast<uint32_t>(ctx->h_pin[0]);
+  });
+}
+
+int refsig_gpu_sign(refsig_gpu_ctx* ctx) {
+  return guard(ctx, [&] {
+    require(ctx->counted, "count() not called");
+    const refsig_gpu_ctx* refc = ctx->db ? ctx->db : ctx;
+    require(refc->have_ref, "no reference set");
+    const uint32_t N = ctx->n_docs, K = refc->K;
+    ctx->S.ensure(sizeof(float) * static_cast<size_t>(N) * K);
+    ctx->Sn.ensure(sizeof(float) * static_cast<size_t>(N) * K);
+    ctx->inv_norm.ensure(sizeof(float) * N);
+    if (ctx->db) ck(cudaStreamSynchronize(ctx->db->stream), "sync database");
+    SignArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->info.as<TermInfo>(),
+               refc->R.as<float>(), N, K, ctx->S.as<float>(), ctx->Sn.as<float>(), ctx->inv_norm.as<float>()};
+    launch_sign(a, ctx->stream);
+    launched("sign");
+    ctx->K = K;
+    ctx->signed_ = true;
+    ctx->have_inv_norm = true;
+  });
+}
+
+int refsig_gpu_get_signatures(refsig_gpu_ctx* ctx, float* S) {
+  return guard(ctx, [&] {
+    require(ctx->signed_, "sign() not called");
+    require(S != nullptr, "NULL output");
+    ck(cudaMemcpyAsync(S, ctx->S.p, sizeof(float) * static_cast<size_t>(ctx->n_docs) * ctx->K,
+                       cudaMemcpyDeviceToHost, ctx->stream),
+       "D2H signatures");
+    sync(ctx);
+  });
+}
+
+int refsig_gpu_mrc_pairs(refsig_gpu_ctx* ctx, float tau, uint64_t* out_pairs, uint64_t capacity,
+                         uint64_t* out_count) {
+  int rc2 = REFSIG_OK;
+  int rc = guard(ctx, [&] {
+    require(ctx->signed_, "sign() not called");
+    require(out_count != nullptr, "out_count is NULL");
+    require(!std::isnan(tau), "tau is NaN");
+    require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
+    const PairGrid g = self_grid(ctx);
+    prepare_bitmap(ctx, g, false);
+    launch_mrc_bitmap(ctx->Sn.as<float>(), ctx->Sn.as<float>(), ctx->K, tau, g, ctx->bitmap.as<uint32_t>(),
+                      ctx->rowcnt.as<uint32_t>(), ctx->stream);
+    launched("mrc bitmap");
+    rc2 = run_emit(ctx, g, out_pairs, capacity, out_count);
+  });
+  return rc != REFSIG_OK ? rc : rc2;
+}
+
+int refsig_gpu_simhash(refsig_gpu_ctx* ctx, uint64_t seed, int weight_mode, const uint64_t* term_hash) {
+  return guard(ctx, [&] {
+    require(ctx->counted, "count() not called");
+    require(weight_mode == REFSIG_WEIGHT_TF || weight_mode == REFSIG_WEIGHT_TFIDF, "bad weight mode");
+    require(weight_mode == REFSIG_WEIGHT_TF || ctx->weight_mode == REFSIG_WEIGHT_TFIDF,
+            "TF-IDF simhash needs count(REFSIG_WEIGHT_TFIDF)");
+    const uint64_t* th = nullptr;
+    if (term_hash) {
+      ctx->term_hash.ensure(8ull * ctx->vocab);
+      ck(cudaMemcpyAsync(ctx->term_hash.p, term_hash, 8ull * ctx->vocab, cudaMemcpyHostToDevice, ctx->stream),
+         "H2D term hash");
+      th = ctx->term_hash.as<uint64_t>();
+    }
+    ctx->fp.ensure(8ull * ctx->n_docs);
+    SimhashArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->info.as<TermInfo>(),
+                  th, seed, ctx->n_docs, weight_mode == REFSIG_WEIGHT_TFIDF, ctx->fp.as<uint64_t>()};
+    launch_simhash(a, ctx->stream);
+    launched("simhash");
+    if (term_hash) ck(cudaStreamSynchronize(ctx->stream), "simhash");
+    ctx->have_fp = true;
+  });
+}
+
+int refsig_gpu_get_fingerprints(refsig_gpu_ctx* ctx, uint64_t* fp) {
+  return guard(ctx, [&] {
+    require(ctx->have_fp, "simhash() not called");
+    require(fp != nullptr, "NULL output");
+    ck(cudaMemcpyAsync(fp, ctx->fp.p, 8ull * ctx->n_docs, cudaMemcpyDeviceToHost, ctx->stream), "D2H fp");
+    sync(ctx);
+  });
+}
+
+int refsig_gpu_hamming_pairs(refsig_gpu_ctx* ctx, int max_dist, uint64_t* out_pairs, uint64_t capacity,
+                             uint64_t* out_count) {
+  int rc2 = REFSIG_OK;
+  int rc = guard(ctx, [&] {
+    require(ctx->have_fp, "simhash() not called");
+    require(out_count != nullptr, "out_count is NULL");
+    require(max_dist >= 0 && max_dist <= 64, "max_dist must be in [0, 64]");
+    require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
+    const PairGrid g = self_grid(ctx);
+    prepare_bitmap(ctx, g, false);
+    launch_hamming_bitmap(ctx->fp.as<uint64_t>(), ctx->fp.as<uint64_t>(), max_dist, g, ctx->bitmap.as<uint32_t>(),
+                          ctx->rowcnt.as<uint32_t>(), ctx->stream);
+    launched("hamming bitmap");
+    rc2 = run_emit(ctx, g, out_pairs, capacity, out_count);
+  });
+  return rc != REFSIG_OK ? rc : rc2;
+}
+
+int refsig_gpu_exact_pairs(refsig_gpu_ctx* ctx, float tau_cos, uint64_t* out_pairs, uint64_t capacity,
+                           uint64_t* out_count) {
+  int rc2 = REFSIG_OK;
+  int rc = guard(ctx, [&] {
+    require(ctx->counted, "count() not called");
+    require(out_count != nullptr, "out_count is NULL");
+    require(tau_cos > 0.0f && tau_cos <= 1.0f, "tau_cos must be in (0, 1]");
+    require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
+    const uint32_t N = ctx->n_docs, V = ctx->vocab;
+    ensure_unit_weights(ctx);
+    // postings: offsets = exclusive scan of df, then an atomic fill
+    ctx->post_off.ensure(8ull * (V + 1));
+    ctx->post_fill.ensure(8ull * (V + 1));
+    ctx->posts.ensure(sizeof(uint2) * std::max<uint64_t>(ctx->n_tokens, 1));
+    ctx->scan_tmp.ensure(scan_tmp_bytes(std::max(N, V)));
+    launch_exclusive_scan_u32_to_u64(ctx->df.as<uint32_t>(), ctx->post_off.as<uint64_t>(), V, ctx->scan_tmp.p,
+                                     ctx->stream);
+    ck(cudaMemcpyAsync(ctx->post_fill.p, ctx->post_off.p, 8ull * (V + 1), cudaMemcpyDeviceToDevice, ctx->stream),
+       "copy");
+    launch_postings_fill(ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(),
+                         ctx->x.as<float>(), N, ctx->post_fill.as<uint64_t>(), ctx->posts.as<uint2>(), ctx->stream);
+    const uint64_t pool = static_cast<uint64_t>(exact_pool_ctas()) * N;
+    if (ctx->acc_pool.ensure(sizeof(float) * pool) || ctx->acc_pool_docs != N) {
+      ck(cudaMemsetAsync(ctx->acc_pool.p, 0, sizeof(float) * pool, ctx->stream), "memset acc");
+      ctx->acc_pool_docs = N;
+    }
+    const PairGrid g = self_grid(ctx);
+    prepare_bitmap(ctx, g, true);
+    ExactArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->x.as<float>(),
+                ctx->post_off.as<uint64_t>(), ctx->posts.as<uint2>(), N, tau_cos, ctx->acc_pool.as<float>(),
+                ctx->bitmap.as<uint32_t>(), g.words_per_row, ctx->rowcnt.as<uint32_t>()};
+    launch_exact_rows(a, 0, N, ctx->stream);
+    launched("exact");
+    rc2 = run_emit(ctx, g, out_pairs, capacity, out_count);
+  });
+  return rc != REFSIG_OK ? rc : rc2;
+}
+
+int refsig_gpu_pair_cosines(refsig_gpu_ctx* ctx, const uint64_t* keys, uint64_t n, float* out) {
+  return guard(ctx, [&] {
+    require(ctx->counted, "count() not called");
+    require(n == 0 || (keys && out), "NULL argument");
+    for (uint64_t q = 0; q < n; ++q)
+      require((keys[q] >> 32) < ctx->n_docs && (keys[q] & 0xffffffffu) < ctx->n_docs, "pair index >= n_docs");
+    if (!n) return;
+    ensure_unit_weights(ctx);
+    DevBuf dk, dout;
+    dk.ensure(8 * n);
+    dout.ensure(4 * n);
+    ck(cudaMemcpyAsync(dk.p, keys, 8 * n, cudaMemcpyHostToDevice, ctx->stream), "H2D keys");
+    launch_pair_cosines(ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->x.as<float>(),
+                        dk.as<uint64_t>(), n, dout.as<float>(), ctx->stream);
+    launched("pair cosines");
+    ck(cudaMemcpyAsync(out, dout.p, 4 * n, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    sync(ctx);
+  });
+}
+
+int refsig_gpu_attach_database(refsig_gpu_ctx* q, refsig_gpu_ctx* db) {
+  return guard(q, [&] {
+    require(db != nullptr && db != q, "bad database context");
+    require(db->device == q->device, "database on another device");
+    require(db->counted && db->have_ref, "database must be counted and have a reference");
+    q->db = db;
+    q->counted = false;
+    reset_downstream(q);
+  });
+}
+
+int refsig_gpu_mrc_query_pairs(refsig_gpu_ctx* q, float tau, uint64_t* out_pairs, uint64_t capacity,
+                               uint64_t* out_count) {
+  int rc2 = REFSIG_OK;
+  int rc = guard(q, [&] {
+    refsig_gpu_ctx* db = q->db;
+    require(db != nullptr, "no database attached");
+    require(q->signed_ && db->signed_, "sign() the queries and the database first");
+    require(q->K == db->K, "queries and database signed with different references");
+    require(out_count != nullptr, "out_count is NULL");
+    require(!std::isnan(tau), "tau is NaN");
+    require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
+    ck(cudaStreamSynchronize(db->stream), "sync database");
+    const PairGrid g{q->n_docs, db->n_docs, words_per_row(db->n_docs), false};
+    prepare_bitmap(q, g, false);
+    launch_mrc_bitmap(q->Sn.as<float>(), db->Sn.as<float>(), q->K, tau, g, q->bitmap.as<uint32_t>(),
+                      q->rowcnt.as<uint32_t>(), q->stream);
+    launched("mrc query bitmap");
+    rc2 = run_emit(q, g, out_pairs, capacity, out_count);
+  });
+  return rc != REFSIG_OK ? rc : rc2;
+}
+
+int refsig_gpu_hamming_query_pairs(refsig_gpu_ctx* q, int max_dist, uint64_t* out_pairs, uint64_t capacity,
+                                   uint64_t* out_count) {
+  int rc2 = REFSIG_OK;
+  int rc = guard(q, [&] {
+    refsig_gpu_ctx* db = q->db;
+    require(db != nullptr, "no database attached");
+    require(q->have_fp && db->have_fp, "simhash() the queries and the database first");
+    require(out_count != nullptr, "out_count is NULL");
+    require(max_dist >= 0 && max_dist <= 64, "max_dist must be in [0, 64]");
+    require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
+    ck(cudaStreamSynchronize(db->stream), "sync database");
+    const PairGrid g{q->n_docs, db->n_docs, words_per_row(db->n_docs), false};
+    prepare_bitmap(q, g, false);
+    launch_hamming_bitmap(q->fp.as<uint64_t>(), db->fp.as<uint64_t>(), max_dist, g, q->bitmap.as<uint32_t>(),
+                          q->rowcnt.as<uint32_t>(), q->stream);
+    launched("hamming query bitmap");
+    rc2 = run_emit(q, g, out_pairs, capacity, out_count);
+  });
+  return rc != REFSIG_OK ? rc : rc2;
+}
+
+int refsig_gpu_get_pairs(refsig_gpu_ctx* ctx, uint64_t* out_pairs, uint64_t capacity) {
+  return guard(ctx, [&] {
+    require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
+    const uint64_t m = std::min(capacity, ctx->cand_count);
+    if (m) ck(cudaMemcpyAsync(out_pairs, ctx->cand.p, 8 * m, cudaMemcpyDeviceToHost, ctx->stream), "D2H pairs");
+    sync(ctx);
+  });
+}
+
+int refsig_gpu_device_buffer(refsig_gpu_ctx* ctx, int which, void** ptr, uint64_t* bytes) {
+  return guard(ctx, [&] {
+    require(ptr && bytes, "NULL output");
+    switch (which) {
+      case REFSIG_BUF_PAIRS:
+        *ptr = ctx->cand.p;
+        *bytes = ctx->cand_count * 8;
+        break;
+      case REFSIG_BUF_SIGNATURES:
+        require(ctx->signed_, "sign() not called");
+        *ptr = ctx->S.p;
+        *bytes = 4ull * ctx->n_docs * ctx->K;
+        break;
+      case REFSIG_BUF_DF:
+        require(ctx->counted, "count() not called");
+        *ptr = ctx->df.p;
+        *bytes = 4ull * ctx->vocab;
+        break;
+      case REFSIG_BUF_FINGERPRINTS:
+        require(ctx->have_fp, "simhash() not called");
+        *ptr = ctx->fp.p;
+        *bytes = 8ull * ctx->n_docs;
+        break;
+      default:
+        fail(REFSIG_E_VALIDATION, "unknown buffer");
+    }
+  });
+}
+
+}  // extern "C"

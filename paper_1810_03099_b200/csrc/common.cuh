@@ -1,0 +1,58 @@
+// common.cuh — shared device helpers for the refsig B200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace refsig_gpu {
+
+constexpr int kWarp = 32;
+constexpr uint32_t kPadKey = 0xFFFFFFFFu;
+constexpr int kTile = 128;  // pair-tile edge (rows and columns) of the all-pairs kernels
+
+// Packed per-term info gathered once per nonzero: x = idf32 bits, y = row of
+// the term in the compact reference table (or -1 when not in the union U).
+struct TermInfo {
+  float idf;
+  int32_t ref_row;
+};
+static_assert(sizeof(TermInfo) == 8, "TermInfo is one 8-byte gather");
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
+  return __reduce_add_sync(0xffffffffu, v);
+}
+
+// Inclusive warp scan (Kogge-Stone over shuffles).
+__device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+// splitmix64 term hash, SURVEY.md Appendix A6 (replaces the MD5 word hash of
+// reference simhash.hpp:23-29 for integer term ids).
+__device__ __forceinline__ uint64_t term_hash64(uint64_t seed, uint32_t t) {
+  uint64_t z = seed + (static_cast<uint64_t>(t) + 1ull) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+}  // namespace refsig_gpu

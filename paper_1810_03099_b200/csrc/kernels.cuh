@@ -1,0 +1,142 @@
+// kernels.cuh — launcher declarations for the refsig B200 kernels.
+//
+// K1 count  : per-doc sort + run-length encode, df, idf      (ngram.hpp:62-75,170-178)
+// K2 sign   : warp-per-doc gather against the compact reference table
+// K3 pairs  : all-pairs signature compare -> pair bitmap -> sorted keys
+// K4 simhash: exact column sums + ballot-free bit build; Hamming pairs (simhash.hpp:35-47)
+// K5 exact  : exact sparse cosine verifier (ngram.hpp:184-202)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace refsig_gpu {
+
+// ---- K1 -------------------------------------------------------------------
+// Length bins of the count kernel; docs longer than kCountSmemMax are sorted
+// in a global scratch region (next_pow2(len) keys each).
+constexpr uint32_t kBinCap[4] = {256, 1024, 4096, 8192};
+constexpr uint32_t kCountSmemMax = 8192;
+
+struct CountArgs {
+  const uint32_t* tokens;
+  const uint64_t* doc_off;
+  uint32_t vocab;
+  uint2* ent;        // padded CSR: doc d's (id,count) rows at ent[doc_off[d] ..)
+  uint32_t* nnz;     // [n_docs]
+  uint32_t* df;      // [vocab], zeroed by the launcher
+  uint32_t* err;     // bit 0: token id >= vocab
+};
+
+void launch_count_bin(int bin, const CountArgs& a, const uint32_t* bin_docs, uint32_t n_bin, cudaStream_t s);
+void launch_count_large(const CountArgs& a, const uint32_t* long_docs, const uint64_t* scratch_off,
+                        uint32_t n_long, uint32_t* scratch, cudaStream_t s);
+// idf32[t] = fl32(ln((1+N)/(1+df))+1) (or 1 for raw-TF weighting); ref_row = -1.
+void launch_idf(const uint32_t* df, uint32_t vocab, uint32_t n_docs, int weight_mode, TermInfo* info,
+                cudaStream_t s);
+// Compact padded CSR -> rowptr/ids/counts (rowptr from an exclusive scan of nnz).
+void launch_compact_csr(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const uint64_t* rowptr,
+                        uint32_t n_docs, uint32_t* ids, uint32_t* counts, cudaStream_t s);
+// inv_norm[d] = 1/||w_d|| (0 for an empty doc), w = count*idf.
+void launch_inv_norm(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const TermInfo* info,
+                     uint32_t n_docs, float* inv_norm, cudaStream_t s);
+
+// ---- scans ----------------------------------------------------------------
+// out[0..n] = exclusive prefix of in[0..n) (out[n] = total). tmp >= scan_tmp_bytes(n).
+size_t scan_tmp_bytes(uint64_t n);
+void launch_exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp, cudaStream_t s);
+
+// ---- A5 reference table ----------------------------------------------------
+// K reference vectors, vector k = ent[start[k] .. start[k]+n[k]) with unique
+// ids. Docs mode: ent.y is a count (w = count*idf). Explicit mode: ent.y holds
+// the float bits of the raw weight (partition vectors use 1.0).
+struct RefArgs {
+  uint32_t K;
+  const uint64_t* start;
+  const uint32_t* n;
+  const uint2* ent;
+  bool explicit_w;
+};
+// start/n of K reference docs taken from the padded CSR.
+void launch_ref_doc_ranges(const uint64_t* doc_off, const uint32_t* nnz, const uint32_t* ref_docs, uint32_t K,
+                           uint64_t* start, uint32_t* n, cudaStream_t s);
+// flags[t] = 1 for every t in the union U (flags zeroed by the caller).
+void launch_ref_mark(const RefArgs& r, uint32_t* flags, cudaStream_t s);
+// info[t].ref_row = flags[t] ? prefix[t] : -1
+void launch_ref_remap(const uint32_t* flags, const uint64_t* prefix, uint32_t vocab, TermInfo* info, cudaStream_t s);
+// R[row*K + k] = w_k[t]/||w_k|| (R zeroed by the caller).
+void launch_ref_fill(const RefArgs& r, const TermInfo* info, float* R, cudaStream_t s);
+
+// ---- K2 sign ----------------------------------------------------------------
+struct SignArgs {
+  const uint2* ent;
+  const uint64_t* doc_off;
+  const uint32_t* nnz;
+  const TermInfo* info;
+  const float* R;
+  uint32_t n_docs;
+  uint32_t K;
+  float* S;         // [n_docs*K] raw cosines, row-major (API output)
+  float* Sn;        // [n_docs*K] unit-normalised signatures (K3 operand; 0 row if all-zero)
+  float* inv_norm;  // [n_docs] 1/||w_d||
+};
+void launch_sign(const SignArgs& a, cudaStream_t s);
+
+// ---- K3 / K4b pair bitmaps --------------------------------------------------
+// bitmap: row-major, words_per_row = n_pad_cols/32. Bits (i,j) set iff pair
+// matches; only tiles with col-tile >= row-tile are written (i<j triangle) for
+// the self-join, all tiles for the query join. rowcnt[i] += matches in row i.
+struct PairGrid {
+  uint32_t n_rows;      // rows (queries for a join)
+  uint32_t n_cols;      // columns (= n_rows for a self-join)
+  uint32_t words_per_row;
+  bool triangle;        // self-join: only j > i
+};
+void launch_mrc_bitmap(const float* Sn_rows, const float* Sn_cols, uint32_t K, float tau, const PairGrid& g, uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s);
+void launch_hamming_bitmap(const uint64_t* f_rows, const uint64_t* f_cols, int max_dist, const PairGrid& g,
+                           uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s);
+// keys (i<<32|j) in ascending order at rowstart[i]..; writes only < capacity.
+void launch_emit_pairs(const uint32_t* bitmap, const PairGrid& g, const uint32_t* rowcnt, const uint64_t* rowstart,
+                       uint64_t* out, uint64_t capacity, cudaStream_t s);
+
+// ---- K4a simhash -------------------------------------------------------------
+struct SimhashArgs {
+  const uint2* ent;
+  const uint64_t* doc_off;
+  const uint32_t* nnz;
+  const TermInfo* info;
+  const uint64_t* term_hash;  // optional [vocab] table (NULL: splitmix64 with seed)
+  uint64_t seed;
+  uint32_t n_docs;
+  bool use_idf;               // false: raw TF weights (the reference's +-1 per occurrence)
+  uint64_t* fp;
+};
+void launch_simhash(const SimhashArgs& a, cudaStream_t s);
+
+// ---- K5 exact cosine --------------------------------------------------------
+struct ExactArgs {
+  const uint2* ent;
+  const uint64_t* doc_off;
+  const uint32_t* nnz;
+  const float* x;          // unit weights aligned with ent (padded CSR)
+  const uint64_t* post_off;  // [vocab+1] postings offsets (exclusive scan of df)
+  const uint2* posts;      // (doc, x bits) per posting
+  uint32_t n_docs;
+  float tau;
+  float* acc_pool;         // exact_pool_ctas() * n_docs floats, zero on entry and exit
+  uint32_t* bitmap;        // zeroed rows, words_per_row words each
+  uint32_t words_per_row;
+  uint32_t* rowcnt;
+};
+uint32_t exact_pool_ctas();
+void launch_unit_weights(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const TermInfo* info,
+                         const float* inv_norm, uint32_t n_docs, float* x, cudaStream_t s);
+void launch_postings_fill(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const float* x,
+                          uint32_t n_docs, uint64_t* fill, uint2* posts, cudaStream_t s);
+void launch_exact_rows(const ExactArgs& a, uint32_t row_lo, uint32_t row_hi, cudaStream_t s);
+void launch_pair_cosines(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const float* x,
+                         const uint64_t* keys, uint64_t n_keys, float* out, cudaStream_t s);
+
+}  // namespace refsig_gpu

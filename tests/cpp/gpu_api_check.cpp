@@ -1,0 +1,54 @@
+// gpu_api_check.cpp — exercises the C++ host API (include/refsig/gpu.hpp) on
+// the reference SPEC's known answers. Run by tests/test_gpu_cpp_api.py on a
+// GPU box; exits non-zero on any mismatch.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "refsig/gpu.hpp"
+
+#define EXPECT(c)                                                  \
+  do {                                                             \
+    if (!(c)) {                                                    \
+      std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #c); \
+      std::exit(1);                                                \
+    }                                                              \
+  } while (0)
+
+int main() {
+  using refsig::gpu::Context;
+  using refsig::gpu::Weighting;
+  // 3-gram ids (ngram.hpp:33-37): abc=28, bca=728, cab=1353, xyz=16197.
+  // docs: "abcabc", the same again, and "xyz".
+  std::vector<uint32_t> tokens = {28, 728, 1353, 28, 28, 728, 1353, 28, 16197};
+  std::vector<uint64_t> off = {0, 4, 8, 9};
+  Context ctx(0);
+  ctx.load_corpus(tokens, off, 17576);
+  ctx.count(Weighting::tf);
+  auto m = ctx.counts();
+  // "abcabc" -> {abc:2, bca:1, cab:1}
+  EXPECT(m.rowptr[1] == 3 && m.ids[0] == 28 && m.counts[0] == 2 && m.ids[1] == 728 && m.counts[1] == 1);
+  // partitions [{abc}], [{xyz}] -> [2/sqrt(6), 0]
+  ctx.set_reference_partitions({{28}, {16197}});
+  auto S = ctx.sign();
+  EXPECT(std::fabs(S[0] - 2.0 / std::sqrt(6.0)) < 1e-6 && S[1] == 0.0f);
+  EXPECT(S[4] == 0.0f && std::fabs(S[5] - 1.0f) < 1e-6);  // "xyz" vs {xyz}
+  // compare: identical signatures -> 1; orthogonal -> 0 (:376)
+  auto p = ctx.mrc_pairs(0.999f);
+  EXPECT(p.size() == 1 && refsig::gpu::pair_first(p[0]) == 0 && refsig::gpu::pair_second(p[0]) == 1);
+  // hamming(x,x) = 0
+  auto fp = ctx.simhash(0, Weighting::tf);
+  EXPECT(fp[0] == fp[1]);
+  auto h = ctx.hamming_pairs(0);
+  EXPECT(h.size() == 1 && h[0] == p[0]);
+  // validation errors map to refsig::validation_error (error.hpp:8-14)
+  bool threw = false;
+  try {
+    ctx.set_reference_docs({});
+  } catch (const refsig::validation_error&) {
+    threw = true;
+  }
+  EXPECT(threw);
+  std::printf("gpu_api_check OK\n");
+  return 0;
+}
