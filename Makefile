@@ -24,7 +24,7 @@ ORC_LIB := oracle/liboracle.so
 REF_LIB := oracle/_ref/librefshim.so
 CPP_CHK := $(LIBDIR)/refsig_gpu_cpp_check
 
-all: $(GPU_LIB) $(GEN_LIB) $(ORC_LIB) $(CPP_CHK)
+all: $(GPU_LIB) $(GEN_LIB) $(ORC_LIB) $(CPP_CHK) tools
 
 $(BUILD)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(BUILD)
@@ -54,3 +54,9 @@ clean:
 	rm -rf $(BUILD) $(LIBDIR)/*.so $(CPP_CHK) $(ORC_LIB) $(REF_LIB)
 
 .PHONY: all ref clean
+
+TOOLS := tools/alu_peaks
+tools: $(TOOLS)
+tools/alu_peaks: tools/alu_peaks.cu
+	$(NVCC) -O3 -std=c++17 $(ARCH) -lineinfo --extended-lambda $< -o $@
+.PHONY: tools

@@ -1,0 +1,454 @@
+#!/usr/bin/env python3
+"""bench.py — MRC batch-similarity path on B200 (BASELINE.json metric).
+
+One step = one pass of the hot path over the configs[1] stand-in corpus
+(18,846 docs, K=20), everything device-resident when the timed region starts:
+  K1 count (sort+RLE, df, idf) -> A5 reference table -> K2 sign ->
+  K3 all-pairs compare (tau_mrc) -> row-count scan -> sorted key emission.
+value = all i<j doc-pairs of the corpus / step time (doc-pairs/s, whole job).
+signatures_per_sec = docs / (K1+A5+K2 time).
+
+The L2 is flushed (512 MB write) before every timed step. Times are CUDA
+events on the stream the library launches on, max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference CPU path (the oracle restatement in
+oracle/; the reference has no MRC sign/compare code) on this host's cores.
+N>1 (torchrun): the pair triangle is split into row panels (shard.py), K1/K2
+are replicated per rank (no data-path collective), scaling "strong".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "MRC doc-pairs/sec (all-pairs) and signatures/sec at 1 GPU; % of roofline"
+UNIT = "doc-pairs/s"
+L2_FLUSH_BYTES = 512 << 20
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def load_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def corpus_and_config(name):
+    from paper_1810_03099_b200 import corpus as C
+    cfgs = C.load_configs()
+    cp, cfg = C.config_corpus(name)
+    refs = C.sample_refs(cfg["ref_seed"], cp.n_docs, cfg["K"])
+    return cp, cfg, refs, cfgs["thresholds"]
+
+
+# --------------------------------------------------------------------------
+# CPU baseline: the oracle restatement on the host's cores (test infrastructure
+# executed here only as the timed baseline, never as the measured product).
+# --------------------------------------------------------------------------
+
+def cpu_pipeline_once(cp, refs, tau, threads):
+    import oracle
+    t0 = time.perf_counter()
+    o = oracle.mrc_pipeline(cp.tokens, cp.doc_off, cp.vocab, refs, "tfidf", threads)
+    t1 = time.perf_counter()
+    pairs, _ = oracle.mrc_pairs(o.S, tau, 1e-5, threads=threads)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, len(pairs)
+
+
+def cpu_baseline(cp, refs, tau):
+    threads = os.cpu_count() or 1
+    ts, tp, npairs = cpu_pipeline_once(cp, refs, tau, threads)
+    n = cp.n_docs
+    P = n * (n - 1) // 2
+    return {"value": P / (ts + tp), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"full configs[1] workload once: oracle count+tfidf+sign ({ts:.2f}s) + all {P} pairs "
+                      f"compare ({tp:.2f}s), {threads} threads",
+            "signatures_per_sec": n / ts, "pairs_per_sec_compare_only": P / tp, "candidates": npairs,
+            "cpu_model": cpu_model()}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    cp, cfg, refs, thr = corpus_and_config(args.config)
+    tau = args.tau if args.tau is not None else thr["tau_mrc"]
+    threads = os.cpu_count() or 1
+    n = cp.n_docs
+    P = n * (n - 1) // 2
+    for _ in range(args.warmup):
+        cpu_pipeline_once(cp, refs, tau, threads)
+    times = []
+    for _ in range(args.steps):
+        ts, tp, npairs = cpu_pipeline_once(cp, refs, tau, threads)
+        times.append(ts + tp)
+    t = sum(times)
+    v = P * args.steps / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": data_desc(cfg),
+            "config": workload_config(cfg, cp, tau, world),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"each step = full configs[1] MRC pipeline on the CPU (oracle restatement "
+                                       f"of SPEC.md:360-377; the reference ships no MRC code), {threads} threads",
+                             "cpu_model": cpu_model()},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def data_desc(cfg):
+    return ("synthetic: seeded stand-in for configs[1] (NEWS20 absent) — 20 topic Zipf(1.05) mixtures 70/30, "
+            "lognormal lengths (median 220, sigma 1.0), 5% near-dups with 10% resampling; see configs/mrc_configs.json")
+
+
+def workload_config(cfg, cp, tau, world):
+    return {"workload": f"configs[1]: {cp.n_docs} docs, vocab {cp.vocab}, K={cfg['K']} reference docs, TF-IDF fp32, "
+                        f"all-pairs MRC compare at tau={tau} with sorted candidate emission",
+            "n_docs": cp.n_docs, "tokens": int(cp.doc_off[-1]), "K": cfg["K"], "tau": tau,
+            "pairs_per_step": cp.n_docs * (cp.n_docs - 1) // 2,
+            "l2": "flushed before every timed step (512 MB write); inputs < L2 otherwise",
+            "parallelism": f"pair-triangle row panels x{world}" if world > 1 else "single GPU"}
+
+
+# --------------------------------------------------------------------------
+# Our arm
+# --------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import paper_1810_03099_b200 as R
+    from paper_1810_03099_b200 import shard
+
+    world, rank, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    cp, cfg, refs, thr = corpus_and_config(args.config)
+    tau = args.tau if args.tau is not None else thr["tau_mrc"]
+    N, K = cp.n_docs, cfg["K"]
+    lo, hi = shard.row_shards(N, world)[rank]
+    my_pairs = shard.pairs_in_rows(N, lo, hi)
+    P = N * (N - 1) // 2
+
+    stream = torch.cuda.Stream(dev)
+    ctx = R.Context(local)
+    ctx.set_stream(stream.cuda_stream)
+    tok_dev = torch.from_numpy(cp.tokens.view(np.int32)).to(dev)
+    ctx.load_corpus_device(tok_dev.data_ptr(), cp.doc_off, cp.vocab)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+
+    def step():
+        ctx.count(R.WEIGHT_TFIDF)
+        ctx.set_reference_docs(refs)
+        ctx.sign(fetch=False)
+
+    def pairs():
+        return ctx.mrc_pairs_rows(tau, lo, hi, fetch=False)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            flush.fill_(1)
+            step()
+            n_cand = pairs()
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        clocks = ClockSampler(local)
+        clocks.start()
+        time.sleep(0.3)
+        ctx.set_profiling(True)
+        l0 = R.Context.launch_count()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+               torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for s in range(args.steps):
+            flush.fill_(s)
+            ev[s][0].record(stream)
+            step()
+            ev[s][1].record(stream)
+            n_cand = pairs()
+            ev[s][2].record(stream)
+        torch.cuda.synchronize(dev)
+        launches = R.Context.launch_count() - l0
+        phases = ctx.phase_times()
+        ctx.set_profiling(False)
+        clk = clocks.stop()
+    step_ms = [a.elapsed_time(c) for a, b, c in ev]
+    sign_ms = [a.elapsed_time(b) for a, b, c in ev]
+    tot_ms = sum(step_ms)
+    tot_sign = sum(sign_ms)
+    if dist:
+        t = torch.tensor([tot_ms, tot_sign], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms, tot_sign = t.tolist()
+        c = torch.tensor([n_cand], dtype=torch.int64, device=dev)
+        dist.all_reduce(c)
+        n_cand = int(c.item())
+    ms_per_step = tot_ms / args.steps
+    value = P / (ms_per_step / 1e3)
+    sig_per_s = N / (tot_sign / args.steps / 1e3)
+
+    # Isolated K2 with a cold L2 (HBM roofline of the signature kernel).
+    sign_iso = measure_sign_isolated(ctx, stream, flush, dev, reps=max(5, args.steps))
+
+    # End to end through the public API with HOST buffers: pinned tokens H2D,
+    # full pipeline, candidate keys D2H into pinned memory.
+    e2e = measure_e2e(ctx, cp, refs, tau, lo, hi, stream, dev, steps=args.steps, warmup=2)
+    if dist:
+        t = torch.tensor([e2e["_ms"]], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e["_ms"] = t.item()
+    e2e_value = P / (e2e["_ms"] / 1e3)
+
+    if rank == 0:
+        peaks, peaks_src = load_peaks()
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        clock_mhz = clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+        roof = rooflines(phases, sign_iso, N, K, P if world == 1 else my_pairs, cp, peaks, peaks_src, n_sm,
+                         clock_mhz, ms_per_step)
+        traffic = load_traffic()
+        for k, r in roof.items():
+            r["traffic"] = traffic.get(k)
+        dominant = max(("mrc_tiles", "sign", "count", "pair_emit"), key=lambda k: roof[k]["share_of_step"])
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": data_desc(cfg),
+                "config": workload_config(cfg, cp, tau, world),
+                "signatures_per_sec": sig_per_s, "candidates_per_step": n_cand,
+                "roofline": {**roof[dominant], "kernel": dominant},
+                "rooflines": roof,
+                "phase_ms_per_step": {k: v[0] / args.steps for k, v in phases.items() if v[1]},
+                "clocks": clk, "gpu_launches": int(launches),
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
+                        "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["_ms"],
+                        "note": "load_corpus(pinned host tokens) + count + reference + sign + mrc_pairs with the "
+                                "sorted keys copied to pinned host memory; host wall clock, synchronised"}}
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cp, refs, tau)
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def measure_sign_isolated(ctx, stream, flush, dev, reps):
+    import torch
+    ms = []
+    with torch.cuda.stream(stream):
+        ctx.set_profiling(True)
+        for r in range(reps):
+            flush.fill_(r + 7)
+            ctx.sign(fetch=False)
+        torch.cuda.synchronize(dev)
+        ph = ctx.phase_times()
+        ctx.set_profiling(False)
+    t, calls = ph["sign"]
+    return t / max(calls, 1)
+
+
+def measure_e2e(ctx, cp, refs, tau, lo, hi, stream, dev, steps, warmup):
+    import torch
+    import paper_1810_03099_b200 as R
+    tok_pin = torch.from_numpy(cp.tokens.view(np.int32)).pin_memory()
+    tok_np = tok_pin.numpy().view(np.uint32)
+    n_guess = ctx.mrc_pairs_rows(tau, lo, hi, fetch=False)
+    out = torch.empty(int(n_guess * 1.1) + 1024, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    times = []
+    n = 0
+    for s in range(warmup + steps):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        ctx.load_corpus(tok_np, cp.doc_off, cp.vocab)
+        ctx.count(R.WEIGHT_TFIDF)
+        ctx.set_reference_docs(refs)
+        ctx.sign(fetch=False)
+        keys = ctx.mrc_pairs_rows(tau, lo, hi, out=out)
+        n = len(keys)
+        t1 = time.perf_counter()
+        if s >= warmup:
+            times.append(t1 - t0)
+    h2d = cp.tokens.nbytes + cp.doc_off.nbytes + refs.nbytes
+    return {"_ms": 1e3 * sum(times) / len(times), "h2d": int(h2d), "d2h": int(n * 8 + 8)}
+
+
+def rooflines(phases, sign_iso_ms, N, K, pairs, cp, peaks, peaks_src, n_sm, clock_mhz, ms_per_step):
+    """achieved = algorithmic work per launch / average launch time (CUDA events)."""
+    def per_launch(name):
+        t, c = phases[name]
+        return (t / c if c else 0.0), c
+
+    out = {}
+    # K3: FP32 FMA bound, 2*K flop per pair (unit signatures: cosine = dot).
+    t3, _ = per_launch("pair_tiles")
+    fp32_peak = n_sm * 128 * 2 * clock_mhz * 1e6 / 1e12  # TFLOP/s at the clock sampled under load
+    ach = 2.0 * K * pairs / (t3 / 1e3) / 1e12 if t3 else 0.0
+    out["mrc_tiles"] = {"bound": "fp32", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
+                        "frac": ach / fp32_peak, "ms_per_launch": t3,
+                        "peak_source": f"{n_sm} SMs x 128 FFMA/clk x 2 x {clock_mhz:.0f} MHz (median SM clock "
+                                       f"sampled during the timed region)",
+                        "share_of_step": t3 / ms_per_step}
+    # K2: HBM bound; survey §8d per-signature bytes 8*nnz + 4*K + 4.
+    nnz = nnz_total(cp)
+    bytes_sign = 8 * nnz + (4 * K + 4) * N
+    t2, _ = per_launch("sign")
+    hbm = peaks["hbm_gbs"]
+    out["sign"] = {"bound": "hbm", "achieved": bytes_sign / (sign_iso_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                   "frac": bytes_sign / (sign_iso_ms / 1e3) / 1e9 / hbm, "ms_per_launch": sign_iso_ms,
+                   "ms_per_launch_in_step": t2, "peak_source": peaks_src,
+                   "note": "isolated launch after an L2 flush (in-step K2 reads K1's output from L2)",
+                   "share_of_step": t2 / ms_per_step}
+    # K1: HBM bound; 4*tokens + 8*nnz + 4 per doc (+4*V df).
+    t1, _ = per_launch("count")
+    bytes_count = 4 * int(cp.doc_off[-1]) + 8 * nnz + 12 * N + 12 * cp.vocab
+    out["count"] = {"bound": "hbm", "achieved": bytes_count / (t1 / 1e3) / 1e9 if t1 else 0.0, "peak": hbm,
+                    "unit": "GB/s", "frac": (bytes_count / (t1 / 1e3) / 1e9 / hbm) if t1 else 0.0,
+                    "ms_per_launch": t1, "peak_source": peaks_src, "share_of_step": t1 / ms_per_step}
+    te, _ = per_launch("pair_emit")
+    out["pair_emit"] = {"bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
+                        "ms_per_launch": te, "share_of_step": te / ms_per_step}
+    return out
+
+
+_NNZ = {}
+
+
+def nnz_total(cp):
+    key = id(cp)
+    if key not in _NNZ:
+        tot = 0
+        off = cp.doc_off
+        for d in range(cp.n_docs):
+            tot += len(np.unique(cp.tokens[off[d]:off[d + 1]]))
+        _NNZ[key] = tot
+    return _NNZ[key]
+
+
+def load_traffic():
+    """Per-launch DRAM bytes from the committed ncu summary, if any."""
+    p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--tau", type=float, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        log("note: warmup < 3 is below the timing contract")
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

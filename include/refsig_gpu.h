@@ -120,6 +120,12 @@ int refsig_gpu_get_signatures(refsig_gpu_ctx* ctx, float* S);
 int refsig_gpu_mrc_pairs(refsig_gpu_ctx* ctx, float tau, uint64_t* out_pairs, uint64_t capacity,
                          uint64_t* out_count);
 
+/* Rows [row_lo, row_hi) of the same triangle (pairs i<j with row_lo <= i <
+ * row_hi): the unit a rank owns when the triangle is sharded across GPUs.
+ * Row ranges are aligned to the 128-row tile internally; keys are global. */
+int refsig_gpu_mrc_pairs_rows(refsig_gpu_ctx* ctx, float tau, uint32_t row_lo, uint32_t row_hi, uint64_t* out_pairs,
+                              uint64_t capacity, uint64_t* out_count);
+
 /* ---- K4: Simhash + Hamming (A8-A10) -----------------------------------------
  * weight_mode as above (TF reproduces the reference's per-occurrence rule).
  * term_hash: optional HOST table of vocab 64-bit hashes (e.g. word_hash64 of
@@ -154,6 +160,25 @@ int refsig_gpu_get_pairs(refsig_gpu_ctx* ctx, uint64_t* out_pairs, uint64_t capa
 #define REFSIG_BUF_DF 2         /* uint32 df[vocab] */
 #define REFSIG_BUF_FINGERPRINTS 3
 int refsig_gpu_device_buffer(refsig_gpu_ctx* ctx, int which, void** ptr, uint64_t* bytes);
+
+/* ---- measurement -------------------------------------------------------------
+ * With profiling on, every phase below is bracketed by CUDA events recorded on
+ * the context's stream (the stream its kernels run on). phase_times syncs and
+ * returns the summed device time (ms) and call count per phase since the last
+ * set_profiling call. */
+#define REFSIG_PHASE_COUNT 0      /* K1: sort + RLE + df + idf */
+#define REFSIG_PHASE_REFERENCE 1  /* A5: union, remap, reference table */
+#define REFSIG_PHASE_SIGN 2       /* K2 */
+#define REFSIG_PHASE_PAIR_TILES 3 /* K3 / K4b / K5 tile kernel */
+#define REFSIG_PHASE_PAIR_EMIT 4  /* row-count scan + sorted key emission */
+#define REFSIG_PHASE_SIMHASH 5    /* K4a */
+#define REFSIG_PHASE_H2D 6        /* corpus upload */
+#define REFSIG_PHASE_D2H 7        /* result download */
+#define REFSIG_N_PHASES 8
+int refsig_gpu_set_profiling(refsig_gpu_ctx* ctx, int on);
+int refsig_gpu_phase_times(refsig_gpu_ctx* ctx, double* ms, uint64_t* calls);
+/* Kernels launched by this library in this process so far. */
+uint64_t refsig_gpu_launch_count(void);
 
 #ifdef __cplusplus
 }

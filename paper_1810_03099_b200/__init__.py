@@ -93,7 +93,13 @@ SIGNATURES = {
                                        _c.c_int),
     "refsig_gpu_get_pairs": ([_c.c_void_p, _P(_c.c_uint64), _c.c_uint64], _c.c_int),
     "refsig_gpu_device_buffer": ([_c.c_void_p, _c.c_int, _P(_c.c_void_p), _P(_c.c_uint64)], _c.c_int),
+    "refsig_gpu_mrc_pairs_rows": ([_c.c_void_p, _c.c_float, _c.c_uint32, _c.c_uint32, _P(_c.c_uint64), _c.c_uint64,
+                                   _P(_c.c_uint64)], _c.c_int),
+    "refsig_gpu_set_profiling": ([_c.c_void_p, _c.c_int], _c.c_int),
+    "refsig_gpu_phase_times": ([_c.c_void_p, _P(_c.c_double), _P(_c.c_uint64)], _c.c_int),
+    "refsig_gpu_launch_count": ([], _c.c_uint64),
 }
+PHASES = ["count", "reference", "sign", "pair_tiles", "pair_emit", "simhash", "h2d", "d2h"]
 
 _lib = None
 
@@ -287,6 +293,40 @@ class Context:
     def mrc_pairs(self, tau: float, out: np.ndarray | None = None, fetch: bool = True):
         """Sorted keys (i<<32|j) of all i<j with compare(S_i,S_j) >= tau."""
         return self._pairs(self._L.refsig_gpu_mrc_pairs, ctypes.c_float(tau), out, fetch)
+
+    def mrc_pairs_rows(self, tau: float, row_lo: int, row_hi: int, out: np.ndarray | None = None,
+                       fetch: bool = True):
+        """Pairs i<j with row_lo <= i < row_hi (a rank's shard of the triangle)."""
+        n = ctypes.c_uint64()
+        if out is not None:
+            rc = self._L.refsig_gpu_mrc_pairs_rows(self._h, ctypes.c_float(tau), row_lo, row_hi,
+                                                   _ptr(out, ctypes.c_uint64), len(out), ctypes.byref(n))
+            self._check(rc, n.value)
+            return out[: n.value]
+        rc = self._L.refsig_gpu_mrc_pairs_rows(self._h, ctypes.c_float(tau), row_lo, row_hi, None, 0,
+                                               ctypes.byref(n))
+        self._check(rc, n.value)
+        if not fetch:
+            return n.value
+        keys = np.empty(n.value, np.uint64)
+        if n.value:
+            self._check(self._L.refsig_gpu_get_pairs(self._h, _ptr(keys, ctypes.c_uint64), n.value))
+        return keys
+
+    # -- measurement ----------------------------------------------------------
+    def set_profiling(self, on: bool):
+        self._check(self._L.refsig_gpu_set_profiling(self._h, 1 if on else 0))
+
+    def phase_times(self) -> dict:
+        """{phase: (total_ms, calls)} since set_profiling (events on this stream)."""
+        ms = (ctypes.c_double * len(PHASES))()
+        calls = (ctypes.c_uint64 * len(PHASES))()
+        self._check(self._L.refsig_gpu_phase_times(self._h, ms, calls))
+        return {p: (ms[i], calls[i]) for i, p in enumerate(PHASES)}
+
+    @staticmethod
+    def launch_count() -> int:
+        return load_library().refsig_gpu_launch_count()
 
     def simhash(self, seed: int = 0, weighting: int = WEIGHT_TFIDF, term_hash: np.ndarray | None = None,
                 fetch: bool = True):

@@ -15,6 +15,16 @@
 
 using namespace refsig_gpu;
 
+#include <atomic>
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+}  // namespace
+
+namespace refsig_gpu {
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace refsig_gpu
+
 namespace {
 
 struct Status {
@@ -112,6 +122,30 @@ struct refsig_gpu_ctx {
 
   // query mode
   refsig_gpu_ctx* db = nullptr;
+
+  // pinned staging for small uploads (no hidden stream sync of pageable H2D)
+  void* h_stage = nullptr;
+  size_t stage_cap = 0;
+  cudaEvent_t stage_done = nullptr;
+
+  // profiling: event pairs per phase on `stream`, resolved lazily
+  bool prof = false;
+  struct Mark {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  std::vector<Mark> marks;
+  std::vector<cudaEvent_t> ev_free;
+
+  ~refsig_gpu_ctx() {
+    for (auto& m : marks) {
+      cudaEventDestroy(m.a);
+      cudaEventDestroy(m.b);
+    }
+    for (auto e : ev_free) cudaEventDestroy(e);
+    if (h_stage) cudaFreeHost(h_stage);
+    if (stage_done) cudaEventDestroy(stage_done);
+  }
 };
 
 namespace {
@@ -151,6 +185,61 @@ void sync(refsig_gpu_ctx* c) {
 
 void launched(const char* what) { ck(cudaGetLastError(), what); }
 
+cudaEvent_t take_event(refsig_gpu_ctx* c) {
+  if (!c->ev_free.empty()) {
+    cudaEvent_t e = c->ev_free.back();
+    c->ev_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  ck(cudaEventCreate(&e), "cudaEventCreate");
+  return e;
+}
+
+// RAII: brackets the enqueued work of one phase with events on ctx->stream.
+struct Phase {
+  refsig_gpu_ctx* c;
+  int id;
+  cudaEvent_t a = nullptr;
+  Phase(refsig_gpu_ctx* ctx, int phase) : c(ctx), id(phase) {
+    if (!c->prof) return;
+    a = take_event(c);
+    ck(cudaEventRecord(a, c->stream), "cudaEventRecord");
+  }
+  ~Phase() {
+    if (!a) return;
+    cudaEvent_t b = nullptr;
+    if (!c->ev_free.empty()) {
+      b = c->ev_free.back();
+      c->ev_free.pop_back();
+    } else if (cudaEventCreate(&b) != cudaSuccess) {
+      c->ev_free.push_back(a);
+      return;
+    }
+    cudaEventRecord(b, c->stream);
+    c->marks.push_back({id, a, b});
+  }
+};
+
+// Copy a small host array to the device through the pinned staging buffer:
+// returns without waiting for the stream (the caller's buffer is free to reuse).
+void upload(refsig_gpu_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  if (!c->stage_done) ck(cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming), "event");
+  ck(cudaEventSynchronize(c->stage_done), "staging");  // previous upload consumed
+  if (bytes > c->stage_cap) {
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    c->h_stage = nullptr;
+    c->stage_cap = 0;
+    size_t cap = std::max<size_t>(bytes, 1 << 16);
+    ck(cudaMallocHost(&c->h_stage, cap), "cudaMallocHost");
+    c->stage_cap = cap;
+  }
+  std::memcpy(c->h_stage, src, bytes);
+  ck(cudaMemcpyAsync(dst, c->h_stage, bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
+  ck(cudaEventRecord(c->stage_done, c->stream), "event");
+}
+
 void reset_downstream(refsig_gpu_ctx* c) {
   c->have_ref = c->signed_ = c->have_fp = c->have_x = c->have_inv_norm = false;
   c->cand_count = 0;
@@ -164,18 +253,22 @@ int run_emit(refsig_gpu_ctx* c, const PairGrid& g, uint64_t* out, uint64_t capac
   const uint64_t n = g.n_rows;
   c->rowstart.ensure(sizeof(uint64_t) * (n + 1));
   c->scan_tmp.ensure(scan_tmp_bytes(n));
-  launch_exclusive_scan_u32_to_u64(c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(), n, c->scan_tmp.p,
-                                   c->stream);
   c->cand.ensure(sizeof(uint64_t) * (1u << 20));
   uint64_t cap_keys = c->cand.cap / sizeof(uint64_t);
-  launch_emit_pairs(c->bitmap.as<uint32_t>(), g, c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(),
-                    c->cand.as<uint64_t>(), cap_keys, c->stream);
-  launched("emit");
+  {
+    Phase ph(c, REFSIG_PHASE_PAIR_EMIT);
+    launch_exclusive_scan_u32_to_u64(c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(), n, c->scan_tmp.p,
+                                     c->stream);
+    launch_emit_pairs(c->bitmap.as<uint32_t>(), g, c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(),
+                      c->cand.as<uint64_t>(), cap_keys, c->stream);
+    launched("emit");
+  }
   ck(cudaMemcpyAsync(c->h_pin, c->rowstart.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, c->stream), "D2H count");
   sync(c);
   const uint64_t total = c->h_pin[0];
   if (total > cap_keys) {
     c->cand.ensure(sizeof(uint64_t) * (total + total / 4 + 1024));
+    Phase ph(c, REFSIG_PHASE_PAIR_EMIT);
     launch_emit_pairs(c->bitmap.as<uint32_t>(), g, c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(),
                       c->cand.as<uint64_t>(), c->cand.cap / sizeof(uint64_t), c->stream);
     launched("emit");
@@ -184,6 +277,7 @@ int run_emit(refsig_gpu_ctx* c, const PairGrid& g, uint64_t* out, uint64_t capac
   *out_count = total;
   if (out && capacity) {
     const uint64_t m = std::min(total, capacity);
+    Phase ph(c, REFSIG_PHASE_D2H);
     if (m) ck(cudaMemcpyAsync(out, c->cand.p, m * 8, cudaMemcpyDeviceToHost, c->stream), "D2H pairs");
   }
   sync(c);
@@ -210,14 +304,15 @@ void build_reference(refsig_gpu_ctx* c, const RefArgs& r, uint64_t u_cap) {
   c->ref_mark.ensure(sizeof(uint32_t) * V);
   c->ref_prefix.ensure(sizeof(uint64_t) * (V + 1));
   c->scan_tmp.ensure(scan_tmp_bytes(V));
+  if (u_cap > V) u_cap = V;
+  const size_t rbytes = sizeof(float) * std::max<uint64_t>(u_cap, 1) * r.K;
+  c->R.ensure(rbytes);
+  Phase ph(c, REFSIG_PHASE_REFERENCE);
   ck(cudaMemsetAsync(c->ref_mark.p, 0, sizeof(uint32_t) * V, c->stream), "memset");
   launch_ref_mark(r, c->ref_mark.as<uint32_t>(), c->stream);
   launch_exclusive_scan_u32_to_u64(c->ref_mark.as<uint32_t>(), c->ref_prefix.as<uint64_t>(), V, c->scan_tmp.p,
                                    c->stream);
   launch_ref_remap(c->ref_mark.as<uint32_t>(), c->ref_prefix.as<uint64_t>(), V, c->info.as<TermInfo>(), c->stream);
-  if (u_cap > V) u_cap = V;
-  const size_t rbytes = sizeof(float) * std::max<uint64_t>(u_cap, 1) * r.K;
-  c->R.ensure(rbytes);
   ck(cudaMemsetAsync(c->R.p, 0, rbytes, c->stream), "memset R");
   launch_ref_fill(r, c->info.as<TermInfo>(), c->R.as<float>(), c->stream);
   launched("reference");
@@ -298,7 +393,9 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
   reset_downstream(c);
 }
 
-PairGrid self_grid(const refsig_gpu_ctx* c) { return PairGrid{c->n_docs, c->n_docs, words_per_row(c->n_docs), true}; }
+PairGrid self_grid(const refsig_gpu_ctx* c) {
+  return PairGrid{c->n_docs, c->n_docs, words_per_row(c->n_docs), true, 0, c->n_docs, 0};
+}
 
 }  // namespace
 
@@ -362,9 +459,11 @@ int refsig_gpu_load_corpus(refsig_gpu_ctx* ctx, const uint32_t* tokens, const ui
     require(tokens != nullptr || doc_off[n_docs] == 0, "tokens is NULL");
     const uint64_t T = doc_off[n_docs];
     ctx->tokens.ensure(sizeof(uint32_t) * std::max<uint64_t>(T, 1));
-    if (T)
+    if (T) {
+      Phase ph(ctx, REFSIG_PHASE_H2D);
       ck(cudaMemcpyAsync(ctx->tokens.p, tokens, sizeof(uint32_t) * T, cudaMemcpyHostToDevice, ctx->stream),
          "H2D tokens");
+    }
     ctx->tok = ctx->tokens.as<uint32_t>();
     load_common(ctx, doc_off, n_docs, vocab);
   });
@@ -396,6 +495,7 @@ int refsig_gpu_count(refsig_gpu_ctx* ctx, int weight_mode) {
     ctx->df.ensure(sizeof(uint32_t) * V);
     ctx->info.ensure(sizeof(TermInfo) * V);
     if (ctx->flags.ensure(16)) ck(cudaMemsetAsync(ctx->flags.p, 0, 16, ctx->stream), "memset");
+    Phase ph(ctx, REFSIG_PHASE_COUNT);
     ck(cudaMemsetAsync(ctx->df.p, 0, sizeof(uint32_t) * V, ctx->stream), "memset df");
     CountArgs a{ctx->tok, ctx->doc_off.as<uint64_t>(), V, ctx->ent.as<uint2>(), ctx->nnz.as<uint32_t>(),
                 ctx->df.as<uint32_t>(), ctx->flags.as<uint32_t>()};
@@ -503,13 +603,11 @@ int refsig_gpu_set_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_i
     ctx->ref_docs.ensure(4ull * K);
     ctx->ref_start.ensure(8ull * K);
     ctx->ref_n.ensure(4ull * K);
-    ck(cudaMemcpyAsync(ctx->ref_docs.p, ref_doc_ids, 4ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D refs");
+    upload(ctx, ctx->ref_docs.p, ref_doc_ids, 4ull * K);
     launch_ref_doc_ranges(ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->ref_docs.as<uint32_t>(), K,
                           ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->stream);
     RefArgs r{K, ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->ent.as<uint2>(), false};
     build_reference(ctx, r, u_cap);
-    // the H2D source is a caller buffer: finish before returning
-    ck(cudaStreamSynchronize(ctx->stream), "reference");
   });
 }
 
@@ -580,8 +678,11 @@ int refsig_gpu_sign(refsig_gpu_ctx* ctx) {
     if (ctx->db) ck(cudaStreamSynchronize(ctx->db->stream), "sync database");
     SignArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->info.as<TermInfo>(),
                refc->R.as<float>(), N, K, ctx->S.as<float>(), ctx->Sn.as<float>(), ctx->inv_norm.as<float>()};
-    launch_sign(a, ctx->stream);
-    launched("sign");
+    {
+      Phase ph(ctx, REFSIG_PHASE_SIGN);
+      launch_sign(a, ctx->stream);
+      launched("sign");
+    }
     ctx->K = K;
     ctx->signed_ = true;
     ctx->have_inv_norm = true;
@@ -608,10 +709,13 @@ int refsig_gpu_mrc_pairs(refsig_gpu_ctx* ctx, float tau, uint64_t* out_pairs, ui
     require(!std::isnan(tau), "tau is NaN");
     require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
     const PairGrid g = self_grid(ctx);
-    prepare_bitmap(ctx, g, false);
-    launch_mrc_bitmap(ctx->Sn.as<float>(), ctx->Sn.as<float>(), ctx->K, tau, g, ctx->bitmap.as<uint32_t>(),
-                      ctx->rowcnt.as<uint32_t>(), ctx->stream);
-    launched("mrc bitmap");
+    {
+      Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
+      prepare_bitmap(ctx, g, false);
+      launch_mrc_bitmap(ctx->Sn.as<float>(), ctx->Sn.as<float>(), ctx->K, tau, g, ctx->bitmap.as<uint32_t>(),
+                        ctx->rowcnt.as<uint32_t>(), ctx->stream);
+      launched("mrc bitmap");
+    }
     rc2 = run_emit(ctx, g, out_pairs, capacity, out_count);
   });
   return rc != REFSIG_OK ? rc : rc2;
@@ -633,8 +737,11 @@ int refsig_gpu_simhash(refsig_gpu_ctx* ctx, uint64_t seed, int weight_mode, cons
     ctx->fp.ensure(8ull * ctx->n_docs);
     SimhashArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->info.as<TermInfo>(),
                   th, seed, ctx->n_docs, weight_mode == REFSIG_WEIGHT_TFIDF, ctx->fp.as<uint64_t>()};
-    launch_simhash(a, ctx->stream);
-    launched("simhash");
+    {
+      Phase ph(ctx, REFSIG_PHASE_SIMHASH);
+      launch_simhash(a, ctx->stream);
+      launched("simhash");
+    }
     if (term_hash) ck(cudaStreamSynchronize(ctx->stream), "simhash");
     ctx->have_fp = true;
   });
@@ -658,10 +765,13 @@ int refsig_gpu_hamming_pairs(refsig_gpu_ctx* ctx, int max_dist, uint64_t* out_pa
     require(max_dist >= 0 && max_dist <= 64, "max_dist must be in [0, 64]");
     require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
     const PairGrid g = self_grid(ctx);
-    prepare_bitmap(ctx, g, false);
-    launch_hamming_bitmap(ctx->fp.as<uint64_t>(), ctx->fp.as<uint64_t>(), max_dist, g, ctx->bitmap.as<uint32_t>(),
-                          ctx->rowcnt.as<uint32_t>(), ctx->stream);
-    launched("hamming bitmap");
+    {
+      Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
+      prepare_bitmap(ctx, g, false);
+      launch_hamming_bitmap(ctx->fp.as<uint64_t>(), ctx->fp.as<uint64_t>(), max_dist, g, ctx->bitmap.as<uint32_t>(),
+                            ctx->rowcnt.as<uint32_t>(), ctx->stream);
+      launched("hamming bitmap");
+    }
     rc2 = run_emit(ctx, g, out_pairs, capacity, out_count);
   });
   return rc != REFSIG_OK ? rc : rc2;
@@ -694,12 +804,15 @@ int refsig_gpu_exact_pairs(refsig_gpu_ctx* ctx, float tau_cos, uint64_t* out_pai
       ctx->acc_pool_docs = N;
     }
     const PairGrid g = self_grid(ctx);
-    prepare_bitmap(ctx, g, true);
-    ExactArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->x.as<float>(),
-                ctx->post_off.as<uint64_t>(), ctx->posts.as<uint2>(), N, tau_cos, ctx->acc_pool.as<float>(),
-                ctx->bitmap.as<uint32_t>(), g.words_per_row, ctx->rowcnt.as<uint32_t>()};
-    launch_exact_rows(a, 0, N, ctx->stream);
-    launched("exact");
+    {
+      Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
+      prepare_bitmap(ctx, g, true);
+      ExactArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->x.as<float>(),
+                  ctx->post_off.as<uint64_t>(), ctx->posts.as<uint2>(), N, tau_cos, ctx->acc_pool.as<float>(),
+                  ctx->bitmap.as<uint32_t>(), g.words_per_row, ctx->rowcnt.as<uint32_t>()};
+      launch_exact_rows(a, 0, N, ctx->stream);
+      launched("exact");
+    }
     rc2 = run_emit(ctx, g, out_pairs, capacity, out_count);
   });
   return rc != REFSIG_OK ? rc : rc2;
@@ -748,11 +861,14 @@ int refsig_gpu_mrc_query_pairs(refsig_gpu_ctx* q, float tau, uint64_t* out_pairs
     require(!std::isnan(tau), "tau is NaN");
     require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
     ck(cudaStreamSynchronize(db->stream), "sync database");
-    const PairGrid g{q->n_docs, db->n_docs, words_per_row(db->n_docs), false};
-    prepare_bitmap(q, g, false);
-    launch_mrc_bitmap(q->Sn.as<float>(), db->Sn.as<float>(), q->K, tau, g, q->bitmap.as<uint32_t>(),
-                      q->rowcnt.as<uint32_t>(), q->stream);
-    launched("mrc query bitmap");
+    const PairGrid g{q->n_docs, db->n_docs, words_per_row(db->n_docs), false, 0, q->n_docs, 0};
+    {
+      Phase ph_tiles(q, REFSIG_PHASE_PAIR_TILES);
+      prepare_bitmap(q, g, false);
+      launch_mrc_bitmap(q->Sn.as<float>(), db->Sn.as<float>(), q->K, tau, g, q->bitmap.as<uint32_t>(),
+                        q->rowcnt.as<uint32_t>(), q->stream);
+      launched("mrc query bitmap");
+    }
     rc2 = run_emit(q, g, out_pairs, capacity, out_count);
   });
   return rc != REFSIG_OK ? rc : rc2;
@@ -769,15 +885,75 @@ int refsig_gpu_hamming_query_pairs(refsig_gpu_ctx* q, int max_dist, uint64_t* ou
     require(max_dist >= 0 && max_dist <= 64, "max_dist must be in [0, 64]");
     require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
     ck(cudaStreamSynchronize(db->stream), "sync database");
-    const PairGrid g{q->n_docs, db->n_docs, words_per_row(db->n_docs), false};
-    prepare_bitmap(q, g, false);
-    launch_hamming_bitmap(q->fp.as<uint64_t>(), db->fp.as<uint64_t>(), max_dist, g, q->bitmap.as<uint32_t>(),
-                          q->rowcnt.as<uint32_t>(), q->stream);
-    launched("hamming query bitmap");
+    const PairGrid g{q->n_docs, db->n_docs, words_per_row(db->n_docs), false, 0, q->n_docs, 0};
+    {
+      Phase ph_tiles(q, REFSIG_PHASE_PAIR_TILES);
+      prepare_bitmap(q, g, false);
+      launch_hamming_bitmap(q->fp.as<uint64_t>(), db->fp.as<uint64_t>(), max_dist, g, q->bitmap.as<uint32_t>(),
+                            q->rowcnt.as<uint32_t>(), q->stream);
+      launched("hamming query bitmap");
+    }
     rc2 = run_emit(q, g, out_pairs, capacity, out_count);
   });
   return rc != REFSIG_OK ? rc : rc2;
 }
+
+int refsig_gpu_mrc_pairs_rows(refsig_gpu_ctx* ctx, float tau, uint32_t row_lo, uint32_t row_hi, uint64_t* out_pairs,
+                              uint64_t capacity, uint64_t* out_count) {
+  int rc2 = REFSIG_OK;
+  int rc = guard(ctx, [&] {
+    require(ctx->signed_, "sign() not called");
+    require(out_count != nullptr, "out_count is NULL");
+    require(!std::isnan(tau), "tau is NaN");
+    require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
+    require(row_lo <= row_hi && row_hi <= ctx->n_docs, "bad row range");
+    require(row_lo % kTile == 0 && (row_hi % kTile == 0 || row_hi == ctx->n_docs),
+            "row range must be aligned to 128-row tiles");
+    PairGrid g = self_grid(ctx);
+    g.row_begin = row_lo;
+    g.row_end = row_hi;
+    {
+      Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
+      prepare_bitmap(ctx, g, false);
+      launch_mrc_bitmap(ctx->Sn.as<float>(), ctx->Sn.as<float>(), ctx->K, tau, g, ctx->bitmap.as<uint32_t>(),
+                        ctx->rowcnt.as<uint32_t>(), ctx->stream);
+      launched("mrc bitmap");
+    }
+    rc2 = run_emit(ctx, g, out_pairs, capacity, out_count);
+  });
+  return rc != REFSIG_OK ? rc : rc2;
+}
+
+int refsig_gpu_set_profiling(refsig_gpu_ctx* ctx, int on) {
+  return guard(ctx, [&] {
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    for (auto& m : ctx->marks) {
+      ctx->ev_free.push_back(m.a);
+      ctx->ev_free.push_back(m.b);
+    }
+    ctx->marks.clear();
+    ctx->prof = on != 0;
+  });
+}
+
+int refsig_gpu_phase_times(refsig_gpu_ctx* ctx, double* ms, uint64_t* calls) {
+  return guard(ctx, [&] {
+    require(ms != nullptr, "NULL output");
+    sync(ctx);
+    for (int p = 0; p < REFSIG_N_PHASES; ++p) {
+      ms[p] = 0.0;
+      if (calls) calls[p] = 0;
+    }
+    for (auto& m : ctx->marks) {
+      float t = 0.0f;
+      ck(cudaEventElapsedTime(&t, m.a, m.b), "cudaEventElapsedTime");
+      ms[m.phase] += t;
+      if (calls) calls[m.phase] += 1;
+    }
+  });
+}
+
+uint64_t refsig_gpu_launch_count(void) { return g_launches.load(); }
 
 int refsig_gpu_get_pairs(refsig_gpu_ctx* ctx, uint64_t* out_pairs, uint64_t capacity) {
   return guard(ctx, [&] {

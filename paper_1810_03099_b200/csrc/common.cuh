@@ -56,3 +56,8 @@ __device__ __forceinline__ uint64_t term_hash64(uint64_t seed, uint32_t t) {
 __host__ __device__ __forceinline__ uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
 }  // namespace refsig_gpu
+
+namespace refsig_gpu {
+// Counts kernel launches issued by this library (refsig_gpu_launch_count).
+void note_launch();
+}  // namespace refsig_gpu

@@ -223,15 +223,19 @@ void launch_count_bin(int bin, const CountArgs& a, const uint32_t* bin_docs, uin
   switch (bin) {
     case 0:
       count_smem_kernel<256, 128><<<grid_for(n_bin, 16), 128, 0, s>>>(a, bin_docs, n_bin);
+      note_launch();
       break;
     case 1:
       count_smem_kernel<1024, 256><<<grid_for(n_bin, 8), 256, 0, s>>>(a, bin_docs, n_bin);
+      note_launch();
       break;
     case 2:
       count_smem_kernel<4096, 512><<<grid_for(n_bin, 4), 512, 0, s>>>(a, bin_docs, n_bin);
+      note_launch();
       break;
     default:
       count_smem_kernel<8192, 1024><<<grid_for(n_bin, 2), 1024, 0, s>>>(a, bin_docs, n_bin);
+      note_launch();
       break;
   }
 }
@@ -240,23 +244,27 @@ void launch_count_large(const CountArgs& a, const uint32_t* long_docs, const uin
                         uint32_t* scratch, cudaStream_t s) {
   if (n_long == 0) return;
   count_large_kernel<<<grid_for(n_long, 1), 1024, 0, s>>>(a, long_docs, scratch_off, n_long, scratch);
+  note_launch();
 }
 
 void launch_idf(const uint32_t* df, uint32_t vocab, uint32_t n_docs, int weight_mode, TermInfo* info,
                 cudaStream_t s) {
   idf_kernel<<<grid_for((vocab + 255) / 256, 8), 256, 0, s>>>(df, vocab, n_docs, weight_mode, info);
+  note_launch();
 }
 
 void launch_compact_csr(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const uint64_t* rowptr,
                         uint32_t n_docs, uint32_t* ids, uint32_t* counts, cudaStream_t s) {
   if (n_docs == 0) return;
   compact_csr_kernel<<<grid_for((n_docs + 7) / 8, 16), 256, 0, s>>>(ent, doc_off, nnz, rowptr, n_docs, ids, counts);
+  note_launch();
 }
 
 void launch_inv_norm(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const TermInfo* info,
                      uint32_t n_docs, float* inv_norm, cudaStream_t s) {
   if (n_docs == 0) return;
   inv_norm_kernel<<<grid_for((n_docs + 7) / 8, 16), 256, 0, s>>>(ent, doc_off, nnz, info, n_docs, inv_norm);
+  note_launch();
 }
 
 }  // namespace refsig_gpu

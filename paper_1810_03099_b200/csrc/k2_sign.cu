@@ -154,10 +154,12 @@ __global__ void __launch_bounds__(256) sign_kernel(SignArgs a) {
 void launch_ref_doc_ranges(const uint64_t* doc_off, const uint32_t* nnz, const uint32_t* ref_docs, uint32_t K,
                            uint64_t* start, uint32_t* n, cudaStream_t s) {
   ref_doc_ranges_kernel<<<(K + 127) / 128, 128, 0, s>>>(doc_off, nnz, ref_docs, K, start, n);
+  note_launch();
 }
 
 void launch_ref_mark(const RefArgs& r, uint32_t* flags, cudaStream_t s) {
   ref_mark_kernel<<<r.K < 1024 ? r.K : 1024, 256, 0, s>>>(r, flags);
+  note_launch();
 }
 
 void launch_ref_remap(const uint32_t* flags, const uint64_t* prefix, uint32_t vocab, TermInfo* info,
@@ -165,10 +167,12 @@ void launch_ref_remap(const uint32_t* flags, const uint64_t* prefix, uint32_t vo
   uint32_t g = (vocab + 255) / 256;
   if (g > 4096) g = 4096;
   ref_remap_kernel<<<g, 256, 0, s>>>(flags, prefix, vocab, info);
+  note_launch();
 }
 
 void launch_ref_fill(const RefArgs& r, const TermInfo* info, float* R, cudaStream_t s) {
   ref_fill_kernel<<<r.K < 1024 ? r.K : 1024, 256, 0, s>>>(r, info, R);
+  note_launch();
 }
 
 void launch_sign(const SignArgs& a, cudaStream_t s) {
@@ -183,6 +187,7 @@ void launch_sign(const SignArgs& a, cudaStream_t s) {
     sign_kernel<2><<<static_cast<unsigned>(blocks), 256, 0, s>>>(a);
   else
     sign_kernel<4><<<static_cast<unsigned>(blocks), 256, 0, s>>>(a);
+  note_launch();
 }
 
 }  // namespace refsig_gpu

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel(const float* __restr
   __shared__ __align__(16) float As[kKC][kTile];
   __shared__ __align__(16) float Bs[kKC][kTile];
   uint32_t bi, bj;
-  tile_coords(blockIdx.x, nbr, nbc, g.triangle, bi, bj);
+  tile_coords(blockIdx.x + g.tile0, nbr, nbc, g.triangle, bi, bj);
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const uint32_t row0 = bi * kTile, col0 = bj * kTile;
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(256) hamming_bitmap_kernel(const uint64_t* __r
                                                              uint32_t* __restrict__ rowcnt) {
   __shared__ __align__(16) uint2 Fc[kTile];
   uint32_t bi, bj;
-  tile_coords(blockIdx.x, nbr, nbc, g.triangle, bi, bj);
+  tile_coords(blockIdx.x + g.tile0, nbr, nbc, g.triangle, bi, bj);
   const uint32_t row0 = bi * kTile, col0 = bj * kTile;
   if (threadIdx.x < kTile) {
     const uint32_t j = col0 + threadIdx.x;
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
                                                    uint64_t capacity) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < g.n_rows; i += nwarps) {
+  for (uint32_t i = g.row_begin + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < g.row_end; i += nwarps) {
     uint32_t remaining = rowcnt[i];
     if (remaining == 0) continue;
     uint64_t base = rowstart[i];
@@ -229,38 +229,52 @@ int sms() {
   return n;
 }
 
-uint64_t n_tiles(const PairGrid& g, uint32_t& nbr, uint32_t& nbc) {
+// Tiles of row panels [row_begin/128, ceil(row_end/128)); sets g.tile0.
+uint64_t n_tiles(PairGrid& g, uint32_t& nbr, uint32_t& nbc) {
   nbr = static_cast<uint32_t>(ceil_div(g.n_rows, kTile));
   nbc = static_cast<uint32_t>(ceil_div(g.n_cols, kTile));
-  return g.triangle ? static_cast<uint64_t>(nbc) * (nbc + 1) / 2 : static_cast<uint64_t>(nbr) * nbc;
+  const uint64_t p0 = g.row_begin / kTile, p1 = ceil_div(g.row_end, kTile);
+  if (p1 <= p0) return 0;
+  if (g.triangle) {
+    auto S = [&](uint64_t r) { return r * nbc - r * (r - 1) / 2; };
+    g.tile0 = static_cast<uint32_t>(S(p0));
+    return S(p1) - S(p0);
+  }
+  g.tile0 = static_cast<uint32_t>(p0 * nbc);
+  return (p1 - p0) * nbc;
 }
 
 }  // namespace
 
-void launch_mrc_bitmap(const float* Sn_rows, const float* Sn_cols, uint32_t K, float tau, const PairGrid& g,
+void launch_mrc_bitmap(const float* Sn_rows, const float* Sn_cols, uint32_t K, float tau, const PairGrid& g_in,
                        uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s) {
+  PairGrid g = g_in;
   uint32_t nbr, nbc;
   const uint64_t t = n_tiles(g, nbr, nbc);
   if (t == 0) return;
   mrc_bitmap_kernel<<<static_cast<unsigned>(t), 256, 0, s>>>(Sn_rows, Sn_cols, K, tau, g, nbr, nbc, bitmap, rowcnt);
+  note_launch();
 }
 
-void launch_hamming_bitmap(const uint64_t* f_rows, const uint64_t* f_cols, int max_dist, const PairGrid& g,
+void launch_hamming_bitmap(const uint64_t* f_rows, const uint64_t* f_cols, int max_dist, const PairGrid& g_in,
                            uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s) {
+  PairGrid g = g_in;
   uint32_t nbr, nbc;
   const uint64_t t = n_tiles(g, nbr, nbc);
   if (t == 0) return;
   hamming_bitmap_kernel<<<static_cast<unsigned>(t), 256, 0, s>>>(f_rows, f_cols, max_dist, g, nbr, nbc, bitmap,
                                                                  rowcnt);
+  note_launch();
 }
 
 void launch_emit_pairs(const uint32_t* bitmap, const PairGrid& g, const uint32_t* rowcnt, const uint64_t* rowstart,
                        uint64_t* out, uint64_t capacity, cudaStream_t s) {
-  if (g.n_rows == 0) return;
-  uint64_t blocks = ceil_div(g.n_rows, 8);
+  if (g.row_end <= g.row_begin) return;
+  uint64_t blocks = ceil_div(g.row_end - g.row_begin, 8);
   const uint64_t cap = static_cast<uint64_t>(sms()) * 8;
   if (blocks > cap) blocks = cap;
   emit_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(bitmap, g, rowcnt, rowstart, out, capacity);
+  note_launch();
 }
 
 }  // namespace refsig_gpu

@@ -80,6 +80,7 @@ void launch_simhash(const SimhashArgs& a, cudaStream_t s) {
   const uint64_t cap = static_cast<uint64_t>(sms) * 8;
   if (blocks > cap) blocks = cap;
   simhash_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(a);
+  note_launch();
 }
 
 }  // namespace refsig_gpu

@@ -159,6 +159,7 @@ void launch_unit_weights(const uint2* ent, const uint64_t* doc_off, const uint32
   if (!n_docs) return;
   unsigned g = static_cast<unsigned>(std::min<uint64_t>(ceil_div(n_docs, 8), sm_count() * 16ull));
   unit_weights_kernel<<<g, 256, 0, s>>>(ent, doc_off, nnz, info, inv_norm, n_docs, x);
+  note_launch();
 }
 
 void launch_postings_fill(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const float* x,
@@ -166,12 +167,14 @@ void launch_postings_fill(const uint2* ent, const uint64_t* doc_off, const uint3
   if (!n_docs) return;
   unsigned g = static_cast<unsigned>(std::min<uint64_t>(ceil_div(n_docs, 8), sm_count() * 16ull));
   postings_fill_kernel<<<g, 256, 0, s>>>(ent, doc_off, nnz, x, n_docs, fill, posts);
+  note_launch();
 }
 
 void launch_exact_rows(const ExactArgs& a, uint32_t row_lo, uint32_t row_hi, cudaStream_t s) {
   if (row_hi <= row_lo) return;
   unsigned g = std::min<uint32_t>(row_hi - row_lo, exact_pool_ctas());
   exact_rows_kernel<<<g, 256, 0, s>>>(a, row_lo, row_hi);
+  note_launch();
 }
 
 void launch_pair_cosines(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const float* x,
@@ -179,6 +182,7 @@ void launch_pair_cosines(const uint2* ent, const uint64_t* doc_off, const uint32
   if (!n_keys) return;
   unsigned g = static_cast<unsigned>(std::min<uint64_t>(ceil_div(n_keys, 8), sm_count() * 16ull));
   pair_cosines_kernel<<<g, 256, 0, s>>>(ent, doc_off, nnz, x, keys, n_keys, out);
+  note_launch();
 }
 
 }  // namespace refsig_gpu

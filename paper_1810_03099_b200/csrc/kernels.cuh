@@ -93,6 +93,9 @@ struct PairGrid {
   uint32_t n_cols;      // columns (= n_rows for a self-join)
   uint32_t words_per_row;
   bool triangle;        // self-join: only j > i
+  uint32_t row_begin;   // rows this call covers: [row_begin, row_end), row_begin % 128 == 0
+  uint32_t row_end;
+  uint32_t tile0;       // first tile index (set by the launcher)
 };
 void launch_mrc_bitmap(const float* Sn_rows, const float* Sn_cols, uint32_t K, float tau, const PairGrid& g, uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s);
 void launch_hamming_bitmap(const uint64_t* f_rows, const uint64_t* f_cols, int max_dist, const PairGrid& g,

@@ -106,8 +106,11 @@ void launch_exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_
   }
   uint64_t* partial = static_cast<uint64_t*>(tmp);
   scan_reduce_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, n, partial);
+  note_launch();
   scan_partials_kernel<<<1, kScanThreads, 0, s>>>(partial, nb);
+  note_launch();
   scan_apply_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, n, partial, nb, out);
+  note_launch();
 }
 
 }  // namespace refsig_gpu
