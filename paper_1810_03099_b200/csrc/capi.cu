@@ -86,15 +86,15 @@ struct refsig_gpu_ctx {
   std::vector<uint64_t> h_off;
   DevBuf tokens, doc_off;
   const uint32_t* tok = nullptr;
-  DevBuf bin_docs[4];
-  uint32_t n_bin[4] = {0, 0, 0, 0};
+  DevBuf tiny_docs, chunks, chunk_cnt, chunk_scratch, merge_docs[3];
+  uint32_t n_tiny = 0, n_chunks = 0, n_merge[3] = {0, 0, 0};
   DevBuf long_docs, long_off, long_scratch;
   uint32_t n_long = 0;
 
   // K1
   bool counted = false;
   int weight_mode = REFSIG_WEIGHT_TFIDF;
-  DevBuf ent, nnz, df, info, flags;
+  DevBuf ent, nnz, df, df_rep, info, flags;
   DevBuf rowptr, c_ids, c_counts, inv_norm;
   bool have_inv_norm = false;
 
@@ -105,7 +105,8 @@ struct refsig_gpu_ctx {
 
   // sign
   bool signed_ = false;
-  DevBuf S, Sn;
+  DevBuf S, ST;
+  uint32_t ld = 0;  // leading dimension of ST
 
   // pairs
   DevBuf bitmap, rowcnt, rowstart, cand, scan_tmp;
@@ -347,17 +348,24 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
   c->doc_off.ensure(sizeof(uint64_t) * (n_docs + 1));
   ck(cudaMemcpyAsync(c->doc_off.p, doc_off, sizeof(uint64_t) * (n_docs + 1), cudaMemcpyHostToDevice, c->stream),
      "H2D doc_off");
-  // Length bins for K1 (host metadata only).
-  std::vector<uint32_t> bins[4], longs;
+  // K1 work plan (host metadata only): see k1_count.cu.
+  std::vector<uint32_t> tiny, longs;
+  std::vector<uint2> chunks;
+  std::vector<uint4> merges[3];
   std::vector<uint64_t> loff;
   uint64_t scratch = 0;
   for (uint32_t d = 0; d < n_docs; ++d) {
     const uint64_t len = doc_off[d + 1] - doc_off[d];
     require(len < (1ull << 31), "document longer than 2^31 tokens");
-    int b = 0;
-    while (b < 4 && len > kBinCap[b]) ++b;
-    if (b < 4) {
-      bins[b].push_back(d);
+    if (len <= kTinyMax) {
+      tiny.push_back(d);
+    } else if (len <= kChunk) {
+      chunks.push_back(make_uint2(d, 1u));  // chunk 0, direct
+    } else if (len <= kMergeMax) {
+      const uint32_t m = static_cast<uint32_t>(ceil_div(len, kChunk));
+      const int cls = len <= kMergeCap[0] ? 0 : (len <= kMergeCap[1] ? 1 : 2);
+      merges[cls].push_back(make_uint4(d, static_cast<uint32_t>(chunks.size()), m, 0u));
+      for (uint32_t q = 0; q < m; ++q) chunks.push_back(make_uint2(d, q << 1));
     } else {
       longs.push_back(d);
       loff.push_back(scratch);
@@ -366,27 +374,27 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
       scratch += p;
     }
   }
-  for (int b = 0; b < 4; ++b) {
-    c->n_bin[b] = static_cast<uint32_t>(bins[b].size());
-    if (!bins[b].empty()) {
-      c->bin_docs[b].ensure(sizeof(uint32_t) * bins[b].size());
-      ck(cudaMemcpyAsync(c->bin_docs[b].p, bins[b].data(), sizeof(uint32_t) * bins[b].size(), cudaMemcpyHostToDevice,
-                         c->stream),
-         "H2D bins");
-    }
+  auto up = [&](DevBuf& buf, const void* src, size_t bytes) {
+    if (!bytes) return;
+    buf.ensure(bytes);
+    ck(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, c->stream), "H2D plan");
+  };
+  c->n_tiny = static_cast<uint32_t>(tiny.size());
+  up(c->tiny_docs, tiny.data(), 4 * tiny.size());
+  c->n_chunks = static_cast<uint32_t>(chunks.size());
+  up(c->chunks, chunks.data(), sizeof(uint2) * chunks.size());
+  c->chunk_cnt.ensure(4 * std::max<size_t>(chunks.size(), 1));
+  for (int k = 0; k < 3; ++k) {
+    c->n_merge[k] = static_cast<uint32_t>(merges[k].size());
+    up(c->merge_docs[k], merges[k].data(), sizeof(uint4) * merges[k].size());
   }
   c->n_long = static_cast<uint32_t>(longs.size());
   if (!longs.empty()) {
-    c->long_docs.ensure(sizeof(uint32_t) * longs.size());
-    c->long_off.ensure(sizeof(uint64_t) * loff.size());
     c->long_scratch.ensure(sizeof(uint32_t) * scratch);
-    ck(cudaMemcpyAsync(c->long_docs.p, longs.data(), sizeof(uint32_t) * longs.size(), cudaMemcpyHostToDevice,
-                       c->stream),
-       "H2D long docs");
-    ck(cudaMemcpyAsync(c->long_off.p, loff.data(), sizeof(uint64_t) * loff.size(), cudaMemcpyHostToDevice, c->stream),
-       "H2D long offsets");
+    up(c->long_docs, longs.data(), 4 * longs.size());
+    up(c->long_off, loff.data(), 8 * loff.size());
   }
-  // bin lists are host-local vectors: make sure the copies finished
+  // the plan vectors are host-local: make sure the copies finished
   ck(cudaStreamSynchronize(c->stream), "H2D metadata");
   c->loaded = true;
   c->counted = false;
@@ -491,26 +499,34 @@ int refsig_gpu_count(refsig_gpu_ctx* ctx, int weight_mode) {
     }
     const uint32_t N = ctx->n_docs, V = ctx->vocab;
     ctx->ent.ensure(sizeof(uint2) * std::max<uint64_t>(ctx->n_tokens, 1));
+    ctx->chunk_scratch.ensure(sizeof(uint2) * std::max<uint64_t>(ctx->n_tokens, 1));
     ctx->nnz.ensure(sizeof(uint32_t) * N);
     ctx->df.ensure(sizeof(uint32_t) * V);
     ctx->info.ensure(sizeof(TermInfo) * V);
     if (ctx->flags.ensure(16)) ck(cudaMemsetAsync(ctx->flags.p, 0, 16, ctx->stream), "memset");
     Phase ph(ctx, REFSIG_PHASE_COUNT);
-    ck(cudaMemsetAsync(ctx->df.p, 0, sizeof(uint32_t) * V, ctx->stream), "memset df");
+    // df replicas: ~8 MB budget, 1..16 copies (see k1_count.cu df_add)
+    const uint32_t reps = std::max<uint32_t>(1u, std::min<uint32_t>(16u, (2u << 20) / V));
+    ctx->df_rep.ensure(sizeof(uint32_t) * static_cast<size_t>(V) * reps);
+    ck(cudaMemsetAsync(ctx->df_rep.p, 0, sizeof(uint32_t) * static_cast<size_t>(V) * reps, ctx->stream), "memset df");
     CountArgs a{ctx->tok, ctx->doc_off.as<uint64_t>(), V, ctx->ent.as<uint2>(), ctx->nnz.as<uint32_t>(),
-                ctx->df.as<uint32_t>(), ctx->flags.as<uint32_t>()};
-    for (int b = 0; b < 4; ++b) launch_count_bin(b, a, ctx->bin_docs[b].as<uint32_t>(), ctx->n_bin[b], ctx->stream);
+                ctx->df_rep.as<uint32_t>(), reps, ctx->flags.as<uint32_t>(), ctx->chunk_scratch.as<uint2>(),
+                ctx->chunk_cnt.as<uint32_t>()};
+    launch_count_tiny(a, ctx->tiny_docs.as<uint32_t>(), ctx->n_tiny, ctx->stream);
+    launch_count_chunks(a, ctx->chunks.as<uint2>(), ctx->n_chunks, ctx->stream);
+    for (int k = 0; k < 3; ++k) launch_count_merge(k, a, ctx->merge_docs[k].as<uint4>(), ctx->n_merge[k], ctx->stream);
     launch_count_large(a, ctx->long_docs.as<uint32_t>(), ctx->long_off.as<uint64_t>(), ctx->n_long,
                        ctx->long_scratch.as<uint32_t>(), ctx->stream);
+    launch_idf(ctx->df_rep.as<uint32_t>(), reps, V, N, weight_mode, ctx->df.as<uint32_t>(), ctx->info.as<TermInfo>(),
+               ctx->stream);
+    ctx->weight_mode = weight_mode;
     if (db) {
-      // Query mode: the database's IDF and reference rows (configs[4]).
+      // Query mode: the database's IDF and reference rows (configs[4]); the
+      // query batch keeps its own df.
       ck(cudaStreamSynchronize(db->stream), "sync database");
       ck(cudaMemcpyAsync(ctx->info.p, db->info.p, sizeof(TermInfo) * V, cudaMemcpyDeviceToDevice, ctx->stream),
          "copy database idf");
       ctx->weight_mode = db->weight_mode;
-    } else {
-      launch_idf(ctx->df.as<uint32_t>(), V, N, weight_mode, ctx->info.as<TermInfo>(), ctx->stream);
-      ctx->weight_mode = weight_mode;
     }
     launched("count");
     ctx->counted = true;
@@ -673,11 +689,16 @@ int refsig_gpu_sign(refsig_gpu_ctx* ctx) {
     require(refc->have_ref, "no reference set");
     const uint32_t N = ctx->n_docs, K = refc->K;
     ctx->S.ensure(sizeof(float) * static_cast<size_t>(N) * K);
-    ctx->Sn.ensure(sizeof(float) * static_cast<size_t>(N) * K);
+    const uint32_t ld = static_cast<uint32_t>(ceil_div(N, kTile) * kTile);
+    ctx->ST.ensure(sizeof(float) * static_cast<size_t>(ld) * K);
+    ctx->ld = ld;
+    if (ld > N)  // zero pad columns: the tile kernels read whole 128-column panels
+      ck(cudaMemset2DAsync(ctx->ST.as<float>() + N, sizeof(float) * ld, 0, sizeof(float) * (ld - N), K, ctx->stream),
+         "memset ST pad");
     ctx->inv_norm.ensure(sizeof(float) * N);
     if (ctx->db) ck(cudaStreamSynchronize(ctx->db->stream), "sync database");
     SignArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->info.as<TermInfo>(),
-               refc->R.as<float>(), N, K, ctx->S.as<float>(), ctx->Sn.as<float>(), ctx->inv_norm.as<float>()};
+               refc->R.as<float>(), N, K, ctx->S.as<float>(), ctx->ST.as<float>(), ld, ctx->inv_norm.as<float>()};
     {
       Phase ph(ctx, REFSIG_PHASE_SIGN);
       launch_sign(a, ctx->stream);
@@ -712,7 +733,7 @@ int refsig_gpu_mrc_pairs(refsig_gpu_ctx* ctx, float tau, uint64_t* out_pairs, ui
     {
       Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
       prepare_bitmap(ctx, g, false);
-      launch_mrc_bitmap(ctx->Sn.as<float>(), ctx->Sn.as<float>(), ctx->K, tau, g, ctx->bitmap.as<uint32_t>(),
+      launch_mrc_bitmap(ctx->ST.as<float>(), ctx->ld, ctx->ST.as<float>(), ctx->ld, ctx->K, tau, g, ctx->bitmap.as<uint32_t>(),
                         ctx->rowcnt.as<uint32_t>(), ctx->stream);
       launched("mrc bitmap");
     }
@@ -865,7 +886,7 @@ int refsig_gpu_mrc_query_pairs(refsig_gpu_ctx* q, float tau, uint64_t* out_pairs
     {
       Phase ph_tiles(q, REFSIG_PHASE_PAIR_TILES);
       prepare_bitmap(q, g, false);
-      launch_mrc_bitmap(q->Sn.as<float>(), db->Sn.as<float>(), q->K, tau, g, q->bitmap.as<uint32_t>(),
+      launch_mrc_bitmap(q->ST.as<float>(), q->ld, db->ST.as<float>(), db->ld, q->K, tau, g, q->bitmap.as<uint32_t>(),
                         q->rowcnt.as<uint32_t>(), q->stream);
       launched("mrc query bitmap");
     }
@@ -915,7 +936,7 @@ int refsig_gpu_mrc_pairs_rows(refsig_gpu_ctx* ctx, float tau, uint32_t row_lo, u
     {
       Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
       prepare_bitmap(ctx, g, false);
-      launch_mrc_bitmap(ctx->Sn.as<float>(), ctx->Sn.as<float>(), ctx->K, tau, g, ctx->bitmap.as<uint32_t>(),
+      launch_mrc_bitmap(ctx->ST.as<float>(), ctx->ld, ctx->ST.as<float>(), ctx->ld, ctx->K, tau, g, ctx->bitmap.as<uint32_t>(),
                         ctx->rowcnt.as<uint32_t>(), ctx->stream);
       launched("mrc bitmap");
     }

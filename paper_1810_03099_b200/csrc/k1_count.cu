@@ -13,9 +13,20 @@
 // prefix sum is needed on the hot path; launch_compact_csr produces the
 // compact CSR only when a caller asks for it.
 //
-// Dispatch: docs are binned by length on the host (at upload). Each bin runs a
-// CTA-per-doc shared-memory bitonic sort sized to the bin, grid-strided over
-// the bin's docs; docs > 8192 tokens sort in a global scratch region.
+// Sort: a bitonic network kept in registers. A group of W warps sorts
+// P = 32*IPT*W keys, IPT consecutive keys per thread (blocked layout):
+// compare-exchange distances j < IPT are register ops, IPT <= j < 32*IPT are
+// one SHFL + one predicated IMNMX per key, and j >= 32*IPT (multi-warp
+// groups only) go through shared memory. Run-length encoding is done in
+// registers too (neighbour via SHFL, positions via warp/block scans, run ends
+// via a suffix-min of the next head). Work plan (host-built at upload):
+//   <= 64 tokens: warp per doc, 64-key sort;
+//   65..256: one 256-key warp sort per doc (a "direct" chunk);
+//   257..8192: every 256-token chunk sorted + run-length encoded by a warp,
+//     then one CTA per doc merges the chunks' unique rows in shared memory
+//     (merge path) and sums equal ids — no padding beyond the last chunk and
+//     O(n log(n/256)) merge work instead of a full bitonic network;
+//   > 8192: bitonic sort in a global scratch region.
 
 #include <cmath>
 
@@ -24,12 +35,205 @@
 namespace refsig_gpu {
 namespace {
 
+constexpr uint32_t kInf = 0xFFFFFFFFu;
+
+// df increments: one atomic per (doc, term) run head into one of R replicas
+// of the df array (replica = CTA index mod R). Zipf-head terms occur in nearly
+// every document, so a single array serialises thousands of atomics on a few
+// L2 addresses; replicas divide that contention by R. The idf kernel sums the
+// replicas (measured: a shared-memory aggregation cache was slower — shared
+// atomics cost ~2 cycles per lane).
+__device__ __forceinline__ void df_add(const CountArgs& a, uint32_t key) {
+  atomicAdd(a.df + static_cast<size_t>(blockIdx.x % a.df_reps) * a.vocab + key, 1u);
+}
+
 __device__ __forceinline__ uint32_t next_pow2(uint32_t x) {
   return x <= 1 ? 1u : (1u << (32 - __clz(x - 1)));
 }
 
-// Block-wide exclusive scan of one value per thread; returns the block total
-// through *total. `scratch` holds THREADS/32 words.
+// ---------------------------------------------------------------------------
+// Register bitonic sort of P = 32*IPT*W keys; `t` is the thread's index in the
+// group (0..32W-1), so it holds keys [t*IPT, t*IPT+IPT). sm: P words (W > 1).
+template <int IPT, int W>
+__device__ __forceinline__ void bitonic_regs(uint32_t (&v)[IPT], uint32_t t, uint32_t* sm) {
+  constexpr int P = 32 * IPT * W;
+  constexpr int LANE_SPAN = 32 * IPT;  // keys held by one warp
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= P; k <<= 1) {
+    if constexpr (W > 1) {
+      if (k > LANE_SPAN) {
+        // cross-warp stages j = k/2 .. LANE_SPAN in shared memory
+#pragma unroll
+        for (int q = 0; q < IPT; ++q) sm[t * IPT + q] = v[q];
+        __syncthreads();
+        for (int j = k >> 1; j >= LANE_SPAN; j >>= 1) {
+#pragma unroll
+          for (int p = 0; p < IPT / 2; ++p) {
+            const uint32_t idx = t * (IPT / 2) + p;  // compare-exchange pair index
+            const uint32_t i = ((idx & ~(j - 1)) << 1) | (idx & (j - 1));
+            const uint32_t l = i + j;
+            const uint32_t a = sm[i], b = sm[l];
+            const bool asc = (i & k) == 0;
+            if ((a > b) == asc) {
+              sm[i] = b;
+              sm[l] = a;
+            }
+          }
+          __syncthreads();
+        }
+#pragma unroll
+        for (int q = 0; q < IPT; ++q) v[q] = sm[t * IPT + q];
+        __syncthreads();
+      }
+    }
+    // cross-lane stages IPT <= j < 32*IPT (partner lane = lane ^ (j/IPT))
+#pragma unroll
+    for (int j = ((k >> 1) < LANE_SPAN ? (k >> 1) : (LANE_SPAN >> 1)); j >= IPT; j >>= 1) {
+      const uint32_t lj = j / IPT;
+      const bool lower = (lane & lj) == 0;
+      const bool asc = ((t * IPT) & k) == 0;
+      const bool take_min = lower == asc;
+#pragma unroll
+      for (int q = 0; q < IPT; ++q) {
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, v[q], lj);
+        v[q] = take_min ? min(v[q], y) : max(v[q], y);
+      }
+    }
+    // in-register stages j < IPT
+#pragma unroll
+    for (int j = ((k >> 1) < IPT ? (k >> 1) : (IPT >> 1)); j >= 1; j >>= 1) {
+#pragma unroll
+      for (int q = 0; q < IPT; ++q) {
+        if ((q & j) == 0) {
+          const int l = q | j;
+          const bool asc = ((t * IPT + q) & k) == 0;
+          const uint32_t lo = min(v[q], v[l]), hi = max(v[q], v[l]);
+          v[q] = asc ? lo : hi;
+          v[l] = asc ? hi : lo;
+        }
+      }
+    }
+  }
+}
+
+// Warp inclusive scan / suffix min.
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, uint32_t lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= static_cast<uint32_t>(o)) x += y;
+  }
+  return x;
+}
+__device__ __forceinline__ uint32_t warp_suffix_min_excl(uint32_t x, uint32_t lane) {
+  // min over lanes > lane
+  uint32_t r = __shfl_down_sync(0xffffffffu, x, 1);
+  if (lane == 31) r = kInf;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_down_sync(0xffffffffu, r, o);
+    if (lane + o < 32) r = min(r, y);
+  }
+  return r;
+}
+
+// RLE of the sorted keys (blocked, IPT per thread, first `len` valid) of a
+// group of W warps; writes (id,count) rows at ent[0..nnz) and bumps df.
+// Returns nnz (valid in every thread). sm: >= 3*W+2 words (W > 1).
+template <int IPT, int W, bool DF = true>
+__device__ __forceinline__ uint32_t rle_regs(const uint32_t (&v)[IPT], uint32_t t, uint32_t len, uint2* ent,
+                                             const CountArgs& ca, uint32_t* sm) {
+  const uint32_t lane = threadIdx.x & 31, w = t >> 5;
+  // predecessor of v[0]
+  uint32_t prev = __shfl_up_sync(0xffffffffu, v[IPT - 1], 1);
+  if constexpr (W > 1) {
+    if (lane == 31) sm[w] = v[IPT - 1];
+    __syncthreads();
+    if (lane == 0) prev = w > 0 ? sm[w - 1] : kInf;
+  } else {
+    if (lane == 0) prev = kInf;
+  }
+  const uint32_t base = t * IPT;
+  uint32_t hmask = 0;  // bit q: key q starts a run
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    const uint32_t p = q == 0 ? prev : v[q - 1];
+    if (base + q < len && (base + q == 0 || v[q] != p)) hmask |= 1u << q;
+  }
+  const uint32_t nh = __popc(hmask);
+  const uint32_t first = hmask ? base + (__ffs(hmask) - 1) : kInf;
+  // exclusive position of this thread's first head; total; next head after this thread
+  uint32_t incl = warp_incl_scan(nh, lane);
+  uint32_t next = warp_suffix_min_excl(first, lane);
+  uint32_t total, pos;
+  if constexpr (W > 1) {
+    uint32_t* wsum = sm + W;      // [W] head counts per warp
+    uint32_t* wmin = sm + 2 * W;  // [W] first head of each warp
+    __syncthreads();
+    if (lane == 31) wsum[w] = incl;
+    const uint32_t wfirst = __reduce_min_sync(0xffffffffu, first);
+    if (lane == 0) wmin[w] = wfirst;
+    __syncthreads();
+    uint32_t before = 0, tot = 0, after = kInf;
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      const uint32_t c = wsum[u];
+      before += (u < static_cast<int>(w)) ? c : 0u;
+      tot += c;
+      if (u > static_cast<int>(w)) after = min(after, wmin[u]);
+    }
+    pos = before + incl - nh;
+    total = tot;
+    next = min(next, after);
+    __syncthreads();
+  } else {
+    pos = incl - nh;
+    total = __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (next == kInf) next = len;
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    if (hmask & (1u << q)) {
+      const uint32_t rest = hmask & ~((2u << q) - 1);  // heads after q in this thread
+      const uint32_t end = rest ? base + (__ffs(rest) - 1) : next;
+      ent[pos] = make_uint2(v[q], end - (base + q));
+      if (DF) df_add(ca, v[q]);
+      ++pos;
+    }
+  }
+  return total;
+}
+
+__device__ __forceinline__ uint32_t load_key(const CountArgs& a, uint64_t b, uint32_t i, uint32_t len) {
+  if (i >= len) return kInf;
+  uint32_t v = __ldg(a.tokens + b + i);
+  if (v >= a.vocab) {
+    atomicOr(a.err, 1u);
+    v = a.vocab - 1;
+  }
+  return v;
+}
+
+// One warp per document (P = 32*IPT).
+template <int IPT>
+__global__ void __launch_bounds__(256) count_warp_kernel(CountArgs a, const uint32_t* __restrict__ docs,
+                                                         uint32_t n_docs) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < n_docs; q += nw) {
+    const uint32_t d = docs[q];
+    const uint64_t b = a.doc_off[d];
+    const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
+    uint32_t v[IPT];
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) v[k] = load_key(a, b, k * 32 + lane, len);  // coalesced; any order sorts
+    bitonic_regs<IPT, 1>(v, lane, nullptr);
+    const uint32_t n = rle_regs<IPT, 1>(v, lane, len, a.ent + b, a, nullptr);
+    if (lane == 0) a.nnz[d] = n;
+  }
+}
+
 template <int THREADS>
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* scratch, uint32_t* total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -44,24 +248,163 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
     tot += x;
   }
   *total = tot;
-  __syncthreads();  // scratch reusable after return
+  __syncthreads();
   return wsum + inc - v;
 }
 
-// Bitonic sort (ascending) of P keys (P a power of two) held in `s`
-// (shared or global memory, visible block-wide after __syncthreads).
+// Chunk pass: one warp per 256-token chunk. chunks[q] = {doc, chunk<<1 | direct}.
+// A direct chunk is a whole document (65..256 tokens): its rows go straight to
+// ent/nnz/df. Otherwise the chunk's sorted unique (id,count) rows go to
+// scratch at the chunk's own token offset and chunk_cnt[q] = their number;
+// merge_kernel combines the chunks of a document.
+__global__ void __launch_bounds__(256) chunk_sort_kernel(CountArgs a, const uint2* __restrict__ chunks,
+                                                         uint32_t n_chunks) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < n_chunks; q += nw) {
+    const uint2 ch = chunks[q];
+    const uint32_t d = ch.x, c = ch.y >> 1;
+    const uint64_t b = a.doc_off[d];
+    const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
+    const uint64_t cb = b + static_cast<uint64_t>(c) * 256;
+    const uint32_t clen = min(256u, len - c * 256);
+    uint32_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = load_key(a, cb, k * 32 + lane, clen);
+    bitonic_regs<8, 1>(v, lane, nullptr);
+    if (ch.y & 1) {
+      const uint32_t n = rle_regs<8, 1, true>(v, lane, clen, a.ent + b, a, nullptr);
+      if (lane == 0) a.nnz[d] = n;
+    } else {
+      const uint32_t n = rle_regs<8, 1, false>(v, lane, clen, a.scratch + cb, a, nullptr);
+      if (lane == 0) a.chunk_cnt[q] = n;
+    }
+  }
+}
+
+// Merge pass: one CTA (256 threads) per document of 257..CAP tokens.
+// docs[q] = {doc, first chunk, #chunks}. The chunks' sorted unique rows are
+// loaded into shared memory back to back and merged pairwise (merge path:
+// each thread co-ranks its output range by binary search, then merges
+// serially) until one list remains; equal ids (at most one per chunk,
+// adjacent after the merge) are combined by summing counts while the final
+// rows are written. Per-thread ranges have an odd length so that the threads
+// of a warp hit distinct shared-memory banks.
+template <int CAP>
+__global__ void __launch_bounds__(256) merge_kernel(CountArgs a, const uint4* __restrict__ docs, uint32_t n_docs) {
+  extern __shared__ uint2 mbuf[];  // 2*CAP rows
+  constexpr int MAXL = CAP / 256;  // <= 32 chunks
+  __shared__ uint32_t off[MAXL + 1];
+  __shared__ uint32_t scan_scratch[8];
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t q = blockIdx.x; q < n_docs; q += gridDim.x) {
+    const uint4 md = docs[q];
+    const uint32_t d = md.x, first = md.y, m = md.z;
+    const uint64_t b = a.doc_off[d];
+    if (tid < 32) {  // chunk offsets: warp scan of the chunk counts
+      const uint32_t c = tid < m ? a.chunk_cnt[first + tid] : 0u;
+      const uint32_t inc = warp_inclusive_scan(c, tid);
+      if (tid < m) off[tid] = inc - c;
+      if (tid == m - 1) off[m] = inc;
+    }
+    __syncthreads();
+    const uint32_t M = off[m];
+    uint2* src = mbuf;
+    uint2* dst = mbuf + CAP;
+    for (uint32_t g = tid; g < M; g += 256) {  // all chunk loads in flight at once
+      uint32_t c = 0;
+      while (off[c + 1] <= g) ++c;
+      src[g] = a.scratch[b + static_cast<uint64_t>(c) * 256 + (g - off[c])];
+    }
+    __syncthreads();
+    const uint32_t E = ((M + 255) / 256) | 1u;
+    uint32_t nl = m;
+    while (nl > 1) {
+      uint32_t lo = min(tid * E, M);
+      const uint32_t hi = min(lo + E, M);
+      while (lo < hi) {
+        uint32_t p = 0;  // pair containing lo
+        while (off[min(2 * p + 2, nl)] <= lo) ++p;
+        const uint32_t s0 = off[2 * p], s1 = off[min(2 * p + 1, nl)], s2 = off[min(2 * p + 2, nl)];
+        const uint32_t end = min(hi, s2);
+        if (2 * p + 1 >= nl) {  // unpaired last list
+          for (uint32_t k = lo; k < end; ++k) dst[k] = src[k];
+        } else {
+          const uint2* A = src + s0;
+          const uint2* B = src + s1;
+          const uint32_t na = s1 - s0, nb = s2 - s1, diag = lo - s0;
+          uint32_t i0 = diag > nb ? diag - nb : 0, i1 = min(diag, na);
+          while (i0 < i1) {
+            const uint32_t mid = (i0 + i1) >> 1;
+            if (A[mid].x <= B[diag - mid - 1].x)
+              i0 = mid + 1;
+            else
+              i1 = mid;
+          }
+          uint32_t i = i0, j = diag - i0;
+          for (uint32_t k = lo; k < end; ++k) {
+            const bool takeA = j >= nb || (i < na && A[i].x <= B[j].x);
+            dst[k] = takeA ? A[i++] : B[j++];
+          }
+        }
+        lo = end;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        const uint32_t nn = (nl + 1) / 2;
+        for (uint32_t p = 0; p < nn; ++p) off[p] = off[2 * p];
+        off[nn] = M;
+      }
+      nl = (nl + 1) / 2;
+      uint2* t = src;
+      src = dst;
+      dst = t;
+      __syncthreads();
+    }
+    // combine equal ids (adjacent) and emit the document's rows
+    uint32_t base = 0;
+    uint2* out = a.ent + b;
+    for (uint32_t c0 = 0; c0 < M; c0 += 256 * E) {
+      const uint32_t lo = c0 + tid * E;
+      uint32_t heads = 0;
+      for (uint32_t k = 0; k < E; ++k) {
+        const uint32_t i = lo + k;
+        if (i < M && (i == 0 || src[i].x != src[i - 1].x)) ++heads;
+      }
+      uint32_t total;
+      uint32_t pos = base + block_exclusive_scan<256>(heads, scan_scratch, &total);
+      for (uint32_t k = 0; k < E; ++k) {
+        const uint32_t i = lo + k;
+        if (i < M && (i == 0 || src[i].x != src[i - 1].x)) {
+          const uint32_t key = src[i].x;
+          uint32_t cnt = src[i].y;
+          for (uint32_t e = i + 1; e < M && src[e].x == key; ++e) cnt += src[e].y;
+          out[pos++] = make_uint2(key, cnt);
+          df_add(a, key);
+        }
+      }
+      base += total;
+    }
+    if (tid == 0) a.nnz[d] = base;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Documents longer than 8192 tokens: bitonic sort in a global scratch region
+// (next_pow2(len) keys each), then a chunked block-wide RLE.
 template <int THREADS>
-__device__ __forceinline__ void bitonic_sort(uint32_t* s, uint32_t P) {
+__device__ __forceinline__ void bitonic_sort_mem(uint32_t* s, uint32_t P) {
   for (uint32_t k = 2; k <= P; k <<= 1) {
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
       for (uint32_t idx = threadIdx.x; idx < (P >> 1); idx += THREADS) {
         uint32_t i = ((idx & ~(j - 1)) << 1) | (idx & (j - 1));
         uint32_t l = i + j;
-        uint32_t a = s[i], b = s[l];
+        uint32_t x = s[i], y = s[l];
         bool up = (i & k) == 0;
-        if ((a > b) == up) {
-          s[i] = b;
-          s[l] = a;
+        if ((x > y) == up) {
+          s[i] = y;
+          s[l] = x;
         }
       }
       __syncthreads();
@@ -69,12 +412,9 @@ __device__ __forceinline__ void bitonic_sort(uint32_t* s, uint32_t P) {
   }
 }
 
-// Run-length encode sorted keys s[0..len) into ent[base..]; df += 1 per run.
-// IPT consecutive keys per thread per chunk; runs may cross chunk borders
-// (a run head walks to its end).
 template <int THREADS, int IPT>
-__device__ __forceinline__ uint32_t rle_emit(const uint32_t* s, uint32_t len, uint2* ent, uint32_t* df,
-                                             uint32_t* scan_scratch) {
+__device__ __forceinline__ uint32_t rle_mem(const uint32_t* s, uint32_t len, uint2* ent, const CountArgs& ca,
+                                            uint32_t* scan_scratch) {
   uint32_t base = 0;
   for (uint32_t c0 = 0; c0 < len; c0 += THREADS * IPT) {
     const uint32_t lo = c0 + threadIdx.x * IPT;
@@ -94,42 +434,13 @@ __device__ __forceinline__ uint32_t rle_emit(const uint32_t* s, uint32_t len, ui
         uint32_t e = i + 1;
         while (e < len && s[e] == key) ++e;
         ent[pos] = make_uint2(key, e - i);
-        atomicAdd(df + key, 1u);
+        df_add(ca, key);
         ++pos;
       }
     }
     base += total;
   }
   return base;
-}
-
-template <int CAP, int THREADS>
-__global__ void __launch_bounds__(THREADS) count_smem_kernel(CountArgs a, const uint32_t* __restrict__ bin_docs,
-                                                             uint32_t n_bin) {
-  __shared__ uint32_t keys[CAP];
-  __shared__ uint32_t scan_scratch[THREADS / 32];
-  for (uint32_t q = blockIdx.x; q < n_bin; q += gridDim.x) {
-    const uint32_t d = bin_docs[q];
-    const uint64_t b = a.doc_off[d];
-    const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
-    const uint32_t P = next_pow2(len);
-    for (uint32_t i = threadIdx.x; i < P; i += THREADS) {
-      uint32_t v = kPadKey;
-      if (i < len) {
-        v = __ldg(a.tokens + b + i);
-        if (v >= a.vocab) {
-          atomicOr(a.err, 1u);
-          v = a.vocab - 1;
-        }
-      }
-      keys[i] = v;
-    }
-    __syncthreads();
-    bitonic_sort<THREADS>(keys, P);
-    uint32_t n = rle_emit<THREADS, CAP / THREADS>(keys, len, a.ent + b, a.df, scan_scratch);
-    if (threadIdx.x == 0) a.nnz[d] = n;
-    __syncthreads();
-  }
 }
 
 __global__ void __launch_bounds__(1024) count_large_kernel(CountArgs a, const uint32_t* __restrict__ long_docs,
@@ -142,28 +453,21 @@ __global__ void __launch_bounds__(1024) count_large_kernel(CountArgs a, const ui
     const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
     const uint32_t P = next_pow2(len);
     uint32_t* s = scratch + scratch_off[q];
-    for (uint32_t i = threadIdx.x; i < P; i += 1024) {
-      uint32_t v = kPadKey;
-      if (i < len) {
-        v = a.tokens[b + i];
-        if (v >= a.vocab) {
-          atomicOr(a.err, 1u);
-          v = a.vocab - 1;
-        }
-      }
-      s[i] = v;
-    }
+    for (uint32_t i = threadIdx.x; i < P; i += 1024) s[i] = load_key(a, b, i, len);
     __syncthreads();
-    bitonic_sort<1024>(s, P);
-    uint32_t n = rle_emit<1024, 8>(s, len, a.ent + b, a.df, scan_scratch);
+    bitonic_sort_mem<1024>(s, P);
+    uint32_t n = rle_mem<1024, 8>(s, len, a.ent + b, a, scan_scratch);
     if (threadIdx.x == 0) a.nnz[d] = n;
     __syncthreads();
   }
 }
 
-__global__ void idf_kernel(const uint32_t* __restrict__ df, uint32_t vocab, uint32_t n_docs, int weight_mode,
-                           TermInfo* __restrict__ info) {
+__global__ void idf_kernel(const uint32_t* __restrict__ df_rep, uint32_t reps, uint32_t vocab, uint32_t n_docs,
+                           int weight_mode, uint32_t* __restrict__ df, TermInfo* __restrict__ info) {
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < vocab; t += gridDim.x * blockDim.x) {
+    uint32_t c = 0;
+    for (uint32_t r = 0; r < reps; ++r) c += df_rep[static_cast<size_t>(r) * vocab + t];
+    df[t] = c;
     float idf = 1.0f;
     if (weight_mode == 1) idf = static_cast<float>(log((1.0 + n_docs) / (1.0 + df[t])) + 1.0);
     info[t] = TermInfo{idf, -1};
@@ -207,10 +511,13 @@ __global__ void inv_norm_kernel(const uint2* __restrict__ ent, const uint64_t* _
   }
 }
 
-int grid_for(uint32_t n, int per_sm) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+int grid_for(uint64_t n, int per_sm) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   uint64_t g = static_cast<uint64_t>(sms) * per_sm;
   if (g > n) g = n;
   return static_cast<int>(g < 1 ? 1 : g);
@@ -218,26 +525,38 @@ int grid_for(uint32_t n, int per_sm) {
 
 }  // namespace
 
-void launch_count_bin(int bin, const CountArgs& a, const uint32_t* bin_docs, uint32_t n_bin, cudaStream_t s) {
-  if (n_bin == 0) return;
-  switch (bin) {
+void launch_count_tiny(const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s) {
+  if (n == 0) return;
+  count_warp_kernel<2><<<grid_for(ceil_div(n, 8), 8), 256, 0, s>>>(a, docs, n);
+  note_launch();
+}
+
+void launch_count_chunks(const CountArgs& a, const uint2* chunks, uint32_t n, cudaStream_t s) {
+  if (n == 0) return;
+  chunk_sort_kernel<<<grid_for(ceil_div(n, 8), 8), 256, 0, s>>>(a, chunks, n);
+  note_launch();
+}
+
+void launch_count_merge(int cls, const CountArgs& a, const uint4* docs, uint32_t n, cudaStream_t s) {
+  if (n == 0) return;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(merge_kernel<4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4096 * 8);
+    cudaFuncSetAttribute(merge_kernel<8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 8192 * 8);
+    configured = true;
+  }
+  switch (cls) {
     case 0:
-      count_smem_kernel<256, 128><<<grid_for(n_bin, 16), 128, 0, s>>>(a, bin_docs, n_bin);
-      note_launch();
+      merge_kernel<1024><<<grid_for(n, 12), 256, 2 * 1024 * 8, s>>>(a, docs, n);
       break;
     case 1:
-      count_smem_kernel<1024, 256><<<grid_for(n_bin, 8), 256, 0, s>>>(a, bin_docs, n_bin);
-      note_launch();
-      break;
-    case 2:
-      count_smem_kernel<4096, 512><<<grid_for(n_bin, 4), 512, 0, s>>>(a, bin_docs, n_bin);
-      note_launch();
+      merge_kernel<4096><<<grid_for(n, 3), 256, 2 * 4096 * 8, s>>>(a, docs, n);
       break;
     default:
-      count_smem_kernel<8192, 1024><<<grid_for(n_bin, 2), 1024, 0, s>>>(a, bin_docs, n_bin);
-      note_launch();
+      merge_kernel<8192><<<grid_for(n, 1), 256, 2 * 8192 * 8, s>>>(a, docs, n);
       break;
   }
+  note_launch();
 }
 
 void launch_count_large(const CountArgs& a, const uint32_t* long_docs, const uint64_t* scratch_off, uint32_t n_long,
@@ -247,9 +566,9 @@ void launch_count_large(const CountArgs& a, const uint32_t* long_docs, const uin
   note_launch();
 }
 
-void launch_idf(const uint32_t* df, uint32_t vocab, uint32_t n_docs, int weight_mode, TermInfo* info,
-                cudaStream_t s) {
-  idf_kernel<<<grid_for((vocab + 255) / 256, 8), 256, 0, s>>>(df, vocab, n_docs, weight_mode, info);
+void launch_idf(const uint32_t* df_rep, uint32_t reps, uint32_t vocab, uint32_t n_docs, int weight_mode, uint32_t* df,
+                TermInfo* info, cudaStream_t s) {
+  idf_kernel<<<grid_for((vocab + 255) / 256, 8), 256, 0, s>>>(df_rep, reps, vocab, n_docs, weight_mode, df, info);
   note_launch();
 }
 

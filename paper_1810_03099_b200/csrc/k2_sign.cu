@@ -100,29 +100,52 @@ __global__ void __launch_bounds__(256) sign_kernel(SignArgs a) {
 #pragma unroll
       for (int q = 0; q < KPL; ++q) acc[q] = 0.0f;
       float sq = 0.0f;
+      // software pipeline: the next chunk's rows are in flight while the
+      // current chunk's hits are gathered
+      uint2 xn = lane < n ? __ldg(e + lane) : make_uint2(0u, 0u);
       for (uint32_t c = 0; c < n; c += 32) {
         const uint32_t i = c + lane;
+        const uint2 x = xn;
+        if (i + 32 < n) xn = __ldg(e + i + 32);
         float w = 0.0f;
         int32_t row = -1;
         if (i < n) {
-          const uint2 x = __ldg(e + i);
           const TermInfo ti = a.info[x.x];
           w = static_cast<float>(x.y) * ti.idf;
           row = ti.ref_row;
         }
         sq = fmaf(w, w, sq);
         uint32_t hits = __ballot_sync(0xffffffffu, row >= 0);
+        // hits in ascending term order, 8 reference rows in flight per batch;
+        // FMAs stay in hit order, so every column sums in the same order.
         while (hits) {
-          const int src = __ffs(hits) - 1;
-          hits &= hits - 1;
-          const int32_t rr = __shfl_sync(0xffffffffu, row, src);
-          const float ww = __shfl_sync(0xffffffffu, w, src);
-          const float* __restrict__ Rr = a.R + static_cast<size_t>(rr) * K + k0;
+          constexpr int B = 8;
+          int32_t rr[B];
+          float ww[B];
 #pragma unroll
-          for (int q = 0; q < KPL; ++q) {
-            const uint32_t k = lane + 32 * q;
-            if (k0 + k < K) acc[q] = fmaf(ww, __ldg(Rr + k), acc[q]);
+          for (int u = 0; u < B; ++u) {
+            const int src = hits ? __ffs(hits) - 1 : 0;
+            const bool ok = hits != 0;
+            hits &= hits - 1;
+            rr[u] = __shfl_sync(0xffffffffu, row, src);
+            ww[u] = __shfl_sync(0xffffffffu, w, src);
+            if (!ok) rr[u] = -1;
           }
+          float val[B][KPL];
+#pragma unroll
+          for (int u = 0; u < B; ++u) {
+            const float* __restrict__ Rr = a.R + static_cast<size_t>(rr[u] < 0 ? 0 : rr[u]) * K + k0;
+#pragma unroll
+            for (int q = 0; q < KPL; ++q) {
+              const uint32_t k = lane + 32 * q;
+              val[u][q] = (rr[u] >= 0 && k0 + k < K) ? __ldg(Rr + k) : 0.0f;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < B; ++u)
+#pragma unroll
+            for (int q = 0; q < KPL; ++q)
+              if (rr[u] >= 0) acc[q] = fmaf(ww[u], val[u][q], acc[q]);
         }
       }
       if (k0 == 0) {
@@ -142,10 +165,8 @@ __global__ void __launch_bounds__(256) sign_kernel(SignArgs a) {
     }
     ss = warp_sum(ss);
     const float inv_s = ss > 0.0f ? 1.0f / sqrtf(ss) : 0.0f;  // SPEC.md:372 all-zero -> 0
-    for (uint32_t k = lane; k < K; k += 32) {
-      const size_t o = static_cast<size_t>(d) * K + k;
-      a.Sn[o] = a.S[o] * inv_s;  // same-thread read-after-write
-    }
+    for (uint32_t k = lane; k < K; k += 32)
+      a.ST[static_cast<size_t>(k) * a.ld + d] = a.S[static_cast<size_t>(d) * K + k] * inv_s;  // own write
   }
 }
 

@@ -15,10 +15,7 @@
 // output positions, so the candidate list is sorted and identical for every
 // launch configuration without a device sort.
 //
-// MRC tile: 256 threads, 8x8 register micro-tile per thread over the two
-// halves of the tile (conflict-free float4 LDS), K-chunks of 32 staged in
-// shared memory. Inner loop: 4 LDS.128 per 64 FFMA. Epilogue: per row a
-// nibble per half, OR-combined across the 8 lanes that share a 32-bit word.
+// MRC tile kernel: see the comment above mrc_bitmap_kernel.
 
 #include "kernels.cuh"
 
@@ -58,90 +55,168 @@ __device__ __forceinline__ uint32_t col_mask(uint32_t lo, uint32_t i, const Pair
   return m;
 }
 
-__global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel(const float* __restrict__ Sr,
-                                                            const float* __restrict__ Sc, uint32_t K, float tau,
-                                                            PairGrid g, uint32_t nbr, uint32_t nbc,
-                                                            uint32_t* __restrict__ bitmap,
-                                                            uint32_t* __restrict__ rowcnt) {
-  __shared__ __align__(16) float As[kKC][kTile];
-  __shared__ __align__(16) float Bs[kKC][kTile];
-  uint32_t bi, bj;
-  tile_coords(blockIdx.x + g.tile0, nbr, nbc, g.triangle, bi, bj);
+// ---- K3: MRC tile kernel ---------------------------------------------------
+// Persistent CTAs walk a contiguous range of tiles; (tile, K-chunk) stages are
+// double-buffered in shared memory with cp.async (16 B chunks of the
+// transposed unit signatures ST[k][ld]). Thread (ty,tx) owns rows ty*8..+7
+// and columns tx*8..+7 of the 128x128 tile; shared memory stores each panel
+// in "split" order (columns c%8<4 in the first half) so both float4 loads of
+// a thread are bank-conflict free while its 8 columns stay contiguous. The
+// inner loop is 2+2 LDS.128 and 32 FFMA2 (fma.rn.f32x2, scalar-broadcast A)
+// per k. Epilogue: one byte per owned row (8 contiguous columns, bit c =
+// dot >= tau) -> shared memory -> each of 128 threads assembles a row's 16
+// bytes (the row's 128 bits in natural order), masks, stores 16 B and bumps
+// the row count.
+
+__device__ __forceinline__ uint32_t split_pos(uint32_t c) {  // smem slot of panel column c
+  return (c & 4u) ? 64u + (c >> 3) * 4u + (c & 3u) : (c >> 3) * 4u + (c & 3u);
+}
+
+// d = a*b + c on both fp32 lanes (FFMA2); `a` is broadcast (SASS scalar operand).
+__device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
+  float2 aa = make_float2(a, a);
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&aa)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+struct MrcArgs {
+  const float* STr;
+  const float* STc;
+  uint32_t ldr, ldc;
+  uint32_t K;
+  float tau;
+  PairGrid g;
+  uint32_t nbr, nbc;
+  uint64_t n_tiles;
+  uint32_t* bitmap;
+  uint32_t* rowcnt;
+};
+
+__global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel(MrcArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  const uint32_t kc_max = a.K < kKC ? a.K : kKC;
+  const uint32_t panel = kc_max * kTile;  // floats per panel stage
+  // stage st: A panel at smem + 2*st*panel, B panel right after it
+  uint8_t* rowbytes = reinterpret_cast<uint8_t*>(smem + 4 * panel);  // [128][16]
+
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
-  const uint32_t row0 = bi * kTile, col0 = bj * kTile;
+  const uint64_t t_begin = a.n_tiles * blockIdx.x / gridDim.x;
+  const uint64_t t_end = a.n_tiles * (blockIdx.x + 1) / gridDim.x;
+  if (t_begin >= t_end) return;
+  const uint32_t nchunks = (a.K + kKC - 1) / kKC;
+  const uint64_t items = (t_end - t_begin) * nchunks;
 
-  float acc[8][8];
-#pragma unroll
-  for (int r = 0; r < 8; ++r)
-#pragma unroll
-    for (int c = 0; c < 8; ++c) acc[r][c] = 0.0f;
+  uint32_t bi, bj;
+  tile_coords(static_cast<uint32_t>(t_begin) + a.g.tile0, a.nbr, a.nbc, a.g.triangle, bi, bj);
+  // issue the loads of item `it` (tile t_begin + it / nchunks, chunk it % nchunks) into stage st
+  uint32_t li = bi, lj = bj;  // tile coords of the next item to load
+  uint32_t lchunk = 0;
+  auto issue = [&](int st) {
+    const uint32_t k0 = lchunk * kKC;
+    const uint32_t kc = min(static_cast<uint32_t>(kKC), a.K - k0);
+    const uint32_t n16 = kc * (kTile / 4);  // 16-byte chunks per panel
+    for (uint32_t idx = tid; idx < 2 * n16; idx += 256) {
+      const bool isB = idx >= n16;
+      const uint32_t id = isB ? idx - n16 : idx;
+      const uint32_t k = id >> 5, m = id & 31;  // row k, 16-byte chunk m (cols 4m..4m+3)
+      const float* src = isB ? a.STc + static_cast<size_t>(k0 + k) * a.ldc + lj * kTile + 4 * m
+                             : a.STr + static_cast<size_t>(k0 + k) * a.ldr + li * kTile + 4 * m;
+      float* dst = smem + (2 * st + (isB ? 1 : 0)) * panel + k * kTile + split_pos(4 * m);
+      cp_async16(dst, src);
+    }
+    cp_async_commit();
+    if (++lchunk == nchunks) {
+      lchunk = 0;
+      if (++lj == a.nbc) {
+        ++li;
+        lj = a.g.triangle ? li : 0;
+      }
+    }
+  };
 
-  for (uint32_t k0 = 0; k0 < K; k0 += kKC) {
-    const uint32_t kc = min(static_cast<uint32_t>(kKC), K - k0);
-    // Stage the row and column panels (row-major Sn -> [k][row] in smem).
-    for (uint32_t idx = tid; idx < kTile * kc; idx += 256) {
-      const uint32_t r = idx / kc, k = idx - r * kc;
-      const uint32_t gi = row0 + r, gj = col0 + r;
-      As[k][r] = gi < g.n_rows ? __ldg(Sr + static_cast<size_t>(gi) * K + k0 + k) : 0.0f;
-      Bs[k][r] = gj < g.n_cols ? __ldg(Sc + static_cast<size_t>(gj) * K + k0 + k) : 0.0f;
+  float2 acc[8][4];
+  issue(0);
+  for (uint64_t it = 0; it < items; ++it) {
+    const int st = static_cast<int>(it & 1);
+    const uint32_t chunk = static_cast<uint32_t>(it % nchunks);
+    if (it + 1 < items) {
+      issue(st ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-#pragma unroll 4
-    for (uint32_t k = 0; k < kc; ++k) {
-      const float4 a0 = *reinterpret_cast<const float4*>(&As[k][ty * 4]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&As[k][64 + ty * 4]);
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
-      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[k][64 + tx * 4]);
-      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    if (chunk == 0) {
 #pragma unroll
       for (int r = 0; r < 8; ++r)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
+        for (int c = 0; c < 4; ++c) acc[r][c] = make_float2(0.0f, 0.0f);
     }
-    __syncthreads();
-  }
-
-  // Epilogue: bit (r,c) = acc >= tau; assemble 32-bit words across 8 lanes.
-  const int sh = (tx & 7) * 4;
-  uint32_t my_w0 = 0, my_w1 = 0;
+    const uint32_t kc = min(static_cast<uint32_t>(kKC), a.K - chunk * kKC);
+    const float* A = smem + 2 * st * panel;
+    const float* B = A + panel;
+#pragma unroll 4
+    for (uint32_t k = 0; k < kc; ++k) {
+      const float4 a0 = *reinterpret_cast<const float4*>(A + k * kTile + ty * 4);
+      const float4 a1 = *reinterpret_cast<const float4*>(A + k * kTile + 64 + ty * 4);
+      const float4 b0 = *reinterpret_cast<const float4*>(B + k * kTile + tx * 4);
+      const float4 b1 = *reinterpret_cast<const float4*>(B + k * kTile + 64 + tx * 4);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                            make_float2(b1.z, b1.w)};
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    uint32_t n0 = 0, n1 = 0;
+      for (int r = 0; r < 8; ++r)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      n0 |= (acc[r][c] >= tau ? 1u : 0u) << c;
-      n1 |= (acc[r][c + 4] >= tau ? 1u : 0u) << c;
+        for (int c = 0; c < 4; ++c) acc[r][c] = ffma2(av[r], bv[c], acc[r][c]);
     }
-    uint32_t w0 = n0 << sh, w1 = n1 << sh;
-    w0 |= __shfl_xor_sync(0xffffffffu, w0, 1);
-    w1 |= __shfl_xor_sync(0xffffffffu, w1, 1);
-    w0 |= __shfl_xor_sync(0xffffffffu, w0, 2);
-    w1 |= __shfl_xor_sync(0xffffffffu, w1, 2);
-    w0 |= __shfl_xor_sync(0xffffffffu, w0, 4);
-    w1 |= __shfl_xor_sync(0xffffffffu, w1, 4);
-    if ((tx & 7) == r) {
-      my_w0 = w0;
-      my_w1 = w1;
+    __syncthreads();  // stage st is refilled by the next issue
+    if (chunk + 1 == nchunks) {
+      // bits: row r (ty*8+r), byte tx, bit c = column tx*8+c
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        uint32_t byte = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          byte |= (acc[r][c].x >= a.tau ? 1u : 0u) << (2 * c);
+          byte |= (acc[r][c].y >= a.tau ? 1u : 0u) << (2 * c + 1);
+        }
+        rowbytes[(ty * 8 + r) * 16 + tx] = static_cast<uint8_t>(byte);
+      }
+      __syncthreads();
+      if (tid < kTile) {
+        const uint32_t i = bi * kTile + tid;
+        if (i < a.g.n_rows) {
+          uint4 wv = *reinterpret_cast<const uint4*>(rowbytes + tid * 16);
+          const uint32_t c0 = bj * kTile;
+          wv.x &= col_mask(c0, i, a.g);
+          wv.y &= col_mask(c0 + 32, i, a.g);
+          wv.z &= col_mask(c0 + 64, i, a.g);
+          wv.w &= col_mask(c0 + 96, i, a.g);
+          *reinterpret_cast<uint4*>(a.bitmap + static_cast<size_t>(i) * a.g.words_per_row + bj * 4) = wv;
+          const uint32_t cnt = __popc(wv.x) + __popc(wv.y) + __popc(wv.z) + __popc(wv.w);
+          if (cnt) atomicAdd(a.rowcnt + i, cnt);
+        }
+      }
+      // next tile (rowbytes reuse is ordered by the next item's __syncthreads)
+      if (++bj == a.nbc) {
+        ++bi;
+        bj = a.g.triangle ? bi : 0;
+      }
     }
   }
-  const int r = tx & 7;
-  const uint32_t lr = r < 4 ? ty * 4 + r : 64 + ty * 4 + (r - 4);
-  const uint32_t i = row0 + lr;
-  const uint32_t grp = tx >> 3;  // word 0/1 of each 64-column half
-  uint32_t cnt = 0;
-  if (i < g.n_rows) {
-    const uint32_t wa = grp, wb = 2 + grp;
-    const uint32_t va = my_w0 & col_mask(col0 + wa * 32, i, g);
-    const uint32_t vb = my_w1 & col_mask(col0 + wb * 32, i, g);
-    uint32_t* rowp = bitmap + static_cast<size_t>(i) * g.words_per_row + bj * 4;
-    rowp[wa] = va;
-    rowp[wb] = vb;
-    cnt = __popc(va) + __popc(vb);
-  }
-  cnt += __shfl_xor_sync(0xffffffffu, cnt, 8);
-  if (grp == 0 && cnt && i < g.n_rows) atomicAdd(rowcnt + i, cnt);
 }
 
 // Hamming tile: warp w handles rows (w&3)*32+lane and words (w>>2)*2..+1.
@@ -246,13 +321,23 @@ uint64_t n_tiles(PairGrid& g, uint32_t& nbr, uint32_t& nbc) {
 
 }  // namespace
 
-void launch_mrc_bitmap(const float* Sn_rows, const float* Sn_cols, uint32_t K, float tau, const PairGrid& g_in,
-                       uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s) {
+void launch_mrc_bitmap(const float* ST_rows, uint32_t ld_rows, const float* ST_cols, uint32_t ld_cols, uint32_t K,
+                       float tau, const PairGrid& g_in, uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s) {
   PairGrid g = g_in;
   uint32_t nbr, nbc;
   const uint64_t t = n_tiles(g, nbr, nbc);
-  if (t == 0) return;
-  mrc_bitmap_kernel<<<static_cast<unsigned>(t), 256, 0, s>>>(Sn_rows, Sn_cols, K, tau, g, nbr, nbc, bitmap, rowcnt);
+  if (t == 0 || K == 0) return;
+  const uint32_t kc = K < kKC ? K : kKC;
+  const size_t smem = (4ull * kc * kTile) * sizeof(float) + kTile * 16;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(mrc_bitmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kKC * kTile * 4 + 4096);
+    configured = true;
+  }
+  uint64_t grid = static_cast<uint64_t>(sms()) * 2;
+  if (grid > t) grid = t;
+  MrcArgs a{ST_rows, ST_cols, ld_rows, ld_cols, K, tau, g, nbr, nbc, t, bitmap, rowcnt};
+  mrc_bitmap_kernel<<<static_cast<unsigned>(grid), 256, smem, s>>>(a);
   note_launch();
 }
 

@@ -24,6 +24,16 @@
 namespace refsig_gpu {
 namespace {
 
+// s += w when (h & bit) != 0: one LOP3 (predicate out) + one predicated DADD.
+__device__ __forceinline__ void add_if_bit(double& s, double w, uint32_t h, uint32_t bit) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+      "and.b32 t, %2, %3;\n\t"
+      "setp.ne.u32 p, t, 0;\n\t"
+      "@p add.f64 %0, %0, %1;\n\t}"
+      : "+d"(s)
+      : "d"(w), "r"(h), "r"(bit));
+}
+
 struct __align__(16) Staged {
   uint32_t lo, hi;
   double w;
@@ -57,8 +67,8 @@ __global__ void __launch_bounds__(256) simhash_kernel(SimhashArgs a) {
 #pragma unroll 8
       for (uint32_t q = 0; q < m; ++q) {
         const Staged v = stage[wid][q];
-        if (v.lo & bit) s1a += v.w;
-        if (v.hi & bit) s1b += v.w;
+        add_if_bit(s1a, v.w, v.lo, bit);
+        add_if_bit(s1b, v.w, v.hi, bit);
       }
       __syncwarp();
     }

@@ -15,10 +15,13 @@
 namespace refsig_gpu {
 
 // ---- K1 -------------------------------------------------------------------
-// Length bins of the count kernel; docs longer than kCountSmemMax are sorted
-// in a global scratch region (next_pow2(len) keys each).
-constexpr uint32_t kBinCap[4] = {256, 1024, 4096, 8192};
-constexpr uint32_t kCountSmemMax = 8192;
+// Count work plan (k1_count.cu): tiny docs (<= kTinyMax), 256-token chunks,
+// per-doc chunk merges in three shared-memory size classes, and long docs
+// (> kMergeMax) sorted in a global scratch region.
+constexpr uint32_t kTinyMax = 64;
+constexpr uint32_t kChunk = 256;
+constexpr uint32_t kMergeCap[3] = {1024, 4096, 8192};
+constexpr uint32_t kMergeMax = 8192;
 
 struct CountArgs {
   const uint32_t* tokens;
@@ -26,16 +29,22 @@ struct CountArgs {
   uint32_t vocab;
   uint2* ent;        // padded CSR: doc d's (id,count) rows at ent[doc_off[d] ..)
   uint32_t* nnz;     // [n_docs]
-  uint32_t* df;      // [vocab], zeroed by the launcher
+  uint32_t* df;      // [df_reps][vocab] replicas, zeroed by the caller
+  uint32_t df_reps;
   uint32_t* err;     // bit 0: token id >= vocab
+  uint2* scratch;    // [T] per-chunk sorted unique rows (at the chunk's token offset)
+  uint32_t* chunk_cnt;
 };
 
-void launch_count_bin(int bin, const CountArgs& a, const uint32_t* bin_docs, uint32_t n_bin, cudaStream_t s);
+void launch_count_tiny(const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s);
+void launch_count_chunks(const CountArgs& a, const uint2* chunks, uint32_t n, cudaStream_t s);
+void launch_count_merge(int cls, const CountArgs& a, const uint4* docs, uint32_t n, cudaStream_t s);
 void launch_count_large(const CountArgs& a, const uint32_t* long_docs, const uint64_t* scratch_off,
                         uint32_t n_long, uint32_t* scratch, cudaStream_t s);
-// idf32[t] = fl32(ln((1+N)/(1+df))+1) (or 1 for raw-TF weighting); ref_row = -1.
-void launch_idf(const uint32_t* df, uint32_t vocab, uint32_t n_docs, int weight_mode, TermInfo* info,
-                cudaStream_t s);
+// df[t] = sum of the replicas; idf32[t] = fl32(ln((1+N)/(1+df))+1) (or 1 for
+// raw-TF weighting); ref_row = -1.
+void launch_idf(const uint32_t* df_rep, uint32_t reps, uint32_t vocab, uint32_t n_docs, int weight_mode, uint32_t* df,
+                TermInfo* info, cudaStream_t s);
 // Compact padded CSR -> rowptr/ids/counts (rowptr from an exclusive scan of nnz).
 void launch_compact_csr(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const uint64_t* rowptr,
                         uint32_t n_docs, uint32_t* ids, uint32_t* counts, cudaStream_t s);
@@ -79,7 +88,8 @@ struct SignArgs {
   uint32_t n_docs;
   uint32_t K;
   float* S;         // [n_docs*K] raw cosines, row-major (API output)
-  float* Sn;        // [n_docs*K] unit-normalised signatures (K3 operand; 0 row if all-zero)
+  float* ST;        // [K][ld] unit-normalised signatures, transposed (K3 operand; 0 if all-zero)
+  uint32_t ld;      // leading dimension of ST (n_docs rounded up to 128; pad columns zero)
   float* inv_norm;  // [n_docs] 1/||w_d||
 };
 void launch_sign(const SignArgs& a, cudaStream_t s);
@@ -97,7 +107,8 @@ struct PairGrid {
   uint32_t row_end;
   uint32_t tile0;       // first tile index (set by the launcher)
 };
-void launch_mrc_bitmap(const float* Sn_rows, const float* Sn_cols, uint32_t K, float tau, const PairGrid& g, uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s);
+void launch_mrc_bitmap(const float* ST_rows, uint32_t ld_rows, const float* ST_cols, uint32_t ld_cols, uint32_t K,
+                       float tau, const PairGrid& g, uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s);
 void launch_hamming_bitmap(const uint64_t* f_rows, const uint64_t* f_cols, int max_dist, const PairGrid& g,
                            uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s);
 // keys (i<<32|j) in ascending order at rowstart[i]..; writes only < capacity.
