@@ -76,6 +76,10 @@ struct refsig_gpu_ctx {
   int device = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
+  // side streams + events for the fork/join inside count() (independent K1
+  // work classes overlap instead of serialising their tails)
+  cudaStream_t side[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_mid = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
   std::string err;
   uint64_t* h_pin = nullptr;  // pinned scratch for small D2H reads
 
@@ -86,9 +90,10 @@ struct refsig_gpu_ctx {
   std::vector<uint64_t> h_off;
   DevBuf tokens, doc_off;
   const uint32_t* tok = nullptr;
-  DevBuf tiny_docs, chunks, chunk_cnt, chunk_scratch, merge_docs[3];
-  uint32_t n_tiny = 0, n_chunks = 0, n_merge[3] = {0, 0, 0};
+  DevBuf tiny_docs, chunks[2], chunk_cnt, chunk_scratch, mdocs[kMergeClasses];
+  uint32_t n_tiny = 0, n_chunks[2] = {0, 0}, n_mdocs[kMergeClasses] = {};
   DevBuf long_docs, long_off, long_scratch;
+  DevBuf order;  // docs by decreasing length (per-doc kernels take long docs first)
   uint32_t n_long = 0;
 
   // K1
@@ -100,7 +105,7 @@ struct refsig_gpu_ctx {
 
   // reference
   bool have_ref = false;
-  uint32_t K = 0;
+  uint32_t K = 0, Kp = 0;  // Kp: row stride of R
   DevBuf ref_docs, ref_start, ref_n, ref_ent, ref_mark, ref_prefix, R;
 
   // sign
@@ -306,7 +311,7 @@ void build_reference(refsig_gpu_ctx* c, const RefArgs& r, uint64_t u_cap) {
   c->ref_prefix.ensure(sizeof(uint64_t) * (V + 1));
   c->scan_tmp.ensure(scan_tmp_bytes(V));
   if (u_cap > V) u_cap = V;
-  const size_t rbytes = sizeof(float) * std::max<uint64_t>(u_cap, 1) * r.K;
+  const size_t rbytes = sizeof(float) * std::max<uint64_t>(u_cap, 1) * r.Kp;
   c->R.ensure(rbytes);
   Phase ph(c, REFSIG_PHASE_REFERENCE);
   ck(cudaMemsetAsync(c->ref_mark.p, 0, sizeof(uint32_t) * V, c->stream), "memset");
@@ -318,6 +323,7 @@ void build_reference(refsig_gpu_ctx* c, const RefArgs& r, uint64_t u_cap) {
   launch_ref_fill(r, c->info.as<TermInfo>(), c->R.as<float>(), c->stream);
   launched("reference");
   c->K = r.K;
+  c->Kp = r.Kp;
   c->have_ref = true;
   c->signed_ = false;
 }
@@ -350,8 +356,8 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
      "H2D doc_off");
   // K1 work plan (host metadata only): see k1_count.cu.
   std::vector<uint32_t> tiny, longs;
-  std::vector<uint2> chunks;
-  std::vector<uint4> merges[3];
+  std::vector<uint2> chunks[2];     // warp sorts of 256 / 512 keys
+  std::vector<uint32_t> mdocs[kMergeClasses];  // multi-chunk docs by size class
   std::vector<uint64_t> loff;
   uint64_t scratch = 0;
   for (uint32_t d = 0; d < n_docs; ++d) {
@@ -359,13 +365,16 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
     require(len < (1ull << 31), "document longer than 2^31 tokens");
     if (len <= kTinyMax) {
       tiny.push_back(d);
-    } else if (len <= kChunk) {
-      chunks.push_back(make_uint2(d, 1u));  // chunk 0, direct
+    } else if (len <= 256) {
+      chunks[0].push_back(make_uint2(d, (1u << 16) | 1u));  // whole doc, direct
+    } else if (len <= kMergeChunk) {
+      chunks[1].push_back(make_uint2(d, (1u << 16) | 1u));
     } else if (len <= kMergeMax) {
-      const uint32_t m = static_cast<uint32_t>(ceil_div(len, kChunk));
-      const int cls = len <= kMergeCap[0] ? 0 : (len <= kMergeCap[1] ? 1 : 2);
-      merges[cls].push_back(make_uint4(d, static_cast<uint32_t>(chunks.size()), m, 0u));
-      for (uint32_t q = 0; q < m; ++q) chunks.push_back(make_uint2(d, q << 1));
+      const uint32_t m = static_cast<uint32_t>(ceil_div(len, kMergeChunk));
+      int cls = 0;
+      while (len > kMergeCap[cls]) ++cls;
+      mdocs[cls].push_back(static_cast<uint32_t>(chunks[1].size()));
+      for (uint32_t q = 0; q < m; ++q) chunks[1].push_back(make_uint2(d, (m << 16) | (q << 1)));
     } else {
       longs.push_back(d);
       loff.push_back(scratch);
@@ -379,15 +388,27 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
     buf.ensure(bytes);
     ck(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, c->stream), "H2D plan");
   };
+  std::vector<uint32_t> order(n_docs);
+  for (uint32_t d = 0; d < n_docs; ++d) order[d] = d;
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
+    return doc_off[x + 1] - doc_off[x] > doc_off[y + 1] - doc_off[y];
+  });
+  up(c->order, order.data(), 4ull * n_docs);
   c->n_tiny = static_cast<uint32_t>(tiny.size());
   up(c->tiny_docs, tiny.data(), 4 * tiny.size());
-  c->n_chunks = static_cast<uint32_t>(chunks.size());
-  up(c->chunks, chunks.data(), sizeof(uint2) * chunks.size());
-  c->chunk_cnt.ensure(4 * std::max<size_t>(chunks.size(), 1));
-  for (int k = 0; k < 3; ++k) {
-    c->n_merge[k] = static_cast<uint32_t>(merges[k].size());
-    up(c->merge_docs[k], merges[k].data(), sizeof(uint4) * merges[k].size());
+  for (int k = 0; k < 2; ++k) {
+    c->n_chunks[k] = static_cast<uint32_t>(chunks[k].size());
+    up(c->chunks[k], chunks[k].data(), sizeof(uint2) * chunks[k].size());
   }
+  for (int k = 0; k < kMergeClasses; ++k) {
+    // longest docs first within a merge class
+    std::stable_sort(mdocs[k].begin(), mdocs[k].end(), [&](uint32_t x, uint32_t y) {
+      return (chunks[1][x].y >> 16) > (chunks[1][y].y >> 16);
+    });
+    c->n_mdocs[k] = static_cast<uint32_t>(mdocs[k].size());
+    up(c->mdocs[k], mdocs[k].data(), 4 * mdocs[k].size());
+  }
+  c->chunk_cnt.ensure(4 * std::max<size_t>(chunks[1].size(), 1));
   c->n_long = static_cast<uint32_t>(longs.size());
   if (!longs.empty()) {
     c->long_scratch.ensure(sizeof(uint32_t) * scratch);
@@ -423,9 +444,15 @@ int refsig_gpu_create(int device, refsig_gpu_ctx** out) {
   refsig_gpu_ctx* c = new (std::nothrow) refsig_gpu_ctx();
   if (!c) return REFSIG_E_RUNTIME;
   c->device = device;
-  if (cudaSetDevice(device) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaMallocHost(&c->h_pin, 64) != cudaSuccess) {
+  bool ok = cudaSetDevice(device) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaMallocHost(&c->h_pin, 64) == cudaSuccess &&
+            cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&c->ev_mid, cudaEventDisableTiming) == cudaSuccess;
+  for (int k = 0; ok && k < 3; ++k)
+    ok = cudaStreamCreateWithFlags(&c->side[k], cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&c->ev_join[k], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
     cudaGetLastError();
     delete c;
     return REFSIG_E_RUNTIME;
@@ -439,6 +466,15 @@ void refsig_gpu_destroy(refsig_gpu_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  for (int k = 0; k < 3; ++k) {
+    if (ctx->side[k]) {
+      cudaStreamSynchronize(ctx->side[k]);
+      cudaStreamDestroy(ctx->side[k]);
+    }
+    if (ctx->ev_join[k]) cudaEventDestroy(ctx->ev_join[k]);
+  }
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_mid) cudaEventDestroy(ctx->ev_mid);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
   delete ctx;
@@ -512,11 +548,26 @@ int refsig_gpu_count(refsig_gpu_ctx* ctx, int weight_mode) {
     CountArgs a{ctx->tok, ctx->doc_off.as<uint64_t>(), V, ctx->ent.as<uint2>(), ctx->nnz.as<uint32_t>(),
                 ctx->df_rep.as<uint32_t>(), reps, ctx->flags.as<uint32_t>(), ctx->chunk_scratch.as<uint2>(),
                 ctx->chunk_cnt.as<uint32_t>()};
-    launch_count_tiny(a, ctx->tiny_docs.as<uint32_t>(), ctx->n_tiny, ctx->stream);
-    launch_count_chunks(a, ctx->chunks.as<uint2>(), ctx->n_chunks, ctx->stream);
-    for (int k = 0; k < 3; ++k) launch_count_merge(k, a, ctx->merge_docs[k].as<uint4>(), ctx->n_merge[k], ctx->stream);
+    // fork: the 512-token chunk sorts (critical path, then the merges) on the
+    // main stream; tiny docs, 256-key docs and long docs on side[0]; merge
+    // classes spread over all four streams once the chunks are sorted.
+    cudaStream_t m0 = ctx->stream;
+    ck(cudaEventRecord(ctx->ev_fork, m0), "fork");
+    for (int k = 0; k < 3; ++k) ck(cudaStreamWaitEvent(ctx->side[k], ctx->ev_fork, 0), "fork");
+    launch_count_chunks(16, a, ctx->chunks[1].as<uint2>(), ctx->n_chunks[1], m0);
+    ck(cudaEventRecord(ctx->ev_mid, m0), "mid");
+    launch_count_tiny(a, ctx->tiny_docs.as<uint32_t>(), ctx->n_tiny, ctx->side[0]);
+    launch_count_chunks(8, a, ctx->chunks[0].as<uint2>(), ctx->n_chunks[0], ctx->side[0]);
     launch_count_large(a, ctx->long_docs.as<uint32_t>(), ctx->long_off.as<uint64_t>(), ctx->n_long,
-                       ctx->long_scratch.as<uint32_t>(), ctx->stream);
+                       ctx->long_scratch.as<uint32_t>(), ctx->side[0]);
+    cudaStream_t ms[kMergeClasses] = {ctx->side[0], ctx->side[1], ctx->side[2], m0};
+    for (int k = 0; k < 3; ++k) ck(cudaStreamWaitEvent(ctx->side[k], ctx->ev_mid, 0), "mid");
+    for (int k = kMergeClasses - 1; k >= 0; --k)
+      launch_count_merge(k, a, ctx->chunks[1].as<uint2>(), ctx->mdocs[k].as<uint32_t>(), ctx->n_mdocs[k], ms[k]);
+    for (int k = 0; k < 3; ++k) {  // join
+      ck(cudaEventRecord(ctx->ev_join[k], ctx->side[k]), "join");
+      ck(cudaStreamWaitEvent(m0, ctx->ev_join[k], 0), "join");
+    }
     launch_idf(ctx->df_rep.as<uint32_t>(), reps, V, N, weight_mode, ctx->df.as<uint32_t>(), ctx->info.as<TermInfo>(),
                ctx->stream);
     ctx->weight_mode = weight_mode;
@@ -622,7 +673,7 @@ int refsig_gpu_set_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_i
     upload(ctx, ctx->ref_docs.p, ref_doc_ids, 4ull * K);
     launch_ref_doc_ranges(ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->ref_docs.as<uint32_t>(), K,
                           ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->stream);
-    RefArgs r{K, ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->ent.as<uint2>(), false};
+    RefArgs r{K, ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->ent.as<uint2>(), false, (K + 3) & ~3u};
     build_reference(ctx, r, u_cap);
   });
 }
@@ -664,7 +715,8 @@ int refsig_gpu_set_reference_vectors(refsig_gpu_ctx* ctx, uint32_t K, const uint
     if (n) ck(cudaMemcpyAsync(ctx->ref_ent.p, h.data(), sizeof(uint2) * n, cudaMemcpyHostToDevice, ctx->stream), "H2D");
     ck(cudaMemcpyAsync(ctx->ref_start.p, start.data(), 8ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D");
     ck(cudaMemcpyAsync(ctx->ref_n.p, cnt.data(), 4ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D");
-    RefArgs r{K, ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->ref_ent.as<uint2>(), true};
+    RefArgs r{K, ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->ref_ent.as<uint2>(), true,
+              (K + 3) & ~3u};
     build_reference(ctx, r, n);
     ck(cudaStreamSynchronize(ctx->stream), "reference");
   });
@@ -698,7 +750,8 @@ int refsig_gpu_sign(refsig_gpu_ctx* ctx) {
     ctx->inv_norm.ensure(sizeof(float) * N);
     if (ctx->db) ck(cudaStreamSynchronize(ctx->db->stream), "sync database");
     SignArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->info.as<TermInfo>(),
-               refc->R.as<float>(), N, K, ctx->S.as<float>(), ctx->ST.as<float>(), ld, ctx->inv_norm.as<float>()};
+               refc->R.as<float>(), N, K, refc->Kp, ctx->order.as<uint32_t>(), ctx->S.as<float>(),
+               ctx->ST.as<float>(), ld, ctx->inv_norm.as<float>()};
     {
       Phase ph(ctx, REFSIG_PHASE_SIGN);
       launch_sign(a, ctx->stream);

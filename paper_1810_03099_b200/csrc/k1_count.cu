@@ -21,11 +21,11 @@
 // registers too (neighbour via SHFL, positions via warp/block scans, run ends
 // via a suffix-min of the next head). Work plan (host-built at upload):
 //   <= 64 tokens: warp per doc, 64-key sort;
-//   65..256: one 256-key warp sort per doc (a "direct" chunk);
-//   257..8192: every 256-token chunk sorted + run-length encoded by a warp,
-//     then one CTA per doc merges the chunks' unique rows in shared memory
-//     (merge path) and sums equal ids — no padding beyond the last chunk and
-//     O(n log(n/256)) merge work instead of a full bitonic network;
+//   65..256 / 257..512: one warp per doc sorting 256 / 512 keys in
+//     registers (IPT 8 / 16) — no merge;
+//   513..8192: every 512-token chunk sorted + run-length encoded by a warp,
+//     then one CTA per doc merges the <= 16 chunks' unique rows in shared
+//     memory (merge path) and sums equal ids;
 //   > 8192: bitonic sort in a global scratch region.
 
 #include <cmath>
@@ -52,69 +52,48 @@ __device__ __forceinline__ uint32_t next_pow2(uint32_t x) {
 }
 
 // ---------------------------------------------------------------------------
-// Register bitonic sort of P = 32*IPT*W keys; `t` is the thread's index in the
-// group (0..32W-1), so it holds keys [t*IPT, t*IPT+IPT). sm: P words (W > 1).
-template <int IPT, int W>
-__device__ __forceinline__ void bitonic_regs(uint32_t (&v)[IPT], uint32_t t, uint32_t* sm) {
-  constexpr int P = 32 * IPT * W;
-  constexpr int LANE_SPAN = 32 * IPT;  // keys held by one warp
-  const uint32_t lane = threadIdx.x & 31;
+// Register bitonic sort of P = 32*IPT keys held by one warp, IPT consecutive
+// keys per lane (blocked layout: lane holds [lane*IPT, lane*IPT+IPT)). Every
+// stage is a template instance, so all register indices are compile-time
+// constants (no local-memory arrays even at IPT = 32).
+template <int IPT, int K, int J>
+__device__ __forceinline__ void bitonic_stage(uint32_t (&v)[IPT], uint32_t lane) {
+  if constexpr (J >= IPT) {  // partner in lane ^ (J/IPT)
+    constexpr uint32_t lj = J / IPT;
+    const bool lower = (lane & lj) == 0;
+    const bool asc = ((lane * IPT) & K) == 0;
+    const bool take_min = lower == asc;
 #pragma unroll
-  for (int k = 2; k <= P; k <<= 1) {
-    if constexpr (W > 1) {
-      if (k > LANE_SPAN) {
-        // cross-warp stages j = k/2 .. LANE_SPAN in shared memory
-#pragma unroll
-        for (int q = 0; q < IPT; ++q) sm[t * IPT + q] = v[q];
-        __syncthreads();
-        for (int j = k >> 1; j >= LANE_SPAN; j >>= 1) {
-#pragma unroll
-          for (int p = 0; p < IPT / 2; ++p) {
-            const uint32_t idx = t * (IPT / 2) + p;  // compare-exchange pair index
-            const uint32_t i = ((idx & ~(j - 1)) << 1) | (idx & (j - 1));
-            const uint32_t l = i + j;
-            const uint32_t a = sm[i], b = sm[l];
-            const bool asc = (i & k) == 0;
-            if ((a > b) == asc) {
-              sm[i] = b;
-              sm[l] = a;
-            }
-          }
-          __syncthreads();
-        }
-#pragma unroll
-        for (int q = 0; q < IPT; ++q) v[q] = sm[t * IPT + q];
-        __syncthreads();
-      }
+    for (int q = 0; q < IPT; ++q) {
+      const uint32_t y = __shfl_xor_sync(0xffffffffu, v[q], lj);
+      v[q] = take_min ? min(v[q], y) : max(v[q], y);
     }
-    // cross-lane stages IPT <= j < 32*IPT (partner lane = lane ^ (j/IPT))
+  } else {  // partner in this lane's registers
 #pragma unroll
-    for (int j = ((k >> 1) < LANE_SPAN ? (k >> 1) : (LANE_SPAN >> 1)); j >= IPT; j >>= 1) {
-      const uint32_t lj = j / IPT;
-      const bool lower = (lane & lj) == 0;
-      const bool asc = ((t * IPT) & k) == 0;
-      const bool take_min = lower == asc;
-#pragma unroll
-      for (int q = 0; q < IPT; ++q) {
-        const uint32_t y = __shfl_xor_sync(0xffffffffu, v[q], lj);
-        v[q] = take_min ? min(v[q], y) : max(v[q], y);
-      }
-    }
-    // in-register stages j < IPT
-#pragma unroll
-    for (int j = ((k >> 1) < IPT ? (k >> 1) : (IPT >> 1)); j >= 1; j >>= 1) {
-#pragma unroll
-      for (int q = 0; q < IPT; ++q) {
-        if ((q & j) == 0) {
-          const int l = q | j;
-          const bool asc = ((t * IPT + q) & k) == 0;
-          const uint32_t lo = min(v[q], v[l]), hi = max(v[q], v[l]);
-          v[q] = asc ? lo : hi;
-          v[l] = asc ? hi : lo;
-        }
+    for (int q = 0; q < IPT; ++q) {
+      if ((q & J) == 0) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int l = q | J;
+        const bool asc = ((lane * IPT + q) & K) == 0;
+        const uint32_t lo = min(v[q], v[l]), hi = max(v[q], v[l]);
+        v[q] = asc ? lo : hi;
+        v[l] = asc ? hi : lo;
       }
     }
   }
+  if constexpr (J > 1) bitonic_stage<IPT, K, J / 2>(v, lane);
+}
+
+template <int IPT, int K>
+__device__ __forceinline__ void bitonic_level(uint32_t (&v)[IPT], uint32_t lane) {
+  bitonic_stage<IPT, K, K / 2>(v, lane);
+  if constexpr (K < 32 * IPT) bitonic_level<IPT, 2 * K>(v, lane);
+}
+
+template <int IPT>
+__device__ __forceinline__ void bitonic_regs(uint32_t (&v)[IPT], uint32_t lane) {
+  bitonic_level<IPT, 2>(v, lane);
 }
 
 // Warp inclusive scan / suffix min.
@@ -228,11 +207,12 @@ __global__ void __launch_bounds__(256) count_warp_kernel(CountArgs a, const uint
     uint32_t v[IPT];
 #pragma unroll
     for (int k = 0; k < IPT; ++k) v[k] = load_key(a, b, k * 32 + lane, len);  // coalesced; any order sorts
-    bitonic_regs<IPT, 1>(v, lane, nullptr);
+    bitonic_regs<IPT>(v, lane);
     const uint32_t n = rle_regs<IPT, 1>(v, lane, len, a.ent + b, a, nullptr);
     if (lane == 0) a.nnz[d] = n;
   }
 }
+
 
 template <int THREADS>
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* scratch, uint32_t* total) {
@@ -252,54 +232,58 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
   return wsum + inc - v;
 }
 
-// Chunk pass: one warp per 256-token chunk. chunks[q] = {doc, chunk<<1 | direct}.
-// A direct chunk is a whole document (65..256 tokens): its rows go straight to
-// ent/nnz/df. Otherwise the chunk's sorted unique (id,count) rows go to
-// scratch at the chunk's own token offset and chunk_cnt[q] = their number;
-// merge_kernel combines the chunks of a document.
-__global__ void __launch_bounds__(256) chunk_sort_kernel(CountArgs a, const uint2* __restrict__ chunks,
+// Chunk pass: one warp per chunk of up to 32*IPT tokens. chunks[q] = {doc,
+// m<<16 | lc<<1 | direct} (m chunks in the doc, this is chunk lc). A direct
+// chunk is a whole document: its rows go straight to ent/nnz/df. Otherwise
+// the chunk's sorted unique (id,count) rows go to scratch at the chunk's own
+// token offset and chunk_cnt[q] = their number.
+template <int IPT>
+__global__ void __launch_bounds__(256, IPT <= 8 ? 6 : 4) chunk_sort_kernel(CountArgs a, const uint2* __restrict__ chunks,
                                                          uint32_t n_chunks) {
+  constexpr uint32_t CS = 32 * IPT;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nw = gridDim.x * (blockDim.x >> 5);
   for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < n_chunks; q += nw) {
     const uint2 ch = chunks[q];
-    const uint32_t d = ch.x, c = ch.y >> 1;
+    const uint32_t d = ch.x, c = (ch.y >> 1) & 0x7FFFu;
     const uint64_t b = a.doc_off[d];
     const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
-    const uint64_t cb = b + static_cast<uint64_t>(c) * 256;
-    const uint32_t clen = min(256u, len - c * 256);
-    uint32_t v[8];
+    const uint64_t cb = b + static_cast<uint64_t>(c) * CS;
+    const uint32_t clen = min(CS, len - c * CS);
+    uint32_t v[IPT];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = load_key(a, cb, k * 32 + lane, clen);
-    bitonic_regs<8, 1>(v, lane, nullptr);
+    for (int k = 0; k < IPT; ++k) v[k] = load_key(a, cb, k * 32 + lane, clen);
+    bitonic_regs<IPT>(v, lane);
     if (ch.y & 1) {
-      const uint32_t n = rle_regs<8, 1, true>(v, lane, clen, a.ent + b, a, nullptr);
+      const uint32_t n = rle_regs<IPT, 1, true>(v, lane, clen, a.ent + b, a, nullptr);
       if (lane == 0) a.nnz[d] = n;
     } else {
-      const uint32_t n = rle_regs<8, 1, false>(v, lane, clen, a.scratch + cb, a, nullptr);
+      const uint32_t n = rle_regs<IPT, 1, false>(v, lane, clen, a.scratch + cb, a, nullptr);
       if (lane == 0) a.chunk_cnt[q] = n;
     }
   }
 }
 
-// Merge pass: one CTA (256 threads) per document of 257..CAP tokens.
-// docs[q] = {doc, first chunk, #chunks}. The chunks' sorted unique rows are
-// loaded into shared memory back to back and merged pairwise (merge path:
-// each thread co-ranks its output range by binary search, then merges
-// serially) until one list remains; equal ids (at most one per chunk,
-// adjacent after the merge) are combined by summing counts while the final
-// rows are written. Per-thread ranges have an odd length so that the threads
-// of a warp hit distinct shared-memory banks.
+// Merge pass: one CTA (256 threads) per document of kMergeChunk+1..CAP tokens
+// (mdocs[q] = first chunk index; chunks of kMergeChunk tokens). The chunks'
+// sorted unique rows are loaded into shared memory back to back and merged
+// pairwise (merge path: each thread co-ranks its output range by binary
+// search, then merges serially) until one list remains; equal ids (at most
+// one per chunk, adjacent after the merge) are combined by summing counts
+// while the final rows are written. Per-thread ranges have an odd length so
+// the threads of a warp hit distinct shared-memory banks.
 template <int CAP>
-__global__ void __launch_bounds__(256) merge_kernel(CountArgs a, const uint4* __restrict__ docs, uint32_t n_docs) {
+__global__ void __launch_bounds__(256) merge_kernel(CountArgs a, const uint2* __restrict__ chunks,
+                                                    const uint32_t* __restrict__ mdocs, uint32_t n_docs) {
   extern __shared__ uint2 mbuf[];  // 2*CAP rows
-  constexpr int MAXL = CAP / 256;  // <= 32 chunks
+  constexpr int MAXL = CAP / kMergeChunk;
   __shared__ uint32_t off[MAXL + 1];
   __shared__ uint32_t scan_scratch[8];
   const uint32_t tid = threadIdx.x;
   for (uint32_t q = blockIdx.x; q < n_docs; q += gridDim.x) {
-    const uint4 md = docs[q];
-    const uint32_t d = md.x, first = md.y, m = md.z;
+    const uint32_t first = mdocs[q];
+    const uint2 ch = chunks[first];
+    const uint32_t d = ch.x, m = ch.y >> 16;
     const uint64_t b = a.doc_off[d];
     if (tid < 32) {  // chunk offsets: warp scan of the chunk counts
       const uint32_t c = tid < m ? a.chunk_cnt[first + tid] : 0u;
@@ -314,7 +298,7 @@ __global__ void __launch_bounds__(256) merge_kernel(CountArgs a, const uint4* __
     for (uint32_t g = tid; g < M; g += 256) {  // all chunk loads in flight at once
       uint32_t c = 0;
       while (off[c + 1] <= g) ++c;
-      src[g] = a.scratch[b + static_cast<uint64_t>(c) * 256 + (g - off[c])];
+      src[g] = a.scratch[b + static_cast<uint64_t>(c) * kMergeChunk + (g - off[c])];
     }
     __syncthreads();
     const uint32_t E = ((M + 255) / 256) | 1u;
@@ -531,13 +515,17 @@ void launch_count_tiny(const CountArgs& a, const uint32_t* docs, uint32_t n, cud
   note_launch();
 }
 
-void launch_count_chunks(const CountArgs& a, const uint2* chunks, uint32_t n, cudaStream_t s) {
+void launch_count_chunks(int ipt, const CountArgs& a, const uint2* chunks, uint32_t n, cudaStream_t s) {
   if (n == 0) return;
-  chunk_sort_kernel<<<grid_for(ceil_div(n, 8), 8), 256, 0, s>>>(a, chunks, n);
+  if (ipt == 8)
+    chunk_sort_kernel<8><<<grid_for(ceil_div(n, 8), 6), 256, 0, s>>>(a, chunks, n);
+  else
+    chunk_sort_kernel<16><<<grid_for(ceil_div(n, 8), 4), 256, 0, s>>>(a, chunks, n);
   note_launch();
 }
 
-void launch_count_merge(int cls, const CountArgs& a, const uint4* docs, uint32_t n, cudaStream_t s) {
+void launch_count_merge(int cls, const CountArgs& a, const uint2* chunks, const uint32_t* mdocs, uint32_t n,
+                        cudaStream_t s) {
   if (n == 0) return;
   static bool configured = false;
   if (!configured) {
@@ -547,13 +535,16 @@ void launch_count_merge(int cls, const CountArgs& a, const uint4* docs, uint32_t
   }
   switch (cls) {
     case 0:
-      merge_kernel<1024><<<grid_for(n, 12), 256, 2 * 1024 * 8, s>>>(a, docs, n);
+      merge_kernel<1024><<<grid_for(n, 12), 256, 2 * 1024 * 8, s>>>(a, chunks, mdocs, n);
       break;
     case 1:
-      merge_kernel<4096><<<grid_for(n, 3), 256, 2 * 4096 * 8, s>>>(a, docs, n);
+      merge_kernel<2048><<<grid_for(n, 6), 256, 2 * 2048 * 8, s>>>(a, chunks, mdocs, n);
+      break;
+    case 2:
+      merge_kernel<4096><<<grid_for(n, 3), 256, 2 * 4096 * 8, s>>>(a, chunks, mdocs, n);
       break;
     default:
-      merge_kernel<8192><<<grid_for(n, 1), 256, 2 * 8192 * 8, s>>>(a, docs, n);
+      merge_kernel<8192><<<grid_for(n, 1), 256, 2 * 8192 * 8, s>>>(a, chunks, mdocs, n);
       break;
   }
   note_launch();

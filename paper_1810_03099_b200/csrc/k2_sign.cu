@@ -16,8 +16,9 @@
 // launch configuration. The norm is fused (warp-shuffle tree) and the unit
 // signature for the compare kernel is written in the same pass.
 //
-// Algorithmic bytes per signature: 8*nnz_d (CSR rows) + 8*K (S and Sn rows)
-// + 4 (inv_norm); TermInfo/R gathers are L2 traffic.
+// Algorithmic bytes per signature: 8*nnz_d (CSR rows) + 4*K (S row) + 4
+// (inv_norm); the transposed unit copy for K3, TermInfo and R gathers are
+// L2 traffic. R rows are padded to Kp = roundup(K,4) floats.
 
 #include "kernels.cuh"
 
@@ -78,89 +79,111 @@ __global__ void __launch_bounds__(256) ref_fill_kernel(RefArgs r, const TermInfo
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
       uint2 x = e[i];
       float w = r.explicit_w ? __uint_as_float(x.y) : static_cast<float>(x.y) * info[x.x].idf;
-      R[static_cast<size_t>(info[x.x].ref_row) * r.K + k] = w * inv;
+      R[static_cast<size_t>(info[x.x].ref_row) * r.Kp + k] = w * inv;
     }
     __syncthreads();
   }
 }
 
-// KPL = reference columns per lane per pass (K chunk = 32*KPL).
-template <int KPL>
+// Warp per document, documents in longest-first order (a.order) so the
+// longest ones do not form the tail. Per 32-column slab of the signature:
+//   1. lanes stream the doc's (id,count) rows 32 at a time (coalesced, next
+//      chunk prefetched), gather TermInfo, accumulate ||w||^2, and append the
+//      rows that hit the reference union to a per-warp hit queue in shared
+//      memory (ballot + prefix popcount);
+//   2. every 32 queued hits, each lane takes one hit and adds w*R[row][k0..]
+//      for the slab's columns into its own 32 accumulators (float4 gathers of
+//      the L2-resident table), so all lanes do useful work;
+//   3. the 32x32 partial sums are transposed through shared memory and lane k
+//      sums column k over the lanes in a fixed order (deterministic).
+constexpr int kSignWarps = 8;
+
 __global__ void __launch_bounds__(256) sign_kernel(SignArgs a) {
-  const uint32_t lane = threadIdx.x & 31;
+  __shared__ float part[kSignWarps][32][33];
+  __shared__ int2 queue[kSignWarps][64];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-  const uint32_t K = a.K;
-  for (uint32_t d = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); d < a.n_docs; d += nwarps) {
+  const uint32_t K = a.K, Kp = a.Kp;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + wid; q < a.n_docs; q += nwarps) {
+    const uint32_t d = a.order[q];
     const uint2* __restrict__ e = a.ent + a.doc_off[d];
     const uint32_t n = a.nnz[d];
     float inv = 0.0f;
-    float ss = 0.0f;  // sum of squared (clamped) signature values, per lane
-    for (uint32_t k0 = 0; k0 < K; k0 += 32 * KPL) {
-      float acc[KPL];
+    float ss = 0.0f;  // lane k: squared signature values of its columns
+    for (uint32_t k0 = 0; k0 < K; k0 += 32) {
+      const uint32_t kc = min(32u, K - k0);
+      float acc[32];
 #pragma unroll
-      for (int q = 0; q < KPL; ++q) acc[q] = 0.0f;
+      for (int k = 0; k < 32; ++k) acc[k] = 0.0f;
       float sq = 0.0f;
-      // software pipeline: the next chunk's rows are in flight while the
-      // current chunk's hits are gathered
-      uint2 xn = lane < n ? __ldg(e + lane) : make_uint2(0u, 0u);
-      for (uint32_t c = 0; c < n; c += 32) {
-        const uint32_t i = c + lane;
-        const uint2 x = xn;
-        if (i + 32 < n) xn = __ldg(e + i + 32);
-        float w = 0.0f;
-        int32_t row = -1;
-        if (i < n) {
-          const TermInfo ti = a.info[x.x];
-          w = static_cast<float>(x.y) * ti.idf;
-          row = ti.ref_row;
-        }
-        sq = fmaf(w, w, sq);
-        uint32_t hits = __ballot_sync(0xffffffffu, row >= 0);
-        // hits in ascending term order, 8 reference rows in flight per batch;
-        // FMAs stay in hit order, so every column sums in the same order.
-        while (hits) {
-          constexpr int B = 8;
-          int32_t rr[B];
-          float ww[B];
+      uint32_t qn = 0;  // queued hits (warp-uniform)
+      auto drain = [&](uint32_t cnt) {
+        if (lane < cnt) {
+          const int2 h = queue[wid][lane];
+          const float w = __int_as_float(h.y);
+          const float4* __restrict__ R4 = reinterpret_cast<const float4*>(a.R + static_cast<size_t>(h.x) * Kp + k0);
 #pragma unroll
-          for (int u = 0; u < B; ++u) {
-            const int src = hits ? __ffs(hits) - 1 : 0;
-            const bool ok = hits != 0;
-            hits &= hits - 1;
-            rr[u] = __shfl_sync(0xffffffffu, row, src);
-            ww[u] = __shfl_sync(0xffffffffu, w, src);
-            if (!ok) rr[u] = -1;
-          }
-          float val[B][KPL];
-#pragma unroll
-          for (int u = 0; u < B; ++u) {
-            const float* __restrict__ Rr = a.R + static_cast<size_t>(rr[u] < 0 ? 0 : rr[u]) * K + k0;
-#pragma unroll
-            for (int q = 0; q < KPL; ++q) {
-              const uint32_t k = lane + 32 * q;
-              val[u][q] = (rr[u] >= 0 && k0 + k < K) ? __ldg(Rr + k) : 0.0f;
+          for (int j = 0; j < 8; ++j) {
+            if (4 * j < static_cast<int>(kc)) {
+              const float4 r = __ldg(R4 + j);
+              acc[4 * j + 0] = fmaf(w, r.x, acc[4 * j + 0]);
+              acc[4 * j + 1] = fmaf(w, r.y, acc[4 * j + 1]);
+              acc[4 * j + 2] = fmaf(w, r.z, acc[4 * j + 2]);
+              acc[4 * j + 3] = fmaf(w, r.w, acc[4 * j + 3]);
             }
           }
+        }
+      };
+      // U chunks of 32 rows per step: U coalesced loads, then U TermInfo
+      // gathers in flight together (memory-level parallelism per warp)
+      constexpr int U = 4;
+      for (uint32_t c = 0; c < n; c += 32 * U) {
+        uint2 x[U];
 #pragma unroll
-          for (int u = 0; u < B; ++u)
+        for (int u = 0; u < U; ++u) {
+          const uint32_t i = c + 32 * u + lane;
+          x[u] = i < n ? __ldg(e + i) : make_uint2(0u, 0u);
+        }
+        TermInfo ti[U];
 #pragma unroll
-            for (int q = 0; q < KPL; ++q)
-              if (rr[u] >= 0) acc[q] = fmaf(ww[u], val[u][q], acc[q]);
+        for (int u = 0; u < U; ++u) ti[u] = (c + 32 * u + lane < n) ? a.info[x[u].x] : TermInfo{0.0f, -1};
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float w = static_cast<float>(x[u].y) * ti[u].idf;
+          const int32_t row = ti[u].ref_row;
+          sq = fmaf(w, w, sq);
+          const uint32_t hits = __ballot_sync(0xffffffffu, row >= 0);
+          if (row >= 0) queue[wid][qn + __popc(hits & lt)] = make_int2(row, __float_as_int(w));
+          qn += __popc(hits);
+          __syncwarp();
+          if (qn >= 32) {
+            drain(32);
+            __syncwarp();
+            if (lane < qn - 32) queue[wid][lane] = queue[wid][32 + lane];
+            qn -= 32;
+            __syncwarp();
+          }
         }
       }
+      drain(qn);
       if (k0 == 0) {
         sq = warp_sum(sq);
         inv = sq > 0.0f ? 1.0f / sqrtf(sq) : 0.0f;
         if (lane == 0) a.inv_norm[d] = inv;
       }
+      // transpose-reduce: lane k sums column k over the 32 lanes
 #pragma unroll
-      for (int q = 0; q < KPL; ++q) {
-        const uint32_t k = k0 + lane + 32 * q;
-        if (k < K) {
-          const float s = fminf(acc[q] * inv, 1.0f);  // ngram.hpp:201 clamp
-          a.S[static_cast<size_t>(d) * K + k] = s;
-          ss = fmaf(s, s, ss);
-        }
+      for (int k = 0; k < 32; ++k) part[wid][lane][k] = acc[k];
+      __syncwarp();
+      float sum = 0.0f;
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) sum += part[wid][l][lane];
+      __syncwarp();
+      if (lane < kc) {
+        const float s = fminf(sum * inv, 1.0f);  // ngram.hpp:201 clamp
+        a.S[static_cast<size_t>(d) * K + k0 + lane] = s;
+        ss = fmaf(s, s, ss);
       }
     }
     ss = warp_sum(ss);
@@ -198,16 +221,10 @@ void launch_ref_fill(const RefArgs& r, const TermInfo* info, float* R, cudaStrea
 
 void launch_sign(const SignArgs& a, cudaStream_t s) {
   if (a.n_docs == 0) return;
-  const uint32_t warps_per_block = 8;
-  uint64_t blocks = ceil_div(a.n_docs, warps_per_block);
-  const uint64_t cap = static_cast<uint64_t>(sm_count()) * 8;  // 64 warps/SM resident
+  uint64_t blocks = ceil_div(a.n_docs, kSignWarps);
+  const uint64_t cap = static_cast<uint64_t>(sm_count()) * 4;
   if (blocks > cap) blocks = cap;
-  if (a.K <= 32)
-    sign_kernel<1><<<static_cast<unsigned>(blocks), 256, 0, s>>>(a);
-  else if (a.K <= 64)
-    sign_kernel<2><<<static_cast<unsigned>(blocks), 256, 0, s>>>(a);
-  else
-    sign_kernel<4><<<static_cast<unsigned>(blocks), 256, 0, s>>>(a);
+  sign_kernel<<<static_cast<unsigned>(blocks), 32 * kSignWarps, 0, s>>>(a);
   note_launch();
 }
 

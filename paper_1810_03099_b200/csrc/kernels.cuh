@@ -15,12 +15,15 @@
 namespace refsig_gpu {
 
 // ---- K1 -------------------------------------------------------------------
-// Count work plan (k1_count.cu): tiny docs (<= kTinyMax), 256-token chunks,
-// per-doc chunk merges in three shared-memory size classes, and long docs
-// (> kMergeMax) sorted in a global scratch region.
+// Count work plan (k1_count.cu): tiny docs (<= kTinyMax) and whole docs up
+// to 512 tokens are sorted by one warp each; longer docs are cut into
+// kMergeChunk-token chunks and merged per doc in four shared-memory size
+// classes (<= 1024 / 2048 / 4096 / 8192 tokens); longer than kMergeMax are
+// sorted in a global scratch region.
 constexpr uint32_t kTinyMax = 64;
-constexpr uint32_t kChunk = 256;
-constexpr uint32_t kMergeCap[3] = {1024, 4096, 8192};
+constexpr uint32_t kMergeChunk = 512;
+constexpr int kMergeClasses = 4;
+constexpr uint32_t kMergeCap[kMergeClasses] = {1024, 2048, 4096, 8192};
 constexpr uint32_t kMergeMax = 8192;
 
 struct CountArgs {
@@ -37,8 +40,11 @@ struct CountArgs {
 };
 
 void launch_count_tiny(const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s);
-void launch_count_chunks(const CountArgs& a, const uint2* chunks, uint32_t n, cudaStream_t s);
-void launch_count_merge(int cls, const CountArgs& a, const uint4* docs, uint32_t n, cudaStream_t s);
+// chunks[q] = {doc, m<<16 | lc<<1 | direct}, chunks of 32*ipt tokens (ipt 8/16).
+void launch_count_chunks(int ipt, const CountArgs& a, const uint2* chunks, uint32_t n, cudaStream_t s);
+// mdocs[q] = first chunk index (in the ipt-16 chunk list) of a doc of class cls.
+void launch_count_merge(int cls, const CountArgs& a, const uint2* chunks, const uint32_t* mdocs, uint32_t n,
+                        cudaStream_t s);
 void launch_count_large(const CountArgs& a, const uint32_t* long_docs, const uint64_t* scratch_off,
                         uint32_t n_long, uint32_t* scratch, cudaStream_t s);
 // df[t] = sum of the replicas; idf32[t] = fl32(ln((1+N)/(1+df))+1) (or 1 for
@@ -67,6 +73,7 @@ struct RefArgs {
   const uint32_t* n;
   const uint2* ent;
   bool explicit_w;
+  uint32_t Kp;  // row stride of R (K rounded up to 4)
 };
 // start/n of K reference docs taken from the padded CSR.
 void launch_ref_doc_ranges(const uint64_t* doc_off, const uint32_t* nnz, const uint32_t* ref_docs, uint32_t K,
@@ -75,7 +82,7 @@ void launch_ref_doc_ranges(const uint64_t* doc_off, const uint32_t* nnz, const u
 void launch_ref_mark(const RefArgs& r, uint32_t* flags, cudaStream_t s);
 // info[t].ref_row = flags[t] ? prefix[t] : -1
 void launch_ref_remap(const uint32_t* flags, const uint64_t* prefix, uint32_t vocab, TermInfo* info, cudaStream_t s);
-// R[row*K + k] = w_k[t]/||w_k|| (R zeroed by the caller).
+// R[row*Kp + k] = w_k[t]/||w_k|| (R zeroed by the caller).
 void launch_ref_fill(const RefArgs& r, const TermInfo* info, float* R, cudaStream_t s);
 
 // ---- K2 sign ----------------------------------------------------------------
@@ -87,6 +94,8 @@ struct SignArgs {
   const float* R;
   uint32_t n_docs;
   uint32_t K;
+  uint32_t Kp;           // row stride of R
+  const uint32_t* order; // docs in longest-first order (load balance)
   float* S;         // [n_docs*K] raw cosines, row-major (API output)
   float* ST;        // [K][ld] unit-normalised signatures, transposed (K3 operand; 0 if all-zero)
   uint32_t ld;      // leading dimension of ST (n_docs rounded up to 128; pad columns zero)
