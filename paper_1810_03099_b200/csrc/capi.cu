@@ -106,7 +106,8 @@ struct refsig_gpu_ctx {
   // reference
   bool have_ref = false;
   uint32_t K = 0, Kp = 0;  // Kp: row stride of R
-  DevBuf ref_docs, ref_start, ref_n, ref_ent, ref_mark, ref_prefix, R;
+  DevBuf ref_docs, ref_start, ref_n, ref_ent, ref_count, R;
+  bool ref_dirty = false;  // info[].ref_row holds a previous reference's rows
 
   // sign
   bool signed_ = false;
@@ -307,24 +308,22 @@ void prepare_bitmap(refsig_gpu_ctx* c, const PairGrid& g, bool zero) {
 // A5: union, remap and the compact table from c->ref_{start,n} and `ent`.
 void build_reference(refsig_gpu_ctx* c, const RefArgs& r, uint64_t u_cap) {
   const uint32_t V = c->vocab;
-  c->ref_mark.ensure(sizeof(uint32_t) * V);
-  c->ref_prefix.ensure(sizeof(uint64_t) * (V + 1));
-  c->scan_tmp.ensure(scan_tmp_bytes(V));
   if (u_cap > V) u_cap = V;
   const size_t rbytes = sizeof(float) * std::max<uint64_t>(u_cap, 1) * r.Kp;
   c->R.ensure(rbytes);
+  c->ref_count.ensure(sizeof(uint32_t));
   Phase ph(c, REFSIG_PHASE_REFERENCE);
-  ck(cudaMemsetAsync(c->ref_mark.p, 0, sizeof(uint32_t) * V, c->stream), "memset");
-  launch_ref_mark(r, c->ref_mark.as<uint32_t>(), c->stream);
-  launch_exclusive_scan_u32_to_u64(c->ref_mark.as<uint32_t>(), c->ref_prefix.as<uint64_t>(), V, c->scan_tmp.p,
-                                   c->stream);
-  launch_ref_remap(c->ref_mark.as<uint32_t>(), c->ref_prefix.as<uint64_t>(), V, c->info.as<TermInfo>(), c->stream);
+  // info[].ref_row is -1 right after count(); a replaced reference resets it
+  if (c->ref_dirty) launch_ref_reset(c->info.as<TermInfo>(), V, c->stream);
+  ck(cudaMemsetAsync(c->ref_count.p, 0, sizeof(uint32_t), c->stream), "memset");
+  launch_ref_claim(r, c->info.as<TermInfo>(), c->ref_count.as<uint32_t>(), c->stream);
   ck(cudaMemsetAsync(c->R.p, 0, rbytes, c->stream), "memset R");
   launch_ref_fill(r, c->info.as<TermInfo>(), c->R.as<float>(), c->stream);
   launched("reference");
   c->K = r.K;
   c->Kp = r.Kp;
   c->have_ref = true;
+  c->ref_dirty = true;
   c->signed_ = false;
 }
 
@@ -570,6 +569,7 @@ int refsig_gpu_count(refsig_gpu_ctx* ctx, int weight_mode) {
     }
     launch_idf(ctx->df_rep.as<uint32_t>(), reps, V, N, weight_mode, ctx->df.as<uint32_t>(), ctx->info.as<TermInfo>(),
                ctx->stream);
+    ctx->ref_dirty = false;  // idf_kernel resets info[].ref_row
     ctx->weight_mode = weight_mode;
     if (db) {
       // Query mode: the database's IDF and reference rows (configs[4]); the
@@ -668,12 +668,9 @@ int refsig_gpu_set_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_i
       u_cap += ctx->h_off[ref_doc_ids[k] + 1] - ctx->h_off[ref_doc_ids[k]];
     }
     ctx->ref_docs.ensure(4ull * K);
-    ctx->ref_start.ensure(8ull * K);
-    ctx->ref_n.ensure(4ull * K);
     upload(ctx, ctx->ref_docs.p, ref_doc_ids, 4ull * K);
-    launch_ref_doc_ranges(ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->ref_docs.as<uint32_t>(), K,
-                          ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->stream);
-    RefArgs r{K, ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->ent.as<uint2>(), false, (K + 3) & ~3u};
+    RefArgs r{K,     nullptr, nullptr, ctx->ent.as<uint2>(), false, (K + 3) & ~3u, ctx->ref_docs.as<uint32_t>(),
+              ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>()};
     build_reference(ctx, r, u_cap);
   });
 }
@@ -716,7 +713,7 @@ int refsig_gpu_set_reference_vectors(refsig_gpu_ctx* ctx, uint32_t K, const uint
     ck(cudaMemcpyAsync(ctx->ref_start.p, start.data(), 8ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D");
     ck(cudaMemcpyAsync(ctx->ref_n.p, cnt.data(), 4ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D");
     RefArgs r{K, ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->ref_ent.as<uint2>(), true,
-              (K + 3) & ~3u};
+              (K + 3) & ~3u, nullptr, nullptr, nullptr};
     build_reference(ctx, r, n);
     ck(cudaStreamSynchronize(ctx->stream), "reference");
   });
@@ -726,11 +723,9 @@ int refsig_gpu_reference_union(refsig_gpu_ctx* ctx, uint32_t* out_u) {
   return guard(ctx, [&] {
     require(ctx->have_ref, "no reference set");
     require(out_u != nullptr, "NULL output");
-    ck(cudaMemcpyAsync(ctx->h_pin, ctx->ref_prefix.as<uint64_t>() + ctx->vocab, 8, cudaMemcpyDeviceToHost,
-                       ctx->stream),
-       "D2H");
+    ck(cudaMemcpyAsync(ctx->h_pin, ctx->ref_count.p, 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
     sync(ctx);
-    *out_u = static_cast<uint32_t>(ctx->h_pin[0]);
+    *out_u = static_cast<uint32_t>(ctx->h_pin[0] & 0xffffffffu);
   });
 }
 

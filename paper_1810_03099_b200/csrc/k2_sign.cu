@@ -32,28 +32,32 @@ int sm_count() {
   return sms;
 }
 
-__global__ void ref_doc_ranges_kernel(const uint64_t* __restrict__ doc_off, const uint32_t* __restrict__ nnz,
-                                      const uint32_t* __restrict__ ref_docs, uint32_t K, uint64_t* start,
-                                      uint32_t* n) {
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
-    uint32_t d = ref_docs[k];
-    start[k] = doc_off[d];
-    n[k] = nnz[d];
+__device__ __forceinline__ void ref_range(const RefArgs& r, uint32_t k, const uint2*& e, uint32_t& n) {
+  if (r.docs) {
+    const uint32_t d = r.docs[k];
+    e = r.ent + r.doc_off[d];
+    n = r.nnz[d];
+  } else {
+    e = r.ent + r.start[k];
+    n = r.n[k];
   }
 }
 
-__global__ void ref_mark_kernel(RefArgs r, uint32_t* __restrict__ flags) {
-  for (uint32_t k = blockIdx.x; k < r.K; k += gridDim.x) {
-    const uint2* e = r.ent + r.start[k];
-    const uint32_t n = r.n[k];
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) flags[e[i].x] = 1u;
-  }
-}
-
-__global__ void ref_remap_kernel(const uint32_t* __restrict__ flags, const uint64_t* __restrict__ prefix,
-                                 uint32_t vocab, TermInfo* __restrict__ info) {
+__global__ void ref_reset_kernel(TermInfo* __restrict__ info, uint32_t vocab) {
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < vocab; t += gridDim.x * blockDim.x)
-    info[t].ref_row = flags[t] ? static_cast<int32_t>(prefix[t]) : -1;
+    info[t].ref_row = -1;
+}
+
+__global__ void ref_claim_kernel(RefArgs r, TermInfo* __restrict__ info, uint32_t* __restrict__ counter) {
+  for (uint32_t k = blockIdx.x; k < r.K; k += gridDim.x) {
+    const uint2* e;
+    uint32_t n;
+    ref_range(r, k, e, n);
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      int* slot = &info[e[i].x].ref_row;
+      if (atomicCAS(slot, -1, -2) == -1) *slot = static_cast<int>(atomicAdd(counter, 1u));
+    }
+  }
 }
 
 // One CTA per reference vector: block-tree norm, then scatter unit weights.
@@ -61,8 +65,9 @@ __global__ void __launch_bounds__(256) ref_fill_kernel(RefArgs r, const TermInfo
                                                        float* __restrict__ R) {
   __shared__ float red[8];
   for (uint32_t k = blockIdx.x; k < r.K; k += gridDim.x) {
-    const uint2* e = r.ent + r.start[k];
-    const uint32_t n = r.n[k];
+    const uint2* e;
+    uint32_t n;
+    ref_range(r, k, e, n);
     float sq = 0.0f;
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
       uint2 x = e[i];
@@ -195,22 +200,15 @@ __global__ void __launch_bounds__(256) sign_kernel(SignArgs a) {
 
 }  // namespace
 
-void launch_ref_doc_ranges(const uint64_t* doc_off, const uint32_t* nnz, const uint32_t* ref_docs, uint32_t K,
-                           uint64_t* start, uint32_t* n, cudaStream_t s) {
-  ref_doc_ranges_kernel<<<(K + 127) / 128, 128, 0, s>>>(doc_off, nnz, ref_docs, K, start, n);
-  note_launch();
-}
-
-void launch_ref_mark(const RefArgs& r, uint32_t* flags, cudaStream_t s) {
-  ref_mark_kernel<<<r.K < 1024 ? r.K : 1024, 256, 0, s>>>(r, flags);
-  note_launch();
-}
-
-void launch_ref_remap(const uint32_t* flags, const uint64_t* prefix, uint32_t vocab, TermInfo* info,
-                      cudaStream_t s) {
+void launch_ref_reset(TermInfo* info, uint32_t vocab, cudaStream_t s) {
   uint32_t g = (vocab + 255) / 256;
   if (g > 4096) g = 4096;
-  ref_remap_kernel<<<g, 256, 0, s>>>(flags, prefix, vocab, info);
+  ref_reset_kernel<<<g, 256, 0, s>>>(info, vocab);
+  note_launch();
+}
+
+void launch_ref_claim(const RefArgs& r, TermInfo* info, uint32_t* counter, cudaStream_t s) {
+  ref_claim_kernel<<<r.K < 1024 ? r.K : 1024, 256, 0, s>>>(r, info, counter);
   note_launch();
 }
 

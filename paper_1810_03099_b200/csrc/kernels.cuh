@@ -64,9 +64,11 @@ size_t scan_tmp_bytes(uint64_t n);
 void launch_exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp, cudaStream_t s);
 
 // ---- A5 reference table ----------------------------------------------------
-// K reference vectors, vector k = ent[start[k] .. start[k]+n[k]) with unique
-// ids. Docs mode: ent.y is a count (w = count*idf). Explicit mode: ent.y holds
-// the float bits of the raw weight (partition vectors use 1.0).
+// K reference vectors. Docs mode (docs != NULL): vector k is corpus doc
+// docs[k], rows ent[doc_off[d] ..+nnz[d]) with ent.y a count (w = count*idf).
+// Explicit mode: vector k = ent[start[k] ..+n[k]) with ent.y the float bits of
+// the raw weight (partition vectors use 1.0). Ids are unique
+// within a vector.
 struct RefArgs {
   uint32_t K;
   const uint64_t* start;
@@ -74,14 +76,16 @@ struct RefArgs {
   const uint2* ent;
   bool explicit_w;
   uint32_t Kp;  // row stride of R (K rounded up to 4)
+  const uint32_t* docs;
+  const uint64_t* doc_off;
+  const uint32_t* nnz;
 };
-// start/n of K reference docs taken from the padded CSR.
-void launch_ref_doc_ranges(const uint64_t* doc_off, const uint32_t* nnz, const uint32_t* ref_docs, uint32_t K,
-                           uint64_t* start, uint32_t* n, cudaStream_t s);
-// flags[t] = 1 for every t in the union U (flags zeroed by the caller).
-void launch_ref_mark(const RefArgs& r, uint32_t* flags, cudaStream_t s);
-// info[t].ref_row = flags[t] ? prefix[t] : -1
-void launch_ref_remap(const uint32_t* flags, const uint64_t* prefix, uint32_t vocab, TermInfo* info, cudaStream_t s);
+// info[t].ref_row = -1 for all t (only needed when a reference is replaced).
+void launch_ref_reset(TermInfo* info, uint32_t vocab, cudaStream_t s);
+// Assign compact rows to the union U: first claimant of a term takes the next
+// row from *counter (row numbering is scheduling-dependent; the values the
+// sign kernel reads through it are not).
+void launch_ref_claim(const RefArgs& r, TermInfo* info, uint32_t* counter, cudaStream_t s);
 // R[row*Kp + k] = w_k[t]/||w_k|| (R zeroed by the caller).
 void launch_ref_fill(const RefArgs& r, const TermInfo* info, float* R, cudaStream_t s);
 

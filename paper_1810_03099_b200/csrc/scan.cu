@@ -94,6 +94,28 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t
   if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = partial[nb];
 }
 
+// n <= kSmallScan: one CTA, each thread scans a contiguous run of <= 32 values.
+constexpr uint64_t kSmallScan = kScanThreads * 32;
+
+__global__ void __launch_bounds__(kScanThreads) scan_small_kernel(const uint32_t* __restrict__ in, uint64_t n,
+                                                                  uint64_t* __restrict__ out) {
+  __shared__ uint64_t sh[33];
+  const uint32_t per = static_cast<uint32_t>((n + kScanThreads - 1) / kScanThreads);
+  const uint64_t lo = static_cast<uint64_t>(threadIdx.x) * per;
+  uint64_t s = 0;
+  for (uint32_t k = 0; k < per; ++k)
+    if (lo + k < n) s += in[lo + k];
+  uint64_t tot;
+  uint64_t off = block_exscan_u64(s, sh, &tot);
+  for (uint32_t k = 0; k < per; ++k)
+    if (lo + k < n) {
+      const uint64_t v = in[lo + k];
+      out[lo + k] = off;
+      off += v;
+    }
+  if (threadIdx.x == 0) out[n] = tot;
+}
+
 }  // namespace
 
 size_t scan_tmp_bytes(uint64_t n) { return sizeof(uint64_t) * (ceil_div(n, kScanBlock) + 2); }
@@ -102,6 +124,11 @@ void launch_exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_
   uint64_t nb = ceil_div(n, kScanBlock);
   if (nb == 0) {
     cudaMemsetAsync(out, 0, sizeof(uint64_t), s);
+    return;
+  }
+  if (n <= kSmallScan) {
+    scan_small_kernel<<<1, kScanThreads, 0, s>>>(in, n, out);
+    note_launch();
     return;
   }
   uint64_t* partial = static_cast<uint64_t*>(tmp);

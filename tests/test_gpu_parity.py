@@ -347,3 +347,29 @@ def test_query_vs_database(gpu_ctx_factory):
     hk = qc.hamming_query_pairs(3)
     assert np.array_equal(hk, oracle.hamming_query_pairs(oracle.simhash(cq, od.idf, 0), fd, 3))
     assert np.array_equal(fq, oracle.simhash(cq, od.idf, 0))
+
+
+def test_reference_replaced_and_union(gpu_ctx_factory):
+    # a second reference on the same counts must not see the first one's rows
+    cp, cfg = corpus_c0(800)
+    ctx = gpu_ctx_factory()
+    ctx.load_corpus(cp.tokens, cp.doc_off, cp.vocab)
+    ctx.count()
+    r1 = C.sample_refs(1, cp.n_docs, 10)
+    r2 = C.sample_refs(2, cp.n_docs, 7)
+    ctx.set_reference_docs(r1)
+    ctx.sign(fetch=False)
+    ctx.set_reference_docs(r2)
+    S2 = ctx.sign()
+    o = oracle_pipeline(cp, r2)
+    assert_sig_close(S2, o.S)
+    c = o.counts
+    union = set()
+    for d in r2:
+        union.update(c.ids[c.rowptr[d]:c.rowptr[d + 1]].tolist())
+    assert ctx.reference_union() == len(union)
+    # explicit vectors after doc references
+    ctx.set_reference_partitions([[1, 2, 3], [4, 5]])
+    S3 = ctx.sign()
+    ref = oracle.vectors([0, 3, 5], [1, 2, 3, 4, 5], np.ones(5))
+    assert_sig_close(S3, oracle.sign(o.x, ref))
