@@ -109,7 +109,6 @@ __global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel(MrcArgs a) {
   const uint32_t kc_max = a.K < kKC ? a.K : kKC;
   const uint32_t panel = kc_max * kTile;  // floats per panel stage
   // stage st: A panel at smem + 2*st*panel, B panel right after it
-  uint8_t* rowbytes = reinterpret_cast<uint8_t*>(smem + 4 * panel);  // [128][16]
 
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
@@ -124,18 +123,24 @@ __global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel(MrcArgs a) {
   // issue the loads of item `it` (tile t_begin + it / nchunks, chunk it % nchunks) into stage st
   uint32_t li = bi, lj = bj;  // tile coords of the next item to load
   uint32_t lchunk = 0;
+  // cp.async slots of one stage: 16-byte chunk m = tid%32 of panel rows
+  // tid/32 + 8u (A rows first, then B rows); offsets are tile-invariant.
+  constexpr int kSlots = 2 * kKC / 8;
+  const uint32_t cm = tid & 31, kr = tid >> 5, sp = split_pos(4 * cm);
   auto issue = [&](int st) {
     const uint32_t k0 = lchunk * kKC;
     const uint32_t kc = min(static_cast<uint32_t>(kKC), a.K - k0);
-    const uint32_t n16 = kc * (kTile / 4);  // 16-byte chunks per panel
-    for (uint32_t idx = tid; idx < 2 * n16; idx += 256) {
-      const bool isB = idx >= n16;
-      const uint32_t id = isB ? idx - n16 : idx;
-      const uint32_t k = id >> 5, m = id & 31;  // row k, 16-byte chunk m (cols 4m..4m+3)
-      const float* src = isB ? a.STc + static_cast<size_t>(k0 + k) * a.ldc + lj * kTile + 4 * m
-                             : a.STr + static_cast<size_t>(k0 + k) * a.ldr + li * kTile + 4 * m;
-      float* dst = smem + (2 * st + (isB ? 1 : 0)) * panel + k * kTile + split_pos(4 * m);
-      cp_async16(dst, src);
+    const float* baseA = a.STr + static_cast<size_t>(k0) * a.ldr + li * kTile + 4 * cm;
+    const float* baseB = a.STc + static_cast<size_t>(k0) * a.ldc + lj * kTile + 4 * cm;
+    float* sbase = smem + 2 * st * panel + sp;
+#pragma unroll
+    for (int u = 0; u < kSlots; ++u) {
+      const uint32_t k = kr + 8 * u;
+      const bool isB = k >= kc_max;
+      const uint32_t kk = isB ? k - kc_max : k;
+      if (k < 2 * kc_max && kk < kc)
+        cp_async16(sbase + (isB ? panel : 0u) + kk * kTile,
+                   isB ? baseB + static_cast<size_t>(kk) * a.ldc : baseA + static_cast<size_t>(kk) * a.ldr);
     }
     cp_async_commit();
     if (++lchunk == nchunks) {
@@ -148,22 +153,51 @@ __global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel(MrcArgs a) {
   };
 
   float2 acc[8][4];
-  issue(0);
-  for (uint64_t it = 0; it < items; ++it) {
-    const int st = static_cast<int>(it & 1);
-    const uint32_t chunk = static_cast<uint32_t>(it % nchunks);
-    if (it + 1 < items) {
-      issue(st ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+  // Tile bits are staged per row in shared memory (double-buffered) and the
+  // 128-thread store of tile t happens after the next item's barrier, so the
+  // epilogue needs no barrier of its own.
+  uint8_t* rowbytes = reinterpret_cast<uint8_t*>(smem + 6 * panel);  // [2][128][16]
+  uint32_t pend_bi = 0, pend_bj = 0, pend_buf = 0;
+  bool pending = false;
+  auto flush = [&]() {
+    if (tid < kTile) {
+      const uint32_t i = pend_bi * kTile + tid;
+      if (i < a.g.n_rows) {
+        uint4 wv = *reinterpret_cast<const uint4*>(rowbytes + pend_buf * 2048 + tid * 16);
+        const uint32_t c0 = pend_bj * kTile;
+        wv.x &= col_mask(c0, i, a.g);
+        wv.y &= col_mask(c0 + 32, i, a.g);
+        wv.z &= col_mask(c0 + 64, i, a.g);
+        wv.w &= col_mask(c0 + 96, i, a.g);
+        *reinterpret_cast<uint4*>(a.bitmap + static_cast<size_t>(i) * a.g.words_per_row + pend_bj * 4) = wv;
+        const uint32_t cnt = __popc(wv.x) + __popc(wv.y) + __popc(wv.z) + __popc(wv.w);
+        if (cnt) atomicAdd(a.rowcnt + i, cnt);
+      }
     }
+  };
+  // 3-stage ring: the data of item it+2 streams in while item it computes;
+  // one barrier per item (it also frees the stage item it-1 used).
+  issue(0);
+  if (items > 1) issue(1);
+  uint32_t tiles_done = 0;
+  for (uint64_t it = 0; it < items; ++it) {
+    const int st = static_cast<int>(it % 3);
+    const uint32_t chunk = static_cast<uint32_t>(it % nchunks);
+    if (it + 1 < items)
+      cp_async_wait<1>();
+    else
+      cp_async_wait<0>();
     __syncthreads();
-    if (chunk == 0) {
+    if (it + 2 < items) issue(static_cast<int>((it + 2) % 3));
+    if (pending) {
+      flush();
+      pending = false;
+    }
+    if (chunk == 0) {  // accumulate dot - tau: the match bit is the inverted sign bit
 #pragma unroll
       for (int r = 0; r < 8; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = make_float2(0.0f, 0.0f);
+        for (int c = 0; c < 4; ++c) acc[r][c] = make_float2(-a.tau, -a.tau);
     }
     const uint32_t kc = min(static_cast<uint32_t>(kKC), a.K - chunk * kKC);
     const float* A = smem + 2 * st * panel;
@@ -182,41 +216,35 @@ __global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel(MrcArgs a) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[r][c] = ffma2(av[r], bv[c], acc[r][c]);
     }
-    __syncthreads();  // stage st is refilled by the next issue
     if (chunk + 1 == nchunks) {
-      // bits: row r (ty*8+r), byte tx, bit c = column tx*8+c
+      // Row ty*8+r, columns tx*8..+7 -> byte tx of the tile row (natural
+      // column order). acc = dot - tau, so bit = NOT sign(acc) (acc is never
+      // -0: it starts at -tau and adds non-negative products); funnel shifts
+      // collect the sign bits.
+      const uint32_t buf = tiles_done & 1u;
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         uint32_t byte = 0;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          byte |= (acc[r][c].x >= a.tau ? 1u : 0u) << (2 * c);
-          byte |= (acc[r][c].y >= a.tau ? 1u : 0u) << (2 * c + 1);
+        for (int c = 3; c >= 0; --c) {
+          byte = __funnelshift_l(__float_as_uint(acc[r][c].y), byte, 1);
+          byte = __funnelshift_l(__float_as_uint(acc[r][c].x), byte, 1);
         }
-        rowbytes[(ty * 8 + r) * 16 + tx] = static_cast<uint8_t>(byte);
+        rowbytes[buf * 2048 + (ty * 8 + r) * 16 + tx] = static_cast<uint8_t>(~byte);
       }
-      __syncthreads();
-      if (tid < kTile) {
-        const uint32_t i = bi * kTile + tid;
-        if (i < a.g.n_rows) {
-          uint4 wv = *reinterpret_cast<const uint4*>(rowbytes + tid * 16);
-          const uint32_t c0 = bj * kTile;
-          wv.x &= col_mask(c0, i, a.g);
-          wv.y &= col_mask(c0 + 32, i, a.g);
-          wv.z &= col_mask(c0 + 64, i, a.g);
-          wv.w &= col_mask(c0 + 96, i, a.g);
-          *reinterpret_cast<uint4*>(a.bitmap + static_cast<size_t>(i) * a.g.words_per_row + bj * 4) = wv;
-          const uint32_t cnt = __popc(wv.x) + __popc(wv.y) + __popc(wv.z) + __popc(wv.w);
-          if (cnt) atomicAdd(a.rowcnt + i, cnt);
-        }
-      }
-      // next tile (rowbytes reuse is ordered by the next item's __syncthreads)
+      pending = true;
+      pend_bi = bi;
+      pend_bj = bj;
+      pend_buf = buf;
+      ++tiles_done;
       if (++bj == a.nbc) {
         ++bi;
         bj = a.g.triangle ? bi : 0;
       }
     }
   }
+  __syncthreads();
+  if (pending) flush();
 }
 
 // Hamming tile: warp w handles rows (w&3)*32+lane and words (w>>2)*2..+1.
@@ -328,10 +356,10 @@ void launch_mrc_bitmap(const float* ST_rows, uint32_t ld_rows, const float* ST_c
   const uint64_t t = n_tiles(g, nbr, nbc);
   if (t == 0 || K == 0) return;
   const uint32_t kc = K < kKC ? K : kKC;
-  const size_t smem = (4ull * kc * kTile) * sizeof(float) + kTile * 16;
+  const size_t smem = (6ull * kc * kTile) * sizeof(float) + 2 * 2048;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(mrc_bitmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kKC * kTile * 4 + 4096);
+    cudaFuncSetAttribute(mrc_bitmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * kKC * kTile * 4 + 4096);
     configured = true;
   }
   uint64_t grid = static_cast<uint64_t>(sms()) * 2;

@@ -27,6 +27,32 @@ __global__ void ffma_kernel(float* out, float a, float b, long long* cyc) {
   if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
 }
 
+__device__ __forceinline__ unsigned long long ffma2u(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+// FFMA2 (fma.rn.f32x2): 2 FMAs per lane per instruction.
+__global__ void ffma2_kernel(float* out, float a, float b, long long* cyc) {
+  unsigned long long r[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) r[c] = 0x3f8000003f800000ull + threadIdx.x + c;
+  const unsigned long long aa = (static_cast<unsigned long long>(__float_as_uint(a)) << 32) | __float_as_uint(a);
+  const unsigned long long bb = (static_cast<unsigned long long>(__float_as_uint(b)) << 32) | __float_as_uint(b);
+  long long t0 = clock64();
+  for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) r[c] = ffma2u(r[c], aa, bb);
+  }
+  long long t1 = clock64();
+  unsigned long long s = 0;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) s ^= r[c];
+  if (s == 12345ull) out[0] = 1.0f;
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+}
+
 __global__ void popc_kernel(unsigned* out, unsigned m, long long* cyc) {
   unsigned r[kChains];
 #pragma unroll
@@ -93,6 +119,8 @@ int main() {
   cudaMalloc(&fo, 64);
   std::printf("{\n  \"sms\": %d,\n", sms);
   run("ffma", [&](int g, int t, long long* c) { ffma_kernel<<<g, t>>>(fo, 1.0001f, 1e-7f, c); }, 1.0, sms, false);
+  run("ffma2_fma_ops", [&](int g, int t, long long* c) { ffma2_kernel<<<g, t>>>(fo, 1.0001f, 1e-7f, c); }, 2.0, sms,
+      false);
   run("popc_xor_add", [&](int g, int t, long long* c) {
     popc_kernel<<<g, t>>>(reinterpret_cast<unsigned*>(fo), 0x9E3779B9u, c);
   }, 1.0, sms, false);
