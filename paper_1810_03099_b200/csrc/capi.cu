@@ -976,7 +976,7 @@ int refsig_gpu_mrc_pairs_rows(refsig_gpu_ctx* ctx, float tau, uint32_t row_lo, u
     require(!std::isnan(tau), "tau is NaN");
     require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
     require(row_lo <= row_hi && row_hi <= ctx->n_docs, "bad row range");
-    require(row_lo % kTile == 0 && (row_hi % kTile == 0 || row_hi == ctx->n_docs),
+    require(row_lo == row_hi || (row_lo % kTile == 0 && (row_hi % kTile == 0 || row_hi == ctx->n_docs)),
             "row range must be aligned to 128-row tiles");
     PairGrid g = self_grid(ctx);
     g.row_begin = row_lo;

@@ -45,3 +45,12 @@ def pairs_in_rows(n_docs: int, lo: int, hi: int) -> int:
     if hi <= lo:
         return 0
     return (hi - lo) * (n_docs - 1) - (hi * (hi - 1) // 2 - lo * (lo - 1) // 2)
+
+
+def gather_sorted_keys(local_keys, world: int, all_gather_object) -> "list":
+    """Concatenate the ranks' sorted key arrays in rank order (the global sorted
+    candidate list, since ranks own increasing row ranges)."""
+    parts = [None] * world
+    all_gather_object(parts, local_keys)
+    import numpy as np
+    return np.concatenate([np.asarray(p, dtype=np.uint64) for p in parts]) if parts else np.zeros(0, np.uint64)

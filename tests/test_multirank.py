@@ -1,0 +1,83 @@
+"""Multi-rank host logic on CPU (gloo, world size 2): the triangle row-panel
+sharding used by bench.py --gpus N. Each rank computes its
+rows' MRC/Hamming pairs (the oracle stands in for the GPU kernel here), the
+rank-ordered concatenation must equal the single-rank result, and the
+max-over-ranks timing reduction works."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_1810_03099_b200 import shard
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_row_shards_cover_triangle_once():
+    for n in [1, 127, 128, 129, 2000, 18846]:
+        for w in [1, 2, 3, 4, 8]:
+            sh = shard.row_shards(n, w)
+            assert len(sh) == w and sh[0][0] == 0 and sh[-1][1] == n
+            for (a, b), (c, d) in zip(sh, sh[1:]):
+                assert b == c and a <= b
+            assert all(lo % 128 == 0 or lo == hi == n for lo, hi in sh)
+            assert sum(shard.pairs_in_rows(n, lo, hi) for lo, hi in sh) == n * (n - 1) // 2
+
+
+def test_row_shards_balanced():
+    sh = shard.row_shards(18846, 8)
+    tiles = shard.panel_tiles(18846)
+    per = [sum(tiles[lo // 128:(hi + 127) // 128]) for lo, hi in sh]
+    assert max(per) / (sum(per) / 8) < 1.1  # 128-row panel granularity
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_1810_03099_b200 import corpus as C
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cp, cfg = C.config_corpus("c0")
+    cp = cp.slice_docs(600)
+    refs = C.sample_refs(0, cp.n_docs, 10)
+    o = oracle.mrc_pipeline(cp.tokens, cp.doc_off, cp.vocab, refs)
+    lo, hi = shard.row_shards(cp.n_docs, world)[rank]
+    mine, _ = oracle.mrc_pairs(o.S, 0.95, 1e-5, lo, hi, threads=1)
+    keys = shard.gather_sorted_keys(mine, world, dist.all_gather_object)
+    fp = oracle.simhash(o.counts, o.idf, 0, threads=1)
+    hk = shard.gather_sorted_keys(oracle.hamming_pairs(fp, 20, lo, hi, threads=1), world, dist.all_gather_object)
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        full, _ = oracle.mrc_pairs(o.S, 0.95, 1e-5, threads=1)
+        fullh = oracle.hamming_pairs(fp, 20, threads=1)
+        q.put((bool(np.array_equal(keys, full)), bool(np.array_equal(hk, fullh)), len(full), t.item()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_pairs_equal_single_rank():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    same_mrc, same_ham, n, tmax = res
+    assert same_mrc and same_ham and n > 0
+    assert tmax == 2.0
