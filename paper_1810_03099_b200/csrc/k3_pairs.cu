@@ -337,7 +337,7 @@ uint64_t n_tiles(PairGrid& g, uint32_t& nbr, uint32_t& nbc) {
   nbr = static_cast<uint32_t>(ceil_div(g.n_rows, kTile));
   nbc = static_cast<uint32_t>(ceil_div(g.n_cols, kTile));
   const uint64_t p0 = g.row_begin / kTile, p1 = ceil_div(g.row_end, kTile);
-  if (p1 <= p0) return 0;
+  if (g.row_end <= g.row_begin || p1 <= p0) return 0;
   if (g.triangle) {
     auto S = [&](uint64_t r) { return r * nbc - r * (r - 1) / 2; };
     g.tile0 = static_cast<uint32_t>(S(p0));
