@@ -126,6 +126,18 @@ int refsig_gpu_mrc_pairs(refsig_gpu_ctx* ctx, float tau, uint64_t* out_pairs, ui
 int refsig_gpu_mrc_pairs_rows(refsig_gpu_ctx* ctx, float tau, uint32_t row_lo, uint32_t row_hi, uint64_t* out_pairs,
                               uint64_t capacity, uint64_t* out_count);
 
+/* The whole MRC step — count(weight_mode) -> set_reference_docs -> sign ->
+ * pairs of rows [row_lo,row_hi) with compare >= tau — enqueued without any host
+ * synchronisation. The first call for a given (corpus, weighting, references,
+ * tau, rows, stream) runs eagerly and captures the sequence as a CUDA graph;
+ * later identical calls replay the graph (one launch). Collect the result with
+ * refsig_gpu_step_result before the next step. */
+int refsig_gpu_mrc_step(refsig_gpu_ctx* ctx, int weight_mode, const uint32_t* ref_doc_ids, uint32_t K, float tau,
+                        uint32_t row_lo, uint32_t row_hi);
+/* Wait for the step; *out_count = pairs; copies min(count, capacity) sorted
+ * keys to out_pairs (may be NULL: keys stay on the device, refsig_gpu_get_pairs). */
+int refsig_gpu_step_result(refsig_gpu_ctx* ctx, uint64_t* out_pairs, uint64_t capacity, uint64_t* out_count);
+
 /* ---- K4: Simhash + Hamming (A8-A10) -----------------------------------------
  * weight_mode as above (TF reproduces the reference's per-occurrence rule).
  * term_hash: optional HOST table of vocab 64-bit hashes (e.g. word_hash64 of

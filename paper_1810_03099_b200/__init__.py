@@ -98,6 +98,9 @@ SIGNATURES = {
     "refsig_gpu_set_profiling": ([_c.c_void_p, _c.c_int], _c.c_int),
     "refsig_gpu_phase_times": ([_c.c_void_p, _P(_c.c_double), _P(_c.c_uint64)], _c.c_int),
     "refsig_gpu_launch_count": ([], _c.c_uint64),
+    "refsig_gpu_mrc_step": ([_c.c_void_p, _c.c_int, _P(_c.c_uint32), _c.c_uint32, _c.c_float, _c.c_uint32, _c.c_uint32],
+                            _c.c_int),
+    "refsig_gpu_step_result": ([_c.c_void_p, _P(_c.c_uint64), _c.c_uint64, _P(_c.c_uint64)], _c.c_int),
 }
 PHASES = ["count", "reference", "sign", "pair_tiles", "pair_emit", "simhash", "h2d", "d2h"]
 
@@ -306,6 +309,30 @@ class Context:
         rc = self._L.refsig_gpu_mrc_pairs_rows(self._h, ctypes.c_float(tau), row_lo, row_hi, None, 0,
                                                ctypes.byref(n))
         self._check(rc, n.value)
+        if not fetch:
+            return n.value
+        keys = np.empty(n.value, np.uint64)
+        if n.value:
+            self._check(self._L.refsig_gpu_get_pairs(self._h, _ptr(keys, ctypes.c_uint64), n.value))
+        return keys
+
+    def mrc_step(self, ref_doc_ids, tau: float, weighting: int = WEIGHT_TFIDF, row_lo: int = 0,
+                 row_hi: int | None = None):
+        """count -> reference -> sign -> pairs, enqueued as one CUDA-graph replay
+        after the first call; collect with step_result()."""
+        ids = np.ascontiguousarray(ref_doc_ids, np.uint32)
+        hi = self.n_docs if row_hi is None else row_hi
+        self._check(self._L.refsig_gpu_mrc_step(self._h, weighting, _ptr(ids, ctypes.c_uint32), len(ids),
+                                                ctypes.c_float(tau), row_lo, hi))
+        self.K = len(ids)
+
+    def step_result(self, out: np.ndarray | None = None, fetch: bool = False):
+        n = ctypes.c_uint64()
+        if out is not None:
+            rc = self._L.refsig_gpu_step_result(self._h, _ptr(out, ctypes.c_uint64), len(out), ctypes.byref(n))
+            self._check(rc, n.value)
+            return out[: n.value]
+        self._check(self._L.refsig_gpu_step_result(self._h, None, 0, ctypes.byref(n)), n.value)
         if not fetch:
             return n.value
         keys = np.empty(n.value, np.uint64)

@@ -19,6 +19,7 @@ using namespace refsig_gpu;
 
 namespace {
 std::atomic<uint64_t> g_launches{0};
+std::atomic<uint64_t> g_alloc_gen{0};  // bumped on every device (re)allocation: invalidates captured graphs
 }  // namespace
 
 namespace refsig_gpu {
@@ -62,6 +63,7 @@ struct DevBuf {
     }
     ck(cudaMalloc(&p, bytes), "cudaMalloc");
     cap = bytes;
+    g_alloc_gen.fetch_add(1);
     return true;
   }
   template <class T>
@@ -130,6 +132,27 @@ struct refsig_gpu_ctx {
   // query mode
   refsig_gpu_ctx* db = nullptr;
 
+  // emit in flight (enqueue_emit -> finish_emit)
+  bool emit_pending = false;
+  PairGrid emit_grid{};
+
+  // captured MRC step (refsig_gpu_mrc_step)
+  cudaGraphExec_t step_exec = nullptr;
+  struct StepKey {
+    uint64_t alloc_gen = ~0ull, load_gen = 0;
+    int weight_mode = -1;
+    std::vector<uint32_t> refs;
+    float tau = 0.0f;
+    uint32_t lo = 0, hi = 0;
+    cudaStream_t stream = nullptr;
+    bool operator==(const StepKey& o) const {
+      return alloc_gen == o.alloc_gen && load_gen == o.load_gen && weight_mode == o.weight_mode && refs == o.refs &&
+             tau == o.tau && lo == o.lo && hi == o.hi && stream == o.stream;
+    }
+  } step_key;
+  uint64_t load_gen = 0;
+  bool capturing = false;
+
   // pinned staging for small uploads (no hidden stream sync of pageable H2D)
   void* h_stage = nullptr;
   size_t stage_cap = 0;
@@ -152,6 +175,7 @@ struct refsig_gpu_ctx {
     for (auto e : ev_free) cudaEventDestroy(e);
     if (h_stage) cudaFreeHost(h_stage);
     if (stage_done) cudaEventDestroy(stage_done);
+    if (step_exec) cudaGraphExecDestroy(step_exec);
   }
 };
 
@@ -233,7 +257,7 @@ struct Phase {
 void upload(refsig_gpu_ctx* c, void* dst, const void* src, size_t bytes) {
   if (!bytes) return;
   if (!c->stage_done) ck(cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming), "event");
-  ck(cudaEventSynchronize(c->stage_done), "staging");  // previous upload consumed
+  if (!c->capturing) ck(cudaEventSynchronize(c->stage_done), "staging");  // previous upload consumed
   if (bytes > c->stage_cap) {
     if (c->h_stage) cudaFreeHost(c->h_stage);
     c->h_stage = nullptr;
@@ -241,10 +265,13 @@ void upload(refsig_gpu_ctx* c, void* dst, const void* src, size_t bytes) {
     size_t cap = std::max<size_t>(bytes, 1 << 16);
     ck(cudaMallocHost(&c->h_stage, cap), "cudaMallocHost");
     c->stage_cap = cap;
+    g_alloc_gen.fetch_add(1);  // captured copies read from h_stage
   }
   std::memcpy(c->h_stage, src, bytes);
   ck(cudaMemcpyAsync(dst, c->h_stage, bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
-  ck(cudaEventRecord(c->stage_done, c->stream), "event");
+  // (while capturing, the record would become a graph node and the event
+  // could no longer be waited on from the host; mrc_step records it itself)
+  if (!c->capturing) ck(cudaEventRecord(c->stage_done, c->stream), "event");
 }
 
 void reset_downstream(refsig_gpu_ctx* c) {
@@ -254,26 +281,35 @@ void reset_downstream(refsig_gpu_ctx* c) {
 
 uint32_t words_per_row(uint32_t n_cols) { return static_cast<uint32_t>(ceil_div(n_cols, kTile) * 4); }
 
-// Scan rowcnt, emit sorted keys into ctx->cand (growing it if needed), and
-// optionally copy them to the caller's host buffer.
-int run_emit(refsig_gpu_ctx* c, const PairGrid& g, uint64_t* out, uint64_t capacity, uint64_t* out_count) {
+// Scan rowcnt and emit sorted keys into ctx->cand with its current capacity;
+// the total is copied (async) to h_pin[0]. No host synchronisation.
+void enqueue_emit(refsig_gpu_ctx* c, const PairGrid& g) {
   const uint64_t n = g.n_rows;
   c->rowstart.ensure(sizeof(uint64_t) * (n + 1));
   c->scan_tmp.ensure(scan_tmp_bytes(n));
   c->cand.ensure(sizeof(uint64_t) * (1u << 20));
-  uint64_t cap_keys = c->cand.cap / sizeof(uint64_t);
   {
     Phase ph(c, REFSIG_PHASE_PAIR_EMIT);
     launch_exclusive_scan_u32_to_u64(c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(), n, c->scan_tmp.p,
                                      c->stream);
     launch_emit_pairs(c->bitmap.as<uint32_t>(), g, c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(),
-                      c->cand.as<uint64_t>(), cap_keys, c->stream);
+                      c->cand.as<uint64_t>(), c->cand.cap / sizeof(uint64_t), c->stream);
     launched("emit");
   }
   ck(cudaMemcpyAsync(c->h_pin, c->rowstart.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, c->stream), "D2H count");
+  c->emit_pending = true;
+  c->emit_grid = g;
+}
+
+// Wait for the enqueued emission; if ctx->cand was too small, grow it and
+// emit again (the bitmap is still valid); optionally copy to the caller.
+int finish_emit(refsig_gpu_ctx* c, uint64_t* out, uint64_t capacity, uint64_t* out_count) {
+  require(c->emit_pending, "no pair computation in flight");
   sync(c);
+  c->emit_pending = false;
+  const PairGrid& g = c->emit_grid;
   const uint64_t total = c->h_pin[0];
-  if (total > cap_keys) {
+  if (total > c->cand.cap / sizeof(uint64_t)) {
     c->cand.ensure(sizeof(uint64_t) * (total + total / 4 + 1024));
     Phase ph(c, REFSIG_PHASE_PAIR_EMIT);
     launch_emit_pairs(c->bitmap.as<uint32_t>(), g, c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(),
@@ -293,6 +329,11 @@ int run_emit(refsig_gpu_ctx* c, const PairGrid& g, uint64_t* out, uint64_t capac
     return REFSIG_E_OVERFLOW;
   }
   return REFSIG_OK;
+}
+
+int run_emit(refsig_gpu_ctx* c, const PairGrid& g, uint64_t* out, uint64_t capacity, uint64_t* out_count) {
+  enqueue_emit(c, g);
+  return finish_emit(c, out, capacity, out_count);
 }
 
 void prepare_bitmap(refsig_gpu_ctx* c, const PairGrid& g, bool zero) {
@@ -418,6 +459,7 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
   ck(cudaStreamSynchronize(c->stream), "H2D metadata");
   c->loaded = true;
   c->counted = false;
+  ++c->load_gen;
   reset_downstream(c);
 }
 
@@ -523,66 +565,68 @@ int refsig_gpu_load_corpus_device(refsig_gpu_ctx* ctx, const uint32_t* d_tokens,
   });
 }
 
+static void do_count(refsig_gpu_ctx* ctx, int weight_mode) {
+  require(ctx->loaded, "no corpus loaded");
+  require(weight_mode == REFSIG_WEIGHT_TF || weight_mode == REFSIG_WEIGHT_TFIDF, "bad weight mode");
+  refsig_gpu_ctx* db = ctx->db;
+  if (db) {
+    require(db->counted, "attached database not counted");
+    require(db->vocab == ctx->vocab, "query vocab differs from database vocab");
+  }
+  const uint32_t N = ctx->n_docs, V = ctx->vocab;
+  ctx->ent.ensure(sizeof(uint2) * std::max<uint64_t>(ctx->n_tokens, 1));
+  ctx->chunk_scratch.ensure(sizeof(uint2) * std::max<uint64_t>(ctx->n_tokens, 1));
+  ctx->nnz.ensure(sizeof(uint32_t) * N);
+  ctx->df.ensure(sizeof(uint32_t) * V);
+  ctx->info.ensure(sizeof(TermInfo) * V);
+  if (ctx->flags.ensure(16)) ck(cudaMemsetAsync(ctx->flags.p, 0, 16, ctx->stream), "memset");
+  Phase ph(ctx, REFSIG_PHASE_COUNT);
+  // df replicas: ~8 MB budget, 1..16 copies (see k1_count.cu df_add)
+  const uint32_t reps = std::max<uint32_t>(1u, std::min<uint32_t>(16u, (2u << 20) / V));
+  ctx->df_rep.ensure(sizeof(uint32_t) * static_cast<size_t>(V) * reps);
+  ck(cudaMemsetAsync(ctx->df_rep.p, 0, sizeof(uint32_t) * static_cast<size_t>(V) * reps, ctx->stream), "memset df");
+  CountArgs a{ctx->tok, ctx->doc_off.as<uint64_t>(), V, ctx->ent.as<uint2>(), ctx->nnz.as<uint32_t>(),
+              ctx->df_rep.as<uint32_t>(), reps, ctx->flags.as<uint32_t>(), ctx->chunk_scratch.as<uint2>(),
+              ctx->chunk_cnt.as<uint32_t>()};
+  // fork: the 512-token chunk sorts (critical path, then the merges) on the
+  // main stream; tiny docs, 256-key docs and long docs on side[0]; merge
+  // classes spread over all four streams once the chunks are sorted.
+  cudaStream_t m0 = ctx->stream;
+  ck(cudaEventRecord(ctx->ev_fork, m0), "fork");
+  for (int k = 0; k < 3; ++k) ck(cudaStreamWaitEvent(ctx->side[k], ctx->ev_fork, 0), "fork");
+  launch_count_chunks(16, a, ctx->chunks[1].as<uint2>(), ctx->n_chunks[1], m0);
+  ck(cudaEventRecord(ctx->ev_mid, m0), "mid");
+  launch_count_tiny(a, ctx->tiny_docs.as<uint32_t>(), ctx->n_tiny, ctx->side[0]);
+  launch_count_chunks(8, a, ctx->chunks[0].as<uint2>(), ctx->n_chunks[0], ctx->side[0]);
+  launch_count_large(a, ctx->long_docs.as<uint32_t>(), ctx->long_off.as<uint64_t>(), ctx->n_long,
+                     ctx->long_scratch.as<uint32_t>(), ctx->side[0]);
+  cudaStream_t ms[kMergeClasses] = {ctx->side[0], ctx->side[1], ctx->side[2], m0};
+  for (int k = 0; k < 3; ++k) ck(cudaStreamWaitEvent(ctx->side[k], ctx->ev_mid, 0), "mid");
+  for (int k = kMergeClasses - 1; k >= 0; --k)
+    launch_count_merge(k, a, ctx->chunks[1].as<uint2>(), ctx->mdocs[k].as<uint32_t>(), ctx->n_mdocs[k], ms[k]);
+  for (int k = 0; k < 3; ++k) {  // join
+    ck(cudaEventRecord(ctx->ev_join[k], ctx->side[k]), "join");
+    ck(cudaStreamWaitEvent(m0, ctx->ev_join[k], 0), "join");
+  }
+  launch_idf(ctx->df_rep.as<uint32_t>(), reps, V, N, weight_mode, ctx->df.as<uint32_t>(), ctx->info.as<TermInfo>(),
+             ctx->stream);
+  ctx->ref_dirty = false;  // idf_kernel resets info[].ref_row
+  ctx->weight_mode = weight_mode;
+  if (db) {
+    // Query mode: the database's IDF and reference rows (configs[4]); the
+    // query batch keeps its own df.
+    ck(cudaStreamSynchronize(db->stream), "sync database");
+    ck(cudaMemcpyAsync(ctx->info.p, db->info.p, sizeof(TermInfo) * V, cudaMemcpyDeviceToDevice, ctx->stream),
+       "copy database idf");
+    ctx->weight_mode = db->weight_mode;
+  }
+  launched("count");
+  ctx->counted = true;
+  reset_downstream(ctx);
+}
+
 int refsig_gpu_count(refsig_gpu_ctx* ctx, int weight_mode) {
-  return guard(ctx, [&] {
-    require(ctx->loaded, "no corpus loaded");
-    require(weight_mode == REFSIG_WEIGHT_TF || weight_mode == REFSIG_WEIGHT_TFIDF, "bad weight mode");
-    refsig_gpu_ctx* db = ctx->db;
-    if (db) {
-      require(db->counted, "attached database not counted");
-      require(db->vocab == ctx->vocab, "query vocab differs from database vocab");
-    }
-    const uint32_t N = ctx->n_docs, V = ctx->vocab;
-    ctx->ent.ensure(sizeof(uint2) * std::max<uint64_t>(ctx->n_tokens, 1));
-    ctx->chunk_scratch.ensure(sizeof(uint2) * std::max<uint64_t>(ctx->n_tokens, 1));
-    ctx->nnz.ensure(sizeof(uint32_t) * N);
-    ctx->df.ensure(sizeof(uint32_t) * V);
-    ctx->info.ensure(sizeof(TermInfo) * V);
-    if (ctx->flags.ensure(16)) ck(cudaMemsetAsync(ctx->flags.p, 0, 16, ctx->stream), "memset");
-    Phase ph(ctx, REFSIG_PHASE_COUNT);
-    // df replicas: ~8 MB budget, 1..16 copies (see k1_count.cu df_add)
-    const uint32_t reps = std::max<uint32_t>(1u, std::min<uint32_t>(16u, (2u << 20) / V));
-    ctx->df_rep.ensure(sizeof(uint32_t) * static_cast<size_t>(V) * reps);
-    ck(cudaMemsetAsync(ctx->df_rep.p, 0, sizeof(uint32_t) * static_cast<size_t>(V) * reps, ctx->stream), "memset df");
-    CountArgs a{ctx->tok, ctx->doc_off.as<uint64_t>(), V, ctx->ent.as<uint2>(), ctx->nnz.as<uint32_t>(),
-                ctx->df_rep.as<uint32_t>(), reps, ctx->flags.as<uint32_t>(), ctx->chunk_scratch.as<uint2>(),
-                ctx->chunk_cnt.as<uint32_t>()};
-    // fork: the 512-token chunk sorts (critical path, then the merges) on the
-    // main stream; tiny docs, 256-key docs and long docs on side[0]; merge
-    // classes spread over all four streams once the chunks are sorted.
-    cudaStream_t m0 = ctx->stream;
-    ck(cudaEventRecord(ctx->ev_fork, m0), "fork");
-    for (int k = 0; k < 3; ++k) ck(cudaStreamWaitEvent(ctx->side[k], ctx->ev_fork, 0), "fork");
-    launch_count_chunks(16, a, ctx->chunks[1].as<uint2>(), ctx->n_chunks[1], m0);
-    ck(cudaEventRecord(ctx->ev_mid, m0), "mid");
-    launch_count_tiny(a, ctx->tiny_docs.as<uint32_t>(), ctx->n_tiny, ctx->side[0]);
-    launch_count_chunks(8, a, ctx->chunks[0].as<uint2>(), ctx->n_chunks[0], ctx->side[0]);
-    launch_count_large(a, ctx->long_docs.as<uint32_t>(), ctx->long_off.as<uint64_t>(), ctx->n_long,
-                       ctx->long_scratch.as<uint32_t>(), ctx->side[0]);
-    cudaStream_t ms[kMergeClasses] = {ctx->side[0], ctx->side[1], ctx->side[2], m0};
-    for (int k = 0; k < 3; ++k) ck(cudaStreamWaitEvent(ctx->side[k], ctx->ev_mid, 0), "mid");
-    for (int k = kMergeClasses - 1; k >= 0; --k)
-      launch_count_merge(k, a, ctx->chunks[1].as<uint2>(), ctx->mdocs[k].as<uint32_t>(), ctx->n_mdocs[k], ms[k]);
-    for (int k = 0; k < 3; ++k) {  // join
-      ck(cudaEventRecord(ctx->ev_join[k], ctx->side[k]), "join");
-      ck(cudaStreamWaitEvent(m0, ctx->ev_join[k], 0), "join");
-    }
-    launch_idf(ctx->df_rep.as<uint32_t>(), reps, V, N, weight_mode, ctx->df.as<uint32_t>(), ctx->info.as<TermInfo>(),
-               ctx->stream);
-    ctx->ref_dirty = false;  // idf_kernel resets info[].ref_row
-    ctx->weight_mode = weight_mode;
-    if (db) {
-      // Query mode: the database's IDF and reference rows (configs[4]); the
-      // query batch keeps its own df.
-      ck(cudaStreamSynchronize(db->stream), "sync database");
-      ck(cudaMemcpyAsync(ctx->info.p, db->info.p, sizeof(TermInfo) * V, cudaMemcpyDeviceToDevice, ctx->stream),
-         "copy database idf");
-      ctx->weight_mode = db->weight_mode;
-    }
-    launched("count");
-    ctx->counted = true;
-    reset_downstream(ctx);
-  });
+  return guard(ctx, [&] { do_count(ctx, weight_mode); });
 }
 
 int refsig_gpu_get_counts(refsig_gpu_ctx* ctx, uint64_t* rowptr, uint32_t* ids, uint32_t* counts, uint64_t cap,
@@ -656,23 +700,25 @@ int refsig_gpu_get_inv_norm(refsig_gpu_ctx* ctx, float* inv_norm) {
   });
 }
 
+static void do_set_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_ids, uint32_t K) {
+  require(ctx->counted, "count() not called");
+  require(!ctx->db, "query context uses the attached database's reference");
+  require(ref_doc_ids != nullptr, "ref_doc_ids is NULL");
+  require(K >= 1, "K must be >= 1");
+  uint64_t u_cap = 0;
+  for (uint32_t k = 0; k < K; ++k) {
+    require(ref_doc_ids[k] < ctx->n_docs, "reference doc id >= n_docs");
+    u_cap += ctx->h_off[ref_doc_ids[k] + 1] - ctx->h_off[ref_doc_ids[k]];
+  }
+  ctx->ref_docs.ensure(4ull * K);
+  upload(ctx, ctx->ref_docs.p, ref_doc_ids, 4ull * K);
+  RefArgs r{K,     nullptr, nullptr, ctx->ent.as<uint2>(), false, (K + 3) & ~3u, ctx->ref_docs.as<uint32_t>(),
+            ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>()};
+  build_reference(ctx, r, u_cap);
+}
+
 int refsig_gpu_set_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_ids, uint32_t K) {
-  return guard(ctx, [&] {
-    require(ctx->counted, "count() not called");
-    require(!ctx->db, "query context uses the attached database's reference");
-    require(ref_doc_ids != nullptr, "ref_doc_ids is NULL");
-    require(K >= 1, "K must be >= 1");
-    uint64_t u_cap = 0;
-    for (uint32_t k = 0; k < K; ++k) {
-      require(ref_doc_ids[k] < ctx->n_docs, "reference doc id >= n_docs");
-      u_cap += ctx->h_off[ref_doc_ids[k] + 1] - ctx->h_off[ref_doc_ids[k]];
-    }
-    ctx->ref_docs.ensure(4ull * K);
-    upload(ctx, ctx->ref_docs.p, ref_doc_ids, 4ull * K);
-    RefArgs r{K,     nullptr, nullptr, ctx->ent.as<uint2>(), false, (K + 3) & ~3u, ctx->ref_docs.as<uint32_t>(),
-              ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>()};
-    build_reference(ctx, r, u_cap);
-  });
+  return guard(ctx, [&] { do_set_reference_docs(ctx, ref_doc_ids, K); });
 }
 
 int refsig_gpu_set_reference_vectors(refsig_gpu_ctx* ctx, uint32_t K, const uint64_t* rowptr, const uint32_t* term_ids,
@@ -729,33 +775,35 @@ int refsig_gpu_reference_union(refsig_gpu_ctx* ctx, uint32_t* out_u) {
   });
 }
 
+static void do_sign(refsig_gpu_ctx* ctx) {
+  require(ctx->counted, "count() not called");
+  const refsig_gpu_ctx* refc = ctx->db ? ctx->db : ctx;
+  require(refc->have_ref, "no reference set");
+  const uint32_t N = ctx->n_docs, K = refc->K;
+  ctx->S.ensure(sizeof(float) * static_cast<size_t>(N) * K);
+  const uint32_t ld = static_cast<uint32_t>(ceil_div(N, kTile) * kTile);
+  ctx->ST.ensure(sizeof(float) * static_cast<size_t>(ld) * K);
+  ctx->ld = ld;
+  if (ld > N)  // zero pad columns: the tile kernels read whole 128-column panels
+    ck(cudaMemset2DAsync(ctx->ST.as<float>() + N, sizeof(float) * ld, 0, sizeof(float) * (ld - N), K, ctx->stream),
+       "memset ST pad");
+  ctx->inv_norm.ensure(sizeof(float) * N);
+  if (ctx->db) ck(cudaStreamSynchronize(ctx->db->stream), "sync database");
+  SignArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->info.as<TermInfo>(),
+             refc->R.as<float>(), N, K, refc->Kp, ctx->order.as<uint32_t>(), ctx->S.as<float>(),
+             ctx->ST.as<float>(), ld, ctx->inv_norm.as<float>()};
+  {
+    Phase ph(ctx, REFSIG_PHASE_SIGN);
+    launch_sign(a, ctx->stream);
+    launched("sign");
+  }
+  ctx->K = K;
+  ctx->signed_ = true;
+  ctx->have_inv_norm = true;
+}
+
 int refsig_gpu_sign(refsig_gpu_ctx* ctx) {
-  return guard(ctx, [&] {
-    require(ctx->counted, "count() not called");
-    const refsig_gpu_ctx* refc = ctx->db ? ctx->db : ctx;
-    require(refc->have_ref, "no reference set");
-    const uint32_t N = ctx->n_docs, K = refc->K;
-    ctx->S.ensure(sizeof(float) * static_cast<size_t>(N) * K);
-    const uint32_t ld = static_cast<uint32_t>(ceil_div(N, kTile) * kTile);
-    ctx->ST.ensure(sizeof(float) * static_cast<size_t>(ld) * K);
-    ctx->ld = ld;
-    if (ld > N)  // zero pad columns: the tile kernels read whole 128-column panels
-      ck(cudaMemset2DAsync(ctx->ST.as<float>() + N, sizeof(float) * ld, 0, sizeof(float) * (ld - N), K, ctx->stream),
-         "memset ST pad");
-    ctx->inv_norm.ensure(sizeof(float) * N);
-    if (ctx->db) ck(cudaStreamSynchronize(ctx->db->stream), "sync database");
-    SignArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->info.as<TermInfo>(),
-               refc->R.as<float>(), N, K, refc->Kp, ctx->order.as<uint32_t>(), ctx->S.as<float>(),
-               ctx->ST.as<float>(), ld, ctx->inv_norm.as<float>()};
-    {
-      Phase ph(ctx, REFSIG_PHASE_SIGN);
-      launch_sign(a, ctx->stream);
-      launched("sign");
-    }
-    ctx->K = K;
-    ctx->signed_ = true;
-    ctx->have_inv_norm = true;
-  });
+  return guard(ctx, [&] { do_sign(ctx); });
 }
 
 int refsig_gpu_get_signatures(refsig_gpu_ctx* ctx, float* S) {
@@ -989,6 +1037,122 @@ int refsig_gpu_mrc_pairs_rows(refsig_gpu_ctx* ctx, float tau, uint32_t row_lo, u
       launched("mrc bitmap");
     }
     rc2 = run_emit(ctx, g, out_pairs, capacity, out_count);
+  });
+  return rc != REFSIG_OK ? rc : rc2;
+}
+
+// The hot path as one enqueue: count -> reference docs -> sign -> tiles ->
+// scan -> emit (rows [lo, hi)), no host synchronisation.
+static void enqueue_step(refsig_gpu_ctx* ctx, int weight_mode, const uint32_t* refs, uint32_t K, float tau,
+                         uint32_t lo, uint32_t hi) {
+  do_count(ctx, weight_mode);
+  do_set_reference_docs(ctx, refs, K);
+  do_sign(ctx);
+  PairGrid g = self_grid(ctx);
+  g.row_begin = lo;
+  g.row_end = hi;
+  {
+    Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
+    prepare_bitmap(ctx, g, false);
+    launch_mrc_bitmap(ctx->ST.as<float>(), ctx->ld, ctx->ST.as<float>(), ctx->ld, ctx->K, tau, g,
+                      ctx->bitmap.as<uint32_t>(), ctx->rowcnt.as<uint32_t>(), ctx->stream);
+    launched("mrc bitmap");
+  }
+  enqueue_emit(ctx, g);
+}
+
+int refsig_gpu_mrc_step(refsig_gpu_ctx* ctx, int weight_mode, const uint32_t* ref_doc_ids, uint32_t K, float tau,
+                        uint32_t row_lo, uint32_t row_hi) {
+  return guard(ctx, [&] {
+    require(ctx->loaded, "no corpus loaded");
+    require(!ctx->db, "query contexts use the attached database's reference");
+    require(!ctx->emit_pending, "previous step not collected (refsig_gpu_step_result)");
+    require(ref_doc_ids != nullptr && K >= 1, "reference docs required");
+    require(!std::isnan(tau), "tau is NaN");
+    require(row_lo <= row_hi && row_hi <= ctx->n_docs, "bad row range");
+    require(row_lo == row_hi || (row_lo % kTile == 0 && (row_hi % kTile == 0 || row_hi == ctx->n_docs)),
+            "row range must be aligned to 128-row tiles");
+    refsig_gpu_ctx::StepKey key;
+    key.load_gen = ctx->load_gen;
+    key.weight_mode = weight_mode;
+    key.refs.assign(ref_doc_ids, ref_doc_ids + K);
+    key.tau = tau;
+    key.lo = row_lo;
+    key.hi = row_hi;
+    key.stream = ctx->stream;
+    key.alloc_gen = g_alloc_gen.load();
+    if (ctx->step_exec && key == ctx->step_key) {
+      // replay: every buffer and the candidate capacity are exactly as
+      // captured; the captured H2D copy reads the reference ids from the
+      // pinned staging buffer, which other calls may have reused
+      ck(cudaEventSynchronize(ctx->stage_done), "staging");
+      std::memcpy(ctx->h_stage, ref_doc_ids, 4ull * K);
+      ck(cudaGraphLaunch(ctx->step_exec, ctx->stream), "cudaGraphLaunch");
+      ck(cudaEventRecord(ctx->stage_done, ctx->stream), "event");
+      ctx->emit_pending = true;
+      ctx->emit_grid = self_grid(ctx);
+      ctx->emit_grid.row_begin = row_lo;
+      ctx->emit_grid.row_end = row_hi;
+      ctx->counted = ctx->have_ref = ctx->signed_ = true;
+      ctx->have_fp = ctx->have_x = false;
+      return;
+    }
+    // First run for this key: eager (sizes every buffer, results are valid),
+    // then capture the same enqueue sequence for later calls.
+    if (ctx->step_exec) {
+      cudaGraphExecDestroy(ctx->step_exec);
+      ctx->step_exec = nullptr;
+    }
+    enqueue_step(ctx, weight_mode, ref_doc_ids, K, tau, row_lo, row_hi);
+    uint64_t total = 0;
+    const int rc = finish_emit(ctx, nullptr, 0, &total);  // grows ctx->cand if needed
+    (void)rc;
+    const uint64_t keep_count = total;
+    key.alloc_gen = g_alloc_gen.load();
+    const bool prof = ctx->prof;
+    ctx->prof = false;
+    ctx->capturing = true;
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed);
+    if (e == cudaSuccess) {
+      try {
+        enqueue_step(ctx, weight_mode, ref_doc_ids, K, tau, row_lo, row_hi);
+      } catch (...) {
+        cudaStreamEndCapture(ctx->stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        ctx->capturing = false;
+        ctx->prof = prof;
+        throw;
+      }
+      e = cudaStreamEndCapture(ctx->stream, &graph);
+    }
+    ctx->capturing = false;
+    ctx->prof = prof;
+    ck(e, "stream capture");
+    ck(cudaEventRecord(ctx->stage_done, ctx->stream), "event");
+    e = cudaGraphInstantiate(&ctx->step_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    ck(e, "cudaGraphInstantiate");
+    ctx->step_key = key;
+    if (key.alloc_gen != g_alloc_gen.load()) {  // capture allocated: do not trust the graph
+      cudaGraphExecDestroy(ctx->step_exec);
+      ctx->step_exec = nullptr;
+    }
+    // the eager results stand: report them through step_result
+    ctx->h_pin[0] = keep_count;
+    ctx->emit_pending = true;
+    ctx->emit_grid = self_grid(ctx);
+    ctx->emit_grid.row_begin = row_lo;
+    ctx->emit_grid.row_end = row_hi;
+  });
+}
+
+int refsig_gpu_step_result(refsig_gpu_ctx* ctx, uint64_t* out_pairs, uint64_t capacity, uint64_t* out_count) {
+  int rc2 = REFSIG_OK;
+  int rc = guard(ctx, [&] {
+    require(out_count != nullptr, "out_count is NULL");
+    require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
+    rc2 = finish_emit(ctx, out_pairs, capacity, out_count);
   });
   return rc != REFSIG_OK ? rc : rc2;
 }
