@@ -120,9 +120,9 @@ __device__ __forceinline__ uint32_t warp_suffix_min_excl(uint32_t x, uint32_t la
 // RLE of the sorted keys (blocked, IPT per thread, first `len` valid) of a
 // group of W warps; writes (id,count) rows at ent[0..nnz) and bumps df.
 // Returns nnz (valid in every thread). sm: >= 3*W+2 words (W > 1).
-template <int IPT, int W, bool DF = true>
+template <int IPT, int W>
 __device__ __forceinline__ uint32_t rle_regs(const uint32_t (&v)[IPT], uint32_t t, uint32_t len, uint2* ent,
-                                             const CountArgs& ca, uint32_t* sm) {
+                                             const CountArgs& ca, uint32_t* sm, bool do_df = true) {
   const uint32_t lane = threadIdx.x & 31, w = t >> 5;
   // predecessor of v[0]
   uint32_t prev = __shfl_up_sync(0xffffffffu, v[IPT - 1], 1);
@@ -177,7 +177,7 @@ __device__ __forceinline__ uint32_t rle_regs(const uint32_t (&v)[IPT], uint32_t 
       const uint32_t rest = hmask & ~((2u << q) - 1);  // heads after q in this thread
       const uint32_t end = rest ? base + (__ffs(rest) - 1) : next;
       ent[pos] = make_uint2(v[q], end - (base + q));
-      if (DF) df_add(ca, v[q]);
+      if (do_df) df_add(ca, v[q]);
       ++pos;
     }
   }
@@ -194,25 +194,23 @@ __device__ __forceinline__ uint32_t load_key(const CountArgs& a, uint64_t b, uin
   return v;
 }
 
-// One warp per document (P = 32*IPT).
+// One warp per document (P = 32*IPT), one document per warp (see chunk_sort_kernel).
 template <int IPT>
 __global__ void __launch_bounds__(256) count_warp_kernel(CountArgs a, const uint32_t* __restrict__ docs,
                                                          uint32_t n_docs) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < n_docs; q += nw) {
-    const uint32_t d = docs[q];
-    const uint64_t b = a.doc_off[d];
-    const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
-    uint32_t v[IPT];
+  const uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q >= n_docs) return;
+  const uint32_t d = docs[q];
+  const uint64_t b = a.doc_off[d];
+  const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
+  uint32_t v[IPT];
 #pragma unroll
-    for (int k = 0; k < IPT; ++k) v[k] = load_key(a, b, k * 32 + lane, len);  // coalesced; any order sorts
-    bitonic_regs<IPT>(v, lane);
-    const uint32_t n = rle_regs<IPT, 1>(v, lane, len, a.ent + b, a, nullptr);
-    if (lane == 0) a.nnz[d] = n;
-  }
+  for (int k = 0; k < IPT; ++k) v[k] = load_key(a, b, k * 32 + lane, len);  // coalesced; any order sorts
+  bitonic_regs<IPT>(v, lane);
+  const uint32_t n = rle_regs<IPT, 1>(v, lane, len, a.ent + b, a, nullptr);
+  if (lane == 0) a.nnz[d] = n;
 }
-
 
 template <int THREADS>
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* scratch, uint32_t* total) {
@@ -237,30 +235,35 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
 // chunk is a whole document: its rows go straight to ent/nnz/df. Otherwise
 // the chunk's sorted unique (id,count) rows go to scratch at the chunk's own
 // token offset and chunk_cnt[q] = their number.
+// One warp per chunk and no grid-stride loop: with warp-uniform control flow
+// that the compiler can see, the shuffles need no collective fallback paths
+// (which doubled the code size of the unrolled network and thrashed the
+// instruction cache).
 template <int IPT>
 __global__ void __launch_bounds__(256, IPT <= 8 ? 6 : 4) chunk_sort_kernel(CountArgs a, const uint2* __restrict__ chunks,
-                                                         uint32_t n_chunks) {
+                                                                           uint32_t n_chunks) {
   constexpr uint32_t CS = 32 * IPT;
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < n_chunks; q += nw) {
-    const uint2 ch = chunks[q];
-    const uint32_t d = ch.x, c = (ch.y >> 1) & 0x7FFFu;
-    const uint64_t b = a.doc_off[d];
-    const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
-    const uint64_t cb = b + static_cast<uint64_t>(c) * CS;
-    const uint32_t clen = min(CS, len - c * CS);
-    uint32_t v[IPT];
+  const uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q >= n_chunks) return;
+  const uint2 ch = chunks[q];
+  const uint32_t d = ch.x, c = (ch.y >> 1) & 0x7FFFu;
+  const bool direct = ch.y & 1;
+  const uint64_t b = a.doc_off[d];
+  const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
+  const uint64_t cb = b + static_cast<uint64_t>(c) * CS;
+  const uint32_t clen = min(CS, len - c * CS);
+  uint32_t v[IPT];
 #pragma unroll
-    for (int k = 0; k < IPT; ++k) v[k] = load_key(a, cb, k * 32 + lane, clen);
-    bitonic_regs<IPT>(v, lane);
-    if (ch.y & 1) {
-      const uint32_t n = rle_regs<IPT, 1, true>(v, lane, clen, a.ent + b, a, nullptr);
-      if (lane == 0) a.nnz[d] = n;
-    } else {
-      const uint32_t n = rle_regs<IPT, 1, false>(v, lane, clen, a.scratch + cb, a, nullptr);
-      if (lane == 0) a.chunk_cnt[q] = n;
-    }
+  for (int k = 0; k < IPT; ++k) v[k] = load_key(a, cb, k * 32 + lane, clen);
+  bitonic_regs<IPT>(v, lane);
+  // a direct chunk is the whole doc: final rows + df; otherwise chunk rows for the merge
+  const uint32_t n = rle_regs<IPT, 1>(v, lane, clen, direct ? a.ent + b : a.scratch + cb, a, nullptr, direct);
+  if (lane == 0) {
+    if (direct)
+      a.nnz[d] = n;
+    else
+      a.chunk_cnt[q] = n;
   }
 }
 
@@ -511,16 +514,17 @@ int grid_for(uint64_t n, int per_sm) {
 
 void launch_count_tiny(const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s) {
   if (n == 0) return;
-  count_warp_kernel<2><<<grid_for(ceil_div(n, 8), 8), 256, 0, s>>>(a, docs, n);
+  count_warp_kernel<2><<<static_cast<unsigned>(ceil_div(n, 8)), 256, 0, s>>>(a, docs, n);
   note_launch();
 }
 
 void launch_count_chunks(int ipt, const CountArgs& a, const uint2* chunks, uint32_t n, cudaStream_t s) {
   if (n == 0) return;
+  const unsigned blocks = static_cast<unsigned>(ceil_div(n, 8));  // one warp per chunk
   if (ipt == 8)
-    chunk_sort_kernel<8><<<grid_for(ceil_div(n, 8), 6), 256, 0, s>>>(a, chunks, n);
+    chunk_sort_kernel<8><<<blocks, 256, 0, s>>>(a, chunks, n);
   else
-    chunk_sort_kernel<16><<<grid_for(ceil_div(n, 8), 4), 256, 0, s>>>(a, chunks, n);
+    chunk_sort_kernel<16><<<blocks, 256, 0, s>>>(a, chunks, n);
   note_launch();
 }
 

@@ -107,10 +107,14 @@ __global__ void __launch_bounds__(256) sign_kernel(SignArgs a) {
   __shared__ float part[kSignWarps][32][33];
   __shared__ int2 queue[kSignWarps][64];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   const uint32_t K = a.K, Kp = a.Kp;
   const uint32_t lt = (1u << lane) - 1u;
-  for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + wid; q < a.n_docs; q += nwarps) {
+  // one document per warp (no grid-stride loop: keeps the shuffles free of
+  // collective fallback code); blocks start in launch order, so `order`
+  // (longest first) still front-loads the long documents
+  const uint32_t q = blockIdx.x * (blockDim.x >> 5) + wid;
+  if (q >= a.n_docs) return;
+  {
     const uint32_t d = a.order[q];
     const uint2* __restrict__ e = a.ent + a.doc_off[d];
     const uint32_t n = a.nnz[d];
@@ -219,9 +223,7 @@ void launch_ref_fill(const RefArgs& r, const TermInfo* info, float* R, cudaStrea
 
 void launch_sign(const SignArgs& a, cudaStream_t s) {
   if (a.n_docs == 0) return;
-  uint64_t blocks = ceil_div(a.n_docs, kSignWarps);
-  const uint64_t cap = static_cast<uint64_t>(sm_count()) * 4;
-  if (blocks > cap) blocks = cap;
+  const uint64_t blocks = ceil_div(a.n_docs, kSignWarps);
   sign_kernel<<<static_cast<unsigned>(blocks), 32 * kSignWarps, 0, s>>>(a);
   note_launch();
 }

@@ -298,10 +298,11 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
                                                    const uint64_t* __restrict__ rowstart, uint64_t* __restrict__ out,
                                                    uint64_t capacity) {
   const int lane = threadIdx.x & 31;
-  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t i = g.row_begin + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < g.row_end; i += nwarps) {
+  const uint32_t i = g.row_begin + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // one row per warp
+  if (i >= g.row_end) return;
+  {
     uint32_t remaining = rowcnt[i];
-    if (remaining == 0) continue;
+    if (remaining == 0) return;
     uint64_t base = rowstart[i];
     const uint32_t* row = bitmap + static_cast<size_t>(i) * g.words_per_row;
     const uint32_t wbeg = g.triangle ? (i / kTile) * 4 : 0;
@@ -383,9 +384,7 @@ void launch_hamming_bitmap(const uint64_t* f_rows, const uint64_t* f_cols, int m
 void launch_emit_pairs(const uint32_t* bitmap, const PairGrid& g, const uint32_t* rowcnt, const uint64_t* rowstart,
                        uint64_t* out, uint64_t capacity, cudaStream_t s) {
   if (g.row_end <= g.row_begin) return;
-  uint64_t blocks = ceil_div(g.row_end - g.row_begin, 8);
-  const uint64_t cap = static_cast<uint64_t>(sms()) * 8;
-  if (blocks > cap) blocks = cap;
+  const uint64_t blocks = ceil_div(g.row_end - g.row_begin, 8);  // one row per warp
   emit_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(bitmap, g, rowcnt, rowstart, out, capacity);
   note_launch();
 }

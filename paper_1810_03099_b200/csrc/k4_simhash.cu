@@ -42,8 +42,9 @@ struct __align__(16) Staged {
 __global__ void __launch_bounds__(256) simhash_kernel(SimhashArgs a) {
   __shared__ Staged stage[8][32];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t d = blockIdx.x * (blockDim.x >> 5) + wid; d < a.n_docs; d += nwarps) {
+  const uint32_t d = blockIdx.x * (blockDim.x >> 5) + wid;  // one document per warp
+  if (d >= a.n_docs) return;
+  {
     const uint2* __restrict__ e = a.ent + a.doc_off[d];
     const uint32_t n = a.nnz[d];
     double s1a = 0.0, s1b = 0.0, tot = 0.0;
@@ -83,12 +84,7 @@ __global__ void __launch_bounds__(256) simhash_kernel(SimhashArgs a) {
 
 void launch_simhash(const SimhashArgs& a, cudaStream_t s) {
   if (a.n_docs == 0) return;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  uint64_t blocks = ceil_div(a.n_docs, 8);
-  const uint64_t cap = static_cast<uint64_t>(sms) * 8;
-  if (blocks > cap) blocks = cap;
+  const uint64_t blocks = ceil_div(a.n_docs, 8);
   simhash_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(a);
   note_launch();
 }
