@@ -95,7 +95,9 @@ struct refsig_gpu_ctx {
   DevBuf tiny_docs, chunks[2], chunk_cnt, chunk_scratch, mdocs[kMergeClasses];
   uint32_t n_tiny = 0, n_chunks[2] = {0, 0}, n_mdocs[kMergeClasses] = {};
   DevBuf long_docs, long_off, long_scratch;
-  DevBuf order;  // docs by decreasing length (per-doc kernels take long docs first)
+  DevBuf sign_segs;  // K2 plan: {doc, segment} by decreasing doc length
+  uint32_t n_sign_segs = 0;
+  DevBuf sign_part, sign_part_sq, sign_arrive;  // K2 multi-segment partials + arrival counters
   uint32_t n_long = 0;
 
   // K1
@@ -428,12 +430,25 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
     buf.ensure(bytes);
     ck(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, c->stream), "H2D plan");
   };
+  // K2 plan: every document gets ceil(tokens/256) segments (nnz <= tokens;
+  // segments past the document's nonzeros exit at once), longest docs first.
   std::vector<uint32_t> order(n_docs);
   for (uint32_t d = 0; d < n_docs; ++d) order[d] = d;
   std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
     return doc_off[x + 1] - doc_off[x] > doc_off[y + 1] - doc_off[y];
   });
-  up(c->order, order.data(), 4ull * n_docs);
+  std::vector<uint2> segs;
+  segs.reserve(n_docs + c->n_tokens / kSignSegRows);
+  for (uint32_t d : order) {
+    const uint64_t m = std::max<uint64_t>(1, ceil_div(doc_off[d + 1] - doc_off[d], kSignSegRows));
+    for (uint64_t t = 0; t < m; ++t) segs.push_back(make_uint2(d, static_cast<uint32_t>(t)));
+  }
+  require(segs.size() < (1ull << 32), "too many K2 segments");
+  c->n_sign_segs = static_cast<uint32_t>(segs.size());
+  up(c->sign_segs, segs.data(), sizeof(uint2) * segs.size());
+  c->sign_part_sq.ensure(sizeof(float) * segs.size());
+  c->sign_arrive.ensure(sizeof(uint32_t) * n_docs);
+  ck(cudaMemsetAsync(c->sign_arrive.p, 0, sizeof(uint32_t) * n_docs, c->stream), "memset arrive");
   c->n_tiny = static_cast<uint32_t>(tiny.size());
   up(c->tiny_docs, tiny.data(), 4 * tiny.size());
   for (int k = 0; k < 2; ++k) {
@@ -789,9 +804,11 @@ static void do_sign(refsig_gpu_ctx* ctx) {
        "memset ST pad");
   ctx->inv_norm.ensure(sizeof(float) * N);
   if (ctx->db) ck(cudaStreamSynchronize(ctx->db->stream), "sync database");
+  ctx->sign_part.ensure(sizeof(float) * static_cast<size_t>(ctx->n_sign_segs) * refc->Kp);
   SignArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->info.as<TermInfo>(),
-             refc->R.as<float>(), N, K, refc->Kp, ctx->order.as<uint32_t>(), ctx->S.as<float>(),
-             ctx->ST.as<float>(), ld, ctx->inv_norm.as<float>()};
+             refc->R.as<float>(), N, K, refc->Kp, ctx->sign_segs.as<uint2>(), ctx->n_sign_segs,
+             ctx->sign_part.as<float>(), ctx->sign_part_sq.as<float>(), ctx->sign_arrive.as<uint32_t>(),
+             ctx->S.as<float>(), ctx->ST.as<float>(), ld, ctx->inv_norm.as<float>()};
   {
     Phase ph(ctx, REFSIG_PHASE_SIGN);
     launch_sign(a, ctx->stream);

@@ -104,6 +104,10 @@ struct MrcArgs {
   uint32_t* rowcnt;
 };
 
+// KC > 0: every K chunk has exactly KC columns (K <= 32 with K == KC, or
+// K % 32 == 0 with KC == 32), so the k loop is fully unrolled; KC == 0 is the
+// general path.
+template <int KC>
 __global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel(MrcArgs a) {
   extern __shared__ __align__(16) float smem[];
   const uint32_t kc_max = a.K < kKC ? a.K : kKC;
@@ -193,17 +197,11 @@ __global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel(MrcArgs a) {
       flush();
       pending = false;
     }
-    if (chunk == 0) {  // accumulate dot - tau: the match bit is the inverted sign bit
-#pragma unroll
-      for (int r = 0; r < 8; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = make_float2(-a.tau, -a.tau);
-    }
-    const uint32_t kc = min(static_cast<uint32_t>(kKC), a.K - chunk * kKC);
     const float* A = smem + 2 * st * panel;
     const float* B = A + panel;
-#pragma unroll 4
-    for (uint32_t k = 0; k < kc; ++k) {
+    // one k step: 2+2 LDS.128, 32 FFMA2; `first` starts the dot at -tau (the
+    // match bit is then the inverted sign bit) without separate moves
+    auto kstep = [&](uint32_t k, bool first) {
       const float4 a0 = *reinterpret_cast<const float4*>(A + k * kTile + ty * 4);
       const float4 a1 = *reinterpret_cast<const float4*>(A + k * kTile + 64 + ty * 4);
       const float4 b0 = *reinterpret_cast<const float4*>(B + k * kTile + tx * 4);
@@ -211,10 +209,27 @@ __global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel(MrcArgs a) {
       const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
       const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
                             make_float2(b1.z, b1.w)};
+      const float2 nt = make_float2(-a.tau, -a.tau);
 #pragma unroll
       for (int r = 0; r < 8; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = ffma2(av[r], bv[c], acc[r][c]);
+        for (int c = 0; c < 4; ++c) acc[r][c] = ffma2(av[r], bv[c], first ? nt : acc[r][c]);
+    };
+    if constexpr (KC > 0) {
+      if (chunk == 0) {
+        kstep(0, true);
+#pragma unroll
+        for (uint32_t k = 1; k < KC; ++k) kstep(k, false);
+      } else {
+#pragma unroll
+        for (uint32_t k = 0; k < KC; ++k) kstep(k, false);
+      }
+    } else {
+      const uint32_t kc = min(static_cast<uint32_t>(kKC), a.K - chunk * kKC);
+      uint32_t k = 0;
+      if (chunk == 0) kstep(k++, true);
+#pragma unroll 4
+      for (; k < kc; ++k) kstep(k, false);
     }
     if (chunk + 1 == nchunks) {
       // Row ty*8+r, columns tx*8..+7 -> byte tx of the tile row (natural
@@ -360,13 +375,28 @@ void launch_mrc_bitmap(const float* ST_rows, uint32_t ld_rows, const float* ST_c
   const size_t smem = (6ull * kc * kTile) * sizeof(float) + 2 * 2048;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(mrc_bitmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * kKC * kTile * 4 + 4096);
+    const int mx = 6 * kKC * kTile * 4 + 4096;
+    cudaFuncSetAttribute(mrc_bitmap_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(mrc_bitmap_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(mrc_bitmap_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(mrc_bitmap_kernel<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(mrc_bitmap_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     configured = true;
   }
   uint64_t grid = static_cast<uint64_t>(sms()) * 2;
   if (grid > t) grid = t;
   MrcArgs a{ST_rows, ST_cols, ld_rows, ld_cols, K, tau, g, nbr, nbc, t, bitmap, rowcnt};
-  mrc_bitmap_kernel<<<static_cast<unsigned>(grid), 256, smem, s>>>(a);
+  const dim3 gr(static_cast<unsigned>(grid));
+  if (K == 20)
+    mrc_bitmap_kernel<20><<<gr, 256, smem, s>>>(a);
+  else if (K == 10)
+    mrc_bitmap_kernel<10><<<gr, 256, smem, s>>>(a);
+  else if (K == 16)
+    mrc_bitmap_kernel<16><<<gr, 256, smem, s>>>(a);
+  else if (K % 32 == 0)
+    mrc_bitmap_kernel<32><<<gr, 256, smem, s>>>(a);
+  else
+    mrc_bitmap_kernel<0><<<gr, 256, smem, s>>>(a);
   note_launch();
 }
 

@@ -99,12 +99,17 @@ struct SignArgs {
   uint32_t n_docs;
   uint32_t K;
   uint32_t Kp;           // row stride of R
-  const uint32_t* order; // docs in longest-first order (load balance)
+  const uint2* segs;     // {doc, segment}: 256-nonzero segments, longest docs first (k2_sign.cu)
+  uint32_t n_segs;
+  float* part;           // [n_segs*Kp] per-segment column sums (multi-segment docs)
+  float* part_sq;        // [n_segs] per-segment ||w||^2
+  uint32_t* arrive;      // [n_docs] segment arrival counters (zero between launches)
   float* S;         // [n_docs*K] raw cosines, row-major (API output)
   float* ST;        // [K][ld] unit-normalised signatures, transposed (K3 operand; 0 if all-zero)
   uint32_t ld;      // leading dimension of ST (n_docs rounded up to 128; pad columns zero)
   float* inv_norm;  // [n_docs] 1/||w_d||
 };
+constexpr uint32_t kSignSegRows = 256;  // nonzeros per K2 segment
 void launch_sign(const SignArgs& a, cudaStream_t s);
 
 // ---- K3 / K4b pair bitmaps --------------------------------------------------
