@@ -110,41 +110,42 @@ struct MrcArgs {
 template <int KC>
 __global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel(MrcArgs a) {
   extern __shared__ __align__(16) float smem[];
-  const uint32_t kc_max = a.K < kKC ? a.K : kKC;
-  const uint32_t panel = kc_max * kTile;  // floats per panel stage
+  const uint32_t kcm = KC > 0 ? static_cast<uint32_t>(KC) : (a.K < kKC ? a.K : kKC);  // columns per chunk
+  const uint32_t panel = kcm * kTile;  // floats per panel stage
   // stage st: A panel at smem + 2*st*panel, B panel right after it
 
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
-  const uint64_t t_begin = a.n_tiles * blockIdx.x / gridDim.x;
-  const uint64_t t_end = a.n_tiles * (blockIdx.x + 1) / gridDim.x;
+  const uint32_t t_begin = static_cast<uint32_t>(a.n_tiles * blockIdx.x / gridDim.x);
+  const uint32_t t_end = static_cast<uint32_t>(a.n_tiles * (blockIdx.x + 1) / gridDim.x);
   if (t_begin >= t_end) return;
-  const uint32_t nchunks = (a.K + kKC - 1) / kKC;
-  const uint64_t items = (t_end - t_begin) * nchunks;
+  const uint32_t nchunks = KC > 0 ? (a.K / KC) : (a.K + kKC - 1) / kKC;
+  const uint32_t items = (t_end - t_begin) * nchunks;
 
   uint32_t bi, bj;
-  tile_coords(static_cast<uint32_t>(t_begin) + a.g.tile0, a.nbr, a.nbc, a.g.triangle, bi, bj);
-  // issue the loads of item `it` (tile t_begin + it / nchunks, chunk it % nchunks) into stage st
+  tile_coords(t_begin + a.g.tile0, a.nbr, a.nbc, a.g.triangle, bi, bj);
   uint32_t li = bi, lj = bj;  // tile coords of the next item to load
   uint32_t lchunk = 0;
-  // cp.async slots of one stage: 16-byte chunk m = tid%32 of panel rows
-  // tid/32 + 8u (A rows first, then B rows); offsets are tile-invariant.
-  constexpr int kSlots = 2 * kKC / 8;
+  // cp.async slots of one stage: 16-byte chunk cm = tid%32 of panel rows
+  // kr + 8u, kr = warp id (A rows first, then B rows): every slot condition
+  // is warp-uniform and the offsets are tile-invariant.
+  constexpr int kSlots = KC > 0 ? (2 * KC + 7) / 8 : 2 * kKC / 8;
   const uint32_t cm = tid & 31, kr = tid >> 5, sp = split_pos(4 * cm);
-  auto issue = [&](int st) {
-    const uint32_t k0 = lchunk * kKC;
-    const uint32_t kc = min(static_cast<uint32_t>(kKC), a.K - k0);
+  auto issue = [&](uint32_t st) {
+    const uint32_t k0 = lchunk * kcm;
+    const uint32_t kc = KC > 0 ? static_cast<uint32_t>(KC) : min(kcm, a.K - k0);
     const float* baseA = a.STr + static_cast<size_t>(k0) * a.ldr + li * kTile + 4 * cm;
     const float* baseB = a.STc + static_cast<size_t>(k0) * a.ldc + lj * kTile + 4 * cm;
     float* sbase = smem + 2 * st * panel + sp;
 #pragma unroll
     for (int u = 0; u < kSlots; ++u) {
       const uint32_t k = kr + 8 * u;
-      const bool isB = k >= kc_max;
-      const uint32_t kk = isB ? k - kc_max : k;
-      if (k < 2 * kc_max && kk < kc)
-        cp_async16(sbase + (isB ? panel : 0u) + kk * kTile,
-                   isB ? baseB + static_cast<size_t>(kk) * a.ldc : baseA + static_cast<size_t>(kk) * a.ldr);
+      if (k < kcm) {
+        if (KC > 0 || k < kc) cp_async16(sbase + k * kTile, baseA + static_cast<size_t>(k) * a.ldr);
+      } else if (k < 2 * kcm) {
+        const uint32_t kk = k - kcm;
+        if (KC > 0 || kk < kc) cp_async16(sbase + panel + kk * kTile, baseB + static_cast<size_t>(kk) * a.ldc);
+      }
     }
     cp_async_commit();
     if (++lchunk == nchunks) {
@@ -184,15 +185,17 @@ __global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel(MrcArgs a) {
   issue(0);
   if (items > 1) issue(1);
   uint32_t tiles_done = 0;
-  for (uint64_t it = 0; it < items; ++it) {
-    const int st = static_cast<int>(it % 3);
-    const uint32_t chunk = static_cast<uint32_t>(it % nchunks);
+  uint32_t st = 0, ist = 2, chunk = 0;  // stage of item it, stage for item it+2, chunk of item it
+  for (uint32_t it = 0; it < items; ++it) {
     if (it + 1 < items)
       cp_async_wait<1>();
     else
       cp_async_wait<0>();
     __syncthreads();
-    if (it + 2 < items) issue(static_cast<int>((it + 2) % 3));
+    if (it + 2 < items) {
+      issue(ist);
+      ist = ist == 2 ? 0 : ist + 1;
+    }
     if (pending) {
       flush();
       pending = false;
@@ -216,22 +219,24 @@ __global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel(MrcArgs a) {
         for (int c = 0; c < 4; ++c) acc[r][c] = ffma2(av[r], bv[c], first ? nt : acc[r][c]);
     };
     if constexpr (KC > 0) {
-      if (chunk == 0) {
+      if (KC == static_cast<int>(kKC) && chunk != 0) {  // later chunks of K % 32 == 0
+#pragma unroll
+        for (uint32_t k = 0; k < KC; ++k) kstep(k, false);
+      } else {
         kstep(0, true);
 #pragma unroll
         for (uint32_t k = 1; k < KC; ++k) kstep(k, false);
-      } else {
-#pragma unroll
-        for (uint32_t k = 0; k < KC; ++k) kstep(k, false);
       }
     } else {
-      const uint32_t kc = min(static_cast<uint32_t>(kKC), a.K - chunk * kKC);
+      const uint32_t kc = min(kcm, a.K - chunk * kcm);
       uint32_t k = 0;
       if (chunk == 0) kstep(k++, true);
 #pragma unroll 4
       for (; k < kc; ++k) kstep(k, false);
     }
-    if (chunk + 1 == nchunks) {
+    st = st == 2 ? 0 : st + 1;
+    if (++chunk == nchunks) {
+      chunk = 0;
       // Row ty*8+r, columns tx*8..+7 -> byte tx of the tile row (natural
       // column order). acc = dot - tau, so bit = NOT sign(acc) (acc is never
       // -0: it starts at -tau and adds non-negative products); funnel shifts
