@@ -94,6 +94,7 @@ struct refsig_gpu_ctx {
   const uint32_t* tok = nullptr;
   DevBuf tiny_docs, chunks[2], chunk_cnt, chunk_scratch, mdocs[kMergeClasses];
   uint32_t n_tiny = 0, n_chunks[2] = {0, 0}, n_mdocs[kMergeClasses] = {};
+  uint32_t n_chunks_long = 0;  // chunks[1][0, n_chunks_long): docs of merge classes 2 and 3
   DevBuf long_docs, long_off, long_scratch;
   DevBuf sign_segs;  // K2 plan: {doc, segment} by decreasing doc length
   uint32_t n_sign_segs = 0;
@@ -412,11 +413,9 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
     } else if (len <= kMergeChunk) {
       chunks[1].push_back(make_uint2(d, (1u << 16) | 1u));
     } else if (len <= kMergeMax) {
-      const uint32_t m = static_cast<uint32_t>(ceil_div(len, kMergeChunk));
       int cls = 0;
       while (len > kMergeCap[cls]) ++cls;
-      mdocs[cls].push_back(static_cast<uint32_t>(chunks[1].size()));
-      for (uint32_t q = 0; q < m; ++q) chunks[1].push_back(make_uint2(d, (m << 16) | (q << 1)));
+      mdocs[cls].push_back(d);  // doc ids for now; chunk indices below
     } else {
       longs.push_back(d);
       loff.push_back(scratch);
@@ -451,15 +450,36 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
   ck(cudaMemsetAsync(c->sign_arrive.p, 0, sizeof(uint32_t) * n_docs, c->stream), "memset arrive");
   c->n_tiny = static_cast<uint32_t>(tiny.size());
   up(c->tiny_docs, tiny.data(), 4 * tiny.size());
+  // 512-token chunks of merged docs: the two longest classes first (their
+  // sorts and merges run on their own streams from the fork, see do_count),
+  // then the direct 257..512 docs, then the two shorter classes. Longest docs
+  // first within a class; mdocs[k] become first-chunk indices.
+  {
+    std::vector<uint2> direct = std::move(chunks[1]);
+    chunks[1].clear();
+    auto add_class = [&](int k) {
+      std::stable_sort(mdocs[k].begin(), mdocs[k].end(), [&](uint32_t x, uint32_t y) {
+        return doc_off[x + 1] - doc_off[x] > doc_off[y + 1] - doc_off[y];
+      });
+      for (uint32_t& d : mdocs[k]) {
+        const uint32_t m = static_cast<uint32_t>(ceil_div(doc_off[d + 1] - doc_off[d], kMergeChunk));
+        const uint32_t first = static_cast<uint32_t>(chunks[1].size());
+        for (uint32_t q = 0; q < m; ++q) chunks[1].push_back(make_uint2(d, (m << 16) | (q << 1)));
+        d = first;
+      }
+    };
+    add_class(3);
+    add_class(2);
+    c->n_chunks_long = static_cast<uint32_t>(chunks[1].size());
+    chunks[1].insert(chunks[1].end(), direct.begin(), direct.end());
+    add_class(1);
+    add_class(0);
+  }
   for (int k = 0; k < 2; ++k) {
     c->n_chunks[k] = static_cast<uint32_t>(chunks[k].size());
     up(c->chunks[k], chunks[k].data(), sizeof(uint2) * chunks[k].size());
   }
   for (int k = 0; k < kMergeClasses; ++k) {
-    // longest docs first within a merge class
-    std::stable_sort(mdocs[k].begin(), mdocs[k].end(), [&](uint32_t x, uint32_t y) {
-      return (chunks[1][x].y >> 16) > (chunks[1][y].y >> 16);
-    });
     c->n_mdocs[k] = static_cast<uint32_t>(mdocs[k].size());
     up(c->mdocs[k], mdocs[k].data(), 4 * mdocs[k].size());
   }
@@ -603,22 +623,31 @@ static void do_count(refsig_gpu_ctx* ctx, int weight_mode) {
   CountArgs a{ctx->tok, ctx->doc_off.as<uint64_t>(), V, ctx->ent.as<uint2>(), ctx->nnz.as<uint32_t>(),
               ctx->df_rep.as<uint32_t>(), reps, ctx->flags.as<uint32_t>(), ctx->chunk_scratch.as<uint2>(),
               ctx->chunk_cnt.as<uint32_t>()};
-  // fork: the 512-token chunk sorts (critical path, then the merges) on the
-  // main stream; tiny docs, 256-key docs and long docs on side[0]; merge
-  // classes spread over all four streams once the chunks are sorted.
+  // fork: side[1] sorts the chunks of the longest docs (merge classes 2, 3)
+  // and merges them, in parallel with the bulk of the 512-token chunk sorts
+  // on the main stream (then merge classes 0, 1); tiny docs, 256-key docs and
+  // > 8192-token docs on side[0]. The long-doc merges are latency-bound (one
+  // CTA per doc), so they start as early as possible.
   cudaStream_t m0 = ctx->stream;
   ck(cudaEventRecord(ctx->ev_fork, m0), "fork");
   for (int k = 0; k < 3; ++k) ck(cudaStreamWaitEvent(ctx->side[k], ctx->ev_fork, 0), "fork");
-  launch_count_chunks(16, a, ctx->chunks[1].as<uint2>(), ctx->n_chunks[1], m0);
-  ck(cudaEventRecord(ctx->ev_mid, m0), "mid");
+  const uint32_t nl = ctx->n_chunks_long;
+  launch_count_chunks(16, a, ctx->chunks[1].as<uint2>(), nl, ctx->side[1]);
+  ck(cudaEventRecord(ctx->ev_mid, ctx->side[1]), "mid");
+  ck(cudaStreamWaitEvent(ctx->side[2], ctx->ev_mid, 0), "mid");
+  launch_count_merge(3, a, ctx->chunks[1].as<uint2>(), ctx->mdocs[3].as<uint32_t>(), ctx->n_mdocs[3], ctx->side[1]);
+  launch_count_merge(2, a, ctx->chunks[1].as<uint2>(), ctx->mdocs[2].as<uint32_t>(), ctx->n_mdocs[2], ctx->side[2]);
+  {
+    CountArgs b = a;  // chunk_sort indexes chunk_cnt by its own chunk index
+    b.chunk_cnt += nl;
+    launch_count_chunks(16, b, ctx->chunks[1].as<uint2>() + nl, ctx->n_chunks[1] - nl, m0);
+  }
   launch_count_tiny(a, ctx->tiny_docs.as<uint32_t>(), ctx->n_tiny, ctx->side[0]);
   launch_count_chunks(8, a, ctx->chunks[0].as<uint2>(), ctx->n_chunks[0], ctx->side[0]);
   launch_count_large(a, ctx->long_docs.as<uint32_t>(), ctx->long_off.as<uint64_t>(), ctx->n_long,
                      ctx->long_scratch.as<uint32_t>(), ctx->side[0]);
-  cudaStream_t ms[kMergeClasses] = {ctx->side[0], ctx->side[1], ctx->side[2], m0};
-  for (int k = 0; k < 3; ++k) ck(cudaStreamWaitEvent(ctx->side[k], ctx->ev_mid, 0), "mid");
-  for (int k = kMergeClasses - 1; k >= 0; --k)
-    launch_count_merge(k, a, ctx->chunks[1].as<uint2>(), ctx->mdocs[k].as<uint32_t>(), ctx->n_mdocs[k], ms[k]);
+  launch_count_merge(1, a, ctx->chunks[1].as<uint2>(), ctx->mdocs[1].as<uint32_t>(), ctx->n_mdocs[1], m0);
+  launch_count_merge(0, a, ctx->chunks[1].as<uint2>(), ctx->mdocs[0].as<uint32_t>(), ctx->n_mdocs[0], m0);
   for (int k = 0; k < 3; ++k) {  // join
     ck(cudaEventRecord(ctx->ev_join[k], ctx->side[k]), "join");
     ck(cudaStreamWaitEvent(m0, ctx->ev_join[k], 0), "join");

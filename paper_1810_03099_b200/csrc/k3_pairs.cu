@@ -326,19 +326,51 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
     uint64_t base = rowstart[i];
     const uint32_t* row = bitmap + static_cast<size_t>(i) * g.words_per_row;
     const uint32_t wbeg = g.triangle ? (i / kTile) * 4 : 0;
-    for (uint32_t c = wbeg; c < g.words_per_row && remaining; c += 32) {
+    const uint32_t wpr = g.words_per_row;
+    const uint64_t hi = static_cast<uint64_t>(i) << 32;
+    // the next batch's word is loaded before this batch is expanded, so the
+    // load latency overlaps the expansion
+    uint32_t word_next = wbeg + lane < wpr ? row[wbeg + lane] : 0u;
+    for (uint32_t c = wbeg; c < wpr && remaining; c += 32) {
       const uint32_t wi = c + lane;
-      uint32_t word = wi < g.words_per_row ? row[wi] : 0u;
+      uint32_t word = word_next;
+      word_next = c + 32 + lane < wpr ? row[c + 32 + lane] : 0u;
       const uint32_t n = __popc(word);
       const uint32_t inc = warp_inclusive_scan(n, lane);
       const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-      uint64_t pos = base + inc - n;
-      const uint64_t hi = static_cast<uint64_t>(i) << 32;
-      while (word) {
-        const int b = __ffs(word) - 1;
-        word &= word - 1;
-        if (pos < capacity) out[pos] = hi | (wi * 32u + b);
-        ++pos;
+      if (base + tot <= capacity) {  // common case: no per-key capacity checks
+        // Two expansions with warp-uniform trip counts; take the shorter:
+        // (a) every lane walks its own word's bits (max popcount iterations);
+        // (b) the warp walks the nonzero words and lane l tests bit l (one
+        //     iteration per nonzero word: dense near-duplicate clusters).
+        const uint32_t maxn = __reduce_max_sync(0xffffffffu, n);
+        const uint32_t nzmask = __ballot_sync(0xffffffffu, word != 0u);
+        if (maxn <= static_cast<uint32_t>(__popc(nzmask))) {
+          uint64_t* o = out + base + (inc - n);
+          const uint32_t col = wi * 32u;
+          while (word) {
+            const int b = __ffs(word) - 1;
+            word &= word - 1;
+            *o++ = hi | (col + b);
+          }
+        } else {
+          uint64_t* o = out + base;
+          const uint32_t lt = (1u << lane) - 1u, ex = inc - n;
+          for (uint32_t m = nzmask; m; m &= m - 1) {
+            const int w = __ffs(m) - 1;
+            const uint32_t wv = __shfl_sync(0xffffffffu, word, w);
+            const uint32_t e = __shfl_sync(0xffffffffu, ex, w);
+            if ((wv >> lane) & 1u) o[e + __popc(wv & lt)] = hi | ((c + w) * 32u + lane);
+          }
+        }
+      } else {
+        uint64_t pos = base + inc - n;
+        while (word) {
+          const int b = __ffs(word) - 1;
+          word &= word - 1;
+          if (pos < capacity) out[pos] = hi | (wi * 32u + b);
+          ++pos;
+        }
       }
       base += tot;
       remaining -= tot;

@@ -94,26 +94,57 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t
   if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = partial[nb];
 }
 
-// n <= kSmallScan: one CTA, each thread scans a contiguous run of <= 32 values.
-constexpr uint64_t kSmallScan = kScanThreads * 32;
+// n <= kSmallScan: one 256-thread CTA per tile of 1024 values (thread t owns
+// values 4t..4t+3: one 16-byte load, two 16-byte stores). Each CTA first
+// reduces all values before its tile itself (<= 128 KB of L2-resident reads),
+// so the tiles are independent: one launch, no serial chain across CTAs.
+constexpr uint64_t kSmallScan = 32768;
+constexpr int kSmallThreads = 256;
+constexpr uint32_t kSmallTile = 4 * kSmallThreads;
 
-__global__ void __launch_bounds__(kScanThreads) scan_small_kernel(const uint32_t* __restrict__ in, uint64_t n,
-                                                                  uint64_t* __restrict__ out) {
+__device__ __forceinline__ uint4 load4(const uint32_t* __restrict__ in, uint32_t i, uint32_t n) {
+  if (i + 4 <= n) return __ldg(reinterpret_cast<const uint4*>(in + i));
+  uint4 v = make_uint4(0u, 0u, 0u, 0u);
+  if (i < n) v.x = in[i];
+  if (i + 1 < n) v.y = in[i + 1];
+  if (i + 2 < n) v.z = in[i + 2];
+  return v;
+}
+
+__global__ void __launch_bounds__(kSmallThreads) scan_small_kernel(const uint32_t* __restrict__ in, uint64_t n,
+                                                                   uint64_t* __restrict__ out) {
   __shared__ uint64_t sh[33];
-  const uint32_t per = static_cast<uint32_t>((n + kScanThreads - 1) / kScanThreads);
-  const uint64_t lo = static_cast<uint64_t>(threadIdx.x) * per;
-  uint64_t s = 0;
-  for (uint32_t k = 0; k < per; ++k)
-    if (lo + k < n) s += in[lo + k];
-  uint64_t tot;
-  uint64_t off = block_exscan_u64(s, sh, &tot);
-  for (uint32_t k = 0; k < per; ++k)
-    if (lo + k < n) {
-      const uint64_t v = in[lo + k];
-      out[lo + k] = off;
-      off += v;
+  const uint32_t nn = static_cast<uint32_t>(n);
+  const uint32_t t0 = blockIdx.x * kSmallTile;
+  const uint32_t i = t0 + threadIdx.x * 4;
+  const uint4 v = load4(in, i, nn);
+  // prefix = sum of in[0 .. t0): 4 independent 16-byte loads per step
+  uint64_t pre = 0;
+  for (uint32_t j0 = threadIdx.x * 4; j0 < t0; j0 += 4 * kSmallTile) {
+    uint4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t j = j0 + u * kSmallTile;
+      x[u] = j < t0 ? __ldg(reinterpret_cast<const uint4*>(in + j)) : make_uint4(0u, 0u, 0u, 0u);
     }
-  if (threadIdx.x == 0) out[n] = tot;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) pre += static_cast<uint64_t>(x[u].x) + x[u].y + x[u].z + x[u].w;
+  }
+  uint64_t pre_tot;
+  block_exscan_u64(pre, sh, &pre_tot);
+  const uint64_t s = static_cast<uint64_t>(v.x) + v.y + v.z + v.w;
+  uint64_t tot;
+  const uint64_t o0 = pre_tot + block_exscan_u64(s, sh, &tot);
+  const uint64_t o1 = o0 + v.x, o2 = o1 + v.y, o3 = o2 + v.z;
+  if (i + 4 <= nn) {
+    reinterpret_cast<ulonglong2*>(out + i)[0] = make_ulonglong2(o0, o1);
+    reinterpret_cast<ulonglong2*>(out + i)[1] = make_ulonglong2(o2, o3);
+  } else {
+    if (i < nn) out[i] = o0;
+    if (i + 1 < nn) out[i + 1] = o1;
+    if (i + 2 < nn) out[i + 2] = o2;
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = pre_tot + tot;
 }
 
 }  // namespace
@@ -127,7 +158,7 @@ void launch_exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_
     return;
   }
   if (n <= kSmallScan) {
-    scan_small_kernel<<<1, kScanThreads, 0, s>>>(in, n, out);
+    scan_small_kernel<<<static_cast<unsigned>(ceil_div(n, kSmallTile)), kSmallThreads, 0, s>>>(in, n, out);
     note_launch();
     return;
   }
