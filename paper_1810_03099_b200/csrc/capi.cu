@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -95,10 +96,10 @@ struct refsig_gpu_ctx {
   DevBuf tiny_docs, chunks[2], chunk_cnt, chunk_scratch, mdocs[kMergeClasses];
   uint32_t n_tiny = 0, n_chunks[2] = {0, 0}, n_mdocs[kMergeClasses] = {};
   uint32_t n_chunks_long = 0;  // chunks[1][0, n_chunks_long): docs of merge classes 2 and 3
+  bool k1_group = true;        // 513..8192-token docs: CTA group sorts (else chunk sorts + merges)
   DevBuf long_docs, long_off, long_scratch;
-  DevBuf sign_segs;  // K2 plan: {doc, segment} by decreasing doc length
-  uint32_t n_sign_segs = 0;
-  DevBuf sign_part, sign_part_sq, sign_arrive;  // K2 multi-segment partials + arrival counters
+  DevBuf order;             // docs by decreasing length (K2 plan)
+  uint32_t n_sign_long = 0;  // order[0, n_sign_long): > kSignLongTokens tokens, one CTA each in K2
   uint32_t n_long = 0;
 
   // K1
@@ -429,25 +430,17 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
     buf.ensure(bytes);
     ck(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, c->stream), "H2D plan");
   };
-  // K2 plan: every document gets ceil(tokens/256) segments (nnz <= tokens;
-  // segments past the document's nonzeros exit at once), longest docs first.
+  // K2 plan: documents longest first; the long ones get a CTA each
   std::vector<uint32_t> order(n_docs);
   for (uint32_t d = 0; d < n_docs; ++d) order[d] = d;
   std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
     return doc_off[x + 1] - doc_off[x] > doc_off[y + 1] - doc_off[y];
   });
-  std::vector<uint2> segs;
-  segs.reserve(n_docs + c->n_tokens / kSignSegRows);
-  for (uint32_t d : order) {
-    const uint64_t m = std::max<uint64_t>(1, ceil_div(doc_off[d + 1] - doc_off[d], kSignSegRows));
-    for (uint64_t t = 0; t < m; ++t) segs.push_back(make_uint2(d, static_cast<uint32_t>(t)));
-  }
-  require(segs.size() < (1ull << 32), "too many K2 segments");
-  c->n_sign_segs = static_cast<uint32_t>(segs.size());
-  up(c->sign_segs, segs.data(), sizeof(uint2) * segs.size());
-  c->sign_part_sq.ensure(sizeof(float) * segs.size());
-  c->sign_arrive.ensure(sizeof(uint32_t) * n_docs);
-  ck(cudaMemsetAsync(c->sign_arrive.p, 0, sizeof(uint32_t) * n_docs, c->stream), "memset arrive");
+  c->n_sign_long = 0;
+  while (c->n_sign_long < n_docs &&
+         doc_off[order[c->n_sign_long] + 1] - doc_off[order[c->n_sign_long]] > kSignLongTokens)
+    ++c->n_sign_long;
+  up(c->order, order.data(), 4ull * n_docs);
   c->n_tiny = static_cast<uint32_t>(tiny.size());
   up(c->tiny_docs, tiny.data(), 4 * tiny.size());
   // 512-token chunks of merged docs: the two longest classes first (their
@@ -461,6 +454,7 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
       std::stable_sort(mdocs[k].begin(), mdocs[k].end(), [&](uint32_t x, uint32_t y) {
         return doc_off[x + 1] - doc_off[x] > doc_off[y + 1] - doc_off[y];
       });
+      if (c->k1_group) return;  // group sorts take doc ids
       for (uint32_t& d : mdocs[k]) {
         const uint32_t m = static_cast<uint32_t>(ceil_div(doc_off[d + 1] - doc_off[d], kMergeChunk));
         const uint32_t first = static_cast<uint32_t>(chunks[1].size());
@@ -498,6 +492,10 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
   reset_downstream(c);
 }
 
+// R row stride: K <= 32 -> roundup(K,4) (float4 rows, lane-per-hit K2);
+// K > 32 -> roundup(K,32) (column-owner K2 reads lane-indexed columns).
+uint32_t ref_row_stride(uint32_t K) { return K <= 32 ? (K + 3) & ~3u : (K + 31) & ~31u; }
+
 PairGrid self_grid(const refsig_gpu_ctx* c) {
   return PairGrid{c->n_docs, c->n_docs, words_per_row(c->n_docs), true, 0, c->n_docs, 0};
 }
@@ -520,6 +518,7 @@ int refsig_gpu_create(int device, refsig_gpu_ctx** out) {
   refsig_gpu_ctx* c = new (std::nothrow) refsig_gpu_ctx();
   if (!c) return REFSIG_E_RUNTIME;
   c->device = device;
+  if (const char* m = std::getenv("REFSIG_K1_MODE")) c->k1_group = std::string(m) != "merge";
   bool ok = cudaSetDevice(device) == cudaSuccess &&
             cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) == cudaSuccess &&
             cudaMallocHost(&c->h_pin, 64) == cudaSuccess &&
@@ -631,6 +630,18 @@ static void do_count(refsig_gpu_ctx* ctx, int weight_mode) {
   cudaStream_t m0 = ctx->stream;
   ck(cudaEventRecord(ctx->ev_fork, m0), "fork");
   for (int k = 0; k < 3; ++k) ck(cudaStreamWaitEvent(ctx->side[k], ctx->ev_fork, 0), "fork");
+  if (ctx->k1_group) {
+    // classes 3, 2 on side[1], side[2]; 1, 0 after the 512-key sorts on main
+    launch_count_group(3, a, ctx->mdocs[3].as<uint32_t>(), ctx->n_mdocs[3], ctx->side[1]);
+    launch_count_group(2, a, ctx->mdocs[2].as<uint32_t>(), ctx->n_mdocs[2], ctx->side[2]);
+    launch_count_group(1, a, ctx->mdocs[1].as<uint32_t>(), ctx->n_mdocs[1], m0);
+    launch_count_group(0, a, ctx->mdocs[0].as<uint32_t>(), ctx->n_mdocs[0], m0);
+    launch_count_chunks(16, a, ctx->chunks[1].as<uint2>(), ctx->n_chunks[1], m0);
+    launch_count_tiny(a, ctx->tiny_docs.as<uint32_t>(), ctx->n_tiny, ctx->side[0]);
+    launch_count_chunks(8, a, ctx->chunks[0].as<uint2>(), ctx->n_chunks[0], ctx->side[0]);
+    launch_count_large(a, ctx->long_docs.as<uint32_t>(), ctx->long_off.as<uint64_t>(), ctx->n_long,
+                       ctx->long_scratch.as<uint32_t>(), ctx->side[0]);
+  } else {
   const uint32_t nl = ctx->n_chunks_long;
   launch_count_chunks(16, a, ctx->chunks[1].as<uint2>(), nl, ctx->side[1]);
   ck(cudaEventRecord(ctx->ev_mid, ctx->side[1]), "mid");
@@ -648,6 +659,7 @@ static void do_count(refsig_gpu_ctx* ctx, int weight_mode) {
                      ctx->long_scratch.as<uint32_t>(), ctx->side[0]);
   launch_count_merge(1, a, ctx->chunks[1].as<uint2>(), ctx->mdocs[1].as<uint32_t>(), ctx->n_mdocs[1], m0);
   launch_count_merge(0, a, ctx->chunks[1].as<uint2>(), ctx->mdocs[0].as<uint32_t>(), ctx->n_mdocs[0], m0);
+  }
   for (int k = 0; k < 3; ++k) {  // join
     ck(cudaEventRecord(ctx->ev_join[k], ctx->side[k]), "join");
     ck(cudaStreamWaitEvent(m0, ctx->ev_join[k], 0), "join");
@@ -748,7 +760,7 @@ static void do_set_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_i
   require(ctx->counted, "count() not called");
   require(!ctx->db, "query context uses the attached database's reference");
   require(ref_doc_ids != nullptr, "ref_doc_ids is NULL");
-  require(K >= 1, "K must be >= 1");
+  require(K >= 1 && K <= kMaxRefs, "K must be in 1..256");
   uint64_t u_cap = 0;
   for (uint32_t k = 0; k < K; ++k) {
     require(ref_doc_ids[k] < ctx->n_docs, "reference doc id >= n_docs");
@@ -756,7 +768,7 @@ static void do_set_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_i
   }
   ctx->ref_docs.ensure(4ull * K);
   upload(ctx, ctx->ref_docs.p, ref_doc_ids, 4ull * K);
-  RefArgs r{K,     nullptr, nullptr, ctx->ent.as<uint2>(), false, (K + 3) & ~3u, ctx->ref_docs.as<uint32_t>(),
+  RefArgs r{K,     nullptr, nullptr, ctx->ent.as<uint2>(), false, ref_row_stride(K), ctx->ref_docs.as<uint32_t>(),
             ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>()};
   build_reference(ctx, r, u_cap);
 }
@@ -770,7 +782,7 @@ int refsig_gpu_set_reference_vectors(refsig_gpu_ctx* ctx, uint32_t K, const uint
   return guard(ctx, [&] {
     require(ctx->counted, "count() not called");
     require(!ctx->db, "query context uses the attached database's reference");
-    require(K >= 1, "K must be >= 1");
+    require(K >= 1 && K <= kMaxRefs, "K must be in 1..256");
     require(rowptr != nullptr, "rowptr is NULL");
     require(rowptr[0] == 0, "rowptr[0] must be 0");
     for (uint32_t k = 0; k < K; ++k) require(rowptr[k + 1] >= rowptr[k], "rowptr must be non-decreasing");
@@ -803,7 +815,7 @@ int refsig_gpu_set_reference_vectors(refsig_gpu_ctx* ctx, uint32_t K, const uint
     ck(cudaMemcpyAsync(ctx->ref_start.p, start.data(), 8ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D");
     ck(cudaMemcpyAsync(ctx->ref_n.p, cnt.data(), 4ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D");
     RefArgs r{K, ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->ref_ent.as<uint2>(), true,
-              (K + 3) & ~3u, nullptr, nullptr, nullptr};
+              ref_row_stride(K), nullptr, nullptr, nullptr};
     build_reference(ctx, r, n);
     ck(cudaStreamSynchronize(ctx->stream), "reference");
   });
@@ -833,10 +845,8 @@ static void do_sign(refsig_gpu_ctx* ctx) {
        "memset ST pad");
   ctx->inv_norm.ensure(sizeof(float) * N);
   if (ctx->db) ck(cudaStreamSynchronize(ctx->db->stream), "sync database");
-  ctx->sign_part.ensure(sizeof(float) * static_cast<size_t>(ctx->n_sign_segs) * refc->Kp);
   SignArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->info.as<TermInfo>(),
-             refc->R.as<float>(), N, K, refc->Kp, ctx->sign_segs.as<uint2>(), ctx->n_sign_segs,
-             ctx->sign_part.as<float>(), ctx->sign_part_sq.as<float>(), ctx->sign_arrive.as<uint32_t>(),
+             refc->R.as<float>(), N, K, refc->Kp, ctx->order.as<uint32_t>(), ctx->n_sign_long,
              ctx->S.as<float>(), ctx->ST.as<float>(), ld, ctx->inv_norm.as<float>()};
   {
     Phase ph(ctx, REFSIG_PHASE_SIGN);
@@ -1113,7 +1123,7 @@ int refsig_gpu_mrc_step(refsig_gpu_ctx* ctx, int weight_mode, const uint32_t* re
     require(ctx->loaded, "no corpus loaded");
     require(!ctx->db, "query contexts use the attached database's reference");
     require(!ctx->emit_pending, "previous step not collected (refsig_gpu_step_result)");
-    require(ref_doc_ids != nullptr && K >= 1, "reference docs required");
+    require(ref_doc_ids != nullptr && K >= 1 && K <= kMaxRefs, "reference docs required (K in 1..256)");
     require(!std::isnan(tau), "tau is NaN");
     require(row_lo <= row_hi && row_hi <= ctx->n_docs, "bad row range");
     require(row_lo == row_hi || (row_lo % kTile == 0 && (row_hi % kTile == 0 || row_hi == ctx->n_docs)),

@@ -96,6 +96,53 @@ __device__ __forceinline__ void bitonic_regs(uint32_t (&v)[IPT], uint32_t lane) 
   bitonic_level<IPT, 2>(v, lane);
 }
 
+// Group variant: T = 32*W threads of one CTA sort P = T*IPT keys, thread t
+// holding [t*IPT, t*IPT+IPT). Distances j < IPT are register ops, IPT <= j <
+// 32*IPT shuffles, j >= 32*IPT go through shared memory (sm: IPT*T words,
+// element-major so both the stores and the partner loads are conflict-free).
+template <int IPT, int T, int K, int J>
+__device__ __forceinline__ void gbitonic_stage(uint32_t (&v)[IPT], uint32_t t, uint32_t* sm) {
+  if constexpr (J >= 32 * IPT) {
+    constexpr uint32_t tj = J / IPT;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) sm[q * T + t] = v[q];
+    __syncthreads();
+    const bool take_min = ((t & tj) == 0) == (((t * IPT) & K) == 0);
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      const uint32_t y = sm[q * T + (t ^ tj)];
+      v[q] = take_min ? min(v[q], y) : max(v[q], y);
+    }
+  } else if constexpr (J >= IPT) {
+    constexpr uint32_t lj = J / IPT;
+    const bool take_min = ((t & lj) == 0) == (((t * IPT) & K) == 0);
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      const uint32_t y = __shfl_xor_sync(0xffffffffu, v[q], lj);
+      v[q] = take_min ? min(v[q], y) : max(v[q], y);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      if ((q & J) == 0) {
+        const int l = q | J;
+        const bool asc = ((t * IPT + q) & K) == 0;
+        const uint32_t lo = min(v[q], v[l]), hi = max(v[q], v[l]);
+        v[q] = asc ? lo : hi;
+        v[l] = asc ? hi : lo;
+      }
+    }
+  }
+  if constexpr (J > 1) gbitonic_stage<IPT, T, K, J / 2>(v, t, sm);
+}
+
+template <int IPT, int T, int K>
+__device__ __forceinline__ void gbitonic_level(uint32_t (&v)[IPT], uint32_t t, uint32_t* sm) {
+  gbitonic_stage<IPT, T, K, K / 2>(v, t, sm);
+  if constexpr (K < T * IPT) gbitonic_level<IPT, T, 2 * K>(v, t, sm);
+}
+
 // Warp inclusive scan / suffix min.
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, uint32_t lane) {
 #pragma unroll
@@ -265,6 +312,27 @@ __global__ void __launch_bounds__(256, IPT <= 8 ? 6 : 4) chunk_sort_kernel(Count
     else
       a.chunk_cnt[q] = n;
   }
+}
+
+// Group pass: one CTA of W warps per document of up to 512*W tokens, sorted
+// as 512*W keys (IPT 16) in registers/shuffles/shared memory and run-length
+// encoded straight into the final rows (no chunk scratch, no merge).
+template <int W>
+__global__ void __launch_bounds__(32 * W) group_sort_kernel(CountArgs a, const uint32_t* __restrict__ docs,
+                                                           uint32_t n_docs) {
+  constexpr int IPT = 16, T = 32 * W;
+  __shared__ uint32_t sm[IPT * T];
+  __shared__ uint32_t rle_sm[3 * W + 2];
+  const uint32_t t = threadIdx.x;
+  const uint32_t d = docs[blockIdx.x];
+  const uint64_t b = a.doc_off[d];
+  const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
+  uint32_t v[IPT];
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) v[k] = load_key(a, b, k * T + t, len);  // coalesced; any order sorts
+  gbitonic_level<IPT, T, 2>(v, t, sm);
+  const uint32_t n = rle_regs<IPT, W>(v, t, len, a.ent + b, a, rle_sm);
+  if (t == 0) a.nnz[d] = n;
 }
 
 // Merge pass: one CTA (256 threads) per document of kMergeChunk+1..CAP tokens
@@ -525,6 +593,25 @@ void launch_count_chunks(int ipt, const CountArgs& a, const uint2* chunks, uint3
     chunk_sort_kernel<8><<<blocks, 256, 0, s>>>(a, chunks, n);
   else
     chunk_sort_kernel<16><<<blocks, 256, 0, s>>>(a, chunks, n);
+  note_launch();
+}
+
+void launch_count_group(int cls, const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s) {
+  if (n == 0) return;
+  switch (cls) {
+    case 0:
+      group_sort_kernel<2><<<n, 64, 0, s>>>(a, docs, n);
+      break;
+    case 1:
+      group_sort_kernel<4><<<n, 128, 0, s>>>(a, docs, n);
+      break;
+    case 2:
+      group_sort_kernel<8><<<n, 256, 0, s>>>(a, docs, n);
+      break;
+    default:
+      group_sort_kernel<16><<<n, 512, 0, s>>>(a, docs, n);
+      break;
+  }
   note_launch();
 }
 

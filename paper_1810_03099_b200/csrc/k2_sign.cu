@@ -23,13 +23,6 @@
 namespace refsig_gpu {
 namespace {
 
-int sm_count() {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms;
-}
-
 __device__ __forceinline__ void ref_range(const RefArgs& r, uint32_t k, const uint2*& e, uint32_t& n) {
   if (r.docs) {
     const uint32_t d = r.docs[k];
@@ -88,164 +81,163 @@ __global__ void __launch_bounds__(256) ref_fill_kernel(RefArgs r, const TermInfo
   }
 }
 
-// Warp per segment: a document's nonzeros are cut into segments of
-// kSignSeg = 256 rows (8 per lane); one warp handles one segment, so the
-// longest document is no longer the critical path (docs of 2,400 nonzeros
-// used to keep one warp busy for the whole kernel) and every warp has 8
-// independent 8-byte row loads and 8 TermInfo gathers in flight.
-//   1. lanes load their 8 rows, gather TermInfo, accumulate ||w||^2, and the
-//      rows that hit the reference union go to a per-warp hit queue in shared
-//      memory (ballot + prefix popcount; queue order = ascending term id);
-//   2. the warp splits into 4 groups of 8 lanes; group g takes hits g, g+4, ...
-//      and lane j of a group accumulates columns 4j..4j+3 of the current
-//      32-column slab with float4 gathers of the L2-resident table R; the 4
-//      group sums are combined with two xor-shuffles (fixed order);
-//   3. single-segment documents finish in place; a multi-segment document
-//      writes per-segment partials, and the warp that arrives last (atomic
-//      per-document counter, reset by that warp) adds the partials in segment
-//      order and finishes. Every sum has a fixed order, so signatures do not
-//      depend on the launch configuration or on scheduling.
+// K2 is an SpMM, S = X_hit * R, with X_hit the doc rows restricted to the
+// union U (hits). Per step of 128 nonzeros (4 per lane): coalesced row loads,
+// TermInfo gathers, ||w||^2, and the hits appended to a per-warp queue in
+// shared memory (ballot + prefix popcount; queue order = ascending term id).
+// Then lane l takes hits l, l+32, ... and adds w * R[row][c0 .. c0+KW) into
+// its own KW accumulators with float4 loads of the row (all lanes busy, KW/4
+// independent 16-byte loads per hit in flight). After the document, the 32
+// per-lane vectors are transposed through shared memory and lane k adds column
+// k over the lanes in lane order. Columns are processed in slabs of KW <= 32.
+// Work split: documents of > kSignLongTokens tokens get a CTA (8 warps take
+// interleaved steps; the 8 column vectors are added in warp order), shorter
+// ones a warp. Every sum has a fixed order: signatures do not depend on
+// scheduling.
 constexpr int kSignWarps = 8;
-constexpr uint32_t kSignSeg = kSignSegRows;
+constexpr uint32_t kSignStep = 128;
 
-// Lanes 0..7 hold the 32 raw column sums of slab k0 as float4 (columns
-// k0+4*lane..). Writes S = min(sum*inv, 1) and returns this lane's sum of S^2.
-__device__ __forceinline__ float sign_finish_slab(const SignArgs& a, uint32_t d, uint32_t k0, uint32_t lane,
-                                                  float4 v, float inv) {
-  float ss = 0.0f;
-  if (lane < 8) {
-    const float x[4] = {v.x, v.y, v.z, v.w};
+template <int KW>
+__device__ __forceinline__ void sign_slab_steps(const SignArgs& a, const uint2* __restrict__ e, uint32_t n,
+                                                uint32_t s0, uint32_t stride, uint32_t c0, uint32_t lane, int2* qw,
+                                                float (&acc)[KW], float& sq, bool do_sq) {
+  const uint32_t lt = (1u << lane) - 1u;
+  for (uint32_t c = s0 * kSignStep; c < n; c += stride * kSignStep) {
+    uint2 x[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t k = k0 + 4 * lane + j;
-      if (k < a.K) {
-        const float sv = fminf(x[j] * inv, 1.0f);  // ngram.hpp:201 clamp
-        a.S[static_cast<size_t>(d) * a.K + k] = sv;
-        ss = fmaf(sv, sv, ss);
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = c + 32u * u + lane;
+      x[u] = i < n ? __ldg(e + i) : make_uint2(0u, 0u);
+    }
+    TermInfo ti[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) ti[u] = (c + 32u * u + lane < n) ? a.info[x[u].x] : TermInfo{0.0f, -1};
+    uint32_t qn = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float w = static_cast<float>(x[u].y) * ti[u].idf;
+      if (do_sq) sq = fmaf(w, w, sq);
+      const uint32_t hits = __ballot_sync(0xffffffffu, ti[u].ref_row >= 0);
+      if (ti[u].ref_row >= 0) qw[qn + __popc(hits & lt)] = make_int2(ti[u].ref_row, __float_as_int(w));
+      qn += __popc(hits);
+    }
+    __syncwarp();
+    for (uint32_t h = lane; h < qn; h += 32) {
+      const int2 hv = qw[h];
+      const float w = __int_as_float(hv.y);
+      const float4* __restrict__ r4 = reinterpret_cast<const float4*>(a.R + static_cast<size_t>(hv.x) * a.Kp + c0);
+      constexpr int G = KW / 4 < 8 ? KW / 4 : 8;  // float4 loads in flight per group
+#pragma unroll
+      for (int j0 = 0; j0 < KW / 4; j0 += G) {
+        float4 r[G];
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+          r[j] = (c0 + 4u * (j0 + j) < a.Kp) ? __ldg(r4 + j0 + j) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          acc[4 * (j0 + j) + 0] = fmaf(w, r[j].x, acc[4 * (j0 + j) + 0]);
+          acc[4 * (j0 + j) + 1] = fmaf(w, r[j].y, acc[4 * (j0 + j) + 1]);
+          acc[4 * (j0 + j) + 2] = fmaf(w, r[j].z, acc[4 * (j0 + j) + 2]);
+          acc[4 * (j0 + j) + 3] = fmaf(w, r[j].w, acc[4 * (j0 + j) + 3]);
+        }
       }
     }
+    __syncwarp();
   }
-  return ss;
 }
 
-__global__ void __launch_bounds__(256, 5) sign_kernel(SignArgs a) {
-  __shared__ int2 queue[kSignWarps][kSignSeg];
-  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t q = blockIdx.x * kSignWarps + wid;
-  if (q >= a.n_segs) return;
-  const uint2 sg = a.segs[q];
-  const uint32_t d = sg.x, s = sg.y;
-  const uint32_t n = a.nnz[d];
-  const uint32_t ns = n > kSignSeg ? (n + kSignSeg - 1) / kSignSeg : 1u;
-  if (s >= ns) return;  // the plan sizes segments by tokens; nnz <= tokens
-  const uint2* __restrict__ e = a.ent + a.doc_off[d] + s * kSignSeg;
-  const uint32_t cnt = min(kSignSeg, n - min(n, s * kSignSeg));
-  const uint32_t lt = (1u << lane) - 1u;
-  int2* qw = queue[wid];
-
-  uint2 x[8];
+// Lane-order column sums of the warp's KW-vectors: col[t] = column
+// 32*t + lane (0 past KW). tw: 32*(KW+1) floats of this warp.
+template <int KW, int CPL>
+__device__ __forceinline__ void sign_transpose_sum(const float (&acc)[KW], uint32_t lane, float* tw,
+                                                   float (&col)[CPL]) {
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const uint32_t i = 32 * u + lane;
-    x[u] = i < cnt ? __ldg(e + i) : make_uint2(0u, 0u);
-  }
-  TermInfo ti[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) ti[u] = (32 * u + lane < cnt) ? a.info[x[u].x] : TermInfo{0.0f, -1};
-  float sq = 0.0f;
-  uint32_t qn = 0;
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const float w = static_cast<float>(x[u].y) * ti[u].idf;
-    sq = fmaf(w, w, sq);
-    const uint32_t hits = __ballot_sync(0xffffffffu, ti[u].ref_row >= 0);
-    if (ti[u].ref_row >= 0) qw[qn + __popc(hits & lt)] = make_int2(ti[u].ref_row, __float_as_int(w));
-    qn += __popc(hits);
-  }
-  sq = warp_sum(sq);
+  for (int k = 0; k < KW; ++k) tw[lane * (KW + 1) + k] = acc[k];
   __syncwarp();
+#pragma unroll
+  for (int t = 0; t < CPL; ++t) {
+    float x = 0.0f;
+    const uint32_t k = 32u * t + lane;
+    if (k < static_cast<uint32_t>(KW)) {
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) x += tw[l * (KW + 1) + k];
+    }
+    col[t] = x;
+  }
+  __syncwarp();
+}
 
-  const uint32_t g = lane >> 3, sub = lane & 7;
-  const bool multi = ns > 1;
-  float ss = 0.0f;
-  float inv = 0.0f;
-  if (!multi) {
-    inv = sq > 0.0f ? 1.0f / sqrtf(sq) : 0.0f;
-    if (lane == 0) a.inv_norm[d] = inv;
+template <int KW>
+__global__ void __launch_bounds__(256, KW <= 24 ? 4 : (KW <= 32 ? 3 : 2)) sign_kernel(SignArgs a) {
+  constexpr int CPL = (KW + 31) / 32;  // columns per lane
+  // per-warp area: the 128-entry hit queue, then the 32 x (KW+1) transpose
+  constexpr int TW = 32 * (KW + 1) > 2 * static_cast<int>(kSignStep) ? 32 * (KW + 1) : 2 * kSignStep;
+  extern __shared__ __align__(16) float tsm_dyn[];  // [kSignWarps][TW]
+  __shared__ float red[kSignWarps][32 * CPL + 1];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float* tw = tsm_dyn + wid * TW;
+  int2* qw = reinterpret_cast<int2*>(tw);
+  const bool cta = blockIdx.x < a.n_long;  // one long document per CTA
+  uint32_t q;
+  if (cta) {
+    q = blockIdx.x;
+  } else {
+    q = a.n_long + (blockIdx.x - a.n_long) * kSignWarps + wid;
+    if (q >= a.n_docs) return;
   }
-  for (uint32_t k0 = 0; k0 < a.K; k0 += 32) {
-    const uint32_t col = k0 + 4 * sub;
-    const bool on = col < a.Kp;  // R rows are zero-padded to Kp (multiple of 4)
-    float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-    for (uint32_t h0 = 0; h0 < qn; h0 += 32) {
-      float4 r[8];
-      float w[8];
+  const uint32_t d = a.order[q];
+  const uint2* __restrict__ e = a.ent + a.doc_off[d];
+  const uint32_t n = a.nnz[d];
+  const uint32_t s0 = cta ? wid : 0u, stride = cta ? kSignWarps : 1u;
+  float sq = 0.0f, inv = 0.0f, ss = 0.0f;
+  for (uint32_t c0 = 0; c0 < a.K; c0 += KW) {
+    float acc[KW];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t h = h0 + 4 * j + g;
-        w[j] = 0.0f;
-        r[j] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        if (h < qn && on) {
-          const int2 hv = qw[h];
-          w[j] = __int_as_float(hv.y);
-          r[j] = __ldg(reinterpret_cast<const float4*>(a.R + static_cast<size_t>(hv.x) * a.Kp + col));
-        }
-      }
+    for (int k = 0; k < KW; ++k) acc[k] = 0.0f;
+    sign_slab_steps<KW>(a, e, n, s0, stride, c0, lane, qw, acc, sq, c0 == 0);
+    float col[CPL];
+    sign_transpose_sum<KW, CPL>(acc, lane, tw, col);
+    if (c0 == 0) sq = warp_sum(sq);
+    if (cta) {  // add the 8 warps' columns (and norms) in warp order
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        acc.x = fmaf(w[j], r[j].x, acc.x);
-        acc.y = fmaf(w[j], r[j].y, acc.y);
-        acc.z = fmaf(w[j], r[j].z, acc.z);
-        acc.w = fmaf(w[j], r[j].w, acc.w);
+      for (int t = 0; t < CPL; ++t) red[wid][32 * t + lane] = col[t];
+      if (c0 == 0 && lane == 0) red[wid][32 * CPL] = sq;
+      __syncthreads();
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) {
+        float x = 0.0f;
+#pragma unroll
+        for (int u = 0; u < kSignWarps; ++u) x += red[u][32 * t + lane];
+        col[t] = x;
       }
+      if (c0 == 0) {
+        float x = 0.0f;
+#pragma unroll
+        for (int u = 0; u < kSignWarps; ++u) x += red[u][32 * CPL];
+        sq = x;
+      }
+      __syncthreads();
+    }
+    if (c0 == 0) {
+      inv = sq > 0.0f ? 1.0f / sqrtf(sq) : 0.0f;
+      if (lane == 0 && wid == 0) a.inv_norm[d] = inv;
     }
 #pragma unroll
-    for (int m = 8; m <= 16; m <<= 1) {
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, m);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, m);
-      acc.z += __shfl_xor_sync(0xffffffffu, acc.z, m);
-      acc.w += __shfl_xor_sync(0xffffffffu, acc.w, m);
-    }
-    if (multi) {
-      if (lane < 8 && on) *reinterpret_cast<float4*>(a.part + static_cast<size_t>(q) * a.Kp + col) = acc;
-    } else {
-      ss += sign_finish_slab(a, d, k0, lane, acc, inv);
-    }
-  }
-  if (multi) {
-    // publish this segment, then the last of the document's ns segments finishes it
-    if (lane == 0) a.part_sq[q] = sq;
-    __threadfence();
-    uint32_t last = 0;
-    if (lane == 0) last = atomicAdd(a.arrive + d, 1u) == ns - 1;
-    if (!__shfl_sync(0xffffffffu, last, 0)) return;
-    __threadfence();
-    if (lane == 0) a.arrive[d] = 0;  // ready for the next launch
-    const uint32_t q0 = q - s;
-    float tot = 0.0f;
-    for (uint32_t t = 0; t < ns; ++t) tot += __ldcg(a.part_sq + q0 + t);  // segment order
-    inv = tot > 0.0f ? 1.0f / sqrtf(tot) : 0.0f;
-    if (lane == 0) a.inv_norm[d] = inv;
-    for (uint32_t k0 = 0; k0 < a.K; k0 += 32) {
-      const uint32_t col = k0 + 4 * lane;
-      float4 v = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      if (lane < 8 && col < a.Kp) {
-        for (uint32_t t = 0; t < ns; ++t) {
-          const float4 p4 = __ldcg(reinterpret_cast<const float4*>(a.part + static_cast<size_t>(q0 + t) * a.Kp + col));
-          v.x += p4.x;
-          v.y += p4.y;
-          v.z += p4.z;
-          v.w += p4.w;
-        }
+    for (int t = 0; t < CPL; ++t) {
+      const uint32_t kk = 32u * t + lane, k = c0 + kk;
+      if (kk < static_cast<uint32_t>(KW) && k < a.K) {
+        const float v = fminf(col[t] * inv, 1.0f);  // ngram.hpp:201 clamp
+        if (wid == 0 || !cta) a.S[static_cast<size_t>(d) * a.K + k] = v;
+        ss = fmaf(v, v, ss);
       }
-      ss += sign_finish_slab(a, d, k0, lane, v, inv);
     }
   }
+  if (cta && wid != 0) return;
   ss = warp_sum(ss);
   const float inv_s = ss > 0.0f ? 1.0f / sqrtf(ss) : 0.0f;  // SPEC.md:372 all-zero -> 0
   __syncwarp();
   for (uint32_t k = lane; k < a.K; k += 32)
-    a.ST[static_cast<size_t>(k) * a.ld + d] = a.S[static_cast<size_t>(d) * a.K + k] * inv_s;  // own warp's writes
+    a.ST[static_cast<size_t>(k) * a.ld + d] = a.S[static_cast<size_t>(d) * a.K + k] * inv_s;  // own writes
 }
 
 }  // namespace
@@ -267,11 +259,161 @@ void launch_ref_fill(const RefArgs& r, const TermInfo* info, float* R, cudaStrea
   note_launch();
 }
 
+// K > 32: lane k owns columns k, k+32, ... (KS = Kp/32 slabs, Kp =
+// roundup(K,32) so every lane load is in bounds): per step the hits are queued
+// as above (padded to a multiple of 4 with zero-weight entries) and every lane
+// walks the queue (broadcast LDS.64), 4 hits = 4*KS coalesced 128-byte row
+// loads in flight. No transpose; each step's column sums are added to the
+// running total (two-level summation). Dense lane-per-hit accumulators would
+// need 64+ registers per lane and read whole 256-byte rows per hit.
+template <int KS>
+__device__ __forceinline__ void signc_steps(const SignArgs& a, const uint2* __restrict__ e, uint32_t n, uint32_t s0,
+                                            uint32_t stride, uint32_t lane, int2* qw, float (&acc)[KS], float& sq) {
+  const uint32_t lt = (1u << lane) - 1u;
+  for (uint32_t c = s0 * kSignStep; c < n; c += stride * kSignStep) {
+    uint2 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = c + 32u * u + lane;
+      x[u] = i < n ? __ldg(e + i) : make_uint2(0u, 0u);
+    }
+    TermInfo ti[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) ti[u] = (c + 32u * u + lane < n) ? a.info[x[u].x] : TermInfo{0.0f, -1};
+    uint32_t qn = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float w = static_cast<float>(x[u].y) * ti[u].idf;
+      sq = fmaf(w, w, sq);
+      const uint32_t hits = __ballot_sync(0xffffffffu, ti[u].ref_row >= 0);
+      if (ti[u].ref_row >= 0) qw[qn + __popc(hits & lt)] = make_int2(ti[u].ref_row, __float_as_int(w));
+      qn += __popc(hits);
+    }
+    const uint32_t qp = (qn + 3) & ~3u;
+    if (lane < qp - qn) qw[qn + lane] = make_int2(0, 0);  // row 0 exists when qn > 0; weight 0 adds +0
+    __syncwarp();
+    float part[KS];
+#pragma unroll
+    for (int t = 0; t < KS; ++t) part[t] = 0.0f;
+    for (uint32_t h = 0; h < qp; h += 4) {
+      int2 hv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) hv[j] = qw[h + j];
+      float r[4][KS];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int t = 0; t < KS; ++t) r[j][t] = __ldg(a.R + static_cast<size_t>(hv[j].x) * a.Kp + 32u * t + lane);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int t = 0; t < KS; ++t) part[t] = fmaf(__int_as_float(hv[j].y), r[j][t], part[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < KS; ++t) acc[t] += part[t];
+    __syncwarp();
+  }
+}
+
+template <int KS>
+__global__ void __launch_bounds__(256) sign_col_kernel(SignArgs a) {
+  __shared__ int2 queue[kSignWarps][kSignStep];
+  __shared__ float red[kSignWarps][32 * KS + 1];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int2* qw = queue[wid];
+  const bool cta = blockIdx.x < a.n_long;  // one long document per CTA
+  uint32_t q;
+  if (cta) {
+    q = blockIdx.x;
+  } else {
+    q = a.n_long + (blockIdx.x - a.n_long) * kSignWarps + wid;
+    if (q >= a.n_docs) return;
+  }
+  const uint32_t d = a.order[q];
+  const uint2* __restrict__ e = a.ent + a.doc_off[d];
+  const uint32_t n = a.nnz[d];
+  float acc[KS];
+#pragma unroll
+  for (int t = 0; t < KS; ++t) acc[t] = 0.0f;
+  float sq = 0.0f;
+  signc_steps<KS>(a, e, n, cta ? wid : 0u, cta ? kSignWarps : 1u, lane, qw, acc, sq);
+  sq = warp_sum(sq);
+  if (cta) {  // add the 8 warps' columns (and norms) in warp order
+#pragma unroll
+    for (int t = 0; t < KS; ++t) red[wid][32 * t + lane] = acc[t];
+    if (lane == 0) red[wid][32 * KS] = sq;
+    __syncthreads();
+    if (wid != 0) return;
+#pragma unroll
+    for (int t = 0; t < KS; ++t) {
+      float x = 0.0f;
+#pragma unroll
+      for (int u = 0; u < kSignWarps; ++u) x += red[u][32 * t + lane];
+      acc[t] = x;
+    }
+    float x = 0.0f;
+#pragma unroll
+    for (int u = 0; u < kSignWarps; ++u) x += red[u][32 * KS];
+    sq = x;
+  }
+  const float inv = sq > 0.0f ? 1.0f / sqrtf(sq) : 0.0f;
+  if (lane == 0) a.inv_norm[d] = inv;
+  float v[KS], ss = 0.0f;
+#pragma unroll
+  for (int t = 0; t < KS; ++t) {
+    const uint32_t k = 32u * t + lane;
+    v[t] = fminf(acc[t] * inv, 1.0f);  // ngram.hpp:201 clamp
+    if (k < a.K) {
+      a.S[static_cast<size_t>(d) * a.K + k] = v[t];
+      ss = fmaf(v[t], v[t], ss);
+    }
+  }
+  ss = warp_sum(ss);
+  const float inv_s = ss > 0.0f ? 1.0f / sqrtf(ss) : 0.0f;  // SPEC.md:372 all-zero -> 0
+#pragma unroll
+  for (int t = 0; t < KS; ++t) {
+    const uint32_t k = 32u * t + lane;
+    if (k < a.K) a.ST[static_cast<size_t>(k) * a.ld + d] = v[t] * inv_s;
+  }
+}
+
+template <int KW>
+void launch_sign_kw(const SignArgs& a, unsigned g, cudaStream_t s) {
+  constexpr int TW = 32 * (KW + 1) > 2 * static_cast<int>(kSignStep) ? 32 * (KW + 1) : 2 * kSignStep;
+  constexpr size_t smem = sizeof(float) * kSignWarps * TW;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(sign_kernel<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    configured = true;
+  }
+  sign_kernel<KW><<<g, 32 * kSignWarps, smem, s>>>(a);
+}
+
 void launch_sign(const SignArgs& a, cudaStream_t s) {
   if (a.n_docs == 0) return;
-  if (a.n_segs == 0) return;
-  const uint64_t blocks = ceil_div(a.n_segs, kSignWarps);  // one warp per segment
-  sign_kernel<<<static_cast<unsigned>(blocks), 32 * kSignWarps, 0, s>>>(a);
+  const unsigned g = static_cast<unsigned>(a.n_long + ceil_div(a.n_docs - a.n_long, kSignWarps));
+  if (a.K > 32) {  // column-owner variant, Kp = roundup(K, 32)
+    switch (a.Kp / 32) {
+      case 2: sign_col_kernel<2><<<g, 32 * kSignWarps, 0, s>>>(a); break;
+      case 3: sign_col_kernel<3><<<g, 32 * kSignWarps, 0, s>>>(a); break;
+      case 4: sign_col_kernel<4><<<g, 32 * kSignWarps, 0, s>>>(a); break;
+      default: sign_col_kernel<8><<<g, 32 * kSignWarps, 0, s>>>(a); break;
+    }
+    note_launch();
+    return;
+  }
+  // lane-per-hit slab width: K rounded up to 4
+  const uint32_t kw = (a.K + 3) & ~3u;
+  switch (kw) {
+    case 4: launch_sign_kw<4>(a, g, s); break;
+    case 8: launch_sign_kw<8>(a, g, s); break;
+    case 12: launch_sign_kw<12>(a, g, s); break;
+    case 16: launch_sign_kw<16>(a, g, s); break;
+    case 20: launch_sign_kw<20>(a, g, s); break;
+    case 24: launch_sign_kw<24>(a, g, s); break;
+    case 28: launch_sign_kw<28>(a, g, s); break;
+    default: launch_sign_kw<32>(a, g, s); break;
+  }
   note_launch();
 }
 

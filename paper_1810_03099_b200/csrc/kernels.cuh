@@ -43,6 +43,8 @@ void launch_count_tiny(const CountArgs& a, const uint32_t* docs, uint32_t n, cud
 // chunks[q] = {doc, m<<16 | lc<<1 | direct}, chunks of 32*ipt tokens (ipt 8/16).
 void launch_count_chunks(int ipt, const CountArgs& a, const uint2* chunks, uint32_t n, cudaStream_t s);
 // mdocs[q] = first chunk index (in the ipt-16 chunk list) of a doc of class cls.
+// One CTA of 2/4/8/16 warps per doc of merge class cls (docs = doc ids).
+void launch_count_group(int cls, const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s);
 void launch_count_merge(int cls, const CountArgs& a, const uint2* chunks, const uint32_t* mdocs, uint32_t n,
                         cudaStream_t s);
 void launch_count_large(const CountArgs& a, const uint32_t* long_docs, const uint64_t* scratch_off,
@@ -99,17 +101,15 @@ struct SignArgs {
   uint32_t n_docs;
   uint32_t K;
   uint32_t Kp;           // row stride of R
-  const uint2* segs;     // {doc, segment}: 256-nonzero segments, longest docs first (k2_sign.cu)
-  uint32_t n_segs;
-  float* part;           // [n_segs*Kp] per-segment column sums (multi-segment docs)
-  float* part_sq;        // [n_segs] per-segment ||w||^2
-  uint32_t* arrive;      // [n_docs] segment arrival counters (zero between launches)
+  const uint32_t* order;  // docs by decreasing length; the first n_long get a CTA each (k2_sign.cu)
+  uint32_t n_long;
   float* S;         // [n_docs*K] raw cosines, row-major (API output)
   float* ST;        // [K][ld] unit-normalised signatures, transposed (K3 operand; 0 if all-zero)
   uint32_t ld;      // leading dimension of ST (n_docs rounded up to 128; pad columns zero)
   float* inv_norm;  // [n_docs] 1/||w_d||
 };
-constexpr uint32_t kSignSegRows = 256;  // nonzeros per K2 segment
+constexpr uint32_t kSignLongTokens = 2048;  // K2: longer documents get a CTA
+constexpr uint32_t kMaxRefs = 256;          // K limit (K2 keeps a signature row in registers)
 void launch_sign(const SignArgs& a, cudaStream_t s);
 
 // ---- K3 / K4b pair bitmaps --------------------------------------------------
