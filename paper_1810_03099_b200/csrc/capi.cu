@@ -361,9 +361,7 @@ void build_reference(refsig_gpu_ctx* c, const RefArgs& r, uint64_t u_cap) {
   // info[].ref_row is -1 right after count(); a replaced reference resets it
   if (c->ref_dirty) launch_ref_reset(c->info.as<TermInfo>(), V, c->stream);
   ck(cudaMemsetAsync(c->ref_count.p, 0, sizeof(uint32_t), c->stream), "memset");
-  launch_ref_claim(r, c->info.as<TermInfo>(), c->ref_count.as<uint32_t>(), c->stream);
-  ck(cudaMemsetAsync(c->R.p, 0, rbytes, c->stream), "memset R");
-  launch_ref_fill(r, c->info.as<TermInfo>(), c->R.as<float>(), c->stream);
+  launch_ref_build(r, c->info.as<TermInfo>(), V, c->ref_count.as<uint32_t>(), c->R.as<float>(), c->stream);
   launched("reference");
   c->K = r.K;
   c->Kp = r.Kp;

@@ -12,7 +12,7 @@ constexpr int kTile = 128;  // pair-tile edge (rows and columns) of the all-pair
 
 // Packed per-term info gathered once per nonzero: x = idf32 bits, y = row of
 // the term in the compact reference table (or -1 when not in the union U).
-struct TermInfo {
+struct __align__(8) TermInfo {
   float idf;
   int32_t ref_row;
 };

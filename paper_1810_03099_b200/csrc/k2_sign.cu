@@ -39,45 +39,112 @@ __global__ void ref_reset_kernel(TermInfo* __restrict__ info, uint32_t vocab) {
     info[t].ref_row = -1;
 }
 
-__global__ void ref_claim_kernel(RefArgs r, TermInfo* __restrict__ info, uint32_t* __restrict__ counter) {
-  for (uint32_t k = blockIdx.x; k < r.K; k += gridDim.x) {
-    const uint2* e;
-    uint32_t n;
-    ref_range(r, k, e, n);
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-      int* slot = &info[e[i].x].ref_row;
-      if (atomicCAS(slot, -1, -2) == -1) *slot = static_cast<int>(atomicAdd(counter, 1u));
+// A5 in three launches, no contended atomics:
+//   mark   (CTA per reference): info[t].ref_row = -2 for every reference term
+//          (plain idempotent stores);
+//   assign (vocabulary-parallel): marked terms get compact rows (warp ballot +
+//          block scan, one counter atomic per CTA) and their R row is zeroed;
+//          the row numbering depends on CTA order, the values the sign kernel
+//          reads through it do not;
+//   fill   (CTA per reference): block-tree norm of the reference's weights
+//          (fixed order), then w/||w|| into column k of each term's row.
+// Entries are taken kRefIpt per thread per pass so each thread has all its
+// loads in flight. (A CAS-per-term claim serialised on shared cache lines of
+// the Zipf-head terms every reference contains: 18 us at configs[1].)
+constexpr int kRefIpt = 16;
+constexpr uint32_t kRefPass = 256 * kRefIpt;
+
+__global__ void __launch_bounds__(256) ref_mark_kernel(RefArgs r, TermInfo* __restrict__ info) {
+  const uint2* e;
+  uint32_t n;
+  ref_range(r, blockIdx.x, e, n);
+  for (uint32_t p0 = 0; p0 < n; p0 += kRefPass) {
+    uint32_t t[kRefIpt];
+#pragma unroll
+    for (int j = 0; j < kRefIpt; ++j) {
+      const uint32_t i = p0 + j * 256 + threadIdx.x;
+      t[j] = i < n ? e[i].x : 0xFFFFFFFFu;
     }
+#pragma unroll
+    for (int j = 0; j < kRefIpt; ++j)
+      if (t[j] != 0xFFFFFFFFu) info[t[j]].ref_row = -2;
   }
 }
 
-// One CTA per reference vector: block-tree norm, then scatter unit weights.
+__global__ void __launch_bounds__(256) ref_assign_kernel(TermInfo* __restrict__ info, uint32_t vocab,
+                                                         uint32_t* __restrict__ counter, float* __restrict__ R,
+                                                         uint32_t Kp) {
+  __shared__ uint32_t wsum[9];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t t = blockIdx.x * 256 + threadIdx.x;
+  const bool mk = t < vocab && info[t].ref_row == -2;
+  const uint32_t b = __ballot_sync(0xffffffffu, mk);
+  if (lane == 0) wsum[wid] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t x = wsum[w];
+      wsum[w] = tot;
+      tot += x;
+    }
+    wsum[8] = tot ? atomicAdd(counter, tot) : 0u;
+  }
+  __syncthreads();
+  if (mk) {
+    const uint32_t u = wsum[8] + wsum[wid] + __popc(b & ((1u << lane) - 1u));
+    float* row = R + static_cast<size_t>(u) * Kp;
+    for (uint32_t q = 0; q < Kp; ++q) row[q] = 0.0f;
+    info[t].ref_row = static_cast<int>(u);
+  }
+}
+
 __global__ void __launch_bounds__(256) ref_fill_kernel(RefArgs r, const TermInfo* __restrict__ info,
                                                        float* __restrict__ R) {
   __shared__ float red[8];
-  for (uint32_t k = blockIdx.x; k < r.K; k += gridDim.x) {
-    const uint2* e;
-    uint32_t n;
-    ref_range(r, k, e, n);
-    float sq = 0.0f;
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-      uint2 x = e[i];
-      float w = r.explicit_w ? __uint_as_float(x.y) : static_cast<float>(x.y) * info[x.x].idf;
-      sq = fmaf(w, w, sq);
-    }
-    sq = warp_sum(sq);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
-    __syncthreads();
-    float tot = 0.0f;
+  const uint32_t k = blockIdx.x;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint2* e;
+  uint32_t n;
+  ref_range(r, k, e, n);
+  float sq = 0.0f;
+  for (uint32_t p0 = 0; p0 < n; p0 += kRefPass) {
+    float w[kRefIpt];
 #pragma unroll
-    for (int w = 0; w < 8; ++w) tot += red[w];
-    const float inv = tot > 0.0f ? 1.0f / sqrtf(tot) : 0.0f;
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-      uint2 x = e[i];
-      float w = r.explicit_w ? __uint_as_float(x.y) : static_cast<float>(x.y) * info[x.x].idf;
-      R[static_cast<size_t>(info[x.x].ref_row) * r.Kp + k] = w * inv;
+    for (int j = 0; j < kRefIpt; ++j) {
+      const uint32_t i = p0 + j * 256 + threadIdx.x;
+      w[j] = 0.0f;
+      if (i < n) {
+        const uint2 x = e[i];
+        w[j] = r.explicit_w ? __uint_as_float(x.y) : static_cast<float>(x.y) * info[x.x].idf;
+      }
     }
-    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kRefIpt; ++j) sq = fmaf(w[j], w[j], sq);
+  }
+  sq = warp_sum(sq);
+  if (lane == 0) red[wid] = sq;
+  __syncthreads();
+  float tot = 0.0f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tot += red[w];
+  const float inv = tot > 0.0f ? 1.0f / sqrtf(tot) : 0.0f;
+  for (uint32_t p0 = 0; p0 < n; p0 += kRefPass) {
+    uint2 x[kRefIpt];
+#pragma unroll
+    for (int j = 0; j < kRefIpt; ++j) {
+      const uint32_t i = p0 + j * 256 + threadIdx.x;
+      x[j] = i < n ? e[i] : make_uint2(0xFFFFFFFFu, 0u);
+    }
+    TermInfo ti[kRefIpt];
+#pragma unroll
+    for (int j = 0; j < kRefIpt; ++j) ti[j] = x[j].x != 0xFFFFFFFFu ? info[x[j].x] : TermInfo{0.0f, 0};
+#pragma unroll
+    for (int j = 0; j < kRefIpt; ++j)
+      if (x[j].x != 0xFFFFFFFFu) {
+        const float w = r.explicit_w ? __uint_as_float(x[j].y) : static_cast<float>(x[j].y) * ti[j].idf;
+        R[static_cast<size_t>(ti[j].ref_row) * r.Kp + k] = w * inv;
+      }
   }
 }
 
@@ -240,25 +307,6 @@ __global__ void __launch_bounds__(256, KW <= 24 ? 4 : (KW <= 32 ? 3 : 2)) sign_k
     a.ST[static_cast<size_t>(k) * a.ld + d] = a.S[static_cast<size_t>(d) * a.K + k] * inv_s;  // own writes
 }
 
-}  // namespace
-
-void launch_ref_reset(TermInfo* info, uint32_t vocab, cudaStream_t s) {
-  uint32_t g = (vocab + 255) / 256;
-  if (g > 4096) g = 4096;
-  ref_reset_kernel<<<g, 256, 0, s>>>(info, vocab);
-  note_launch();
-}
-
-void launch_ref_claim(const RefArgs& r, TermInfo* info, uint32_t* counter, cudaStream_t s) {
-  ref_claim_kernel<<<r.K < 1024 ? r.K : 1024, 256, 0, s>>>(r, info, counter);
-  note_launch();
-}
-
-void launch_ref_fill(const RefArgs& r, const TermInfo* info, float* R, cudaStream_t s) {
-  ref_fill_kernel<<<r.K < 1024 ? r.K : 1024, 256, 0, s>>>(r, info, R);
-  note_launch();
-}
-
 // K > 32: lane k owns columns k, k+32, ... (KS = Kp/32 slabs, Kp =
 // roundup(K,32) so every lane load is in bounds): per step the hits are queued
 // as above (padded to a multiple of 4 with zero-weight entries) and every lane
@@ -375,6 +423,25 @@ __global__ void __launch_bounds__(256) sign_col_kernel(SignArgs a) {
     const uint32_t k = 32u * t + lane;
     if (k < a.K) a.ST[static_cast<size_t>(k) * a.ld + d] = v[t] * inv_s;
   }
+}
+
+}  // namespace
+
+void launch_ref_reset(TermInfo* info, uint32_t vocab, cudaStream_t s) {
+  uint32_t g = (vocab + 255) / 256;
+  if (g > 4096) g = 4096;
+  ref_reset_kernel<<<g, 256, 0, s>>>(info, vocab);
+  note_launch();
+}
+
+void launch_ref_build(const RefArgs& r, TermInfo* info, uint32_t vocab, uint32_t* counter, float* R,
+                      cudaStream_t s) {
+  ref_mark_kernel<<<r.K, 256, 0, s>>>(r, info);
+  ref_assign_kernel<<<static_cast<unsigned>(ceil_div(vocab, 256)), 256, 0, s>>>(info, vocab, counter, R, r.Kp);
+  ref_fill_kernel<<<r.K, 256, 0, s>>>(r, info, R);
+  note_launch();
+  note_launch();
+  note_launch();
 }
 
 template <int KW>

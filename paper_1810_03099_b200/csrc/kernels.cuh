@@ -84,12 +84,11 @@ struct RefArgs {
 };
 // info[t].ref_row = -1 for all t (only needed when a reference is replaced).
 void launch_ref_reset(TermInfo* info, uint32_t vocab, cudaStream_t s);
-// Assign compact rows to the union U: first claimant of a term takes the next
-// row from *counter (row numbering is scheduling-dependent; the values the
-// sign kernel reads through it are not).
-void launch_ref_claim(const RefArgs& r, TermInfo* info, uint32_t* counter, cudaStream_t s);
-// R[row*Kp + k] = w_k[t]/||w_k|| (R zeroed by the caller).
-void launch_ref_fill(const RefArgs& r, const TermInfo* info, float* R, cudaStream_t s);
+// Compact rows for the union U (marked terms get the next rows from *counter,
+// zeroed), then R[row*Kp + k] = w_k[t]/||w_k|| (three launches, k2_sign.cu).
+// *counter must be 0 and info[].ref_row -1.
+void launch_ref_build(const RefArgs& r, TermInfo* info, uint32_t vocab, uint32_t* counter, float* R,
+                      cudaStream_t s);
 
 // ---- K2 sign ----------------------------------------------------------------
 struct SignArgs {
