@@ -17,6 +17,8 @@
 //
 // MRC tile kernel: see the comment above mrc_bitmap_kernel.
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace refsig_gpu {
@@ -267,6 +269,211 @@ __global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel(MrcArgs a) {
   if (pending) flush();
 }
 
+// ---- K3 v2: mbarrier ring, warp-local epilogue ------------------------------
+// Same tiles, thread tiling, shared-memory layout and FFMA2 inner loop as
+// mrc_bitmap_kernel, but no CTA-wide barrier in the main loop: a 4-stage ring
+// of (tile, K-chunk) items where each stage has a "full" mbarrier (256
+// arrivals: every thread's cp.async.mbarrier.arrive) and an "empty" mbarrier
+// (8 arrivals: one per warp after its last read). A stage is refilled two
+// items ahead, so warps may drift up to two items apart and one warp's
+// epilogue overlaps the others' FFMA2 stream. The epilogue stays in the warp:
+// a warp owns 16 whole tile rows (ty = 2w, 2w+1); each lane packs its 8 row
+// bytes into two words, a 4x4 byte transpose inside each lane quad (2 SHFL +
+// 2 PRMT per word) gives lane (ty, 4q+i) word q of rows ty*8+i and ty*8+4+i,
+// which it stores directly. Row match counts stay in registers until the CTA
+// moves to the next row panel (one atomic per row per panel, not per tile).
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+               "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.shared.b64 st, [%0]; }" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{ .reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+      "@!p bra W; }" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+
+constexpr int mrc2_stages(int KC) { return KC > 0 && KC <= 24 ? 4 : 3; }
+
+template <int KC>
+__global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel2(MrcArgs a) {
+  constexpr int S = mrc2_stages(KC);  // ring stages (2 CTAs/SM must fit)
+  constexpr int D = S - 2;             // refill distance: warps may drift D items apart
+  extern __shared__ __align__(16) float smem[];
+  __shared__ __align__(8) uint64_t full_bar[S], empty_bar[S];
+  const uint32_t kcm = KC > 0 ? static_cast<uint32_t>(KC) : (a.K < kKC ? a.K : kKC);
+  const uint32_t panel = kcm * kTile;
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const uint32_t lane = tid & 31, wid = tid >> 5;
+  const uint32_t t_begin = static_cast<uint32_t>(a.n_tiles * blockIdx.x / gridDim.x);
+  const uint32_t t_end = static_cast<uint32_t>(a.n_tiles * (blockIdx.x + 1) / gridDim.x);
+  if (t_begin >= t_end) return;
+  const uint32_t nchunks = KC > 0 ? (a.K / KC) : (a.K + kKC - 1) / kKC;
+  const uint32_t items = (t_end - t_begin) * nchunks;
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full_bar[i], 256);
+      mbar_init(&empty_bar[i], 8);
+    }
+  }
+  __syncthreads();
+
+  uint32_t bi, bj;
+  tile_coords(t_begin + a.g.tile0, a.nbr, a.nbc, a.g.triangle, bi, bj);
+  uint32_t li = bi, lj = bj, lchunk = 0;
+  constexpr int kSlots = KC > 0 ? (2 * KC + 7) / 8 : 2 * kKC / 8;
+  const uint32_t cm = tid & 31, kr = tid >> 5, sp = split_pos(4 * cm);
+  auto issue = [&](uint32_t st) {
+    const uint32_t k0 = lchunk * kcm;
+    const uint32_t kc = KC > 0 ? static_cast<uint32_t>(KC) : min(kcm, a.K - k0);
+    const float* baseA = a.STr + static_cast<size_t>(k0) * a.ldr + li * kTile + 4 * cm;
+    const float* baseB = a.STc + static_cast<size_t>(k0) * a.ldc + lj * kTile + 4 * cm;
+    float* sbase = smem + 2 * st * panel + sp;
+#pragma unroll
+    for (int u = 0; u < kSlots; ++u) {
+      const uint32_t k = kr + 8 * u;
+      if (k < kcm) {
+        if (KC > 0 || k < kc) cp_async16(sbase + k * kTile, baseA + static_cast<size_t>(k) * a.ldr);
+      } else if (k < 2 * kcm) {
+        const uint32_t kk = k - kcm;
+        if (KC > 0 || kk < kc) cp_async16(sbase + panel + kk * kTile, baseB + static_cast<size_t>(kk) * a.ldc);
+      }
+    }
+    cp_async_mbar_arrive(&full_bar[st]);
+    if (++lchunk == nchunks) {
+      lchunk = 0;
+      if (++lj == a.nbc) {
+        ++li;
+        lj = a.g.triangle ? li : 0;
+      }
+    }
+  };
+
+  // byte-transpose selectors (lane-constant)
+  const uint32_t qi = tx & 3;
+  const uint32_t sel1 = (qi & 1) ? 0x3715u : 0x6240u;
+  const uint32_t sel2 = (qi & 2) ? 0x3276u : 0x5410u;
+  auto transpose = [&](uint32_t v) {
+    const uint32_t p = __shfl_xor_sync(0xffffffffu, v, 1);
+    v = __byte_perm(v, p, sel1);
+    const uint32_t q = __shfl_xor_sync(0xffffffffu, v, 2);
+    return __byte_perm(v, q, sel2);
+  };
+  uint32_t cntA = 0, cntB = 0;  // matches of rows ty*8+qi and ty*8+4+qi in the current row panel (this lane's words)
+  auto flush_counts = [&](uint32_t pbi) {
+    cntA += __shfl_xor_sync(0xffffffffu, cntA, 4);
+    cntA += __shfl_xor_sync(0xffffffffu, cntA, 8);
+    cntB += __shfl_xor_sync(0xffffffffu, cntB, 4);
+    cntB += __shfl_xor_sync(0xffffffffu, cntB, 8);
+    if (tx < 4) {
+      const uint32_t r0 = pbi * kTile + ty * 8 + qi;
+      if (cntA && r0 < a.g.n_rows) atomicAdd(a.rowcnt + r0, cntA);
+      if (cntB && r0 + 4 < a.g.n_rows) atomicAdd(a.rowcnt + r0 + 4, cntB);
+    }
+    cntA = cntB = 0;
+  };
+
+  float2 acc[8][4];
+  for (uint32_t j = 0; j < D && j < items; ++j) issue(j);
+  uint32_t chunk = 0;
+  for (uint32_t it = 0; it < items; ++it) {
+    const uint32_t st = it % S;
+    if (it + D < items) {
+      const uint32_t j = it + D, sj = j % S;
+      if (j >= S) mbar_wait(&empty_bar[sj], ((j / S) - 1) & 1u);
+      issue(sj);
+    }
+    mbar_wait(&full_bar[st], (it / S) & 1u);
+    const float* A = smem + 2 * st * panel;
+    const float* B = A + panel;
+    auto kstep = [&](uint32_t k, bool first) {
+      const float4 a0 = *reinterpret_cast<const float4*>(A + k * kTile + ty * 4);
+      const float4 a1 = *reinterpret_cast<const float4*>(A + k * kTile + 64 + ty * 4);
+      const float4 b0 = *reinterpret_cast<const float4*>(B + k * kTile + tx * 4);
+      const float4 b1 = *reinterpret_cast<const float4*>(B + k * kTile + 64 + tx * 4);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                            make_float2(b1.z, b1.w)};
+      const float2 nt = make_float2(-a.tau, -a.tau);
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = ffma2(av[r], bv[c], first ? nt : acc[r][c]);
+    };
+    if constexpr (KC > 0) {
+      if (KC == static_cast<int>(kKC) && chunk != 0) {
+#pragma unroll
+        for (uint32_t k = 0; k < KC; ++k) kstep(k, false);
+      } else {
+        kstep(0, true);
+#pragma unroll
+        for (uint32_t k = 1; k < KC; ++k) kstep(k, false);
+      }
+    } else {
+      const uint32_t kc = min(kcm, a.K - chunk * kcm);
+      uint32_t k = 0;
+      if (chunk == 0) kstep(k++, true);
+#pragma unroll 4
+      for (; k < kc; ++k) kstep(k, false);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[st]);
+    if (++chunk == nchunks) {
+      chunk = 0;
+      // rows ty*8 + 0..3 -> wA (byte r = row r), rows ty*8 + 4..7 -> wB; bit c
+      // of a byte = column tx*8 + c; match = NOT sign(dot - tau)
+      uint32_t wA = 0, wB = 0;
+#pragma unroll
+      for (int r = 3; r >= 0; --r)
+#pragma unroll
+        for (int c = 3; c >= 0; --c) {
+          wA = __funnelshift_l(__float_as_uint(acc[r][c].y), wA, 1);
+          wA = __funnelshift_l(__float_as_uint(acc[r][c].x), wA, 1);
+        }
+#pragma unroll
+      for (int r = 7; r >= 4; --r)
+#pragma unroll
+        for (int c = 3; c >= 0; --c) {
+          wB = __funnelshift_l(__float_as_uint(acc[r][c].y), wB, 1);
+          wB = __funnelshift_l(__float_as_uint(acc[r][c].x), wB, 1);
+        }
+      wA = transpose(~wA);  // lane (ty, 4q+qi): word q of row ty*8+qi
+      wB = transpose(~wB);  //                   word q of row ty*8+4+qi
+      const uint32_t q = tx >> 2;
+      const uint32_t rA = bi * kTile + ty * 8 + qi, rB = rA + 4;
+      const uint32_t c0 = bj * kTile + 32 * q;
+      if ((a.g.triangle && bj == bi) || bj + 1 == a.nbc) {  // diagonal / last column tile
+        wA &= col_mask(c0, rA, a.g);
+        wB &= col_mask(c0, rB, a.g);
+      }
+      if (rA < a.g.n_rows) a.bitmap[static_cast<size_t>(rA) * a.g.words_per_row + bj * 4 + q] = wA;
+      if (rB < a.g.n_rows) a.bitmap[static_cast<size_t>(rB) * a.g.words_per_row + bj * 4 + q] = wB;
+      cntA += __popc(wA);
+      cntB += __popc(wB);
+      const uint32_t pbi = bi;
+      if (++bj == a.nbc) {
+        ++bi;
+        bj = a.g.triangle ? bi : 0;
+      }
+      if (bi != pbi || it + 1 == items) flush_counts(pbi);
+    }
+  }
+}
+
 // Hamming tile: warp w handles rows (w&3)*32+lane and words (w>>2)*2..+1.
 __global__ void __launch_bounds__(256) hamming_bitmap_kernel(const uint64_t* __restrict__ fr,
                                                              const uint64_t* __restrict__ fc, int max_dist,
@@ -424,6 +631,36 @@ void launch_mrc_bitmap(const float* ST_rows, uint32_t ld_rows, const float* ST_c
   if (grid > t) grid = t;
   MrcArgs a{ST_rows, ST_cols, ld_rows, ld_cols, K, tau, g, nbr, nbc, t, bitmap, rowcnt};
   const dim3 gr(static_cast<unsigned>(grid));
+  static const bool v2 = [] {
+    const char* m = std::getenv("REFSIG_K3");
+    return !(m && m[0] == '1');
+  }();
+  if (v2) {
+    const int kt = K == 20 ? 20 : K == 10 ? 10 : K == 16 ? 16 : K % 32 == 0 ? 32 : 0;
+    const size_t smem2 = (2ull * mrc2_stages(kt) * kc * kTile) * sizeof(float);
+    static bool configured2 = false;
+    if (!configured2) {
+      const int mx = 8 * kKC * kTile * 4;
+      cudaFuncSetAttribute(mrc_bitmap_kernel2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(mrc_bitmap_kernel2<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(mrc_bitmap_kernel2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(mrc_bitmap_kernel2<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      cudaFuncSetAttribute(mrc_bitmap_kernel2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      configured2 = true;
+    }
+    if (K == 20)
+      mrc_bitmap_kernel2<20><<<gr, 256, smem2, s>>>(a);
+    else if (K == 10)
+      mrc_bitmap_kernel2<10><<<gr, 256, smem2, s>>>(a);
+    else if (K == 16)
+      mrc_bitmap_kernel2<16><<<gr, 256, smem2, s>>>(a);
+    else if (K % 32 == 0)
+      mrc_bitmap_kernel2<32><<<gr, 256, smem2, s>>>(a);
+    else
+      mrc_bitmap_kernel2<0><<<gr, 256, smem2, s>>>(a);
+    note_launch();
+    return;
+  }
   if (K == 20)
     mrc_bitmap_kernel<20><<<gr, 256, smem, s>>>(a);
   else if (K == 10)
