@@ -296,6 +296,9 @@ def run_ours(args):
 
     # Isolated K2 with a cold L2 (HBM roofline of the signature kernel).
     sign_iso = measure_sign_isolated(ctx, stream, flush, dev, reps=max(5, args.steps))
+    # The rival path (§8 row d): Simhash + Hamming all-pairs on the same corpus
+    # (not part of the MRC step; reported per kernel).
+    rivals = measure_rivals(ctx, stream, flush, dev, thr, reps=max(5, args.steps))
 
     # End to end through the public API with HOST buffers: pinned tokens H2D,
     # full pipeline, candidate keys D2H into pinned memory.
@@ -311,7 +314,9 @@ def run_ours(args):
         n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
         clock_mhz = clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
         roof = rooflines(phases, sign_iso, N, K, P if world == 1 else my_pairs, cp, peaks, peaks_src, n_sm,
-                         clock_mhz, ms_per_step)
+                         clock_mhz, ms_per_step, n_cand)
+        roof.update(rival_rooflines(rivals, N, P if world == 1 else my_pairs, cp, peaks, peaks_src, n_sm,
+                                    clock_mhz))
         traffic = load_traffic()
         for k, r in roof.items():
             r["traffic"] = traffic.get(k)
@@ -381,7 +386,53 @@ def measure_e2e(ctx, cp, refs, tau, lo, hi, stream, dev, steps, warmup):
     return {"_ms": 1e3 * sum(times) / len(times), "h2d": int(h2d), "d2h": int(n * 8 + 8)}
 
 
-def rooflines(phases, sign_iso_ms, N, K, pairs, cp, peaks, peaks_src, n_sm, clock_mhz, ms_per_step):
+def measure_rivals(ctx, stream, flush, dev, thr, reps):
+    """Device times of the Simhash kernel and the Hamming all-pairs (tiles +
+    emission), each launch after an L2 flush."""
+    import torch
+    with torch.cuda.stream(stream):
+        ctx.simhash(0, fetch=False)
+        ctx.hamming_pairs(thr["hamming_max"], fetch=False)
+        torch.cuda.synchronize(dev)
+        ctx.set_profiling(True)
+        n_ham = 0
+        for r in range(reps):
+            flush.fill_(r + 11)
+            ctx.simhash(0, fetch=False)
+            flush.fill_(r + 12)
+            n_ham = ctx.hamming_pairs(thr["hamming_max"], fetch=False)
+        torch.cuda.synchronize(dev)
+        ph = ctx.phase_times()
+        ctx.set_profiling(False)
+    per = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in ph.items()}
+    return {"simhash_ms": per["simhash"], "hamming_tiles_ms": per["pair_tiles"],
+            "hamming_emit_ms": per["pair_emit"], "hamming_pairs": int(n_ham)}
+
+
+def rival_rooflines(rv, N, pairs, cp, peaks, peaks_src, n_sm, clock_mhz):
+    nnz = nnz_total(cp)
+    ts = rv["simhash_ms"]
+    # K4a: 64 exact column updates per nonzero (2*S1_j > S rule, simhash.hpp:35-45)
+    dadd_peak = n_sm * 64 * clock_mhz * 1e6 / 1e12  # FP64 adds, Tops/s (measured 64/clk/SM, profiles/alu_peaks)
+    ach = 64.0 * nnz / (ts / 1e3) / 1e12 if ts else 0.0
+    out = {"simhash": {"bound": "fp64-add", "achieved": ach, "peak": dadd_peak, "unit": "Tops/s",
+                       "frac": ach / dadd_peak if dadd_peak else None, "ms_per_launch": ts,
+                       "hbm_gbs": (8 * nnz + 8 * N) / (ts / 1e3) / 1e9 if ts else None,
+                       "peak_source": f"{n_sm} SMs x 64 DADD/clk x {clock_mhz:.0f} MHz",
+                       "fingerprints_per_sec": N / (ts / 1e3) if ts else None}}
+    th = rv["hamming_tiles_ms"]
+    # K4b: one 64-bit XOR + popcount (2 POPC) per pair; POPC pipe 16/clk/SM (profiles/alu_peaks)
+    popc_peak = n_sm * 16 * clock_mhz * 1e6 / 2 / 1e12  # 1e12 pairs/s
+    ach = pairs / (th / 1e3) / 1e12 if th else 0.0
+    out["hamming_tiles"] = {"bound": "popc", "achieved": ach, "peak": popc_peak, "unit": "Tpairs/s",
+                            "frac": ach / popc_peak if popc_peak else None, "ms_per_launch": th,
+                            "peak_source": f"{n_sm} SMs x 16 POPC/clk / 2 per 64-bit pair x {clock_mhz:.0f} MHz",
+                            "emit_ms": rv["hamming_emit_ms"], "candidates": rv["hamming_pairs"],
+                            "doc_pairs_per_sec": pairs / ((th + rv["hamming_emit_ms"]) / 1e3)}
+    return out
+
+
+def rooflines(phases, sign_iso_ms, N, K, pairs, cp, peaks, peaks_src, n_sm, clock_mhz, ms_per_step, n_cand):
     """achieved = algorithmic work per launch / average launch time (CUDA events)."""
     def per_launch(name):
         t, c = phases[name]
@@ -414,8 +465,11 @@ def rooflines(phases, sign_iso_ms, N, K, pairs, cp, peaks, peaks_src, n_sm, cloc
                     "unit": "GB/s", "frac": (bytes_count / (t1 / 1e3) / 1e9 / hbm) if t1 else 0.0,
                     "ms_per_launch": t1, "peak_source": peaks_src, "share_of_step": t1 / ms_per_step}
     te, _ = per_launch("pair_emit")
-    out["pair_emit"] = {"bound": "hbm", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
-                        "ms_per_launch": te, "share_of_step": te / ms_per_step}
+    # row-count scan + bitmap words of the triangle (1 bit per pair) + 8 B per sorted candidate key
+    bytes_emit = pairs / 8 + 8 * n_cand + 12 * N
+    out["pair_emit"] = {"bound": "hbm", "achieved": bytes_emit / (te / 1e3) / 1e9 if te else 0.0, "peak": hbm,
+                        "unit": "GB/s", "frac": (bytes_emit / (te / 1e3) / 1e9 / hbm) if te else 0.0,
+                        "ms_per_launch": te, "peak_source": peaks_src, "share_of_step": te / ms_per_step}
     return out
 
 

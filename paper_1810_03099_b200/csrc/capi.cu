@@ -907,7 +907,8 @@ int refsig_gpu_simhash(refsig_gpu_ctx* ctx, uint64_t seed, int weight_mode, cons
     }
     ctx->fp.ensure(8ull * ctx->n_docs);
     SimhashArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->info.as<TermInfo>(),
-                  th, seed, ctx->n_docs, weight_mode == REFSIG_WEIGHT_TFIDF, ctx->fp.as<uint64_t>()};
+                  th, seed, ctx->n_docs, weight_mode == REFSIG_WEIGHT_TFIDF, ctx->fp.as<uint64_t>(),
+                  ctx->order.as<uint32_t>(), ctx->n_sign_long};
     {
       Phase ph(ctx, REFSIG_PHASE_SIMHASH);
       launch_simhash(a, ctx->stream);

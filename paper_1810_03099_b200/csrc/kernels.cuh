@@ -143,6 +143,8 @@ struct SimhashArgs {
   uint32_t n_docs;
   bool use_idf;               // false: raw TF weights (the reference's +-1 per occurrence)
   uint64_t* fp;
+  const uint32_t* order;      // docs by decreasing length; the first n_long get a CTA each
+  uint32_t n_long;
 };
 void launch_simhash(const SimhashArgs& a, cudaStream_t s);
 
