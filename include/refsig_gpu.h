@@ -99,11 +99,12 @@ int refsig_gpu_get_df(refsig_gpu_ctx* ctx, uint32_t* df, float* idf32);
 int refsig_gpu_get_inv_norm(refsig_gpu_ctx* ctx, float* inv_norm);
 
 /* ---- A5: reference vectors ------------------------------------------------- */
-/* K corpus docs (indices < n_docs) as references, weighted like the corpus. */
+/* K corpus docs (indices < n_docs) as references, weighted like the corpus.
+ * 1 <= K <= 256 (validation error otherwise). */
 int refsig_gpu_set_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_ids, uint32_t K);
 /* K explicit reference vectors (host CSR): vector k = term_ids[rowptr[k] ..
  * rowptr[k+1]) with weights (NULL: all 1.0, the reference's count-1 partition
- * vectors). Ids must be unique within a vector and < vocab. */
+ * vectors). Ids must be unique within a vector and < vocab; 1 <= K <= 256. */
 int refsig_gpu_set_reference_vectors(refsig_gpu_ctx* ctx, uint32_t K, const uint64_t* rowptr, const uint32_t* term_ids,
                                      const float* weights);
 /* Size of the compact reference table (terms in the union U). */

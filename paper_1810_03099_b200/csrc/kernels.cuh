@@ -77,7 +77,7 @@ struct RefArgs {
   const uint32_t* n;
   const uint2* ent;
   bool explicit_w;
-  uint32_t Kp;  // row stride of R (K rounded up to 4)
+  uint32_t Kp;  // row stride of R: roundup(K,4) for K <= 32, roundup(K,32) above (k2_sign.cu)
   const uint32_t* docs;
   const uint64_t* doc_off;
   const uint32_t* nnz;

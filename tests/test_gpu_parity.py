@@ -306,6 +306,8 @@ def test_validation_errors(gpu_ctx_factory):
         ctx.set_reference_docs([])
     with pytest.raises(R.ValidationError):
         ctx.set_reference_docs([5])  # >= n_docs
+    with pytest.raises(R.ValidationError, match="1..256"):
+        ctx.set_reference_docs(np.zeros(257, np.uint32))  # K above the K2 register budget
     with pytest.raises(R.ValidationError):
         ctx.mrc_pairs(0.9)  # not signed
     with pytest.raises(R.ValidationError):
