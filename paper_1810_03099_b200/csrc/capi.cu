@@ -82,7 +82,7 @@ struct refsig_gpu_ctx {
   // side streams + events for the fork/join inside count() (independent K1
   // work classes overlap instead of serialising their tails)
   cudaStream_t side[3] = {nullptr, nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_mid = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
   std::string err;
   uint64_t* h_pin = nullptr;  // pinned scratch for small D2H reads
 
@@ -93,14 +93,17 @@ struct refsig_gpu_ctx {
   std::vector<uint64_t> h_off;
   DevBuf tokens, doc_off;
   const uint32_t* tok = nullptr;
-  DevBuf tiny_docs, chunks[2], chunk_cnt, chunk_scratch, mdocs[kMergeClasses];
-  uint32_t n_tiny = 0, n_chunks[2] = {0, 0}, n_mdocs[kMergeClasses] = {};
-  uint32_t n_chunks_long = 0;  // chunks[1][0, n_chunks_long): docs of merge classes 2 and 3
-  bool k1_group = true;        // 513..8192-token docs: CTA group sorts (else chunk sorts + merges)
-  DevBuf long_docs, long_off, long_scratch;
-  DevBuf order;             // docs by decreasing length (K2 plan)
-  uint32_t n_sign_long = 0;  // order[0, n_sign_long): > kSignLongTokens tokens, one CTA each in K2
-  uint32_t n_long = 0;
+  // K1/K2/K4a work plan, one device buffer (plan), written from one pinned host
+  // buffer (h_plan) by one copy: doc lists by work class, longest docs first.
+  DevBuf plan;
+  uint32_t* h_plan = nullptr;
+  size_t h_plan_cap = 0;
+  cudaEvent_t plan_done = nullptr;  // h_plan consumed by its copy
+  enum { kPlanTiny, kPlanW8, kPlanW16, kPlanG0, kPlanG1, kPlanG2, kPlanG3, kPlanLong, kPlanOrder, kPlanLists };
+  uint32_t plan_off[kPlanLists] = {}, plan_n[kPlanLists] = {};
+  const uint32_t* plan_list(int k) const { return plan.as<uint32_t>() + plan_off[k]; }
+  DevBuf long_off, long_scratch;
+  uint32_t n_sign_long = 0;  // order[0, n_sign_long): > kSignLongTokens tokens, one CTA each in K2/K4a
 
   // K1
   bool counted = false;
@@ -179,6 +182,8 @@ struct refsig_gpu_ctx {
     for (auto e : ev_free) cudaEventDestroy(e);
     if (h_stage) cudaFreeHost(h_stage);
     if (stage_done) cudaEventDestroy(stage_done);
+    if (h_plan) cudaFreeHost(h_plan);
+    if (plan_done) cudaEventDestroy(plan_done);
     if (step_exec) cudaGraphExecDestroy(step_exec);
   }
 };
@@ -388,102 +393,95 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
   require(n_docs >= 1, "empty corpus");
   require(vocab >= 1 && vocab < 0x7fffffffu, "vocab out of range");
   require(doc_off[0] == 0, "doc_off[0] must be 0");
-  for (uint32_t d = 0; d < n_docs; ++d) require(doc_off[d + 1] >= doc_off[d], "doc_off must be non-decreasing");
+  uint64_t max_len = 0;
+  for (uint32_t d = 0; d < n_docs; ++d) {
+    require(doc_off[d + 1] >= doc_off[d], "doc_off must be non-decreasing");
+    max_len = std::max<uint64_t>(max_len, doc_off[d + 1] - doc_off[d]);
+  }
+  require(max_len < (1ull << 31), "document longer than 2^31 tokens");
   c->h_off.assign(doc_off, doc_off + n_docs + 1);
   c->n_docs = n_docs;
   c->vocab = vocab;
   c->n_tokens = doc_off[n_docs];
   c->doc_off.ensure(sizeof(uint64_t) * (n_docs + 1));
-  ck(cudaMemcpyAsync(c->doc_off.p, doc_off, sizeof(uint64_t) * (n_docs + 1), cudaMemcpyHostToDevice, c->stream),
-     "H2D doc_off");
-  // K1 work plan (host metadata only): see k1_count.cu.
-  std::vector<uint32_t> tiny, longs;
-  std::vector<uint2> chunks[2];     // warp sorts of 256 / 512 keys
-  std::vector<uint32_t> mdocs[kMergeClasses];  // multi-chunk docs by size class
+  // Work plan: documents in decreasing length (counting sort on the length
+  // for the usual corpora, a key sort otherwise; ties by id), then split by
+  // work class, each list keeping that order (longest first = fewest tails).
+  std::vector<uint32_t> order(n_docs);
+  auto len = [&](uint32_t d) { return doc_off[d + 1] - doc_off[d]; };
+  if (max_len <= (1u << 20)) {
+    std::vector<uint32_t> cnt(max_len + 2, 0);
+    for (uint32_t d = 0; d < n_docs; ++d) ++cnt[max_len - len(d) + 1];
+    for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
+    for (uint32_t d = 0; d < n_docs; ++d) order[cnt[max_len - len(d)]++] = d;
+  } else {
+    std::vector<uint64_t> key(n_docs);
+    for (uint32_t d = 0; d < n_docs; ++d) key[d] = ((max_len - len(d)) << 32) | d;
+    std::sort(key.begin(), key.end());
+    for (uint32_t d = 0; d < n_docs; ++d) order[d] = static_cast<uint32_t>(key[d]);
+  }
+  uint32_t n_class[refsig_gpu_ctx::kPlanLists] = {};
+  auto cls_of = [&](uint64_t l) -> int {
+    if (l <= kTinyMax) return refsig_gpu_ctx::kPlanTiny;
+    if (l <= 256) return refsig_gpu_ctx::kPlanW8;
+    if (l <= 512) return refsig_gpu_ctx::kPlanW16;
+    if (l <= kGroupMax) {
+      int g = 0;
+      while (l > kGroupCap[g]) ++g;
+      return refsig_gpu_ctx::kPlanG0 + g;
+    }
+    return refsig_gpu_ctx::kPlanLong;
+  };
+  for (uint32_t d = 0; d < n_docs; ++d) ++n_class[cls_of(len(d))];
+  n_class[refsig_gpu_ctx::kPlanOrder] = n_docs;
+  // one pinned staging area: doc_off (u64), then the u32 lists
+  uint32_t off = 0;
+  for (int k = 0; k < refsig_gpu_ctx::kPlanLists; ++k) {
+    c->plan_off[k] = off;
+    c->plan_n[k] = n_class[k];
+    off += n_class[k];
+  }
+  const size_t off_bytes = sizeof(uint64_t) * (n_docs + 1), list_bytes = sizeof(uint32_t) * std::max(off, 1u);
+  const size_t bytes = off_bytes + list_bytes;
+  if (!c->plan_done) ck(cudaEventCreateWithFlags(&c->plan_done, cudaEventDisableTiming), "event");
+  ck(cudaEventSynchronize(c->plan_done), "plan staging");  // the previous copy consumed h_plan
+  if (bytes > c->h_plan_cap) {
+    if (c->h_plan) cudaFreeHost(c->h_plan);
+    c->h_plan = nullptr;
+    c->h_plan_cap = 0;
+    ck(cudaMallocHost(reinterpret_cast<void**>(&c->h_plan), bytes), "cudaMallocHost");
+    c->h_plan_cap = bytes;
+  }
+  std::memcpy(c->h_plan, doc_off, off_bytes);
+  uint32_t* lists = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(c->h_plan) + off_bytes);
+  uint32_t fill[refsig_gpu_ctx::kPlanLists];
+  for (int k = 0; k < refsig_gpu_ctx::kPlanLists; ++k) fill[k] = c->plan_off[k];
   std::vector<uint64_t> loff;
   uint64_t scratch = 0;
-  for (uint32_t d = 0; d < n_docs; ++d) {
-    const uint64_t len = doc_off[d + 1] - doc_off[d];
-    require(len < (1ull << 31), "document longer than 2^31 tokens");
-    if (len <= kTinyMax) {
-      tiny.push_back(d);
-    } else if (len <= 256) {
-      chunks[0].push_back(make_uint2(d, (1u << 16) | 1u));  // whole doc, direct
-    } else if (len <= kMergeChunk) {
-      chunks[1].push_back(make_uint2(d, (1u << 16) | 1u));
-    } else if (len <= kMergeMax) {
-      int cls = 0;
-      while (len > kMergeCap[cls]) ++cls;
-      mdocs[cls].push_back(d);  // doc ids for now; chunk indices below
-    } else {
-      longs.push_back(d);
+  for (uint32_t i = 0; i < n_docs; ++i) {
+    const uint32_t d = order[i];
+    lists[fill[refsig_gpu_ctx::kPlanOrder]++] = d;
+    const int k = cls_of(len(d));
+    lists[fill[k]++] = d;
+    if (k == refsig_gpu_ctx::kPlanLong) {
       loff.push_back(scratch);
       uint64_t p = 1;
-      while (p < len) p <<= 1;
+      while (p < len(d)) p <<= 1;
       scratch += p;
     }
   }
-  auto up = [&](DevBuf& buf, const void* src, size_t bytes) {
-    if (!bytes) return;
-    buf.ensure(bytes);
-    ck(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, c->stream), "H2D plan");
-  };
-  // K2 plan: documents longest first; the long ones get a CTA each
-  std::vector<uint32_t> order(n_docs);
-  for (uint32_t d = 0; d < n_docs; ++d) order[d] = d;
-  std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
-    return doc_off[x + 1] - doc_off[x] > doc_off[y + 1] - doc_off[y];
-  });
   c->n_sign_long = 0;
-  while (c->n_sign_long < n_docs &&
-         doc_off[order[c->n_sign_long] + 1] - doc_off[order[c->n_sign_long]] > kSignLongTokens)
-    ++c->n_sign_long;
-  up(c->order, order.data(), 4ull * n_docs);
-  c->n_tiny = static_cast<uint32_t>(tiny.size());
-  up(c->tiny_docs, tiny.data(), 4 * tiny.size());
-  // 512-token chunks of merged docs: the two longest classes first (their
-  // sorts and merges run on their own streams from the fork, see do_count),
-  // then the direct 257..512 docs, then the two shorter classes. Longest docs
-  // first within a class; mdocs[k] become first-chunk indices.
-  {
-    std::vector<uint2> direct = std::move(chunks[1]);
-    chunks[1].clear();
-    auto add_class = [&](int k) {
-      std::stable_sort(mdocs[k].begin(), mdocs[k].end(), [&](uint32_t x, uint32_t y) {
-        return doc_off[x + 1] - doc_off[x] > doc_off[y + 1] - doc_off[y];
-      });
-      if (c->k1_group) return;  // group sorts take doc ids
-      for (uint32_t& d : mdocs[k]) {
-        const uint32_t m = static_cast<uint32_t>(ceil_div(doc_off[d + 1] - doc_off[d], kMergeChunk));
-        const uint32_t first = static_cast<uint32_t>(chunks[1].size());
-        for (uint32_t q = 0; q < m; ++q) chunks[1].push_back(make_uint2(d, (m << 16) | (q << 1)));
-        d = first;
-      }
-    };
-    add_class(3);
-    add_class(2);
-    c->n_chunks_long = static_cast<uint32_t>(chunks[1].size());
-    chunks[1].insert(chunks[1].end(), direct.begin(), direct.end());
-    add_class(1);
-    add_class(0);
-  }
-  for (int k = 0; k < 2; ++k) {
-    c->n_chunks[k] = static_cast<uint32_t>(chunks[k].size());
-    up(c->chunks[k], chunks[k].data(), sizeof(uint2) * chunks[k].size());
-  }
-  for (int k = 0; k < kMergeClasses; ++k) {
-    c->n_mdocs[k] = static_cast<uint32_t>(mdocs[k].size());
-    up(c->mdocs[k], mdocs[k].data(), 4 * mdocs[k].size());
-  }
-  c->chunk_cnt.ensure(4 * std::max<size_t>(chunks[1].size(), 1));
-  c->n_long = static_cast<uint32_t>(longs.size());
-  if (!longs.empty()) {
+  while (c->n_sign_long < n_docs && len(order[c->n_sign_long]) > kSignLongTokens) ++c->n_sign_long;
+  c->plan.ensure(list_bytes);
+  ck(cudaMemcpyAsync(c->doc_off.p, c->h_plan, off_bytes, cudaMemcpyHostToDevice, c->stream), "H2D doc_off");
+  ck(cudaMemcpyAsync(c->plan.p, lists, list_bytes, cudaMemcpyHostToDevice, c->stream), "H2D plan");
+  ck(cudaEventRecord(c->plan_done, c->stream), "event");
+  if (!loff.empty()) {
     c->long_scratch.ensure(sizeof(uint32_t) * scratch);
-    up(c->long_docs, longs.data(), 4 * longs.size());
-    up(c->long_off, loff.data(), 8 * loff.size());
+    c->long_off.ensure(8 * loff.size());
+    // rare (documents > 8192 tokens): a small synchronous copy
+    ck(cudaMemcpy(c->long_off.p, loff.data(), 8 * loff.size(), cudaMemcpyHostToDevice), "H2D long offsets");
   }
-  // the plan vectors are host-local: make sure the copies finished
-  ck(cudaStreamSynchronize(c->stream), "H2D metadata");
   c->loaded = true;
   c->counted = false;
   ++c->load_gen;
@@ -516,12 +514,10 @@ int refsig_gpu_create(int device, refsig_gpu_ctx** out) {
   refsig_gpu_ctx* c = new (std::nothrow) refsig_gpu_ctx();
   if (!c) return REFSIG_E_RUNTIME;
   c->device = device;
-  if (const char* m = std::getenv("REFSIG_K1_MODE")) c->k1_group = std::string(m) != "merge";
   bool ok = cudaSetDevice(device) == cudaSuccess &&
             cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) == cudaSuccess &&
             cudaMallocHost(&c->h_pin, 64) == cudaSuccess &&
-            cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
-            cudaEventCreateWithFlags(&c->ev_mid, cudaEventDisableTiming) == cudaSuccess;
+            cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess;
   for (int k = 0; ok && k < 3; ++k)
     ok = cudaStreamCreateWithFlags(&c->side[k], cudaStreamNonBlocking) == cudaSuccess &&
          cudaEventCreateWithFlags(&c->ev_join[k], cudaEventDisableTiming) == cudaSuccess;
@@ -547,7 +543,6 @@ void refsig_gpu_destroy(refsig_gpu_ctx* ctx) {
     if (ctx->ev_join[k]) cudaEventDestroy(ctx->ev_join[k]);
   }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
-  if (ctx->ev_mid) cudaEventDestroy(ctx->ev_mid);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
   delete ctx;
@@ -607,7 +602,6 @@ static void do_count(refsig_gpu_ctx* ctx, int weight_mode) {
   }
   const uint32_t N = ctx->n_docs, V = ctx->vocab;
   ctx->ent.ensure(sizeof(uint2) * std::max<uint64_t>(ctx->n_tokens, 1));
-  ctx->chunk_scratch.ensure(sizeof(uint2) * std::max<uint64_t>(ctx->n_tokens, 1));
   ctx->nnz.ensure(sizeof(uint32_t) * N);
   ctx->df.ensure(sizeof(uint32_t) * V);
   ctx->info.ensure(sizeof(TermInfo) * V);
@@ -618,46 +612,24 @@ static void do_count(refsig_gpu_ctx* ctx, int weight_mode) {
   ctx->df_rep.ensure(sizeof(uint32_t) * static_cast<size_t>(V) * reps);
   ck(cudaMemsetAsync(ctx->df_rep.p, 0, sizeof(uint32_t) * static_cast<size_t>(V) * reps, ctx->stream), "memset df");
   CountArgs a{ctx->tok, ctx->doc_off.as<uint64_t>(), V, ctx->ent.as<uint2>(), ctx->nnz.as<uint32_t>(),
-              ctx->df_rep.as<uint32_t>(), reps, ctx->flags.as<uint32_t>(), ctx->chunk_scratch.as<uint2>(),
-              ctx->chunk_cnt.as<uint32_t>()};
-  // fork: side[1] sorts the chunks of the longest docs (merge classes 2, 3)
-  // and merges them, in parallel with the bulk of the 512-token chunk sorts
-  // on the main stream (then merge classes 0, 1); tiny docs, 256-key docs and
-  // > 8192-token docs on side[0]. The long-doc merges are latency-bound (one
-  // CTA per doc), so they start as early as possible.
+              ctx->df_rep.as<uint32_t>(), reps, ctx->flags.as<uint32_t>()};
+  // fork: the two longest group classes on side[1] / side[2] (one CTA per
+  // doc: latency-bound, so they start first), the other two and the 512-key
+  // warp sorts on the main stream, tiny / 256-key / > 8192-token docs on
+  // side[0]; joined before the idf kernel.
+  using P = refsig_gpu_ctx;
   cudaStream_t m0 = ctx->stream;
   ck(cudaEventRecord(ctx->ev_fork, m0), "fork");
   for (int k = 0; k < 3; ++k) ck(cudaStreamWaitEvent(ctx->side[k], ctx->ev_fork, 0), "fork");
-  if (ctx->k1_group) {
-    // classes 3, 2 on side[1], side[2]; 1, 0 after the 512-key sorts on main
-    launch_count_group(3, a, ctx->mdocs[3].as<uint32_t>(), ctx->n_mdocs[3], ctx->side[1]);
-    launch_count_group(2, a, ctx->mdocs[2].as<uint32_t>(), ctx->n_mdocs[2], ctx->side[2]);
-    launch_count_group(1, a, ctx->mdocs[1].as<uint32_t>(), ctx->n_mdocs[1], m0);
-    launch_count_group(0, a, ctx->mdocs[0].as<uint32_t>(), ctx->n_mdocs[0], m0);
-    launch_count_chunks(16, a, ctx->chunks[1].as<uint2>(), ctx->n_chunks[1], m0);
-    launch_count_tiny(a, ctx->tiny_docs.as<uint32_t>(), ctx->n_tiny, ctx->side[0]);
-    launch_count_chunks(8, a, ctx->chunks[0].as<uint2>(), ctx->n_chunks[0], ctx->side[0]);
-    launch_count_large(a, ctx->long_docs.as<uint32_t>(), ctx->long_off.as<uint64_t>(), ctx->n_long,
-                       ctx->long_scratch.as<uint32_t>(), ctx->side[0]);
-  } else {
-  const uint32_t nl = ctx->n_chunks_long;
-  launch_count_chunks(16, a, ctx->chunks[1].as<uint2>(), nl, ctx->side[1]);
-  ck(cudaEventRecord(ctx->ev_mid, ctx->side[1]), "mid");
-  ck(cudaStreamWaitEvent(ctx->side[2], ctx->ev_mid, 0), "mid");
-  launch_count_merge(3, a, ctx->chunks[1].as<uint2>(), ctx->mdocs[3].as<uint32_t>(), ctx->n_mdocs[3], ctx->side[1]);
-  launch_count_merge(2, a, ctx->chunks[1].as<uint2>(), ctx->mdocs[2].as<uint32_t>(), ctx->n_mdocs[2], ctx->side[2]);
-  {
-    CountArgs b = a;  // chunk_sort indexes chunk_cnt by its own chunk index
-    b.chunk_cnt += nl;
-    launch_count_chunks(16, b, ctx->chunks[1].as<uint2>() + nl, ctx->n_chunks[1] - nl, m0);
-  }
-  launch_count_tiny(a, ctx->tiny_docs.as<uint32_t>(), ctx->n_tiny, ctx->side[0]);
-  launch_count_chunks(8, a, ctx->chunks[0].as<uint2>(), ctx->n_chunks[0], ctx->side[0]);
-  launch_count_large(a, ctx->long_docs.as<uint32_t>(), ctx->long_off.as<uint64_t>(), ctx->n_long,
+  launch_count_group(3, a, ctx->plan_list(P::kPlanG3), ctx->plan_n[P::kPlanG3], ctx->side[1]);
+  launch_count_group(2, a, ctx->plan_list(P::kPlanG2), ctx->plan_n[P::kPlanG2], ctx->side[2]);
+  launch_count_group(1, a, ctx->plan_list(P::kPlanG1), ctx->plan_n[P::kPlanG1], m0);
+  launch_count_group(0, a, ctx->plan_list(P::kPlanG0), ctx->plan_n[P::kPlanG0], m0);
+  launch_count_warp(16, a, ctx->plan_list(P::kPlanW16), ctx->plan_n[P::kPlanW16], m0);
+  launch_count_warp(2, a, ctx->plan_list(P::kPlanTiny), ctx->plan_n[P::kPlanTiny], ctx->side[0]);
+  launch_count_warp(8, a, ctx->plan_list(P::kPlanW8), ctx->plan_n[P::kPlanW8], ctx->side[0]);
+  launch_count_large(a, ctx->plan_list(P::kPlanLong), ctx->long_off.as<uint64_t>(), ctx->plan_n[P::kPlanLong],
                      ctx->long_scratch.as<uint32_t>(), ctx->side[0]);
-  launch_count_merge(1, a, ctx->chunks[1].as<uint2>(), ctx->mdocs[1].as<uint32_t>(), ctx->n_mdocs[1], m0);
-  launch_count_merge(0, a, ctx->chunks[1].as<uint2>(), ctx->mdocs[0].as<uint32_t>(), ctx->n_mdocs[0], m0);
-  }
   for (int k = 0; k < 3; ++k) {  // join
     ck(cudaEventRecord(ctx->ev_join[k], ctx->side[k]), "join");
     ck(cudaStreamWaitEvent(m0, ctx->ev_join[k], 0), "join");
@@ -844,7 +816,7 @@ static void do_sign(refsig_gpu_ctx* ctx) {
   ctx->inv_norm.ensure(sizeof(float) * N);
   if (ctx->db) ck(cudaStreamSynchronize(ctx->db->stream), "sync database");
   SignArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->info.as<TermInfo>(),
-             refc->R.as<float>(), N, K, refc->Kp, ctx->order.as<uint32_t>(), ctx->n_sign_long,
+             refc->R.as<float>(), N, K, refc->Kp, ctx->plan_list(refsig_gpu_ctx::kPlanOrder), ctx->n_sign_long,
              ctx->S.as<float>(), ctx->ST.as<float>(), ld, ctx->inv_norm.as<float>()};
   {
     Phase ph(ctx, REFSIG_PHASE_SIGN);
@@ -908,7 +880,7 @@ int refsig_gpu_simhash(refsig_gpu_ctx* ctx, uint64_t seed, int weight_mode, cons
     ctx->fp.ensure(8ull * ctx->n_docs);
     SimhashArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->info.as<TermInfo>(),
                   th, seed, ctx->n_docs, weight_mode == REFSIG_WEIGHT_TFIDF, ctx->fp.as<uint64_t>(),
-                  ctx->order.as<uint32_t>(), ctx->n_sign_long};
+                  ctx->plan_list(refsig_gpu_ctx::kPlanOrder), ctx->n_sign_long};
     {
       Phase ph(ctx, REFSIG_PHASE_SIMHASH);
       launch_simhash(a, ctx->stream);

@@ -22,10 +22,8 @@
 // via a suffix-min of the next head). Work plan (host-built at upload):
 //   <= 64 tokens: warp per doc, 64-key sort;
 //   65..256 / 257..512: one warp per doc sorting 256 / 512 keys in
-//     registers (IPT 8 / 16) — no merge;
-//   513..8192: every 512-token chunk sorted + run-length encoded by a warp,
-//     then one CTA per doc merges the <= 16 chunks' unique rows in shared
-//     memory (merge path) and sums equal ids;
+//     registers (IPT 8 / 16);
+//   513..8192: one CTA of 2/4/8/16 warps per doc (group_sort_kernel);
 //   > 8192: bitonic sort in a global scratch region.
 
 #include <cmath>
@@ -169,7 +167,7 @@ __device__ __forceinline__ uint32_t warp_suffix_min_excl(uint32_t x, uint32_t la
 // Returns nnz (valid in every thread). sm: >= 3*W+2 words (W > 1).
 template <int IPT, int W>
 __device__ __forceinline__ uint32_t rle_regs(const uint32_t (&v)[IPT], uint32_t t, uint32_t len, uint2* ent,
-                                             const CountArgs& ca, uint32_t* sm, bool do_df = true) {
+                                             const CountArgs& ca, uint32_t* sm) {
   const uint32_t lane = threadIdx.x & 31, w = t >> 5;
   // predecessor of v[0]
   uint32_t prev = __shfl_up_sync(0xffffffffu, v[IPT - 1], 1);
@@ -224,7 +222,7 @@ __device__ __forceinline__ uint32_t rle_regs(const uint32_t (&v)[IPT], uint32_t 
       const uint32_t rest = hmask & ~((2u << q) - 1);  // heads after q in this thread
       const uint32_t end = rest ? base + (__ffs(rest) - 1) : next;
       ent[pos] = make_uint2(v[q], end - (base + q));
-      if (do_df) df_add(ca, v[q]);
+      df_add(ca, v[q]);
       ++pos;
     }
   }
@@ -241,10 +239,14 @@ __device__ __forceinline__ uint32_t load_key(const CountArgs& a, uint64_t b, uin
   return v;
 }
 
-// One warp per document (P = 32*IPT), one document per warp (see chunk_sort_kernel).
+// One warp per document of up to P = 32*IPT tokens (IPT 2 / 8 / 16). One
+// work item per warp and no grid-stride loop: with warp-uniform control flow
+// that the compiler can see, the shuffles need no collective fallback paths
+// (which doubled the code size of the unrolled network).
 template <int IPT>
-__global__ void __launch_bounds__(256) count_warp_kernel(CountArgs a, const uint32_t* __restrict__ docs,
-                                                         uint32_t n_docs) {
+__global__ void __launch_bounds__(256, IPT <= 8 ? 6 : 4) count_warp_kernel(CountArgs a,
+                                                                           const uint32_t* __restrict__ docs,
+                                                                           uint32_t n_docs) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= n_docs) return;
@@ -277,43 +279,6 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
   return wsum + inc - v;
 }
 
-// Chunk pass: one warp per chunk of up to 32*IPT tokens. chunks[q] = {doc,
-// m<<16 | lc<<1 | direct} (m chunks in the doc, this is chunk lc). A direct
-// chunk is a whole document: its rows go straight to ent/nnz/df. Otherwise
-// the chunk's sorted unique (id,count) rows go to scratch at the chunk's own
-// token offset and chunk_cnt[q] = their number.
-// One warp per chunk and no grid-stride loop: with warp-uniform control flow
-// that the compiler can see, the shuffles need no collective fallback paths
-// (which doubled the code size of the unrolled network and thrashed the
-// instruction cache).
-template <int IPT>
-__global__ void __launch_bounds__(256, IPT <= 8 ? 6 : 4) chunk_sort_kernel(CountArgs a, const uint2* __restrict__ chunks,
-                                                                           uint32_t n_chunks) {
-  constexpr uint32_t CS = 32 * IPT;
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (q >= n_chunks) return;
-  const uint2 ch = chunks[q];
-  const uint32_t d = ch.x, c = (ch.y >> 1) & 0x7FFFu;
-  const bool direct = ch.y & 1;
-  const uint64_t b = a.doc_off[d];
-  const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
-  const uint64_t cb = b + static_cast<uint64_t>(c) * CS;
-  const uint32_t clen = min(CS, len - c * CS);
-  uint32_t v[IPT];
-#pragma unroll
-  for (int k = 0; k < IPT; ++k) v[k] = load_key(a, cb, k * 32 + lane, clen);
-  bitonic_regs<IPT>(v, lane);
-  // a direct chunk is the whole doc: final rows + df; otherwise chunk rows for the merge
-  const uint32_t n = rle_regs<IPT, 1>(v, lane, clen, direct ? a.ent + b : a.scratch + cb, a, nullptr, direct);
-  if (lane == 0) {
-    if (direct)
-      a.nnz[d] = n;
-    else
-      a.chunk_cnt[q] = n;
-  }
-}
-
 // Group pass: one CTA of W warps per document of up to 512*W tokens, sorted
 // as 512*W keys (IPT 16) in registers/shuffles/shared memory and run-length
 // encoded straight into the final rows (no chunk scratch, no merge).
@@ -333,116 +298,6 @@ __global__ void __launch_bounds__(32 * W) group_sort_kernel(CountArgs a, const u
   gbitonic_level<IPT, T, 2>(v, t, sm);
   const uint32_t n = rle_regs<IPT, W>(v, t, len, a.ent + b, a, rle_sm);
   if (t == 0) a.nnz[d] = n;
-}
-
-// Merge pass: one CTA (256 threads) per document of kMergeChunk+1..CAP tokens
-// (mdocs[q] = first chunk index; chunks of kMergeChunk tokens). The chunks'
-// sorted unique rows are loaded into shared memory back to back and merged
-// pairwise (merge path: each thread co-ranks its output range by binary
-// search, then merges serially) until one list remains; equal ids (at most
-// one per chunk, adjacent after the merge) are combined by summing counts
-// while the final rows are written. Per-thread ranges have an odd length so
-// the threads of a warp hit distinct shared-memory banks.
-template <int CAP>
-__global__ void __launch_bounds__(256) merge_kernel(CountArgs a, const uint2* __restrict__ chunks,
-                                                    const uint32_t* __restrict__ mdocs, uint32_t n_docs) {
-  extern __shared__ uint2 mbuf[];  // 2*CAP rows
-  constexpr int MAXL = CAP / kMergeChunk;
-  __shared__ uint32_t off[MAXL + 1];
-  __shared__ uint32_t scan_scratch[8];
-  const uint32_t tid = threadIdx.x;
-  for (uint32_t q = blockIdx.x; q < n_docs; q += gridDim.x) {
-    const uint32_t first = mdocs[q];
-    const uint2 ch = chunks[first];
-    const uint32_t d = ch.x, m = ch.y >> 16;
-    const uint64_t b = a.doc_off[d];
-    if (tid < 32) {  // chunk offsets: warp scan of the chunk counts
-      const uint32_t c = tid < m ? a.chunk_cnt[first + tid] : 0u;
-      const uint32_t inc = warp_inclusive_scan(c, tid);
-      if (tid < m) off[tid] = inc - c;
-      if (tid == m - 1) off[m] = inc;
-    }
-    __syncthreads();
-    const uint32_t M = off[m];
-    uint2* src = mbuf;
-    uint2* dst = mbuf + CAP;
-    for (uint32_t g = tid; g < M; g += 256) {  // all chunk loads in flight at once
-      uint32_t c = 0;
-      while (off[c + 1] <= g) ++c;
-      src[g] = a.scratch[b + static_cast<uint64_t>(c) * kMergeChunk + (g - off[c])];
-    }
-    __syncthreads();
-    const uint32_t E = ((M + 255) / 256) | 1u;
-    uint32_t nl = m;
-    while (nl > 1) {
-      uint32_t lo = min(tid * E, M);
-      const uint32_t hi = min(lo + E, M);
-      while (lo < hi) {
-        uint32_t p = 0;  // pair containing lo
-        while (off[min(2 * p + 2, nl)] <= lo) ++p;
-        const uint32_t s0 = off[2 * p], s1 = off[min(2 * p + 1, nl)], s2 = off[min(2 * p + 2, nl)];
-        const uint32_t end = min(hi, s2);
-        if (2 * p + 1 >= nl) {  // unpaired last list
-          for (uint32_t k = lo; k < end; ++k) dst[k] = src[k];
-        } else {
-          const uint2* A = src + s0;
-          const uint2* B = src + s1;
-          const uint32_t na = s1 - s0, nb = s2 - s1, diag = lo - s0;
-          uint32_t i0 = diag > nb ? diag - nb : 0, i1 = min(diag, na);
-          while (i0 < i1) {
-            const uint32_t mid = (i0 + i1) >> 1;
-            if (A[mid].x <= B[diag - mid - 1].x)
-              i0 = mid + 1;
-            else
-              i1 = mid;
-          }
-          uint32_t i = i0, j = diag - i0;
-          for (uint32_t k = lo; k < end; ++k) {
-            const bool takeA = j >= nb || (i < na && A[i].x <= B[j].x);
-            dst[k] = takeA ? A[i++] : B[j++];
-          }
-        }
-        lo = end;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        const uint32_t nn = (nl + 1) / 2;
-        for (uint32_t p = 0; p < nn; ++p) off[p] = off[2 * p];
-        off[nn] = M;
-      }
-      nl = (nl + 1) / 2;
-      uint2* t = src;
-      src = dst;
-      dst = t;
-      __syncthreads();
-    }
-    // combine equal ids (adjacent) and emit the document's rows
-    uint32_t base = 0;
-    uint2* out = a.ent + b;
-    for (uint32_t c0 = 0; c0 < M; c0 += 256 * E) {
-      const uint32_t lo = c0 + tid * E;
-      uint32_t heads = 0;
-      for (uint32_t k = 0; k < E; ++k) {
-        const uint32_t i = lo + k;
-        if (i < M && (i == 0 || src[i].x != src[i - 1].x)) ++heads;
-      }
-      uint32_t total;
-      uint32_t pos = base + block_exclusive_scan<256>(heads, scan_scratch, &total);
-      for (uint32_t k = 0; k < E; ++k) {
-        const uint32_t i = lo + k;
-        if (i < M && (i == 0 || src[i].x != src[i - 1].x)) {
-          const uint32_t key = src[i].x;
-          uint32_t cnt = src[i].y;
-          for (uint32_t e = i + 1; e < M && src[e].x == key; ++e) cnt += src[e].y;
-          out[pos++] = make_uint2(key, cnt);
-          df_add(a, key);
-        }
-      }
-      base += total;
-    }
-    if (tid == 0) a.nnz[d] = base;
-    __syncthreads();
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -580,19 +435,15 @@ int grid_for(uint64_t n, int per_sm) {
 
 }  // namespace
 
-void launch_count_tiny(const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s) {
+void launch_count_warp(int ipt, const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s) {
   if (n == 0) return;
-  count_warp_kernel<2><<<static_cast<unsigned>(ceil_div(n, 8)), 256, 0, s>>>(a, docs, n);
-  note_launch();
-}
-
-void launch_count_chunks(int ipt, const CountArgs& a, const uint2* chunks, uint32_t n, cudaStream_t s) {
-  if (n == 0) return;
-  const unsigned blocks = static_cast<unsigned>(ceil_div(n, 8));  // one warp per chunk
-  if (ipt == 8)
-    chunk_sort_kernel<8><<<blocks, 256, 0, s>>>(a, chunks, n);
+  const unsigned blocks = static_cast<unsigned>(ceil_div(n, 8));  // one warp per doc
+  if (ipt == 2)
+    count_warp_kernel<2><<<blocks, 256, 0, s>>>(a, docs, n);
+  else if (ipt == 8)
+    count_warp_kernel<8><<<blocks, 256, 0, s>>>(a, docs, n);
   else
-    chunk_sort_kernel<16><<<blocks, 256, 0, s>>>(a, chunks, n);
+    count_warp_kernel<16><<<blocks, 256, 0, s>>>(a, docs, n);
   note_launch();
 }
 
@@ -610,32 +461,6 @@ void launch_count_group(int cls, const CountArgs& a, const uint32_t* docs, uint3
       break;
     default:
       group_sort_kernel<16><<<n, 512, 0, s>>>(a, docs, n);
-      break;
-  }
-  note_launch();
-}
-
-void launch_count_merge(int cls, const CountArgs& a, const uint2* chunks, const uint32_t* mdocs, uint32_t n,
-                        cudaStream_t s) {
-  if (n == 0) return;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(merge_kernel<4096>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4096 * 8);
-    cudaFuncSetAttribute(merge_kernel<8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 8192 * 8);
-    configured = true;
-  }
-  switch (cls) {
-    case 0:
-      merge_kernel<1024><<<grid_for(n, 12), 256, 2 * 1024 * 8, s>>>(a, chunks, mdocs, n);
-      break;
-    case 1:
-      merge_kernel<2048><<<grid_for(n, 6), 256, 2 * 2048 * 8, s>>>(a, chunks, mdocs, n);
-      break;
-    case 2:
-      merge_kernel<4096><<<grid_for(n, 3), 256, 2 * 4096 * 8, s>>>(a, chunks, mdocs, n);
-      break;
-    default:
-      merge_kernel<8192><<<grid_for(n, 1), 256, 2 * 8192 * 8, s>>>(a, chunks, mdocs, n);
       break;
   }
   note_launch();

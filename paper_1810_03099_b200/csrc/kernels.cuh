@@ -15,16 +15,14 @@
 namespace refsig_gpu {
 
 // ---- K1 -------------------------------------------------------------------
-// Count work plan (k1_count.cu): tiny docs (<= kTinyMax) and whole docs up
-// to 512 tokens are sorted by one warp each; longer docs are cut into
-// kMergeChunk-token chunks and merged per doc in four shared-memory size
-// classes (<= 1024 / 2048 / 4096 / 8192 tokens); longer than kMergeMax are
-// sorted in a global scratch region.
+// Count work plan (k1_count.cu, built at upload): documents of <= 64 / 256 /
+// 512 tokens are sorted by one warp each (64 / 256 / 512 keys in registers);
+// 513..8192 tokens by one CTA of 2/4/8/16 warps (kGroupCap classes); longer
+// ones in a global scratch region.
 constexpr uint32_t kTinyMax = 64;
-constexpr uint32_t kMergeChunk = 512;
-constexpr int kMergeClasses = 4;
-constexpr uint32_t kMergeCap[kMergeClasses] = {1024, 2048, 4096, 8192};
-constexpr uint32_t kMergeMax = 8192;
+constexpr int kGroupClasses = 4;
+constexpr uint32_t kGroupCap[kGroupClasses] = {1024, 2048, 4096, 8192};
+constexpr uint32_t kGroupMax = 8192;
 
 struct CountArgs {
   const uint32_t* tokens;
@@ -35,18 +33,12 @@ struct CountArgs {
   uint32_t* df;      // [df_reps][vocab] replicas, zeroed by the caller
   uint32_t df_reps;
   uint32_t* err;     // bit 0: token id >= vocab
-  uint2* scratch;    // [T] per-chunk sorted unique rows (at the chunk's token offset)
-  uint32_t* chunk_cnt;
 };
 
-void launch_count_tiny(const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s);
-// chunks[q] = {doc, m<<16 | lc<<1 | direct}, chunks of 32*ipt tokens (ipt 8/16).
-void launch_count_chunks(int ipt, const CountArgs& a, const uint2* chunks, uint32_t n, cudaStream_t s);
-// mdocs[q] = first chunk index (in the ipt-16 chunk list) of a doc of class cls.
-// One CTA of 2/4/8/16 warps per doc of merge class cls (docs = doc ids).
+// One warp per doc, 32*ipt keys (ipt 2 / 8 / 16).
+void launch_count_warp(int ipt, const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s);
+// One CTA of 2/4/8/16 warps per doc of group class cls (docs = doc ids).
 void launch_count_group(int cls, const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s);
-void launch_count_merge(int cls, const CountArgs& a, const uint2* chunks, const uint32_t* mdocs, uint32_t n,
-                        cudaStream_t s);
 void launch_count_large(const CountArgs& a, const uint32_t* long_docs, const uint64_t* scratch_off,
                         uint32_t n_long, uint32_t* scratch, cudaStream_t s);
 // df[t] = sum of the replicas; idf32[t] = fl32(ln((1+N)/(1+df))+1) (or 1 for
