@@ -166,6 +166,11 @@ int refsig_gpu_hamming_query_pairs(refsig_gpu_ctx* q, int max_dist, uint64_t* ou
 /* Copy the first min(capacity, count) keys of the last pair call (any of the
  * *_pairs functions) to a host buffer. */
 int refsig_gpu_get_pairs(refsig_gpu_ctx* ctx, uint64_t* out_pairs, uint64_t capacity);
+/* The same pairs as CSR over rows [row_lo, row_hi) of the last pair call:
+ * rowptr[0..n] (n = row_hi-row_lo, rowptr[0] = 0) and the sorted column ids
+ * of each row in cols (up to capacity). Half the bytes of the 64-bit keys. */
+int refsig_gpu_get_pairs_csr(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_hi, uint64_t* rowptr, uint32_t* cols,
+                             uint64_t capacity, uint64_t* out_count);
 
 /* ---- device views (for frameworks / collectives; read-only) ------------------ */
 #define REFSIG_BUF_PAIRS 0      /* uint64 keys of the last pair call */

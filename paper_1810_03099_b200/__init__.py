@@ -92,6 +92,8 @@ SIGNATURES = {
     "refsig_gpu_hamming_query_pairs": ([_c.c_void_p, _c.c_int, _P(_c.c_uint64), _c.c_uint64, _P(_c.c_uint64)],
                                        _c.c_int),
     "refsig_gpu_get_pairs": ([_c.c_void_p, _P(_c.c_uint64), _c.c_uint64], _c.c_int),
+    "refsig_gpu_get_pairs_csr": ([_c.c_void_p, _c.c_uint32, _c.c_uint32, _P(_c.c_uint64), _P(_c.c_uint32), _c.c_uint64,
+                                  _P(_c.c_uint64)], _c.c_int),
     "refsig_gpu_device_buffer": ([_c.c_void_p, _c.c_int, _P(_c.c_void_p), _P(_c.c_uint64)], _c.c_int),
     "refsig_gpu_mrc_pairs_rows": ([_c.c_void_p, _c.c_float, _c.c_uint32, _c.c_uint32, _P(_c.c_uint64), _c.c_uint64,
                                    _P(_c.c_uint64)], _c.c_int),
@@ -292,6 +294,27 @@ class Context:
         if n.value:
             self._check(self._L.refsig_gpu_get_pairs(self._h, _ptr(keys, ctypes.c_uint64), n.value))
         return keys
+
+    def pairs_csr(self, row_lo: int = 0, row_hi: int | None = None, rowptr: np.ndarray | None = None,
+                  cols: np.ndarray | None = None):
+        """The last pair call's pairs as CSR over rows [row_lo, row_hi):
+        (rowptr[n+1] from 0, sorted column ids). Caller buffers (e.g. pinned)
+        may be passed; cols must hold all pairs of the rows."""
+        hi = self.n_docs if row_hi is None else row_hi
+        n_rows = hi - row_lo
+        if rowptr is None:
+            rowptr = np.empty(n_rows + 1, np.uint64)
+        n = ctypes.c_uint64()
+        if cols is None:  # size query first (capacity 0: overflow status, exact count)
+            rc = self._L.refsig_gpu_get_pairs_csr(self._h, row_lo, hi, _ptr(rowptr, ctypes.c_uint64), None, 0,
+                                                  ctypes.byref(n))
+            if rc != E_OVERFLOW:
+                self._check(rc, n.value)
+            cols = np.empty(max(n.value, 1), np.uint32)
+        rc = self._L.refsig_gpu_get_pairs_csr(self._h, row_lo, hi, _ptr(rowptr, ctypes.c_uint64),
+                                              _ptr(cols, ctypes.c_uint32), len(cols), ctypes.byref(n))
+        self._check(rc, n.value)
+        return rowptr[: n_rows + 1], cols[: n.value]
 
     def mrc_pairs(self, tau: float, out: np.ndarray | None = None, fetch: bool = True):
         """Sorted keys (i<<32|j) of all i<j with compare(S_i,S_j) >= tau."""

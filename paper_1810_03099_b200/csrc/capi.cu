@@ -124,8 +124,9 @@ struct refsig_gpu_ctx {
   uint32_t ld = 0;  // leading dimension of ST
 
   // pairs
-  DevBuf bitmap, rowcnt, rowstart, cand, scan_tmp;
+  DevBuf bitmap, rowcnt, rowstart, cand, scan_tmp, cols;
   uint64_t cand_count = 0;
+  bool have_pairs = false;  // cand/rowstart/emit_grid hold the last pair computation
 
   // simhash
   bool have_fp = false;
@@ -286,6 +287,7 @@ void upload(refsig_gpu_ctx* c, void* dst, const void* src, size_t bytes) {
 void reset_downstream(refsig_gpu_ctx* c) {
   c->have_ref = c->signed_ = c->have_fp = c->have_x = c->have_inv_norm = false;
   c->cand_count = 0;
+  c->have_pairs = false;
 }
 
 uint32_t words_per_row(uint32_t n_cols) { return static_cast<uint32_t>(ceil_div(n_cols, kTile) * 4); }
@@ -307,6 +309,7 @@ void enqueue_emit(refsig_gpu_ctx* c, const PairGrid& g) {
   }
   ck(cudaMemcpyAsync(c->h_pin, c->rowstart.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, c->stream), "D2H count");
   c->emit_pending = true;
+  c->have_pairs = false;
   c->emit_grid = g;
 }
 
@@ -326,6 +329,7 @@ int finish_emit(refsig_gpu_ctx* c, uint64_t* out, uint64_t capacity, uint64_t* o
     launched("emit");
   }
   c->cand_count = total;
+  c->have_pairs = true;
   *out_count = total;
   if (out && capacity) {
     const uint64_t m = std::min(total, capacity);
@@ -1222,6 +1226,39 @@ int refsig_gpu_get_pairs(refsig_gpu_ctx* ctx, uint64_t* out_pairs, uint64_t capa
     if (m) ck(cudaMemcpyAsync(out_pairs, ctx->cand.p, 8 * m, cudaMemcpyDeviceToHost, ctx->stream), "D2H pairs");
     sync(ctx);
   });
+}
+
+int refsig_gpu_get_pairs_csr(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_hi, uint64_t* rowptr, uint32_t* cols,
+                             uint64_t capacity, uint64_t* out_count) {
+  int rc2 = REFSIG_OK;
+  int rc = guard(ctx, [&] {
+    require(ctx->have_pairs && !ctx->emit_pending, "no finished pair computation to fetch");
+    require(rowptr != nullptr && out_count != nullptr, "NULL output");
+    require(capacity == 0 || cols != nullptr, "cols is NULL");
+    const PairGrid& g = ctx->emit_grid;
+    require(row_lo <= row_hi && row_hi <= g.n_rows, "bad row range");
+    const uint64_t n_rows = row_hi - row_lo;
+    ck(cudaMemcpyAsync(rowptr, ctx->rowstart.as<uint64_t>() + row_lo, 8 * (n_rows + 1), cudaMemcpyDeviceToHost,
+                       ctx->stream),
+       "D2H rowptr");
+    sync(ctx);
+    const uint64_t base = rowptr[0], total = rowptr[n_rows] - base;
+    for (uint64_t r = 0; r <= n_rows; ++r) rowptr[r] -= base;
+    *out_count = total;
+    const uint64_t m = std::min(total, capacity);
+    if (m) {
+      ctx->cols.ensure(4 * m);
+      launch_keys_to_cols(ctx->cand.as<uint64_t>() + base, m, ctx->cols.as<uint32_t>(), ctx->stream);
+      Phase ph(ctx, REFSIG_PHASE_D2H);
+      ck(cudaMemcpyAsync(cols, ctx->cols.p, 4 * m, cudaMemcpyDeviceToHost, ctx->stream), "D2H cols");
+    }
+    sync(ctx);
+    if (total > capacity) {
+      ctx->err = "candidate buffer overflow: " + std::to_string(total) + " pairs > capacity " + std::to_string(capacity);
+      rc2 = REFSIG_E_OVERFLOW;
+    }
+  });
+  return rc != REFSIG_OK ? rc : rc2;
 }
 
 int refsig_gpu_device_buffer(refsig_gpu_ctx* ctx, int which, void** ptr, uint64_t* bytes) {

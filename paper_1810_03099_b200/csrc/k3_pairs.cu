@@ -585,6 +585,16 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
   }
 }
 
+// cols[i] = low 32 bits of keys[i] (the column of each sorted key); 16-byte
+// loads, two keys per thread.
+__global__ void keys_to_cols_kernel(const ulonglong2* __restrict__ keys, uint64_t n2, uint2* __restrict__ cols) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n2;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const ulonglong2 k = keys[i];
+    cols[i] = make_uint2(static_cast<uint32_t>(k.x), static_cast<uint32_t>(k.y));
+  }
+}
+
 int sms() {
   int dev = 0, n = 148;
   cudaGetDevice(&dev);
@@ -683,6 +693,20 @@ void launch_hamming_bitmap(const uint64_t* f_rows, const uint64_t* f_cols, int m
   hamming_bitmap_kernel<<<static_cast<unsigned>(t), 256, 0, s>>>(f_rows, f_cols, max_dist, g, nbr, nbc, bitmap,
                                                                  rowcnt);
   note_launch();
+}
+
+void launch_keys_to_cols(const uint64_t* keys, uint64_t n, uint32_t* cols, cudaStream_t s) {
+  if (n == 0) return;
+  const uint64_t n2 = n / 2;
+  if (n2) {
+    uint64_t blocks = ceil_div(n2, 256);
+    const uint64_t cap = static_cast<uint64_t>(sms()) * 8;
+    if (blocks > cap) blocks = cap;
+    keys_to_cols_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(reinterpret_cast<const ulonglong2*>(keys), n2,
+                                                                     reinterpret_cast<uint2*>(cols));
+    note_launch();
+  }
+  if (n & 1) cudaMemcpyAsync(cols + n - 1, keys + n - 1, 4, cudaMemcpyDeviceToDevice, s);  // low word (little endian)
 }
 
 void launch_emit_pairs(const uint32_t* bitmap, const PairGrid& g, const uint32_t* rowcnt, const uint64_t* rowstart,

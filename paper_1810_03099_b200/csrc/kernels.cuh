@@ -121,6 +121,8 @@ void launch_mrc_bitmap(const float* ST_rows, uint32_t ld_rows, const float* ST_c
 void launch_hamming_bitmap(const uint64_t* f_rows, const uint64_t* f_cols, int max_dist, const PairGrid& g,
                            uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s);
 // keys (i<<32|j) in ascending order at rowstart[i]..; writes only < capacity.
+// cols[i] = (uint32)keys[i]: sorted keys -> CSR column array.
+void launch_keys_to_cols(const uint64_t* keys, uint64_t n, uint32_t* cols, cudaStream_t s);
 void launch_emit_pairs(const uint32_t* bitmap, const PairGrid& g, const uint32_t* rowcnt, const uint64_t* rowstart,
                        uint64_t* out, uint64_t capacity, cudaStream_t s);
 

@@ -375,3 +375,28 @@ def test_reference_replaced_and_union(gpu_ctx_factory):
     S3 = ctx.sign()
     ref = oracle.vectors([0, 3, 5], [1, 2, 3, 4, 5], np.ones(5))
     assert_sig_close(S3, oracle.sign(o.x, ref))
+
+
+def test_pairs_csr_matches_keys(gpu_ctx_factory):
+    """get_pairs_csr is the same sorted pair list as the 64-bit keys."""
+    cp, cfg = C.config_corpus("c1")
+    cp = cp.slice_docs(5000)
+    refs = C.sample_refs(0, cp.n_docs, 20)
+    ctx = gpu_ctx_factory()
+    ctx.load_corpus(cp.tokens, cp.doc_off, cp.vocab)
+    ctx.count()
+    ctx.set_reference_docs(refs)
+    ctx.sign(fetch=False)
+    keys = ctx.mrc_pairs(0.95)
+    rowptr, cols = ctx.pairs_csr()
+    assert rowptr[0] == 0 and rowptr[-1] == len(keys) == len(cols)
+    rows = np.repeat(np.arange(cp.n_docs, dtype=np.uint64), np.diff(rowptr).astype(np.int64))
+    assert np.array_equal((rows << np.uint64(32)) | cols.astype(np.uint64), keys)
+    # a row slice, caller buffers, and overflow reporting
+    rp, cs = ctx.pairs_csr(128, 1024)
+    lo, hi = np.searchsorted(keys >> np.uint64(32), [128, 1024])
+    assert np.array_equal(cs, (keys[lo:hi] & np.uint64(0xFFFFFFFF)).astype(np.uint32))
+    assert np.array_equal(rp, np.searchsorted(keys[lo:hi] >> np.uint64(32), np.arange(128, 1025)))
+    if len(keys) > 1:
+        with pytest.raises(R.PairOverflowError):
+            ctx.pairs_csr(cols=np.empty(len(keys) - 1, np.uint32))
