@@ -134,8 +134,7 @@ struct refsig_gpu_ctx {
 
   // exact
   bool have_x = false;
-  DevBuf x, post_off, post_fill, posts, acc_pool;
-  uint64_t acc_pool_docs = 0;
+  DevBuf x, post_off, post_fill, posts, head_col, headA, head_norm, tail_df;  // K5
 
   // query mode
   refsig_gpu_ctx* db = nullptr;
@@ -935,30 +934,52 @@ int refsig_gpu_exact_pairs(refsig_gpu_ctx* ctx, float tau_cos, uint64_t* out_pai
     require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
     const uint32_t N = ctx->n_docs, V = ctx->vocab;
     ensure_unit_weights(ctx);
-    // postings: offsets = exclusive scan of df, then an atomic fill
+    // head terms: the kExactHead highest df (ties by id), from the device df
+    const uint32_t H = std::min<uint32_t>(kExactHead, (V + 3) & ~3u);
+    std::vector<uint32_t> hdf(V);
+    ck(cudaMemcpyAsync(hdf.data(), ctx->df.p, 4ull * V, cudaMemcpyDeviceToHost, ctx->stream), "D2H df");
+    sync(ctx);
+    std::vector<uint32_t> ids(V);
+    for (uint32_t t = 0; t < V; ++t) ids[t] = t;
+    const uint32_t nh = std::min(H, V);
+    std::partial_sort(ids.begin(), ids.begin() + nh, ids.end(),
+                      [&](uint32_t a, uint32_t b) { return hdf[a] != hdf[b] ? hdf[a] > hdf[b] : a < b; });
+    std::vector<int32_t> head_col(V, -1);
+    for (uint32_t k = 0; k < nh; ++k) head_col[ids[k]] = static_cast<int32_t>(k);
+    ctx->head_col.ensure(4ull * V);
+    upload(ctx, ctx->head_col.p, head_col.data(), 4ull * V);
+    // dense head rows + their norms
+    ctx->headA.ensure(sizeof(float) * static_cast<size_t>(N) * H);
+    ctx->head_norm.ensure(sizeof(float) * N);
+    ck(cudaMemsetAsync(ctx->headA.p, 0, sizeof(float) * static_cast<size_t>(N) * H, ctx->stream), "memset A");
+    launch_head_rows(ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->x.as<float>(),
+                     ctx->head_col.as<int32_t>(), N, H, ctx->headA.as<float>(), ctx->head_norm.as<float>(),
+                     ctx->stream);
+    // tail postings: offsets = exclusive scan of the tail df, then an atomic fill
     ctx->post_off.ensure(8ull * (V + 1));
     ctx->post_fill.ensure(8ull * (V + 1));
+    ctx->tail_df.ensure(4ull * V);
     ctx->posts.ensure(sizeof(uint2) * std::max<uint64_t>(ctx->n_tokens, 1));
     ctx->scan_tmp.ensure(scan_tmp_bytes(std::max(N, V)));
-    launch_exclusive_scan_u32_to_u64(ctx->df.as<uint32_t>(), ctx->post_off.as<uint64_t>(), V, ctx->scan_tmp.p,
+    launch_tail_df(ctx->df.as<uint32_t>(), ctx->head_col.as<int32_t>(), V, ctx->tail_df.as<uint32_t>(), ctx->stream);
+    launch_exclusive_scan_u32_to_u64(ctx->tail_df.as<uint32_t>(), ctx->post_off.as<uint64_t>(), V, ctx->scan_tmp.p,
                                      ctx->stream);
     ck(cudaMemcpyAsync(ctx->post_fill.p, ctx->post_off.p, 8ull * (V + 1), cudaMemcpyDeviceToDevice, ctx->stream),
        "copy");
     launch_postings_fill(ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(),
-                         ctx->x.as<float>(), N, ctx->post_fill.as<uint64_t>(), ctx->posts.as<uint2>(), ctx->stream);
-    const uint64_t pool = static_cast<uint64_t>(exact_pool_ctas()) * N;
-    if (ctx->acc_pool.ensure(sizeof(float) * pool) || ctx->acc_pool_docs != N) {
-      ck(cudaMemsetAsync(ctx->acc_pool.p, 0, sizeof(float) * pool, ctx->stream), "memset acc");
-      ctx->acc_pool_docs = N;
-    }
+                         ctx->x.as<float>(), ctx->head_col.as<int32_t>(), N, ctx->post_fill.as<uint64_t>(),
+                         ctx->posts.as<uint2>(), ctx->stream);
     const PairGrid g = self_grid(ctx);
     {
       Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
       prepare_bitmap(ctx, g, true);
-      ExactArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->x.as<float>(),
-                  ctx->post_off.as<uint64_t>(), ctx->posts.as<uint2>(), N, tau_cos, ctx->acc_pool.as<float>(),
-                  ctx->bitmap.as<uint32_t>(), g.words_per_row, ctx->rowcnt.as<uint32_t>()};
-      launch_exact_rows(a, 0, N, ctx->stream);
+      ExactArgs a{ctx->ent.as<uint2>(),        ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(),
+                  ctx->x.as<float>(),          ctx->head_col.as<int32_t>(), ctx->post_off.as<uint64_t>(),
+                  ctx->posts.as<uint2>(),      ctx->headA.as<float>(),      ctx->head_norm.as<float>(),
+                  H,                           N,                           std::min<uint32_t>(N, kExactPanel),
+                  tau_cos,                     ctx->bitmap.as<uint32_t>(),  g.words_per_row,
+                  ctx->rowcnt.as<uint32_t>()};
+      launch_exact_tail(a, 0, N, ctx->stream);
       launched("exact");
     }
     rc2 = run_emit(ctx, g, out_pairs, capacity, out_count);

@@ -143,26 +143,36 @@ struct SimhashArgs {
 void launch_simhash(const SimhashArgs& a, cudaStream_t s);
 
 // ---- K5 exact cosine --------------------------------------------------------
+constexpr uint32_t kExactHead = 64;     // dense head terms (highest df)
+constexpr uint32_t kExactPanel = 49152;  // docs per shared-memory column panel (192 KB)
 struct ExactArgs {
   const uint2* ent;
   const uint64_t* doc_off;
   const uint32_t* nnz;
-  const float* x;          // unit weights aligned with ent (padded CSR)
-  const uint64_t* post_off;  // [vocab+1] postings offsets (exclusive scan of df)
-  const uint2* posts;      // (doc, x bits) per posting
+  const float* x;            // unit weights aligned with ent (padded CSR)
+  const int32_t* head_col;   // [vocab] column in A of a head term, -1 for tail terms
+  const uint64_t* post_off;  // [vocab+1] tail postings offsets (exclusive scan of tail df)
+  const uint2* posts;        // (doc, x bits) per tail posting
+  const float* A;            // [n_docs][H] dense head rows
+  const float* hn;           // [n_docs] norm of the head part
+  uint32_t H;                // multiple of 4
   uint32_t n_docs;
+  uint32_t panel;            // column panel (docs)
   float tau;
-  float* acc_pool;         // exact_pool_ctas() * n_docs floats, zero on entry and exit
-  uint32_t* bitmap;        // zeroed rows, words_per_row words each
+  uint32_t* bitmap;          // zeroed rows, words_per_row words each
   uint32_t words_per_row;
   uint32_t* rowcnt;
 };
-uint32_t exact_pool_ctas();
 void launch_unit_weights(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const TermInfo* info,
                          const float* inv_norm, uint32_t n_docs, float* x, cudaStream_t s);
+// Tail postings (head_col NULL: all terms).
 void launch_postings_fill(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const float* x,
-                          uint32_t n_docs, uint64_t* fill, uint2* posts, cudaStream_t s);
-void launch_exact_rows(const ExactArgs& a, uint32_t row_lo, uint32_t row_hi, cudaStream_t s);
+                          const int32_t* head_col, uint32_t n_docs, uint64_t* fill, uint2* posts, cudaStream_t s);
+void launch_tail_df(const uint32_t* df, const int32_t* head_col, uint32_t vocab, uint32_t* tdf, cudaStream_t s);
+void launch_head_rows(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const float* x,
+                      const int32_t* head_col, uint32_t n_docs, uint32_t H, float* A, float* hn, cudaStream_t s);
+// Rows [row_lo, row_hi): tail accumulation, bound, head dot, threshold into the bitmap.
+void launch_exact_tail(const ExactArgs& a, uint32_t row_lo, uint32_t row_hi, cudaStream_t s);
 void launch_pair_cosines(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const float* x,
                          const uint64_t* keys, uint64_t n_keys, float* out, cudaStream_t s);
 
