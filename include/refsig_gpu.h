@@ -86,6 +86,18 @@ int refsig_gpu_load_corpus(refsig_gpu_ctx* ctx, const uint32_t* tokens, const ui
 int refsig_gpu_load_corpus_device(refsig_gpu_ctx* ctx, const uint32_t* d_tokens, const uint64_t* doc_off,
                                   uint32_t n_docs, uint32_t vocab);
 
+/* ---- text front end -----------------------------------
+ * Raw documents text[byte_off[d] .. byte_off[d+1]) (HOST pointers): the corpus
+ * becomes each document's character 3-grams — normalize (ngram.hpp:114-129) +
+ * extract_3grams (ngram.hpp:149-180), ids ((c0*26)+c1)*26+c2 < 17576 — in
+ * document order, so count() yields exactly the reference's NgramVector
+ * entries; vocab = 17576. The bytes stay resident for simhash_text. */
+int refsig_gpu_load_text(refsig_gpu_ctx* ctx, const uint8_t* text, const uint64_t* byte_off, uint32_t n_docs);
+/* Per-document simhash(extract_words(normalize(text))) (simhash.hpp:35-45,
+ * word_hash64 = first 8 MD5 bytes big-endian, simhash.hpp:23-29) of the text
+ * loaded by refsig_gpu_load_text; read with refsig_gpu_get_fingerprints. */
+int refsig_gpu_simhash_text(refsig_gpu_ctx* ctx);
+
 /* ---- K1: counts, df, idf (A2-A4) ------------------------------------------ */
 int refsig_gpu_count(refsig_gpu_ctx* ctx, int weight_mode);
 /* Compact CSR of the per-doc sorted (id,count) rows, exactly the reference's

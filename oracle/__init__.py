@@ -75,6 +75,12 @@ def lib():
         L.orc_exact_pairs.argtypes = [u64p, u32p, f64p, f64p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_double,
                                       ctypes.c_double, ctypes.c_uint32, ctypes.c_uint32, P(_Pairs), ctypes.c_int]
         L.orc_cosine_pairs.argtypes = [u64p, u32p, f64p, f64p, u64p, ctypes.c_uint64, f64p, ctypes.c_int]
+        u8p = P(ctypes.c_uint8)
+        L.orc_text_grams.argtypes = [u8p, u64p, ctypes.c_uint32, u32p, u64p]
+        L.orc_text_grams.restype = ctypes.c_uint64
+        L.orc_word_hash64.argtypes = [u8p, ctypes.c_uint64]
+        L.orc_word_hash64.restype = ctypes.c_uint64
+        L.orc_text_simhash.argtypes = [u8p, u64p, ctypes.c_uint32, u64p, ctypes.c_int]
         _orc = L
     return _orc
 
@@ -251,6 +257,37 @@ def simhash(c: Counts, idf: np.ndarray | None, seed: int = 0, table: np.ndarray 
     lib().orc_simhash(_p(c.rowptr, ctypes.c_uint64), _p(c.ids, ctypes.c_uint32), _p(c.counts, ctypes.c_uint32),
                       c.n_docs, _p(idf, ctypes.c_float) if idf is not None else None, seed,
                       _p(table, ctypes.c_uint64) if table is not None else None, _p(fp, ctypes.c_uint64), threads)
+    return fp
+
+
+def text_grams(text: np.ndarray, off: np.ndarray):
+    """3-gram id stream per doc of raw text bytes (ngram.hpp:114-180):
+    (tokens u32, gram_off u64[n+1]); vocabulary 26^3 = 17576."""
+    text = np.ascontiguousarray(text, np.uint8)
+    off = np.ascontiguousarray(off, np.uint64)
+    n = len(off) - 1
+    gram_off = np.empty(n + 1, np.uint64)
+    tot = lib().orc_text_grams(_p(text, ctypes.c_uint8), _p(off, ctypes.c_uint64), n, None,
+                               _p(gram_off, ctypes.c_uint64))
+    tokens = np.empty(max(tot, 1), np.uint32)
+    lib().orc_text_grams(_p(text, ctypes.c_uint8), _p(off, ctypes.c_uint64), n, _p(tokens, ctypes.c_uint32),
+                         _p(gram_off, ctypes.c_uint64))
+    return tokens[:tot], gram_off
+
+
+def word_hash64(word: bytes) -> int:
+    """First 8 bytes of MD5(word), big-endian (simhash.hpp:23-29)."""
+    b = np.frombuffer(word, np.uint8) if len(word) else np.zeros(1, np.uint8)
+    return int(lib().orc_word_hash64(_p(np.ascontiguousarray(b), ctypes.c_uint8), len(word)))
+
+
+def text_simhash(text: np.ndarray, off: np.ndarray, threads: int = 0) -> np.ndarray:
+    """simhash(extract_words(normalize(doc))) per doc (simhash.hpp:35-45)."""
+    text = np.ascontiguousarray(text, np.uint8)
+    off = np.ascontiguousarray(off, np.uint64)
+    fp = np.empty(len(off) - 1, np.uint64)
+    lib().orc_text_simhash(_p(text, ctypes.c_uint8), _p(off, ctypes.c_uint64), len(off) - 1, _p(fp, ctypes.c_uint64),
+                           threads)
     return fp
 
 

@@ -384,4 +384,116 @@ void orc_cosine_pairs(const uint64_t* rowptr, const uint32_t* ids, const double*
   });
 }
 
+
+// ---- Text front end ----------------------------------
+// normalize (ngram.hpp:114-129): ASCII letters lowercased, every maximal run
+// of other bytes is a word break. A 3-gram is any window of three letters
+// inside one word (ngram.hpp:149-166, id = ((c0*26)+c1)*26+c2 over 'a'..'z',
+// ngram.hpp:33-37), so on the raw bytes: three consecutive letters.
+static inline int orc_letter(uint8_t c) {
+  if (c >= 'A' && c <= 'Z') return c - 'A';
+  if (c >= 'a' && c <= 'z') return c - 'a';
+  return -1;
+}
+
+// Per doc the 3-gram ids in document order (before sorting). gram_off[n+1].
+// tokens may be NULL (counts only). Returns the total.
+uint64_t orc_text_grams(const uint8_t* bytes, const uint64_t* off, uint32_t n, uint32_t* tokens, uint64_t* gram_off) {
+  uint64_t k = 0;
+  for (uint32_t d = 0; d < n; ++d) {
+    gram_off[d] = k;
+    for (uint64_t p = off[d]; p + 3 <= off[d + 1]; ++p) {
+      int a = orc_letter(bytes[p]), b = orc_letter(bytes[p + 1]), c = orc_letter(bytes[p + 2]);
+      if (a >= 0 && b >= 0 && c >= 0) {
+        if (tokens) tokens[k] = static_cast<uint32_t>((a * 26 + b) * 26 + c);
+        ++k;
+      }
+    }
+  }
+  gram_off[n] = k;
+  return k;
+}
+
+// MD5 (RFC 1321), restated: 64-byte blocks, little-endian words, four rounds
+// of 16 steps with the sine table T[i] = floor(2^32 |sin(i+1)|).
+static void orc_md5(const uint8_t* msg, uint64_t len, uint8_t digest[16]) {
+  static uint32_t T[64];
+  static bool init = false;
+  if (!init) {
+    for (int i = 0; i < 64; ++i) T[i] = static_cast<uint32_t>(std::floor(std::fabs(std::sin(i + 1.0)) * 4294967296.0));
+    init = true;
+  }
+  static const int R[4][4] = {{7, 12, 17, 22}, {5, 9, 14, 20}, {4, 11, 16, 23}, {6, 10, 15, 21}};
+  uint32_t h0 = 0x67452301u, h1 = 0xefcdab89u, h2 = 0x98badcfeu, h3 = 0x10325476u;
+  const uint64_t nblk = (len + 8) / 64 + 1;
+  for (uint64_t blk = 0; blk < nblk; ++blk) {
+    uint8_t buf[64];
+    for (int i = 0; i < 64; ++i) {
+      const uint64_t q = blk * 64 + i;
+      uint8_t v = 0;
+      if (q < len) v = msg[q];
+      else if (q == len) v = 0x80;
+      else if (q >= nblk * 64 - 8) v = static_cast<uint8_t>((len * 8) >> (8 * (q - (nblk * 64 - 8))));
+      buf[i] = v;
+    }
+    uint32_t M[16];
+    for (int i = 0; i < 16; ++i)
+      M[i] = buf[4 * i] | (buf[4 * i + 1] << 8) | (buf[4 * i + 2] << 16) | (static_cast<uint32_t>(buf[4 * i + 3]) << 24);
+    uint32_t a = h0, b = h1, c = h2, d = h3;
+    for (int i = 0; i < 64; ++i) {
+      uint32_t f;
+      int g;
+      if (i < 16) { f = (b & c) | (~b & d); g = i; }
+      else if (i < 32) { f = (d & b) | (~d & c); g = (5 * i + 1) % 16; }
+      else if (i < 48) { f = b ^ c ^ d; g = (3 * i + 5) % 16; }
+      else { f = c ^ (b | ~d); g = (7 * i) % 16; }
+      const uint32_t x = a + f + T[i] + M[g];
+      const int r = R[i / 16][i % 4];
+      a = d;
+      d = c;
+      c = b;
+      b = b + ((x << r) | (x >> (32 - r)));
+    }
+    h0 += a; h1 += b; h2 += c; h3 += d;
+  }
+  const uint32_t h[4] = {h0, h1, h2, h3};
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) digest[4 * i + j] = static_cast<uint8_t>(h[i] >> (8 * j));
+}
+
+// word_hash64 (simhash.hpp:23-29): the first 8 digest bytes, big-endian.
+uint64_t orc_word_hash64(const uint8_t* word, uint64_t len) {
+  uint8_t dg[16];
+  orc_md5(word, len, dg);
+  uint64_t h = 0;
+  for (int i = 0; i < 8; ++i) h = (h << 8) | dg[i];
+  return h;
+}
+
+// simhash(extract_words(normalize(text))) per doc (simhash.hpp:35-45,
+// ngram.hpp:132-145): words are the lowercased maximal letter runs, every
+// occurrence votes +-1 per bit column, bit = column > 0, no words -> 0.
+void orc_text_simhash(const uint8_t* bytes, const uint64_t* off, uint32_t n, uint64_t* fp, int threads) {
+  parallel_rows(0, n, threads, 64, [&](uint64_t d, int) {
+    int64_t col[64] = {0};
+    std::vector<uint8_t> w;
+    auto flush = [&]() {
+      if (w.empty()) return;
+      const uint64_t h = orc_word_hash64(w.data(), w.size());
+      for (int j = 0; j < 64; ++j) col[j] += (h >> j & 1u) ? 1 : -1;
+      w.clear();
+    };
+    for (uint64_t p = off[d]; p < off[d + 1]; ++p) {
+      const int l = orc_letter(bytes[p]);
+      if (l >= 0) w.push_back(static_cast<uint8_t>('a' + l));
+      else flush();
+    }
+    flush();
+    uint64_t out = 0;
+    for (int j = 0; j < 64; ++j)
+      if (col[j] > 0) out |= 1ull << j;
+    fp[d] = out;
+  });
+}
+
 }  // extern "C"

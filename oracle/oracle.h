@@ -106,6 +106,14 @@ int orc_exact_pairs(const uint64_t* rowptr, const uint32_t* ids, const double* w
 void orc_cosine_pairs(const uint64_t* rowptr, const uint32_t* ids, const double* w, const double* norm,
                       const uint64_t* keys, uint64_t n_keys, double* out, int threads);
 
+/* Text front end (ngram.hpp:114-180, simhash.hpp:23-45): per doc the 3-gram
+ * ids in document order (tokens may be NULL), gram_off[n+1]; returns the total. */
+uint64_t orc_text_grams(const uint8_t* bytes, const uint64_t* off, uint32_t n, uint32_t* tokens, uint64_t* gram_off);
+/* word_hash64: first 8 bytes of MD5(word), big-endian (RFC 1321 restated). */
+uint64_t orc_word_hash64(const uint8_t* word, uint64_t len);
+/* simhash over each doc's normalized words, per occurrence +-1. */
+void orc_text_simhash(const uint8_t* bytes, const uint64_t* off, uint32_t n, uint64_t* fp, int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -92,6 +92,8 @@ SIGNATURES = {
     "refsig_gpu_hamming_query_pairs": ([_c.c_void_p, _c.c_int, _P(_c.c_uint64), _c.c_uint64, _P(_c.c_uint64)],
                                        _c.c_int),
     "refsig_gpu_get_pairs": ([_c.c_void_p, _P(_c.c_uint64), _c.c_uint64], _c.c_int),
+    "refsig_gpu_load_text": ([_c.c_void_p, _P(_c.c_uint8), _P(_c.c_uint64), _c.c_uint32], _c.c_int),
+    "refsig_gpu_simhash_text": ([_c.c_void_p], _c.c_int),
     "refsig_gpu_get_pairs_csr": ([_c.c_void_p, _c.c_uint32, _c.c_uint32, _P(_c.c_uint64), _P(_c.c_uint32), _c.c_uint64,
                                   _P(_c.c_uint64)], _c.c_int),
     "refsig_gpu_device_buffer": ([_c.c_void_p, _c.c_int, _P(_c.c_void_p), _P(_c.c_uint64)], _c.c_int),
@@ -377,6 +379,25 @@ class Context:
     @staticmethod
     def launch_count() -> int:
         return load_library().refsig_gpu_launch_count()
+
+    def load_text(self, text, byte_off: np.ndarray):
+        """Raw documents text[byte_off[d]:byte_off[d+1]] (bytes or uint8 array):
+        the corpus becomes their character 3-grams (vocab 17576)."""
+        t = np.frombuffer(text, np.uint8) if isinstance(text, (bytes, bytearray)) else np.ascontiguousarray(text, np.uint8)
+        off = np.ascontiguousarray(byte_off, np.uint64)
+        if len(off) < 2 or int(off[-1]) > len(t):
+            raise ValidationError("byte_off must have n_docs+1 entries within the text")
+        if len(t) == 0:
+            t = np.zeros(1, np.uint8)
+        self._check(self._L.refsig_gpu_load_text(self._h, _ptr(t, ctypes.c_uint8), _ptr(off, ctypes.c_uint64),
+                                                 len(off) - 1))
+        self.n_docs = len(off) - 1
+        self.vocab = 26 ** 3
+
+    def simhash_text(self, fetch: bool = True):
+        """Per-document simhash of the loaded text's words (MD5, +-1 votes)."""
+        self._check(self._L.refsig_gpu_simhash_text(self._h))
+        return self.fingerprints() if fetch else None
 
     def simhash(self, seed: int = 0, weighting: int = WEIGHT_TFIDF, term_hash: np.ndarray | None = None,
                 fetch: bool = True):

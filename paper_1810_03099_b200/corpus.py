@@ -147,3 +147,59 @@ def config_corpus(name: str, threads: int = 0) -> tuple[Corpus, dict]:
         base = cfgs[c["same_corpus_as"]]
         return generate(base["corpus"], threads), {**base, **c}
     return generate(c["corpus"], threads), c
+
+
+# ---------------------------------------------------------------------------
+# Synthetic raw text for the text front end (tests, bench). Each term id maps to
+# a fixed pseudo-word (base-26 letters); words are joined by separators drawn
+# from a seeded generator (spaces, punctuation, digits, newlines, a two-byte
+# UTF-8 letter that the reference's ASCII normalize treats as a break), with
+# some capitalised words. No dataset text is involved.
+_SEPS = [b" ", b" ", b" ", b" ", b", ", b". ", b"\n", b" - ", b"; ", b" 42 ", b"\xc3\xa9", b"'", b"(", b") "]
+
+
+def term_word(t: int) -> str:
+    """Deterministic word for term id t: bijective base-26 letters (>= 1 char)."""
+    s = ""
+    t += 1
+    while t > 0:
+        t, r = divmod(t - 1, 26)
+        s = chr(ord("a") + r) + s
+    return s
+
+
+def synth_text(tokens: np.ndarray, doc_off: np.ndarray, vocab: int, seed: int = 0):
+    """(text uint8, byte_off uint64) with one word per token, vectorised."""
+    rng = np.random.default_rng(seed)
+    words = [term_word(t).encode() for t in range(vocab)]
+    wlen = np.fromiter((len(w) for w in words), np.int64, vocab)
+    wstart = np.zeros(vocab + 1, np.int64)
+    np.cumsum(wlen, out=wstart[1:])
+    wbytes = np.frombuffer(b"".join(words), np.uint8)
+    sep_b = [np.frombuffer(x, np.uint8) for x in _SEPS]
+    slen = np.array([len(x) for x in _SEPS], np.int64)
+    sstart = np.zeros(len(_SEPS) + 1, np.int64)
+    np.cumsum(slen, out=sstart[1:])
+    sbytes = np.concatenate(sep_b)
+    T = len(tokens)
+    sep = rng.integers(0, len(_SEPS), T)
+    tok = tokens.astype(np.int64)
+    piece = wlen[tok] + slen[sep]
+    pstart = np.zeros(T + 1, np.int64)
+    np.cumsum(piece, out=pstart[1:])
+    out = np.empty(pstart[-1], np.uint8)
+    # word bytes
+    wl = wlen[tok]
+    idx = np.repeat(pstart[:-1], wl) + (np.arange(wl.sum()) - np.repeat(np.cumsum(wl) - wl, wl))
+    src = np.repeat(wstart[tok], wl) + (np.arange(wl.sum()) - np.repeat(np.cumsum(wl) - wl, wl))
+    out[idx] = wbytes[src]
+    # separator bytes
+    sl = slen[sep]
+    idx = np.repeat(pstart[:-1] + wl, sl) + (np.arange(sl.sum()) - np.repeat(np.cumsum(sl) - sl, sl))
+    src = np.repeat(sstart[sep], sl) + (np.arange(sl.sum()) - np.repeat(np.cumsum(sl) - sl, sl))
+    out[idx] = sbytes[src]
+    # capitalise ~10% of the words (first letter)
+    cap = rng.random(T) < 0.1
+    out[pstart[:-1][cap]] -= 32
+    byte_off = pstart[doc_off.astype(np.int64)].astype(np.uint64)
+    return out, byte_off

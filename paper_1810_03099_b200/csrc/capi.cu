@@ -130,6 +130,10 @@ struct refsig_gpu_ctx {
 
   // simhash
   bool have_fp = false;
+  // text front end: the raw corpus stays resident for simhash_text
+  DevBuf text, text_off, text_cnt;
+  uint32_t text_docs = 0;
+  bool have_text = false;
   DevBuf fp, term_hash;
 
   // exact
@@ -403,6 +407,7 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
   }
   require(max_len < (1ull << 31), "document longer than 2^31 tokens");
   c->h_off.assign(doc_off, doc_off + n_docs + 1);
+  c->have_text = false;  // refsig_gpu_load_text sets it after this
   c->n_docs = n_docs;
   c->vocab = vocab;
   c->n_tokens = doc_off[n_docs];
@@ -890,6 +895,57 @@ int refsig_gpu_simhash(refsig_gpu_ctx* ctx, uint64_t seed, int weight_mode, cons
       launched("simhash");
     }
     if (term_hash) ck(cudaStreamSynchronize(ctx->stream), "simhash");
+    ctx->have_fp = true;
+  });
+}
+
+int refsig_gpu_load_text(refsig_gpu_ctx* ctx, const uint8_t* text, const uint64_t* byte_off, uint32_t n_docs) {
+  return guard(ctx, [&] {
+    require(byte_off != nullptr, "byte_off is NULL");
+    require(n_docs >= 1, "empty corpus");
+    require(byte_off[0] == 0, "byte_off[0] must be 0");
+    for (uint32_t d = 0; d < n_docs; ++d) require(byte_off[d + 1] >= byte_off[d], "byte_off must be non-decreasing");
+    const uint64_t B = byte_off[n_docs];
+    require(text != nullptr || B == 0, "text is NULL");
+    ctx->text.ensure(std::max<uint64_t>(B, 1));
+    ctx->text_off.ensure(8ull * (n_docs + 1));
+    ctx->text_cnt.ensure(4ull * n_docs);
+    {
+      Phase ph(ctx, REFSIG_PHASE_H2D);
+      if (B) ck(cudaMemcpyAsync(ctx->text.p, text, B, cudaMemcpyHostToDevice, ctx->stream), "H2D text");
+      ck(cudaMemcpyAsync(ctx->text_off.p, byte_off, 8ull * (n_docs + 1), cudaMemcpyHostToDevice, ctx->stream),
+         "H2D text offsets");
+    }
+    // pass 1: 3-grams per doc -> host offsets (the K1 plan needs them)
+    launch_text_grams(ctx->text.as<uint8_t>(), ctx->text_off.as<uint64_t>(), n_docs, nullptr,
+                      ctx->text_cnt.as<uint32_t>(), nullptr, ctx->stream);
+    std::vector<uint32_t> cnt(n_docs);
+    ck(cudaMemcpyAsync(cnt.data(), ctx->text_cnt.p, 4ull * n_docs, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    sync(ctx);
+    std::vector<uint64_t> goff(n_docs + 1, 0);
+    for (uint32_t d = 0; d < n_docs; ++d) goff[d + 1] = goff[d] + cnt[d];
+    ctx->tokens.ensure(sizeof(uint32_t) * std::max<uint64_t>(goff[n_docs], 1));
+    ctx->tok = ctx->tokens.as<uint32_t>();
+    load_common(ctx, goff.data(), n_docs, kGramSpace);  // uploads the gram offsets to ctx->doc_off
+    // pass 2: the 3-gram ids in document order
+    launch_text_grams(ctx->text.as<uint8_t>(), ctx->text_off.as<uint64_t>(), n_docs, ctx->doc_off.as<uint64_t>(),
+                      nullptr, ctx->tokens.as<uint32_t>(), ctx->stream);
+    launched("text grams");
+    ctx->text_docs = n_docs;
+    ctx->have_text = true;
+  });
+}
+
+int refsig_gpu_simhash_text(refsig_gpu_ctx* ctx) {
+  return guard(ctx, [&] {
+    require(ctx->have_text && ctx->loaded && ctx->text_docs == ctx->n_docs, "load_text() not called");
+    ctx->fp.ensure(8ull * ctx->n_docs);
+    {
+      Phase ph(ctx, REFSIG_PHASE_SIMHASH);
+      launch_text_simhash(ctx->text.as<uint8_t>(), ctx->text_off.as<uint64_t>(), ctx->n_docs, ctx->fp.as<uint64_t>(),
+                          ctx->stream);
+      launched("text simhash");
+    }
     ctx->have_fp = true;
   });
 }

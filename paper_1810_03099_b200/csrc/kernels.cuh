@@ -14,6 +14,15 @@
 
 namespace refsig_gpu {
 
+// ---- text front end (k0_text.cu) -------------------------------------------
+// Per doc of raw bytes [off[d], off[d+1]): tokens == NULL -> cnt[d] = number of
+// 3-grams; else the 3-gram ids (vocabulary 17576) at tokens[gram_off[d] ..).
+void launch_text_grams(const uint8_t* text, const uint64_t* off, uint32_t n_docs, const uint64_t* gram_off,
+                       uint32_t* cnt, uint32_t* tokens, cudaStream_t s);
+// fp[d] = simhash of the doc's normalized words (MD5 word hashes, +-1 votes).
+void launch_text_simhash(const uint8_t* text, const uint64_t* off, uint32_t n_docs, uint64_t* fp, cudaStream_t s);
+constexpr uint32_t kGramSpace = 26u * 26u * 26u;  // ngram.hpp: 17576 3-grams
+
 // ---- K1 -------------------------------------------------------------------
 // Count work plan (k1_count.cu, built at upload): documents of <= 64 / 256 /
 // 512 tokens are sorted by one warp each (64 / 256 / 512 keys in registers);

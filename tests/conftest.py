@@ -37,6 +37,11 @@ def golden_small():
 
 
 @pytest.fixture(scope="session")
+def golden_text():
+    return dict(np.load(os.path.join(GOLDEN, "text_small.npz")))
+
+
+@pytest.fixture(scope="session")
 def spec_examples():
     import json
     with open(os.path.join(GOLDEN, "spec_examples.json")) as f:

@@ -178,5 +178,48 @@ def main():
     print("wrote", os.listdir(HERE))
 
 
+def text_fixture(R):
+    """text_small.npz: seeded synthetic raw text (corpus.synth_text over a
+    configs[0]-shaped corpus) plus edge documents, with the reference's
+    extract_3grams(normalize(doc)) entries and simhash(words) per doc, and
+    word_hash64 of words at the MD5 padding edges."""
+    cfg = C.load_configs()["configs"]["c0"]["corpus"].copy()
+    cfg["n_docs"] = 200
+    cp = C.generate(cfg, threads=1)
+    txt, off = C.synth_text(cp.tokens, cp.doc_off, cp.vocab, seed=7)
+    docs = [bytes(txt[off[d]:off[d + 1]]) for d in range(cp.n_docs)]
+    docs += [b"", b"!!! ... ,,, 123 456", b"AbC dEF-ghi", b"x" * 70 + b" " + b"y" * 55 + b"." + b"Z" * 56,
+             "na\u00efve caf\u00e9 r\u00e9sum\u00e9 \u00fcber".encode(), b"ab", b"abc", b"a-b-c-d-e",
+             b"The the THE tHe", b"  leading and trailing  ", b"q" * 64 + b"," + b"w" * 63 + b";" + b"e" * 65]
+    text = np.frombuffer(b"".join(docs), np.uint8)
+    boff = np.zeros(len(docs) + 1, np.uint64)
+    np.cumsum([len(x) for x in docs], out=boff[1:])
+    rowptr = [0]
+    ids, cnts, fps = [], [], []
+    for x in docs:
+        cap = len(x) + 8
+        oi = np.empty(cap, np.uint32)
+        oc = np.empty(cap, np.uint32)
+        k = R.ref_extract_3grams(x, len(x), oi.ctypes.data_as(U32), oc.ctypes.data_as(U32), cap)
+        ids.append(oi[:k].copy())
+        cnts.append(oc[:k].copy())
+        rowptr.append(rowptr[-1] + k)
+        nb = ctypes.create_string_buffer(len(x) + 1)
+        m = R.ref_normalize(x, len(x), nb, len(x) + 1)
+        words = [w for w in nb.raw[:m].decode().split(" ") if w]
+        fps.append(ref_simhash_words(R, words))
+    edge_words = ["a", "ab", "abc", "x" * 55, "x" * 56, "x" * 63, "x" * 64, "x" * 65, "y" * 119, "y" * 120,
+                  "z" * 200]
+    np.savez_compressed(os.path.join(HERE, "text_small.npz"), text=text, byte_off=boff,
+                        rowptr=np.array(rowptr, np.uint64), ids=np.concatenate(ids).astype(np.uint32),
+                        counts=np.concatenate(cnts).astype(np.uint32), fp=np.array(fps, np.uint64),
+                        words=np.array(edge_words), word_hash=np.array([ref_hash(R, w) for w in edge_words],
+                                                                       np.uint64))
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "text":
+        text_fixture(oracle.ref_lib())
+    else:
+        main()
+        text_fixture(oracle.ref_lib())
