@@ -299,6 +299,7 @@ def run_ours(args):
     # The rival path (§8 row d): Simhash + Hamming all-pairs on the same corpus
     # (not part of the MRC step; reported per kernel).
     rivals = measure_rivals(ctx, stream, flush, dev, thr, reps=max(5, args.steps))
+    text_fe = measure_text_front_end(cp, stream, dev, reps=max(3, args.steps // 2)) if world == 1 else None
 
     # End to end through the public API with HOST buffers: pinned tokens H2D,
     # full pipeline, candidate keys D2H into pinned memory.
@@ -318,6 +319,8 @@ def run_ours(args):
                          clock_mhz, ms_per_step, n_cand)
         roof.update(rival_rooflines(rivals, N, P if world == 1 else my_pairs, cp, peaks, peaks_src, n_sm,
                                     clock_mhz))
+        if text_fe:
+            roof["text_front_end"] = text_fe
         traffic = load_traffic()
         for k, r in roof.items():
             r["traffic"] = traffic.get(k)
@@ -406,6 +409,45 @@ def measure_e2e(ctx, cp, refs, tau, lo, hi, stream, dev, steps, warmup):
         d2h = n * 4 + (hi - lo + 1) * 8 if mode == "csr" else n * 8 + 8
         res[mode] = {"_ms": 1e3 * sum(times) / len(times), "h2d": int(h2d), "d2h": int(d2h)}
     return res
+
+
+def measure_text_front_end(cp, stream, dev, reps):
+    """Raw text -> 3-gram corpus (load_text: H2D + count pass + host offsets +
+    write pass) and the MD5 word Simhash, on seeded synthetic text with one
+    word per configs[1] token (corpus.synth_text). load_text is host wall
+    clock (it synchronises once for the per-doc gram counts); simhash_text is
+    device time (CUDA events on the library's stream)."""
+    import torch
+    import paper_1810_03099_b200 as R
+    from paper_1810_03099_b200 import corpus as C
+    text, off = C.synth_text(cp.tokens, cp.doc_off, cp.vocab, seed=0)
+    pin = torch.from_numpy(text).pin_memory().numpy()
+    ctx = R.Context(torch.cuda.current_device())
+    ctx.set_stream(stream.cuda_stream)
+    with torch.cuda.stream(stream):
+        ctx.load_text(pin, off)
+        ctx.simhash_text(fetch=False)
+        torch.cuda.synchronize(dev)
+        t_load = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            ctx.load_text(pin, off)
+            ctx.synchronize()
+            t_load.append(time.perf_counter() - t0)
+        ctx.set_profiling(True)
+        for _ in range(reps):
+            ctx.simhash_text(fetch=False)
+        torch.cuda.synchronize(dev)
+        ph = ctx.phase_times()
+        ctx.set_profiling(False)
+    ctx.close()
+    tl = float(np.median(t_load))
+    ts = ph["simhash"][0] / max(ph["simhash"][1], 1) / 1e3
+    nb = int(len(text))
+    return {"bytes": nb, "docs": int(len(off) - 1), "load_text_ms": tl * 1e3, "load_text_gbs": nb / tl / 1e9,
+            "simhash_text_ms": ts * 1e3, "simhash_text_gbs": nb / ts / 1e9,
+            "note": "load_text = pinned H2D + gram-count pass + D2H counts + plan + gram-write pass (host wall "
+                    "clock); simhash_text = MD5 per word + per-occurrence votes (device time)"}
 
 
 def measure_rivals(ctx, stream, flush, dev, thr, reps):

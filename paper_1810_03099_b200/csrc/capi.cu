@@ -907,7 +907,8 @@ int refsig_gpu_load_text(refsig_gpu_ctx* ctx, const uint8_t* text, const uint64_
     for (uint32_t d = 0; d < n_docs; ++d) require(byte_off[d + 1] >= byte_off[d], "byte_off must be non-decreasing");
     const uint64_t B = byte_off[n_docs];
     require(text != nullptr || B == 0, "text is NULL");
-    ctx->text.ensure(std::max<uint64_t>(B, 1));
+    ctx->text.ensure(B + 16);  // padded: 32-bit loads may read up to 8 bytes past the end
+    ck(cudaMemsetAsync(static_cast<uint8_t*>(ctx->text.p) + B, 0, 16, ctx->stream), "memset text pad");
     ctx->text_off.ensure(8ull * (n_docs + 1));
     ctx->text_cnt.ensure(4ull * n_docs);
     {

@@ -12,13 +12,15 @@
 //     8 bytes of the word's MD5, big-endian) + simhash (simhash.hpp:35-45: per
 //     occurrence +-1 per bit column, bit = column > 0, no words -> 0).
 //
-// Mapping: warp per document, 32 bytes per step (lane = byte; the next two
-// bytes via SHFL). Grams: ballot + prefix popcount place each id; a first
-// pass only counts (the host needs the per-doc gram counts to plan K1).
-// Words: word starts/ends per step come from two ballots; completed words
-// (start, length) are queued in shared memory and hashed 32 at a time, one
-// word per lane (MD5 over 64-byte blocks, RFC 1321); the bit columns are
-// counted with 64 ballots + popcounts per 32 words.
+// Mapping: warp per document, 128 bytes per step (4 per lane, read by
+// aligned 32-bit loads; neighbour bytes via SHFL). Grams: a warp scan of the
+// per-lane counts places each id; a first pass only counts (the host needs
+// the per-doc gram counts to plan K1). Words: each lane finds word starts and
+// ends in its 4 bytes, the start of a word ending in a lane comes from a warp
+// max-scan of the last start per lane (or a word left open by the previous
+// step); completed words (start, length) are queued in shared memory and
+// hashed 32 at a time, one word per lane (MD5 over 64-byte blocks, RFC 1321);
+// the bit columns are counted by a 32x32 warp bit transpose + popcount.
 
 #include "kernels.cuh"
 
@@ -42,6 +44,13 @@ __device__ __forceinline__ void load3(const uint8_t* __restrict__ text, uint64_t
   }
 }
 
+// 4 bytes at an arbitrary byte address from aligned 32-bit loads (the text
+// buffer is padded by 8 bytes so the second load never leaves it).
+__device__ __forceinline__ uint32_t load4u(const uint8_t* __restrict__ text, uint64_t q) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(text + (q & ~3ull));
+  return __funnelshift_r(__ldg(w), __ldg(w + 1), static_cast<uint32_t>(q & 3) * 8);
+}
+
 __global__ void __launch_bounds__(256) text_grams_kernel(const uint8_t* __restrict__ text,
                                                          const uint64_t* __restrict__ off, uint32_t n_docs,
                                                          const uint64_t* __restrict__ gram_off,
@@ -52,15 +61,46 @@ __global__ void __launch_bounds__(256) text_grams_kernel(const uint8_t* __restri
   const uint64_t beg = off[d], end = off[d + 1];
   uint64_t out = tokens ? gram_off[d] : 0;
   uint32_t total = 0;
-  for (uint64_t p = beg; p < end; p += 32) {
-    uint32_t b0, b1, b2;
-    load3(text, p, end, lane, b0, b1, b2);
-    const uint32_t l0 = lower_letter(b0), l1 = lower_letter(b1), l2 = lower_letter(b2);
-    const bool g = l0 < 26 && l1 < 26 && l2 < 26 && p + lane + 2 < end;
-    const uint32_t m = __ballot_sync(0xffffffffu, g);
-    if (tokens && g) tokens[out + __popc(m & ((1u << lane) - 1u))] = (l0 * 26 + l1) * 26 + l2;
-    out += __popc(m);
-    total += __popc(m);
+  // 128 bytes per step, 4 per lane (the two bytes after a lane's four come
+  // from the next lane); four steps' loads are issued together
+  constexpr int U = 4;
+  for (uint64_t p0 = beg; p0 < end; p0 += 128 * U) {
+    uint32_t wv[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t q = p0 + 128 * u + 4 * lane;
+      wv[u] = q < end ? load4u(text, q) : 0u;
+      xv[u] = (lane == 31 && q + 4 < end) ? load4u(text, q + 4) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+    const uint64_t p = p0 + 128 * u;
+    if (p >= end) break;  // warp-uniform
+    const uint64_t q = p + 4 * lane;
+    const uint32_t w = wv[u];
+    uint32_t nx = __shfl_down_sync(0xffffffffu, w, 1);
+    if (lane == 31) nx = xv[u];
+    uint32_t l[6];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) l[k] = lower_letter((w >> (8 * k)) & 0xffu);
+    l[4] = lower_letter(nx & 0xffu);
+    l[5] = lower_letter((nx >> 8) & 0xffu);
+    uint32_t gm = 0;  // bit k: a gram starts at q+k
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (l[k] < 26 && l[k + 1] < 26 && l[k + 2] < 26 && q + k + 2 < end) gm |= 1u << k;
+    const uint32_t c = __popc(gm);
+    const uint32_t inc = warp_inclusive_scan(c, lane);
+    if (tokens) {
+      uint64_t o = out + inc - c;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (gm & (1u << k)) tokens[o++] = (l[k] * 26 + l[k + 1]) * 26 + l[k + 2];
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+    out += tot;
+    total += tot;
+    }
   }
   if (cnt && lane == 0) cnt[d] = total;
 }
@@ -74,17 +114,13 @@ __device__ uint64_t word_md5_64(const uint8_t* __restrict__ text, uint64_t s, ui
     uint32_t M[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
+      const uint32_t q = blk * 64 + 4 * i;  // message bytes q .. q+3
       uint32_t w = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t q = blk * 64 + 4 * i + k;
-        uint32_t v = 0;
-        if (q < len)
-          v = text[s + q] | 32u;  // letters only: lowercase
-        else if (q == len)
-          v = 0x80u;
-        w |= v << (8 * k);
+      if (q < len) {
+        w = load4u(text, s + q) | 0x20202020u;  // letters only: lowercase
+        if (len - q < 4) w &= (1u << (8 * (len - q))) - 1u;
       }
+      if (q <= len && len < q + 4) w |= 0x80u << (8 * (len - q));
       M[i] = w;
     }
     if (blk + 1 == nblk) {  // length in bits, little-endian, in the last 8 bytes
@@ -129,7 +165,22 @@ __device__ uint64_t word_md5_64(const uint8_t* __restrict__ text, uint64_t s, ui
   return (static_cast<uint64_t>(__byte_perm(h0, 0, 0x0123)) << 32) | __byte_perm(h1, 0, 0x0123);
 }
 
-constexpr int kWordQ = 64;  // per-warp queue of completed words
+constexpr int kWordQ = 128;  // per-warp queue of completed words (<= 64 per step + < 32 carried)
+
+// 32x32 bit transpose across the warp (row = lane): returns in lane l the
+// bits of column 31-l of all lanes' rows (bit b of the result = row 31-b).
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, uint32_t lane) {
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) {
+    const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu : j == 2 ? 0x33333333u
+                                                                                                  : 0x55555555u;
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+    const bool up = lane & j;
+    const uint32_t t = ((up ? y : x) ^ ((up ? x : y) >> j)) & m;
+    x ^= up ? (t << j) : t;
+  }
+  return x;
+}
 
 __global__ void __launch_bounds__(256) text_simhash_kernel(const uint8_t* __restrict__ text,
                                                            const uint64_t* __restrict__ off, uint32_t n_docs,
@@ -139,71 +190,79 @@ __global__ void __launch_bounds__(256) text_simhash_kernel(const uint8_t* __rest
   const uint32_t d = blockIdx.x * (blockDim.x >> 5) + wid;
   if (d >= n_docs) return;
   const uint64_t beg = off[d], end = off[d + 1];
-  uint32_t c0 = 0, c1 = 0, nw = 0;  // lane: votes of columns lane and lane+32; words seen
-  uint32_t qn = 0;                  // queued words (warp-uniform)
-  int64_t open = -1;                // start of a word still running at the step boundary
+  uint32_t c_lo = 0, c_hi = 0, nw = 0;  // lane l: votes of columns 31-l and 63-l; words seen
+  uint32_t qn = 0;                      // queued words (warp-uniform)
+  int64_t open = -1;                    // start of a word still running at the step boundary
   auto hash_batch = [&](uint32_t m) {
-    const bool v = lane < m;
     uint64_t h = 0;
-    if (v) {
+    if (lane < m) {
       const uint2 w = q[wid][lane];
       h = word_md5_64(text, beg + w.x, w.y);
     }
-    const uint32_t lo = static_cast<uint32_t>(h), hi = static_cast<uint32_t>(h >> 32);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const uint32_t bl = __ballot_sync(0xffffffffu, v && ((lo >> j) & 1u));
-      const uint32_t bh = __ballot_sync(0xffffffffu, v && ((hi >> j) & 1u));
-      if (lane == static_cast<uint32_t>(j)) {
-        c0 += __popc(bl);
-        c1 += __popc(bh);
-      }
-    }
+    // column votes: transpose the 32 hashes' bits, popcount per column
+    c_lo += __popc(warp_transpose32(static_cast<uint32_t>(h), lane));
+    c_hi += __popc(warp_transpose32(static_cast<uint32_t>(h >> 32), lane));
     nw += m;
   };
-  for (uint64_t p = beg; p < end; p += 32) {
-    uint32_t b0, b1, b2;
-    load3(text, p, end, lane, b0, b1, b2);
-    (void)b2;
-    const uint64_t pos = p + lane;
-    const bool in = pos < end;
-    const bool let = in && lower_letter(b0) < 26;
-    const uint32_t prev = __shfl_up_sync(0xffffffffu, b0, 1);
-    const bool prev_let = lane == 0 ? (p > beg && lower_letter(text[p - 1]) < 26) : lower_letter(prev) < 26;
-    const bool next_let = pos + 1 < end && lower_letter(b1) < 26;
-    const uint32_t S = __ballot_sync(0xffffffffu, let && !prev_let);  // word starts
-    const uint32_t E = __ballot_sync(0xffffffffu, let && !next_let);  // last letter of a word
-    // pair ends with starts in order: an open word takes the first end
-    uint32_t s_rem = S, e_rem = E;
-    while (e_rem) {
-      const int e = __ffs(e_rem) - 1;
-      e_rem &= e_rem - 1;
-      uint64_t st;
-      if (open >= 0) {
-        st = static_cast<uint64_t>(open);
-        open = -1;
-      } else {
-        const int s = __ffs(s_rem) - 1;
-        s_rem &= s_rem - 1;
-        st = p + s;
-      }
-      if (lane == 0) q[wid][qn] = make_uint2(static_cast<uint32_t>(st - beg), static_cast<uint32_t>(p + e + 1 - st));
-      ++qn;
+  // 128 bytes per step, 4 per lane; neighbour bytes via SHFL
+  for (uint64_t p = beg; p < end; p += 128) {
+    const uint64_t q0 = p + 4 * lane;
+    const uint32_t w = q0 < end ? load4u(text, q0) : 0u;
+    uint32_t prev = __shfl_up_sync(0xffffffffu, w, 1) >> 24;   // byte q0-1
+    uint32_t next = __shfl_down_sync(0xffffffffu, w, 1) & 0xffu;  // byte q0+4
+    if (lane == 0) prev = p > beg ? text[p - 1] : 0u;
+    if (lane == 31) next = q0 + 4 < end ? text[q0 + 4] : 0u;
+    uint32_t let = 0;  // bit k: byte q0+k is a letter of this doc
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (q0 + k < end && lower_letter((w >> (8 * k)) & 0xffu) < 26) let |= 1u << k;
+    const uint32_t lp = (let << 1) | (lower_letter(prev) < 26 ? 1u : 0u);         // bit k: byte q0+k-1
+    const uint32_t ln = (let >> 1) | ((q0 + 4 < end && lower_letter(next) < 26) ? 8u : 0u);  // bit k: q0+k+1
+    const uint32_t sm = let & ~lp & 0xfu;  // word starts
+    const uint32_t em = let & ~ln & 0xfu;  // last letters of words
+    // latest start before this lane's bytes: max-scan of "last start" over lanes
+    int64_t ls = sm ? static_cast<int64_t>(q0 + 31 - __clz(sm)) : -1;
+    int64_t run = ls;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, run, o);
+      if (lane >= static_cast<uint32_t>(o)) run = max(run, y);
     }
-    if (s_rem) open = static_cast<int64_t>(p + (31 - __clz(s_rem)));  // a start without its end yet
+    int64_t before = __shfl_up_sync(0xffffffffu, run, 1);
+    if (lane == 0) before = -1;
+    if (before < 0) before = open;
+    const uint32_t ne = __popc(em);
+    const uint32_t inc = warp_inclusive_scan(ne, lane);
+    uint32_t slot = qn + inc - ne;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (em & (1u << k)) {
+        const uint32_t sk = sm & ((2u << k) - 1u);  // starts at or before byte k in this lane
+        const uint64_t st = sk ? q0 + 31 - __clz(sk) : static_cast<uint64_t>(before);
+        q[wid][slot++] = make_uint2(static_cast<uint32_t>(st - beg), static_cast<uint32_t>(q0 + k + 1 - st));
+      }
+    qn += __shfl_sync(0xffffffffu, inc, 31);
+    // a word left open at the end of the step: the last start after the last end
+    const int64_t last_s = __shfl_sync(0xffffffffu, run, 31);
+    const int64_t le = em ? static_cast<int64_t>(q0 + 31 - __clz(em)) : -1;
+    int64_t lem = le;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lem = max(lem, __shfl_xor_sync(0xffffffffu, lem, o));
+    if (last_s > lem) open = last_s;
+    else if (lem >= 0) open = -1;
     __syncwarp();
-    if (qn >= 32) {
+    while (qn >= 32) {
       hash_batch(32);
       __syncwarp();
-      if (lane < qn - 32) q[wid][lane] = q[wid][32 + lane];
+      for (uint32_t i = lane; i + 32 < qn; i += 32) q[wid][i] = q[wid][i + 32];
       qn -= 32;
       __syncwarp();
     }
   }
   if (qn) hash_batch(qn);
-  // bit j = votes_j > words - votes_j (2*votes > words; tie -> 0)
-  const uint32_t lo = __ballot_sync(0xffffffffu, 2 * c0 > nw);
-  const uint32_t hi = __ballot_sync(0xffffffffu, 2 * c1 > nw);
+  // bit j = 2*votes_j > words (tie -> 0); lane l holds columns 31-l / 63-l
+  const uint32_t lo = __brev(__ballot_sync(0xffffffffu, 2 * c_lo > nw));
+  const uint32_t hi = __brev(__ballot_sync(0xffffffffu, 2 * c_hi > nw));
   if (lane == 0) fp[d] = (static_cast<uint64_t>(hi) << 32) | lo;
 }
 
