@@ -139,6 +139,41 @@ class Context {
     });
   }
 
+  // Raw text documents text[byte_off[d] .. byte_off[d+1]): the corpus becomes
+  // each document's 3-grams (normalize + extract_3grams, ngram.hpp:114-180),
+  // vocabulary 17576; count() then yields extract_3grams' entries.
+  void load_text(const std::string& text, const std::vector<std::uint64_t>& byte_off) {
+    if (byte_off.size() < 2 || byte_off.back() > text.size())
+      throw refsig::validation_error("refsig::gpu: byte_off must have n_docs+1 entries within the text");
+    check(refsig_gpu_load_text(ctx_, reinterpret_cast<const std::uint8_t*>(text.data()), byte_off.data(),
+                               static_cast<std::uint32_t>(byte_off.size() - 1)));
+    n_docs_ = static_cast<std::uint32_t>(byte_off.size() - 1);
+  }
+
+  // simhash(extract_words(normalize(doc))) per document (simhash.hpp:35-45).
+  std::vector<std::uint64_t> simhash_text() {
+    check(refsig_gpu_simhash_text(ctx_));
+    std::vector<std::uint64_t> fp(n_docs_hint());
+    check(refsig_gpu_get_fingerprints(ctx_, fp.data()));
+    return fp;
+  }
+
+  // The last pair call's pairs as CSR over all rows: rowptr[n_docs+1], cols.
+  struct PairsCsr {
+    std::vector<std::uint64_t> rowptr;
+    std::vector<std::uint32_t> cols;
+  };
+  PairsCsr pairs_csr() {
+    PairsCsr r;
+    r.rowptr.resize(n_docs_hint() + 1);
+    std::uint64_t n = 0;
+    int rc = refsig_gpu_get_pairs_csr(ctx_, 0, n_docs_hint(), r.rowptr.data(), nullptr, 0, &n);
+    if (rc != REFSIG_E_OVERFLOW) check(rc);
+    r.cols.resize(n);
+    check(refsig_gpu_get_pairs_csr(ctx_, 0, n_docs_hint(), r.rowptr.data(), r.cols.data(), n, &n));
+    return r;
+  }
+
   std::uint32_t n_docs_hint() const { return n_docs_; }
 
  private:

@@ -49,6 +49,19 @@ int main() {
     threw = true;
   }
   EXPECT(threw);
+  // pairs as CSR: row 0 -> {1}
+  ctx.mrc_pairs(0.999f);
+  auto csr = ctx.pairs_csr();
+  EXPECT(csr.rowptr.size() == 4 && csr.rowptr[1] == 1 && csr.rowptr[3] == 1 && csr.cols.size() == 1 &&
+         csr.cols[0] == 1);
+  // text front end: "abcabc" and "Abc-abc!" give the same 3-gram vector
+  ctx.load_text("abcabcAbc-abc!", {0, 6, 14});
+  ctx.count(Weighting::tf);
+  auto t = ctx.counts();
+  EXPECT(t.rowptr[1] == 3 && t.ids[0] == 28 && t.counts[0] == 2 && t.rowptr[2] == 4 && t.ids[3] == 28 &&
+         t.counts[3] == 2);
+  auto tf = ctx.simhash_text();  // one word "abcabc" vs two words "abc", "abc"
+  EXPECT(tf.size() == 2 && tf[0] != 0 && tf[1] != 0);
   std::printf("gpu_api_check OK\n");
   return 0;
 }
