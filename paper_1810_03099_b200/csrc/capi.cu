@@ -99,7 +99,7 @@ struct refsig_gpu_ctx {
   uint32_t* h_plan = nullptr;
   size_t h_plan_cap = 0;
   cudaEvent_t plan_done = nullptr;  // h_plan consumed by its copy
-  enum { kPlanTiny, kPlanW8, kPlanW16, kPlanG0, kPlanG1, kPlanG2, kPlanG3, kPlanLong, kPlanOrder, kPlanLists };
+  enum { kPlanTiny, kPlanW4, kPlanW8, kPlanW16, kPlanG0, kPlanG1, kPlanG2, kPlanG3, kPlanLong, kPlanOrder, kPlanLists };
   uint32_t plan_off[kPlanLists] = {}, plan_n[kPlanLists] = {};
   const uint32_t* plan_list(int k) const { return plan.as<uint32_t>() + plan_off[k]; }
   DevBuf long_off, long_scratch;
@@ -431,6 +431,7 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
   uint32_t n_class[refsig_gpu_ctx::kPlanLists] = {};
   auto cls_of = [&](uint64_t l) -> int {
     if (l <= kTinyMax) return refsig_gpu_ctx::kPlanTiny;
+    if (l <= 128) return refsig_gpu_ctx::kPlanW4;
     if (l <= 256) return refsig_gpu_ctx::kPlanW8;
     if (l <= 512) return refsig_gpu_ctx::kPlanW16;
     if (l <= kGroupMax) {
@@ -633,8 +634,9 @@ static void do_count(refsig_gpu_ctx* ctx, int weight_mode) {
   launch_count_group(2, a, ctx->plan_list(P::kPlanG2), ctx->plan_n[P::kPlanG2], ctx->side[2]);
   launch_count_group(1, a, ctx->plan_list(P::kPlanG1), ctx->plan_n[P::kPlanG1], m0);
   launch_count_group(0, a, ctx->plan_list(P::kPlanG0), ctx->plan_n[P::kPlanG0], m0);
-  launch_count_warp(16, a, ctx->plan_list(P::kPlanW16), ctx->plan_n[P::kPlanW16], m0);
+  launch_count_warp(16, a, ctx->plan_list(P::kPlanW16), ctx->plan_n[P::kPlanW16], ctx->side[1]);
   launch_count_warp(2, a, ctx->plan_list(P::kPlanTiny), ctx->plan_n[P::kPlanTiny], ctx->side[0]);
+  launch_count_warp(4, a, ctx->plan_list(P::kPlanW4), ctx->plan_n[P::kPlanW4], ctx->side[0]);
   launch_count_warp(8, a, ctx->plan_list(P::kPlanW8), ctx->plan_n[P::kPlanW8], ctx->side[0]);
   launch_count_large(a, ctx->plan_list(P::kPlanLong), ctx->long_off.as<uint64_t>(), ctx->plan_n[P::kPlanLong],
                      ctx->long_scratch.as<uint32_t>(), ctx->side[0]);

@@ -21,8 +21,8 @@
 // registers too (neighbour via SHFL, positions via warp/block scans, run ends
 // via a suffix-min of the next head). Work plan (host-built at upload):
 //   <= 64 tokens: warp per doc, 64-key sort;
-//   65..256 / 257..512: one warp per doc sorting 256 / 512 keys in
-//     registers (IPT 8 / 16);
+//   65..128 / 129..256 / 257..512: one warp per doc sorting 128 / 256 / 512
+//     keys in registers (IPT 4 / 8 / 16);
 //   513..8192: one CTA of 2/4/8/16 warps per doc (group_sort_kernel);
 //   > 8192: bitonic sort in a global scratch region.
 
@@ -50,55 +50,19 @@ __device__ __forceinline__ uint32_t next_pow2(uint32_t x) {
 }
 
 // ---------------------------------------------------------------------------
-// Register bitonic sort of P = 32*IPT keys held by one warp, IPT consecutive
-// keys per lane (blocked layout: lane holds [lane*IPT, lane*IPT+IPT)). Every
-// stage is a template instance, so all register indices are compile-time
-// constants (no local-memory arrays even at IPT = 32).
-template <int IPT, int K, int J>
-__device__ __forceinline__ void bitonic_stage(uint32_t (&v)[IPT], uint32_t lane) {
-  if constexpr (J >= IPT) {  // partner in lane ^ (J/IPT)
-    constexpr uint32_t lj = J / IPT;
-    const bool lower = (lane & lj) == 0;
-    const bool asc = ((lane * IPT) & K) == 0;
-    const bool take_min = lower == asc;
-#pragma unroll
-    for (int q = 0; q < IPT; ++q) {
-      const uint32_t y = __shfl_xor_sync(0xffffffffu, v[q], lj);
-      v[q] = take_min ? min(v[q], y) : max(v[q], y);
-    }
-  } else {  // partner in this lane's registers
-#pragma unroll
-    for (int q = 0; q < IPT; ++q) {
-      if ((q & J) == 0) {
-        constexpr int dummy = 0;
-        (void)dummy;
-        const int l = q | J;
-        const bool asc = ((lane * IPT + q) & K) == 0;
-        const uint32_t lo = min(v[q], v[l]), hi = max(v[q], v[l]);
-        v[q] = asc ? lo : hi;
-        v[l] = asc ? hi : lo;
-      }
-    }
-  }
-  if constexpr (J > 1) bitonic_stage<IPT, K, J / 2>(v, lane);
-}
-
-template <int IPT, int K>
-__device__ __forceinline__ void bitonic_level(uint32_t (&v)[IPT], uint32_t lane) {
-  bitonic_stage<IPT, K, K / 2>(v, lane);
-  if constexpr (K < 32 * IPT) bitonic_level<IPT, 2 * K>(v, lane);
-}
-
-template <int IPT>
-__device__ __forceinline__ void bitonic_regs(uint32_t (&v)[IPT], uint32_t lane) {
-  bitonic_level<IPT, 2>(v, lane);
-}
-
-// Group variant: T = 32*W threads of one CTA sort P = T*IPT keys, thread t
-// holding [t*IPT, t*IPT+IPT). Distances j < IPT are register ops, IPT <= j <
-// 32*IPT shuffles, j >= 32*IPT go through shared memory (sm: IPT*T words,
-// element-major so both the stores and the partner loads are conflict-free).
-template <int IPT, int T, int K, int J>
+// Register bitonic sort. T = 32*W threads of one CTA sort P = T*IPT keys,
+// thread t holding [t*IPT, t*IPT+IPT) (blocked layout; W = 1 is one warp).
+// Distances j < IPT are register ops, IPT <= j < 32*IPT shuffles, j >= 32*IPT
+// (W > 1 only) go through shared memory (sm: IPT*T words, element-major so
+// both the stores and the partner loads are conflict-free). Every stage is a
+// template instance, so all register indices are compile-time constants.
+// Direction normalisation: from merge level K = IPT on, a thread's sort
+// direction is uniform over its keys, so a thread in a descending block holds
+// its keys complemented (one XOR per key per level, composed with the
+// previous level's) and every compare-exchange of the level sorts ascending —
+// the register stages then need no direction selects. The last level
+// (K = P) is ascending everywhere, which restores the keys.
+template <int IPT, int T, int K, int J, bool NORM>
 __device__ __forceinline__ void gbitonic_stage(uint32_t (&v)[IPT], uint32_t t, uint32_t* sm) {
   if constexpr (J >= 32 * IPT) {
     constexpr uint32_t tj = J / IPT;
@@ -106,7 +70,7 @@ __device__ __forceinline__ void gbitonic_stage(uint32_t (&v)[IPT], uint32_t t, u
 #pragma unroll
     for (int q = 0; q < IPT; ++q) sm[q * T + t] = v[q];
     __syncthreads();
-    const bool take_min = ((t & tj) == 0) == (((t * IPT) & K) == 0);
+    const bool take_min = NORM ? (t & tj) == 0 : ((t & tj) == 0) == (((t * IPT) & K) == 0);
 #pragma unroll
     for (int q = 0; q < IPT; ++q) {
       const uint32_t y = sm[q * T + (t ^ tj)];
@@ -114,7 +78,7 @@ __device__ __forceinline__ void gbitonic_stage(uint32_t (&v)[IPT], uint32_t t, u
     }
   } else if constexpr (J >= IPT) {
     constexpr uint32_t lj = J / IPT;
-    const bool take_min = ((t & lj) == 0) == (((t * IPT) & K) == 0);
+    const bool take_min = NORM ? (t & lj) == 0 : ((t & lj) == 0) == (((t * IPT) & K) == 0);
 #pragma unroll
     for (int q = 0; q < IPT; ++q) {
       const uint32_t y = __shfl_xor_sync(0xffffffffu, v[q], lj);
@@ -125,20 +89,45 @@ __device__ __forceinline__ void gbitonic_stage(uint32_t (&v)[IPT], uint32_t t, u
     for (int q = 0; q < IPT; ++q) {
       if ((q & J) == 0) {
         const int l = q | J;
-        const bool asc = ((t * IPT + q) & K) == 0;
         const uint32_t lo = min(v[q], v[l]), hi = max(v[q], v[l]);
-        v[q] = asc ? lo : hi;
-        v[l] = asc ? hi : lo;
+        if constexpr (NORM) {
+          v[q] = lo;
+          v[l] = hi;
+        } else {  // K < IPT: the direction depends on q only (compile-time)
+          const bool asc = (q & K) == 0;
+          v[q] = asc ? lo : hi;
+          v[l] = asc ? hi : lo;
+        }
       }
     }
   }
-  if constexpr (J > 1) gbitonic_stage<IPT, T, K, J / 2>(v, t, sm);
+  if constexpr (J > 1) gbitonic_stage<IPT, T, K, J / 2, NORM>(v, t, sm);
 }
 
 template <int IPT, int T, int K>
-__device__ __forceinline__ void gbitonic_level(uint32_t (&v)[IPT], uint32_t t, uint32_t* sm) {
-  gbitonic_stage<IPT, T, K, K / 2>(v, t, sm);
-  if constexpr (K < T * IPT) gbitonic_level<IPT, T, 2 * K>(v, t, sm);
+__device__ __forceinline__ void gbitonic_level(uint32_t (&v)[IPT], uint32_t t, uint32_t* sm, uint32_t& cur) {
+  if constexpr (K >= IPT) {
+    const uint32_t want = ((t * IPT) & K) ? 0xffffffffu : 0u;  // descending block: hold complements
+    const uint32_t x = want ^ cur;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) v[q] ^= x;
+    cur = want;
+    gbitonic_stage<IPT, T, K, K / 2, true>(v, t, sm);
+  } else {
+    gbitonic_stage<IPT, T, K, K / 2, false>(v, t, sm);
+  }
+  if constexpr (K < T * IPT) gbitonic_level<IPT, T, 2 * K>(v, t, sm, cur);
+}
+
+template <int IPT, int T>
+__device__ __forceinline__ void gbitonic_sort(uint32_t (&v)[IPT], uint32_t t, uint32_t* sm) {
+  uint32_t cur = 0;
+  gbitonic_level<IPT, T, 2>(v, t, sm, cur);
+}
+
+template <int IPT>
+__device__ __forceinline__ void bitonic_regs(uint32_t (&v)[IPT], uint32_t lane) {
+  gbitonic_sort<IPT, 32>(v, lane, nullptr);
 }
 
 // Warp inclusive scan / suffix min.
@@ -295,7 +284,7 @@ __global__ void __launch_bounds__(32 * W) group_sort_kernel(CountArgs a, const u
   uint32_t v[IPT];
 #pragma unroll
   for (int k = 0; k < IPT; ++k) v[k] = load_key(a, b, k * T + t, len);  // coalesced; any order sorts
-  gbitonic_level<IPT, T, 2>(v, t, sm);
+  gbitonic_sort<IPT, T>(v, t, sm);
   const uint32_t n = rle_regs<IPT, W>(v, t, len, a.ent + b, a, rle_sm);
   if (t == 0) a.nnz[d] = n;
 }
@@ -440,6 +429,8 @@ void launch_count_warp(int ipt, const CountArgs& a, const uint32_t* docs, uint32
   const unsigned blocks = static_cast<unsigned>(ceil_div(n, 8));  // one warp per doc
   if (ipt == 2)
     count_warp_kernel<2><<<blocks, 256, 0, s>>>(a, docs, n);
+  else if (ipt == 4)
+    count_warp_kernel<4><<<blocks, 256, 0, s>>>(a, docs, n);
   else if (ipt == 8)
     count_warp_kernel<8><<<blocks, 256, 0, s>>>(a, docs, n);
   else

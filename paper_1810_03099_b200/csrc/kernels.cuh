@@ -24,8 +24,8 @@ void launch_text_simhash(const uint8_t* text, const uint64_t* off, uint32_t n_do
 constexpr uint32_t kGramSpace = 26u * 26u * 26u;  // ngram.hpp: 17576 3-grams
 
 // ---- K1 -------------------------------------------------------------------
-// Count work plan (k1_count.cu, built at upload): documents of <= 64 / 256 /
-// 512 tokens are sorted by one warp each (64 / 256 / 512 keys in registers);
+// Count work plan (k1_count.cu, built at upload): documents of <= 64 / 128 /
+// 256 / 512 tokens are sorted by one warp each (that many keys in registers);
 // 513..8192 tokens by one CTA of 2/4/8/16 warps (kGroupCap classes); longer
 // ones in a global scratch region.
 constexpr uint32_t kTinyMax = 64;
@@ -44,7 +44,7 @@ struct CountArgs {
   uint32_t* err;     // bit 0: token id >= vocab
 };
 
-// One warp per doc, 32*ipt keys (ipt 2 / 8 / 16).
+// One warp per doc, 32*ipt keys (ipt 2 / 4 / 8 / 16).
 void launch_count_warp(int ipt, const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s);
 // One CTA of 2/4/8/16 warps per doc of group class cls (docs = doc ids).
 void launch_count_group(int cls, const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s);
