@@ -634,7 +634,7 @@ static void do_count(refsig_gpu_ctx* ctx, int weight_mode) {
   launch_count_group(2, a, ctx->plan_list(P::kPlanG2), ctx->plan_n[P::kPlanG2], ctx->side[2]);
   launch_count_group(1, a, ctx->plan_list(P::kPlanG1), ctx->plan_n[P::kPlanG1], m0);
   launch_count_group(0, a, ctx->plan_list(P::kPlanG0), ctx->plan_n[P::kPlanG0], m0);
-  launch_count_warp(16, a, ctx->plan_list(P::kPlanW16), ctx->plan_n[P::kPlanW16], ctx->side[1]);
+  launch_count_group(-1, a, ctx->plan_list(P::kPlanW16), ctx->plan_n[P::kPlanW16], ctx->side[1]);
   launch_count_warp(2, a, ctx->plan_list(P::kPlanTiny), ctx->plan_n[P::kPlanTiny], ctx->side[0]);
   launch_count_warp(4, a, ctx->plan_list(P::kPlanW4), ctx->plan_n[P::kPlanW4], ctx->side[0]);
   launch_count_warp(8, a, ctx->plan_list(P::kPlanW8), ctx->plan_n[P::kPlanW8], ctx->side[0]);

@@ -25,9 +25,9 @@ constexpr uint32_t kGramSpace = 26u * 26u * 26u;  // ngram.hpp: 17576 3-grams
 
 // ---- K1 -------------------------------------------------------------------
 // Count work plan (k1_count.cu, built at upload): documents of <= 64 / 128 /
-// 256 / 512 tokens are sorted by one warp each (that many keys in registers);
-// 513..8192 tokens by one CTA of 2/4/8/16 warps (kGroupCap classes); longer
-// ones in a global scratch region.
+// 256 tokens are sorted by one warp each (that many keys in registers);
+// 257..8192 tokens by one CTA of 2..32 warps (8 keys per thread; kGroupCap
+// classes above 512); longer ones in a global scratch region.
 constexpr uint32_t kTinyMax = 64;
 constexpr int kGroupClasses = 4;
 constexpr uint32_t kGroupCap[kGroupClasses] = {1024, 2048, 4096, 8192};
@@ -44,9 +44,10 @@ struct CountArgs {
   uint32_t* err;     // bit 0: token id >= vocab
 };
 
-// One warp per doc, 32*ipt keys (ipt 2 / 4 / 8 / 16).
+// One warp per doc, 32*ipt keys (ipt 2 / 4 / 8).
 void launch_count_warp(int ipt, const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s);
-// One CTA of 2/4/8/16 warps per doc of group class cls (docs = doc ids).
+// One CTA per doc, 8 keys per thread: cls -1 = 257..512 tokens (2 warps),
+// 0..3 = the kGroupCap classes (4/8/16/32 warps).
 void launch_count_group(int cls, const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s);
 void launch_count_large(const CountArgs& a, const uint32_t* long_docs, const uint64_t* scratch_off,
                         uint32_t n_long, uint32_t* scratch, cudaStream_t s);
