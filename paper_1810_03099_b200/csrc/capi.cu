@@ -124,9 +124,12 @@ struct refsig_gpu_ctx {
   uint32_t ld = 0;  // leading dimension of ST
 
   // pairs
-  DevBuf bitmap, rowcnt, rowstart, cand, scan_tmp, cols;
+  // pair output: sorted CSR columns (cand) over rowstart; the 64-bit keys
+  // (keys) are materialised only when a caller asks for them
+  DevBuf bitmap, rowcnt, rowstart, cand, scan_tmp, keys;
   uint64_t cand_count = 0;
   bool have_pairs = false;  // cand/rowstart/emit_grid hold the last pair computation
+  bool keys_valid = false;
 
   // simhash
   bool have_fp = false;
@@ -295,24 +298,36 @@ void reset_downstream(refsig_gpu_ctx* c) {
 
 uint32_t words_per_row(uint32_t n_cols) { return static_cast<uint32_t>(ceil_div(n_cols, kTile) * 4); }
 
-// Scan rowcnt and emit sorted keys into ctx->cand with its current capacity;
+// The 64-bit keys (i<<32|j) of the last pair computation, built on demand
+// from the CSR columns (rows outside the emit range have no pairs).
+void materialize_keys(refsig_gpu_ctx* c) {
+  if (c->keys_valid) return;
+  c->keys.ensure(sizeof(uint64_t) * std::max<uint64_t>(c->cand_count, 1));
+  const PairGrid& g = c->emit_grid;
+  launch_cols_to_keys(c->rowstart.as<uint64_t>(), g.row_begin, g.row_end, c->cand.as<uint32_t>(),
+                      c->keys.as<uint64_t>(), c->stream);
+  c->keys_valid = true;
+}
+
+// Scan rowcnt and emit sorted CSR columns into ctx->cand with its capacity;
 // the total is copied (async) to h_pin[0]. No host synchronisation.
 void enqueue_emit(refsig_gpu_ctx* c, const PairGrid& g) {
   const uint64_t n = g.n_rows;
   c->rowstart.ensure(sizeof(uint64_t) * (n + 1));
   c->scan_tmp.ensure(scan_tmp_bytes(n));
-  c->cand.ensure(sizeof(uint64_t) * (1u << 20));
+  c->cand.ensure(sizeof(uint32_t) * (1u << 20));
   {
     Phase ph(c, REFSIG_PHASE_PAIR_EMIT);
     launch_exclusive_scan_u32_to_u64(c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(), n, c->scan_tmp.p,
                                      c->stream);
     launch_emit_pairs(c->bitmap.as<uint32_t>(), g, c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(),
-                      c->cand.as<uint64_t>(), c->cand.cap / sizeof(uint64_t), c->stream);
+                      c->cand.as<uint32_t>(), c->cand.cap / sizeof(uint32_t), c->stream);
     launched("emit");
   }
   ck(cudaMemcpyAsync(c->h_pin, c->rowstart.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, c->stream), "D2H count");
   c->emit_pending = true;
   c->have_pairs = false;
+  c->keys_valid = false;
   c->emit_grid = g;
 }
 
@@ -324,11 +339,11 @@ int finish_emit(refsig_gpu_ctx* c, uint64_t* out, uint64_t capacity, uint64_t* o
   c->emit_pending = false;
   const PairGrid& g = c->emit_grid;
   const uint64_t total = c->h_pin[0];
-  if (total > c->cand.cap / sizeof(uint64_t)) {
-    c->cand.ensure(sizeof(uint64_t) * (total + total / 4 + 1024));
+  if (total > c->cand.cap / sizeof(uint32_t)) {
+    c->cand.ensure(sizeof(uint32_t) * (total + total / 4 + 1024));
     Phase ph(c, REFSIG_PHASE_PAIR_EMIT);
     launch_emit_pairs(c->bitmap.as<uint32_t>(), g, c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(),
-                      c->cand.as<uint64_t>(), c->cand.cap / sizeof(uint64_t), c->stream);
+                      c->cand.as<uint32_t>(), c->cand.cap / sizeof(uint32_t), c->stream);
     launched("emit");
   }
   c->cand_count = total;
@@ -336,8 +351,9 @@ int finish_emit(refsig_gpu_ctx* c, uint64_t* out, uint64_t capacity, uint64_t* o
   *out_count = total;
   if (out && capacity) {
     const uint64_t m = std::min(total, capacity);
+    materialize_keys(c);
     Phase ph(c, REFSIG_PHASE_D2H);
-    if (m) ck(cudaMemcpyAsync(out, c->cand.p, m * 8, cudaMemcpyDeviceToHost, c->stream), "D2H pairs");
+    if (m) ck(cudaMemcpyAsync(out, c->keys.p, m * 8, cudaMemcpyDeviceToHost, c->stream), "D2H pairs");
   }
   sync(c);
   if (total > capacity && out) {
@@ -1201,6 +1217,7 @@ int refsig_gpu_mrc_step(refsig_gpu_ctx* ctx, int weight_mode, const uint32_t* re
       ck(cudaGraphLaunch(ctx->step_exec, ctx->stream), "cudaGraphLaunch");
       ck(cudaEventRecord(ctx->stage_done, ctx->stream), "event");
       ctx->emit_pending = true;
+      ctx->have_pairs = ctx->keys_valid = false;
       ctx->emit_grid = self_grid(ctx);
       ctx->emit_grid.row_begin = row_lo;
       ctx->emit_grid.row_end = row_hi;
@@ -1252,6 +1269,7 @@ int refsig_gpu_mrc_step(refsig_gpu_ctx* ctx, int weight_mode, const uint32_t* re
     // the eager results stand: report them through step_result
     ctx->h_pin[0] = keep_count;
     ctx->emit_pending = true;
+    ctx->have_pairs = ctx->keys_valid = false;
     ctx->emit_grid = self_grid(ctx);
     ctx->emit_grid.row_begin = row_lo;
     ctx->emit_grid.row_end = row_hi;
@@ -1303,7 +1321,11 @@ int refsig_gpu_get_pairs(refsig_gpu_ctx* ctx, uint64_t* out_pairs, uint64_t capa
   return guard(ctx, [&] {
     require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
     const uint64_t m = std::min(capacity, ctx->cand_count);
-    if (m) ck(cudaMemcpyAsync(out_pairs, ctx->cand.p, 8 * m, cudaMemcpyDeviceToHost, ctx->stream), "D2H pairs");
+    if (m) {
+      require(ctx->have_pairs && !ctx->emit_pending, "no finished pair computation to fetch");
+      materialize_keys(ctx);
+      ck(cudaMemcpyAsync(out_pairs, ctx->keys.p, 8 * m, cudaMemcpyDeviceToHost, ctx->stream), "D2H pairs");
+    }
     sync(ctx);
   });
 }
@@ -1327,10 +1349,9 @@ int refsig_gpu_get_pairs_csr(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_
     *out_count = total;
     const uint64_t m = std::min(total, capacity);
     if (m) {
-      ctx->cols.ensure(4 * m);
-      launch_keys_to_cols(ctx->cand.as<uint64_t>() + base, m, ctx->cols.as<uint32_t>(), ctx->stream);
       Phase ph(ctx, REFSIG_PHASE_D2H);
-      ck(cudaMemcpyAsync(cols, ctx->cols.p, 4 * m, cudaMemcpyDeviceToHost, ctx->stream), "D2H cols");
+      ck(cudaMemcpyAsync(cols, ctx->cand.as<uint32_t>() + base, 4 * m, cudaMemcpyDeviceToHost, ctx->stream),
+         "D2H cols");
     }
     sync(ctx);
     if (total > capacity) {
@@ -1346,7 +1367,10 @@ int refsig_gpu_device_buffer(refsig_gpu_ctx* ctx, int which, void** ptr, uint64_
     require(ptr && bytes, "NULL output");
     switch (which) {
       case REFSIG_BUF_PAIRS:
-        *ptr = ctx->cand.p;
+        require(ctx->have_pairs && !ctx->emit_pending, "no finished pair computation");
+        materialize_keys(ctx);
+        sync(ctx);
+        *ptr = ctx->keys.p;
         *bytes = ctx->cand_count * 8;
         break;
       case REFSIG_BUF_SIGNATURES:

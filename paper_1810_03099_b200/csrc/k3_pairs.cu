@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(256) hamming_bitmap_kernel(const uint64_t* __r
 // Warp per row: scan the row's words from its first written tile, write keys.
 __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ bitmap, PairGrid g,
                                                    const uint32_t* __restrict__ rowcnt,
-                                                   const uint64_t* __restrict__ rowstart, uint64_t* __restrict__ out,
+                                                   const uint64_t* __restrict__ rowstart, uint32_t* __restrict__ out,
                                                    uint64_t capacity) {
   const int lane = threadIdx.x & 31;
   const uint32_t i = g.row_begin + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // one row per warp
@@ -534,7 +534,6 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
     const uint32_t* row = bitmap + static_cast<size_t>(i) * g.words_per_row;
     const uint32_t wbeg = g.triangle ? (i / kTile) * 4 : 0;
     const uint32_t wpr = g.words_per_row;
-    const uint64_t hi = static_cast<uint64_t>(i) << 32;
     // the next batch's word is loaded before this batch is expanded, so the
     // load latency overlaps the expansion
     uint32_t word_next = wbeg + lane < wpr ? row[wbeg + lane] : 0u;
@@ -553,21 +552,21 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
         const uint32_t maxn = __reduce_max_sync(0xffffffffu, n);
         const uint32_t nzmask = __ballot_sync(0xffffffffu, word != 0u);
         if (maxn <= static_cast<uint32_t>(__popc(nzmask))) {
-          uint64_t* o = out + base + (inc - n);
+          uint32_t* o = out + base + (inc - n);
           const uint32_t col = wi * 32u;
           while (word) {
             const int b = __ffs(word) - 1;
             word &= word - 1;
-            *o++ = hi | (col + b);
+            *o++ = col + b;
           }
         } else {
-          uint64_t* o = out + base;
+          uint32_t* o = out + base;
           const uint32_t lt = (1u << lane) - 1u, ex = inc - n;
           for (uint32_t m = nzmask; m; m &= m - 1) {
             const int w = __ffs(m) - 1;
             const uint32_t wv = __shfl_sync(0xffffffffu, word, w);
             const uint32_t e = __shfl_sync(0xffffffffu, ex, w);
-            if ((wv >> lane) & 1u) o[e + __popc(wv & lt)] = hi | ((c + w) * 32u + lane);
+            if ((wv >> lane) & 1u) o[e + __popc(wv & lt)] = (c + w) * 32u + lane;
           }
         }
       } else {
@@ -575,7 +574,7 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
         while (word) {
           const int b = __ffs(word) - 1;
           word &= word - 1;
-          if (pos < capacity) out[pos] = hi | (wi * 32u + b);
+          if (pos < capacity) out[pos] = wi * 32u + b;
           ++pos;
         }
       }
@@ -585,14 +584,15 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
   }
 }
 
-// cols[i] = low 32 bits of keys[i] (the column of each sorted key); 16-byte
-// loads, two keys per thread.
-__global__ void keys_to_cols_kernel(const ulonglong2* __restrict__ keys, uint64_t n2, uint2* __restrict__ cols) {
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n2;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const ulonglong2 k = keys[i];
-    cols[i] = make_uint2(static_cast<uint32_t>(k.x), static_cast<uint32_t>(k.y));
-  }
+// keys[k] = (i << 32) | cols[k] for the pairs of row i (warp per row).
+__global__ void __launch_bounds__(256) cols_to_keys_kernel(const uint64_t* __restrict__ rowstart, uint32_t row_begin,
+                                                           uint32_t row_end, const uint32_t* __restrict__ cols,
+                                                           uint64_t* __restrict__ keys) {
+  const uint32_t i = row_begin + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= row_end) return;
+  const uint64_t hi = static_cast<uint64_t>(i) << 32;
+  const uint64_t e = rowstart[i + 1];
+  for (uint64_t k = rowstart[i] + (threadIdx.x & 31); k < e; k += 32) keys[k] = hi | cols[k];
 }
 
 int sms() {
@@ -695,22 +695,16 @@ void launch_hamming_bitmap(const uint64_t* f_rows, const uint64_t* f_cols, int m
   note_launch();
 }
 
-void launch_keys_to_cols(const uint64_t* keys, uint64_t n, uint32_t* cols, cudaStream_t s) {
-  if (n == 0) return;
-  const uint64_t n2 = n / 2;
-  if (n2) {
-    uint64_t blocks = ceil_div(n2, 256);
-    const uint64_t cap = static_cast<uint64_t>(sms()) * 8;
-    if (blocks > cap) blocks = cap;
-    keys_to_cols_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(reinterpret_cast<const ulonglong2*>(keys), n2,
-                                                                     reinterpret_cast<uint2*>(cols));
-    note_launch();
-  }
-  if (n & 1) cudaMemcpyAsync(cols + n - 1, keys + n - 1, 4, cudaMemcpyDeviceToDevice, s);  // low word (little endian)
+void launch_cols_to_keys(const uint64_t* rowstart, uint32_t row_begin, uint32_t row_end, const uint32_t* cols,
+                         uint64_t* keys, cudaStream_t s) {
+  if (row_end <= row_begin) return;
+  cols_to_keys_kernel<<<static_cast<unsigned>(ceil_div(row_end - row_begin, 8)), 256, 0, s>>>(rowstart, row_begin,
+                                                                                            row_end, cols, keys);
+  note_launch();
 }
 
 void launch_emit_pairs(const uint32_t* bitmap, const PairGrid& g, const uint32_t* rowcnt, const uint64_t* rowstart,
-                       uint64_t* out, uint64_t capacity, cudaStream_t s) {
+                       uint32_t* out, uint64_t capacity, cudaStream_t s) {
   if (g.row_end <= g.row_begin) return;
   const uint64_t blocks = ceil_div(g.row_end - g.row_begin, 8);  // one row per warp
   emit_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(bitmap, g, rowcnt, rowstart, out, capacity);

@@ -130,11 +130,13 @@ void launch_mrc_bitmap(const float* ST_rows, uint32_t ld_rows, const float* ST_c
                        float tau, const PairGrid& g, uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s);
 void launch_hamming_bitmap(const uint64_t* f_rows, const uint64_t* f_cols, int max_dist, const PairGrid& g,
                            uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s);
-// keys (i<<32|j) in ascending order at rowstart[i]..; writes only < capacity.
-// cols[i] = (uint32)keys[i]: sorted keys -> CSR column array.
-void launch_keys_to_cols(const uint64_t* keys, uint64_t n, uint32_t* cols, cudaStream_t s);
+// keys[k] = (i<<32) | cols[k] for rows [row_begin, row_end) (CSR -> sorted keys).
+void launch_cols_to_keys(const uint64_t* rowstart, uint32_t row_begin, uint32_t row_end, const uint32_t* cols,
+                         uint64_t* keys, cudaStream_t s);
+// Sorted CSR columns: row i's matches j ascending at cols[rowstart[i] ..);
+// writes only below capacity.
 void launch_emit_pairs(const uint32_t* bitmap, const PairGrid& g, const uint32_t* rowcnt, const uint64_t* rowstart,
-                       uint64_t* out, uint64_t capacity, cudaStream_t s);
+                       uint32_t* out, uint64_t capacity, cudaStream_t s);
 
 // ---- K4a simhash -------------------------------------------------------------
 struct SimhashArgs {
