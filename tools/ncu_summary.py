@@ -24,8 +24,9 @@ PROF = os.path.join(REPO, "profiles")
 
 # bench.py roofline keys -> kernel name fragments
 ROOF_KERNELS = {"mrc_tiles": ["mrc_bitmap_kernel"], "sign": ["sign_kernel"], "pair_emit": ["emit_kernel"],
-                "count": ["count_warp_kernel", "chunk_sort_kernel", "merge_kernel", "count_large_kernel",
-                          "idf_kernel"]}
+                "count": ["count_warp_kernel", "group_sort_kernel", "count_large_kernel", "idf_kernel"],
+                "reference": ["ref_mark_kernel", "ref_assign_kernel", "ref_fill_kernel"],
+                "simhash": ["simhash_kernel"], "hamming_tiles": ["hamming_bitmap_kernel"]}
 
 
 def short(name):
@@ -88,7 +89,7 @@ def full(path, tag):
     stall = [h for h in hdr if "issue_stalled" in h and h.endswith("per_issue_active.ratio")]
     lines = [f"# ncu --set full ({tag}) — per-kernel metrics", "",
              "Captured with `--set full --clock-control none --import-source on`; one launch per kernel of "
-             "tools/prof_pipeline.py --steps 1 --simhash (configs[1]). DRAM bytes are cold-cache (ncu flushes "
+             "tools/prof_pipeline.py --steps 1 (configs[1]: the MRC step). DRAM bytes are cold-cache (ncu flushes "
              "caches between replays).", ""]
     traffic = {}
     for r in rows[2:]:
@@ -105,7 +106,7 @@ def full(path, tag):
         rd = to_bytes(r[idx["dram__bytes_read.sum"]], units[idx["dram__bytes_read.sum"]])
         wr = to_bytes(r[idx["dram__bytes_write.sum"]], units[idx["dram__bytes_write.sum"]])
         for key, frags in ROOF_KERNELS.items():
-            if any(f in k for f in frags):
+            if any(f in k for f in frags) and not (key == "simhash" and "text_" in k):
                 traffic[key] = traffic.get(key, 0.0) + rd + wr
     open(os.path.join(PROF, f"ncu_full_{tag}.md"), "w").write("\n".join(lines) + "\n")
     json.dump({k: v for k, v in traffic.items()}, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
