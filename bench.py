@@ -300,6 +300,7 @@ def run_ours(args):
     # (not part of the MRC step; reported per kernel).
     rivals = measure_rivals(ctx, stream, flush, dev, thr, reps=max(5, args.steps))
     text_fe = measure_text_front_end(cp, stream, dev, reps=max(3, args.steps // 2)) if world == 1 else None
+    evaluation = measure_evaluation(ctx, stream, dev, refs, K) if world == 1 else None
 
     # End to end through the public API with HOST buffers: pinned tokens H2D,
     # full pipeline, candidate keys D2H into pinned memory.
@@ -321,6 +322,8 @@ def run_ours(args):
                                     clock_mhz))
         if text_fe:
             roof["text_front_end"] = text_fe
+        if evaluation:
+            roof["evaluation"] = evaluation
         traffic = load_traffic()
         for k, r in roof.items():
             r["traffic"] = traffic.get(k)
@@ -409,6 +412,28 @@ def measure_e2e(ctx, cp, refs, tau, lo, hi, stream, dev, steps, warmup):
         d2h = n * 4 + (hi - lo + 1) * 8 if mode == "csr" else n * 8 + 8
         res[mode] = {"_ms": 1e3 * sum(times) / len(times), "h2d": int(h2d), "d2h": int(d2h)}
     return res
+
+
+def measure_evaluation(ctx, stream, dev, refs, K):
+    """SPEC eval (Eq. 2/3) fused on the GPU over all C(N,2) pairs: exact cosine
+    (dense head + fixed-point tail) against MRC and Simhash, host wall clock of
+    one refsig_gpu_evaluate call (it synchronises)."""
+    import torch
+    import paper_1810_03099_b200 as R
+    with torch.cuda.stream(stream):
+        ctx.count(R.WEIGHT_TFIDF)
+        ctx.set_reference_docs(refs)
+        ctx.sign(fetch=False)
+        ctx.simhash(0, R.WEIGHT_TFIDF, fetch=False)
+        ctx.evaluate()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        e = ctx.evaluate()
+        t = time.perf_counter() - t0
+    return {"ms": t * 1e3, "pairs": e["pairs"], "pairs_per_sec": e["pairs"] / t,
+            **{k: v for k, v in e.items() if k != "pairs"},
+            "note": "exact cosine of every pair (64 dense head terms + fixed-point tail) vs MRC compare and "
+                    "Simhash similarity, MAE / mean error / variance in double (configs[1], TF-IDF)"}
 
 
 def measure_text_front_end(cp, stream, dev, reps):

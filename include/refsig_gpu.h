@@ -166,6 +166,21 @@ int refsig_gpu_exact_pairs(refsig_gpu_ctx* ctx, float tau_cos, uint64_t* out_pai
 /* Exact cosine (fp32) of the corpus' weighted vectors for n pair keys. */
 int refsig_gpu_pair_cosines(refsig_gpu_ctx* ctx, const uint64_t* keys, uint64_t n, float* out);
 
+/* ---- evaluation (SPEC.md eval, Eq. 2/3) -----------------
+ * Over all pairs i<j with row_lo <= i < row_hi (row_lo a multiple of 128):
+ * e = score - exact cosine of the weighted vectors (the exact verifier's
+ * definition; count(REFSIG_WEIGHT_TF) gives the reference's 3-gram-count
+ * cosine); mae = mean |e|, mean_error = mean e, variance = mean (e -
+ * mean_error)^2, for MRC (compare of the signatures) and, when fingerprints
+ * exist, Simhash (1 - hd/64). Fused on the GPU: no pair list is materialised;
+ * sums are accumulated in double in a fixed order (deterministic). */
+typedef struct {
+  uint64_t pairs;
+  double mrc_mae, mrc_mean_error, mrc_variance;
+  double simhash_mae, simhash_mean_error, simhash_variance; /* NaN without fingerprints */
+} refsig_gpu_eval;
+int refsig_gpu_evaluate(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_hi, refsig_gpu_eval* out);
+
 /* ---- query-vs-database mode (configs[4]) -------------------------------------
  * `db` holds the signed/fingerprinted database; `q` holds the query corpus,
  * counted with the database's IDF and signed against its reference. */

@@ -81,6 +81,8 @@ def lib():
         L.orc_word_hash64.argtypes = [u8p, ctypes.c_uint64]
         L.orc_word_hash64.restype = ctypes.c_uint64
         L.orc_text_simhash.argtypes = [u8p, u64p, ctypes.c_uint32, u64p, ctypes.c_int]
+        L.orc_evaluate.argtypes = [u64p, u32p, f64p, f64p, ctypes.c_uint32, f64p, ctypes.c_uint32, u64p,
+                                   ctypes.c_uint32, ctypes.c_uint32, f64p, ctypes.c_int]
         _orc = L
     return _orc
 
@@ -236,6 +238,30 @@ def mrc_pairs(S: np.ndarray, tau: float, band: float = 1e-5, row_lo: int = 0, ro
     lib().orc_mrc_pairs(_p(S, ctypes.c_double), n, K, tau, band, row_lo, n if row_hi is None else row_hi,
                         ctypes.byref(pr), threads)
     return _take_pairs(pr)
+
+
+def evaluate(x: Weighted, S: np.ndarray, fp: np.ndarray | None = None, row_lo: int = 0,
+             row_hi: int | None = None, threads: int = 0) -> dict:
+    """SPEC eval (Eq. 2/3) over pairs i<j of rows [row_lo, row_hi): MAE, mean
+    error and variance of MRC (and Simhash) against the exact cosine."""
+    S = np.ascontiguousarray(S, np.float64)
+    n, K = S.shape
+    out = np.zeros(7, np.float64)
+    fpa = None if fp is None else np.ascontiguousarray(fp, np.uint64)
+    lib().orc_evaluate(_p(x.rowptr, ctypes.c_uint64), _p(x.ids, ctypes.c_uint32), _p(x.w, ctypes.c_double),
+                       _p(x.norm, ctypes.c_double), n, _p(S, ctypes.c_double), K, _p(fpa, ctypes.c_uint64), row_lo,
+                       n if row_hi is None else row_hi, _p(out, ctypes.c_double), threads)
+    m = out[0]
+    res = {"pairs": int(m)}
+    for name, o in (("mrc", 1), ("simhash", 4)):
+        mean = out[o] / m
+        res[name + "_mae"] = out[o + 2] / m
+        res[name + "_mean_error"] = mean
+        res[name + "_variance"] = max(0.0, out[o + 1] / m - mean * mean)
+    if fp is None:
+        for k in ("simhash_mae", "simhash_mean_error", "simhash_variance"):
+            res[k] = float("nan")
+    return res
 
 
 def mrc_query_pairs(Sq, Sd, tau: float, band: float = 1e-5, threads: int = 0):

@@ -6,6 +6,7 @@
 #include "oracle.h"
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -494,6 +495,43 @@ void orc_text_simhash(const uint8_t* bytes, const uint64_t* off, uint32_t n, uin
       if (col[j] > 0) out |= 1ull << j;
     fp[d] = out;
   });
+}
+
+
+// ---- evaluation (SPEC.md eval: evaluate, Eq. 2/3) ---------------------------
+// Over all pairs i<j of rows [row_lo, row_hi): exact = cosine of the weighted
+// vectors (merge-join, ngram.hpp:184-202), mrc = compare of the signatures
+// (SPEC.md:369-377), sim = 1 - hd/64 (simhash.hpp:49-52); e = score - exact.
+// out[0..6] = {pairs, sum e_mrc, sum e_mrc^2, sum |e_mrc|, sum e_sim,
+// sum e_sim^2, sum |e_sim|} (fp may be NULL: Simhash sums 0).
+void orc_evaluate(const uint64_t* rowptr, const uint32_t* ids, const double* w, const double* norm, uint32_t n,
+                  const double* S, uint32_t K, const uint64_t* fp, uint32_t row_lo, uint32_t row_hi, double* out,
+                  int threads) {
+  const int T = threads > 0 ? threads : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  std::vector<std::array<double, 7>> acc(T);
+  for (auto& a : acc) a.fill(0.0);
+  parallel_rows(row_lo, row_hi, threads, 8, [&](uint64_t i, int tid) {
+    auto& a = acc[tid];
+    for (uint64_t j = i + 1; j < n; ++j) {
+      const double ex = orc_cosine(ids + rowptr[i], w + rowptr[i], rowptr[i + 1] - rowptr[i], norm[i],
+                                   ids + rowptr[j], w + rowptr[j], rowptr[j + 1] - rowptr[j], norm[j]);
+      const double em = orc_compare(S + i * K, S + j * K, K) - ex;
+      a[0] += 1;
+      a[1] += em;
+      a[2] += em * em;
+      a[3] += std::fabs(em);
+      if (fp) {
+        const double es = (1.0 - __builtin_popcountll(fp[i] ^ fp[j]) / 64.0) - ex;
+        a[4] += es;
+        a[5] += es * es;
+        a[6] += std::fabs(es);
+      }
+    }
+  });
+  for (int q = 0; q < 7; ++q) {
+    out[q] = 0;
+    for (int t = 0; t < T; ++t) out[q] += acc[t][q];
+  }
 }
 
 }  // extern "C"

@@ -106,6 +106,11 @@ int orc_exact_pairs(const uint64_t* rowptr, const uint32_t* ids, const double* w
 void orc_cosine_pairs(const uint64_t* rowptr, const uint32_t* ids, const double* w, const double* norm,
                       const uint64_t* keys, uint64_t n_keys, double* out, int threads);
 
+/* SPEC eval over pairs i<j of rows [row_lo,row_hi): out[7] = {pairs, sum e, sum e^2,
+ * sum |e| for MRC, then the same for Simhash (fp NULL: zeros)}, e = score - exact. */
+void orc_evaluate(const uint64_t* rowptr, const uint32_t* ids, const double* w, const double* norm, uint32_t n,
+                  const double* S, uint32_t K, const uint64_t* fp, uint32_t row_lo, uint32_t row_hi, double* out,
+                  int threads);
 /* Text front end (ngram.hpp:114-180, simhash.hpp:23-45): per doc the 3-gram
  * ids in document order (tokens may be NULL), gram_off[n+1]; returns the total. */
 uint64_t orc_text_grams(const uint8_t* bytes, const uint64_t* off, uint32_t n, uint32_t* tokens, uint64_t* gram_off);

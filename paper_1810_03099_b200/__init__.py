@@ -92,6 +92,7 @@ SIGNATURES = {
     "refsig_gpu_hamming_query_pairs": ([_c.c_void_p, _c.c_int, _P(_c.c_uint64), _c.c_uint64, _P(_c.c_uint64)],
                                        _c.c_int),
     "refsig_gpu_get_pairs": ([_c.c_void_p, _P(_c.c_uint64), _c.c_uint64], _c.c_int),
+    "refsig_gpu_evaluate": ([_c.c_void_p, _c.c_uint32, _c.c_uint32, _c.c_void_p], _c.c_int),
     "refsig_gpu_load_text": ([_c.c_void_p, _P(_c.c_uint8), _P(_c.c_uint64), _c.c_uint32], _c.c_int),
     "refsig_gpu_simhash_text": ([_c.c_void_p], _c.c_int),
     "refsig_gpu_get_pairs_csr": ([_c.c_void_p, _c.c_uint32, _c.c_uint32, _P(_c.c_uint64), _P(_c.c_uint32), _c.c_uint64,
@@ -379,6 +380,19 @@ class Context:
     @staticmethod
     def launch_count() -> int:
         return load_library().refsig_gpu_launch_count()
+
+    def evaluate(self, row_lo: int = 0, row_hi: int | None = None) -> dict:
+        """SPEC eval (Eq. 2/3) over all pairs i<j, row_lo <= i < row_hi: MAE,
+        mean error and variance of MRC (and Simhash, if fingerprints exist)
+        against the exact cosine, fused on the GPU."""
+        class _Eval(ctypes.Structure):
+            _fields_ = [("pairs", ctypes.c_uint64)] + [(k, ctypes.c_double) for k in (
+                "mrc_mae", "mrc_mean_error", "mrc_variance", "simhash_mae", "simhash_mean_error",
+                "simhash_variance")]
+        e = _Eval()
+        hi = self.n_docs if row_hi is None else row_hi
+        self._check(self._L.refsig_gpu_evaluate(self._h, row_lo, hi, ctypes.byref(e)))
+        return {k: getattr(e, k) for k, _ in _Eval._fields_}
 
     def load_text(self, text, byte_off: np.ndarray):
         """Raw documents text[byte_off[d]:byte_off[d+1]] (bytes or uint8 array):

@@ -142,6 +142,7 @@ struct refsig_gpu_ctx {
   // exact
   bool have_x = false;
   DevBuf x, post_off, post_fill, posts, head_col, headA, head_norm, tail_df;  // K5
+  DevBuf headAT, eval_tail, eval_part;                                         // evaluation
 
   // query mode
   refsig_gpu_ctx* db = nullptr;
@@ -522,6 +523,49 @@ PairGrid self_grid(const refsig_gpu_ctx* c) {
 }
 
 }  // namespace
+
+// K5 inputs (exact verifier and evaluation): unit weights, the kExactHead
+// highest-df terms as dense rows + norms, and the tail postings. Returns H.
+uint32_t prepare_exact(refsig_gpu_ctx* ctx) {
+  const uint32_t N = ctx->n_docs, V = ctx->vocab;
+  ensure_unit_weights(ctx);
+  // head terms: the kExactHead highest df (ties by id), from the device df
+  const uint32_t H = std::min<uint32_t>(kExactHead, (V + 3) & ~3u);
+  std::vector<uint32_t> hdf(V);
+  ck(cudaMemcpyAsync(hdf.data(), ctx->df.p, 4ull * V, cudaMemcpyDeviceToHost, ctx->stream), "D2H df");
+  sync(ctx);
+  std::vector<uint32_t> ids(V);
+  for (uint32_t t = 0; t < V; ++t) ids[t] = t;
+  const uint32_t nh = std::min(H, V);
+  std::partial_sort(ids.begin(), ids.begin() + nh, ids.end(),
+                    [&](uint32_t a, uint32_t b) { return hdf[a] != hdf[b] ? hdf[a] > hdf[b] : a < b; });
+  std::vector<int32_t> head_col(V, -1);
+  for (uint32_t k = 0; k < nh; ++k) head_col[ids[k]] = static_cast<int32_t>(k);
+  ctx->head_col.ensure(4ull * V);
+  upload(ctx, ctx->head_col.p, head_col.data(), 4ull * V);
+  // dense head rows + their norms
+  ctx->headA.ensure(sizeof(float) * static_cast<size_t>(N) * H);
+  ctx->head_norm.ensure(sizeof(float) * N);
+  ck(cudaMemsetAsync(ctx->headA.p, 0, sizeof(float) * static_cast<size_t>(N) * H, ctx->stream), "memset A");
+  launch_head_rows(ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->x.as<float>(),
+                   ctx->head_col.as<int32_t>(), N, H, ctx->headA.as<float>(), ctx->head_norm.as<float>(),
+                   ctx->stream);
+  // tail postings: offsets = exclusive scan of the tail df, then an atomic fill
+  ctx->post_off.ensure(8ull * (V + 1));
+  ctx->post_fill.ensure(8ull * (V + 1));
+  ctx->tail_df.ensure(4ull * V);
+  ctx->posts.ensure(sizeof(uint2) * std::max<uint64_t>(ctx->n_tokens, 1));
+  ctx->scan_tmp.ensure(scan_tmp_bytes(std::max(N, V)));
+  launch_tail_df(ctx->df.as<uint32_t>(), ctx->head_col.as<int32_t>(), V, ctx->tail_df.as<uint32_t>(), ctx->stream);
+  launch_exclusive_scan_u32_to_u64(ctx->tail_df.as<uint32_t>(), ctx->post_off.as<uint64_t>(), V, ctx->scan_tmp.p,
+                                   ctx->stream);
+  ck(cudaMemcpyAsync(ctx->post_fill.p, ctx->post_off.p, 8ull * (V + 1), cudaMemcpyDeviceToDevice, ctx->stream),
+     "copy");
+  launch_postings_fill(ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(),
+                       ctx->x.as<float>(), ctx->head_col.as<int32_t>(), N, ctx->post_fill.as<uint64_t>(),
+                       ctx->posts.as<uint2>(), ctx->stream);
+  return H;
+}
 
 extern "C" {
 
@@ -1008,42 +1052,7 @@ int refsig_gpu_exact_pairs(refsig_gpu_ctx* ctx, float tau_cos, uint64_t* out_pai
     require(tau_cos > 0.0f && tau_cos <= 1.0f, "tau_cos must be in (0, 1]");
     require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
     const uint32_t N = ctx->n_docs, V = ctx->vocab;
-    ensure_unit_weights(ctx);
-    // head terms: the kExactHead highest df (ties by id), from the device df
-    const uint32_t H = std::min<uint32_t>(kExactHead, (V + 3) & ~3u);
-    std::vector<uint32_t> hdf(V);
-    ck(cudaMemcpyAsync(hdf.data(), ctx->df.p, 4ull * V, cudaMemcpyDeviceToHost, ctx->stream), "D2H df");
-    sync(ctx);
-    std::vector<uint32_t> ids(V);
-    for (uint32_t t = 0; t < V; ++t) ids[t] = t;
-    const uint32_t nh = std::min(H, V);
-    std::partial_sort(ids.begin(), ids.begin() + nh, ids.end(),
-                      [&](uint32_t a, uint32_t b) { return hdf[a] != hdf[b] ? hdf[a] > hdf[b] : a < b; });
-    std::vector<int32_t> head_col(V, -1);
-    for (uint32_t k = 0; k < nh; ++k) head_col[ids[k]] = static_cast<int32_t>(k);
-    ctx->head_col.ensure(4ull * V);
-    upload(ctx, ctx->head_col.p, head_col.data(), 4ull * V);
-    // dense head rows + their norms
-    ctx->headA.ensure(sizeof(float) * static_cast<size_t>(N) * H);
-    ctx->head_norm.ensure(sizeof(float) * N);
-    ck(cudaMemsetAsync(ctx->headA.p, 0, sizeof(float) * static_cast<size_t>(N) * H, ctx->stream), "memset A");
-    launch_head_rows(ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->x.as<float>(),
-                     ctx->head_col.as<int32_t>(), N, H, ctx->headA.as<float>(), ctx->head_norm.as<float>(),
-                     ctx->stream);
-    // tail postings: offsets = exclusive scan of the tail df, then an atomic fill
-    ctx->post_off.ensure(8ull * (V + 1));
-    ctx->post_fill.ensure(8ull * (V + 1));
-    ctx->tail_df.ensure(4ull * V);
-    ctx->posts.ensure(sizeof(uint2) * std::max<uint64_t>(ctx->n_tokens, 1));
-    ctx->scan_tmp.ensure(scan_tmp_bytes(std::max(N, V)));
-    launch_tail_df(ctx->df.as<uint32_t>(), ctx->head_col.as<int32_t>(), V, ctx->tail_df.as<uint32_t>(), ctx->stream);
-    launch_exclusive_scan_u32_to_u64(ctx->tail_df.as<uint32_t>(), ctx->post_off.as<uint64_t>(), V, ctx->scan_tmp.p,
-                                     ctx->stream);
-    ck(cudaMemcpyAsync(ctx->post_fill.p, ctx->post_off.p, 8ull * (V + 1), cudaMemcpyDeviceToDevice, ctx->stream),
-       "copy");
-    launch_postings_fill(ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(),
-                         ctx->x.as<float>(), ctx->head_col.as<int32_t>(), N, ctx->post_fill.as<uint64_t>(),
-                         ctx->posts.as<uint2>(), ctx->stream);
+    const uint32_t H = prepare_exact(ctx);
     const PairGrid g = self_grid(ctx);
     {
       Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
@@ -1053,13 +1062,76 @@ int refsig_gpu_exact_pairs(refsig_gpu_ctx* ctx, float tau_cos, uint64_t* out_pai
                   ctx->posts.as<uint2>(),      ctx->headA.as<float>(),      ctx->head_norm.as<float>(),
                   H,                           N,                           std::min<uint32_t>(N, kExactPanel),
                   tau_cos,                     ctx->bitmap.as<uint32_t>(),  g.words_per_row,
-                  ctx->rowcnt.as<uint32_t>()};
+                  ctx->rowcnt.as<uint32_t>(),  nullptr};
       launch_exact_tail(a, 0, N, ctx->stream);
       launched("exact");
     }
     rc2 = run_emit(ctx, g, out_pairs, capacity, out_count);
   });
   return rc != REFSIG_OK ? rc : rc2;
+}
+
+int refsig_gpu_evaluate(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_hi, refsig_gpu_eval* out) {
+  return guard(ctx, [&] {
+    require(ctx->counted && ctx->signed_, "count() and sign() first");
+    require(out != nullptr, "NULL output");
+    const uint32_t N = ctx->n_docs;
+    require(row_lo <= row_hi && row_hi <= N, "bad row range");
+    require(row_lo % 128 == 0, "row_lo must be a multiple of 128");
+    require(ctx->emit_pending == false, "pair computation in flight");
+    const uint32_t H = prepare_exact(ctx);
+    const uint32_t ld = ctx->ld;
+    ctx->headAT.ensure(sizeof(float) * static_cast<size_t>(H) * ld);
+    launch_transpose_head(ctx->headA.as<float>(), N, H, ld, ctx->headAT.as<float>(), ctx->stream);
+    // row panels (multiples of 128 rows) whose fixed-point tail sums fit ~2 GB
+    uint64_t panel = std::max<uint64_t>(128, ((2ull << 30) / (4ull * N)) / 128 * 128);
+    const uint32_t grid = eval_grid();
+    ctx->eval_part.ensure(sizeof(double) * 8 * grid);
+    std::vector<double> part(8 * grid);
+    double sum[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (uint64_t p0 = row_lo; p0 < row_hi; p0 += panel) {
+      const uint32_t p1 = static_cast<uint32_t>(std::min<uint64_t>(row_hi, p0 + panel));
+      ctx->eval_tail.ensure(4ull * (p1 - p0) * N);
+      {
+        Phase ph(ctx, REFSIG_PHASE_PAIR_TILES);
+        ExactArgs a{ctx->ent.as<uint2>(),        ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(),
+                    ctx->x.as<float>(),          ctx->head_col.as<int32_t>(), ctx->post_off.as<uint64_t>(),
+                    ctx->posts.as<uint2>(),      ctx->headA.as<float>(),      ctx->head_norm.as<float>(),
+                    H,                           N,                           std::min<uint32_t>(N, kExactPanel),
+                    0.0f,                        nullptr,                     0,
+                    nullptr,                     ctx->eval_tail.as<uint32_t>()};
+        launch_exact_tail(a, static_cast<uint32_t>(p0), p1, ctx->stream);
+        EvalArgs e{ctx->headAT.as<float>(), H, ctx->ST.as<float>(), ctx->K, ld,
+                   ctx->have_fp ? ctx->fp.as<uint64_t>() : nullptr, ctx->eval_tail.as<uint32_t>(), N,
+                   static_cast<uint32_t>(p0), p1, ctx->eval_part.as<double>()};
+        launch_eval_tiles(e, ctx->stream);
+        launched("evaluate");
+      }
+      ck(cudaMemcpyAsync(part.data(), ctx->eval_part.p, sizeof(double) * 8 * grid, cudaMemcpyDeviceToHost,
+                         ctx->stream),
+         "D2H eval");
+      sync(ctx);
+      for (uint32_t b = 0; b < grid; ++b)  // CTA order: deterministic
+        for (int q = 0; q < 7; ++q) sum[q] += part[8 * b + q];
+    }
+    const double n = sum[0];
+    out->pairs = static_cast<uint64_t>(n);
+    const double nan = std::nan("");
+    auto fill = [&](double se, double sq, double sa, double* mae, double* me, double* var) {
+      if (n <= 0) {
+        *mae = *me = *var = nan;
+        return;
+      }
+      *mae = sa / n;
+      *me = se / n;
+      *var = std::max(0.0, sq / n - (*me) * (*me));
+    };
+    fill(sum[1], sum[2], sum[3], &out->mrc_mae, &out->mrc_mean_error, &out->mrc_variance);
+    if (ctx->have_fp)
+      fill(sum[4], sum[5], sum[6], &out->simhash_mae, &out->simhash_mean_error, &out->simhash_variance);
+    else
+      out->simhash_mae = out->simhash_mean_error = out->simhash_variance = nan;
+  });
 }
 
 int refsig_gpu_pair_cosines(refsig_gpu_ctx* ctx, const uint64_t* keys, uint64_t n, float* out) {

@@ -129,6 +129,12 @@ __global__ void __launch_bounds__(512) exact_tail_kernel(ExactArgs a, uint32_t r
       }
     }
     __syncthreads();
+    if (a.tail_out) {  // evaluation mode: hand the exact tail sums to the tile pass
+      uint32_t* dst = a.tail_out + static_cast<size_t>(blockIdx.x) * a.n_docs;
+      for (uint32_t j = jlo + threadIdx.x; j < c1; j += blockDim.x) dst[j] = acc[j - c0];
+      __syncthreads();
+      continue;
+    }
     // 2. bound, head dot, threshold
     for (uint32_t j = jlo + threadIdx.x; j < c1; j += blockDim.x) {
       const float tail = static_cast<float>(acc[j - c0]) * (1.0f / kFix);
@@ -154,10 +160,143 @@ __global__ void __launch_bounds__(512) exact_tail_kernel(ExactArgs a, uint32_t r
   cnt = warp_sum_u32(cnt);
   if (lane == 0) red[wid] = cnt;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && !a.tail_out) {
     uint32_t s = 0;
     for (uint32_t w = 0; w < nwarp; ++w) s += red[w];
     a.rowcnt[i] = s;
+  }
+}
+
+// ---- fused evaluation tiles (Eq. 2/3 of the paper, SPEC.md eval) ----------
+// 64 x 128 pair tiles of the triangle, contiguous tile ranges per CTA; thread
+// (ty, tx) owns rows ty*4..+3 and columns tx*8..+7 (32 pairs). Per tile: the
+// head dot (H k-steps) and the MRC dot (K k-steps) from k-major panels staged
+// in shared memory, the tail sums T (exact fixed point), the fingerprints;
+// per pair the two errors against the exact cosine go into per-thread double
+// sums (n, sum e, sum e^2, sum |e|) that are reduced in a fixed order.
+constexpr int kEvR = 64, kEvC = 128;
+
+// Tile t of row blocks br0.. (64 rows each): row block r has the col blocks
+// r/2 .. nbc-1 (128 columns each, the ones holding some j > i).
+__device__ __forceinline__ void eval_tile_coords(uint32_t t, uint32_t br0, uint32_t br1, uint32_t nbc, uint32_t& bi,
+                                                 uint32_t& bj) {
+  uint32_t r = br0;
+  while (r < br1) {
+    const uint32_t cnt = nbc - r / 2;
+    if (t < cnt) break;
+    t -= cnt;
+    ++r;
+  }
+  bi = r;
+  bj = r / 2 + t;
+}
+
+template <bool HEAD>
+__device__ __forceinline__ void eval_dot(const float* __restrict__ src, uint32_t KK, uint32_t ld, uint32_t r0,
+                                         uint32_t cb, float* P, float* Q, uint32_t tid, uint32_t tx, uint32_t ty,
+                                         float (&acc)[4][8]) {
+  for (uint32_t k0 = 0; k0 < KK; k0 += 32) {
+    const uint32_t kc = min(32u, KK - k0);
+    __syncthreads();
+    for (uint32_t idx = tid; idx < kc * kEvR; idx += 256) {
+      const uint32_t k = idx / kEvR, rr = idx % kEvR;
+      P[k * kEvR + rr] = src[static_cast<size_t>(k0 + k) * ld + r0 + rr];
+    }
+    for (uint32_t idx = tid; idx < kc * kEvC; idx += 256) {
+      const uint32_t k = idx / kEvC, cc = idx % kEvC;
+      Q[k * kEvC + cc] = src[static_cast<size_t>(k0 + k) * ld + cb + cc];
+    }
+    __syncthreads();
+    for (uint32_t k = 0; k < kc; ++k) {
+      const float4 pa = *reinterpret_cast<const float4*>(P + k * kEvR + ty * 4);
+      const float4 q0 = *reinterpret_cast<const float4*>(Q + k * kEvC + tx * 8);
+      const float4 q1 = *reinterpret_cast<const float4*>(Q + k * kEvC + tx * 8 + 4);
+      const float av[4] = {pa.x, pa.y, pa.z, pa.w};
+      const float bv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(av[r], bv[c], acc[r][c]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) eval_tiles_kernel(EvalArgs a, uint32_t nbr, uint32_t nbc, uint32_t br0,
+                                                         uint64_t n_tiles) {
+  extern __shared__ __align__(16) float esm[];  // A rows [kk][64] | A cols [kk][128], kk <= 32 per chunk
+  __shared__ double red[8][8];
+  const uint32_t tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const uint64_t t0 = n_tiles * blockIdx.x / gridDim.x, t1 = n_tiles * (blockIdx.x + 1) / gridDim.x;
+  double sm_e = 0, sm_q = 0, sm_a = 0, ss_e = 0, ss_q = 0, ss_a = 0;
+  uint64_t cnt = 0;
+  float* P = esm;               // rows panel [32][64]
+  float* Q = esm + 32 * kEvR;   // cols panel [32][128]
+  for (uint64_t t = t0; t < t1; ++t) {
+    uint32_t bi, bj;
+    eval_tile_coords(static_cast<uint32_t>(t), br0, br0 + nbr, nbc, bi, bj);
+    const uint32_t r0 = bi * kEvR, cb = bj * kEvC;
+    float hd[4][8], md[4][8];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) hd[r][c] = md[r][c] = 0.0f;
+    eval_dot<true>(a.AT, a.H, a.ld, r0, cb, P, Q, tid, tx, ty, hd);   // head dot (exact cosine part)
+    eval_dot<false>(a.ST, a.K, a.ld, r0, cb, P, Q, tid, tx, ty, md);  // MRC compare
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t i = r0 + ty * 4 + r;
+      if (i < a.row_lo || i >= a.row_hi) continue;
+      const uint32_t* trow = a.T + static_cast<size_t>(i - a.row_lo) * a.n_docs;
+      const uint64_t fi = a.fp ? a.fp[i] : 0ull;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t j = cb + tx * 8 + c;
+        if (j <= i || j >= a.n_docs) continue;
+        const float ex = fminf(hd[r][c] + static_cast<float>(trow[j]) * (1.0f / 1073741824.0f), 1.0f);
+        const double em = static_cast<double>(fminf(md[r][c], 1.0f)) - static_cast<double>(ex);
+        sm_e += em;
+        sm_q = fma(em, em, sm_q);
+        sm_a += fabs(em);
+        if (a.fp) {
+          const double es = (1.0 - __popcll(fi ^ a.fp[j]) / 64.0) - static_cast<double>(ex);
+          ss_e += es;
+          ss_q = fma(es, es, ss_q);
+          ss_a += fabs(es);
+        }
+        ++cnt;
+      }
+    }
+  }
+  // fixed-order reduction: warp tree, then warps in order
+  double v[7] = {static_cast<double>(cnt), sm_e, sm_q, sm_a, ss_e, ss_q, ss_a};
+#pragma unroll
+  for (int q = 0; q < 7; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+  if ((tid & 31) == 0)
+#pragma unroll
+    for (int q = 0; q < 7; ++q) red[tid >> 5][q] = v[q];
+  __syncthreads();
+  if (tid < 7) {
+    double x = 0;
+    for (int w = 0; w < 8; ++w) x += red[w][tid];
+    a.out[blockIdx.x * 8 + tid] = x;
+  }
+  if (tid == 7) a.out[blockIdx.x * 8 + 7] = 0.0;
+}
+
+__global__ void transpose_head_kernel(const float* __restrict__ A, uint32_t n, uint32_t H, uint32_t ld,
+                                      float* __restrict__ AT) {
+  __shared__ float tile[32][33];
+  const uint32_t d0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  for (uint32_t r = threadIdx.y; r < 32; r += blockDim.y) {
+    const uint32_t d = d0 + r, c = c0 + threadIdx.x;
+    tile[r][threadIdx.x] = (d < n && c < H) ? A[static_cast<size_t>(d) * H + c] : 0.0f;
+  }
+  __syncthreads();
+  for (uint32_t r = threadIdx.y; r < 32; r += blockDim.y) {
+    const uint32_t c = c0 + r, d = d0 + threadIdx.x;
+    if (c < H && d < ld) AT[static_cast<size_t>(c) * ld + d] = tile[threadIdx.x][r];
   }
 }
 
@@ -248,6 +387,28 @@ void launch_exact_tail(const ExactArgs& a, uint32_t row_lo, uint32_t row_hi, cud
     configured = smem;
   }
   exact_tail_kernel<<<row_hi - row_lo, 512, smem, s>>>(a, row_lo);
+  note_launch();
+}
+
+uint32_t eval_grid() { return static_cast<uint32_t>(sm_count()) * 2; }
+
+void launch_eval_tiles(const EvalArgs& a, cudaStream_t s) {
+  if (a.row_hi <= a.row_lo) return;
+  const uint32_t br0 = a.row_lo / kEvR, br1 = static_cast<uint32_t>(ceil_div(a.row_hi, kEvR));
+  const uint32_t nbc = static_cast<uint32_t>(ceil_div(a.n_docs, kEvC));
+  // tiles of row blocks [br0, br1): block r has col blocks r/2 .. nbc-1 (global r)
+  uint64_t n_tiles = 0;
+  for (uint32_t r = br0; r < br1; ++r) n_tiles += nbc - r / 2;
+  // eval_tile_coords enumerates from row block br0 with the same rule: shift by br0 (even, panels
+  // start at multiples of 128 rows = 2 row blocks) so r/2 stays the global value
+  const size_t smem = sizeof(float) * 32 * (kEvR + kEvC);
+  eval_tiles_kernel<<<eval_grid(), 256, smem, s>>>(a, br1 - br0, nbc, br0, n_tiles);
+  note_launch();
+}
+
+void launch_transpose_head(const float* A, uint32_t n_docs, uint32_t H, uint32_t ld, float* AT, cudaStream_t s) {
+  dim3 g(static_cast<unsigned>(ceil_div(ld, 32)), static_cast<unsigned>(ceil_div(H, 32)));
+  transpose_head_kernel<<<g, dim3(32, 8), 0, s>>>(A, n_docs, H, ld, AT);
   note_launch();
 }
 

@@ -174,6 +174,8 @@ struct ExactArgs {
   uint32_t* bitmap;          // zeroed rows, words_per_row words each
   uint32_t words_per_row;
   uint32_t* rowcnt;
+  uint32_t* tail_out;        // evaluation mode: the fixed-point tail sums of rows [row_lo, row_hi) for
+                             // j > i, row-major [row_hi-row_lo][n_docs] (no threshold, no bitmap)
 };
 void launch_unit_weights(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const TermInfo* info,
                          const float* inv_norm, uint32_t n_docs, float* x, cudaStream_t s);
@@ -185,6 +187,26 @@ void launch_head_rows(const uint2* ent, const uint64_t* doc_off, const uint32_t*
                       const int32_t* head_col, uint32_t n_docs, uint32_t H, float* A, float* hn, cudaStream_t s);
 // Rows [row_lo, row_hi): tail accumulation, bound, head dot, threshold into the bitmap.
 void launch_exact_tail(const ExactArgs& a, uint32_t row_lo, uint32_t row_hi, cudaStream_t s);
+// ---- fused evaluation -------------------------------------
+// Per pair i<j of rows [row_lo, row_hi): exact = min(A_i.A_j + T_ij * 2^-30, 1)
+// (dense head + fixed-point tail), mrc = min(S^_i.S^_j, 1), sim = 1 - hd/64;
+// e = score - exact. out[cta*8 + {0..7}] = {n, sum e_mrc, sum e_mrc^2,
+// sum |e_mrc|, sum e_sim, sum e_sim^2, sum |e_sim|, 0} (double, fixed order).
+struct EvalArgs {
+  const float* AT;   // [H][ld] head rows, k-major, zero-padded columns
+  uint32_t H;        // multiple of 4
+  const float* ST;   // [K][ld] unit signatures
+  uint32_t K;
+  uint32_t ld;
+  const uint64_t* fp;  // [n_docs] fingerprints (NULL: no Simhash errors)
+  const uint32_t* T;   // tail sums, row-major [row_hi-row_lo][n_docs]
+  uint32_t n_docs, row_lo, row_hi;
+  double* out;         // [grid*8]
+};
+uint32_t eval_grid();
+void launch_eval_tiles(const EvalArgs& a, cudaStream_t s);
+// AT[c*ld + d] = A[d*H + c] (ld >= n_docs, pad columns zero).
+void launch_transpose_head(const float* A, uint32_t n_docs, uint32_t H, uint32_t ld, float* AT, cudaStream_t s);
 void launch_pair_cosines(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const float* x,
                          const uint64_t* keys, uint64_t n_keys, float* out, cudaStream_t s);
 

@@ -400,3 +400,33 @@ def test_pairs_csr_matches_keys(gpu_ctx_factory):
     if len(keys) > 1:
         with pytest.raises(R.PairOverflowError):
             ctx.pairs_csr(cols=np.empty(len(keys) - 1, np.uint32))
+
+
+@pytest.mark.parametrize("weighting", [R.WEIGHT_TF, R.WEIGHT_TFIDF])
+def test_evaluate_vs_oracle(gpu_ctx_factory, weighting):
+    """SPEC eval (Eq. 2/3) fused on the GPU: MAE, mean error and variance of MRC
+    and Simhash against the exact cosine over all pairs (c0 shape, 1200 docs)."""
+    cp, cfg = C.config_corpus("c0")
+    cp = cp.slice_docs(1200)
+    refs = C.sample_refs(0, cp.n_docs, cfg["K"])
+    ctx = gpu_ctx_factory()
+    ctx.load_corpus(cp.tokens, cp.doc_off, cp.vocab)
+    ctx.count(weighting)
+    ctx.set_reference_docs(refs)
+    ctx.sign(fetch=False)
+    ctx.simhash(0, weighting)
+    g = ctx.evaluate()
+    o = oracle.mrc_pipeline(cp.tokens, cp.doc_off, cp.vocab, refs,
+                            "tfidf" if weighting == R.WEIGHT_TFIDF else "tf")
+    fp = oracle.simhash(o.counts, o.idf if weighting == R.WEIGHT_TFIDF else None, 0)
+    ref = oracle.evaluate(o.x, o.S, fp)
+    assert g["pairs"] == ref["pairs"] == cp.n_docs * (cp.n_docs - 1) // 2
+    for k in ("mrc_mae", "mrc_mean_error", "simhash_mae", "simhash_mean_error"):
+        assert abs(g[k] - ref[k]) <= 2e-6 + 1e-5 * abs(ref[k]), (k, g[k], ref[k])
+    for k in ("mrc_variance", "simhash_variance"):
+        assert abs(g[k] - ref[k]) <= 1e-7 + 1e-4 * abs(ref[k]), (k, g[k], ref[k])
+    # a row range (two 128-row panels) matches the oracle's same range
+    g2 = ctx.evaluate(128, 384)
+    ref2 = oracle.evaluate(o.x, o.S, fp, 128, 384)
+    assert g2["pairs"] == ref2["pairs"]
+    assert abs(g2["mrc_mae"] - ref2["mrc_mae"]) <= 2e-6 + 1e-5 * abs(ref2["mrc_mae"])
