@@ -73,6 +73,7 @@ class Context {
     check(refsig_gpu_load_corpus(ctx_, tokens.data(), doc_off.data(), static_cast<std::uint32_t>(doc_off.size() - 1),
                                  vocab));
     n_docs_ = static_cast<std::uint32_t>(doc_off.size() - 1);
+    vocab_ = vocab;
   }
   void count(Weighting w = Weighting::tfidf) { check(refsig_gpu_count(ctx_, static_cast<int>(w))); }
 
@@ -86,6 +87,13 @@ class Context {
     m.counts.resize(nnz);
     check(refsig_gpu_get_counts(ctx_, m.rowptr.data(), m.ids.data(), m.counts.data(), nnz, &nnz));
     return m;
+  }
+
+  // FrequencyTable corpus_freq per term id; doc_freq via refsig_gpu_get_df.
+  std::vector<std::uint64_t> corpus_freq() {
+    std::vector<std::uint64_t> cf(vocab_);
+    check(refsig_gpu_get_corpus_freq(ctx_, cf.data()));
+    return cf;
   }
 
   void set_reference_docs(const std::vector<std::uint32_t>& doc_ids) {
@@ -111,6 +119,13 @@ class Context {
     std::vector<float> S(static_cast<size_t>(n_docs_hint()) * K_);
     check(refsig_gpu_get_signatures(ctx_, S.data()));
     return S;
+  }
+
+  // One MRCS signature file image per document, 20 + 8K bytes each, back to back.
+  std::vector<std::uint8_t> signature_records(std::uint64_t ref_id) {
+    std::vector<std::uint8_t> r(static_cast<size_t>(n_docs_hint()) * (20u + 8u * K_));
+    check(refsig_gpu_get_signature_records(ctx_, ref_id, r.data(), r.size()));
+    return r;
   }
 
   std::vector<PairKey> mrc_pairs(float tau) {
@@ -148,6 +163,7 @@ class Context {
     check(refsig_gpu_load_text(ctx_, reinterpret_cast<const std::uint8_t*>(text.data()), byte_off.data(),
                                static_cast<std::uint32_t>(byte_off.size() - 1)));
     n_docs_ = static_cast<std::uint32_t>(byte_off.size() - 1);
+    vocab_ = 17576;
   }
 
   // simhash(extract_words(normalize(doc))) per document (simhash.hpp:35-45).
@@ -198,6 +214,7 @@ class Context {
   refsig_gpu_ctx* ctx_ = nullptr;
   std::uint32_t K_ = 0;
   std::uint32_t n_docs_ = 0;
+  std::uint32_t vocab_ = 0;
 };
 
 }  // namespace refsig::gpu

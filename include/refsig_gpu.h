@@ -107,6 +107,9 @@ int refsig_gpu_get_counts(refsig_gpu_ctx* ctx, uint64_t* rowptr, uint32_t* ids, 
                           uint64_t* nnz);
 /* df[vocab] and idf32[vocab] (either may be NULL). */
 int refsig_gpu_get_df(refsig_gpu_ctx* ctx, uint32_t* df, float* idf32);
+/* cf[vocab]: total occurrences of each term over the corpus (the corpus_freq
+ * column of SPEC.md's FrequencyTable, build_frequency_table SPEC.md:214-222). */
+int refsig_gpu_get_corpus_freq(refsig_gpu_ctx* ctx, uint64_t* cf);
 /* 1/||w_d|| per doc (0 for an empty doc). */
 int refsig_gpu_get_inv_norm(refsig_gpu_ctx* ctx, float* inv_norm);
 
@@ -126,6 +129,12 @@ int refsig_gpu_reference_union(refsig_gpu_ctx* ctx, uint32_t* out_u);
 int refsig_gpu_sign(refsig_gpu_ctx* ctx);
 /* S[n_docs*K] row-major: S[d*K+k] = cosine(doc d, reference k). */
 int refsig_gpu_get_signatures(refsig_gpu_ctx* ctx, float* S);
+
+/* f4: one MRCS signature file image per document: magic "MRCS",
+ * u32 version 1, u32 P=K, u64 ref_id, K float64 (exact widening of the fp32
+ * signatures), little-endian, 20 + 8K bytes each, records back to back in
+ * document order. out_bytes >= n_docs * (20 + 8K). */
+int refsig_gpu_get_signature_records(refsig_gpu_ctx* ctx, uint64_t ref_id, uint8_t* out, uint64_t out_bytes);
 
 /* ---- K3: MRC all-pairs (A7) -------------------------------------------------
  * All i<j with compare(S_i,S_j) >= tau. out_pairs: host buffer of `capacity`

@@ -93,6 +93,8 @@ SIGNATURES = {
                                        _c.c_int),
     "refsig_gpu_get_pairs": ([_c.c_void_p, _P(_c.c_uint64), _c.c_uint64], _c.c_int),
     "refsig_gpu_evaluate": ([_c.c_void_p, _c.c_uint32, _c.c_uint32, _c.c_void_p], _c.c_int),
+    "refsig_gpu_get_corpus_freq": ([_c.c_void_p, _P(_c.c_uint64)], _c.c_int),
+    "refsig_gpu_get_signature_records": ([_c.c_void_p, _c.c_uint64, _P(_c.c_uint8), _c.c_uint64], _c.c_int),
     "refsig_gpu_load_text": ([_c.c_void_p, _P(_c.c_uint8), _P(_c.c_uint64), _c.c_uint32], _c.c_int),
     "refsig_gpu_simhash_text": ([_c.c_void_p], _c.c_int),
     "refsig_gpu_get_pairs_csr": ([_c.c_void_p, _c.c_uint32, _c.c_uint32, _P(_c.c_uint64), _P(_c.c_uint32), _c.c_uint64,
@@ -233,6 +235,12 @@ class Context:
                                                   _ptr(cnt, ctypes.c_uint32), n, ctypes.byref(nnz)))
         return rowptr, ids[:n], cnt[:n]
 
+    def corpus_freq(self) -> np.ndarray:
+        """cf[vocab]: total occurrences of each term (SPEC FrequencyTable corpus_freq)."""
+        cf = np.empty(self.vocab, np.uint64)
+        self._check(self._L.refsig_gpu_get_corpus_freq(self._h, _ptr(cf, ctypes.c_uint64)))
+        return cf
+
     def df(self):
         d = np.empty(self.vocab, np.uint32)
         idf = np.empty(self.vocab, np.float32)
@@ -281,6 +289,14 @@ class Context:
         S = np.empty((self.n_docs, self.K), np.float32)
         self._check(self._L.refsig_gpu_get_signatures(self._h, _ptr(S, ctypes.c_float)))
         return S
+
+    def signature_records(self, ref_id: int) -> np.ndarray:
+        """uint8 [n_docs, 20 + 8K]: row d is the MRCS signature file of doc d
+        (SPEC.md:401), written on the device."""
+        rec = np.empty((self.n_docs, 20 + 8 * self.K), np.uint8)
+        self._check(self._L.refsig_gpu_get_signature_records(self._h, ctypes.c_uint64(ref_id),
+                                                             _ptr(rec, ctypes.c_uint8), rec.size))
+        return rec
 
     # -- pairs ----------------------------------------------------------------
     def _pairs(self, fn, arg, out, fetch):

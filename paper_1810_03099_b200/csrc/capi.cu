@@ -143,6 +143,8 @@ struct refsig_gpu_ctx {
   bool have_x = false;
   DevBuf x, post_off, post_fill, posts, head_col, headA, head_norm, tail_df;  // K5
   DevBuf headAT, eval_tail, eval_part;                                         // evaluation
+  DevBuf cf_rep, cf;                                                           // corpus frequencies
+  DevBuf records;                                                              // MRCS records
 
   // query mode
   refsig_gpu_ctx* db = nullptr;
@@ -782,6 +784,21 @@ int refsig_gpu_get_df(refsig_gpu_ctx* ctx, uint32_t* df, float* idf32) {
   });
 }
 
+int refsig_gpu_get_corpus_freq(refsig_gpu_ctx* ctx, uint64_t* cf) {
+  return guard(ctx, [&] {
+    require(ctx->counted, "count() not called");
+    require(cf != nullptr, "NULL output");
+    const uint32_t V = ctx->vocab;
+    const uint32_t reps = std::max<uint32_t>(1u, std::min<uint32_t>(8u, (1u << 20) / V));
+    ctx->cf_rep.ensure(sizeof(unsigned long long) * static_cast<size_t>(reps) * V);
+    ctx->cf.ensure(sizeof(uint64_t) * V);
+    launch_corpus_freq(ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->n_docs, V, reps,
+                       ctx->cf_rep.as<unsigned long long>(), ctx->cf.as<uint64_t>(), ctx->stream);
+    ck(cudaMemcpyAsync(cf, ctx->cf.p, 8ull * V, cudaMemcpyDeviceToHost, ctx->stream), "D2H cf");
+    sync(ctx);
+  });
+}
+
 int refsig_gpu_get_inv_norm(refsig_gpu_ctx* ctx, float* inv_norm) {
   return guard(ctx, [&] {
     require(ctx->counted, "count() not called");
@@ -909,6 +926,21 @@ int refsig_gpu_get_signatures(refsig_gpu_ctx* ctx, float* S) {
     ck(cudaMemcpyAsync(S, ctx->S.p, sizeof(float) * static_cast<size_t>(ctx->n_docs) * ctx->K,
                        cudaMemcpyDeviceToHost, ctx->stream),
        "D2H signatures");
+    sync(ctx);
+  });
+}
+
+int refsig_gpu_get_signature_records(refsig_gpu_ctx* ctx, uint64_t ref_id, uint8_t* out, uint64_t out_bytes) {
+  return guard(ctx, [&] {
+    require(ctx->signed_, "sign() not called");
+    require(out != nullptr, "NULL output");
+    const uint64_t bytes = static_cast<uint64_t>(ctx->n_docs) * (20ull + 8ull * ctx->K);
+    require(out_bytes >= bytes, "output buffer smaller than n_docs * (20 + 8K) bytes");
+    if (!bytes) return;
+    ctx->records.ensure(bytes);
+    launch_mrcs_records(ctx->S.as<float>(), ctx->n_docs, ctx->K, ref_id, ctx->records.as<uint32_t>(), ctx->stream);
+    launched("mrcs records");
+    ck(cudaMemcpyAsync(out, ctx->records.p, bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H records");
     sync(ctx);
   });
 }

@@ -375,6 +375,32 @@ __global__ void idf_kernel(const uint32_t* __restrict__ df_rep, uint32_t reps, u
   }
 }
 
+// corpus_freq (SPEC.md FrequencyTable): cf[t] += count of every (doc, t) row,
+// 64-bit atomics into R replicas (replica = warp index mod R: Zipf-head terms
+// are in every document), then summed by cf_sum_kernel. Integer sums: exact.
+__global__ void __launch_bounds__(256) cf_rows_kernel(const uint2* __restrict__ ent, const uint64_t* __restrict__ doc_off,
+                                                      const uint32_t* __restrict__ nnz, uint32_t n_docs, uint32_t vocab,
+                                                      uint32_t reps, unsigned long long* __restrict__ cf_rep) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t d = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (d >= n_docs) return;
+  unsigned long long* rep = cf_rep + static_cast<size_t>(d % reps) * vocab;
+  const uint2* e = ent + doc_off[d];
+  for (uint32_t i = lane; i < nnz[d]; i += 32) {
+    const uint2 x = e[i];
+    atomicAdd(rep + x.x, static_cast<unsigned long long>(x.y));
+  }
+}
+
+__global__ void cf_sum_kernel(const unsigned long long* __restrict__ cf_rep, uint32_t reps, uint32_t vocab,
+                              uint64_t* __restrict__ cf) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < vocab; t += gridDim.x * blockDim.x) {
+    unsigned long long c = 0;
+    for (uint32_t r = 0; r < reps; ++r) c += cf_rep[static_cast<size_t>(r) * vocab + t];
+    cf[t] = c;
+  }
+}
+
 // Warp per doc.
 __global__ void compact_csr_kernel(const uint2* __restrict__ ent, const uint64_t* __restrict__ doc_off,
                                    const uint32_t* __restrict__ nnz, const uint64_t* __restrict__ rowptr,
@@ -472,6 +498,17 @@ void launch_count_large(const CountArgs& a, const uint32_t* long_docs, const uin
 void launch_idf(const uint32_t* df_rep, uint32_t reps, uint32_t vocab, uint32_t n_docs, int weight_mode, uint32_t* df,
                 TermInfo* info, cudaStream_t s) {
   idf_kernel<<<grid_for((vocab + 255) / 256, 8), 256, 0, s>>>(df_rep, reps, vocab, n_docs, weight_mode, df, info);
+  note_launch();
+}
+
+void launch_corpus_freq(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, uint32_t n_docs,
+                        uint32_t vocab, uint32_t reps, unsigned long long* cf_rep, uint64_t* cf, cudaStream_t s) {
+  cudaMemsetAsync(cf_rep, 0, sizeof(unsigned long long) * static_cast<size_t>(reps) * vocab, s);
+  if (n_docs)
+    cf_rows_kernel<<<static_cast<unsigned>(ceil_div(n_docs, 8)), 256, 0, s>>>(ent, doc_off, nnz, n_docs, vocab, reps,
+                                                                             cf_rep);
+  cf_sum_kernel<<<grid_for((vocab + 255) / 256, 8), 256, 0, s>>>(cf_rep, reps, vocab, cf);
+  note_launch();
   note_launch();
 }
 

@@ -55,6 +55,12 @@ void launch_count_large(const CountArgs& a, const uint32_t* long_docs, const uin
 // raw-TF weighting); ref_row = -1.
 void launch_idf(const uint32_t* df_rep, uint32_t reps, uint32_t vocab, uint32_t n_docs, int weight_mode, uint32_t* df,
                 TermInfo* info, cudaStream_t s);
+// MRCS signature records, 20 + 8K bytes per doc, as 32-bit words.
+void launch_mrcs_records(const float* S, uint32_t n_docs, uint32_t K, uint64_t ref_id, uint32_t* out,
+                         cudaStream_t s);
+// cf[t] = sum of the counts of term t over all documents (exact, 64-bit).
+void launch_corpus_freq(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, uint32_t n_docs,
+                        uint32_t vocab, uint32_t reps, unsigned long long* cf_rep, uint64_t* cf, cudaStream_t s);
 // Compact padded CSR -> rowptr/ids/counts (rowptr from an exclusive scan of nnz).
 void launch_compact_csr(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const uint64_t* rowptr,
                         uint32_t n_docs, uint32_t* ids, uint32_t* counts, cudaStream_t s);

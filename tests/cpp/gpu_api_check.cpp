@@ -3,6 +3,7 @@
 // GPU box; exits non-zero on any mismatch.
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 
 #include "refsig/gpu.hpp"
@@ -62,6 +63,15 @@ int main() {
          t.counts[3] == 2);
   auto tf = ctx.simhash_text();  // one word "abcabc" vs two words "abc", "abc"
   EXPECT(tf.size() == 2 && tf[0] != 0 && tf[1] != 0);
+  auto cf = ctx.corpus_freq();  // abc x2 in each doc
+  EXPECT(cf.size() == 17576 && cf[28] == 4);
+  ctx.set_reference_partitions({{28}});
+  auto S1 = ctx.sign();
+  auto rec = ctx.signature_records(0x1234);  // MRCS, 28 bytes per doc
+  double v = 0;
+  std::memcpy(&v, rec.data() + 28 + 20, 8);
+  EXPECT(rec.size() == 56 && std::memcmp(rec.data(), "MRCS", 4) == 0 && rec[8] == 1 && rec[12] == 0x34 &&
+         v == static_cast<double>(S1[1]));
   std::printf("gpu_api_check OK\n");
   return 0;
 }
