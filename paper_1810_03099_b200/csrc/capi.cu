@@ -145,6 +145,7 @@ struct refsig_gpu_ctx {
   DevBuf headAT, eval_tail, eval_part;                                         // evaluation
   DevBuf cf_rep, cf;                                                           // corpus frequencies
   DevBuf records;                                                              // MRCS records
+  DevBuf tc_forms;                                                             // K3 tcgen05 operand forms
 
   // query mode
   refsig_gpu_ctx* db = nullptr;
@@ -379,6 +380,35 @@ void prepare_bitmap(refsig_gpu_ctx* c, const PairGrid& g, bool zero) {
     ck(cudaMemsetAsync(c->bitmap.p, 0, sizeof(uint32_t) * static_cast<size_t>(g.n_rows) * g.words_per_row,
                        c->stream),
        "memset bitmap");
+}
+
+// K3: the tcgen05 kernel when K fits (3K+3 <= 128), else the CUDA-core tiles.
+// REFSIG_K3=fp32 (or 1 = v1) forces the CUDA-core kernel.
+bool k3_use_tc(uint32_t K, float tau) {
+  static const bool off = [] {
+    const char* m = std::getenv("REFSIG_K3");
+    return m && (m[0] == '1' || std::strcmp(m, "fp32") == 0);
+  }();
+  return !off && mrc_tc_supported(K, tau);
+}
+
+void run_mrc_tiles(refsig_gpu_ctx* c, const float* STr, uint32_t ldr, uint32_t nr, const float* STc, uint32_t ldc,
+                   uint32_t ncl, bool self, uint32_t K, float tau, const PairGrid& g) {
+  if (!k3_use_tc(K, tau)) {
+    launch_mrc_bitmap(STr, ldr, STc, ldc, K, tau, g, c->bitmap.as<uint32_t>(), c->rowcnt.as<uint32_t>(), c->stream);
+    return;
+  }
+  const size_t rb = mrc_tc_form_bytes(K, nr), cb = mrc_tc_form_bytes(K, ncl);
+  c->tc_forms.ensure(rb + cb);
+  char* rowf = c->tc_forms.as<char>();
+  char* colf = rowf + rb;
+  if (self) {
+    launch_mrc_tc_forms(STr, ldr, nr, K, tau, rowf, colf, c->stream);
+  } else {
+    launch_mrc_tc_forms(STr, ldr, nr, K, tau, rowf, nullptr, c->stream);
+    launch_mrc_tc_forms(STc, ldc, ncl, K, tau, nullptr, colf, c->stream);
+  }
+  launch_mrc_tc(rowf, colf, K, g, c->bitmap.as<uint32_t>(), c->rowcnt.as<uint32_t>(), c->stream);
 }
 
 // A5: union, remap and the compact table from c->ref_{start,n} and `ent`.
@@ -957,8 +987,8 @@ int refsig_gpu_mrc_pairs(refsig_gpu_ctx* ctx, float tau, uint64_t* out_pairs, ui
     {
       Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
       prepare_bitmap(ctx, g, false);
-      launch_mrc_bitmap(ctx->ST.as<float>(), ctx->ld, ctx->ST.as<float>(), ctx->ld, ctx->K, tau, g, ctx->bitmap.as<uint32_t>(),
-                        ctx->rowcnt.as<uint32_t>(), ctx->stream);
+      run_mrc_tiles(ctx, ctx->ST.as<float>(), ctx->ld, ctx->n_docs, ctx->ST.as<float>(), ctx->ld, ctx->n_docs, true,
+                    ctx->K, tau, g);
       launched("mrc bitmap");
     }
     rc2 = run_emit(ctx, g, out_pairs, capacity, out_count);
@@ -1213,8 +1243,8 @@ int refsig_gpu_mrc_query_pairs(refsig_gpu_ctx* q, float tau, uint64_t* out_pairs
     {
       Phase ph_tiles(q, REFSIG_PHASE_PAIR_TILES);
       prepare_bitmap(q, g, false);
-      launch_mrc_bitmap(q->ST.as<float>(), q->ld, db->ST.as<float>(), db->ld, q->K, tau, g, q->bitmap.as<uint32_t>(),
-                        q->rowcnt.as<uint32_t>(), q->stream);
+      run_mrc_tiles(q, q->ST.as<float>(), q->ld, q->n_docs, db->ST.as<float>(), db->ld, db->n_docs, false, q->K, tau,
+                    g);
       launched("mrc query bitmap");
     }
     rc2 = run_emit(q, g, out_pairs, capacity, out_count);
@@ -1263,8 +1293,8 @@ int refsig_gpu_mrc_pairs_rows(refsig_gpu_ctx* ctx, float tau, uint32_t row_lo, u
     {
       Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
       prepare_bitmap(ctx, g, false);
-      launch_mrc_bitmap(ctx->ST.as<float>(), ctx->ld, ctx->ST.as<float>(), ctx->ld, ctx->K, tau, g, ctx->bitmap.as<uint32_t>(),
-                        ctx->rowcnt.as<uint32_t>(), ctx->stream);
+      run_mrc_tiles(ctx, ctx->ST.as<float>(), ctx->ld, ctx->n_docs, ctx->ST.as<float>(), ctx->ld, ctx->n_docs, true,
+                    ctx->K, tau, g);
       launched("mrc bitmap");
     }
     rc2 = run_emit(ctx, g, out_pairs, capacity, out_count);
@@ -1285,8 +1315,8 @@ static void enqueue_step(refsig_gpu_ctx* ctx, int weight_mode, const uint32_t* r
   {
     Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
     prepare_bitmap(ctx, g, false);
-    launch_mrc_bitmap(ctx->ST.as<float>(), ctx->ld, ctx->ST.as<float>(), ctx->ld, ctx->K, tau, g,
-                      ctx->bitmap.as<uint32_t>(), ctx->rowcnt.as<uint32_t>(), ctx->stream);
+    run_mrc_tiles(ctx, ctx->ST.as<float>(), ctx->ld, ctx->n_docs, ctx->ST.as<float>(), ctx->ld, ctx->n_docs, true,
+                  ctx->K, tau, g);
     launched("mrc bitmap");
   }
   enqueue_emit(ctx, g);

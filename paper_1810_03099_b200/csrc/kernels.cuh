@@ -134,6 +134,15 @@ struct PairGrid {
 };
 void launch_mrc_bitmap(const float* ST_rows, uint32_t ld_rows, const float* ST_cols, uint32_t ld_cols, uint32_t K,
                        float tau, const PairGrid& g, uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s);
+// K3 on tcgen05 (k3_tc.cu): split-fp16 operand forms of the unit signatures,
+// then the tile kernel writing the same bitmap + row counts as launch_mrc_bitmap.
+uint32_t mrc_tc_kp(uint32_t K);
+bool mrc_tc_supported(uint32_t K, float tau);
+size_t mrc_tc_form_bytes(uint32_t K, uint32_t n_docs);
+void launch_mrc_tc_forms(const float* ST, uint32_t ld, uint32_t n_docs, uint32_t K, float tau, void* rowf, void* colf,
+                         cudaStream_t s);
+void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
+                   uint32_t* rowcnt, cudaStream_t s);
 void launch_hamming_bitmap(const uint64_t* f_rows, const uint64_t* f_cols, int max_dist, const PairGrid& g,
                            uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s);
 // keys[k] = (i<<32) | cols[k] for rows [row_begin, row_end) (CSR -> sorted keys).
