@@ -36,12 +36,19 @@
 
 #include <cuda_fp16.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace refsig_gpu {
 namespace {
 
-constexpr uint32_t kTcThreads = 320;
+constexpr uint32_t kTcThreads = 608;  // producer warp, 2 MMA warps, 16 epilogue warps
+__device__ long long g_tc_trace[12][64];  // REFSIG_TC_DEBUG & 8: CTA 0 event clocks per tile
+__device__ __forceinline__ void tc_trace(const uint32_t dbg, int ev, uint32_t it) {
+  if ((dbg & 8) && blockIdx.x == ((dbg & 16) ? gridDim.x - 1 : 0) && it < 64) g_tc_trace[ev][it] = clock64();
+}
 constexpr uint32_t kTcMaxKP = 128;  // 3K + 3 <= 128  <=>  K <= 41
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -89,6 +96,29 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b,
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
 }
+// Warp-converged variants: every lane evaluates the (uniform) operands, the
+// elected lane issues; keeps descriptors in uniform registers (no per-lane
+// R2UR waterfall around each instruction).
+__device__ __forceinline__ uint32_t elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+  return pred;
+}
+__device__ __forceinline__ void mma_f16_e(uint32_t e, uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate), "r"(e));
+}
+__device__ __forceinline__ void mma_commit_e(uint32_t e, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(e)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -121,53 +151,69 @@ struct TcArgs {
   const __half* Bc;  // column-form panels
   uint32_t KP;       // K' (multiple of 16)
   PairGrid g;
-  uint32_t nbc;          // 128-column blocks
-  uint32_t rb0, rb1;     // row blocks [rb0, rb1)
+  uint32_t nbr, nbc;     // 128-row / 128-column blocks
+  uint32_t rb0, rb1;     // row blocks [rb0, rb1) of this call
   uint64_t n_tiles;
   uint32_t stages;
   uint32_t* bitmap;
   uint32_t* rowcnt;
+  uint32_t dbg;  // timing experiments only (REFSIG_TC_DEBUG): 1 no epilogue math, 2 no B refill, 4 no MMA
 };
 
-// Column tiles (256 wide) of row block r, and the first column block.
-__device__ __forceinline__ uint32_t tc_ct(const TcArgs& a, uint32_t r) {
-  return a.g.triangle ? (a.nbc - r + 1) / 2 : (a.nbc + 1) / 2;
-}
-__device__ __forceinline__ uint32_t tc_cs(const TcArgs& a, uint32_t r) { return a.g.triangle ? r : 0u; }
+// Row group p = row blocks rb0 + 2p, +1 (A resident in smem while the CTA
+// walks the group's column blocks). Column blocks of group p: from its first
+// row block on the triangle, all of them for a rectangle.
+__device__ __forceinline__ uint32_t tc_r0(const TcArgs& a, uint32_t p) { return a.rb0 + 2 * p; }
+__device__ __forceinline__ uint32_t tc_cs(const TcArgs& a, uint32_t p) { return a.g.triangle ? tc_r0(a, p) : 0u; }
+__device__ __forceinline__ uint32_t tc_ct(const TcArgs& a, uint32_t p) { return a.nbc - tc_cs(a, p); }
+// row block r0 + h exists in this call
+__device__ __forceinline__ bool tc_rvalid(const TcArgs& a, uint32_t p, uint32_t h) { return tc_r0(a, p) + h < a.rb1; }
 
 struct TileWalk {
-  uint32_t r, c;
+  uint32_t p, c;
   __device__ void start(const TcArgs& a, uint64_t t) {
-    r = a.rb0;
-    while (t >= tc_ct(a, r)) {
-      t -= tc_ct(a, r);
-      ++r;
+    p = 0;
+    while (t >= tc_ct(a, p)) {
+      t -= tc_ct(a, p);
+      ++p;
     }
     c = static_cast<uint32_t>(t);
   }
-  __device__ void next(const TcArgs& a) {
-    if (++c == tc_ct(a, r)) {
+  // returns true when the next tile starts a new row group
+  __device__ bool next(const TcArgs& a) {
+    if (++c == tc_ct(a, p)) {
       c = 0;
-      ++r;
+      ++p;
+      return true;
     }
+    return false;
   }
 };
 
+// Tile = 256 rows (row group: two 128-row blocks, A panels resident and
+// double-buffered per group) x 128 columns (one B panel streamed per tile
+// through an S-stage ring). Per K step: one N=128 MMA per valid row block.
+template <uint32_t KS>
 __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t tsm[];
-  __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], tfull_bar[2], tempty_bar[2];
+  __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], afull_bar[2], aempty_bar[2], tfull_bar[2],
+      tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t t0 = a.n_tiles * blockIdx.x / gridDim.x, t1 = a.n_tiles * (blockIdx.x + 1) / gridDim.x;
   const uint32_t n_it = static_cast<uint32_t>(t1 - t0);
   const uint32_t PB = 256u * a.KP;  // bytes per operand panel
   const uint32_t S = a.stages;
+  uint8_t* sAbase = tsm;               // 2 buffers x 2 panels
+  uint8_t* sBbase = tsm + 4 * PB;      // S stages x 1 panel
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < S; ++s) {
       mb_init(&full_bar[s], 1);
       mb_init(&empty_bar[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
+      mb_init(&afull_bar[s], 1);
+      mb_init(&aempty_bar[s], 2);
       mb_init(&tfull_bar[s], 1);
       mb_init(&tempty_bar[s], 8);
     }
@@ -184,97 +230,162 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
   const uint32_t tmem = tmem_base_sh;
 
   if (warp == 0) {
-    if (lane == 0) {  // producer: A panel + one or two B panels per tile
+    if (lane == 0 && n_it) {  // producer
       TileWalk w;
       w.start(a, t0);
+      uint32_t g = 0;  // row groups started by this CTA
+      bool new_group = true;
       for (uint32_t it = 0; it < n_it; ++it) {
+        if (new_group) {  // A panels of the group into buffer g & 1
+          const uint32_t ab = g & 1;
+          if (g >= 2) mb_wait(&aempty_bar[ab], ((g >> 1) - 1) & 1u);
+          const uint32_t np = tc_rvalid(a, w.p, 1) ? 2u : 1u;
+          mb_expect_tx(&afull_bar[ab], np * PB);
+          bulk_g2s(sAbase + ab * 2 * PB, reinterpret_cast<const uint8_t*>(a.Ar) + static_cast<size_t>(tc_r0(a, w.p)) * PB,
+                   np * PB, &afull_bar[ab]);
+          ++g;
+        }
         const uint32_t st = it % S;
         if (it >= S) mb_wait(&empty_bar[st], ((it / S) - 1) & 1u);
-        const uint32_t bj = tc_cs(a, w.r) + 2 * w.c;
-        const uint32_t nb = bj + 1 < a.nbc ? 2u : 1u;
-        uint8_t* sA = tsm + static_cast<size_t>(st) * 3 * PB;
-        mb_expect_tx(&full_bar[st], PB * (1 + nb));
-        bulk_g2s(sA, reinterpret_cast<const uint8_t*>(a.Ar) + static_cast<size_t>(w.r) * PB, PB, &full_bar[st]);
-        bulk_g2s(sA + PB, reinterpret_cast<const uint8_t*>(a.Bc) + static_cast<size_t>(bj) * PB, nb * PB,
-                 &full_bar[st]);
-        w.next(a);
+        const uint32_t bj = tc_cs(a, w.p) + w.c;
+        if ((a.dbg & 2) && it >= S) {
+          mb_arrive(&full_bar[st]);
+        } else {
+          mb_expect_tx(&full_bar[st], PB);
+          bulk_g2s(sBbase + static_cast<size_t>(st) * PB,
+                   reinterpret_cast<const uint8_t*>(a.Bc) + static_cast<size_t>(bj) * PB, PB, &full_bar[st]);
+        }
+        new_group = w.next(a);
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
-    if (lane == 0) {  // MMA issuer
+  } else if (warp == 1 || warp == 2) {
+    // MMA issuers: warp 1 + m issues the tiles with it % 2 == m into
+    // accumulator m (two threads in flight hide each one's issue latency);
+    // whole warp converged, one elected lane issues
+    const uint32_t m = warp - 1;
+    if (n_it) {
       TileWalk w;
       w.start(a, t0);
-      const uint32_t ksteps = a.KP / 16;
+      const uint64_t dA0 = smem_desc(smem_u32(sAbase)), dB0 = smem_desc(smem_u32(sBbase));
+      const uint64_t dPB = PB >> 4;
+      uint32_t g = 0;
+      bool new_group = true;
       for (uint32_t it = 0; it < n_it; ++it) {
+        const uint32_t ab = (g - (new_group ? 0u : 1u)) & 1u;
+        if (new_group) {
+          mb_wait(&afull_bar[g & 1], (g >> 1) & 1u);
+          ++g;
+        }
         const uint32_t st = it % S, acc = it & 1;
-        const uint32_t bj = tc_cs(a, w.r) + 2 * w.c;
-        const uint32_t nb = bj + 1 < a.nbc ? 2u : 1u;
-        mb_wait(&full_bar[st], (it / S) & 1u);
-        if (it >= 2) mb_wait(&tempty_bar[acc], ((it >> 1) - 1) & 1u);
-        tc_fence_after();
-        const uint32_t sA = smem_u32(tsm + static_cast<size_t>(st) * 3 * PB);
-        for (uint32_t h = 0; h < nb; ++h)
-          for (uint32_t k = 0; k < ksteps; ++k)
-            mma_f16(tmem + acc * 256 + h * 128, smem_desc(sA + k * 4096), smem_desc(sA + (1 + h) * PB + k * 4096),
-                    k > 0);
-        mma_commit(&empty_bar[st]);
-        mma_commit(&tfull_bar[acc]);
-        w.next(a);
+        const bool mine = acc == m;
+        if (mine) {
+          const uint32_t bj = tc_cs(a, w.p) + w.c;
+          const uint32_t r0 = tc_r0(a, w.p);
+          const bool v1 = tc_rvalid(a, w.p, 1) && !(a.g.triangle && bj < r0 + 1);
+          if (lane == 0 && m == 0) tc_trace(a.dbg, 0, it);
+          mb_wait(&full_bar[st], (it / S) & 1u);
+          if (lane == 0 && m == 0) tc_trace(a.dbg, 1, it);
+          if (it >= 2) mb_wait(&tempty_bar[acc], ((it >> 1) - 1) & 1u);
+          if (lane == 0 && m == 0) tc_trace(a.dbg, 2, it);
+          tc_fence_after();
+          const uint64_t dA = dA0 + ab * 2 * dPB, dB = dB0 + st * dPB;
+          const uint32_t d0 = tmem + acc * 256;
+          const uint32_t e = elect_one();
+          if (!(a.dbg & 4)) {
+            mma_f16_e(e, d0, dA, dB, 0);
+#pragma unroll
+            for (uint32_t k = 1; k < KS; ++k) mma_f16_e(e, d0, dA + k * 256, dB + k * 256, 1);
+            if (v1) {
+              mma_f16_e(e, d0 + 128, dA + dPB, dB, 0);
+#pragma unroll
+              for (uint32_t k = 1; k < KS; ++k) mma_f16_e(e, d0 + 128, dA + dPB + k * 256, dB + k * 256, 1);
+            }
+          }
+          if (lane == 0 && m == 0) tc_trace(a.dbg, 3, it);
+          mma_commit_e(e, &empty_bar[st]);
+          mma_commit_e(e, &tfull_bar[acc]);
+        }
+        new_group = w.next(a);
+        // both issuers release the group's A buffer (a commit with nothing
+        // outstanding from this thread arrives at once)
+        if (new_group || it + 1 == n_it) mma_commit_e(elect_one(), &aempty_bar[ab]);
+        __syncwarp();
       }
     }
     __syncwarp();
-  } else {  // epilogue warps 2..9
-    const uint32_t q = warp & 3, h = (warp - 2) >> 2;
+  } else {  // epilogue warps 3..18: group eg = tiles with it % 2 == eg (accumulator eg),
+             // lane quarter q, row block h of the row group; all 128 columns in two halves
+    const uint32_t q = warp & 3, eg = (warp - 3) >> 3, h = ((warp - 3) >> 2) & 1;
     const uint32_t wpr = a.g.words_per_row;
     TileWalk w;
-    w.start(a, t0);
+    if (n_it) w.start(a, t0);
     uint32_t cnt = 0;
     for (uint32_t it = 0; it < n_it; ++it) {
       const uint32_t acc = it & 1;
-      const uint32_t r = w.r;
-      const uint32_t bj = tc_cs(a, r) + 2 * w.c + h;
-      mb_wait(&tfull_bar[acc], (it >> 1) & 1u);
-      tc_fence_after();
-      uint32_t v0[32], v1[32], v2[32], v3[32];
-      const bool valid = bj < a.nbc;
-      if (valid) {
-        const uint32_t ta = tmem + ((q * 32u) << 16) + acc * 256 + h * 128;
-        TC_LD32(ta, v0);
-        TC_LD32(ta + 32, v1);
-        TC_LD32(ta + 64, v2);
-        TC_LD32(ta + 96, v3);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mb_arrive(&tempty_bar[acc]);
-      if (valid) {
-        uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;  // bit c = sign(dot - tau) of column 32j + c
+      const uint32_t p = w.p;
+      const uint32_t r = tc_r0(a, p) + h;
+      const uint32_t bj = tc_cs(a, p) + w.c;
+      const uint32_t i = r * 128 + q * 32 + lane;
+      if (acc == eg) {
+        const uint32_t u = it >> 1;  // this group's use count of its accumulator
+        if (warp == 3 && lane == 0) tc_trace(a.dbg, 4, it);
+        mb_wait(&tfull_bar[acc], u & 1u);
+        if (warp == 3 && lane == 0) tc_trace(a.dbg, 5, it);
+        tc_fence_after();
+        const bool valid = tc_rvalid(a, p, h) && !(a.g.triangle && bj < r);
+        const bool edge = (a.g.triangle && bj == r) || bj + 1 == a.nbc;
+        uint32_t mw[4];
 #pragma unroll
-        for (int c = 31; c >= 0; --c) {
-          m0 = __funnelshift_l(v0[c], m0, 1);
-          m1 = __funnelshift_l(v1[c], m1, 1);
-          m2 = __funnelshift_l(v2[c], m2, 1);
-          m3 = __funnelshift_l(v3[c], m3, 1);
+        for (int half = 0; half < 2; ++half) {
+          uint32_t v0[32], v1[32];
+          if (valid) {
+            const uint32_t ta = tmem + ((q * 32u) << 16) + acc * 256 + h * 128 + half * 64;
+            TC_LD32(ta, v0);
+            TC_LD32(ta + 32, v1);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          }
+          if (warp == 3 && lane == 0) tc_trace(a.dbg, 8 + 2 * half, it);
+          if (half == 1) {  // accumulator fully read: hand it back to the MMA issuer
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mb_arrive(&tempty_bar[acc]);
+            if (warp == 3 && lane == 0) tc_trace(a.dbg, 6, it);
+          }
+          if (valid && !(a.dbg & 1)) {
+            // bit c = sign(dot - tau) of column c: eight independent 8-deep
+            // funnel chains (one per byte), then bytes -> words with PRMT
+            uint32_t b[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) b[k] = 0;
+#pragma unroll
+            for (int c = 7; c >= 0; --c) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                b[k] = __funnelshift_l(v0[8 * k + c], b[k], 1);
+                b[4 + k] = __funnelshift_l(v1[8 * k + c], b[4 + k], 1);
+              }
+            }
+            mw[2 * half] = ~__byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+            mw[2 * half + 1] = ~__byte_perm(__byte_perm(b[4], b[5], 0x0040), __byte_perm(b[6], b[7], 0x0040), 0x5410);
+          }
+          if (warp == 3 && lane == 0) tc_trace(a.dbg, 9 + 2 * half, it);
         }
-        m0 = ~m0, m1 = ~m1, m2 = ~m2, m3 = ~m3;
-        const uint32_t i = r * 128 + q * 32 + lane;
-        if ((a.g.triangle && bj == r) || bj + 1 == a.nbc) {
-          const uint32_t c0 = bj * 128;
-          m0 &= tc_col_mask(c0, i, a.g);
-          m1 &= tc_col_mask(c0 + 32, i, a.g);
-          m2 &= tc_col_mask(c0 + 64, i, a.g);
-          m3 &= tc_col_mask(c0 + 96, i, a.g);
+        if (valid && !(a.dbg & 1)) {
+          if (edge) {
+            const uint32_t c0 = bj * 128;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) mw[k] &= tc_col_mask(c0 + 32 * k, i, a.g);
+          }
+          if (i < a.g.n_rows) {
+            *reinterpret_cast<uint4*>(a.bitmap + static_cast<size_t>(i) * wpr + bj * 4) =
+                make_uint4(mw[0], mw[1], mw[2], mw[3]);
+            cnt += __popc(mw[0]) + __popc(mw[1]) + __popc(mw[2]) + __popc(mw[3]);
+          }
         }
-        if (i < a.g.n_rows) {
-          *reinterpret_cast<uint4*>(a.bitmap + static_cast<size_t>(i) * wpr + bj * 4) = make_uint4(m0, m1, m2, m3);
-          cnt += __popc(m0) + __popc(m1) + __popc(m2) + __popc(m3);
-        }
+        if (warp == 3 && lane == 0) tc_trace(a.dbg, 7, it);
       }
-      w.next(a);
-      if (w.r != r || it + 1 == n_it) {
-        const uint32_t i = r * 128 + q * 32 + lane;
+      if (w.next(a) || it + 1 == n_it) {
         if (cnt && i < a.g.n_rows) atomicAdd(a.rowcnt + i, cnt);
         cnt = 0;
       }
@@ -289,51 +400,69 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
 }
 
 // Row form [hi | hi | lo | -tau pieces] or column form [hi | lo | hi | 1 1 1]
-// of every document, panel layout (see the top comment). Thread per (doc, K
-// chunk of 8); consecutive threads = consecutive docs: reads of ST[k][d] and
-// 16-byte writes are both coalesced.
+// of every document, panel layout (see the top comment). CTA per 128-doc
+// panel: threads convert ST[k][d] (coalesced along d) once into both forms
+// in shared memory ([doc][K'] halves, row stride padded by 8 halves), then
+// write each panel as 16-byte chunks in [chunk][doc] order (coalesced).
 __global__ void __launch_bounds__(256) tc_forms_kernel(const float* __restrict__ ST, uint32_t ld, uint32_t n_docs,
-                                                       uint32_t K, uint32_t KP, uint32_t n_pan, float tau,
-                                                       __half* __restrict__ rowf, __half* __restrict__ colf) {
-  const uint32_t chunks = KP / 8;
-  const uint64_t total = static_cast<uint64_t>(n_pan) * 128 * chunks;
-  // tau = t0 + t1 + t2 in fp16 pieces (exact for any fp32 tau in fp16 range)
+                                                       uint32_t K, uint32_t KP, float tau, __half* __restrict__ rowf,
+                                                       __half* __restrict__ colf) {
+  extern __shared__ __align__(16) __half fsm[];
+  const uint32_t stride = KP + 8;  // halves per doc row (16-byte aligned, staggers banks)
+  __half* R = fsm;
+  __half* C = fsm + 128 * stride;
+  const uint32_t pan = blockIdx.x, d0 = pan * 128;
   const __half t0 = __float2half_rn(tau);
   const float r1 = tau - __half2float(t0);
   const __half t1 = __float2half_rn(r1);
   const __half t2 = __float2half_rn(r1 - __half2float(t1));
   const __half one = __float2half_rn(1.0f), zero = __float2half_rn(0.0f);
-  for (uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t dl = static_cast<uint32_t>(idx % 128);
-    const uint64_t pc = idx / 128;
-    const uint32_t kc = static_cast<uint32_t>(pc % chunks), pan = static_cast<uint32_t>(pc / chunks);
-    const uint32_t d = pan * 128 + dl;
-    __align__(16) __half rv[8], cv[8];
+  {
+    // thread (dl, k0): values k0, k0 + 2, ... of doc d0 + dl; all loads issued before any use
+    constexpr uint32_t kPer = (kTcMaxKP / 3 + 1) / 2 + 1;  // ceil(41 / 2)
+    const uint32_t dl = threadIdx.x & 127, k0 = threadIdx.x >> 7, d = d0 + dl;
+    float v[kPer];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const uint32_t p = kc * 8 + e;
-      __half rr = zero, cc = zero;
-      if (p < 3 * K) {
-        const uint32_t seg = p / K, k = p - seg * K;
-        const float v = d < n_docs ? ST[static_cast<size_t>(k) * ld + d] : 0.0f;
-        const __half hi = __float2half_rn(v);
-        const __half lo = __float2half_rn(v - __half2float(hi));
-        rr = seg == 2 ? lo : hi;
-        cc = seg == 1 ? lo : hi;
-      } else if (p < 3 * K + 3) {
-        const uint32_t j = p - 3 * K;
-        const __half tj = j == 0 ? t0 : (j == 1 ? t1 : t2);
-        rr = __hneg(tj);
-        if (__half2float(tj) == 0.0f) rr = zero;  // +0, never -0: tau = 0 keeps dot = 0 a match
-        cc = one;
-      }
-      rv[e] = rr;
-      cv[e] = cc;
+    for (uint32_t u = 0; u < kPer; ++u) {
+      const uint32_t k = k0 + 2 * u;
+      v[u] = (k < K && d < n_docs) ? ST[static_cast<size_t>(k) * ld + d] : 0.0f;
     }
-    const size_t off = ((static_cast<size_t>(pan) * chunks + kc) * 128 + dl) * 8;
-    if (rowf) *reinterpret_cast<uint4*>(rowf + off) = *reinterpret_cast<const uint4*>(rv);
-    if (colf) *reinterpret_cast<uint4*>(colf + off) = *reinterpret_cast<const uint4*>(cv);
+    __half* rr = R + dl * stride;
+    __half* cc = C + dl * stride;
+#pragma unroll
+    for (uint32_t u = 0; u < kPer; ++u) {
+      const uint32_t k = k0 + 2 * u;
+      if (k < K) {
+        const __half hi = __float2half_rn(v[u]);
+        const __half lo = __float2half_rn(v[u] - __half2float(hi));
+        rr[k] = hi;
+        rr[K + k] = hi;
+        rr[2 * K + k] = lo;
+        cc[k] = hi;
+        cc[K + k] = lo;
+        cc[2 * K + k] = hi;
+      }
+    }
+  }
+  for (uint32_t idx = threadIdx.x; idx < (KP - 3 * K) * 128; idx += blockDim.x) {
+    const uint32_t j = idx >> 7, dl = idx & 127, p = 3 * K + j;
+    __half rv = zero, cv = zero;
+    if (j < 3) {
+      const __half tj = j == 0 ? t0 : (j == 1 ? t1 : t2);
+      rv = __half2float(tj) == 0.0f ? zero : __hneg(tj);  // +0, never -0: tau = 0 keeps dot = 0 a match
+      cv = one;
+    }
+    R[dl * stride + p] = rv;
+    C[dl * stride + p] = cv;
+  }
+  __syncthreads();
+  const uint32_t chunks = KP / 8;
+  const size_t base = static_cast<size_t>(pan) * chunks * 128 * 8;
+  for (uint32_t idx = threadIdx.x; idx < chunks * 128; idx += blockDim.x) {
+    const uint32_t kc = idx >> 7, dl = idx & 127;
+    const size_t off = base + (static_cast<size_t>(kc) * 128 + dl) * 8;
+    if (rowf) *reinterpret_cast<uint4*>(rowf + off) = *reinterpret_cast<const uint4*>(R + dl * stride + kc * 8);
+    if (colf) *reinterpret_cast<uint4*>(colf + off) = *reinterpret_cast<const uint4*>(C + dl * stride + kc * 8);
   }
 }
 
@@ -357,46 +486,96 @@ void launch_mrc_tc_forms(const float* ST, uint32_t ld, uint32_t n_docs, uint32_t
                          cudaStream_t s) {
   const uint32_t KP = mrc_tc_kp(K);
   const uint32_t n_pan = static_cast<uint32_t>(ceil_div(n_docs, 128));
-  const uint64_t total = static_cast<uint64_t>(n_pan) * 128 * (KP / 8);
-  if (!total) return;
-  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 8));
-  tc_forms_kernel<<<blocks, 256, 0, s>>>(ST, ld, n_docs, K, KP, n_pan, tau, static_cast<__half*>(rowf),
-                                         static_cast<__half*>(colf));
+  if (!n_pan) return;
+  const size_t smem = 2ull * 128 * (KP + 8) * sizeof(__half);  // <= 69.6 KB at K' = 128
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(tc_forms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024);
+    configured = true;
+  }
+  tc_forms_kernel<<<n_pan, 256, smem, s>>>(ST, ld, n_docs, K, KP, tau, static_cast<__half*>(rowf),
+                                           static_cast<__half*>(colf));
   note_launch();
 }
 
-void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGrid& g_in, uint32_t* bitmap,
+void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
                    uint32_t* rowcnt, cudaStream_t s) {
-  PairGrid g = g_in;
   TcArgs a{};
   a.Ar = static_cast<const __half*>(rowf);
   a.Bc = static_cast<const __half*>(colf);
   a.KP = mrc_tc_kp(K);
   a.g = g;
+  a.nbr = static_cast<uint32_t>(ceil_div(g.n_rows, 128));
   a.nbc = static_cast<uint32_t>(ceil_div(g.n_cols, 128));
   a.rb0 = g.row_begin / 128;
   a.rb1 = static_cast<uint32_t>(ceil_div(g.row_end, 128));
+  if (a.rb1 > a.nbr) a.rb1 = a.nbr;
   if (g.row_end <= g.row_begin || a.rb1 <= a.rb0 || a.nbc == 0) return;
   uint64_t T = 0;
-  for (uint32_t r = a.rb0; r < a.rb1; ++r) T += g.triangle ? (a.nbc - r + 1) / 2 : (a.nbc + 1) / 2;
+  for (uint32_t r0 = a.rb0; r0 < a.rb1; r0 += 2) T += a.nbc - (g.triangle ? r0 : 0u);
   if (T == 0) return;
   a.n_tiles = T;
   a.bitmap = bitmap;
   a.rowcnt = rowcnt;
-  const uint32_t stage_bytes = 3u * 256u * a.KP;
-  a.stages = std::max<uint32_t>(2u, std::min<uint32_t>(8u, (200u * 1024u) / stage_bytes));
+  static const uint32_t dbg = [] {
+    const char* m = std::getenv("REFSIG_TC_DEBUG");
+    return m ? static_cast<uint32_t>(std::atoi(m)) : 0u;
+  }();
+  a.dbg = dbg;
+  const uint32_t PB = 256u * a.KP;
+  // 2 x 2 resident A panels + S streamed B panels within ~200 KB
+  a.stages = std::max<uint32_t>(2u, std::min<uint32_t>(8u, (200u * 1024u - 4u * PB) / PB));
   // at least ~116 KB so that exactly one CTA (the TMEM owner of all 512 columns) fits per SM
-  const size_t smem = std::max<size_t>(static_cast<size_t>(a.stages) * stage_bytes, 116u * 1024u);
+  const size_t smem = std::max<size_t>(static_cast<size_t>(4 + a.stages) * PB, 116u * 1024u);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(mrc_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(mrc_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(mrc_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(mrc_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(mrc_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(mrc_tc_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(mrc_tc_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(mrc_tc_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(mrc_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(T, static_cast<uint64_t>(sms)));
-  mrc_tc_kernel<<<grid, kTcThreads, smem, s>>>(a);
+  if (dbg & 8) {
+    static bool dumped = false;
+    if (dumped) {
+    } else {
+      dumped = true;
+      long long z[12][64] = {};
+      cudaMemcpyToSymbolAsync(g_tc_trace, z, sizeof(z), 0, cudaMemcpyHostToDevice, s);
+    }
+  }
+  switch (a.KP / 16) {
+    case 1: mrc_tc_kernel<1><<<grid, kTcThreads, smem, s>>>(a); break;
+    case 2: mrc_tc_kernel<2><<<grid, kTcThreads, smem, s>>>(a); break;
+    case 3: mrc_tc_kernel<3><<<grid, kTcThreads, smem, s>>>(a); break;
+    case 4: mrc_tc_kernel<4><<<grid, kTcThreads, smem, s>>>(a); break;
+    case 5: mrc_tc_kernel<5><<<grid, kTcThreads, smem, s>>>(a); break;
+    case 6: mrc_tc_kernel<6><<<grid, kTcThreads, smem, s>>>(a); break;
+    case 7: mrc_tc_kernel<7><<<grid, kTcThreads, smem, s>>>(a); break;
+    default: mrc_tc_kernel<8><<<grid, kTcThreads, smem, s>>>(a); break;
+  }
+  if (dbg & 8) {
+    static int calls = 0;
+    if (++calls == 3) {
+      long long z[12][64];
+      cudaStreamSynchronize(s);
+      cudaMemcpyFromSymbol(z, g_tc_trace, sizeof(z));
+      const long long t0 = z[0][0];
+      std::fprintf(stderr, "it  mma_start full tempty issued | epi_wait tfull ld0 c0 ld1 arrive c1 done\n");
+      for (int it = 0; it < 40; it += 2)
+        std::fprintf(stderr, "%2d %7lld %7lld %7lld %7lld | %7lld %7lld %7lld %7lld %7lld %7lld %7lld %7lld\n", it,
+                     z[0][it] - t0, z[1][it] - t0, z[2][it] - t0, z[3][it] - t0, z[4][it] - t0, z[5][it] - t0,
+                     z[8][it] - t0, z[9][it] - t0, z[10][it] - t0, z[6][it] - t0, z[11][it] - t0, z[7][it] - t0);
+    }
+  }
   note_launch();
 }
 
