@@ -528,14 +528,24 @@ def rooflines(phases, sign_iso_ms, N, K, pairs, cp, peaks, peaks_src, n_sm, cloc
         return (t / c if c else 0.0), c
 
     out = {}
-    # K3: FP32 FMA bound, 2*K flop per pair (unit signatures: cosine = dot).
+    # K3 on tcgen05 (k3_tc.cu): tensor bound. Executed MMA flops = 2 * K' * 128 * 128 per
+    # computed 128x128 block (K' = roundup16(3K + 3): split-fp16 hi/lo operands + folded tau);
+    # the fp32-equivalent algorithmic rate (2K flop per pair) is reported beside it.
     t3, _ = per_launch("pair_tiles")
-    fp32_peak = n_sm * 128 * 2 * clock_mhz * 1e6 / 1e12  # TFLOP/s at the clock sampled under load
-    ach = 2.0 * K * pairs / (t3 / 1e3) / 1e12 if t3 else 0.0
-    out["mrc_tiles"] = {"bound": "fp32", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
-                        "frac": ach / fp32_peak, "ms_per_launch": t3,
-                        "peak_source": f"{n_sm} SMs x 128 FFMA/clk x 2 x {clock_mhz:.0f} MHz (median SM clock "
-                                       f"sampled during the timed region)",
+    kp = ((3 * K + 3) + 15) // 16 * 16
+    nb = (N + 127) // 128
+    blocks = sum(1 + (1 if (r0 + 1 < nb and bj >= r0 + 1) else 0) for r0 in range(0, nb, 2) for bj in range(r0, nb))
+    mma_flops = 2.0 * kp * 128 * 128 * blocks
+    tc_peak = peaks.get("bf16_tflops", 2250.0)
+    ach = mma_flops / (t3 / 1e3) / 1e12 if t3 else 0.0
+    out["mrc_tiles"] = {"bound": "tensor", "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s",
+                        "frac": ach / tc_peak, "ms_per_launch": t3,
+                        "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; fp16 kind::f16 has the same rate)",
+                        "mma_flops_per_launch": mma_flops, "k_prime": kp, "blocks_128x128": blocks,
+                        "fp32_equiv_tflops": 2.0 * K * pairs / (t3 / 1e3) / 1e12 if t3 else 0.0,
+                        "note": "phase = operand-form kernel + tcgen05 tile kernel; per tile the epilogue's "
+                                "sign-bit packing (1 ALU op per pair, ALU pipe 2 cyc/warp-instr) matches the "
+                                "MMA time, see DESIGN.md K3",
                         "share_of_step": t3 / ms_per_step}
     # K2: HBM bound; survey §8d per-signature bytes 8*nnz + 4*K + 4.
     nnz = nnz_total(cp)
