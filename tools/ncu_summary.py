@@ -23,7 +23,7 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROF = os.path.join(REPO, "profiles")
 
 # bench.py roofline keys -> kernel name fragments
-ROOF_KERNELS = {"mrc_tiles": ["mrc_bitmap_kernel"], "sign": ["sign_kernel"], "pair_emit": ["emit_kernel"],
+ROOF_KERNELS = {"mrc_tiles": ["mrc_tc_kernel", "tc_forms_kernel", "mrc_bitmap_kernel"], "sign": ["sign_kernel"], "pair_emit": ["emit_kernel"],
                 "count": ["count_warp_kernel", "group_sort_kernel", "count_large_kernel", "idf_kernel"],
                 "reference": ["ref_mark_kernel", "ref_assign_kernel", "ref_fill_kernel"],
                 "simhash": ["simhash_kernel"], "hamming_tiles": ["hamming_bitmap_kernel"]}
@@ -73,7 +73,9 @@ WANT = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "dram r
         ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue %"),
         ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps %"),
         ("launch__registers_per_thread", "regs"), ("launch__grid_size", "grid"),
-        ("smsp__inst_executed.sum", "warp inst"), ("lts__t_sector_hit_rate.pct", "L2 hit %")]
+        ("smsp__inst_executed.sum", "warp inst"), ("lts__t_sector_hit_rate.pct", "L2 hit %"),
+        ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %"),
+        ("sm__ops_path_tensor_src_fp16_dst_fp32.sum", "tensor fp16->fp32 ops")]
 
 
 def to_bytes(v, unit):
