@@ -164,6 +164,21 @@ def test_mrc_pairs_c0_vs_oracle(gpu_ctx_factory, tau):
     assert_pairs_match(keys, pairs, border, f"tau={tau}")
 
 
+@pytest.mark.parametrize("K", [1, 2, 7, 41, 42])
+def test_mrc_pairs_tensor_core_k_edges(gpu_ctx_factory, K):
+    """K3 runs on tcgen05 for 3K + 3 <= 128 (K <= 41) and on FP32 CUDA cores
+    above: both sides of the switch, and the smallest K'."""
+    cp, cfg = corpus_c0(1500)
+    refs = C.sample_refs(7, cp.n_docs, K)
+    ctx = gpu_ctx_factory()
+    gpu_pipeline(ctx, cp, refs)
+    o = oracle_pipeline(cp, refs)
+    for tau in (0.5, 0.9):
+        keys = ctx.mrc_pairs(tau)
+        pairs, border = oracle.mrc_pairs(o.S, tau, BAND)
+        assert_pairs_match(keys, pairs, border, f"K={K} tau={tau}")
+
+
 def test_mrc_pairs_c1_vs_oracle(gpu_ctx_factory):
     cp, cfg = C.config_corpus("c1")
     refs = C.sample_refs(cfg["ref_seed"], cp.n_docs, cfg["K"])
