@@ -4,7 +4,7 @@
 NVCC     ?= /usr/local/cuda/bin/nvcc
 CXX      ?= g++
 ARCH     := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude --expt-relaxed-constexpr -Xptxas -v
+NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude --expt-relaxed-constexpr -Xptxas -v $(NVEXTRA)
 CPUFLAGS := -O3 -std=c++20 -fPIC -march=x86-64-v3 -ffp-contract=off -pthread
 REF_INC  ?= /root/reference/proj/include
 

@@ -45,10 +45,19 @@ namespace refsig_gpu {
 namespace {
 
 constexpr uint32_t kTcThreads = 608;  // producer warp, 2 MMA warps, 16 epilogue warps
-__device__ long long g_tc_trace[12][64];  // REFSIG_TC_DEBUG & 8: CTA 0 event clocks per tile
+// Timing experiments (build with -DREFSIG_TC_TRACE; tools/tc_trace_run.py):
+// REFSIG_TC_DEBUG bits 1 no epilogue math, 2 no B refill, 4 no MMA, 8 record
+// per-tile clock64 events of CTA 0 (16: the last CTA) and print them.
+#ifdef REFSIG_TC_TRACE
+__device__ long long g_tc_trace[12][64];
 __device__ __forceinline__ void tc_trace(const uint32_t dbg, int ev, uint32_t it) {
   if ((dbg & 8) && blockIdx.x == ((dbg & 16) ? gridDim.x - 1 : 0) && it < 64) g_tc_trace[ev][it] = clock64();
 }
+#define TC_DBG(a) ((a).dbg)
+#else
+__device__ __forceinline__ void tc_trace(uint32_t, int, uint32_t) {}
+#define TC_DBG(a) 0u
+#endif
 constexpr uint32_t kTcMaxKP = 128;  // 3K + 3 <= 128  <=>  K <= 41
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -134,6 +143,16 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
         "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                  \
       : "r"(addr))
 
+// (b << 1) | (v >> 31) on the FMA pipe: mul.hi(v, 2) = v >> 31, then b*2 + that.
+// `two` is a runtime 2 (kernel argument) so ptxas keeps IMADs instead of
+// turning them into ALU shifts.
+__device__ __forceinline__ uint32_t fma_pipe_shift_in(uint32_t b, uint32_t v, uint32_t two) {
+  uint32_t s, r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(s) : "r"(v), "r"(two));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(two), "r"(s));
+  return r;
+}
+
 // Valid-column mask for the 32 columns starting at lo in row i (k3_pairs.cu col_mask).
 __device__ __forceinline__ uint32_t tc_col_mask(uint32_t lo, uint32_t i, const PairGrid& g) {
   uint32_t m = 0xffffffffu;
@@ -157,6 +176,7 @@ struct TcArgs {
   uint32_t stages;
   uint32_t* bitmap;
   uint32_t* rowcnt;
+  uint32_t two;  // 2, as data (see fma_pipe_shift_in)
   uint32_t dbg;  // timing experiments only (REFSIG_TC_DEBUG): 1 no epilogue math, 2 no B refill, 4 no MMA
 };
 
@@ -248,7 +268,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
         const uint32_t st = it % S;
         if (it >= S) mb_wait(&empty_bar[st], ((it / S) - 1) & 1u);
         const uint32_t bj = tc_cs(a, w.p) + w.c;
-        if ((a.dbg & 2) && it >= S) {
+        if ((TC_DBG(a) & 2) && it >= S) {
           mb_arrive(&full_bar[st]);
         } else {
           mb_expect_tx(&full_bar[st], PB);
@@ -283,16 +303,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
           const uint32_t bj = tc_cs(a, w.p) + w.c;
           const uint32_t r0 = tc_r0(a, w.p);
           const bool v1 = tc_rvalid(a, w.p, 1) && !(a.g.triangle && bj < r0 + 1);
-          if (lane == 0 && m == 0) tc_trace(a.dbg, 0, it);
+          if (lane == 0 && m == 0) tc_trace(TC_DBG(a), 0, it);
           mb_wait(&full_bar[st], (it / S) & 1u);
-          if (lane == 0 && m == 0) tc_trace(a.dbg, 1, it);
+          if (lane == 0 && m == 0) tc_trace(TC_DBG(a), 1, it);
           if (it >= 2) mb_wait(&tempty_bar[acc], ((it >> 1) - 1) & 1u);
-          if (lane == 0 && m == 0) tc_trace(a.dbg, 2, it);
+          if (lane == 0 && m == 0) tc_trace(TC_DBG(a), 2, it);
           tc_fence_after();
           const uint64_t dA = dA0 + ab * 2 * dPB, dB = dB0 + st * dPB;
           const uint32_t d0 = tmem + acc * 256;
           const uint32_t e = elect_one();
-          if (!(a.dbg & 4)) {
+          if (!(TC_DBG(a) & 4)) {
             mma_f16_e(e, d0, dA, dB, 0);
 #pragma unroll
             for (uint32_t k = 1; k < KS; ++k) mma_f16_e(e, d0, dA + k * 256, dB + k * 256, 1);
@@ -302,7 +322,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
               for (uint32_t k = 1; k < KS; ++k) mma_f16_e(e, d0 + 128, dA + dPB + k * 256, dB + k * 256, 1);
             }
           }
-          if (lane == 0 && m == 0) tc_trace(a.dbg, 3, it);
+          if (lane == 0 && m == 0) tc_trace(TC_DBG(a), 3, it);
           mma_commit_e(e, &empty_bar[st]);
           mma_commit_e(e, &tfull_bar[acc]);
         }
@@ -318,6 +338,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
              // lane quarter q, row block h of the row group; all 128 columns in two halves
     const uint32_t q = warp & 3, eg = (warp - 3) >> 3, h = ((warp - 3) >> 2) & 1;
     const uint32_t wpr = a.g.words_per_row;
+    const uint32_t two = a.two;
     TileWalk w;
     if (n_it) w.start(a, t0);
     uint32_t cnt = 0;
@@ -329,9 +350,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
       const uint32_t i = r * 128 + q * 32 + lane;
       if (acc == eg) {
         const uint32_t u = it >> 1;  // this group's use count of its accumulator
-        if (warp == 3 && lane == 0) tc_trace(a.dbg, 4, it);
+        if (warp == 3 && lane == 0) tc_trace(TC_DBG(a), 4, it);
         mb_wait(&tfull_bar[acc], u & 1u);
-        if (warp == 3 && lane == 0) tc_trace(a.dbg, 5, it);
+        if (warp == 3 && lane == 0) tc_trace(TC_DBG(a), 5, it);
         tc_fence_after();
         const bool valid = tc_rvalid(a, p, h) && !(a.g.triangle && bj < r);
         const bool edge = (a.g.triangle && bj == r) || bj + 1 == a.nbc;
@@ -345,33 +366,39 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
             TC_LD32(ta + 32, v1);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           }
-          if (warp == 3 && lane == 0) tc_trace(a.dbg, 8 + 2 * half, it);
+          if (warp == 3 && lane == 0) tc_trace(TC_DBG(a), 8 + 2 * half, it);
           if (half == 1) {  // accumulator fully read: hand it back to the MMA issuer
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mb_arrive(&tempty_bar[acc]);
-            if (warp == 3 && lane == 0) tc_trace(a.dbg, 6, it);
+            if (warp == 3 && lane == 0) tc_trace(TC_DBG(a), 6, it);
           }
-          if (valid && !(a.dbg & 1)) {
+          if (valid && !(TC_DBG(a) & 1)) {
             // bit c = sign(dot - tau) of column c: eight independent 8-deep
-            // funnel chains (one per byte), then bytes -> words with PRMT
+            // chains (one per byte), then bytes -> words with PRMT. Bytes 0-2 of
+            // each word use the ALU funnel shift (1 op per bit), byte 3 the FMA
+            // pipe (IMAD.HI gives v >> 31, IMAD appends it: 2 ops per bit), so
+            // the two 2-cycle pipes share the per-pair work ~48:32 instead of
+            // 64:0 cycles per 32 pairs.
             uint32_t b[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) b[k] = 0;
 #pragma unroll
             for (int c = 7; c >= 0; --c) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k) {
+              for (int k = 0; k < 3; ++k) {
                 b[k] = __funnelshift_l(v0[8 * k + c], b[k], 1);
                 b[4 + k] = __funnelshift_l(v1[8 * k + c], b[4 + k], 1);
               }
+              b[3] = fma_pipe_shift_in(b[3], v0[24 + c], two);
+              b[7] = fma_pipe_shift_in(b[7], v1[24 + c], two);
             }
             mw[2 * half] = ~__byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
             mw[2 * half + 1] = ~__byte_perm(__byte_perm(b[4], b[5], 0x0040), __byte_perm(b[6], b[7], 0x0040), 0x5410);
           }
-          if (warp == 3 && lane == 0) tc_trace(a.dbg, 9 + 2 * half, it);
+          if (warp == 3 && lane == 0) tc_trace(TC_DBG(a), 9 + 2 * half, it);
         }
-        if (valid && !(a.dbg & 1)) {
+        if (valid && !(TC_DBG(a) & 1)) {
           if (edge) {
             const uint32_t c0 = bj * 128;
 #pragma unroll
@@ -383,7 +410,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
             cnt += __popc(mw[0]) + __popc(mw[1]) + __popc(mw[2]) + __popc(mw[3]);
           }
         }
-        if (warp == 3 && lane == 0) tc_trace(a.dbg, 7, it);
+        if (warp == 3 && lane == 0) tc_trace(TC_DBG(a), 7, it);
       }
       if (w.next(a) || it + 1 == n_it) {
         if (cnt && i < a.g.n_rows) atomicAdd(a.rowcnt + i, cnt);
@@ -517,6 +544,7 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
   a.n_tiles = T;
   a.bitmap = bitmap;
   a.rowcnt = rowcnt;
+  a.two = 2;
   static const uint32_t dbg = [] {
     const char* m = std::getenv("REFSIG_TC_DEBUG");
     return m ? static_cast<uint32_t>(std::atoi(m)) : 0u;
@@ -543,6 +571,7 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(T, static_cast<uint64_t>(sms)));
+#ifdef REFSIG_TC_TRACE
   if (dbg & 8) {
     static bool dumped = false;
     if (dumped) {
@@ -552,6 +581,7 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
       cudaMemcpyToSymbolAsync(g_tc_trace, z, sizeof(z), 0, cudaMemcpyHostToDevice, s);
     }
   }
+#endif
   switch (a.KP / 16) {
     case 1: mrc_tc_kernel<1><<<grid, kTcThreads, smem, s>>>(a); break;
     case 2: mrc_tc_kernel<2><<<grid, kTcThreads, smem, s>>>(a); break;
@@ -562,6 +592,7 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
     case 7: mrc_tc_kernel<7><<<grid, kTcThreads, smem, s>>>(a); break;
     default: mrc_tc_kernel<8><<<grid, kTcThreads, smem, s>>>(a); break;
   }
+#ifdef REFSIG_TC_TRACE
   if (dbg & 8) {
     static int calls = 0;
     if (++calls == 3) {
@@ -577,6 +608,7 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
     }
   }
   note_launch();
+#endif
 }
 
 }  // namespace refsig_gpu
