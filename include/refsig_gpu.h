@@ -190,6 +190,27 @@ typedef struct {
 } refsig_gpu_eval;
 int refsig_gpu_evaluate(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_hi, refsig_gpu_eval* out);
 
+/* ---- multi-GPU building blocks -----------------------------
+ * One rank per GPU holds a contiguous shard of the documents:
+ *   1. refsig_gpu_count() on the shard; all-reduce the df table in place
+ *      (refsig_gpu_device_buffer(REFSIG_BUF_DF), NCCL sum) or pass the global
+ *      table from the host, then refsig_gpu_set_global_df(ctx, df|NULL, N):
+ *      idf from the global df and N (bit-identical on every rank);
+ *   2. the K reference documents' (id, count) rows (from their owners) via
+ *      refsig_gpu_set_reference_counts: weighted count * idf on the device,
+ *      exactly as refsig_gpu_set_reference_docs weights them;
+ *   3. refsig_gpu_sign(); all-gather the shards' S (REFSIG_BUF_SIGNATURES) in
+ *      rank order;
+ *   4. on a pairs context: refsig_gpu_set_signatures(ctx, N, K, S_all, on_device)
+ *      builds the unit transposed signatures (bit-identical to sign()'s), then
+ *      refsig_gpu_mrc_pairs_rows() over this rank's row panel (shard.row_shards).
+ * The resulting candidate lists concatenate, in rank order, into the
+ * single-GPU list. */
+int refsig_gpu_set_global_df(refsig_gpu_ctx* ctx, const uint32_t* df_global, uint32_t n_docs_global);
+int refsig_gpu_set_reference_counts(refsig_gpu_ctx* ctx, uint32_t K, const uint64_t* rowptr, const uint32_t* term_ids,
+                                    const uint32_t* counts);
+int refsig_gpu_set_signatures(refsig_gpu_ctx* ctx, uint32_t n_docs, uint32_t K, const float* S, int on_device);
+
 /* ---- query-vs-database mode (configs[4]) -------------------------------------
  * `db` holds the signed/fingerprinted database; `q` holds the query corpus,
  * counted with the database's IDF and signed against its reference. */

@@ -95,6 +95,10 @@ SIGNATURES = {
     "refsig_gpu_evaluate": ([_c.c_void_p, _c.c_uint32, _c.c_uint32, _c.c_void_p], _c.c_int),
     "refsig_gpu_get_corpus_freq": ([_c.c_void_p, _P(_c.c_uint64)], _c.c_int),
     "refsig_gpu_get_signature_records": ([_c.c_void_p, _c.c_uint64, _P(_c.c_uint8), _c.c_uint64], _c.c_int),
+    "refsig_gpu_set_global_df": ([_c.c_void_p, _P(_c.c_uint32), _c.c_uint32], _c.c_int),
+    "refsig_gpu_set_reference_counts": ([_c.c_void_p, _c.c_uint32, _P(_c.c_uint64), _P(_c.c_uint32),
+                                         _P(_c.c_uint32)], _c.c_int),
+    "refsig_gpu_set_signatures": ([_c.c_void_p, _c.c_uint32, _c.c_uint32, _c.c_void_p, _c.c_int], _c.c_int),
     "refsig_gpu_load_text": ([_c.c_void_p, _P(_c.c_uint8), _P(_c.c_uint64), _c.c_uint32], _c.c_int),
     "refsig_gpu_simhash_text": ([_c.c_void_p], _c.c_int),
     "refsig_gpu_get_pairs_csr": ([_c.c_void_p, _c.c_uint32, _c.c_uint32, _P(_c.c_uint64), _P(_c.c_uint32), _c.c_uint64,
@@ -273,6 +277,43 @@ class Context:
         rowptr[1:] = np.cumsum([len(p) for p in parts])
         ids = np.concatenate([np.asarray(p, np.uint32) for p in parts]) if parts else np.zeros(0, np.uint32)
         self.set_reference_vectors(rowptr, ids, None)
+
+    def set_reference_counts(self, rowptr, term_ids, counts):
+        """Reference vectors from (id, count) rows, weighted count * idf on the
+        device like set_reference_docs (multi-GPU: the reference docs' rows
+        come from the ranks that own them)."""
+        rowptr = np.ascontiguousarray(rowptr, np.uint64)
+        term_ids = np.ascontiguousarray(term_ids, np.uint32)
+        counts = np.ascontiguousarray(counts, np.uint32)
+        K = len(rowptr) - 1
+        self._check(self._L.refsig_gpu_set_reference_counts(self._h, K, _ptr(rowptr, ctypes.c_uint64),
+                                                            _ptr(term_ids, ctypes.c_uint32),
+                                                            _ptr(counts, ctypes.c_uint32)))
+        self.K = K
+
+    # -- multi-GPU building blocks (include/refsig_gpu.h) ----------------------
+    def set_global_df(self, n_docs_global: int, df: np.ndarray | None = None):
+        """idf from the global document frequencies: `df` from the host, or
+        None when the device df buffer already holds the reduced table."""
+        d = None if df is None else np.ascontiguousarray(df, np.uint32)
+        if d is not None and len(d) != self.vocab:
+            raise ValidationError("df must have vocab entries")
+        self._check(self._L.refsig_gpu_set_global_df(self._h, _ptr(d, ctypes.c_uint32), int(n_docs_global)))
+
+    def set_signatures(self, S, n_docs: int | None = None, K: int | None = None):
+        """Install signatures for pair computations (a pairs-only context):
+        `S` is a host float32 [n_docs, K] array or a device pointer (int)."""
+        if isinstance(S, int):
+            if n_docs is None or K is None:
+                raise ValidationError("n_docs and K are required with a device pointer")
+            self._check(self._L.refsig_gpu_set_signatures(self._h, int(n_docs), int(K), ctypes.c_void_p(S), 1))
+        else:
+            S = np.ascontiguousarray(S, np.float32)
+            if S.ndim != 2:
+                raise ValidationError("S must be [n_docs, K]")
+            n_docs, K = S.shape
+            self._check(self._L.refsig_gpu_set_signatures(self._h, n_docs, K, S.ctypes.data_as(ctypes.c_void_p), 0))
+        self.n_docs, self.K = int(n_docs), int(K)
 
     def reference_union(self) -> int:
         u = ctypes.c_uint32()

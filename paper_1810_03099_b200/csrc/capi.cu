@@ -864,47 +864,106 @@ int refsig_gpu_set_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_i
   return guard(ctx, [&] { do_set_reference_docs(ctx, ref_doc_ids, K); });
 }
 
-int refsig_gpu_set_reference_vectors(refsig_gpu_ctx* ctx, uint32_t K, const uint64_t* rowptr, const uint32_t* term_ids,
-                                     const float* weights) {
-  return guard(ctx, [&] {
-    require(ctx->counted, "count() not called");
-    require(!ctx->db, "query context uses the attached database's reference");
-    require(K >= 1 && K <= kMaxRefs, "K must be in 1..256");
-    require(rowptr != nullptr, "rowptr is NULL");
-    require(rowptr[0] == 0, "rowptr[0] must be 0");
-    for (uint32_t k = 0; k < K; ++k) require(rowptr[k + 1] >= rowptr[k], "rowptr must be non-decreasing");
-    const uint64_t n = rowptr[K];
-    require(n == 0 || term_ids != nullptr, "term_ids is NULL");
-    std::vector<uint2> h(n);
-    std::vector<uint64_t> start(K);
-    std::vector<uint32_t> cnt(K);
-    for (uint32_t k = 0; k < K; ++k) {
-      start[k] = rowptr[k];
-      cnt[k] = static_cast<uint32_t>(rowptr[k + 1] - rowptr[k]);
-      std::vector<uint32_t> ids(term_ids + rowptr[k], term_ids + rowptr[k + 1]);
-      std::sort(ids.begin(), ids.end());
-      for (size_t i = 0; i < ids.size(); ++i) {
-        require(ids[i] < ctx->vocab, "reference term id >= vocab");
-        require(i == 0 || ids[i] != ids[i - 1], "duplicate term in a reference vector");
-      }
-      for (uint64_t p = rowptr[k]; p < rowptr[k + 1]; ++p) {
+// Explicit reference vectors: weights as given (explicit_w) or counts weighted
+// on the device with this context's idf (count * idf, like reference docs).
+static void do_set_reference_table(refsig_gpu_ctx* ctx, uint32_t K, const uint64_t* rowptr, const uint32_t* term_ids,
+                                   const float* weights, bool from_counts, const uint32_t* counts) {
+  require(ctx->counted, "count() not called");
+  require(!ctx->db, "query context uses the attached database's reference");
+  require(K >= 1 && K <= kMaxRefs, "K must be in 1..256");
+  require(rowptr != nullptr, "rowptr is NULL");
+  require(rowptr[0] == 0, "rowptr[0] must be 0");
+  for (uint32_t k = 0; k < K; ++k) require(rowptr[k + 1] >= rowptr[k], "rowptr must be non-decreasing");
+  const uint64_t n = rowptr[K];
+  require(n == 0 || term_ids != nullptr, "term_ids is NULL");
+  require(!from_counts || n == 0 || counts != nullptr, "counts is NULL");
+  std::vector<uint2> h(n);
+  std::vector<uint64_t> start(K);
+  std::vector<uint32_t> cnt(K);
+  for (uint32_t k = 0; k < K; ++k) {
+    start[k] = rowptr[k];
+    cnt[k] = static_cast<uint32_t>(rowptr[k + 1] - rowptr[k]);
+    std::vector<uint32_t> ids(term_ids + rowptr[k], term_ids + rowptr[k + 1]);
+    std::sort(ids.begin(), ids.end());
+    for (size_t i = 0; i < ids.size(); ++i) {
+      require(ids[i] < ctx->vocab, "reference term id >= vocab");
+      require(i == 0 || ids[i] != ids[i - 1], "duplicate term in a reference vector");
+    }
+    for (uint64_t p = rowptr[k]; p < rowptr[k + 1]; ++p) {
+      uint32_t bits;
+      if (from_counts) {
+        bits = counts[p];
+      } else {
         const float w = weights ? weights[p] : 1.0f;
         require(std::isfinite(w) && w >= 0.0f, "reference weights must be finite and >= 0");
-        uint32_t bits;
         std::memcpy(&bits, &w, 4);
-        h[p] = make_uint2(term_ids[p], bits);
       }
+      h[p] = make_uint2(term_ids[p], bits);
     }
-    ctx->ref_ent.ensure(sizeof(uint2) * std::max<uint64_t>(n, 1));
-    ctx->ref_start.ensure(8ull * K);
-    ctx->ref_n.ensure(4ull * K);
-    if (n) ck(cudaMemcpyAsync(ctx->ref_ent.p, h.data(), sizeof(uint2) * n, cudaMemcpyHostToDevice, ctx->stream), "H2D");
-    ck(cudaMemcpyAsync(ctx->ref_start.p, start.data(), 8ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D");
-    ck(cudaMemcpyAsync(ctx->ref_n.p, cnt.data(), 4ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D");
-    RefArgs r{K, ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->ref_ent.as<uint2>(), true,
-              ref_row_stride(K), nullptr, nullptr, nullptr};
-    build_reference(ctx, r, n);
-    ck(cudaStreamSynchronize(ctx->stream), "reference");
+  }
+  ctx->ref_ent.ensure(sizeof(uint2) * std::max<uint64_t>(n, 1));
+  ctx->ref_start.ensure(8ull * K);
+  ctx->ref_n.ensure(4ull * K);
+  if (n) ck(cudaMemcpyAsync(ctx->ref_ent.p, h.data(), sizeof(uint2) * n, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  ck(cudaMemcpyAsync(ctx->ref_start.p, start.data(), 8ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  ck(cudaMemcpyAsync(ctx->ref_n.p, cnt.data(), 4ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+  RefArgs r{K, ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->ref_ent.as<uint2>(), !from_counts,
+            ref_row_stride(K), nullptr, nullptr, nullptr};
+  build_reference(ctx, r, n);
+  ck(cudaStreamSynchronize(ctx->stream), "reference");
+}
+
+int refsig_gpu_set_reference_vectors(refsig_gpu_ctx* ctx, uint32_t K, const uint64_t* rowptr, const uint32_t* term_ids,
+                                     const float* weights) {
+  return guard(ctx, [&] { do_set_reference_table(ctx, K, rowptr, term_ids, weights, false, nullptr); });
+}
+
+int refsig_gpu_set_reference_counts(refsig_gpu_ctx* ctx, uint32_t K, const uint64_t* rowptr, const uint32_t* term_ids,
+                                    const uint32_t* counts) {
+  return guard(ctx, [&] { do_set_reference_table(ctx, K, rowptr, term_ids, nullptr, true, counts); });
+}
+
+int refsig_gpu_set_global_df(refsig_gpu_ctx* ctx, const uint32_t* df_global, uint32_t n_docs_global) {
+  return guard(ctx, [&] {
+    require(ctx->counted, "count() not called");
+    require(!ctx->db, "query contexts use the attached database's idf");
+    require(n_docs_global >= ctx->n_docs, "n_docs_global is smaller than this shard");
+    if (df_global)
+      ck(cudaMemcpyAsync(ctx->df.p, df_global, 4ull * ctx->vocab, cudaMemcpyHostToDevice, ctx->stream), "H2D df");
+    launch_idf_from_df(ctx->df.as<uint32_t>(), ctx->vocab, n_docs_global, ctx->weight_mode, ctx->info.as<TermInfo>(),
+                       ctx->stream);
+    launched("global idf");
+    ctx->ref_dirty = false;  // idf_from_df resets info[].ref_row
+    reset_downstream(ctx);
+    sync(ctx);
+  });
+}
+
+int refsig_gpu_set_signatures(refsig_gpu_ctx* ctx, uint32_t n_docs, uint32_t K, const float* S, int on_device) {
+  return guard(ctx, [&] {
+    require(K >= 1 && K <= kMaxRefs, "K must be in 1..256");
+    require(S != nullptr || n_docs == 0, "S is NULL");
+    require(!ctx->emit_pending, "pair computation in flight");
+    const uint32_t ld = static_cast<uint32_t>(ceil_div(n_docs, kTile) * kTile);
+    ctx->S.ensure(sizeof(float) * static_cast<size_t>(n_docs) * K);
+    ctx->ST.ensure(sizeof(float) * static_cast<size_t>(std::max<uint32_t>(ld, 1)) * K);
+    if (n_docs)
+      ck(cudaMemcpyAsync(ctx->S.p, S, sizeof(float) * static_cast<size_t>(n_docs) * K,
+                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream),
+         "copy signatures");
+    if (ld > n_docs)
+      ck(cudaMemset2DAsync(ctx->ST.as<float>() + n_docs, sizeof(float) * ld, 0, sizeof(float) * (ld - n_docs), K,
+                           ctx->stream),
+         "memset ST pad");
+    launch_st_from_s(ctx->S.as<float>(), n_docs, K, ld, ctx->ST.as<float>(), ctx->stream);
+    launched("signatures");
+    reset_downstream(ctx);
+    ctx->n_docs = n_docs;
+    ctx->K = K;
+    ctx->ld = ld;
+    ctx->signed_ = true;
+    ctx->counted = ctx->loaded = false;  // a pairs-only context until the next load
+    sync(ctx);
   });
 }
 

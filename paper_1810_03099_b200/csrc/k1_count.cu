@@ -375,6 +375,17 @@ __global__ void idf_kernel(const uint32_t* __restrict__ df_rep, uint32_t reps, u
   }
 }
 
+// idf from an externally reduced df (multi-GPU: each rank counts its shard of
+// documents, df is all-reduced, then every rank recomputes the same table).
+__global__ void idf_from_df_kernel(const uint32_t* __restrict__ df, uint32_t vocab, uint32_t n_docs, int weight_mode,
+                                   TermInfo* __restrict__ info) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < vocab; t += gridDim.x * blockDim.x) {
+    float idf = 1.0f;
+    if (weight_mode == 1) idf = static_cast<float>(log((1.0 + n_docs) / (1.0 + df[t])) + 1.0);
+    info[t] = TermInfo{idf, -1};
+  }
+}
+
 // corpus_freq (SPEC.md FrequencyTable): cf[t] += count of every (doc, t) row,
 // 64-bit atomics into R replicas (replica = warp index mod R: Zipf-head terms
 // are in every document), then summed by cf_sum_kernel. Integer sums: exact.
@@ -498,6 +509,12 @@ void launch_count_large(const CountArgs& a, const uint32_t* long_docs, const uin
 void launch_idf(const uint32_t* df_rep, uint32_t reps, uint32_t vocab, uint32_t n_docs, int weight_mode, uint32_t* df,
                 TermInfo* info, cudaStream_t s) {
   idf_kernel<<<grid_for((vocab + 255) / 256, 8), 256, 0, s>>>(df_rep, reps, vocab, n_docs, weight_mode, df, info);
+  note_launch();
+}
+
+void launch_idf_from_df(const uint32_t* df, uint32_t vocab, uint32_t n_docs, int weight_mode, TermInfo* info,
+                        cudaStream_t s) {
+  idf_from_df_kernel<<<grid_for((vocab + 255) / 256, 8), 256, 0, s>>>(df, vocab, n_docs, weight_mode, info);
   note_launch();
 }
 

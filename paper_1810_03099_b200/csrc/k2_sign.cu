@@ -18,6 +18,8 @@
 // (inv_norm); the transposed unit copy for K3, TermInfo and R gathers are
 // L2 traffic. R rows are padded to Kp = roundup(K,4) floats.
 
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace refsig_gpu {
@@ -425,7 +427,34 @@ __global__ void __launch_bounds__(256) sign_col_kernel(SignArgs a) {
   }
 }
 
+// Unit-signature transpose for externally supplied signatures (multi-GPU:
+// the all-gathered S of every rank). Same arithmetic and order as the sign
+// kernels' epilogue (per-lane fmaf over columns lane, lane+32, ..., then the
+// xor-butterfly warp sum), so ST is bit-identical to a single-GPU sign().
+__global__ void __launch_bounds__(256) st_from_s_kernel(const float* __restrict__ S, uint32_t n_docs, uint32_t K,
+                                                        uint32_t ld, float* __restrict__ ST) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t d = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); d < n_docs; d += nw) {
+    float ss = 0.0f;
+    for (uint32_t k = lane; k < K; k += 32) {
+      const float v = S[static_cast<size_t>(d) * K + k];
+      ss = fmaf(v, v, ss);
+    }
+    ss = warp_sum(ss);
+    const float inv_s = ss > 0.0f ? 1.0f / sqrtf(ss) : 0.0f;
+    for (uint32_t k = lane; k < K; k += 32) ST[static_cast<size_t>(k) * ld + d] = S[static_cast<size_t>(d) * K + k] * inv_s;
+  }
+}
+
 }  // namespace
+
+void launch_st_from_s(const float* S, uint32_t n_docs, uint32_t K, uint32_t ld, float* ST, cudaStream_t s) {
+  if (!n_docs) return;
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>(ceil_div(n_docs, 8), 148ull * 16));
+  st_from_s_kernel<<<g, 256, 0, s>>>(S, n_docs, K, ld, ST);
+  note_launch();
+}
 
 void launch_ref_reset(TermInfo* info, uint32_t vocab, cudaStream_t s) {
   uint32_t g = (vocab + 255) / 256;

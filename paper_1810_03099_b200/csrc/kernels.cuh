@@ -58,6 +58,11 @@ void launch_idf(const uint32_t* df_rep, uint32_t reps, uint32_t vocab, uint32_t 
 // MRCS signature records, 20 + 8K bytes per doc, as 32-bit words.
 void launch_mrcs_records(const float* S, uint32_t n_docs, uint32_t K, uint64_t ref_id, uint32_t* out,
                          cudaStream_t s);
+// info[t] = {idf(df[t], n_docs), -1} from a (globally reduced) df table.
+void launch_idf_from_df(const uint32_t* df, uint32_t vocab, uint32_t n_docs, int weight_mode, TermInfo* info,
+                        cudaStream_t s);
+// ST[k][ld] = unit(S[d][.]) for externally supplied signatures (k2_sign.cu).
+void launch_st_from_s(const float* S, uint32_t n_docs, uint32_t K, uint32_t ld, float* ST, cudaStream_t s);
 // cf[t] = sum of the counts of term t over all documents (exact, 64-bit).
 void launch_corpus_freq(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, uint32_t n_docs,
                         uint32_t vocab, uint32_t reps, unsigned long long* cf_rep, uint64_t* cf, cudaStream_t s);

@@ -81,3 +81,66 @@ def test_gloo_world2_sharded_pairs_equal_single_rank():
     same_mrc, same_ham, n, tmax = res
     assert same_mrc and same_ham and n > 0
     assert tmax == 2.0
+
+
+class _FakeShardCtx:
+    """The two calls TorchComm's gloo path makes on a context."""
+
+    def __init__(self, df, S):
+        self._df, self._S = df, S
+
+    def df(self):
+        return self._df, None
+
+    def signatures(self):
+        return self._S
+
+
+def _comm_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(rank)
+    n_local = [5, 3][rank]
+    ctx = _FakeShardCtx(rng.integers(0, 9, 50).astype(np.uint32), rng.random((n_local, 4)).astype(np.float32))
+    comm = shard.TorchComm(dist)
+    df = comm.allreduce_df(ctx)
+    S, counts = comm.allgather_signatures(ctx, n_local, 4, 5)
+    q.put((rank, df, S, counts))
+    dist.destroy_process_group()
+
+
+def test_torch_comm_gloo_df_sum_and_ordered_signatures():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_comm_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    ref_df = sum(np.random.default_rng(r).integers(0, 9, 50) for r in range(world))
+    # each fake context draws df, then S, from its rank's generator
+    ref_S = []
+    for r, n in zip(range(world), [5, 3]):
+        g = np.random.default_rng(r)
+        g.integers(0, 9, 50)
+        ref_S.append(g.random((n, 4)).astype(np.float32))
+    ref_S = np.concatenate(ref_S)
+    for rank, df, S, counts in res:
+        assert np.array_equal(df, ref_df.astype(np.uint32))
+        assert counts == [5, 3]
+        assert S.tobytes() == ref_S.tobytes()
+
+
+def test_doc_shards_cover_and_balance():
+    from paper_1810_03099_b200 import corpus as C
+    cp, _ = C.config_corpus("c0")
+    for w in [1, 2, 3, 8]:
+        sh = shard.doc_shards(cp.doc_off, w)
+        assert sh[0][0] == 0 and sh[-1][1] == cp.n_docs and all(b == c for (_, b), (c, _) in zip(sh, sh[1:]))
+        toks = [int(cp.doc_off[hi]) - int(cp.doc_off[lo]) for lo, hi in sh]
+        assert max(toks) <= sum(toks) / w * 1.1 + 5000
