@@ -121,6 +121,23 @@ class Context {
     return S;
   }
 
+  // Multi-GPU building blocks (include/refsig_gpu.h).
+  void set_global_df(std::uint32_t n_docs_global, const std::vector<std::uint32_t>* df_global = nullptr) {
+    check(refsig_gpu_set_global_df(ctx_, df_global ? df_global->data() : nullptr, n_docs_global));
+  }
+  void set_reference_counts(const std::vector<std::uint64_t>& rowptr, const std::vector<std::uint32_t>& ids,
+                            const std::vector<std::uint32_t>& counts) {
+    if (rowptr.empty()) throw refsig::validation_error("rowptr must hold K+1 offsets");
+    check(refsig_gpu_set_reference_counts(ctx_, static_cast<std::uint32_t>(rowptr.size() - 1), rowptr.data(),
+                                          ids.data(), counts.data()));
+    K_ = static_cast<std::uint32_t>(rowptr.size() - 1);
+  }
+  void set_signatures(const std::vector<float>& S, std::uint32_t n_docs, std::uint32_t K) {
+    check(refsig_gpu_set_signatures(ctx_, n_docs, K, S.data(), 0));
+    n_docs_ = n_docs;
+    K_ = K;
+  }
+
   // One MRCS signature file image per document, 20 + 8K bytes each, back to back.
   std::vector<std::uint8_t> signature_records(std::uint64_t ref_id) {
     std::vector<std::uint8_t> r(static_cast<size_t>(n_docs_hint()) * (20u + 8u * K_));
