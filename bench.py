@@ -305,11 +305,14 @@ def run_ours(args):
     # End to end through the public API with HOST buffers: pinned tokens H2D,
     # full pipeline, candidate keys D2H into pinned memory.
     e2e_all = measure_e2e(ctx, cp, refs, tau, lo, hi, stream, dev, steps=args.steps, warmup=2)
+    modes = sorted(e2e_all)
     if dist:
-        t = torch.tensor([e2e_all["csr"]["_ms"], e2e_all["keys"]["_ms"]], dtype=torch.float64, device=dev)
+        t = torch.tensor([e2e_all[m]["_ms"] for m in modes], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_all["csr"]["_ms"], e2e_all["keys"]["_ms"] = t.tolist()
-    e2e = e2e_all["csr"]
+        for m, v in zip(modes, t.tolist()):
+            e2e_all[m]["_ms"] = v
+    main_mode = "csr16" if "csr16" in e2e_all else "csr"
+    e2e = e2e_all[main_mode]
     e2e_value = P / (e2e["_ms"] / 1e3)
 
     if rank == 0:
@@ -342,8 +345,15 @@ def run_ours(args):
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
                         "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["_ms"],
                         "note": "load_corpus(pinned host tokens) + count + set_reference_docs + sign + "
-                                "mrc_pairs_rows + get_pairs_csr (rowptr + sorted uint32 columns into pinned host "
-                                "memory); host wall clock, synchronised",
+                                "mrc_pairs_rows + " + ("get_pairs_csr16 (rowptr + sorted uint16 columns, N <= "
+                                                       "65536" if main_mode == "csr16" else
+                                                       "get_pairs_csr (rowptr + sorted uint32 columns")
+                                + ") into pinned host memory; host wall clock, synchronised",
+                        **({"csr32_variant": {"value": P / (e2e_all["csr"]["_ms"] / 1e3),
+                                              "ms_per_step": e2e_all["csr"]["_ms"],
+                                              "d2h_bytes_per_step": e2e_all["csr"]["d2h"],
+                                              "note": "same, uint32 columns (get_pairs_csr)"}}
+                           if main_mode == "csr16" else {}),
                         "keys_variant": {"value": P / (e2e_all["keys"]["_ms"] / 1e3),
                                          "ms_per_step": e2e_all["keys"]["_ms"],
                                          "d2h_bytes_per_step": e2e_all["keys"]["d2h"],
@@ -377,8 +387,8 @@ def measure_e2e(ctx, cp, refs, tau, lo, hi, stream, dev, steps, warmup):
     """Host-buffer round trip through the public API, host wall clock: pinned
     tokens -> load_corpus (H2D) -> count -> set_reference_docs -> sign ->
     mrc_pairs_rows -> the sorted pairs back in pinned host memory, as CSR
-    (rowptr + uint32 columns, `get_pairs_csr`) and, separately, as the 64-bit
-    keys."""
+    (rowptr + uint16 columns, `get_pairs_csr16`, when N <= 65536; rowptr +
+    uint32 columns, `get_pairs_csr`) and, separately, as the 64-bit keys."""
     import torch
     import paper_1810_03099_b200 as R
     tok_pin = torch.from_numpy(cp.tokens.view(np.int32)).pin_memory()
@@ -387,9 +397,11 @@ def measure_e2e(ctx, cp, refs, tau, lo, hi, stream, dev, steps, warmup):
     cap = int(n_guess * 1.1) + 1024
     keys_out = torch.empty(cap, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
     cols_out = torch.empty(cap, dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+    cols16_out = torch.empty(cap, dtype=torch.int16).pin_memory().numpy().view(np.uint16)
     rowptr_out = torch.empty(hi - lo + 1, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
     res = {}
-    for mode in ("csr", "keys"):
+    modes = ("csr16", "csr", "keys") if cp.n_docs <= 65536 else ("csr", "keys")
+    for mode in modes:
         times = []
         n = 0
         for s in range(warmup + steps):
@@ -399,7 +411,11 @@ def measure_e2e(ctx, cp, refs, tau, lo, hi, stream, dev, steps, warmup):
             ctx.count(R.WEIGHT_TFIDF)
             ctx.set_reference_docs(refs)
             ctx.sign(fetch=False)
-            if mode == "csr":
+            if mode == "csr16":
+                ctx.mrc_pairs_rows(tau, lo, hi, fetch=False)
+                _, cols = ctx.pairs_csr16(lo, hi, rowptr=rowptr_out, cols=cols16_out)
+                n = len(cols)
+            elif mode == "csr":
                 ctx.mrc_pairs_rows(tau, lo, hi, fetch=False)
                 _, cols = ctx.pairs_csr(lo, hi, rowptr=rowptr_out, cols=cols_out)
                 n = len(cols)
@@ -409,7 +425,7 @@ def measure_e2e(ctx, cp, refs, tau, lo, hi, stream, dev, steps, warmup):
             if s >= warmup:
                 times.append(t1 - t0)
         h2d = cp.tokens.nbytes + cp.doc_off.nbytes + refs.nbytes
-        d2h = n * 4 + (hi - lo + 1) * 8 if mode == "csr" else n * 8 + 8
+        d2h = {"csr16": n * 2 + (hi - lo + 1) * 8, "csr": n * 4 + (hi - lo + 1) * 8}.get(mode, n * 8 + 8)
         res[mode] = {"_ms": 1e3 * sum(times) / len(times), "h2d": int(h2d), "d2h": int(d2h)}
     return res
 

@@ -229,6 +229,11 @@ int refsig_gpu_get_pairs(refsig_gpu_ctx* ctx, uint64_t* out_pairs, uint64_t capa
 int refsig_gpu_get_pairs_csr(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_hi, uint64_t* rowptr, uint32_t* cols,
                              uint64_t capacity, uint64_t* out_count);
 
+/* The same, with 16-bit column ids (the grid's n_cols <= 65536): half the
+ * device->host bytes of get_pairs_csr; narrowed on the device. */
+int refsig_gpu_get_pairs_csr16(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_hi, uint64_t* rowptr,
+                               uint16_t* cols, uint64_t capacity, uint64_t* out_count);
+
 /* ---- device views (for frameworks / collectives; read-only) ------------------ */
 #define REFSIG_BUF_PAIRS 0      /* uint64 keys of the last pair call */
 #define REFSIG_BUF_SIGNATURES 1 /* float S[n_docs*K] */

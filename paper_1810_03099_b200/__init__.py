@@ -95,6 +95,8 @@ SIGNATURES = {
     "refsig_gpu_evaluate": ([_c.c_void_p, _c.c_uint32, _c.c_uint32, _c.c_void_p], _c.c_int),
     "refsig_gpu_get_corpus_freq": ([_c.c_void_p, _P(_c.c_uint64)], _c.c_int),
     "refsig_gpu_get_signature_records": ([_c.c_void_p, _c.c_uint64, _P(_c.c_uint8), _c.c_uint64], _c.c_int),
+    "refsig_gpu_get_pairs_csr16": ([_c.c_void_p, _c.c_uint32, _c.c_uint32, _P(_c.c_uint64), _P(_c.c_uint16),
+                                    _c.c_uint64, _P(_c.c_uint64)], _c.c_int),
     "refsig_gpu_set_global_df": ([_c.c_void_p, _P(_c.c_uint32), _c.c_uint32], _c.c_int),
     "refsig_gpu_set_reference_counts": ([_c.c_void_p, _c.c_uint32, _P(_c.c_uint64), _P(_c.c_uint32),
                                          _P(_c.c_uint32)], _c.c_int),
@@ -373,6 +375,25 @@ class Context:
             cols = np.empty(max(n.value, 1), np.uint32)
         rc = self._L.refsig_gpu_get_pairs_csr(self._h, row_lo, hi, _ptr(rowptr, ctypes.c_uint64),
                                               _ptr(cols, ctypes.c_uint32), len(cols), ctypes.byref(n))
+        self._check(rc, n.value)
+        return rowptr[: n_rows + 1], cols[: n.value]
+
+    def pairs_csr16(self, row_lo: int = 0, row_hi: int | None = None, rowptr: np.ndarray | None = None,
+                    cols: np.ndarray | None = None):
+        """pairs_csr with uint16 column ids (n_docs <= 65536): half the bytes."""
+        hi = self.n_docs if row_hi is None else row_hi
+        n_rows = hi - row_lo
+        if rowptr is None:
+            rowptr = np.empty(n_rows + 1, np.uint64)
+        n = ctypes.c_uint64()
+        if cols is None:
+            rc = self._L.refsig_gpu_get_pairs_csr16(self._h, row_lo, hi, _ptr(rowptr, ctypes.c_uint64), None, 0,
+                                                    ctypes.byref(n))
+            if rc != E_OVERFLOW:
+                self._check(rc, n.value)
+            cols = np.empty(max(n.value, 1), np.uint16)
+        rc = self._L.refsig_gpu_get_pairs_csr16(self._h, row_lo, hi, _ptr(rowptr, ctypes.c_uint64),
+                                                _ptr(cols, ctypes.c_uint16), len(cols), ctypes.byref(n))
         self._check(rc, n.value)
         return rowptr[: n_rows + 1], cols[: n.value]
 

@@ -127,6 +127,7 @@ struct refsig_gpu_ctx {
   // pair output: sorted CSR columns (cand) over rowstart; the 64-bit keys
   // (keys) are materialised only when a caller asks for them
   DevBuf bitmap, rowcnt, rowstart, cand, scan_tmp, keys;
+  DevBuf cand16;  // 16-bit column copy for get_pairs_csr16
   uint64_t cand_count = 0;
   bool have_pairs = false;  // cand/rowstart/emit_grid hold the last pair computation
   bool keys_valid = false;
@@ -1545,6 +1546,41 @@ int refsig_gpu_get_pairs_csr(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_
       Phase ph(ctx, REFSIG_PHASE_D2H);
       ck(cudaMemcpyAsync(cols, ctx->cand.as<uint32_t>() + base, 4 * m, cudaMemcpyDeviceToHost, ctx->stream),
          "D2H cols");
+    }
+    sync(ctx);
+    if (total > capacity) {
+      ctx->err = "candidate buffer overflow: " + std::to_string(total) + " pairs > capacity " + std::to_string(capacity);
+      rc2 = REFSIG_E_OVERFLOW;
+    }
+  });
+  return rc != REFSIG_OK ? rc : rc2;
+}
+
+int refsig_gpu_get_pairs_csr16(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_hi, uint64_t* rowptr,
+                               uint16_t* cols, uint64_t capacity, uint64_t* out_count) {
+  int rc2 = REFSIG_OK;
+  int rc = guard(ctx, [&] {
+    require(ctx->have_pairs && !ctx->emit_pending, "no finished pair computation to fetch");
+    require(rowptr != nullptr && out_count != nullptr, "NULL output");
+    require(capacity == 0 || cols != nullptr, "cols is NULL");
+    const PairGrid& g = ctx->emit_grid;
+    require(g.n_cols <= 65536u, "16-bit columns need n_cols <= 65536 (use get_pairs_csr)");
+    require(row_lo <= row_hi && row_hi <= g.n_rows, "bad row range");
+    const uint64_t n_rows = row_hi - row_lo;
+    ck(cudaMemcpyAsync(rowptr, ctx->rowstart.as<uint64_t>() + row_lo, 8 * (n_rows + 1), cudaMemcpyDeviceToHost,
+                       ctx->stream),
+       "D2H rowptr");
+    sync(ctx);
+    const uint64_t base = rowptr[0], total = rowptr[n_rows] - base;
+    for (uint64_t r = 0; r <= n_rows; ++r) rowptr[r] -= base;
+    *out_count = total;
+    const uint64_t m = std::min(total, capacity);
+    if (m) {
+      ctx->cand16.ensure(2 * m + 16);
+      launch_narrow_cols(ctx->cand.as<uint32_t>() + base, m, ctx->cand16.as<uint16_t>(), ctx->stream);
+      launched("narrow");
+      Phase ph(ctx, REFSIG_PHASE_D2H);
+      ck(cudaMemcpyAsync(cols, ctx->cand16.p, 2 * m, cudaMemcpyDeviceToHost, ctx->stream), "D2H cols");
     }
     sync(ctx);
     if (total > capacity) {

@@ -17,6 +17,7 @@
 //
 // MRC tile kernel: see the comment above mrc_bitmap_kernel.
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -617,7 +618,26 @@ uint64_t n_tiles(PairGrid& g, uint32_t& nbr, uint32_t& nbc) {
   return (p1 - p0) * nbc;
 }
 
+// u32 -> u16 column ids (n_cols <= 65536): two per thread per step, one
+// 32-bit store (the input may start at any element of the CSR array).
+__global__ void __launch_bounds__(256) narrow_cols_kernel(const uint32_t* __restrict__ in, uint64_t n,
+                                                          uint16_t* __restrict__ out) {
+  const uint64_t n2 = n / 2;
+  uint32_t* o32 = reinterpret_cast<uint32_t*>(out);
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n2;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    o32[i] = in[2 * i] | (in[2 * i + 1] << 16);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) out[n - 1] = static_cast<uint16_t>(in[n - 1]);
+}
+
 }  // namespace
+
+void launch_narrow_cols(const uint32_t* in, uint64_t n, uint16_t* out, cudaStream_t s) {
+  if (!n) return;
+  const uint64_t blocks = std::min<uint64_t>(ceil_div(n / 2 + 1, 256), 148ull * 16);
+  narrow_cols_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(in, n, out);
+  note_launch();
+}
 
 void launch_mrc_bitmap(const float* ST_rows, uint32_t ld_rows, const float* ST_cols, uint32_t ld_cols, uint32_t K,
                        float tau, const PairGrid& g_in, uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s) {

@@ -445,3 +445,27 @@ def test_evaluate_vs_oracle(gpu_ctx_factory, weighting):
     ref2 = oracle.evaluate(o.x, o.S, fp, 128, 384)
     assert g2["pairs"] == ref2["pairs"]
     assert abs(g2["mrc_mae"] - ref2["mrc_mae"]) <= 2e-6 + 1e-5 * abs(ref2["mrc_mae"])
+
+
+def test_pairs_csr16_matches_csr32(gpu_ctx_factory):
+    cp, cfg = corpus_c0()
+    refs = C.sample_refs(cfg["ref_seed"], cp.n_docs, cfg["K"])
+    ctx = gpu_ctx_factory()
+    gpu_pipeline(ctx, cp, refs)
+    ctx.mrc_pairs(0.9, fetch=False)
+    rp32, c32 = ctx.pairs_csr()
+    rp16, c16 = ctx.pairs_csr16()
+    assert c16.dtype == np.uint16 and np.array_equal(rp16, rp32) and np.array_equal(c16.astype(np.uint32), c32)
+    rp, c = ctx.pairs_csr16(128, 640)  # a row range, rowptr rebased to 0
+    r32, c3 = ctx.pairs_csr(128, 640)
+    assert np.array_equal(rp, r32) and np.array_equal(c.astype(np.uint32), c3)
+    # more than 65536 columns: 16-bit ids refused
+    n = 70000
+    big = gpu_ctx_factory()
+    big.load_corpus(np.arange(n, dtype=np.uint32) % 50, np.arange(n + 1, dtype=np.uint64), 50)
+    big.count(R.WEIGHT_TF)
+    big.set_reference_docs(np.arange(4, dtype=np.uint32))
+    big.sign(fetch=False)
+    big.mrc_pairs(2.0, fetch=False)
+    with pytest.raises(R.ValidationError, match="65536"):
+        big.pairs_csr16()
