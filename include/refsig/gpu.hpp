@@ -207,6 +207,22 @@ class Context {
     return r;
   }
 
+  // The same with 16-bit column ids (n_docs <= 65536): half the bytes.
+  struct PairsCsr16 {
+    std::vector<std::uint64_t> rowptr;
+    std::vector<std::uint16_t> cols;
+  };
+  PairsCsr16 pairs_csr16() {
+    PairsCsr16 r;
+    r.rowptr.resize(n_docs_hint() + 1);
+    std::uint64_t n = 0;
+    int rc = refsig_gpu_get_pairs_csr16(ctx_, 0, n_docs_hint(), r.rowptr.data(), nullptr, 0, &n);
+    if (rc != REFSIG_E_OVERFLOW) check(rc);
+    r.cols.resize(n);
+    check(refsig_gpu_get_pairs_csr16(ctx_, 0, n_docs_hint(), r.rowptr.data(), r.cols.data(), n, &n));
+    return r;
+  }
+
   std::uint32_t n_docs_hint() const { return n_docs_; }
 
  private:

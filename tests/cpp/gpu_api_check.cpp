@@ -55,6 +55,8 @@ int main() {
   auto csr = ctx.pairs_csr();
   EXPECT(csr.rowptr.size() == 4 && csr.rowptr[1] == 1 && csr.rowptr[3] == 1 && csr.cols.size() == 1 &&
          csr.cols[0] == 1);
+  auto csr16 = ctx.pairs_csr16();
+  EXPECT(csr16.rowptr == csr.rowptr && csr16.cols.size() == 1 && csr16.cols[0] == 1);
   // text front end: "abcabc" and "Abc-abc!" give the same 3-gram vector
   ctx.load_text("abcabcAbc-abc!", {0, 6, 14});
   ctx.count(Weighting::tf);
