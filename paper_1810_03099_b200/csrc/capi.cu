@@ -128,6 +128,7 @@ struct refsig_gpu_ctx {
   // (keys) are materialised only when a caller asks for them
   DevBuf bitmap, rowcnt, rowstart, cand, scan_tmp, keys;
   DevBuf cand16;  // 16-bit column copy for get_pairs_csr16
+  const uint32_t* plan_tok = nullptr;  // token pointer the plan / step graph were built with
   uint64_t cand_count = 0;
   bool have_pairs = false;  // cand/rowstart/emit_grid hold the last pair computation
   bool keys_valid = false;
@@ -456,6 +457,18 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
     max_len = std::max<uint64_t>(max_len, doc_off[d + 1] - doc_off[d]);
   }
   require(max_len < (1ull << 31), "document longer than 2^31 tokens");
+  // Same document layout as the loaded corpus (a new batch of the same shape,
+  // or the same batch re-uploaded): the work plan is a function of doc_off
+  // only, so it and the device copy of doc_off stay valid, and so does a
+  // captured step graph (it reads the token buffer, which was just rewritten).
+  if (c->loaded && c->plan_tok == c->tok && n_docs == c->n_docs && vocab == c->vocab &&
+      c->h_off.size() == static_cast<size_t>(n_docs) + 1 &&
+      std::memcmp(c->h_off.data(), doc_off, sizeof(uint64_t) * (n_docs + 1)) == 0) {
+    c->have_text = false;
+    c->counted = false;
+    reset_downstream(c);
+    return;
+  }
   c->h_off.assign(doc_off, doc_off + n_docs + 1);
   c->have_text = false;  // refsig_gpu_load_text sets it after this
   c->n_docs = n_docs;
@@ -543,6 +556,7 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
   }
   c->loaded = true;
   c->counted = false;
+  c->plan_tok = c->tok;
   ++c->load_gen;
   reset_downstream(c);
 }

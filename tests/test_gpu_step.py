@@ -68,3 +68,33 @@ def test_step_requires_collect(gpu_ctx_factory):
     with pytest.raises(R.ValidationError):
         ctx.mrc_step(refs, 0.99)
     ctx.step_result()
+
+
+def test_same_layout_reload_keeps_step_graph_but_reads_new_tokens(gpu_ctx_factory):
+    """A batch with the same doc_off reuses the work plan and the captured
+    step graph; the graph must read the newly uploaded tokens."""
+    cp, cfg = C.config_corpus("c1")
+    cp = cp.slice_docs(3000)
+    refs = C.sample_refs(0, cp.n_docs, 20)
+    rng = np.random.default_rng(3)
+    tok2 = cp.tokens.copy()
+    flip = rng.random(len(tok2)) < 0.3
+    tok2[flip] = rng.integers(0, cp.vocab, int(flip.sum()), dtype=np.uint32)
+    fresh = gpu_ctx_factory()
+    fresh.load_corpus(tok2, cp.doc_off, cp.vocab)
+    want2 = eager(fresh, refs, 0.95)
+    fresh.load_corpus(cp.tokens, cp.doc_off, cp.vocab)
+    want1 = eager(fresh, refs, 0.95)
+    assert not np.array_equal(want1, want2)
+    ctx = gpu_ctx_factory()
+    for tok, want in [(cp.tokens, want1), (tok2, want2), (cp.tokens, want1), (tok2, want2)]:
+        ctx.load_corpus(tok, cp.doc_off, cp.vocab)
+        ctx.mrc_step(refs, 0.95)
+        assert np.array_equal(ctx.step_result(fetch=True), want)
+        rowptr, ids, counts = ctx.counts()  # counted rows are the new batch's
+        assert int(rowptr[-1]) == int(fresh_counts_total(tok, cp))
+
+
+def fresh_counts_total(tok, cp):
+    import oracle
+    return len(oracle.count(tok, cp.doc_off).ids)
