@@ -305,6 +305,7 @@ def run_ours(args):
     # End to end through the public API with HOST buffers: pinned tokens H2D,
     # full pipeline, candidate keys D2H into pinned memory.
     e2e_all = measure_e2e(ctx, cp, refs, tau, lo, hi, stream, dev, steps=args.steps, warmup=2)
+    e2e_pipe = measure_e2e_pipelined(cp, refs, tau, lo, hi, dev, steps=max(args.steps, 5)) if world == 1 else None
     modes = sorted(e2e_all)
     if dist:
         t = torch.tensor([e2e_all[m]["_ms"] for m in modes], dtype=torch.float64, device=dev)
@@ -360,6 +361,12 @@ def run_ours(args):
                                           "ms_per_step": e2e_all["csr"]["_ms"],
                                           "d2h_bytes_per_step": e2e_all["csr"]["d2h"],
                                           "note": "separate calls, uint32 columns (get_pairs_csr)"},
+                        **({"pipelined_2_batches": {
+                            "value": P / (e2e_pipe["ms_per_batch"] / 1e3), "ms_per_batch": e2e_pipe["ms_per_batch"],
+                            "batches": e2e_pipe["batches"],
+                            "note": "two host threads / contexts, same per-batch calls and copies; one batch's "
+                                    "H2D overlaps the other's compute and D2H (wall clock over all batches)"}}
+                           if e2e_pipe else {}),
                         "keys_variant": {"value": P / (e2e_all["keys"]["_ms"] / 1e3),
                                          "ms_per_step": e2e_all["keys"]["_ms"],
                                          "d2h_bytes_per_step": e2e_all["keys"]["d2h"],
@@ -445,6 +452,54 @@ def measure_e2e(ctx, cp, refs, tau, lo, hi, stream, dev, steps, warmup):
                "csr": n * 4 + (hi - lo + 1) * 8, "step": n * 4 + (hi - lo + 1) * 8}.get(mode, n * 8 + 8)
         res[mode] = {"_ms": 1e3 * sum(times) / len(times), "h2d": int(h2d), "d2h": int(d2h)}
     return res
+
+
+def measure_e2e_pipelined(cp, refs, tau, lo, hi, dev, steps, warmup=2):
+    """Two batches in flight: two host threads, each with its own context (own
+    stream, pinned buffers), run the same per-batch call sequence as `e2e`
+    (H2D of the tokens, mrc_step, step_result, get_pairs_csr16 into pinned
+    memory). One batch's host->device copy overlaps the other's compute and
+    device->host copy (PCIe is full duplex). Reported beside `e2e`, not as it:
+    every batch still pays its own copies, the wall clock covers all of them."""
+    import threading
+    import torch
+    import paper_1810_03099_b200 as R
+    tok = torch.from_numpy(cp.tokens.view(np.int32))
+    work = []
+    for _ in range(2):
+        ctx = R.Context(torch.cuda.current_device())
+        tp = tok.pin_memory().numpy().view(np.uint32)
+        ctx.load_corpus(tp, cp.doc_off, cp.vocab)
+        ctx.mrc_step(refs, tau, R.WEIGHT_TFIDF, lo, hi)
+        n = ctx.step_result(fetch=False)
+        cap = int(n * 1.1) + 1024
+        work.append((ctx, tp, torch.empty(hi - lo + 1, dtype=torch.int64).pin_memory().numpy().view(np.uint64),
+                     torch.empty(cap, dtype=torch.int16).pin_memory().numpy().view(np.uint16)))
+    if cp.n_docs > 65536:
+        return None
+    start = threading.Barrier(3)
+
+    def run(ctx, tp, rowptr, cols, count):
+        for _ in range(count):
+            ctx.load_corpus(tp, cp.doc_off, cp.vocab)
+            ctx.mrc_step(refs, tau, R.WEIGHT_TFIDF, lo, hi)
+            ctx.step_result(fetch=False)
+            ctx.pairs_csr16(lo, hi, rowptr=rowptr, cols=cols)
+
+    for w in work:  # warm-up (graphs captured above; settle the pinned paths)
+        run(*w, warmup)
+    torch.cuda.synchronize(dev)
+    threads = [threading.Thread(target=lambda w=w: (start.wait(), run(*w, steps))) for w in work]
+    for t in threads:
+        t.start()
+    start.wait()
+    t0 = time.perf_counter()
+    for t in threads:
+        t.join()
+    t1 = time.perf_counter()
+    for w in work:
+        w[0].close()
+    return {"ms_per_batch": 1e3 * (t1 - t0) / (2 * steps), "batches": 2 * steps}
 
 
 def measure_evaluation(ctx, stream, dev, refs, K):
