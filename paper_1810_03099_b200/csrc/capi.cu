@@ -385,11 +385,11 @@ void prepare_bitmap(refsig_gpu_ctx* c, const PairGrid& g, bool zero) {
 }
 
 // K3: the tcgen05 kernel when K fits (3K+3 <= 128), else the CUDA-core tiles.
-// REFSIG_K3=fp32 (or 1 = v1) forces the CUDA-core kernel.
+// REFSIG_K3=fp32 forces the CUDA-core kernel.
 bool k3_use_tc(uint32_t K, float tau) {
   static const bool off = [] {
     const char* m = std::getenv("REFSIG_K3");
-    return m && (m[0] == '1' || std::strcmp(m, "fp32") == 0);
+    return m && std::strcmp(m, "fp32") == 0;
   }();
   return !off && mrc_tc_supported(K, tau);
 }

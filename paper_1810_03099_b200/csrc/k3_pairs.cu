@@ -15,7 +15,7 @@
 // output positions, so the candidate list is sorted and identical for every
 // launch configuration without a device sort.
 //
-// MRC tile kernel: see the comment above mrc_bitmap_kernel.
+// MRC tile kernel (CUDA cores): see the comment above mrc_bitmap_kernel2.
 
 #include <algorithm>
 #include <cstdlib>
@@ -58,18 +58,14 @@ __device__ __forceinline__ uint32_t col_mask(uint32_t lo, uint32_t i, const Pair
   return m;
 }
 
-// ---- K3: MRC tile kernel ---------------------------------------------------
-// Persistent CTAs walk a contiguous range of tiles; (tile, K-chunk) stages are
-// double-buffered in shared memory with cp.async (16 B chunks of the
-// transposed unit signatures ST[k][ld]). Thread (ty,tx) owns rows ty*8..+7
-// and columns tx*8..+7 of the 128x128 tile; shared memory stores each panel
-// in "split" order (columns c%8<4 in the first half) so both float4 loads of
-// a thread are bank-conflict free while its 8 columns stay contiguous. The
-// inner loop is 2+2 LDS.128 and 32 FFMA2 (fma.rn.f32x2, scalar-broadcast A)
-// per k. Epilogue: one byte per owned row (8 contiguous columns, bit c =
-// dot >= tau) -> shared memory -> each of 128 threads assembles a row's 16
-// bytes (the row's 128 bits in natural order), masks, stores 16 B and bumps
-// the row count.
+// ---- K3 on CUDA cores (K > 41; the tensor-core kernel is k3_tc.cu) ------------
+// Persistent CTAs walk a contiguous range of tiles; (tile, K-chunk) stages
+// stream through shared memory with cp.async (16 B chunks of the transposed
+// unit signatures ST[k][ld]). Thread (ty,tx) owns rows ty*8..+7 and columns
+// tx*8..+7 of the 128x128 tile; shared memory stores each panel in "split"
+// order (columns c%8<4 in the first half) so both float4 loads of a thread are
+// bank-conflict free while its 8 columns stay contiguous. The inner loop is
+// 2+2 LDS.128 and 32 FFMA2 (fma.rn.f32x2, scalar-broadcast A) per k.
 
 __device__ __forceinline__ uint32_t split_pos(uint32_t c) {  // smem slot of panel column c
   return (c & 4u) ? 64u + (c >> 3) * 4u + (c & 3u) : (c >> 3) * 4u + (c & 3u);
@@ -107,172 +103,7 @@ struct MrcArgs {
   uint32_t* rowcnt;
 };
 
-// KC > 0: every K chunk has exactly KC columns (K <= 32 with K == KC, or
-// K % 32 == 0 with KC == 32), so the k loop is fully unrolled; KC == 0 is the
-// general path.
-template <int KC>
-__global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel(MrcArgs a) {
-  extern __shared__ __align__(16) float smem[];
-  const uint32_t kcm = KC > 0 ? static_cast<uint32_t>(KC) : (a.K < kKC ? a.K : kKC);  // columns per chunk
-  const uint32_t panel = kcm * kTile;  // floats per panel stage
-  // stage st: A panel at smem + 2*st*panel, B panel right after it
-
-  const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
-  const uint32_t t_begin = static_cast<uint32_t>(a.n_tiles * blockIdx.x / gridDim.x);
-  const uint32_t t_end = static_cast<uint32_t>(a.n_tiles * (blockIdx.x + 1) / gridDim.x);
-  if (t_begin >= t_end) return;
-  const uint32_t nchunks = KC > 0 ? (a.K / KC) : (a.K + kKC - 1) / kKC;
-  const uint32_t items = (t_end - t_begin) * nchunks;
-
-  uint32_t bi, bj;
-  tile_coords(t_begin + a.g.tile0, a.nbr, a.nbc, a.g.triangle, bi, bj);
-  uint32_t li = bi, lj = bj;  // tile coords of the next item to load
-  uint32_t lchunk = 0;
-  // cp.async slots of one stage: 16-byte chunk cm = tid%32 of panel rows
-  // kr + 8u, kr = warp id (A rows first, then B rows): every slot condition
-  // is warp-uniform and the offsets are tile-invariant.
-  constexpr int kSlots = KC > 0 ? (2 * KC + 7) / 8 : 2 * kKC / 8;
-  const uint32_t cm = tid & 31, kr = tid >> 5, sp = split_pos(4 * cm);
-  auto issue = [&](uint32_t st) {
-    const uint32_t k0 = lchunk * kcm;
-    const uint32_t kc = KC > 0 ? static_cast<uint32_t>(KC) : min(kcm, a.K - k0);
-    const float* baseA = a.STr + static_cast<size_t>(k0) * a.ldr + li * kTile + 4 * cm;
-    const float* baseB = a.STc + static_cast<size_t>(k0) * a.ldc + lj * kTile + 4 * cm;
-    float* sbase = smem + 2 * st * panel + sp;
-#pragma unroll
-    for (int u = 0; u < kSlots; ++u) {
-      const uint32_t k = kr + 8 * u;
-      if (k < kcm) {
-        if (KC > 0 || k < kc) cp_async16(sbase + k * kTile, baseA + static_cast<size_t>(k) * a.ldr);
-      } else if (k < 2 * kcm) {
-        const uint32_t kk = k - kcm;
-        if (KC > 0 || kk < kc) cp_async16(sbase + panel + kk * kTile, baseB + static_cast<size_t>(kk) * a.ldc);
-      }
-    }
-    cp_async_commit();
-    if (++lchunk == nchunks) {
-      lchunk = 0;
-      if (++lj == a.nbc) {
-        ++li;
-        lj = a.g.triangle ? li : 0;
-      }
-    }
-  };
-
-  float2 acc[8][4];
-  // Tile bits are staged per row in shared memory (double-buffered) and the
-  // 128-thread store of tile t happens after the next item's barrier, so the
-  // epilogue needs no barrier of its own.
-  uint8_t* rowbytes = reinterpret_cast<uint8_t*>(smem + 6 * panel);  // [2][128][16]
-  uint32_t pend_bi = 0, pend_bj = 0, pend_buf = 0;
-  bool pending = false;
-  auto flush = [&]() {
-    if (tid < kTile) {
-      const uint32_t i = pend_bi * kTile + tid;
-      if (i < a.g.n_rows) {
-        uint4 wv = *reinterpret_cast<const uint4*>(rowbytes + pend_buf * 2048 + tid * 16);
-        const uint32_t c0 = pend_bj * kTile;
-        wv.x &= col_mask(c0, i, a.g);
-        wv.y &= col_mask(c0 + 32, i, a.g);
-        wv.z &= col_mask(c0 + 64, i, a.g);
-        wv.w &= col_mask(c0 + 96, i, a.g);
-        *reinterpret_cast<uint4*>(a.bitmap + static_cast<size_t>(i) * a.g.words_per_row + pend_bj * 4) = wv;
-        const uint32_t cnt = __popc(wv.x) + __popc(wv.y) + __popc(wv.z) + __popc(wv.w);
-        if (cnt) atomicAdd(a.rowcnt + i, cnt);
-      }
-    }
-  };
-  // 3-stage ring: the data of item it+2 streams in while item it computes;
-  // one barrier per item (it also frees the stage item it-1 used).
-  issue(0);
-  if (items > 1) issue(1);
-  uint32_t tiles_done = 0;
-  uint32_t st = 0, ist = 2, chunk = 0;  // stage of item it, stage for item it+2, chunk of item it
-  for (uint32_t it = 0; it < items; ++it) {
-    if (it + 1 < items)
-      cp_async_wait<1>();
-    else
-      cp_async_wait<0>();
-    __syncthreads();
-    if (it + 2 < items) {
-      issue(ist);
-      ist = ist == 2 ? 0 : ist + 1;
-    }
-    if (pending) {
-      flush();
-      pending = false;
-    }
-    const float* A = smem + 2 * st * panel;
-    const float* B = A + panel;
-    // one k step: 2+2 LDS.128, 32 FFMA2; `first` starts the dot at -tau (the
-    // match bit is then the inverted sign bit) without separate moves
-    auto kstep = [&](uint32_t k, bool first) {
-      const float4 a0 = *reinterpret_cast<const float4*>(A + k * kTile + ty * 4);
-      const float4 a1 = *reinterpret_cast<const float4*>(A + k * kTile + 64 + ty * 4);
-      const float4 b0 = *reinterpret_cast<const float4*>(B + k * kTile + tx * 4);
-      const float4 b1 = *reinterpret_cast<const float4*>(B + k * kTile + 64 + tx * 4);
-      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
-                            make_float2(b1.z, b1.w)};
-      const float2 nt = make_float2(-a.tau, -a.tau);
-#pragma unroll
-      for (int r = 0; r < 8; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = ffma2(av[r], bv[c], first ? nt : acc[r][c]);
-    };
-    if constexpr (KC > 0) {
-      if (KC == static_cast<int>(kKC) && chunk != 0) {  // later chunks of K % 32 == 0
-#pragma unroll
-        for (uint32_t k = 0; k < KC; ++k) kstep(k, false);
-      } else {
-        kstep(0, true);
-#pragma unroll
-        for (uint32_t k = 1; k < KC; ++k) kstep(k, false);
-      }
-    } else {
-      const uint32_t kc = min(kcm, a.K - chunk * kcm);
-      uint32_t k = 0;
-      if (chunk == 0) kstep(k++, true);
-#pragma unroll 4
-      for (; k < kc; ++k) kstep(k, false);
-    }
-    st = st == 2 ? 0 : st + 1;
-    if (++chunk == nchunks) {
-      chunk = 0;
-      // Row ty*8+r, columns tx*8..+7 -> byte tx of the tile row (natural
-      // column order). acc = dot - tau, so bit = NOT sign(acc) (acc is never
-      // -0: it starts at -tau and adds non-negative products); funnel shifts
-      // collect the sign bits.
-      const uint32_t buf = tiles_done & 1u;
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        uint32_t byte = 0;
-#pragma unroll
-        for (int c = 3; c >= 0; --c) {
-          byte = __funnelshift_l(__float_as_uint(acc[r][c].y), byte, 1);
-          byte = __funnelshift_l(__float_as_uint(acc[r][c].x), byte, 1);
-        }
-        rowbytes[buf * 2048 + (ty * 8 + r) * 16 + tx] = static_cast<uint8_t>(~byte);
-      }
-      pending = true;
-      pend_bi = bi;
-      pend_bj = bj;
-      pend_buf = buf;
-      ++tiles_done;
-      if (++bj == a.nbc) {
-        ++bi;
-        bj = a.g.triangle ? bi : 0;
-      }
-    }
-  }
-  __syncthreads();
-  if (pending) flush();
-}
-
-// ---- K3 v2: mbarrier ring, warp-local epilogue ------------------------------
-// Same tiles, thread tiling, shared-memory layout and FFMA2 inner loop as
-// mrc_bitmap_kernel, but no CTA-wide barrier in the main loop: a 4-stage ring
+// mbarrier ring, warp-local epilogue: no CTA-wide barrier in the main loop: a 4-stage ring
 // of (tile, K-chunk) items where each stage has a "full" mbarrier (256
 // arrivals: every thread's cp.async.mbarrier.arrive) and an "empty" mbarrier
 // (8 arrivals: one per warp after its last read). A stage is refilled two
@@ -646,61 +477,32 @@ void launch_mrc_bitmap(const float* ST_rows, uint32_t ld_rows, const float* ST_c
   const uint64_t t = n_tiles(g, nbr, nbc);
   if (t == 0 || K == 0) return;
   const uint32_t kc = K < kKC ? K : kKC;
-  const size_t smem = (6ull * kc * kTile) * sizeof(float) + 2 * 2048;
-  static bool configured = false;
-  if (!configured) {
-    const int mx = 6 * kKC * kTile * 4 + 4096;
-    cudaFuncSetAttribute(mrc_bitmap_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(mrc_bitmap_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(mrc_bitmap_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(mrc_bitmap_kernel<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(mrc_bitmap_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    configured = true;
-  }
   uint64_t grid = static_cast<uint64_t>(sms()) * 2;
   if (grid > t) grid = t;
   MrcArgs a{ST_rows, ST_cols, ld_rows, ld_cols, K, tau, g, nbr, nbc, t, bitmap, rowcnt};
   const dim3 gr(static_cast<unsigned>(grid));
-  static const bool v2 = [] {
-    const char* m = std::getenv("REFSIG_K3");
-    return !(m && m[0] == '1');
-  }();
-  if (v2) {
-    const int kt = K == 20 ? 20 : K == 10 ? 10 : K == 16 ? 16 : K % 32 == 0 ? 32 : 0;
-    const size_t smem2 = (2ull * mrc2_stages(kt) * kc * kTile) * sizeof(float);
-    static bool configured2 = false;
-    if (!configured2) {
-      const int mx = 8 * kKC * kTile * 4;
-      cudaFuncSetAttribute(mrc_bitmap_kernel2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      cudaFuncSetAttribute(mrc_bitmap_kernel2<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      cudaFuncSetAttribute(mrc_bitmap_kernel2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      cudaFuncSetAttribute(mrc_bitmap_kernel2<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      cudaFuncSetAttribute(mrc_bitmap_kernel2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-      configured2 = true;
-    }
-    if (K == 20)
-      mrc_bitmap_kernel2<20><<<gr, 256, smem2, s>>>(a);
-    else if (K == 10)
-      mrc_bitmap_kernel2<10><<<gr, 256, smem2, s>>>(a);
-    else if (K == 16)
-      mrc_bitmap_kernel2<16><<<gr, 256, smem2, s>>>(a);
-    else if (K % 32 == 0)
-      mrc_bitmap_kernel2<32><<<gr, 256, smem2, s>>>(a);
-    else
-      mrc_bitmap_kernel2<0><<<gr, 256, smem2, s>>>(a);
-    note_launch();
-    return;
+  const int kt = K == 20 ? 20 : K == 10 ? 10 : K == 16 ? 16 : K % 32 == 0 ? 32 : 0;
+  const size_t smem2 = (2ull * mrc2_stages(kt) * kc * kTile) * sizeof(float);
+  static bool configured2 = false;
+  if (!configured2) {
+    const int mx = 8 * kKC * kTile * 4;
+    cudaFuncSetAttribute(mrc_bitmap_kernel2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(mrc_bitmap_kernel2<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(mrc_bitmap_kernel2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(mrc_bitmap_kernel2<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(mrc_bitmap_kernel2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    configured2 = true;
   }
   if (K == 20)
-    mrc_bitmap_kernel<20><<<gr, 256, smem, s>>>(a);
+    mrc_bitmap_kernel2<20><<<gr, 256, smem2, s>>>(a);
   else if (K == 10)
-    mrc_bitmap_kernel<10><<<gr, 256, smem, s>>>(a);
+    mrc_bitmap_kernel2<10><<<gr, 256, smem2, s>>>(a);
   else if (K == 16)
-    mrc_bitmap_kernel<16><<<gr, 256, smem, s>>>(a);
+    mrc_bitmap_kernel2<16><<<gr, 256, smem2, s>>>(a);
   else if (K % 32 == 0)
-    mrc_bitmap_kernel<32><<<gr, 256, smem, s>>>(a);
+    mrc_bitmap_kernel2<32><<<gr, 256, smem2, s>>>(a);
   else
-    mrc_bitmap_kernel<0><<<gr, 256, smem, s>>>(a);
+    mrc_bitmap_kernel2<0><<<gr, 256, smem2, s>>>(a);
   note_launch();
 }
 
