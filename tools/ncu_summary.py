@@ -63,8 +63,21 @@ def launches(path, tag):
              "| kernel | launches | mean us | total us | share |", "|---|---:|---:|---:|---:|"]
     for k, v in sorted(by.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"| `{k}` | {len(v)} | {sum(v) / len(v):.1f} | {sum(v):.1f} | {sum(v) / total:.1%} |")
+    # one MRC step: every distinct step kernel once (mean of its launches)
+    step = {k: sum(v) / len(v) for k, v in by.items() if any(f in k for f in STEP_KERNELS)}
+    st = sum(step.values())
+    lines += ["", f"## One MRC step (configs[1]): {len(step)} kernels, {st:.1f} us serialised", "",
+              "Each step kernel's mean launch time and its share of the serialised step (the K1 classes run "
+              "concurrently on side streams in the real step, so their share is an upper bound).", "",
+              "| kernel | mean us | share of step |", "|---|---:|---:|"]
+    for k, v in sorted(step.items(), key=lambda kv: -kv[1]):
+        lines.append(f"| `{k}` | {v:.1f} | {v / st:.1%} |")
     open(os.path.join(PROF, f"ncu_launches_{tag}.md"), "w").write("\n".join(lines) + "\n")
 
+
+STEP_KERNELS = ["count_warp_kernel", "group_sort_kernel", "count_large_kernel", "idf_kernel", "ref_mark_kernel",
+                "ref_assign_kernel", "ref_fill_kernel", "sign_kernel", "sign_col_kernel", "tc_forms_kernel",
+                "mrc_tc_kernel", "mrc_bitmap_kernel2", "scan_small_kernel", "emit_kernel"]
 
 WANT = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "dram read"),
         ("dram__bytes_write.sum", "dram write"), ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM %"),
@@ -93,7 +106,7 @@ def full(path, tag):
              "Captured with `--set full --clock-control none --import-source on`; one launch per kernel of "
              "tools/prof_pipeline.py --steps 1 (configs[1]: the MRC step). DRAM bytes are cold-cache (ncu flushes "
              "caches between replays).", ""]
-    traffic = {}
+    per_kernel = collections.defaultdict(list)  # kernel name -> [bytes per launch]
     for r in rows[2:]:
         k = short(r[idx["Kernel Name"]])
         lines.append(f"## `{k}`")
@@ -107,9 +120,13 @@ def full(path, tag):
         lines.append("")
         rd = to_bytes(r[idx["dram__bytes_read.sum"]], units[idx["dram__bytes_read.sum"]])
         wr = to_bytes(r[idx["dram__bytes_write.sum"]], units[idx["dram__bytes_write.sum"]])
+        per_kernel[k].append(rd + wr)
+    # per step: each distinct kernel of a group once (mean over its captured launches)
+    traffic = {}
+    for k, v in per_kernel.items():
         for key, frags in ROOF_KERNELS.items():
             if any(f in k for f in frags) and not (key == "simhash" and "text_" in k):
-                traffic[key] = traffic.get(key, 0.0) + rd + wr
+                traffic[key] = traffic.get(key, 0.0) + sum(v) / len(v)
     open(os.path.join(PROF, f"ncu_full_{tag}.md"), "w").write("\n".join(lines) + "\n")
     json.dump({k: v for k, v in traffic.items()}, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
 
