@@ -98,3 +98,17 @@ def test_same_layout_reload_keeps_step_graph_but_reads_new_tokens(gpu_ctx_factor
 def fresh_counts_total(tok, cp):
     import oracle
     return len(oracle.count(tok, cp.doc_off).ids)
+
+
+@pytest.mark.parametrize("K", [10, 41, 64])
+def test_step_tensor_core_and_cuda_core_k3(gpu_ctx_factory, K):
+    """The captured step with K3 on tcgen05 (K <= 41) and on CUDA cores (K = 64)."""
+    cp, cfg = C.config_corpus("c1")
+    cp = cp.slice_docs(2500)
+    refs = C.sample_refs(2, cp.n_docs, K)
+    ctx = gpu_ctx_factory()
+    ctx.load_corpus(cp.tokens, cp.doc_off, cp.vocab)
+    want = eager(ctx, refs, 0.9)
+    for _ in range(3):
+        ctx.mrc_step(refs, 0.9)
+        assert np.array_equal(ctx.step_result(fetch=True), want)
