@@ -301,6 +301,7 @@ def run_ours(args):
     rivals = measure_rivals(ctx, stream, flush, dev, thr, reps=max(5, args.steps))
     text_fe = measure_text_front_end(cp, stream, dev, reps=max(3, args.steps // 2)) if world == 1 else None
     evaluation = measure_evaluation(ctx, stream, dev, refs, K) if world == 1 else None
+    exact = measure_exact(ctx, stream, dev, thr, refs) if world == 1 else None
 
     # End to end through the public API with HOST buffers: pinned tokens H2D,
     # full pipeline, candidate keys D2H into pinned memory.
@@ -328,6 +329,17 @@ def run_ours(args):
             roof["text_front_end"] = text_fe
         if evaluation:
             roof["evaluation"] = evaluation
+        if exact:
+            fma_peak = n_sm * 128 * clock_mhz * 1e6 / 1e12  # 1e12 FP32 multiply-adds/s
+            ach = exact["useful_macs"] / (exact["ms"] / 1e3) / 1e12
+            roof["exact"] = {"bound": "fp32-fma", "achieved": ach, "peak": fma_peak, "unit": "TMAC/s",
+                             "frac": ach / fma_peak, "ms_per_launch": exact["ms"],
+                             "doc_pairs_per_sec": P / (exact["ms"] / 1e3), "candidates": exact["candidates"],
+                             "useful_macs": exact["useful_macs"],
+                             "note": "K5 exact cosine over all pairs at tau_cos (SURVEY §8d: useful MACs = "
+                                     "sum_t df_t(df_t-1)/2 over the achieved time; the Cauchy-Schwarz bound "
+                                     "skips most head dots, so the kernel does fewer than these)",
+                             "peak_source": f"{n_sm} SMs x 128 FFMA/clk x {clock_mhz:.0f} MHz"}
         traffic = load_traffic()
         for k, r in roof.items():
             r["traffic"] = traffic.get(k)
@@ -584,6 +596,26 @@ def measure_rivals(ctx, stream, flush, dev, thr, reps):
     per = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in ph.items()}
     return {"simhash_ms": per["simhash"], "hamming_tiles_ms": per["pair_tiles"],
             "hamming_emit_ms": per["pair_emit"], "hamming_pairs": int(n_ham)}
+
+
+def measure_exact(ctx, stream, dev, thr, refs):
+    """K5: the exact all-pairs cosine verifier (A12) at tau_cos, one call after
+    a warm-up (host wall clock; the call synchronises)."""
+    import torch
+    import paper_1810_03099_b200 as R
+    with torch.cuda.stream(stream):
+        ctx.count(R.WEIGHT_TFIDF)
+        ctx.exact_pairs(thr["tau_cos"], fetch=False)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        n = ctx.exact_pairs(thr["tau_cos"], fetch=False)
+        t = time.perf_counter() - t0
+        df, _ = ctx.df()
+        ctx.set_reference_docs(refs)  # leave the context as the step left it
+        ctx.sign(fetch=False)
+    d = df.astype(np.float64)
+    macs = float(np.sum(d * (d - 1) / 2))
+    return {"ms": t * 1e3, "candidates": int(n), "useful_macs": macs}
 
 
 def rival_rooflines(rv, N, pairs, cp, peaks, peaks_src, n_sm, clock_mhz):
