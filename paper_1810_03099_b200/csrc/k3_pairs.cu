@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
                                                    const uint32_t* __restrict__ rowcnt,
                                                    const uint64_t* __restrict__ rowstart, uint32_t* __restrict__ out,
                                                    uint64_t capacity) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const uint32_t i = g.row_begin + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // one row per warp
   if (i >= g.row_end) return;
@@ -529,7 +530,8 @@ void launch_emit_pairs(const uint32_t* bitmap, const PairGrid& g, const uint32_t
                        uint32_t* out, uint64_t capacity, cudaStream_t s) {
   if (g.row_end <= g.row_begin) return;
   const uint64_t blocks = ceil_div(g.row_end - g.row_begin, 8);  // one row per warp
-  emit_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(bitmap, g, rowcnt, rowstart, out, capacity);
+  launch_pdl(emit_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, s, bitmap, g, rowcnt, rowstart, out,
+             capacity);
   note_launch();
 }
 

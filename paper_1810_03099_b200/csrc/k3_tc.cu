@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
+  pdl_wait();  // setup above overlaps the operand-forms kernel's tail
 
   if (warp == 0) {
     if (lane == 0 && n_it) {  // producer
@@ -583,14 +584,14 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
   }
 #endif
   switch (a.KP / 16) {
-    case 1: mrc_tc_kernel<1><<<grid, kTcThreads, smem, s>>>(a); break;
-    case 2: mrc_tc_kernel<2><<<grid, kTcThreads, smem, s>>>(a); break;
-    case 3: mrc_tc_kernel<3><<<grid, kTcThreads, smem, s>>>(a); break;
-    case 4: mrc_tc_kernel<4><<<grid, kTcThreads, smem, s>>>(a); break;
-    case 5: mrc_tc_kernel<5><<<grid, kTcThreads, smem, s>>>(a); break;
-    case 6: mrc_tc_kernel<6><<<grid, kTcThreads, smem, s>>>(a); break;
-    case 7: mrc_tc_kernel<7><<<grid, kTcThreads, smem, s>>>(a); break;
-    default: mrc_tc_kernel<8><<<grid, kTcThreads, smem, s>>>(a); break;
+    case 1: launch_pdl(mrc_tc_kernel<1>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
+    case 2: launch_pdl(mrc_tc_kernel<2>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
+    case 3: launch_pdl(mrc_tc_kernel<3>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
+    case 4: launch_pdl(mrc_tc_kernel<4>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
+    case 5: launch_pdl(mrc_tc_kernel<5>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
+    case 6: launch_pdl(mrc_tc_kernel<6>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
+    case 7: launch_pdl(mrc_tc_kernel<7>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
+    default: launch_pdl(mrc_tc_kernel<8>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
   }
 #ifdef REFSIG_TC_TRACE
   if (dbg & 8) {

@@ -113,6 +113,7 @@ __device__ __forceinline__ uint4 load4(const uint32_t* __restrict__ in, uint32_t
 
 __global__ void __launch_bounds__(kSmallThreads) scan_small_kernel(const uint32_t* __restrict__ in, uint64_t n,
                                                                    uint64_t* __restrict__ out) {
+  pdl_wait();
   __shared__ uint64_t sh[33];
   const uint32_t nn = static_cast<uint32_t>(n);
   const uint32_t t0 = blockIdx.x * kSmallTile;
@@ -158,7 +159,8 @@ void launch_exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_
     return;
   }
   if (n <= kSmallScan) {
-    scan_small_kernel<<<static_cast<unsigned>(ceil_div(n, kSmallTile)), kSmallThreads, 0, s>>>(in, n, out);
+    launch_pdl(scan_small_kernel, dim3(static_cast<unsigned>(ceil_div(n, kSmallTile))), dim3(kSmallThreads), 0, s, in,
+               n, out);
     note_launch();
     return;
   }
