@@ -104,6 +104,7 @@ struct refsig_gpu_ctx {
   const uint32_t* plan_list(int k) const { return plan.as<uint32_t>() + plan_off[k]; }
   DevBuf long_off, long_scratch;
   uint32_t n_sign_long = 0;  // order[0, n_sign_long): > kSignLongTokens tokens, one CTA each in K2/K4a
+  uint32_t n_sign_half = 0;  // order[n_sign_half, N): <= kSignHalfTokens tokens, two per warp in K2
 
   // K1
   bool counted = false;
@@ -544,6 +545,8 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
   }
   c->n_sign_long = 0;
   while (c->n_sign_long < n_docs && len(order[c->n_sign_long]) > kSignLongTokens) ++c->n_sign_long;
+  c->n_sign_half = c->n_sign_long;
+  while (c->n_sign_half < n_docs && len(order[c->n_sign_half]) > kSignHalfTokens) ++c->n_sign_half;
   c->plan.ensure(list_bytes);
   ck(cudaMemcpyAsync(c->doc_off.p, c->h_plan, off_bytes, cudaMemcpyHostToDevice, c->stream), "H2D doc_off");
   ck(cudaMemcpyAsync(c->plan.p, lists, list_bytes, cudaMemcpyHostToDevice, c->stream), "H2D plan");
@@ -1008,6 +1011,7 @@ static void do_sign(refsig_gpu_ctx* ctx) {
   if (ctx->db) ck(cudaStreamSynchronize(ctx->db->stream), "sync database");
   SignArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->info.as<TermInfo>(),
              refc->R.as<float>(), N, K, refc->Kp, ctx->plan_list(refsig_gpu_ctx::kPlanOrder), ctx->n_sign_long,
+             ctx->n_sign_half,
              ctx->S.as<float>(), ctx->ST.as<float>(), ld, ctx->inv_norm.as<float>()};
   {
     Phase ph(ctx, REFSIG_PHASE_SIGN);

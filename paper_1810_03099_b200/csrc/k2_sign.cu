@@ -236,6 +236,106 @@ __device__ __forceinline__ void sign_transpose_sum(const float (&acc)[KW], uint3
   __syncwarp();
 }
 
+// Short documents (<= kSignHalfTokens tokens, the tail of the LPT order): two
+// per warp, one per 16-lane half. Same arithmetic as the warp path per
+// half (64 nonzeros per step, a per-half hit queue, lane-per-hit
+// accumulation, a 16-row transpose-sum in lane order), but the per-document
+// fixed cost (transpose, norms, S/ST epilogue) is shared by two documents.
+// The signature-norm sum keeps the warp path's order exactly (column
+// squares, then the xor butterfly: the 16-lane halves hold columns k and
+// k+16, whose sum is the warp path's first butterfly level), so ST equals
+// what refsig_gpu_set_signatures rebuilds from S.
+template <int KW>
+__device__ __forceinline__ void sign_half_docs(const SignArgs& a, uint32_t q, uint32_t lane, float* tw) {
+  static_assert(KW <= 32, "half-warp path: KW <= 32");
+  const uint32_t h = lane >> 4, hl = lane & 15;
+  const bool has = q < a.n_docs;
+  const uint32_t d = has ? a.order[q] : 0u;
+  const uint2* __restrict__ e = a.ent + a.doc_off[d];
+  const uint32_t n = has ? a.nnz[d] : 0u;
+  const uint32_t nmax = max(n, __shfl_xor_sync(0xffffffffu, n, 16));
+  int2* qw = reinterpret_cast<int2*>(tw) + h * 64;
+  const uint32_t lt = (1u << hl) - 1u;
+  float acc[KW];
+#pragma unroll
+  for (int k = 0; k < KW; ++k) acc[k] = 0.0f;
+  float sq = 0.0f;
+  for (uint32_t c = 0; c < nmax; c += 64) {
+    uint2 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = c + 16u * u + hl;
+      x[u] = i < n ? __ldg(e + i) : make_uint2(0u, 0u);
+    }
+    TermInfo ti[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) ti[u] = (c + 16u * u + hl < n) ? a.info[x[u].x] : TermInfo{0.0f, -1};
+    uint32_t qn = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float w = static_cast<float>(x[u].y) * ti[u].idf;
+      sq = fmaf(w, w, sq);
+      const uint32_t mine = (__ballot_sync(0xffffffffu, ti[u].ref_row >= 0) >> (16 * h)) & 0xffffu;
+      if (ti[u].ref_row >= 0) qw[qn + __popc(mine & lt)] = make_int2(ti[u].ref_row, __float_as_int(w));
+      qn += __popc(mine);
+    }
+    __syncwarp();
+    const uint32_t qmax = max(qn, __shfl_xor_sync(0xffffffffu, qn, 16));
+    for (uint32_t hh = hl; hh < qmax; hh += 16) {
+      if (hh < qn) {
+        const int2 hv = qw[hh];
+        const float w = __int_as_float(hv.y);
+        const float4* __restrict__ r4 = reinterpret_cast<const float4*>(a.R + static_cast<size_t>(hv.x) * a.Kp);
+#pragma unroll
+        for (int j = 0; j < KW / 4; ++j) {
+          const float4 r = __ldg(r4 + j);
+          acc[4 * j + 0] = fmaf(w, r.x, acc[4 * j + 0]);
+          acc[4 * j + 1] = fmaf(w, r.y, acc[4 * j + 1]);
+          acc[4 * j + 2] = fmaf(w, r.z, acc[4 * j + 2]);
+          acc[4 * j + 3] = fmaf(w, r.w, acc[4 * j + 3]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // transpose-sum: half h's 16 KW-vectors at tw[h][16][KW+1]; lane hl sums
+  // columns hl and hl+16 over the half's 16 rows in lane order
+  float* th = tw + h * 16 * (KW + 1);
+#pragma unroll
+  for (int k = 0; k < KW; ++k) th[hl * (KW + 1) + k] = acc[k];
+  __syncwarp();
+  float col0 = 0.0f, col1 = 0.0f;
+  if (hl < static_cast<uint32_t>(KW)) {
+#pragma unroll 8
+    for (int l = 0; l < 16; ++l) col0 += th[l * (KW + 1) + hl];
+  }
+  if (hl + 16 < static_cast<uint32_t>(KW)) {
+#pragma unroll 8
+    for (int l = 0; l < 16; ++l) col1 += th[l * (KW + 1) + hl + 16];
+  }
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  const float inv = sq > 0.0f ? 1.0f / sqrtf(sq) : 0.0f;
+  const float v0 = fminf(col0 * inv, 1.0f), v1 = fminf(col1 * inv, 1.0f);  // ngram.hpp:201 clamp
+  const bool k0ok = hl < a.K, k1ok = hl + 16 < a.K;
+  float ss = (k0ok ? v0 * v0 : 0.0f) + (k1ok ? v1 * v1 : 0.0f);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float inv_s = ss > 0.0f ? 1.0f / sqrtf(ss) : 0.0f;  // SPEC.md:372 all-zero -> 0
+  if (has) {
+    if (hl == 0) a.inv_norm[d] = inv;
+    if (k0ok) {
+      a.S[static_cast<size_t>(d) * a.K + hl] = v0;
+      a.ST[static_cast<size_t>(hl) * a.ld + d] = v0 * inv_s;
+    }
+    if (k1ok) {
+      a.S[static_cast<size_t>(d) * a.K + hl + 16] = v1;
+      a.ST[static_cast<size_t>(hl + 16) * a.ld + d] = v1 * inv_s;
+    }
+  }
+  __syncwarp();
+}
+
 template <int KW>
 __global__ void __launch_bounds__(256, KW <= 24 ? 4 : (KW <= 32 ? 3 : 2)) sign_kernel(SignArgs a) {
   constexpr int CPL = (KW + 31) / 32;  // columns per lane
@@ -247,12 +347,20 @@ __global__ void __launch_bounds__(256, KW <= 24 ? 4 : (KW <= 32 ? 3 : 2)) sign_k
   float* tw = tsm_dyn + wid * TW;
   int2* qw = reinterpret_cast<int2*>(tw);
   const bool cta = blockIdx.x < a.n_long;  // one long document per CTA
+  {
+    const uint32_t warp_blocks = static_cast<uint32_t>(ceil_div(a.n_half - a.n_long, kSignWarps));
+    if (blockIdx.x >= a.n_long + warp_blocks) {  // two short documents per warp
+      const uint32_t pair = (blockIdx.x - a.n_long - warp_blocks) * kSignWarps + wid;
+      sign_half_docs<KW>(a, a.n_half + 2 * pair + (lane >> 4), lane, tw);
+      return;
+    }
+  }
   uint32_t q;
   if (cta) {
     q = blockIdx.x;
   } else {
     q = a.n_long + (blockIdx.x - a.n_long) * kSignWarps + wid;
-    if (q >= a.n_docs) return;
+    if (q >= a.n_half) return;
   }
   const uint32_t d = a.order[q];
   const uint2* __restrict__ e = a.ent + a.doc_off[d];
@@ -488,6 +596,9 @@ void launch_sign_kw(const SignArgs& a, unsigned g, cudaStream_t s) {
 void launch_sign(const SignArgs& a, cudaStream_t s) {
   if (a.n_docs == 0) return;
   const unsigned g = static_cast<unsigned>(a.n_long + ceil_div(a.n_docs - a.n_long, kSignWarps));
+  // K <= 32: documents [n_half, n_docs) of the order go two per warp
+  const unsigned g_half = static_cast<unsigned>(a.n_long + ceil_div(a.n_half - a.n_long, kSignWarps) +
+                                                ceil_div(a.n_docs - a.n_half, 2 * kSignWarps));
   if (a.K > 32) {  // column-owner variant, Kp = roundup(K, 32)
     switch (a.Kp / 32) {
       case 2: sign_col_kernel<2><<<g, 32 * kSignWarps, 0, s>>>(a); break;
@@ -501,14 +612,14 @@ void launch_sign(const SignArgs& a, cudaStream_t s) {
   // lane-per-hit slab width: K rounded up to 4
   const uint32_t kw = (a.K + 3) & ~3u;
   switch (kw) {
-    case 4: launch_sign_kw<4>(a, g, s); break;
-    case 8: launch_sign_kw<8>(a, g, s); break;
-    case 12: launch_sign_kw<12>(a, g, s); break;
-    case 16: launch_sign_kw<16>(a, g, s); break;
-    case 20: launch_sign_kw<20>(a, g, s); break;
-    case 24: launch_sign_kw<24>(a, g, s); break;
-    case 28: launch_sign_kw<28>(a, g, s); break;
-    default: launch_sign_kw<32>(a, g, s); break;
+    case 4: launch_sign_kw<4>(a, g_half, s); break;
+    case 8: launch_sign_kw<8>(a, g_half, s); break;
+    case 12: launch_sign_kw<12>(a, g_half, s); break;
+    case 16: launch_sign_kw<16>(a, g_half, s); break;
+    case 20: launch_sign_kw<20>(a, g_half, s); break;
+    case 24: launch_sign_kw<24>(a, g_half, s); break;
+    case 28: launch_sign_kw<28>(a, g_half, s); break;
+    default: launch_sign_kw<32>(a, g_half, s); break;
   }
   note_launch();
 }

@@ -115,12 +115,14 @@ struct SignArgs {
   uint32_t Kp;           // row stride of R
   const uint32_t* order;  // docs by decreasing length; the first n_long get a CTA each (k2_sign.cu)
   uint32_t n_long;
+  uint32_t n_half;         // K <= 32: order[n_half..) (<= kSignHalfTokens tokens) go two per warp
   float* S;         // [n_docs*K] raw cosines, row-major (API output)
   float* ST;        // [K][ld] unit-normalised signatures, transposed (K3 operand; 0 if all-zero)
   uint32_t ld;      // leading dimension of ST (n_docs rounded up to 128; pad columns zero)
   float* inv_norm;  // [n_docs] 1/||w_d||
 };
 constexpr uint32_t kSignLongTokens = 2048;  // K2: longer documents get a CTA
+constexpr uint32_t kSignHalfTokens = 1024;  // K2 (K <= 32): shorter documents go two per warp (768-1024 best)
 constexpr uint32_t kMaxRefs = 256;          // K limit (K2 keeps a signature row in registers)
 void launch_sign(const SignArgs& a, cudaStream_t s);
 
