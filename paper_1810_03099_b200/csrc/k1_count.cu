@@ -220,14 +220,17 @@ __device__ __forceinline__ uint32_t rle_regs(const uint32_t (&v)[IPT], uint32_t 
   return total;
 }
 
-__device__ __forceinline__ uint32_t load_key(const CountArgs& a, uint64_t b, uint32_t i, uint32_t len) {
-  if (i >= len) return kInf;
-  uint32_t v = __ldg(a.tokens + b + i);
-  if (v >= a.vocab) {
-    atomicOr(a.err, 1u);
-    v = a.vocab - 1;
-  }
-  return v;
+// Branch-free key load: out-of-range ids are clamped (the error flag is
+// raised once per warp after the sort, see flag_bad), padding is kInf.
+__device__ __forceinline__ uint32_t load_key(const CountArgs& a, uint64_t b, uint32_t i, uint32_t len,
+                                             uint32_t& bad) {
+  const bool in = i < len;
+  const uint32_t v = in ? __ldg(a.tokens + b + i) : 0u;
+  bad |= static_cast<uint32_t>(v >= a.vocab);
+  return in ? min(v, a.vocab - 1) : kInf;
+}
+__device__ __forceinline__ void flag_bad(const CountArgs& a, uint32_t bad) {
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.err, 1u);
 }
 
 // One warp per document of up to P = 32*IPT tokens (IPT 2 / 8 / 16). One
@@ -244,10 +247,11 @@ __global__ void __launch_bounds__(256, IPT <= 8 ? 6 : 4) count_warp_kernel(Count
   const uint32_t d = docs[q];
   const uint64_t b = a.doc_off[d];
   const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
-  uint32_t v[IPT];
+  uint32_t v[IPT], bad = 0;
 #pragma unroll
-  for (int k = 0; k < IPT; ++k) v[k] = load_key(a, b, k * 32 + lane, len);  // coalesced; any order sorts
+  for (int k = 0; k < IPT; ++k) v[k] = load_key(a, b, k * 32 + lane, len, bad);  // coalesced; any order sorts
   bitonic_regs<IPT>(v, lane);
+  flag_bad(a, bad);
   const uint32_t n = rle_regs<IPT, 1>(v, lane, len, a.ent + b, a, nullptr);
   if (lane == 0) a.nnz[d] = n;
 }
@@ -283,10 +287,11 @@ __global__ void __launch_bounds__(32 * W) group_sort_kernel(CountArgs a, const u
   const uint32_t d = docs[blockIdx.x];
   const uint64_t b = a.doc_off[d];
   const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
-  uint32_t v[IPT];
+  uint32_t v[IPT], bad = 0;
 #pragma unroll
-  for (int k = 0; k < IPT; ++k) v[k] = load_key(a, b, k * T + t, len);  // coalesced; any order sorts
+  for (int k = 0; k < IPT; ++k) v[k] = load_key(a, b, k * T + t, len, bad);  // coalesced; any order sorts
   gbitonic_sort<IPT, T>(v, t, sm);
+  flag_bad(a, bad);
   const uint32_t n = rle_regs<IPT, W>(v, t, len, a.ent + b, a, rle_sm);
   if (t == 0) a.nnz[d] = n;
 }
@@ -354,7 +359,9 @@ __global__ void __launch_bounds__(1024) count_large_kernel(CountArgs a, const ui
     const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
     const uint32_t P = next_pow2(len);
     uint32_t* s = scratch + scratch_off[q];
-    for (uint32_t i = threadIdx.x; i < P; i += 1024) s[i] = load_key(a, b, i, len);
+    uint32_t bad = 0;
+    for (uint32_t i = threadIdx.x; i < P; i += 1024) s[i] = load_key(a, b, i, len, bad);
+    flag_bad(a, bad);  // P >= 16384: every thread runs the same trip count
     __syncthreads();
     bitonic_sort_mem<1024>(s, P);
     uint32_t n = rle_mem<1024, 8>(s, len, a.ent + b, a, scan_scratch);
