@@ -22,17 +22,20 @@
 // operand panel, and the smem descriptor has LBO = 2048 B (next 8-wide K
 // chunk) and SBO = 128 B (next 8-row group).
 //
-// Kernel. Persistent, one CTA per SM, 320 threads: warp 0 = bulk-copy
-// producer, warp 1 = TMEM owner + MMA issuer (one thread), warps 2..9 =
-// epilogue. Tile = 128 rows x 256 columns (two N=128 MMAs per K step; the
-// column tile starts at the row block on the triangle, so no tile lies below
-// the diagonal), accumulators double-buffered in TMEM (2 x 256 of the 512
-// columns) so the epilogue of tile t overlaps the MMAs of tile t+1. Epilogue
-// warp w reads TMEM lanes 32*(w%4).. (its hardware lane quarter) and column
-// half (w-2)/4: 4 x tcgen05.ld.32x32b.x32, sign bits -> four 32-bit words =
-// the row's 128 bits of one bitmap block, written as one 16-byte store in
-// the same bitmap/rowcnt format as the CUDA-core kernel (k3_pairs.cu), so
-// the scan and emitter are shared.
+// Kernel. Persistent, one CTA per SM, 608 threads (19 warps): warp 0 =
+// bulk-copy producer (A panels resident per row group, B panels through an
+// 8-stage ring), warps 1..2 = MMA issuers (even / odd tiles; warp-converged
+// issue with an elected lane), warps 3..18 = two 8-warp epilogue groups, one
+// per TMEM accumulator. Tile = 256 rows (two 128-row blocks, one 128x128x16
+// MMA each per K step) x 128 columns; on the triangle the column walk starts
+// at the row group, so no tile lies below the diagonal. Accumulators are
+// double-buffered in TMEM (2 x 256 of the 512 columns) so the epilogue of
+// tile t overlaps the MMAs of tile t+1. Epilogue warp w reads TMEM lanes
+// 32*(w%4).. (its hardware lane quarter) of row block ((w-3)>>2)&1 with
+// tcgen05.ld.32x32b.x32, sign bits -> four 32-bit words = the row's 128 bits
+// of one bitmap block, written as one 16-byte store in the same
+// bitmap/rowcnt format as the CUDA-core kernel (k3_pairs.cu), so the scan
+// and emitter are shared.
 
 #include <cuda_fp16.h>
 

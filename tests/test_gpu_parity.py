@@ -304,6 +304,21 @@ def test_pair_cosines_match_reference_golden(gpu_ctx_factory, golden_small):
 
 # ---- errors (reference error.hpp:8-14 mapping) ----------------------------
 
+@pytest.mark.parametrize("length", [3, 100, 200, 400, 1000, 3000, 6000, 12000])
+def test_out_of_vocab_id_every_count_class(gpu_ctx_factory, length):
+    """An id >= vocab is reported (ValidationError) by every K1 work class
+    (warp sorts, CTA sorts, the global-memory path), wherever it sits."""
+    rng = np.random.default_rng(length)
+    for pos in (0, length - 1):
+        tok = rng.integers(0, 1000, length).astype(np.uint32)
+        tok[pos] = 1000
+        ctx = gpu_ctx_factory()
+        ctx.load_corpus(np.r_[tok, tok].astype(np.uint32), np.array([0, length, 2 * length], np.uint64), 1000)
+        ctx.count()
+        with pytest.raises(R.ValidationError, match="vocab"):
+            ctx.synchronize()
+
+
 def test_validation_errors(gpu_ctx_factory):
     ctx = gpu_ctx_factory()
     with pytest.raises(R.ValidationError):
