@@ -106,7 +106,7 @@ __device__ __forceinline__ void gbitonic_stage(uint32_t (&v)[IPT], uint32_t t, u
   if constexpr (J > 1) gbitonic_stage<IPT, T, K, J / 2, NORM>(v, t, sm);
 }
 
-template <int IPT, int T, int K>
+template <int IPT, int T, int K, int KMAX>
 __device__ __forceinline__ void gbitonic_level(uint32_t (&v)[IPT], uint32_t t, uint32_t* sm, uint32_t& cur) {
   if constexpr (K >= IPT) {
     const uint32_t want = ((t * IPT) & K) ? 0xffffffffu : 0u;  // descending block: hold complements
@@ -118,13 +118,33 @@ __device__ __forceinline__ void gbitonic_level(uint32_t (&v)[IPT], uint32_t t, u
   } else {
     gbitonic_stage<IPT, T, K, K / 2, false>(v, t, sm);
   }
-  if constexpr (K < T * IPT) gbitonic_level<IPT, T, 2 * K>(v, t, sm, cur);
+  if constexpr (K < KMAX) gbitonic_level<IPT, T, 2 * K, KMAX>(v, t, sm, cur);
 }
 
 template <int IPT, int T>
 __device__ __forceinline__ void gbitonic_sort(uint32_t (&v)[IPT], uint32_t t, uint32_t* sm) {
   uint32_t cur = 0;
-  gbitonic_level<IPT, T, 2>(v, t, sm, cur);
+  gbitonic_level<IPT, T, 2, T * IPT>(v, t, sm, cur);
+}
+
+// Multi-warp sort whose warp-local levels (K <= 32*IPT: registers and
+// shuffles only, no CTA barrier) are skipped by warps holding only padding:
+// an all-kInf block is sorted in either direction, so such a warp just takes
+// the representation level 32*IPT expects (complemented in descending
+// blocks). Requires warp w to hold keys [w*32*IPT, (w+1)*32*IPT) of the
+// document (see group_sort_kernel's load order).
+template <int IPT, int T>
+__device__ __forceinline__ void gbitonic_sort_skip(uint32_t (&v)[IPT], uint32_t t, uint32_t* sm, bool live) {
+  constexpr uint32_t KW = 32 * IPT;
+  uint32_t cur = 0;
+  if (live) {
+    gbitonic_level<IPT, T, 2, KW>(v, t, sm, cur);
+  } else {
+    cur = ((t * IPT) & KW) ? 0xffffffffu : 0u;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) v[q] = kInf ^ cur;
+  }
+  if constexpr (KW < T * IPT) gbitonic_level<IPT, T, 2 * KW, T * IPT>(v, t, sm, cur);
 }
 
 template <int IPT>
@@ -288,9 +308,12 @@ __global__ void __launch_bounds__(32 * W) group_sort_kernel(CountArgs a, const u
   const uint64_t b = a.doc_off[d];
   const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
   uint32_t v[IPT], bad = 0;
+  // warp w loads tokens [w*32*IPT, (w+1)*32*IPT), lane-strided (coalesced):
+  // any order sorts, and warps past the end hold only padding
+  const uint32_t wbase = (t & ~31u) * IPT, lane = t & 31;
 #pragma unroll
-  for (int k = 0; k < IPT; ++k) v[k] = load_key(a, b, k * T + t, len, bad);  // coalesced; any order sorts
-  gbitonic_sort<IPT, T>(v, t, sm);
+  for (int k = 0; k < IPT; ++k) v[k] = load_key(a, b, wbase + k * 32 + lane, len, bad);
+  gbitonic_sort_skip<IPT, T>(v, t, sm, wbase < len);
   flag_bad(a, bad);
   const uint32_t n = rle_regs<IPT, W>(v, t, len, a.ent + b, a, rle_sm);
   if (t == 0) a.nnz[d] = n;
