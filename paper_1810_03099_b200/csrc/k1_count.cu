@@ -43,8 +43,10 @@ constexpr uint32_t kInf = 0xFFFFFFFFu;
 // L2 addresses; replicas divide that contention by R. The idf kernel sums the
 // replicas (measured: a shared-memory aggregation cache was slower — shared
 // atomics cost ~2 cycles per lane).
-__device__ __forceinline__ void df_add(const CountArgs& a, uint32_t key) {
-  atomicAdd(a.df + static_cast<size_t>(blockIdx.x % a.df_reps) * a.vocab + key, 1u);
+// The replica base is computed once per CTA (df_replica) and kept in a
+// register: recomputing the modulo per run head cost ~25 instructions each.
+__device__ __forceinline__ uint32_t* df_replica(const CountArgs& a) {
+  return a.df + static_cast<size_t>(blockIdx.x % a.df_reps) * a.vocab;
 }
 
 __device__ __forceinline__ uint32_t next_pow2(uint32_t x) {
@@ -190,6 +192,7 @@ __device__ __forceinline__ uint32_t rle_regs(const uint32_t (&v)[IPT], uint32_t 
     if (lane == 0) prev = kInf;
   }
   const uint32_t base = t * IPT;
+  uint32_t* const dfr = df_replica(ca);
   uint32_t hmask = 0;  // bit q: key q starts a run
 #pragma unroll
   for (int q = 0; q < IPT; ++q) {
@@ -233,7 +236,7 @@ __device__ __forceinline__ uint32_t rle_regs(const uint32_t (&v)[IPT], uint32_t 
       const uint32_t rest = hmask & ~((2u << q) - 1);  // heads after q in this thread
       const uint32_t end = rest ? base + (__ffs(rest) - 1) : next;
       ent[pos] = make_uint2(v[q], end - (base + q));
-      df_add(ca, v[q]);
+      atomicAdd(dfr + v[q], 1u);
       ++pos;
     }
   }
@@ -345,6 +348,7 @@ template <int THREADS, int IPT>
 __device__ __forceinline__ uint32_t rle_mem(const uint32_t* s, uint32_t len, uint2* ent, const CountArgs& ca,
                                             uint32_t* scan_scratch) {
   uint32_t base = 0;
+  uint32_t* const dfr = df_replica(ca);
   for (uint32_t c0 = 0; c0 < len; c0 += THREADS * IPT) {
     const uint32_t lo = c0 + threadIdx.x * IPT;
     uint32_t heads = 0;
@@ -363,7 +367,7 @@ __device__ __forceinline__ uint32_t rle_mem(const uint32_t* s, uint32_t len, uin
         uint32_t e = i + 1;
         while (e < len && s[e] == key) ++e;
         ent[pos] = make_uint2(key, e - i);
-        df_add(ca, key);
+        atomicAdd(dfr + key, 1u);
         ++pos;
       }
     }
