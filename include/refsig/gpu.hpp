@@ -85,7 +85,8 @@ class Context {
     if (rc != REFSIG_E_OVERFLOW && rc != REFSIG_OK) check(rc);
     m.ids.resize(nnz);
     m.counts.resize(nnz);
-    check(refsig_gpu_get_counts(ctx_, m.rowptr.data(), m.ids.data(), m.counts.data(), nnz, &nnz));
+    rc = refsig_gpu_get_counts(ctx_, m.rowptr.data(), m.ids.data(), m.counts.data(), nnz, &nnz);
+    check(rc, nnz);
     return m;
   }
 
@@ -203,7 +204,8 @@ class Context {
     int rc = refsig_gpu_get_pairs_csr(ctx_, 0, n_docs_hint(), r.rowptr.data(), nullptr, 0, &n);
     if (rc != REFSIG_E_OVERFLOW) check(rc);
     r.cols.resize(n);
-    check(refsig_gpu_get_pairs_csr(ctx_, 0, n_docs_hint(), r.rowptr.data(), r.cols.data(), n, &n));
+    rc = refsig_gpu_get_pairs_csr(ctx_, 0, n_docs_hint(), r.rowptr.data(), r.cols.data(), n, &n);
+    check(rc, n);
     return r;
   }
 
@@ -219,7 +221,8 @@ class Context {
     int rc = refsig_gpu_get_pairs_csr16(ctx_, 0, n_docs_hint(), r.rowptr.data(), nullptr, 0, &n);
     if (rc != REFSIG_E_OVERFLOW) check(rc);
     r.cols.resize(n);
-    check(refsig_gpu_get_pairs_csr16(ctx_, 0, n_docs_hint(), r.rowptr.data(), r.cols.data(), n, &n));
+    rc = refsig_gpu_get_pairs_csr16(ctx_, 0, n_docs_hint(), r.rowptr.data(), r.cols.data(), n, &n);
+    check(rc, n);
     return r;
   }
 
@@ -230,17 +233,18 @@ class Context {
   std::vector<PairKey> pairs(F&& f) {
     std::uint64_t n = 0;
     int rc = f(nullptr, 0, &n);  // count only; keys stay on the device
-    check(rc);
+    check(rc, n);
     std::vector<PairKey> out(n);
     check(refsig_gpu_get_pairs(ctx_, out.data(), n));  // keys of the call above
     return out;
   }
 
-  void check(int rc) const {
+  // count: the exact total an overflowing call returned through its out_count
+  void check(int rc, std::uint64_t count = 0) const {
     if (rc == REFSIG_OK) return;
     std::string msg = std::string("refsig::gpu: ") + refsig_gpu_last_error(ctx_);
     if (rc == REFSIG_E_VALIDATION) throw refsig::validation_error(msg);
-    if (rc == REFSIG_E_OVERFLOW) throw overflow_error(msg, 0);
+    if (rc == REFSIG_E_OVERFLOW) throw overflow_error(msg, count);
     throw std::runtime_error(msg);
   }
 

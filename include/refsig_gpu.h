@@ -257,6 +257,14 @@ int refsig_gpu_device_buffer(refsig_gpu_ctx* ctx, int which, void** ptr, uint64_
 #define REFSIG_N_PHASES 8
 int refsig_gpu_set_profiling(refsig_gpu_ctx* ctx, int on);
 int refsig_gpu_phase_times(refsig_gpu_ctx* ctx, double* ms, uint64_t* calls);
+/* K3 compare path (testing / A-B measurement): 0 auto (tcgen05 when K <= 128
+ * and |tau| is 0 or >= 2^-14, else FP32 CUDA cores), 1 FP32 CUDA cores,
+ * 2 tcgen05 (validation error at the pair call if K / tau do not fit it).
+ * Both paths apply the same compare rule. */
+#define REFSIG_K3_AUTO 0
+#define REFSIG_K3_FP32 1
+#define REFSIG_K3_TENSOR 2
+int refsig_gpu_set_k3_path(refsig_gpu_ctx* ctx, int path);
 /* Kernels launched by this library in this process so far. */
 uint64_t refsig_gpu_launch_count(void);
 

@@ -26,7 +26,7 @@ import os
 import numpy as np
 
 __all__ = ["Context", "ValidationError", "RefsigRuntimeError", "PairOverflowError", "WEIGHT_TF", "WEIGHT_TFIDF",
-           "library_path", "load_library", "split_keys"]
+           "K3_AUTO", "K3_FP32", "K3_TENSOR", "library_path", "load_library", "split_keys"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 WEIGHT_TF = 0
@@ -51,7 +51,8 @@ class PairOverflowError(RefsigRuntimeError):
 
 
 def library_path() -> str:
-    return os.path.join(_HERE, "lib", "librefsig_gpu.so")
+    # REFSIG_GPU_LIB: another build of the same library (A/B measurement of kernel variants)
+    return os.environ.get("REFSIG_GPU_LIB") or os.path.join(_HERE, "lib", "librefsig_gpu.so")
 
 
 # Exported symbols and their ctypes signatures (tests check this list against
@@ -114,7 +115,9 @@ SIGNATURES = {
     "refsig_gpu_mrc_step": ([_c.c_void_p, _c.c_int, _P(_c.c_uint32), _c.c_uint32, _c.c_float, _c.c_uint32, _c.c_uint32],
                             _c.c_int),
     "refsig_gpu_step_result": ([_c.c_void_p, _P(_c.c_uint64), _c.c_uint64, _P(_c.c_uint64)], _c.c_int),
+    "refsig_gpu_set_k3_path": ([_c.c_void_p, _c.c_int], _c.c_int),
 }
+K3_AUTO, K3_FP32, K3_TENSOR = 0, 1, 2
 PHASES = ["count", "reference", "sign", "pair_tiles", "pair_emit", "simhash", "h2d", "d2h"]
 
 _lib = None
@@ -128,7 +131,10 @@ def load_library():
         if not os.path.exists(path):
             raise RefsigRuntimeError(f"{path} not built: run __graft_entry__.build() / make")
         L = ctypes.CDLL(path)
+        ab = bool(os.environ.get("REFSIG_GPU_LIB"))
         for name, (args, res) in SIGNATURES.items():
+            if ab and not hasattr(L, name):  # an older build under A/B measurement
+                continue
             f = getattr(L, name)
             f.argtypes = args
             f.restype = res
@@ -443,6 +449,10 @@ class Context:
         if n.value:
             self._check(self._L.refsig_gpu_get_pairs(self._h, _ptr(keys, ctypes.c_uint64), n.value))
         return keys
+
+    def set_k3_path(self, path: int):
+        """K3_AUTO / K3_FP32 (CUDA cores) / K3_TENSOR (tcgen05) for the pair calls."""
+        self._check(self._L.refsig_gpu_set_k3_path(self._h, int(path)))
 
     # -- measurement ----------------------------------------------------------
     def set_profiling(self, on: bool):

@@ -17,6 +17,9 @@
 using namespace refsig_gpu;
 
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <utility>
 
 namespace {
 std::atomic<uint64_t> g_launches{0};
@@ -25,6 +28,17 @@ std::atomic<uint64_t> g_alloc_gen{0};  // bumped on every device (re)allocation:
 
 namespace refsig_gpu {
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void ensure_smem_attr(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> set;  // (kernel, device) -> bytes already allowed
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = set[{func, dev}];
+  if (have >= bytes) return;
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess) have = bytes;
+}
 }  // namespace refsig_gpu
 
 namespace {
@@ -152,6 +166,7 @@ struct refsig_gpu_ctx {
 
   // query mode
   refsig_gpu_ctx* db = nullptr;
+  int k3_path = REFSIG_K3_AUTO;  // refsig_gpu_set_k3_path
 
   // emit in flight (enqueue_emit -> finish_emit)
   bool emit_pending = false;
@@ -387,17 +402,22 @@ void prepare_bitmap(refsig_gpu_ctx* c, const PairGrid& g, bool zero) {
 
 // K3: the tcgen05 kernel when K fits (3K+3 <= 128), else the CUDA-core tiles.
 // REFSIG_K3=fp32 forces the CUDA-core kernel.
-bool k3_use_tc(uint32_t K, float tau) {
+bool k3_use_tc(const refsig_gpu_ctx* c, uint32_t K, float tau) {
   static const bool off = [] {
     const char* m = std::getenv("REFSIG_K3");
     return m && std::strcmp(m, "fp32") == 0;
   }();
+  if (c->k3_path == REFSIG_K3_FP32) return false;
+  if (c->k3_path == REFSIG_K3_TENSOR) {
+    require(mrc_tc_supported(K, tau), "tensor-core K3 needs K <= 128 and |tau| = 0 or >= 2^-14");
+    return true;
+  }
   return !off && mrc_tc_supported(K, tau);
 }
 
 void run_mrc_tiles(refsig_gpu_ctx* c, const float* STr, uint32_t ldr, uint32_t nr, const float* STc, uint32_t ldc,
                    uint32_t ncl, bool self, uint32_t K, float tau, const PairGrid& g) {
-  if (!k3_use_tc(K, tau)) {
+  if (!k3_use_tc(c, K, tau)) {
     launch_mrc_bitmap(STr, ldr, STc, ldc, K, tau, g, c->bitmap.as<uint32_t>(), c->rowcnt.as<uint32_t>(), c->stream);
     return;
   }
@@ -515,7 +535,9 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
     off += n_class[k];
   }
   const size_t off_bytes = sizeof(uint64_t) * (n_docs + 1), list_bytes = sizeof(uint32_t) * std::max(off, 1u);
-  const size_t bytes = off_bytes + list_bytes;
+  // documents > 8192 tokens: their scratch offsets (u64) follow the lists in the same staging buffer
+  const size_t loff_at = (off_bytes + list_bytes + 7) & ~size_t{7};
+  const size_t bytes = loff_at + sizeof(uint64_t) * n_class[refsig_gpu_ctx::kPlanLong];
   if (!c->plan_done) ck(cudaEventCreateWithFlags(&c->plan_done, cudaEventDisableTiming), "event");
   ck(cudaEventSynchronize(c->plan_done), "plan staging");  // the previous copy consumed h_plan
   if (bytes > c->h_plan_cap) {
@@ -529,7 +551,8 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
   uint32_t* lists = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(c->h_plan) + off_bytes);
   uint32_t fill[refsig_gpu_ctx::kPlanLists];
   for (int k = 0; k < refsig_gpu_ctx::kPlanLists; ++k) fill[k] = c->plan_off[k];
-  std::vector<uint64_t> loff;
+  uint64_t* loff = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(c->h_plan) + loff_at);
+  uint32_t n_loff = 0;
   uint64_t scratch = 0;
   for (uint32_t i = 0; i < n_docs; ++i) {
     const uint32_t d = order[i];
@@ -537,7 +560,7 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
     const int k = cls_of(len(d));
     lists[fill[k]++] = d;
     if (k == refsig_gpu_ctx::kPlanLong) {
-      loff.push_back(scratch);
+      loff[n_loff++] = scratch;
       uint64_t p = 1;
       while (p < len(d)) p <<= 1;
       scratch += p;
@@ -550,13 +573,15 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
   c->plan.ensure(list_bytes);
   ck(cudaMemcpyAsync(c->doc_off.p, c->h_plan, off_bytes, cudaMemcpyHostToDevice, c->stream), "H2D doc_off");
   ck(cudaMemcpyAsync(c->plan.p, lists, list_bytes, cudaMemcpyHostToDevice, c->stream), "H2D plan");
-  ck(cudaEventRecord(c->plan_done, c->stream), "event");
-  if (!loff.empty()) {
+  if (n_loff) {
+    // (a reallocation here frees the old buffers: cudaFree waits for the device)
     c->long_scratch.ensure(sizeof(uint32_t) * scratch);
-    c->long_off.ensure(8 * loff.size());
-    // rare (documents > 8192 tokens): a small synchronous copy
-    ck(cudaMemcpy(c->long_off.p, loff.data(), 8 * loff.size(), cudaMemcpyHostToDevice), "H2D long offsets");
+    c->long_off.ensure(8ull * n_loff);
+    // ordered on ctx->stream after earlier work that may still read the previous offsets (K1's
+    // side streams fork from and join back into ctx->stream)
+    ck(cudaMemcpyAsync(c->long_off.p, loff, 8ull * n_loff, cudaMemcpyHostToDevice, c->stream), "H2D long offsets");
   }
+  ck(cudaEventRecord(c->plan_done, c->stream), "event");  // h_plan (offsets, lists, long offsets) consumed
   c->loaded = true;
   c->counted = false;
   c->plan_tok = c->tok;
@@ -1528,6 +1553,17 @@ int refsig_gpu_phase_times(refsig_gpu_ctx* ctx, double* ms, uint64_t* calls) {
 }
 
 uint64_t refsig_gpu_launch_count(void) { return g_launches.load(); }
+
+int refsig_gpu_set_k3_path(refsig_gpu_ctx* ctx, int path) {
+  return guard(ctx, [&] {
+    require(path == REFSIG_K3_AUTO || path == REFSIG_K3_FP32 || path == REFSIG_K3_TENSOR, "bad K3 path");
+    if (path != ctx->k3_path && ctx->step_exec) {  // a captured step bakes in the path
+      cudaGraphExecDestroy(ctx->step_exec);
+      ctx->step_exec = nullptr;
+    }
+    ctx->k3_path = path;
+  });
+}
 
 int refsig_gpu_get_pairs(refsig_gpu_ctx* ctx, uint64_t* out_pairs, uint64_t capacity) {
   return guard(ctx, [&] {

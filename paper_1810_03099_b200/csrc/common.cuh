@@ -60,6 +60,14 @@ __host__ __device__ __forceinline__ uint64_t ceil_div(uint64_t a, uint64_t b) { 
 namespace refsig_gpu {
 // Counts kernel launches issued by this library (refsig_gpu_launch_count).
 void note_launch();
+// cudaFuncAttributeMaxDynamicSharedMemorySize >= bytes for `func` on the
+// current device (the attribute is per device context; remembered per
+// (function, device) so repeated launches skip the driver call).
+void ensure_smem_attr(const void* func, int bytes);
+template <typename... KArgs>
+inline void ensure_smem(void (*kernel)(KArgs...), size_t bytes) {
+  ensure_smem_attr(reinterpret_cast<const void*>(kernel), static_cast<int>(bytes));
+}
 
 // Programmatic dependent launch: a kernel launched with launch_pdl may be
 // scheduled while its predecessor in the stream drains; it must call

@@ -22,6 +22,9 @@
 // hashed 32 at a time, one word per lane (MD5 over 64-byte blocks, RFC 1321);
 // the bit columns are counted by a 32x32 warp bit transpose + popcount.
 
+#include <atomic>
+#include <cmath>
+
 #include "kernels.cuh"
 
 namespace refsig_gpu {
@@ -269,12 +272,16 @@ __global__ void __launch_bounds__(256) text_simhash_kernel(const uint8_t* __rest
 }  // namespace
 
 void text_init_tables() {
-  static bool done = false;
-  if (done) return;
+  // __constant__ memory is per device context: one upload per device ordinal
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load() & bit) return;
   uint32_t t[64];
   for (int i = 0; i < 64; ++i) t[i] = static_cast<uint32_t>(std::floor(std::fabs(std::sin(i + 1.0)) * 4294967296.0));
   cudaMemcpyToSymbol(c_md5_t, t, sizeof(t));
-  done = true;
+  done.fetch_or(bit);
 }
 
 void launch_text_grams(const uint8_t* text, const uint64_t* off, uint32_t n_docs, const uint64_t* gram_off,

@@ -585,11 +585,7 @@ template <int KW>
 void launch_sign_kw(const SignArgs& a, unsigned g, cudaStream_t s) {
   constexpr int TW = 32 * (KW + 1) > 2 * static_cast<int>(kSignStep) ? 32 * (KW + 1) : 2 * kSignStep;
   constexpr size_t smem = sizeof(float) * kSignWarps * TW;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(sign_kernel<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    configured = true;
-  }
+  ensure_smem(sign_kernel<KW>, smem);
   sign_kernel<KW><<<g, 32 * kSignWarps, smem, s>>>(a);
 }
 
@@ -604,6 +600,9 @@ void launch_sign(const SignArgs& a, cudaStream_t s) {
       case 2: sign_col_kernel<2><<<g, 32 * kSignWarps, 0, s>>>(a); break;
       case 3: sign_col_kernel<3><<<g, 32 * kSignWarps, 0, s>>>(a); break;
       case 4: sign_col_kernel<4><<<g, 32 * kSignWarps, 0, s>>>(a); break;
+      case 5: sign_col_kernel<5><<<g, 32 * kSignWarps, 0, s>>>(a); break;
+      case 6: sign_col_kernel<6><<<g, 32 * kSignWarps, 0, s>>>(a); break;
+      case 7: sign_col_kernel<7><<<g, 32 * kSignWarps, 0, s>>>(a); break;
       default: sign_col_kernel<8><<<g, 32 * kSignWarps, 0, s>>>(a); break;
     }
     note_launch();

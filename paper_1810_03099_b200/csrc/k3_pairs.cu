@@ -484,15 +484,13 @@ void launch_mrc_bitmap(const float* ST_rows, uint32_t ld_rows, const float* ST_c
   const dim3 gr(static_cast<unsigned>(grid));
   const int kt = K == 20 ? 20 : K == 10 ? 10 : K == 16 ? 16 : K % 32 == 0 ? 32 : 0;
   const size_t smem2 = (2ull * mrc2_stages(kt) * kc * kTile) * sizeof(float);
-  static bool configured2 = false;
-  if (!configured2) {
+  {
     const int mx = 8 * kKC * kTile * 4;
-    cudaFuncSetAttribute(mrc_bitmap_kernel2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(mrc_bitmap_kernel2<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(mrc_bitmap_kernel2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(mrc_bitmap_kernel2<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(mrc_bitmap_kernel2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    configured2 = true;
+    ensure_smem(mrc_bitmap_kernel2<0>, mx);
+    ensure_smem(mrc_bitmap_kernel2<10>, mx);
+    ensure_smem(mrc_bitmap_kernel2<16>, mx);
+    ensure_smem(mrc_bitmap_kernel2<20>, mx);
+    ensure_smem(mrc_bitmap_kernel2<32>, mx);
   }
   if (K == 20)
     mrc_bitmap_kernel2<20><<<gr, 256, smem2, s>>>(a);

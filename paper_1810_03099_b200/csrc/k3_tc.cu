@@ -61,7 +61,7 @@ __device__ __forceinline__ void tc_trace(const uint32_t dbg, int ev, uint32_t it
 __device__ __forceinline__ void tc_trace(uint32_t, int, uint32_t) {}
 #define TC_DBG(a) 0u
 #endif
-constexpr uint32_t kTcMaxKP = 128;  // 3K + 3 <= 128  <=>  K <= 41
+constexpr uint32_t kTcSmallKP = 128;  // tc_forms_kernel (shared-memory staging) up to K' = 128 (K <= 41)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -172,6 +172,11 @@ struct TcArgs {
   const __half* Ar;  // row-form panels
   const __half* Bc;  // column-form panels
   uint32_t KP;       // K' (multiple of 16)
+  uint32_t nch;      // K chunks per tile: 64-wide (4 MMA k-steps), the last one 1..4 k-steps
+  uint32_t last_steps;
+  uint32_t CB;       // bytes of one B chunk stage (128 docs x min(K', 64) halves)
+  uint32_t rb;       // row blocks per row group: 2, or 1 when two A panels and a ring do not fit
+  uint32_t abufs;    // A buffers: 2 (the next group's A loads during the current group) or 1
   PairGrid g;
   uint32_t nbr, nbc;     // 128-row / 128-column blocks
   uint32_t rb0, rb1;     // row blocks [rb0, rb1) of this call
@@ -183,28 +188,38 @@ struct TcArgs {
   uint32_t dbg;  // timing experiments only (REFSIG_TC_DEBUG): 1 no epilogue math, 2 no B refill, 4 no MMA
 };
 
-// Row group p = row blocks rb0 + 2p, +1 (A resident in smem while the CTA
-// walks the group's column blocks). Column blocks of group p: from its first
-// row block on the triangle, all of them for a rectangle.
-__device__ __forceinline__ uint32_t tc_r0(const TcArgs& a, uint32_t p) { return a.rb0 + 2 * p; }
-__device__ __forceinline__ uint32_t tc_cs(const TcArgs& a, uint32_t p) { return a.g.triangle ? tc_r0(a, p) : 0u; }
-__device__ __forceinline__ uint32_t tc_ct(const TcArgs& a, uint32_t p) { return a.nbc - tc_cs(a, p); }
+// Row group p = row blocks rb0 + rb*p (.. + rb - 1): A resident in smem while
+// the CTA walks the group's column blocks. Column blocks of group p: from its
+// first row block on the triangle, all of them for a rectangle. (FS > 0: rb = 2
+// at compile time, see mrc_tc_kernel.)
+template <uint32_t FS>
+__device__ __forceinline__ uint32_t tc_rb(const TcArgs& a) { return FS ? 2u : a.rb; }
+template <uint32_t FS>
+__device__ __forceinline__ uint32_t tc_r0(const TcArgs& a, uint32_t p) { return a.rb0 + tc_rb<FS>(a) * p; }
+template <uint32_t FS>
+__device__ __forceinline__ uint32_t tc_cs(const TcArgs& a, uint32_t p) { return a.g.triangle ? tc_r0<FS>(a, p) : 0u; }
+template <uint32_t FS>
+__device__ __forceinline__ uint32_t tc_ct(const TcArgs& a, uint32_t p) { return a.nbc - tc_cs<FS>(a, p); }
 // row block r0 + h exists in this call
-__device__ __forceinline__ bool tc_rvalid(const TcArgs& a, uint32_t p, uint32_t h) { return tc_r0(a, p) + h < a.rb1; }
+template <uint32_t FS>
+__device__ __forceinline__ bool tc_rvalid(const TcArgs& a, uint32_t p, uint32_t h) {
+  return h < tc_rb<FS>(a) && tc_r0<FS>(a, p) + h < a.rb1;
+}
 
+template <uint32_t FS>
 struct TileWalk {
   uint32_t p, c;
   __device__ void start(const TcArgs& a, uint64_t t) {
     p = 0;
-    while (t >= tc_ct(a, p)) {
-      t -= tc_ct(a, p);
+    while (t >= tc_ct<FS>(a, p)) {
+      t -= tc_ct<FS>(a, p);
       ++p;
     }
     c = static_cast<uint32_t>(t);
   }
   // returns true when the next tile starts a new row group
   __device__ bool next(const TcArgs& a) {
-    if (++c == tc_ct(a, p)) {
+    if (++c == tc_ct<FS>(a, p)) {
       c = 0;
       ++p;
       return true;
@@ -213,10 +228,15 @@ struct TileWalk {
   }
 };
 
-// Tile = 256 rows (row group: two 128-row blocks, A panels resident and
-// double-buffered per group) x 128 columns (one B panel streamed per tile
-// through an S-stage ring). Per K step: one N=128 MMA per valid row block.
-template <uint32_t KS>
+// Tile = rb*128 rows (row group: A panels resident) x 128 columns (one B
+// panel per tile, streamed through an S-stage ring in 64-wide K chunks, so
+// K' is not bounded by the ring: K' = 208 at K = 64 is four chunks, K' = 400
+// at K = 128 seven). Per K step: one N=128 MMA per valid row block into that
+// block's 128 accumulator columns. FS > 0: K' = 16*FS <= 128 as ONE chunk
+// (whole panel per stage), two row blocks and two A buffers, all compile-time
+// (the MMA issue loop fully unrolled: at K = 20 the issuing thread's latency
+// per MMA is on the critical path).
+template <uint32_t FS>
 __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t tsm[];
   __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], afull_bar[2], aempty_bar[2], tfull_bar[2],
@@ -226,9 +246,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
   const uint64_t t0 = a.n_tiles * blockIdx.x / gridDim.x, t1 = a.n_tiles * (blockIdx.x + 1) / gridDim.x;
   const uint32_t n_it = static_cast<uint32_t>(t1 - t0);
   const uint32_t PB = 256u * a.KP;  // bytes per operand panel
-  const uint32_t S = a.stages;
-  uint8_t* sAbase = tsm;               // 2 buffers x 2 panels
-  uint8_t* sBbase = tsm + 4 * PB;      // S stages x 1 panel
+  const uint32_t S = a.stages, NCH = FS ? 1u : a.nch, CB = FS ? PB : a.CB;
+  const uint32_t ABUFS = FS ? 2u : a.abufs, RB = FS ? 2u : a.rb, LAST = FS ? FS : a.last_steps;
+  constexpr uint32_t kStepsMax = FS ? FS : 4u;  // k-steps per chunk
+  uint8_t* sAbase = tsm;                      // ABUFS buffers x RB panels
+  uint8_t* sBbase = tsm + ABUFS * RB * PB;    // S stages x one chunk
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < S; ++s) {
       mb_init(&full_bar[s], 1);
@@ -255,29 +277,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
 
   if (warp == 0) {
     if (lane == 0 && n_it) {  // producer
-      TileWalk w;
+      TileWalk<FS> w;
       w.start(a, t0);
       uint32_t g = 0;  // row groups started by this CTA
+      uint32_t q = 0;  // B chunks issued
       bool new_group = true;
       for (uint32_t it = 0; it < n_it; ++it) {
-        if (new_group) {  // A panels of the group into buffer g & 1
-          const uint32_t ab = g & 1;
-          if (g >= 2) mb_wait(&aempty_bar[ab], ((g >> 1) - 1) & 1u);
-          const uint32_t np = tc_rvalid(a, w.p, 1) ? 2u : 1u;
+        if (new_group) {  // A panels of the group into buffer g % abufs
+          const uint32_t ab = g % ABUFS;
+          if (g >= ABUFS) mb_wait(&aempty_bar[ab], ((g / ABUFS) - 1) & 1u);
+          const uint32_t np = tc_rvalid<FS>(a, w.p, 1) ? 2u : 1u;
           mb_expect_tx(&afull_bar[ab], np * PB);
-          bulk_g2s(sAbase + ab * 2 * PB, reinterpret_cast<const uint8_t*>(a.Ar) + static_cast<size_t>(tc_r0(a, w.p)) * PB,
-                   np * PB, &afull_bar[ab]);
+          bulk_g2s(sAbase + ab * RB * PB,
+                   reinterpret_cast<const uint8_t*>(a.Ar) + static_cast<size_t>(tc_r0<FS>(a, w.p)) * PB, np * PB,
+                   &afull_bar[ab]);
           ++g;
         }
-        const uint32_t st = it % S;
-        if (it >= S) mb_wait(&empty_bar[st], ((it / S) - 1) & 1u);
-        const uint32_t bj = tc_cs(a, w.p) + w.c;
-        if ((TC_DBG(a) & 2) && it >= S) {
-          mb_arrive(&full_bar[st]);
-        } else {
-          mb_expect_tx(&full_bar[st], PB);
-          bulk_g2s(sBbase + static_cast<size_t>(st) * PB,
-                   reinterpret_cast<const uint8_t*>(a.Bc) + static_cast<size_t>(bj) * PB, PB, &full_bar[st]);
+        const uint32_t bj = tc_cs<FS>(a, w.p) + w.c;
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.Bc) + static_cast<size_t>(bj) * PB;
+        for (uint32_t ch = 0; ch < NCH; ++ch, ++q) {
+          const uint32_t st = q % S;
+          if (q >= S) mb_wait(&empty_bar[st], ((q / S) - 1) & 1u);
+          const uint32_t bytes = ch + 1 < NCH ? CB : LAST * 4096u;
+          if ((TC_DBG(a) & 2) && q >= S) {
+            mb_arrive(&full_bar[st]);
+          } else {
+            mb_expect_tx(&full_bar[st], bytes);
+            bulk_g2s(sBbase + static_cast<size_t>(st) * CB, src + static_cast<size_t>(ch) * CB, bytes, &full_bar[st]);
+          }
         }
         new_group = w.next(a);
       }
@@ -289,46 +316,51 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
     // whole warp converged, one elected lane issues
     const uint32_t m = warp - 1;
     if (n_it) {
-      TileWalk w;
+      TileWalk<FS> w;
       w.start(a, t0);
       const uint64_t dA0 = smem_desc(smem_u32(sAbase)), dB0 = smem_desc(smem_u32(sBbase));
-      const uint64_t dPB = PB >> 4;
-      uint32_t g = 0;
+      const uint64_t dPB = PB >> 4, dCB = CB >> 4;
+      uint32_t g = 0, q = 0;
       bool new_group = true;
       for (uint32_t it = 0; it < n_it; ++it) {
-        const uint32_t ab = (g - (new_group ? 0u : 1u)) & 1u;
         if (new_group) {
-          mb_wait(&afull_bar[g & 1], (g >> 1) & 1u);
+          mb_wait(&afull_bar[g % ABUFS], (g / ABUFS) & 1u);
           ++g;
         }
-        const uint32_t st = it % S, acc = it & 1;
-        const bool mine = acc == m;
-        if (mine) {
-          const uint32_t bj = tc_cs(a, w.p) + w.c;
-          const uint32_t r0 = tc_r0(a, w.p);
-          const bool v1 = tc_rvalid(a, w.p, 1) && !(a.g.triangle && bj < r0 + 1);
+        const uint32_t ab = (g - 1) % ABUFS;
+        const uint32_t acc = it & 1;
+        if (acc == m) {
+          const uint32_t bj = tc_cs<FS>(a, w.p) + w.c;
+          const uint32_t r0 = tc_r0<FS>(a, w.p);
+          const bool v1 = tc_rvalid<FS>(a, w.p, 1) && !(a.g.triangle && bj < r0 + 1);
           if (lane == 0 && m == 0) tc_trace(TC_DBG(a), 0, it);
-          mb_wait(&full_bar[st], (it / S) & 1u);
-          if (lane == 0 && m == 0) tc_trace(TC_DBG(a), 1, it);
           if (it >= 2) mb_wait(&tempty_bar[acc], ((it >> 1) - 1) & 1u);
           if (lane == 0 && m == 0) tc_trace(TC_DBG(a), 2, it);
-          tc_fence_after();
-          const uint64_t dA = dA0 + ab * 2 * dPB, dB = dB0 + st * dPB;
+          const uint64_t dA = dA0 + ab * RB * dPB;
           const uint32_t d0 = tmem + acc * 256;
           const uint32_t e = elect_one();
-          if (!(TC_DBG(a) & 4)) {
-            mma_f16_e(e, d0, dA, dB, 0);
+          for (uint32_t ch = 0; ch < NCH; ++ch, ++q) {
+            const uint32_t st = q % S;
+            mb_wait(&full_bar[st], (q / S) & 1u);
+            if (lane == 0 && m == 0 && ch == 0) tc_trace(TC_DBG(a), 1, it);
+            tc_fence_after();
+            const uint32_t steps = ch + 1 < NCH ? kStepsMax : LAST;
+            const uint64_t dB = dB0 + st * dCB, dAc = dA + ch * kStepsMax * 256u;
+            if (!(TC_DBG(a) & 4)) {
 #pragma unroll
-            for (uint32_t k = 1; k < KS; ++k) mma_f16_e(e, d0, dA + k * 256, dB + k * 256, 1);
-            if (v1) {
-              mma_f16_e(e, d0 + 128, dA + dPB, dB, 0);
-#pragma unroll
-              for (uint32_t k = 1; k < KS; ++k) mma_f16_e(e, d0 + 128, dA + dPB + k * 256, dB + k * 256, 1);
+              for (uint32_t j = 0; j < kStepsMax; ++j) {
+                if (j < steps) {
+                  mma_f16_e(e, d0, dAc + j * 256, dB + j * 256, (ch | j) != 0);
+                  if (v1) mma_f16_e(e, d0 + 128, dAc + dPB + j * 256, dB + j * 256, (ch | j) != 0);
+                }
+              }
             }
+            mma_commit_e(e, &empty_bar[st]);
           }
           if (lane == 0 && m == 0) tc_trace(TC_DBG(a), 3, it);
-          mma_commit_e(e, &empty_bar[st]);
           mma_commit_e(e, &tfull_bar[acc]);
+        } else {
+          q += NCH;
         }
         new_group = w.next(a);
         // both issuers release the group's A buffer (a commit with nothing
@@ -343,14 +375,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
     const uint32_t q = warp & 3, eg = (warp - 3) >> 3, h = ((warp - 3) >> 2) & 1;
     const uint32_t wpr = a.g.words_per_row;
     const uint32_t two = a.two;
-    TileWalk w;
+    TileWalk<FS> w;
     if (n_it) w.start(a, t0);
     uint32_t cnt = 0;
     for (uint32_t it = 0; it < n_it; ++it) {
       const uint32_t acc = it & 1;
       const uint32_t p = w.p;
-      const uint32_t r = tc_r0(a, p) + h;
-      const uint32_t bj = tc_cs(a, p) + w.c;
+      const uint32_t r = tc_r0<FS>(a, p) + h;
+      const uint32_t bj = tc_cs<FS>(a, p) + w.c;
       const uint32_t i = r * 128 + q * 32 + lane;
       if (acc == eg) {
         const uint32_t u = it >> 1;  // this group's use count of its accumulator
@@ -358,7 +390,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
         mb_wait(&tfull_bar[acc], u & 1u);
         if (warp == 3 && lane == 0) tc_trace(TC_DBG(a), 5, it);
         tc_fence_after();
-        const bool valid = tc_rvalid(a, p, h) && !(a.g.triangle && bj < r);
+        const bool valid = tc_rvalid<FS>(a, p, h) && !(a.g.triangle && bj < r);
         const bool edge = (a.g.triangle && bj == r) || bj + 1 == a.nbc;
         uint32_t mw[4];
 #pragma unroll
@@ -450,7 +482,7 @@ __global__ void __launch_bounds__(256) tc_forms_kernel(const float* __restrict__
   const __half one = __float2half_rn(1.0f), zero = __float2half_rn(0.0f);
   {
     // thread (dl, k0): values k0, k0 + 2, ... of doc d0 + dl; all loads issued before any use
-    constexpr uint32_t kPer = (kTcMaxKP / 3 + 1) / 2 + 1;  // ceil(41 / 2)
+    constexpr uint32_t kPer = (kTcSmallKP / 3 + 1) / 2 + 1;  // ceil(41 / 2)
     const uint32_t dl = threadIdx.x & 127, k0 = threadIdx.x >> 7, d = d0 + dl;
     float v[kPer];
 #pragma unroll
@@ -497,6 +529,81 @@ __global__ void __launch_bounds__(256) tc_forms_kernel(const float* __restrict__
   }
 }
 
+// Any K': thread (8-value chunk kc, doc dl) computes its 8 halves of both
+// forms straight from ST (reads coalesced along d; each ST value is read by
+// the three chunks that hold its hi / lo copies) and stores 16 bytes at
+// [kc][dl] (coalesced). Grid: (panels, ceil(K'/8 / 2)), 256 threads.
+__global__ void __launch_bounds__(256) tc_forms_any_kernel(const float* __restrict__ ST, uint32_t ld, uint32_t n_docs,
+                                                           uint32_t K, uint32_t KP, float tau,
+                                                           __half* __restrict__ rowf, __half* __restrict__ colf) {
+  const uint32_t pan = blockIdx.x, dl = threadIdx.x & 127, kc = blockIdx.y * 2 + (threadIdx.x >> 7);
+  if (kc * 8 >= KP) return;
+  const uint32_t d = pan * 128 + dl;
+  const __half t0 = __float2half_rn(tau);
+  const float r1 = tau - __half2float(t0);
+  const __half t1 = __float2half_rn(r1);
+  const __half t2 = __float2half_rn(r1 - __half2float(t1));
+  __align__(16) __half rv[8], cv[8];
+#pragma unroll
+  for (uint32_t e = 0; e < 8; ++e) {
+    const uint32_t pos = kc * 8 + e;
+    __half r = __float2half_rn(0.0f), c = r;
+    if (pos < 3 * K) {
+      const uint32_t seg = pos / K, k = pos - seg * K;
+      const float v = d < n_docs ? ST[static_cast<size_t>(k) * ld + d] : 0.0f;
+      const __half hi = __float2half_rn(v);
+      const __half lo = __float2half_rn(v - __half2float(hi));
+      r = seg == 2 ? lo : hi;  // row form [hi | hi | lo]
+      c = seg == 1 ? lo : hi;  // column form [hi | lo | hi]
+    } else if (pos < 3 * K + 3) {
+      const uint32_t j = pos - 3 * K;
+      const __half tj = j == 0 ? t0 : (j == 1 ? t1 : t2);
+      r = __half2float(tj) == 0.0f ? __float2half_rn(0.0f) : __hneg(tj);  // +0, never -0
+      c = __float2half_rn(1.0f);
+    }
+    rv[e] = r;
+    cv[e] = c;
+  }
+  const size_t off = (static_cast<size_t>(pan) * (KP / 8) + kc) * 128 * 8 + static_cast<size_t>(dl) * 8;
+  if (rowf) *reinterpret_cast<uint4*>(rowf + off) = *reinterpret_cast<const uint4*>(rv);
+  if (colf) *reinterpret_cast<uint4*>(colf + off) = *reinterpret_cast<const uint4*>(cv);
+}
+
+// Shared-memory plan of mrc_tc_kernel for a K': row blocks per group, A
+// buffers and B chunk stages (false when fewer than 3 stages fit).
+constexpr uint32_t kTcSmemBudget = 225u * 1024u;
+struct TcPlan {
+  uint32_t rb, abufs, stages, CB;
+  size_t smem;
+};
+bool tc_plan(uint32_t KP, TcPlan& pl) {
+  const uint32_t PB = 256u * KP;
+  if (KP <= kTcSmallKP) {  // one chunk = the whole panel: 2 x 2 resident A panels + S panels within ~200 KB
+    pl.rb = pl.abufs = 2;
+    pl.CB = PB;
+    pl.stages = std::max<uint32_t>(2u, std::min<uint32_t>(8u, (200u * 1024u - 4u * PB) / PB));
+    pl.smem = std::max<size_t>(static_cast<size_t>(4 + pl.stages) * PB, 116u * 1024u);
+    return true;
+  }
+  pl.CB = 256u * 64u;
+  if (4u * PB + 4u * pl.CB <= kTcSmemBudget) {
+    pl.rb = 2;
+    pl.abufs = 2;
+  } else if (2u * PB + 4u * pl.CB <= kTcSmemBudget) {
+    pl.rb = 2;
+    pl.abufs = 1;
+  } else {
+    pl.rb = 1;
+    pl.abufs = (2u * PB + 4u * pl.CB <= kTcSmemBudget) ? 2u : 1u;
+  }
+  const uint32_t a_bytes = pl.abufs * pl.rb * PB;
+  if (a_bytes + 3u * pl.CB > kTcSmemBudget) return false;
+  pl.stages = std::min<uint32_t>(8u, (kTcSmemBudget - a_bytes) / pl.CB);
+  // at least ~116 KB so that exactly one CTA (the TMEM owner of all 512 columns) fits per SM
+  pl.smem = std::max<size_t>(static_cast<size_t>(a_bytes) + static_cast<size_t>(pl.stages) * pl.CB, 116u * 1024u);
+  return true;
+}
+
 }  // namespace
 
 uint32_t mrc_tc_kp(uint32_t K) { return ((3 * K + 3) + 15) / 16 * 16; }
@@ -504,9 +611,11 @@ uint32_t mrc_tc_kp(uint32_t K) { return ((3 * K + 3) + 15) / 16 * 16; }
 bool mrc_tc_supported(uint32_t K, float tau) {
   // fp16 pieces of tau: |tau| < 65504, and tau = 0 or |tau| >= 2^-14 (fp16
   // normal) so that the leading piece is nonzero and a zero signature never
-  // matches a positive tau; K' <= 128 keeps 2+ stages in smem
+  // matches a positive tau; the resident A panels plus 3+ B chunk stages fit
+  // in shared memory (K <= 234; K = 128 -> K' = 400)
   const float at = fabsf(tau);
-  return K >= 1 && mrc_tc_kp(K) <= kTcMaxKP && at < 60000.0f && (at == 0.0f || at >= 6.103515625e-05f);
+  TcPlan pl;
+  return K >= 1 && tc_plan(mrc_tc_kp(K), pl) && at < 60000.0f && (at == 0.0f || at >= 6.103515625e-05f);
 }
 
 size_t mrc_tc_form_bytes(uint32_t K, uint32_t n_docs) {
@@ -518,12 +627,15 @@ void launch_mrc_tc_forms(const float* ST, uint32_t ld, uint32_t n_docs, uint32_t
   const uint32_t KP = mrc_tc_kp(K);
   const uint32_t n_pan = static_cast<uint32_t>(ceil_div(n_docs, 128));
   if (!n_pan) return;
-  const size_t smem = 2ull * 128 * (KP + 8) * sizeof(__half);  // <= 69.6 KB at K' = 128
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(tc_forms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024);
-    configured = true;
+  if (KP > kTcSmallKP) {
+    const dim3 grid(n_pan, static_cast<unsigned>(ceil_div(KP / 8, 2)));
+    tc_forms_any_kernel<<<grid, 256, 0, s>>>(ST, ld, n_docs, K, KP, tau, static_cast<__half*>(rowf),
+                                             static_cast<__half*>(colf));
+    note_launch();
+    return;
   }
+  const size_t smem = 2ull * 128 * (KP + 8) * sizeof(__half);  // <= 69.6 KB at K' = 128
+  ensure_smem(tc_forms_kernel, 72 * 1024);
   tc_forms_kernel<<<n_pan, 256, smem, s>>>(ST, ld, n_docs, K, KP, tau, static_cast<__half*>(rowf),
                                            static_cast<__half*>(colf));
   note_launch();
@@ -542,8 +654,16 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
   a.rb1 = static_cast<uint32_t>(ceil_div(g.row_end, 128));
   if (a.rb1 > a.nbr) a.rb1 = a.nbr;
   if (g.row_end <= g.row_begin || a.rb1 <= a.rb0 || a.nbc == 0) return;
+  TcPlan pl;
+  if (!tc_plan(a.KP, pl)) return;  // callers check mrc_tc_supported
+  a.rb = pl.rb;
+  a.abufs = pl.abufs;
+  a.stages = pl.stages;
+  a.CB = pl.CB;
+  a.nch = static_cast<uint32_t>(ceil_div(a.KP, 64));
+  a.last_steps = (a.KP - 64 * (a.nch - 1)) / 16;
   uint64_t T = 0;
-  for (uint32_t r0 = a.rb0; r0 < a.rb1; r0 += 2) T += a.nbc - (g.triangle ? r0 : 0u);
+  for (uint32_t r0 = a.rb0; r0 < a.rb1; r0 += a.rb) T += a.nbc - (g.triangle ? r0 : 0u);
   if (T == 0) return;
   a.n_tiles = T;
   a.bitmap = bitmap;
@@ -554,23 +674,22 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
     return m ? static_cast<uint32_t>(std::atoi(m)) : 0u;
   }();
   a.dbg = dbg;
-  const uint32_t PB = 256u * a.KP;
-  // 2 x 2 resident A panels + S streamed B panels within ~200 KB
-  a.stages = std::max<uint32_t>(2u, std::min<uint32_t>(8u, (200u * 1024u - 4u * PB) / PB));
-  // at least ~116 KB so that exactly one CTA (the TMEM owner of all 512 columns) fits per SM
-  const size_t smem = std::max<size_t>(static_cast<size_t>(4 + a.stages) * PB, 116u * 1024u);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(mrc_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(mrc_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(mrc_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(mrc_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(mrc_tc_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(mrc_tc_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(mrc_tc_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(mrc_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
+  const size_t smem = pl.smem;
+  // per launch: the attribute is per device context (a process may drive several GPUs)
+  const uint32_t fs = a.KP <= kTcSmallKP ? a.KP / 16 : 0u;
+  void (*kern)(TcArgs) = nullptr;
+  switch (fs) {
+    case 1: kern = mrc_tc_kernel<1>; break;
+    case 2: kern = mrc_tc_kernel<2>; break;
+    case 3: kern = mrc_tc_kernel<3>; break;
+    case 4: kern = mrc_tc_kernel<4>; break;
+    case 5: kern = mrc_tc_kernel<5>; break;
+    case 6: kern = mrc_tc_kernel<6>; break;
+    case 7: kern = mrc_tc_kernel<7>; break;
+    case 8: kern = mrc_tc_kernel<8>; break;
+    default: kern = mrc_tc_kernel<0>; break;
   }
+  ensure_smem(kern, smem);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -586,16 +705,7 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
     }
   }
 #endif
-  switch (a.KP / 16) {
-    case 1: launch_pdl(mrc_tc_kernel<1>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
-    case 2: launch_pdl(mrc_tc_kernel<2>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
-    case 3: launch_pdl(mrc_tc_kernel<3>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
-    case 4: launch_pdl(mrc_tc_kernel<4>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
-    case 5: launch_pdl(mrc_tc_kernel<5>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
-    case 6: launch_pdl(mrc_tc_kernel<6>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
-    case 7: launch_pdl(mrc_tc_kernel<7>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
-    default: launch_pdl(mrc_tc_kernel<8>, dim3(grid), dim3(kTcThreads), smem, s, a); break;
-  }
+  launch_pdl(kern, dim3(grid), dim3(kTcThreads), smem, s, a);
 #ifdef REFSIG_TC_TRACE
   if (dbg & 8) {
     static int calls = 0;
@@ -611,8 +721,8 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
                      z[8][it] - t0, z[9][it] - t0, z[10][it] - t0, z[6][it] - t0, z[11][it] - t0, z[7][it] - t0);
     }
   }
-  note_launch();
 #endif
+  note_launch();
 }
 
 }  // namespace refsig_gpu

@@ -381,11 +381,7 @@ void launch_head_rows(const uint2* ent, const uint64_t* doc_off, const uint32_t*
 void launch_exact_tail(const ExactArgs& a, uint32_t row_lo, uint32_t row_hi, cudaStream_t s) {
   if (row_hi <= row_lo) return;
   const size_t smem = sizeof(uint32_t) * (a.panel + a.H);
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaFuncSetAttribute(exact_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    configured = smem;
-  }
+  ensure_smem(exact_tail_kernel, smem);
   exact_tail_kernel<<<row_hi - row_lo, 512, smem, s>>>(a, row_lo);
   note_launch();
 }

@@ -24,14 +24,7 @@ def assert_sig_close(g, c):
     assert not bad.any(), f"{bad.sum()} signature values out of tolerance, max err {err.max():.3g}"
 
 
-def assert_pairs_match(gpu_keys, orc_keys, border, label=""):
-    gpu_keys = np.asarray(gpu_keys, np.uint64)
-    assert np.all(np.diff(gpu_keys.astype(np.int64)) > 0), "GPU pairs not strictly sorted"
-    g, o, b = set(gpu_keys.tolist()), set(orc_keys.tolist()), set(border.tolist())
-    diff = g ^ o
-    outside = diff - b
-    assert not outside, f"{label}: {len(outside)} pair mismatches outside the 1e-5 band (e.g. {sorted(outside)[:5]})"
-    return len(diff)  # borderline disagreements (listed, allowed)
+from tests.parity_util import assert_pairs_match  # noqa: E402  (numpy set algebra, border rule)
 
 
 def corpus_c0(n=None):

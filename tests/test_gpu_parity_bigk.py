@@ -1,0 +1,110 @@
+"""GPU parity of the compare rule (SPEC.md:369-377 over i<j) at
+the K of configs[3] (K=64) and configs[4] (K=128), on BOTH K3 paths — the
+tcgen05 split-fp16 kernel (k3_tc.cu) and the FP32 CUDA-core tiles
+(k3_pairs.cu) — against the oracle (oracle/oracle.cpp orc_mrc_pairs /
+orc_mrc_query_pairs, fp64).
+
+Bar: candidate sets identical except pairs whose oracle score is within 1e-5
+of tau, which the oracle lists (tests/parity_util.py)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1810_03099_b200 as R
+from paper_1810_03099_b200 import corpus as C
+from tests.parity_util import BAND, assert_pairs_match
+
+pytestmark = pytest.mark.gpu
+
+PATHS = {"tensor": R.K3_TENSOR, "fp32": R.K3_FP32}
+
+
+def _signed(ctx, cp, refs):
+    ctx.load_corpus(cp.tokens, cp.doc_off, cp.vocab)
+    ctx.count()
+    ctx.set_reference_docs(refs)
+    return ctx.sign()
+
+
+@pytest.mark.parametrize("path", list(PATHS))
+@pytest.mark.parametrize("K", [42, 64, 100, 128])
+def test_mrc_pairs_bigk_c0(gpu_ctx_factory, K, path):
+    cp, cfg = C.config_corpus("c0")
+    refs = C.sample_refs(cfg["ref_seed"], cp.n_docs, K)
+    ctx = gpu_ctx_factory()
+    ctx.set_k3_path(PATHS[path])
+    _signed(ctx, cp, refs)
+    o = oracle.mrc_pipeline(cp.tokens, cp.doc_off, cp.vocab, refs)
+    for tau in (0.9, 0.99):
+        keys = ctx.mrc_pairs(tau)
+        pairs, border = oracle.mrc_pairs(o.S, tau, BAND)
+        assert_pairs_match(keys, pairs, border, f"c0 K={K} tau={tau} {path}")
+
+
+@pytest.mark.parametrize("path", list(PATHS))
+@pytest.mark.parametrize("K", [64, 128])
+def test_mrc_pairs_bigk_c1_slice(gpu_ctx_factory, K, path):
+    """5,000-document slice of configs[1] (20 topics, near-duplicates)."""
+    cp, cfg = C.config_corpus("c1")
+    cp = cp.slice_docs(5000)
+    refs = C.sample_refs(cfg["ref_seed"], cp.n_docs, K)
+    ctx = gpu_ctx_factory()
+    ctx.set_k3_path(PATHS[path])
+    _signed(ctx, cp, refs)
+    o = oracle.mrc_pipeline(cp.tokens, cp.doc_off, cp.vocab, refs)
+    for tau in (0.9, 0.99):
+        keys = ctx.mrc_pairs(tau)
+        pairs, border = oracle.mrc_pairs(o.S, tau, BAND)
+        assert_pairs_match(keys, pairs, border, f"c1[:5000] K={K} tau={tau} {path}")
+    # a row panel (the streaming unit of configs[3]) equals the same rows of the full set
+    k2 = ctx.mrc_pairs_rows(0.99, 1024, 2048)
+    full = ctx.mrc_pairs(0.99)
+    rows = full >> np.uint64(32)
+    assert np.array_equal(k2, full[(rows >= 1024) & (rows < 2048)])
+
+
+@pytest.mark.parametrize("path", list(PATHS))
+def test_query_vs_database_k128(gpu_ctx_factory, path):
+    """configs[4]'s K=128 query mode: queries x database rectangle (no triangle)."""
+    cfg = C.load_configs()["configs"]["c4"]
+    db_spec = dict(cfg["corpus"], n_docs=4000, vocab=50000)
+    q_spec = dict(cfg["queries"], n_docs=600, vocab=50000)
+    db = C.generate(db_spec)
+    q = C.generate_queries(q_spec, db_spec, db)
+    K = 128
+    refs = C.sample_refs(0, db.n_docs, K)
+    dbc = gpu_ctx_factory()
+    Sd = _signed(dbc, db, refs)
+    qc = gpu_ctx_factory()
+    qc.set_k3_path(PATHS[path])
+    qc.attach_database(dbc)
+    qc.load_corpus(q.tokens, q.doc_off, q.vocab)
+    qc.count()
+    Sq = qc.sign()
+    od = oracle.mrc_pipeline(db.tokens, db.doc_off, db.vocab, refs)
+    xq = oracle.weighted(oracle.count(q.tokens, q.doc_off), od.idf)
+    oSq = oracle.sign(xq, oracle.rows(od.x, refs))
+    err = np.abs(Sq.astype(np.float64) - oSq)
+    assert np.all(err <= 1e-5 * np.abs(oSq) + 1e-7)
+    for tau in (0.9, 0.99):
+        keys = qc.mrc_query_pairs(tau)
+        pairs, border = oracle.mrc_query_pairs(oSq, od.S, tau, BAND)
+        assert_pairs_match(keys, pairs, border, f"query K=128 tau={tau} {path}")
+
+
+def test_mrc_pairs_c3_sampled_panel(gpu_ctx_factory):
+    """configs[3] at full scale (200,000 docs, V=500k, K=64): signatures of
+    every document within 1e-5, and the candidate set of rows [0, 2048) x all
+    j > i (~4e8 pairs, ~48M candidates at tau=0.99) against the oracle."""
+    cp, cfg = C.config_corpus("c3")
+    refs = C.sample_refs(cfg["ref_seed"], cp.n_docs, cfg["K"])
+    tau = C.load_configs()["thresholds"]["tau_mrc"]
+    ctx = gpu_ctx_factory()
+    S = _signed(ctx, cp, refs)
+    o = oracle.mrc_pipeline(cp.tokens, cp.doc_off, cp.vocab, refs)
+    err = np.abs(S.astype(np.float64) - o.S)
+    assert np.all(err <= 1e-5 * np.abs(o.S) + 1e-7), f"max signature error {err.max():.3g}"
+    keys = ctx.mrc_pairs_rows(tau, 0, 2048)
+    pairs, border = oracle.mrc_pairs(o.S, tau, BAND, 0, 2048)
+    nb = assert_pairs_match(keys, pairs, border, "c3 rows [0,2048)")
+    print(f"c3 panel: {len(keys)} GPU pairs, {len(pairs)} oracle, {len(border)} in band, {nb} differ")
