@@ -141,7 +141,7 @@ struct refsig_gpu_ctx {
   // pairs
   // pair output: sorted CSR columns (cand) over rowstart; the 64-bit keys
   // (keys) are materialised only when a caller asks for them
-  DevBuf bitmap, rowcnt, rowstart, cand, scan_tmp, keys;
+  DevBuf bitmap, rowcnt, rowstart, cand, scan_tmp, keys, emit_ctr;
   DevBuf cand16;  // 16-bit column copy for get_pairs_csr16
   const uint32_t* plan_tok = nullptr;  // token pointer the plan / step graph were built with
   uint64_t cand_count = 0;
@@ -338,12 +338,14 @@ void enqueue_emit(refsig_gpu_ctx* c, const PairGrid& g) {
   c->rowstart.ensure(sizeof(uint64_t) * (n + 1));
   c->scan_tmp.ensure(scan_tmp_bytes(n));
   c->cand.ensure(sizeof(uint32_t) * (1u << 20));
+  if (c->emit_ctr.ensure(2 * sizeof(uint32_t)))  // the emit kernel leaves its counters zero
+    ck(cudaMemsetAsync(c->emit_ctr.p, 0, 2 * sizeof(uint32_t), c->stream), "memset");
   {
     Phase ph(c, REFSIG_PHASE_PAIR_EMIT);
     launch_exclusive_scan_u32_to_u64(c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(), n, c->scan_tmp.p,
                                      c->stream);
     launch_emit_pairs(c->bitmap.as<uint32_t>(), g, c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(),
-                      c->cand.as<uint32_t>(), c->cand.cap / sizeof(uint32_t), c->stream);
+                      c->cand.as<uint32_t>(), c->cand.cap / sizeof(uint32_t), c->emit_ctr.as<uint32_t>(), c->stream);
     launched("emit");
   }
   ck(cudaMemcpyAsync(c->h_pin, c->rowstart.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, c->stream), "D2H count");
@@ -365,7 +367,7 @@ int finish_emit(refsig_gpu_ctx* c, uint64_t* out, uint64_t capacity, uint64_t* o
     c->cand.ensure(sizeof(uint32_t) * (total + total / 4 + 1024));
     Phase ph(c, REFSIG_PHASE_PAIR_EMIT);
     launch_emit_pairs(c->bitmap.as<uint32_t>(), g, c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(),
-                      c->cand.as<uint32_t>(), c->cand.cap / sizeof(uint32_t), c->stream);
+                      c->cand.as<uint32_t>(), c->cand.cap / sizeof(uint32_t), c->emit_ctr.as<uint32_t>(), c->stream);
     launched("emit");
   }
   c->cand_count = total;

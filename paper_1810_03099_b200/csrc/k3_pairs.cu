@@ -351,68 +351,102 @@ __global__ void __launch_bounds__(256) hamming_bitmap_kernel(const uint64_t* __r
   if (cnt) atomicAdd(rowcnt + i, cnt);
 }
 
-// Warp per row: scan the row's words from its first written tile, write keys.
+// Warp per row: the row's set bits as ascending column ids at
+// out[rowstart[i] ..). A row is read in batches of 128 words (4096 columns),
+// lane l loading words c + 32k + l (k = 0..3: four coalesced 128-byte loads;
+// the next batch's loads are in flight during this batch's expansion). Slice
+// k (32 words, 1024 columns) is expanded on its own: the lanes' popcounts of
+// slices (0,1) and (2,3) are scanned as packed 16-bit pairs (two warp scans
+// per batch); a sparse slice (<= 128 matches) is stored by the lanes
+// directly, a denser one through a per-warp shared stage (each lane expands
+// its word at its exclusive offset, then the warp copies the stage out with
+// contiguous 128-byte stores: one sequential output stream per row; a slice
+// never exceeds the 1024-entry stage).
+// Rows: warp w of the grid takes row w first; with `persistent`, later rows
+// come from a counter (rows differ by orders of magnitude in matches).
+constexpr uint32_t kEmitWarps = 8;
+constexpr uint32_t kEmitDirect = 128;  // default (sweep 32..1024 at c1 and c3); REFSIG_EMIT_DIRECT overrides
 __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ bitmap, PairGrid g,
                                                    const uint32_t* __restrict__ rowcnt,
                                                    const uint64_t* __restrict__ rowstart, uint32_t* __restrict__ out,
-                                                   uint64_t capacity) {
+                                                   uint64_t capacity, uint32_t* __restrict__ ctr, int persistent,
+                                                   uint32_t direct_max) {
+  // ctr[0]: next row ticket, ctr[1]: finished CTAs; both zero at launch, and
+  // the last CTA to finish zeroes them again (no memset node between the scan
+  // and this PDL launch)
+  __shared__ uint32_t stage_all[kEmitWarps][1024];
   pdl_wait();
-  const int lane = threadIdx.x & 31;
-  const uint32_t i = g.row_begin + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // one row per warp
-  if (i >= g.row_end) return;
-  {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t* stage = stage_all[threadIdx.x >> 5];
+  const uint32_t wpr = g.words_per_row;
+  const uint32_t n_warps = gridDim.x * kEmitWarps;
+  uint32_t r = blockIdx.x * kEmitWarps + (threadIdx.x >> 5);
+  for (;;) {
+    const uint32_t i = g.row_begin + r;
+    if (i >= g.row_end) break;
+    if (persistent) {  // next row's ticket, fetched while this row is expanded
+      uint32_t t = 0;
+      if (lane == 0) t = atomicAdd(ctr, 1u);
+      r = n_warps + __shfl_sync(0xffffffffu, t, 0);
+    } else {
+      r = ~0u - g.row_begin;  // one row per warp
+    }
     uint32_t remaining = rowcnt[i];
-    if (remaining == 0) return;
+    if (remaining == 0) continue;
     uint64_t base = rowstart[i];
-    const uint32_t* row = bitmap + static_cast<size_t>(i) * g.words_per_row;
-    const uint32_t wbeg = g.triangle ? (i / kTile) * 4 : 0;
-    const uint32_t wpr = g.words_per_row;
-    // the next batch's word is loaded before this batch is expanded, so the
-    // load latency overlaps the expansion
-    uint32_t word_next = wbeg + lane < wpr ? row[wbeg + lane] : 0u;
-    for (uint32_t c = wbeg; c < wpr && remaining; c += 32) {
-      const uint32_t wi = c + lane;
-      uint32_t word = word_next;
-      word_next = c + 32 + lane < wpr ? row[c + 32 + lane] : 0u;
-      const uint32_t n = __popc(word);
-      const uint32_t inc = warp_inclusive_scan(n, lane);
-      const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-      if (base + tot <= capacity) {  // common case: no per-key capacity checks
-        // Two expansions with warp-uniform trip counts; take the shorter:
-        // (a) every lane walks its own word's bits (max popcount iterations);
-        // (b) the warp walks the nonzero words and lane l tests bit l (one
-        //     iteration per nonzero word: dense near-duplicate clusters).
-        const uint32_t maxn = __reduce_max_sync(0xffffffffu, n);
-        const uint32_t nzmask = __ballot_sync(0xffffffffu, word != 0u);
-        if (maxn <= static_cast<uint32_t>(__popc(nzmask))) {
-          uint32_t* o = out + base + (inc - n);
-          const uint32_t col = wi * 32u;
-          while (word) {
-            const int b = __ffs(word) - 1;
-            word &= word - 1;
-            *o++ = col + b;
-          }
-        } else {
-          uint32_t* o = out + base;
-          const uint32_t lt = (1u << lane) - 1u, ex = inc - n;
-          for (uint32_t m = nzmask; m; m &= m - 1) {
-            const int w = __ffs(m) - 1;
-            const uint32_t wv = __shfl_sync(0xffffffffu, word, w);
-            const uint32_t e = __shfl_sync(0xffffffffu, ex, w);
-            if ((wv >> lane) & 1u) o[e + __popc(wv & lt)] = (c + w) * 32u + lane;
-          }
-        }
-      } else {
-        uint64_t pos = base + inc - n;
-        while (word) {
-          const int b = __ffs(word) - 1;
-          word &= word - 1;
-          if (pos < capacity) out[pos] = wi * 32u + b;
-          ++pos;
-        }
+    const uint32_t* row = bitmap + static_cast<size_t>(i) * wpr;
+    uint32_t c = g.triangle ? (i / kTile) * 4 : 0;  // first written word
+    uint32_t nx[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) nx[k] = c + 32 * k + lane < wpr ? row[c + 32 * k + lane] : 0u;
+    for (; c < wpr && remaining; c += 128) {
+      uint32_t w[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        w[k] = nx[k];
+        nx[k] = c + 128 + 32 * k + lane < wpr ? row[c + 128 + 32 * k + lane] : 0u;
       }
-      base += tot;
-      remaining -= tot;
+      // inclusive scans of (n0 | n1 << 16) and (n2 | n3 << 16): counts <= 1024 per field
+      const uint32_t p01 = warp_inclusive_scan(__popc(w[0]) | (__popc(w[1]) << 16), static_cast<int>(lane));
+      const uint32_t p23 = warp_inclusive_scan(__popc(w[2]) | (__popc(w[3]) << 16), static_cast<int>(lane));
+      const uint32_t t01 = __shfl_sync(0xffffffffu, p01, 31), t23 = __shfl_sync(0xffffffffu, p23, 31);
+      if ((t01 | t23) == 0) continue;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t pk = k < 2 ? p01 : p23, tk = k < 2 ? t01 : t23, sh = (k & 1) * 16;
+        const uint32_t inc = (pk >> sh) & 0xffffu, tot = (tk >> sh) & 0xffffu;
+        if (tot == 0) continue;
+        uint32_t word = w[k];
+        const uint32_t ex = inc - __popc(word);
+        const uint32_t col = (c + 32 * k + lane) * 32u;
+        if (base + tot > capacity) {  // overflow: exact positions, writes below capacity only
+          uint64_t pos = base + ex;
+          for (; word; word &= word - 1, ++pos)
+            if (pos < capacity) out[pos] = col + (__ffs(word) - 1);
+        } else if (tot <= direct_max) {
+          uint32_t* o = out + base + ex;
+          for (; word; word &= word - 1) *o++ = col + (__ffs(word) - 1);
+        } else {
+          uint32_t o = ex;
+          for (; word; word &= word - 1) stage[o++] = col + (__ffs(word) - 1);
+          __syncwarp();
+          uint32_t* dst = out + base;
+          for (uint32_t e = lane; e < tot; e += 32) dst[e] = stage[e];
+          __syncwarp();
+        }
+        base += tot;
+        remaining -= tot;
+      }
+    }
+  }
+  if (persistent) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+        ctr[0] = 0;
+        ctr[1] = 0;
+      }
     }
   }
 }
@@ -525,11 +559,20 @@ void launch_cols_to_keys(const uint64_t* rowstart, uint32_t row_begin, uint32_t 
 }
 
 void launch_emit_pairs(const uint32_t* bitmap, const PairGrid& g, const uint32_t* rowcnt, const uint64_t* rowstart,
-                       uint32_t* out, uint64_t capacity, cudaStream_t s) {
+                       uint32_t* out, uint64_t capacity, uint32_t* counter, cudaStream_t s) {
   if (g.row_end <= g.row_begin) return;
-  const uint64_t blocks = ceil_div(g.row_end - g.row_begin, 8);  // one row per warp
-  launch_pdl(emit_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, s, bitmap, g, rowcnt, rowstart, out,
-             capacity);
+  // one row per warp; persistent warps (at most 7 CTAs of 8 warps per SM, 32 KB
+  // of stages each) when there are many more rows than resident warps
+  const uint64_t need = ceil_div(g.row_end - g.row_begin, kEmitWarps);
+  const uint64_t resident = static_cast<uint64_t>(sms()) * 7;
+  const int persistent = need > 4 * resident ? 1 : 0;
+  const uint64_t blocks = persistent ? resident : need;
+  static const uint32_t direct_max = [] {
+    const char* m = std::getenv("REFSIG_EMIT_DIRECT");
+    return m ? static_cast<uint32_t>(std::atoi(m)) : kEmitDirect;
+  }();
+  launch_pdl(emit_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kEmitWarps), 0, s, bitmap, g, rowcnt,
+             rowstart, out, capacity, counter, persistent, direct_max);
   note_launch();
 }
 

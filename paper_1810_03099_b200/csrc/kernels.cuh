@@ -157,8 +157,9 @@ void launch_cols_to_keys(const uint64_t* rowstart, uint32_t row_begin, uint32_t 
                          uint64_t* keys, cudaStream_t s);
 // Sorted CSR columns: row i's matches j ascending at cols[rowstart[i] ..);
 // writes only below capacity.
+// counter: two device words, zero at the first launch; the kernel leaves them zero.
 void launch_emit_pairs(const uint32_t* bitmap, const PairGrid& g, const uint32_t* rowcnt, const uint64_t* rowstart,
-                       uint32_t* out, uint64_t capacity, cudaStream_t s);
+                       uint32_t* out, uint64_t capacity, uint32_t* counter, cudaStream_t s);
 
 // out[k] = (uint16) in[k] (column ids of a grid with n_cols <= 65536).
 void launch_narrow_cols(const uint32_t* in, uint64_t n, uint16_t* out, cudaStream_t s);
