@@ -440,6 +440,8 @@ void run_mrc_tiles(refsig_gpu_ctx* c, const float* STr, uint32_t ldr, uint32_t n
 void build_reference(refsig_gpu_ctx* c, const RefArgs& r, uint64_t u_cap) {
   const uint32_t V = c->vocab;
   if (u_cap > V) u_cap = V;
+  // K2 addresses R rows by 32-bit element offsets (row * Kp)
+  require(u_cap * r.Kp < (1ull << 32), "reference term union too large (|U| * K >= 2^32)");
   const size_t rbytes = sizeof(float) * std::max<uint64_t>(u_cap, 1) * r.Kp;
   c->R.ensure(rbytes);
   c->ref_count.ensure(sizeof(uint32_t));

@@ -187,14 +187,16 @@ __device__ __forceinline__ void sign_slab_steps(const SignArgs& a, const uint2* 
       const float w = static_cast<float>(x[u].y) * ti[u].idf;
       if (do_sq) sq = fmaf(w, w, sq);
       const uint32_t hits = __ballot_sync(0xffffffffu, ti[u].ref_row >= 0);
-      if (ti[u].ref_row >= 0) qw[qn + __popc(hits & lt)] = make_int2(ti[u].ref_row, __float_as_int(w));
+      if (ti[u].ref_row >= 0)  // the R row's element offset, computed once per hit
+        qw[qn + __popc(hits & lt)] = make_int2(static_cast<int>(static_cast<uint32_t>(ti[u].ref_row) * a.Kp),
+                                               __float_as_int(w));
       qn += __popc(hits);
     }
     __syncwarp();
     for (uint32_t h = lane; h < qn; h += 32) {
       const int2 hv = qw[h];
       const float w = __int_as_float(hv.y);
-      const float4* __restrict__ r4 = reinterpret_cast<const float4*>(a.R + static_cast<size_t>(hv.x) * a.Kp + c0);
+      const float4* __restrict__ r4 = reinterpret_cast<const float4*>(a.R + static_cast<uint32_t>(hv.x) + c0);
       constexpr int G = KW / 4 < 8 ? KW / 4 : 8;  // float4 loads in flight per group
 #pragma unroll
       for (int j0 = 0; j0 < KW / 4; j0 += G) {
@@ -276,7 +278,9 @@ __device__ __forceinline__ void sign_half_docs(const SignArgs& a, uint32_t q, ui
       const float w = static_cast<float>(x[u].y) * ti[u].idf;
       sq = fmaf(w, w, sq);
       const uint32_t mine = (__ballot_sync(0xffffffffu, ti[u].ref_row >= 0) >> (16 * h)) & 0xffffu;
-      if (ti[u].ref_row >= 0) qw[qn + __popc(mine & lt)] = make_int2(ti[u].ref_row, __float_as_int(w));
+      if (ti[u].ref_row >= 0)
+        qw[qn + __popc(mine & lt)] = make_int2(static_cast<int>(static_cast<uint32_t>(ti[u].ref_row) * a.Kp),
+                                               __float_as_int(w));
       qn += __popc(mine);
     }
     __syncwarp();
@@ -285,7 +289,7 @@ __device__ __forceinline__ void sign_half_docs(const SignArgs& a, uint32_t q, ui
       if (hh < qn) {
         const int2 hv = qw[hh];
         const float w = __int_as_float(hv.y);
-        const float4* __restrict__ r4 = reinterpret_cast<const float4*>(a.R + static_cast<size_t>(hv.x) * a.Kp);
+        const float4* __restrict__ r4 = reinterpret_cast<const float4*>(a.R + static_cast<uint32_t>(hv.x));
 #pragma unroll
         for (int j = 0; j < KW / 4; ++j) {
           const float4 r = __ldg(r4 + j);
@@ -419,15 +423,20 @@ __global__ void __launch_bounds__(256, KW <= 24 ? 4 : (KW <= 32 ? 3 : 2)) sign_k
 
 // K > 32: lane k owns columns k, k+32, ... (KS = Kp/32 slabs, Kp =
 // roundup(K,32) so every lane load is in bounds): per step the hits are queued
-// as above (padded to a multiple of 4 with zero-weight entries) and every lane
-// walks the queue (broadcast LDS.64), 4 hits = 4*KS coalesced 128-byte row
-// loads in flight. No transpose; each step's column sums are added to the
-// running total (two-level summation). Dense lane-per-hit accumulators would
-// need 64+ registers per lane and read whole 256-byte rows per hit.
+// as above — with the R row's element offset row*Kp precomputed once per hit
+// instead of by every lane — padded to a multiple of kSignColG with zero-weight
+// entries, and every lane walks the queue (broadcast LDS.128 = two hits),
+// kSignColG hits = kSignColG*KS coalesced 128-byte row loads in flight, each
+// address one IMAD.WIDE from the lane's base. No transpose; each step's
+// column sums are added to the running total (two-level summation). Dense
+// lane-per-hit accumulators would need 64+ registers per lane and read whole
+// 256-byte rows per hit.
+constexpr int kSignColG = 8;
 template <int KS>
 __device__ __forceinline__ void signc_steps(const SignArgs& a, const uint2* __restrict__ e, uint32_t n, uint32_t s0,
                                             uint32_t stride, uint32_t lane, int2* qw, float (&acc)[KS], float& sq) {
   const uint32_t lt = (1u << lane) - 1u;
+  const float* __restrict__ Rl = a.R + lane;  // this lane's column within each 32-column slab
   for (uint32_t c = s0 * kSignStep; c < n; c += stride * kSignStep) {
     uint2 x[4];
 #pragma unroll
@@ -444,26 +453,34 @@ __device__ __forceinline__ void signc_steps(const SignArgs& a, const uint2* __re
       const float w = static_cast<float>(x[u].y) * ti[u].idf;
       sq = fmaf(w, w, sq);
       const uint32_t hits = __ballot_sync(0xffffffffu, ti[u].ref_row >= 0);
-      if (ti[u].ref_row >= 0) qw[qn + __popc(hits & lt)] = make_int2(ti[u].ref_row, __float_as_int(w));
+      if (ti[u].ref_row >= 0)
+        qw[qn + __popc(hits & lt)] = make_int2(static_cast<int>(static_cast<uint32_t>(ti[u].ref_row) * a.Kp),
+                                               __float_as_int(w));
       qn += __popc(hits);
     }
-    const uint32_t qp = (qn + 3) & ~3u;
+    const uint32_t qp = (qn + kSignColG - 1) & ~static_cast<uint32_t>(kSignColG - 1);
     if (lane < qp - qn) qw[qn + lane] = make_int2(0, 0);  // row 0 exists when qn > 0; weight 0 adds +0
     __syncwarp();
     float part[KS];
 #pragma unroll
     for (int t = 0; t < KS; ++t) part[t] = 0.0f;
-    for (uint32_t h = 0; h < qp; h += 4) {
-      int2 hv[4];
+    for (uint32_t h = 0; h < qp; h += kSignColG) {
+      int2 hv[kSignColG];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) hv[j] = qw[h + j];
-      float r[4][KS];
+      for (int j = 0; j < kSignColG; j += 2) {
+        const int4 v = *reinterpret_cast<const int4*>(qw + h + j);
+        hv[j] = make_int2(v.x, v.y);
+        hv[j + 1] = make_int2(v.z, v.w);
+      }
+      float r[kSignColG][KS];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < kSignColG; ++j) {
+        const float* __restrict__ row = Rl + static_cast<uint32_t>(hv[j].x);
 #pragma unroll
-        for (int t = 0; t < KS; ++t) r[j][t] = __ldg(a.R + static_cast<size_t>(hv[j].x) * a.Kp + 32u * t + lane);
+        for (int t = 0; t < KS; ++t) r[j][t] = __ldg(row + 32 * t);
+      }
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < kSignColG; ++j)
 #pragma unroll
         for (int t = 0; t < KS; ++t) part[t] = fmaf(__int_as_float(hv[j].y), r[j][t], part[t]);
     }
@@ -475,7 +492,7 @@ __device__ __forceinline__ void signc_steps(const SignArgs& a, const uint2* __re
 
 template <int KS>
 __global__ void __launch_bounds__(256) sign_col_kernel(SignArgs a) {
-  __shared__ int2 queue[kSignWarps][kSignStep];
+  __shared__ __align__(16) int2 queue[kSignWarps][kSignStep];
   __shared__ float red[kSignWarps][32 * KS + 1];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int2* qw = queue[wid];
