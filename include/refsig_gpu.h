@@ -265,6 +265,10 @@ int refsig_gpu_phase_times(refsig_gpu_ctx* ctx, double* ms, uint64_t* calls);
 #define REFSIG_K3_FP32 1
 #define REFSIG_K3_TENSOR 2
 int refsig_gpu_set_k3_path(refsig_gpu_ctx* ctx, int path);
+/* Debug: with REFSIG_CANARY=1 in the environment every device buffer carries
+ * a guard region past its end; this synchronises and returns 1 (runtime)
+ * naming any buffer whose guard a kernel overwrote. 0 when clean or off. */
+int refsig_gpu_debug_check(refsig_gpu_ctx* ctx);
 /* Kernels launched by this library in this process so far. */
 uint64_t refsig_gpu_launch_count(void);
 

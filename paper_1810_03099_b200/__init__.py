@@ -116,6 +116,7 @@ SIGNATURES = {
                             _c.c_int),
     "refsig_gpu_step_result": ([_c.c_void_p, _P(_c.c_uint64), _c.c_uint64, _P(_c.c_uint64)], _c.c_int),
     "refsig_gpu_set_k3_path": ([_c.c_void_p, _c.c_int], _c.c_int),
+    "refsig_gpu_debug_check": ([_c.c_void_p], _c.c_int),
 }
 K3_AUTO, K3_FP32, K3_TENSOR = 0, 1, 2
 PHASES = ["count", "reference", "sign", "pair_tiles", "pair_emit", "simhash", "h2d", "d2h"]
@@ -453,6 +454,10 @@ class Context:
     def set_k3_path(self, path: int):
         """K3_AUTO / K3_FP32 (CUDA cores) / K3_TENSOR (tcgen05) for the pair calls."""
         self._check(self._L.refsig_gpu_set_k3_path(self._h, int(path)))
+
+    def debug_check(self):
+        """With REFSIG_CANARY=1: raise if a kernel wrote past any device buffer."""
+        self._check(self._L.refsig_gpu_debug_check(self._h))
 
     # -- measurement ----------------------------------------------------------
     def set_profiling(self, on: bool):

@@ -58,6 +58,19 @@ void require(bool ok, const std::string& msg) {
   if (!ok) fail(REFSIG_E_VALIDATION, msg);
 }
 
+// Debug guard (REFSIG_CANARY=1): every device buffer gets kCanaryBytes of
+// 0xA5 past its capacity; refsig_gpu_debug_check verifies them (a kernel that
+// wrote past a buffer's end is reported by name). compute-sanitizer is closed
+// on the GPU pool this was built on; this is the out-of-bounds-write check.
+constexpr size_t kCanaryBytes = 4096;
+bool canary_on() {
+  static const bool on = [] {
+    const char* m = std::getenv("REFSIG_CANARY");
+    return m && m[0] == '1';
+  }();
+  return on;
+}
+
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
@@ -76,9 +89,21 @@ struct DevBuf {
       p = nullptr;
       cap = 0;
     }
-    ck(cudaMalloc(&p, bytes), "cudaMalloc");
+    const size_t extra = canary_on() ? kCanaryBytes : 0;
+    ck(cudaMalloc(&p, bytes + extra), "cudaMalloc");
+    if (extra) ck(cudaMemset(static_cast<char*>(p) + bytes, 0xA5, extra), "canary");
     cap = bytes;
     g_alloc_gen.fetch_add(1);
+    return true;
+  }
+  // true if the canary past cap is intact (or canaries are off)
+  bool canary_ok() const {
+    if (!canary_on() || !p) return true;
+    std::vector<unsigned char> h(kCanaryBytes);
+    if (cudaMemcpy(h.data(), static_cast<const char*>(p) + cap, kCanaryBytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return false;
+    for (unsigned char b : h)
+      if (b != 0xA5) return false;
     return true;
   }
   template <class T>
@@ -203,6 +228,21 @@ struct refsig_gpu_ctx {
   std::vector<Mark> marks;
   std::vector<cudaEvent_t> ev_free;
 
+  // (name, buffer) of every device buffer, for refsig_gpu_debug_check
+  std::vector<std::pair<const char*, const DevBuf*>> buffers() const {
+    return {{"tokens", &tokens}, {"doc_off", &doc_off}, {"plan", &plan}, {"long_off", &long_off},
+            {"long_scratch", &long_scratch}, {"ent", &ent}, {"nnz", &nnz}, {"df", &df}, {"df_rep", &df_rep},
+            {"info", &info}, {"flags", &flags}, {"rowptr", &rowptr}, {"c_ids", &c_ids}, {"c_counts", &c_counts},
+            {"inv_norm", &inv_norm}, {"ref_docs", &ref_docs}, {"ref_start", &ref_start}, {"ref_n", &ref_n},
+            {"ref_ent", &ref_ent}, {"ref_count", &ref_count}, {"R", &R}, {"S", &S}, {"ST", &ST}, {"bitmap", &bitmap},
+            {"rowcnt", &rowcnt}, {"rowstart", &rowstart}, {"cand", &cand}, {"scan_tmp", &scan_tmp}, {"keys", &keys},
+            {"emit_ctr", &emit_ctr}, {"cand16", &cand16}, {"text", &text}, {"text_off", &text_off},
+            {"text_cnt", &text_cnt}, {"fp", &fp}, {"term_hash", &term_hash}, {"x", &x}, {"post_off", &post_off},
+            {"post_fill", &post_fill}, {"posts", &posts}, {"head_col", &head_col}, {"headA", &headA},
+            {"head_norm", &head_norm}, {"tail_df", &tail_df}, {"headAT", &headAT}, {"eval_tail", &eval_tail},
+            {"eval_part", &eval_part}, {"cf_rep", &cf_rep}, {"cf", &cf}, {"records", &records},
+            {"tc_forms", &tc_forms}};
+  }
   ~refsig_gpu_ctx() {
     for (auto& m : marks) {
       cudaEventDestroy(m.a);
@@ -1557,6 +1597,17 @@ int refsig_gpu_phase_times(refsig_gpu_ctx* ctx, double* ms, uint64_t* calls) {
 }
 
 uint64_t refsig_gpu_launch_count(void) { return g_launches.load(); }
+
+int refsig_gpu_debug_check(refsig_gpu_ctx* ctx) {
+  return guard(ctx, [&] {
+    sync(ctx);
+    ck(cudaDeviceSynchronize(), "device sync");
+    std::string bad;
+    for (auto& nb : ctx->buffers())
+      if (!nb.second->canary_ok()) bad += std::string(bad.empty() ? "" : ", ") + nb.first;
+    if (!bad.empty()) fail(REFSIG_E_RUNTIME, "write past the end of device buffer(s): " + bad);
+  });
+}
 
 int refsig_gpu_set_k3_path(refsig_gpu_ctx* ctx, int path) {
   return guard(ctx, [&] {
