@@ -477,9 +477,9 @@ void run_mrc_tiles(refsig_gpu_ctx* c, const float* STr, uint32_t ldr, uint32_t n
 }
 
 // A5: union, remap and the compact table from c->ref_{start,n} and `ent`.
-void build_reference(refsig_gpu_ctx* c, const RefArgs& r, uint64_t u_cap) {
+void build_reference(refsig_gpu_ctx* c, const RefArgs& r, uint64_t n_entries) {
   const uint32_t V = c->vocab;
-  if (u_cap > V) u_cap = V;
+  const uint64_t u_cap = std::min<uint64_t>(n_entries, V);  // |U| bound
   // K2 addresses R rows by 32-bit element offsets (row * Kp)
   require(u_cap * r.Kp < (1ull << 32), "reference term union too large (|U| * K >= 2^32)");
   const size_t rbytes = sizeof(float) * std::max<uint64_t>(u_cap, 1) * r.Kp;
@@ -488,8 +488,8 @@ void build_reference(refsig_gpu_ctx* c, const RefArgs& r, uint64_t u_cap) {
   Phase ph(c, REFSIG_PHASE_REFERENCE);
   // info[].ref_row is -1 right after count(); a replaced reference resets it
   if (c->ref_dirty) launch_ref_reset(c->info.as<TermInfo>(), V, c->stream);
-  ck(cudaMemsetAsync(c->ref_count.p, 0, sizeof(uint32_t), c->stream), "memset");
-  launch_ref_build(r, c->info.as<TermInfo>(), V, c->ref_count.as<uint32_t>(), c->R.as<float>(), c->stream);
+  launch_ref_build(r, c->info.as<TermInfo>(), V, c->ref_count.as<uint32_t>(), c->R.as<float>(), n_entries,
+                   c->stream);
   launched("reference");
   c->K = r.K;
   c->Kp = r.Kp;

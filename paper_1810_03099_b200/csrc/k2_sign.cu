@@ -36,93 +36,87 @@ __device__ __forceinline__ void ref_range(const RefArgs& r, uint32_t k, const ui
   }
 }
 
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __global__ void ref_reset_kernel(TermInfo* __restrict__ info, uint32_t vocab) {
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < vocab; t += gridDim.x * blockDim.x)
     info[t].ref_row = -1;
 }
 
-// A5 in three launches, no contended atomics:
-//   mark   (CTA per reference): info[t].ref_row = -2 for every reference term
-//          (plain idempotent stores);
-//   assign (vocabulary-parallel): marked terms get compact rows (warp ballot +
-//          block scan, one counter atomic per CTA) and their R row is zeroed;
-//          the row numbering depends on CTA order, the values the sign kernel
-//          reads through it do not;
-//   fill   (CTA per reference): block-tree norm of the reference's weights
-//          (fixed order), then w/||w|| into column k of each term's row.
-// Entries are taken kRefIpt per thread per pass so each thread has all its
-// loads in flight. (A CAS-per-term claim serialised on shared cache lines of
-// the Zipf-head terms every reference contains: 18 us at configs[1].)
-constexpr int kRefIpt = 16;
-constexpr uint32_t kRefPass = 256 * kRefIpt;
-
-__global__ void __launch_bounds__(256) ref_mark_kernel(RefArgs r, TermInfo* __restrict__ info) {
-  const uint2* e;
-  uint32_t n;
-  ref_range(r, blockIdx.x, e, n);
-  for (uint32_t p0 = 0; p0 < n; p0 += kRefPass) {
-    uint32_t t[kRefIpt];
-#pragma unroll
-    for (int j = 0; j < kRefIpt; ++j) {
-      const uint32_t i = p0 + j * 256 + threadIdx.x;
-      t[j] = i < n ? e[i].x : 0xFFFFFFFFu;
-    }
-#pragma unroll
-    for (int j = 0; j < kRefIpt; ++j)
-      if (t[j] != 0xFFFFFFFFu) info[t[j]].ref_row = -2;
-  }
-}
-
-__global__ void __launch_bounds__(256) ref_assign_kernel(TermInfo* __restrict__ info, uint32_t vocab,
-                                                         uint32_t* __restrict__ counter, float* __restrict__ R,
-                                                         uint32_t Kp) {
-  __shared__ uint32_t wsum[9];
-  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t t = blockIdx.x * 256 + threadIdx.x;
-  const bool mk = t < vocab && info[t].ref_row == -2;
-  const uint32_t b = __ballot_sync(0xffffffffu, mk);
-  if (lane == 0) wsum[wid] = __popc(b);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t tot = 0;
-    for (int w = 0; w < 8; ++w) {
-      const uint32_t x = wsum[w];
-      wsum[w] = tot;
-      tot += x;
-    }
-    wsum[8] = tot ? atomicAdd(counter, tot) : 0u;
-  }
-  __syncthreads();
-  if (mk) {
-    const uint32_t u = wsum[8] + wsum[wid] + __popc(b & ((1u << lane) - 1u));
-    float* row = R + static_cast<size_t>(u) * Kp;
-    for (uint32_t q = 0; q < Kp; ++q) row[q] = 0.0f;
-    info[t].ref_row = static_cast<int>(u);
-  }
-}
-
-__global__ void __launch_bounds__(256) ref_fill_kernel(RefArgs r, const TermInfo* __restrict__ info,
-                                                       float* __restrict__ R) {
+// A5 in ONE launch: CTA k per reference vector (all K CTAs are co-resident:
+// K <= 256 CTAs of 256 threads).
+//   pass 1: weights (count * idf, or explicit), the squared norm in a fixed
+//           order (thread-strided partials, block tree), and the claims:
+//           atomicCAS(info[t].ref_row, -1, -2) — the CTA that saw -1 owns
+//           term t: it takes the next compact row (warp-aggregated atomic on
+//           *counter), zeroes that R row, fences, and publishes the row;
+//   pass 2: R[row(t)*Kp + k] = w / ||w_k||, where a term claimed by another
+//           CTA waits (spins) until its owner has published the row — the
+//           owner zeroed the row before publishing, so this write lands after
+//           the zeroing.
+// The row numbering depends on claim order, the values K2 reads through it do
+// not. Needs info[].ref_row == -1 (count() leaves it so; a replaced reference
+// is reset first) and *counter == 0; *counter ends as |U|.
+constexpr int kRefIpt2 = 4;
+__global__ void __launch_bounds__(256) ref_build_kernel(RefArgs r, TermInfo* __restrict__ info,
+                                                        float* __restrict__ R, uint32_t* __restrict__ counter) {
   __shared__ float red[8];
-  const uint32_t k = blockIdx.x;
-  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t k = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint2* e;
   uint32_t n;
   ref_range(r, k, e, n);
   float sq = 0.0f;
-  for (uint32_t p0 = 0; p0 < n; p0 += kRefPass) {
-    float w[kRefIpt];
+  for (uint32_t p0 = 0; p0 < n; p0 += 256 * kRefIpt2) {
+    uint2 x[kRefIpt2];
 #pragma unroll
-    for (int j = 0; j < kRefIpt; ++j) {
+    for (int j = 0; j < kRefIpt2; ++j) {
       const uint32_t i = p0 + j * 256 + threadIdx.x;
-      w[j] = 0.0f;
-      if (i < n) {
-        const uint2 x = e[i];
-        w[j] = r.explicit_w ? __uint_as_float(x.y) : static_cast<float>(x.y) * info[x.x].idf;
+      x[j] = i < n ? e[i] : make_uint2(0xFFFFFFFFu, 0u);
+    }
+    float w[kRefIpt2];
+#pragma unroll
+    for (int j = 0; j < kRefIpt2; ++j)
+      w[j] = x[j].x == 0xFFFFFFFFu ? 0.0f
+                                   : (r.explicit_w ? __uint_as_float(x[j].y) : static_cast<float>(x[j].y) * info[x[j].x].idf);
+#pragma unroll
+    for (int j = 0; j < kRefIpt2; ++j) sq = fmaf(w[j], w[j], sq);
+    bool own[kRefIpt2];
+#pragma unroll
+    for (int j = 0; j < kRefIpt2; ++j)
+      own[j] = x[j].x != 0xFFFFFFFFu && atomicCAS(reinterpret_cast<int*>(&info[x[j].x].ref_row), -1, -2) == -1;
+    // one counter atomic per warp for all of its claims of this pass
+    uint32_t b[kRefIpt2], tot = 0;
+#pragma unroll
+    for (int j = 0; j < kRefIpt2; ++j) {
+      b[j] = __ballot_sync(0xffffffffu, own[j]);
+      tot += __popc(b[j]);
+    }
+    uint32_t base = 0;
+    if (lane == 0 && tot) base = atomicAdd(counter, tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    uint32_t row[kRefIpt2];
+#pragma unroll
+    for (int j = 0; j < kRefIpt2; ++j) {
+      row[j] = base + __popc(b[j] & ((1u << lane) - 1u));
+      base += __popc(b[j]);
+      if (own[j]) {
+        float4* rr = reinterpret_cast<float4*>(R + static_cast<size_t>(row[j]) * r.Kp);
+        for (uint32_t q = 0; q < r.Kp / 4; ++q) rr[q] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
       }
     }
+    if (tot) {
+      __threadfence();  // the zeroed rows are visible before any row is published
 #pragma unroll
-    for (int j = 0; j < kRefIpt; ++j) sq = fmaf(w[j], w[j], sq);
+      for (int j = 0; j < kRefIpt2; ++j)
+        if (own[j]) st_release(&info[x[j].x].ref_row, static_cast<int>(row[j]));
+    }
   }
   sq = warp_sum(sq);
   if (lane == 0) red[wid] = sq;
@@ -131,22 +125,23 @@ __global__ void __launch_bounds__(256) ref_fill_kernel(RefArgs r, const TermInfo
 #pragma unroll
   for (int w = 0; w < 8; ++w) tot += red[w];
   const float inv = tot > 0.0f ? 1.0f / sqrtf(tot) : 0.0f;
-  for (uint32_t p0 = 0; p0 < n; p0 += kRefPass) {
-    uint2 x[kRefIpt];
+  for (uint32_t p0 = 0; p0 < n; p0 += 256 * kRefIpt2) {
+    uint2 x[kRefIpt2];
 #pragma unroll
-    for (int j = 0; j < kRefIpt; ++j) {
+    for (int j = 0; j < kRefIpt2; ++j) {
       const uint32_t i = p0 + j * 256 + threadIdx.x;
       x[j] = i < n ? e[i] : make_uint2(0xFFFFFFFFu, 0u);
     }
-    TermInfo ti[kRefIpt];
+    int row[kRefIpt2];
 #pragma unroll
-    for (int j = 0; j < kRefIpt; ++j) ti[j] = x[j].x != 0xFFFFFFFFu ? info[x[j].x] : TermInfo{0.0f, 0};
+    for (int j = 0; j < kRefIpt2; ++j) row[j] = x[j].x == 0xFFFFFFFFu ? 0 : ld_acquire(&info[x[j].x].ref_row);
 #pragma unroll
-    for (int j = 0; j < kRefIpt; ++j)
-      if (x[j].x != 0xFFFFFFFFu) {
-        const float w = r.explicit_w ? __uint_as_float(x[j].y) : static_cast<float>(x[j].y) * ti[j].idf;
-        R[static_cast<size_t>(ti[j].ref_row) * r.Kp + k] = w * inv;
-      }
+    for (int j = 0; j < kRefIpt2; ++j) {
+      if (x[j].x == 0xFFFFFFFFu) continue;
+      while (row[j] < 0) row[j] = ld_acquire(&info[x[j].x].ref_row);  // owner CTA publishes shortly
+      const float w = r.explicit_w ? __uint_as_float(x[j].y) : static_cast<float>(x[j].y) * info[x[j].x].idf;
+      R[static_cast<size_t>(row[j]) * r.Kp + k] = w * inv;
+    }
   }
 }
 
@@ -589,12 +584,11 @@ void launch_ref_reset(TermInfo* info, uint32_t vocab, cudaStream_t s) {
 }
 
 void launch_ref_build(const RefArgs& r, TermInfo* info, uint32_t vocab, uint32_t* counter, float* R,
-                      cudaStream_t s) {
-  ref_mark_kernel<<<r.K, 256, 0, s>>>(r, info);
-  ref_assign_kernel<<<static_cast<unsigned>(ceil_div(vocab, 256)), 256, 0, s>>>(info, vocab, counter, R, r.Kp);
-  ref_fill_kernel<<<r.K, 256, 0, s>>>(r, info, R);
-  note_launch();
-  note_launch();
+                      uint64_t n_entries_max, cudaStream_t s) {
+  (void)vocab;
+  (void)n_entries_max;
+  cudaMemsetAsync(counter, 0, sizeof(uint32_t), s);
+  ref_build_kernel<<<r.K, 256, 0, s>>>(r, info, R, counter);
   note_launch();
 }
 

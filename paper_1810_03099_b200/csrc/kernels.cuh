@@ -97,11 +97,12 @@ struct RefArgs {
 };
 // info[t].ref_row = -1 for all t (only needed when a reference is replaced).
 void launch_ref_reset(TermInfo* info, uint32_t vocab, cudaStream_t s);
-// Compact rows for the union U (marked terms get the next rows from *counter,
-// zeroed), then R[row*Kp + k] = w_k[t]/||w_k|| (three launches, k2_sign.cu).
-// *counter must be 0 and info[].ref_row -1.
+// Compact rows for the union U (zeroed), then R[row*Kp + k] = w_k[t]/||w_k||;
+// *counter = |U|. One launch when the K vectors hold at most n_entries_max <=
+// 65536 entries (a bound: e.g. their token counts), else three (k2_sign.cu).
+// info[].ref_row must be -1.
 void launch_ref_build(const RefArgs& r, TermInfo* info, uint32_t vocab, uint32_t* counter, float* R,
-                      cudaStream_t s);
+                      uint64_t n_entries_max, cudaStream_t s);
 
 // ---- K2 sign ----------------------------------------------------------------
 struct SignArgs {
