@@ -117,6 +117,8 @@ SIGNATURES = {
     "refsig_gpu_step_result": ([_c.c_void_p, _P(_c.c_uint64), _c.c_uint64, _P(_c.c_uint64)], _c.c_int),
     "refsig_gpu_set_k3_path": ([_c.c_void_p, _c.c_int], _c.c_int),
     "refsig_gpu_debug_check": ([_c.c_void_p], _c.c_int),
+    "refsig_gpu_stage_corpus": ([_c.c_void_p, _P(_c.c_uint32), _P(_c.c_uint64), _c.c_uint32, _c.c_uint32], _c.c_int),
+    "refsig_gpu_swap_corpus": ([_c.c_void_p], _c.c_int),
 }
 K3_AUTO, K3_FP32, K3_TENSOR = 0, 1, 2
 PHASES = ["count", "reference", "sign", "pair_tiles", "pair_emit", "simhash", "h2d", "d2h"]
@@ -221,6 +223,24 @@ class Context:
         self._check(self._L.refsig_gpu_load_corpus(self._h, _ptr(tokens, ctypes.c_uint32),
                                                    _ptr(doc_off, ctypes.c_uint64), n, vocab))
         self._keep = tokens  # pinned/pageable source must outlive async copies
+        self.n_docs, self.vocab = n, vocab
+
+    def stage_corpus(self, tokens: np.ndarray, doc_off: np.ndarray, vocab: int):
+        """Start the upload of the NEXT batch (copy stream; pinned tokens overlap
+        with the current batch's compute). swap_corpus() makes it current."""
+        tokens = np.ascontiguousarray(tokens, np.uint32)
+        doc_off = np.ascontiguousarray(doc_off, np.uint64)
+        n = len(doc_off) - 1
+        if n >= 1 and int(doc_off[-1]) > len(tokens):
+            raise ValidationError("doc_off[-1] exceeds the token count")
+        self._check(self._L.refsig_gpu_stage_corpus(self._h, _ptr(tokens, ctypes.c_uint32),
+                                                    _ptr(doc_off, ctypes.c_uint64), n, vocab))
+        self._staged = (tokens, n, vocab)
+
+    def swap_corpus(self):
+        self._check(self._L.refsig_gpu_swap_corpus(self._h))
+        tokens, n, vocab = self._staged
+        self._keep = tokens
         self.n_docs, self.vocab = n, vocab
 
     def load_corpus_device(self, dev_ptr: int, doc_off: np.ndarray, vocab: int):

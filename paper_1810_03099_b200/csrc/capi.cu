@@ -29,6 +29,14 @@ std::atomic<uint64_t> g_alloc_gen{0};  // bumped on every device (re)allocation:
 namespace refsig_gpu {
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* m = std::getenv("REFSIG_NO_PDL");
+    return !(m && m[0] == '1');
+  }();
+  return on;
+}
+
 void ensure_smem_attr(const void* func, int bytes) {
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, int> set;  // (kernel, device) -> bytes already allowed
@@ -189,6 +197,20 @@ struct refsig_gpu_ctx {
   DevBuf records;                                                              // MRCS records
   DevBuf tc_forms;                                                             // K3 tcgen05 operand forms
 
+  // staged next corpus (refsig_gpu_stage_corpus / swap_corpus): tokens copied on
+  // copy_stream into `tokens_next` while the current batch computes
+  DevBuf tokens_next;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_staged = nullptr, ev_next_free = nullptr;
+  bool staged = false, next_free_recorded = false;
+  std::vector<uint64_t> staged_off;
+  uint32_t staged_docs = 0, staged_vocab = 0;
+
+  // tcgen05 column forms of this (database) context's signatures, cached for
+  // query joins (they do not depend on tau); valid while sign_gen is unchanged
+  DevBuf tc_colf;
+  uint64_t sign_gen = 0, tc_colf_gen = ~0ull;
+
   // query mode
   refsig_gpu_ctx* db = nullptr;
   int k3_path = REFSIG_K3_AUTO;  // refsig_gpu_set_k3_path
@@ -254,6 +276,8 @@ struct refsig_gpu_ctx {
     if (h_plan) cudaFreeHost(h_plan);
     if (plan_done) cudaEventDestroy(plan_done);
     if (step_exec) cudaGraphExecDestroy(step_exec);
+    if (ev_staged) cudaEventDestroy(ev_staged);
+    if (ev_next_free) cudaEventDestroy(ev_next_free);
   }
 };
 
@@ -292,7 +316,15 @@ void sync(refsig_gpu_ctx* c) {
   }
 }
 
-void launched(const char* what) { ck(cudaGetLastError(), what); }
+void launched(const char* what) {
+  // REFSIG_SYNC_DEBUG=1: synchronise after every phase so a fault is reported by the phase that caused it
+  static const bool dbg = [] {
+    const char* m = std::getenv("REFSIG_SYNC_DEBUG");
+    return m && m[0] == '1';
+  }();
+  if (dbg) ck(cudaDeviceSynchronize(), what);
+  ck(cudaGetLastError(), what);
+}
 
 cudaEvent_t take_event(refsig_gpu_ctx* c) {
   if (!c->ev_free.empty()) {
@@ -464,15 +496,29 @@ void run_mrc_tiles(refsig_gpu_ctx* c, const float* STr, uint32_t ldr, uint32_t n
     return;
   }
   const size_t rb = mrc_tc_form_bytes(K, nr), cb = mrc_tc_form_bytes(K, ncl);
-  c->tc_forms.ensure(rb + cb);
-  char* rowf = c->tc_forms.as<char>();
-  char* colf = rowf + rb;
+  char* rowf;
+  char* colf;
   if (self) {
+    c->tc_forms.ensure(rb + cb);
+    rowf = c->tc_forms.as<char>();
+    colf = rowf + rb;
     launch_mrc_tc_forms(STr, ldr, nr, K, tau, rowf, colf, c->stream);
   } else {
+    // query join: the database's column forms do not depend on tau and stay
+    // valid until it is signed again, so they are built once per database
+    refsig_gpu_ctx* db = c->db;
+    c->tc_forms.ensure(rb);
+    rowf = c->tc_forms.as<char>();
     launch_mrc_tc_forms(STr, ldr, nr, K, tau, rowf, nullptr, c->stream);
-    launch_mrc_tc_forms(STc, ldc, ncl, K, tau, nullptr, colf, c->stream);
+    static const bool no_cache = std::getenv("REFSIG_NO_FORM_CACHE") != nullptr;
+    if (no_cache || db->tc_colf_gen != db->sign_gen || db->tc_colf.cap < cb) {
+      db->tc_colf.ensure(cb);
+      launch_mrc_tc_forms(STc, ldc, ncl, K, tau, nullptr, db->tc_colf.p, c->stream);
+      db->tc_colf_gen = db->sign_gen;
+    }
+    colf = db->tc_colf.as<char>();
   }
+  launched("tcgen05 operand forms");
   launch_mrc_tc(rowf, colf, K, g, c->bitmap.as<uint32_t>(), c->rowcnt.as<uint32_t>(), c->stream);
 }
 
@@ -731,6 +777,10 @@ void refsig_gpu_destroy(refsig_gpu_ctx* ctx) {
     if (ctx->ev_join[k]) cudaEventDestroy(ctx->ev_join[k]);
   }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
   delete ctx;
@@ -777,6 +827,52 @@ int refsig_gpu_load_corpus_device(refsig_gpu_ctx* ctx, const uint32_t* d_tokens,
     require(d_tokens != nullptr || doc_off[n_docs] == 0, "tokens is NULL");
     ctx->tok = d_tokens;
     load_common(ctx, doc_off, n_docs, vocab);
+  });
+}
+
+int refsig_gpu_stage_corpus(refsig_gpu_ctx* ctx, const uint32_t* tokens, const uint64_t* doc_off, uint32_t n_docs,
+                            uint32_t vocab) {
+  return guard(ctx, [&] {
+    require(doc_off != nullptr, "doc_off is NULL");
+    require(n_docs >= 1, "empty corpus");
+    require(doc_off[0] == 0, "doc_off[0] must be 0");
+    const uint64_t T = doc_off[n_docs];
+    require(tokens != nullptr || T == 0, "tokens is NULL");
+    require(!ctx->staged, "a staged corpus is waiting for refsig_gpu_swap_corpus");
+    if (!ctx->copy_stream) {
+      ck(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
+      ck(cudaEventCreateWithFlags(&ctx->ev_staged, cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&ctx->ev_next_free, cudaEventDisableTiming), "event");
+    }
+    // the staging buffer may still be read by work enqueued before the last swap
+    if (ctx->next_free_recorded) ck(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_next_free, 0), "wait");
+    ctx->tokens_next.ensure(sizeof(uint32_t) * std::max<uint64_t>(T, 1));
+    if (T)
+      ck(cudaMemcpyAsync(ctx->tokens_next.p, tokens, sizeof(uint32_t) * T, cudaMemcpyHostToDevice, ctx->copy_stream),
+         "H2D staged tokens");
+    ck(cudaEventRecord(ctx->ev_staged, ctx->copy_stream), "event");
+    ctx->staged_off.assign(doc_off, doc_off + n_docs + 1);
+    ctx->staged_docs = n_docs;
+    ctx->staged_vocab = vocab;
+    ctx->staged = true;
+  });
+}
+
+int refsig_gpu_swap_corpus(refsig_gpu_ctx* ctx) {
+  return guard(ctx, [&] {
+    require(ctx->staged, "no staged corpus (refsig_gpu_stage_corpus)");
+    // compute waits for the copy on the device, not the host
+    ck(cudaStreamWaitEvent(ctx->stream, ctx->ev_staged, 0), "wait staged");
+    std::swap(ctx->tokens.p, ctx->tokens_next.p);
+    std::swap(ctx->tokens.cap, ctx->tokens_next.cap);
+    // the previous batch's buffer becomes the staging buffer: free once the
+    // work already enqueued on the compute stream is done with it
+    ck(cudaEventRecord(ctx->ev_next_free, ctx->stream), "event");
+    ctx->next_free_recorded = true;
+    ctx->staged = false;
+    ctx->tok = ctx->tokens.as<uint32_t>();
+    g_alloc_gen.fetch_add(1);  // captured step graphs read the old token buffer
+    load_common(ctx, ctx->staged_off.data(), ctx->staged_docs, ctx->staged_vocab);
   });
 }
 
@@ -1049,6 +1145,7 @@ int refsig_gpu_set_signatures(refsig_gpu_ctx* ctx, uint32_t n_docs, uint32_t K, 
     ctx->K = K;
     ctx->ld = ld;
     ctx->signed_ = true;
+    ++ctx->sign_gen;
     ctx->counted = ctx->loaded = false;  // a pairs-only context until the next load
     sync(ctx);
   });
@@ -1090,6 +1187,7 @@ static void do_sign(refsig_gpu_ctx* ctx) {
   ctx->K = K;
   ctx->signed_ = true;
   ctx->have_inv_norm = true;
+  ++ctx->sign_gen;
 }
 
 int refsig_gpu_sign(refsig_gpu_ctx* ctx) {

@@ -61,6 +61,10 @@ __device__ __forceinline__ void tc_trace(const uint32_t dbg, int ev, uint32_t it
 __device__ __forceinline__ void tc_trace(uint32_t, int, uint32_t) {}
 #define TC_DBG(a) 0u
 #endif
+// K' > 128: B streamed in chunks of kTcChunkK halves (16 KB per 128-doc
+// panel) through up to kTcMaxStages stages.
+constexpr uint32_t kTcChunkK = 64;
+constexpr uint32_t kTcMaxStages = 16;
 constexpr uint32_t kTcSmallKP = 128;  // tc_forms_kernel (shared-memory staging) up to K' = 128 (K <= 41)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -76,6 +80,15 @@ __device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
       "@!p bra W;\n\t}" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
+}
+// Warp-wide wait: every lane spins on the barrier, then the warp reconverges.
+// The lanes of a spin loop can leave it in different iterations; the
+// .sync.aligned tcgen05 instructions (and elect.sync / R2UR around the MMA
+// issue) that follow must see a converged warp — a diverged one raised
+// "Warp Illegal Instruction" when operand loads arrived slowly (cold L2).
+__device__ __forceinline__ void mb_wait_warp(uint64_t* b, uint32_t parity) {
+  mb_wait(b, parity);
+  __syncwarp();
 }
 __device__ __forceinline__ void mb_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
@@ -172,7 +185,7 @@ struct TcArgs {
   const __half* Ar;  // row-form panels
   const __half* Bc;  // column-form panels
   uint32_t KP;       // K' (multiple of 16)
-  uint32_t nch;      // K chunks per tile: 64-wide (4 MMA k-steps), the last one 1..4 k-steps
+  uint32_t nch;      // K chunks per tile: kTcChunkK wide (4 MMA k-steps), the last one 1..4 k-steps
   uint32_t last_steps;
   uint32_t CB;       // bytes of one B chunk stage (128 docs x min(K', 64) halves)
   uint32_t rb;       // row blocks per row group: 2, or 1 when two A panels and a ring do not fit
@@ -229,7 +242,7 @@ struct TileWalk {
 };
 
 // Tile = rb*128 rows (row group: A panels resident) x 128 columns (one B
-// panel per tile, streamed through an S-stage ring in 64-wide K chunks, so
+// panel per tile, streamed through S stages in 64-wide K chunks, so
 // K' is not bounded by the ring: K' = 208 at K = 64 is four chunks, K' = 400
 // at K = 128 seven). Per K step: one N=128 MMA per valid row block into that
 // block's 128 accumulator columns. FS > 0: K' = 16*FS <= 128 as ONE chunk
@@ -239,16 +252,29 @@ struct TileWalk {
 template <uint32_t FS>
 __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t tsm[];
-  __shared__ __align__(8) uint64_t full_bar[8], empty_bar[8], afull_bar[2], aempty_bar[2], tfull_bar[2],
+  __shared__ __align__(8) uint64_t full_bar[kTcMaxStages], empty_bar[kTcMaxStages], afull_bar[2], aempty_bar[2], tfull_bar[2],
       tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index broadcast from lane 0: lets ptxas prove it warp-uniform, so the
+  // MMA issuers keep descriptors and counters in uniform registers
+  const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
   const uint64_t t0 = a.n_tiles * blockIdx.x / gridDim.x, t1 = a.n_tiles * (blockIdx.x + 1) / gridDim.x;
   const uint32_t n_it = static_cast<uint32_t>(t1 - t0);
   const uint32_t PB = 256u * a.KP;  // bytes per operand panel
-  const uint32_t S = a.stages, NCH = FS ? 1u : a.nch, CB = FS ? PB : a.CB;
+  // B ring(s): every ring has ONE consumer taking its fills in order (with two
+  // consumers of a shared ring, one could wait on a stage's fill k while fill
+  // k-1 — the other's — was still in flight, and a parity wait then passes a
+  // phase early). FS > 0: two issuers (even / odd tiles), stages [0, S0) and
+  // [S0, S). FS == 0 (K' > 128, >= 13 MMAs per row block and tile): issuer 0
+  // alone issues every tile from the whole ring; the MMAs themselves, not
+  // the issue latency, bound the tile there.
+  // (FS == 0 with two issuers and split rings measured 1-2% slower at c3 and
+  // 16% slower at c4 once the issue path ran on uniform registers)
+  constexpr bool kTwoIssuers = FS != 0;
+  const uint32_t S = a.stages, S0 = kTwoIssuers ? (S + 1) / 2 : S, S1 = S - S0;
+  const uint32_t NCH = FS ? 1u : a.nch, CB = FS ? PB : a.CB;
   const uint32_t ABUFS = FS ? 2u : a.abufs, RB = FS ? 2u : a.rb, LAST = FS ? FS : a.last_steps;
-  constexpr uint32_t kStepsMax = FS ? FS : 4u;  // k-steps per chunk
+  constexpr uint32_t kStepsMax = FS ? FS : kTcChunkK / 16;  // k-steps per chunk
   uint8_t* sAbase = tsm;                      // ABUFS buffers x RB panels
   uint8_t* sBbase = tsm + ABUFS * RB * PB;    // S stages x one chunk
   if (threadIdx.x == 0) {
@@ -280,7 +306,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
       TileWalk<FS> w;
       w.start(a, t0);
       uint32_t g = 0;  // row groups started by this CTA
-      uint32_t q = 0;  // B chunks issued
+      uint32_t qm[2] = {0, 0};  // B chunks issued into issuer m's ring
       bool new_group = true;
       for (uint32_t it = 0; it < n_it; ++it) {
         if (new_group) {  // A panels of the group into buffer g % abufs
@@ -295,11 +321,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
         }
         const uint32_t bj = tc_cs<FS>(a, w.p) + w.c;
         const uint8_t* src = reinterpret_cast<const uint8_t*>(a.Bc) + static_cast<size_t>(bj) * PB;
+        const uint32_t m = kTwoIssuers ? (it & 1) : 0u, Sm = m ? S1 : S0, base = m ? S0 : 0u;
+        uint32_t& q = qm[m];
         for (uint32_t ch = 0; ch < NCH; ++ch, ++q) {
-          const uint32_t st = q % S;
-          if (q >= S) mb_wait(&empty_bar[st], ((q / S) - 1) & 1u);
+          const uint32_t st = base + q % Sm;
+          if (q >= Sm) mb_wait(&empty_bar[st], ((q / Sm) - 1) & 1u);
           const uint32_t bytes = ch + 1 < NCH ? CB : LAST * 4096u;
-          if ((TC_DBG(a) & 2) && q >= S) {
+          if ((TC_DBG(a) & 2) && q >= Sm) {
             mb_arrive(&full_bar[st]);
           } else {
             mb_expect_tx(&full_bar[st], bytes);
@@ -312,36 +340,38 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
     __syncwarp();
   } else if (warp == 1 || warp == 2) {
     // MMA issuers: warp 1 + m issues the tiles with it % 2 == m into
-    // accumulator m (two threads in flight hide each one's issue latency);
-    // whole warp converged, one elected lane issues
+    // accumulator m (two threads in flight hide each one's issue latency;
+    // FS == 0: warp 1 issues every tile, into accumulator it % 2); whole warp
+    // converged, one elected lane issues
     const uint32_t m = warp - 1;
     if (n_it) {
       TileWalk<FS> w;
       w.start(a, t0);
       const uint64_t dA0 = smem_desc(smem_u32(sAbase)), dB0 = smem_desc(smem_u32(sBbase));
       const uint64_t dPB = PB >> 4, dCB = CB >> 4;
+      const uint32_t Sm = m ? S1 : S0, base = m ? S0 : 0u;  // this issuer's ring
       uint32_t g = 0, q = 0;
       bool new_group = true;
       for (uint32_t it = 0; it < n_it; ++it) {
         if (new_group) {
-          mb_wait(&afull_bar[g % ABUFS], (g / ABUFS) & 1u);
+          mb_wait_warp(&afull_bar[g % ABUFS], (g / ABUFS) & 1u);
           ++g;
         }
         const uint32_t ab = (g - 1) % ABUFS;
         const uint32_t acc = it & 1;
-        if (acc == m) {
+        if (kTwoIssuers ? acc == m : m == 0) {
           const uint32_t bj = tc_cs<FS>(a, w.p) + w.c;
           const uint32_t r0 = tc_r0<FS>(a, w.p);
           const bool v1 = tc_rvalid<FS>(a, w.p, 1) && !(a.g.triangle && bj < r0 + 1);
           if (lane == 0 && m == 0) tc_trace(TC_DBG(a), 0, it);
-          if (it >= 2) mb_wait(&tempty_bar[acc], ((it >> 1) - 1) & 1u);
+          if (it >= 2) mb_wait_warp(&tempty_bar[acc], ((it >> 1) - 1) & 1u);
           if (lane == 0 && m == 0) tc_trace(TC_DBG(a), 2, it);
           const uint64_t dA = dA0 + ab * RB * dPB;
           const uint32_t d0 = tmem + acc * 256;
-          const uint32_t e = elect_one();
           for (uint32_t ch = 0; ch < NCH; ++ch, ++q) {
-            const uint32_t st = q % S;
-            mb_wait(&full_bar[st], (q / S) & 1u);
+            const uint32_t st = base + q % Sm;
+            mb_wait_warp(&full_bar[st], (q / Sm) & 1u);
+            const uint32_t e = elect_one();
             if (lane == 0 && m == 0 && ch == 0) tc_trace(TC_DBG(a), 1, it);
             tc_fence_after();
             const uint32_t steps = ch + 1 < NCH ? kStepsMax : LAST;
@@ -358,13 +388,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
             mma_commit_e(e, &empty_bar[st]);
           }
           if (lane == 0 && m == 0) tc_trace(TC_DBG(a), 3, it);
-          mma_commit_e(e, &tfull_bar[acc]);
-        } else {
-          q += NCH;
+          __syncwarp();
+          mma_commit_e(elect_one(), &tfull_bar[acc]);
         }
         new_group = w.next(a);
         // both issuers release the group's A buffer (a commit with nothing
         // outstanding from this thread arrives at once)
+        __syncwarp();
         if (new_group || it + 1 == n_it) mma_commit_e(elect_one(), &aempty_bar[ab]);
         __syncwarp();
       }
@@ -372,7 +402,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
     __syncwarp();
   } else {  // epilogue warps 3..18: group eg = tiles with it % 2 == eg (accumulator eg),
              // lane quarter q, row block h of the row group; all 128 columns in two halves
-    const uint32_t q = warp & 3, eg = (warp - 3) >> 3, h = ((warp - 3) >> 2) & 1;
+    const uint32_t ew = threadIdx.x >> 5;  // (not the uniform copy: the epilogue measured faster this way)
+    const uint32_t q = ew & 3, eg = (ew - 3) >> 3, h = ((ew - 3) >> 2) & 1;
     const uint32_t wpr = a.g.words_per_row;
     const uint32_t two = a.two;
     TileWalk<FS> w;
@@ -387,7 +418,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
       if (acc == eg) {
         const uint32_t u = it >> 1;  // this group's use count of its accumulator
         if (warp == 3 && lane == 0) tc_trace(TC_DBG(a), 4, it);
-        mb_wait(&tfull_bar[acc], u & 1u);
+        mb_wait_warp(&tfull_bar[acc], u & 1u);
         if (warp == 3 && lane == 0) tc_trace(TC_DBG(a), 5, it);
         tc_fence_after();
         const bool valid = tc_rvalid<FS>(a, p, h) && !(a.g.triangle && bj < r);
@@ -578,14 +609,14 @@ struct TcPlan {
 };
 bool tc_plan(uint32_t KP, TcPlan& pl) {
   const uint32_t PB = 256u * KP;
-  if (KP <= kTcSmallKP) {  // one chunk = the whole panel: 2 x 2 resident A panels + S panels within ~200 KB
+  if (KP <= kTcSmallKP) {  // one chunk = the whole panel: 2 x 2 resident A panels + S panels
     pl.rb = pl.abufs = 2;
     pl.CB = PB;
-    pl.stages = std::max<uint32_t>(2u, std::min<uint32_t>(8u, (200u * 1024u - 4u * PB) / PB));
+    pl.stages = std::max<uint32_t>(2u, std::min<uint32_t>(8u, (kTcSmemBudget - 4u * PB) / PB));
     pl.smem = std::max<size_t>(static_cast<size_t>(4 + pl.stages) * PB, 116u * 1024u);
     return true;
   }
-  pl.CB = 256u * 64u;
+  pl.CB = 256u * kTcChunkK;
   if (4u * PB + 4u * pl.CB <= kTcSmemBudget) {
     pl.rb = 2;
     pl.abufs = 2;
@@ -597,8 +628,8 @@ bool tc_plan(uint32_t KP, TcPlan& pl) {
     pl.abufs = (2u * PB + 4u * pl.CB <= kTcSmemBudget) ? 2u : 1u;
   }
   const uint32_t a_bytes = pl.abufs * pl.rb * PB;
-  if (a_bytes + 3u * pl.CB > kTcSmemBudget) return false;
-  pl.stages = std::min<uint32_t>(8u, (kTcSmemBudget - a_bytes) / pl.CB);
+  if (a_bytes + 4u * pl.CB > kTcSmemBudget) return false;  // >= 2 stages per issuer ring
+  pl.stages = std::min<uint32_t>(kTcMaxStages, (kTcSmemBudget - a_bytes) / pl.CB);
   // at least ~116 KB so that exactly one CTA (the TMEM owner of all 512 columns) fits per SM
   pl.smem = std::max<size_t>(static_cast<size_t>(a_bytes) + static_cast<size_t>(pl.stages) * pl.CB, 116u * 1024u);
   return true;
@@ -660,8 +691,8 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
   a.abufs = pl.abufs;
   a.stages = pl.stages;
   a.CB = pl.CB;
-  a.nch = static_cast<uint32_t>(ceil_div(a.KP, 64));
-  a.last_steps = (a.KP - 64 * (a.nch - 1)) / 16;
+  a.nch = a.KP <= kTcSmallKP ? 1u : static_cast<uint32_t>(ceil_div(a.KP, kTcChunkK));
+  a.last_steps = a.KP <= kTcSmallKP ? a.KP / 16 : (a.KP - kTcChunkK * (a.nch - 1)) / 16;
   uint64_t T = 0;
   for (uint32_t r0 = a.rb0; r0 < a.rb1; r0 += a.rb) T += a.nbc - (g.triangle ? r0 : 0u);
   if (T == 0) return;
@@ -705,6 +736,14 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
     }
   }
 #endif
+  if (std::getenv("REFSIG_TC_PRINT"))
+    std::fprintf(stderr,
+                 "mrc_tc: KP %u nch %u last %u CB %u rb %u abufs %u stages %u smem %zu grid %u tiles %llu rows %u cols "
+                 "%u wpr %u tri %d rb0 %u rb1 %u nbc %u Ar %p Bc %p bitmap %p\n",
+                 a.KP, a.nch, a.last_steps, a.CB, a.rb, a.abufs, a.stages, smem, grid,
+                 static_cast<unsigned long long>(a.n_tiles), g.n_rows, g.n_cols, g.words_per_row, g.triangle ? 1 : 0,
+                 a.rb0, a.rb1, a.nbc, static_cast<const void*>(a.Ar), static_cast<const void*>(a.Bc),
+                 static_cast<void*>(a.bitmap));
   launch_pdl(kern, dim3(grid), dim3(kTcThreads), smem, s, a);
 #ifdef REFSIG_TC_TRACE
   if (dbg & 8) {

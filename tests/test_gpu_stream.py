@@ -1,0 +1,82 @@
+"""Streaming batches (stage_corpus / swap_corpus: the next batch's upload on a
+copy stream while the current one computes) give exactly what load_corpus
+gives, batch after batch; and the query join's cached database column forms
+(built once per database signature) give what a fresh context gives."""
+import numpy as np
+import pytest
+
+import paper_1810_03099_b200 as R
+from paper_1810_03099_b200 import corpus as C
+
+pytestmark = pytest.mark.gpu
+
+
+def _batches(n_batches=3, n=700):
+    cp, _ = C.config_corpus("c0")
+    out = []
+    for b in range(n_batches):  # different document subsets and layouts
+        lo = b * 400
+        sub = cp.slice_docs(lo + n)
+        off = (sub.doc_off[lo:] - sub.doc_off[lo]).astype(np.uint64)
+        tok = sub.tokens[int(sub.doc_off[lo]):int(sub.doc_off[-1])]
+        out.append((np.ascontiguousarray(tok), off, cp.vocab))
+    return out
+
+
+def test_stage_swap_equals_load(gpu_ctx_factory):
+    batches = _batches()
+    refs = np.arange(10, dtype=np.uint32) * 7
+    a, b = gpu_ctx_factory(), gpu_ctx_factory()
+    b.stage_corpus(*batches[0])
+    for k, (tok, off, V) in enumerate(batches):
+        b.swap_corpus()
+        if k + 1 < len(batches):
+            b.stage_corpus(*batches[k + 1])  # in flight while batch k computes
+        b.count()
+        b.set_reference_docs(refs)
+        Sb = b.sign()
+        kb = b.mrc_pairs(0.95)
+        a.load_corpus(tok, off, V)
+        a.count()
+        a.set_reference_docs(refs)
+        Sa = a.sign()
+        ka = a.mrc_pairs(0.95)
+        assert np.array_equal(Sa, Sb) and np.array_equal(ka, kb), f"batch {k}"
+
+
+def test_query_join_cached_database_forms(gpu_ctx_factory):
+    cp, _ = C.config_corpus("c0")
+    refs = C.sample_refs(0, cp.n_docs, 64)
+    db = gpu_ctx_factory()
+    db.load_corpus(cp.tokens, cp.doc_off, cp.vocab)
+    db.count()
+    db.set_reference_docs(refs)
+    db.sign(fetch=False)
+    q = gpu_ctx_factory()
+    q.attach_database(db)
+    results = []
+    for tau in (0.9, 0.99, 0.9):  # second and third calls reuse the database forms
+        q.load_corpus(cp.tokens[: int(cp.doc_off[300])], cp.doc_off[:301], cp.vocab)
+        q.count()
+        q.sign(fetch=False)
+        results.append(q.mrc_query_pairs(tau))
+    assert np.array_equal(results[0], results[2])
+    fresh = gpu_ctx_factory()
+    fresh.attach_database(db)
+    fresh.load_corpus(cp.tokens[: int(cp.doc_off[300])], cp.doc_off[:301], cp.vocab)
+    fresh.count()
+    fresh.sign(fetch=False)
+    assert np.array_equal(fresh.mrc_query_pairs(0.99), results[1])
+    # re-signing the database with another reference invalidates the cache
+    db.set_reference_docs(C.sample_refs(1, cp.n_docs, 64))
+    db.sign(fetch=False)
+    q.load_corpus(cp.tokens[: int(cp.doc_off[300])], cp.doc_off[:301], cp.vocab)
+    q.count()
+    q.sign(fetch=False)
+    k_new = q.mrc_query_pairs(0.99)
+    ref = gpu_ctx_factory()
+    ref.attach_database(db)
+    ref.load_corpus(cp.tokens[: int(cp.doc_off[300])], cp.doc_off[:301], cp.vocab)
+    ref.count()
+    ref.sign(fetch=False)
+    assert np.array_equal(ref.mrc_query_pairs(0.99), k_new)
