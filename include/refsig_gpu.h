@@ -246,6 +246,16 @@ int refsig_gpu_get_pairs_csr(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_
 int refsig_gpu_get_pairs_csr16(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_hi, uint64_t* rowptr,
                                uint16_t* cols, uint64_t capacity, uint64_t* out_count);
 
+/* Asynchronous get_pairs_csr16 over the last pair call's whole row range: the
+ * rebased rowptr (n_rows + 1) and the first min(count, capacity) 16-bit
+ * columns are copied to the (pinned) host buffers on a separate stream while
+ * the caller moves on to the next batch; *out_count (exact) is returned at
+ * once (3 on overflow, as get_pairs_csr16). The buffers are complete after
+ * refsig_gpu_wait_fetch. Two fetches may be in flight. */
+int refsig_gpu_get_pairs_csr16_async(refsig_gpu_ctx* ctx, uint64_t* rowptr, uint16_t* cols, uint64_t capacity,
+                                     uint64_t* out_count);
+int refsig_gpu_wait_fetch(refsig_gpu_ctx* ctx);
+
 /* ---- device views (for frameworks / collectives; read-only) ------------------ */
 #define REFSIG_BUF_PAIRS 0      /* uint64 keys of the last pair call */
 #define REFSIG_BUF_SIGNATURES 1 /* float S[n_docs*K] */

@@ -119,6 +119,9 @@ SIGNATURES = {
     "refsig_gpu_debug_check": ([_c.c_void_p], _c.c_int),
     "refsig_gpu_stage_corpus": ([_c.c_void_p, _P(_c.c_uint32), _P(_c.c_uint64), _c.c_uint32, _c.c_uint32], _c.c_int),
     "refsig_gpu_swap_corpus": ([_c.c_void_p], _c.c_int),
+    "refsig_gpu_get_pairs_csr16_async": ([_c.c_void_p, _P(_c.c_uint64), _P(_c.c_uint16), _c.c_uint64, _P(_c.c_uint64)],
+                                         _c.c_int),
+    "refsig_gpu_wait_fetch": ([_c.c_void_p], _c.c_int),
 }
 K3_AUTO, K3_FP32, K3_TENSOR = 0, 1, 2
 PHASES = ["count", "reference", "sign", "pair_tiles", "pair_emit", "simhash", "h2d", "d2h"]
@@ -423,6 +426,18 @@ class Context:
                                                 _ptr(cols, ctypes.c_uint16), len(cols), ctypes.byref(n))
         self._check(rc, n.value)
         return rowptr[: n_rows + 1], cols[: n.value]
+
+    def pairs_csr16_async(self, rowptr: np.ndarray, cols: np.ndarray) -> int:
+        """Start copying the last pair call's CSR (uint16 columns) into the given
+        pinned host arrays; returns the exact count at once. wait_fetch() completes it."""
+        n = ctypes.c_uint64()
+        rc = self._L.refsig_gpu_get_pairs_csr16_async(self._h, _ptr(rowptr, ctypes.c_uint64),
+                                                      _ptr(cols, ctypes.c_uint16), len(cols), ctypes.byref(n))
+        self._check(rc, n.value)
+        return n.value
+
+    def wait_fetch(self):
+        self._check(self._L.refsig_gpu_wait_fetch(self._h))
 
     def mrc_pairs(self, tau: float, out: np.ndarray | None = None, fetch: bool = True):
         """Sorted keys (i<<32|j) of all i<j with compare(S_i,S_j) >= tau."""

@@ -4,6 +4,8 @@
 // kernels (kernels.cuh); there is no host compute path.
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -62,6 +64,11 @@ void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(REFSIG_E_RUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// (const char* overload: the message is only built on failure — require() runs
+// per document in the upload validation loops)
+void require(bool ok, const char* msg) {
+  if (!ok) fail(REFSIG_E_VALIDATION, msg);
+}
 void require(bool ok, const std::string& msg) {
   if (!ok) fail(REFSIG_E_VALIDATION, msg);
 }
@@ -206,6 +213,15 @@ struct refsig_gpu_ctx {
   std::vector<uint64_t> staged_off;
   uint32_t staged_docs = 0, staged_vocab = 0;
 
+  // asynchronous result fetch (refsig_gpu_get_pairs_csr16_async): two slots of
+  // device staging (rebased rowptr, 16-bit columns) copied to the host on
+  // d2h_stream while the next batch computes
+  cudaStream_t d2h_stream = nullptr;
+  cudaEvent_t ev_fetch_ready = nullptr, ev_fetched[2] = {nullptr, nullptr};
+  DevBuf fetch_rowptr[2], fetch_cols[2];
+  bool fetch_pending[2] = {false, false};
+  int fetch_slot = 0;
+
   // tcgen05 column forms of this (database) context's signatures, cached for
   // query joins (they do not depend on tau); valid while sign_gen is unchanged
   DevBuf tc_colf;
@@ -263,7 +279,8 @@ struct refsig_gpu_ctx {
             {"post_fill", &post_fill}, {"posts", &posts}, {"head_col", &head_col}, {"headA", &headA},
             {"head_norm", &head_norm}, {"tail_df", &tail_df}, {"headAT", &headAT}, {"eval_tail", &eval_tail},
             {"eval_part", &eval_part}, {"cf_rep", &cf_rep}, {"cf", &cf}, {"records", &records},
-            {"tc_forms", &tc_forms}};
+            {"tc_forms", &tc_forms}, {"fetch_rowptr0", &fetch_rowptr[0]}, {"fetch_rowptr1", &fetch_rowptr[1]},
+            {"fetch_cols0", &fetch_cols[0]}, {"fetch_cols1", &fetch_cols[1]}};
   }
   ~refsig_gpu_ctx() {
     for (auto& m : marks) {
@@ -277,6 +294,9 @@ struct refsig_gpu_ctx {
     if (plan_done) cudaEventDestroy(plan_done);
     if (step_exec) cudaGraphExecDestroy(step_exec);
     if (ev_staged) cudaEventDestroy(ev_staged);
+    if (ev_fetch_ready) cudaEventDestroy(ev_fetch_ready);
+    for (auto e : ev_fetched)
+      if (e) cudaEventDestroy(e);
     if (ev_next_free) cudaEventDestroy(ev_next_free);
   }
 };
@@ -557,7 +577,23 @@ void ensure_unit_weights(refsig_gpu_ctx* c) {
   c->have_inv_norm = true;
 }
 
+struct HostProf {  // REFSIG_HOST_PROF=1: host time of load_common's sections (stderr)
+  const char* name;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  static bool on() {
+    static const bool v = std::getenv("REFSIG_HOST_PROF") != nullptr;
+    return v;
+  }
+  void lap(const char* what) {
+    if (!on()) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "%s %s %.1f us\n", name, what, std::chrono::duration<double, std::micro>(t - t0).count());
+    t0 = t;
+  }
+};
+
 void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, uint32_t vocab) {
+  HostProf hp{"load_common"};
   require(doc_off != nullptr, "doc_off is NULL");
   require(n_docs >= 1, "empty corpus");
   require(vocab >= 1 && vocab < 0x7fffffffu, "vocab out of range");
@@ -580,6 +616,7 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
     reset_downstream(c);
     return;
   }
+  hp.lap("validate");
   c->h_off.assign(doc_off, doc_off + n_docs + 1);
   c->have_text = false;  // refsig_gpu_load_text sets it after this
   c->n_docs = n_docs;
@@ -602,20 +639,26 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
     std::sort(key.begin(), key.end());
     for (uint32_t d = 0; d < n_docs; ++d) order[d] = static_cast<uint32_t>(key[d]);
   }
+  hp.lap("order");
   uint32_t n_class[refsig_gpu_ctx::kPlanLists] = {};
-  auto cls_of = [&](uint64_t l) -> int {
-    if (l <= kTinyMax) return refsig_gpu_ctx::kPlanTiny;
-    if (l <= 128) return refsig_gpu_ctx::kPlanW4;
-    if (l <= 256) return refsig_gpu_ctx::kPlanW8;
-    if (l <= 512) return refsig_gpu_ctx::kPlanW16;
-    if (l <= kGroupMax) {
-      int g = 0;
-      while (l > kGroupCap[g]) ++g;
-      return refsig_gpu_ctx::kPlanG0 + g;
-    }
-    return refsig_gpu_ctx::kPlanLong;
+  // work class by ceil(log2(length)): <= 64 tiny, 128 / 256 / 512 warp sorts, 1024..8192 the
+  // group classes (kGroupCap), longer the global path — one table lookup per document
+  static_assert(kTinyMax == 64 && kGroupCap[0] == 1024 && kGroupCap[3] == 8192 && kGroupMax == 8192,
+                "class table below assumes these bounds");
+  static constexpr uint8_t kClassOfLog[15] = {
+      refsig_gpu_ctx::kPlanTiny, refsig_gpu_ctx::kPlanTiny, refsig_gpu_ctx::kPlanTiny, refsig_gpu_ctx::kPlanTiny,
+      refsig_gpu_ctx::kPlanTiny, refsig_gpu_ctx::kPlanTiny, refsig_gpu_ctx::kPlanTiny, refsig_gpu_ctx::kPlanW4,
+      refsig_gpu_ctx::kPlanW8,   refsig_gpu_ctx::kPlanW16,  refsig_gpu_ctx::kPlanG0,   refsig_gpu_ctx::kPlanG0 + 1,
+      refsig_gpu_ctx::kPlanG0 + 2, refsig_gpu_ctx::kPlanG0 + 3, refsig_gpu_ctx::kPlanLong};
+  auto cls_of = [](uint64_t l) -> int {
+    const int b = l <= 1 ? 0 : 64 - __builtin_clzll(l - 1);  // ceil(log2(l))
+    return kClassOfLog[b < 14 ? b : 14];
   };
-  for (uint32_t d = 0; d < n_docs; ++d) ++n_class[cls_of(len(d))];
+  std::vector<uint8_t> cls(n_docs);
+  for (uint32_t d = 0; d < n_docs; ++d) {
+    cls[d] = static_cast<uint8_t>(cls_of(doc_off[d + 1] - doc_off[d]));
+    ++n_class[cls[d]];
+  }
   n_class[refsig_gpu_ctx::kPlanOrder] = n_docs;
   // one pinned staging area: doc_off (u64), then the u32 lists
   uint32_t off = 0;
@@ -629,7 +672,9 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
   const size_t loff_at = (off_bytes + list_bytes + 7) & ~size_t{7};
   const size_t bytes = loff_at + sizeof(uint64_t) * n_class[refsig_gpu_ctx::kPlanLong];
   if (!c->plan_done) ck(cudaEventCreateWithFlags(&c->plan_done, cudaEventDisableTiming), "event");
+  hp.lap("classes");
   ck(cudaEventSynchronize(c->plan_done), "plan staging");  // the previous copy consumed h_plan
+  hp.lap("plan_done sync");
   if (bytes > c->h_plan_cap) {
     if (c->h_plan) cudaFreeHost(c->h_plan);
     c->h_plan = nullptr;
@@ -647,7 +692,7 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
   for (uint32_t i = 0; i < n_docs; ++i) {
     const uint32_t d = order[i];
     lists[fill[refsig_gpu_ctx::kPlanOrder]++] = d;
-    const int k = cls_of(len(d));
+    const int k = cls[d];
     lists[fill[k]++] = d;
     if (k == refsig_gpu_ctx::kPlanLong) {
       loff[n_loff++] = scratch;
@@ -660,6 +705,7 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
   while (c->n_sign_long < n_docs && len(order[c->n_sign_long]) > kSignLongTokens) ++c->n_sign_long;
   c->n_sign_half = c->n_sign_long;
   while (c->n_sign_half < n_docs && len(order[c->n_sign_half]) > kSignHalfTokens) ++c->n_sign_half;
+  hp.lap("lists");
   c->plan.ensure(list_bytes);
   ck(cudaMemcpyAsync(c->doc_off.p, c->h_plan, off_bytes, cudaMemcpyHostToDevice, c->stream), "H2D doc_off");
   ck(cudaMemcpyAsync(c->plan.p, lists, list_bytes, cudaMemcpyHostToDevice, c->stream), "H2D plan");
@@ -672,6 +718,7 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
     ck(cudaMemcpyAsync(c->long_off.p, loff, 8ull * n_loff, cudaMemcpyHostToDevice, c->stream), "H2D long offsets");
   }
   ck(cudaEventRecord(c->plan_done, c->stream), "event");  // h_plan (offsets, lists, long offsets) consumed
+  hp.lap("copies");
   c->loaded = true;
   c->counted = false;
   c->plan_tok = c->tok;
@@ -780,6 +827,10 @@ void refsig_gpu_destroy(refsig_gpu_ctx* ctx) {
   if (ctx->copy_stream) {
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamDestroy(ctx->copy_stream);
+  }
+  if (ctx->d2h_stream) {
+    cudaStreamSynchronize(ctx->d2h_stream);
+    cudaStreamDestroy(ctx->d2h_stream);
   }
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
@@ -1796,6 +1847,58 @@ int refsig_gpu_get_pairs_csr16(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t ro
     }
   });
   return rc != REFSIG_OK ? rc : rc2;
+}
+
+int refsig_gpu_get_pairs_csr16_async(refsig_gpu_ctx* ctx, uint64_t* rowptr, uint16_t* cols, uint64_t capacity,
+                                     uint64_t* out_count) {
+  int rc2 = REFSIG_OK;
+  int rc = guard(ctx, [&] {
+    require(ctx->have_pairs && !ctx->emit_pending, "no finished pair computation to fetch");
+    require(rowptr != nullptr && out_count != nullptr, "NULL output");
+    require(capacity == 0 || cols != nullptr, "cols is NULL");
+    const PairGrid& g = ctx->emit_grid;
+    require(g.n_cols <= 65536u, "16-bit columns need n_cols <= 65536 (use get_pairs_csr)");
+    if (!ctx->d2h_stream) {
+      ck(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking), "d2h stream");
+      ck(cudaEventCreateWithFlags(&ctx->ev_fetch_ready, cudaEventDisableTiming), "event");
+      for (auto& e : ctx->ev_fetched) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+    const int slot = ctx->fetch_slot;
+    ctx->fetch_slot ^= 1;
+    // the slot's previous copy must have left its staging buffers
+    if (ctx->fetch_pending[slot]) ck(cudaStreamWaitEvent(ctx->stream, ctx->ev_fetched[slot], 0), "wait fetch");
+    const uint64_t n_rows = g.row_end - g.row_begin, total = ctx->cand_count;
+    const uint64_t m = std::min(total, capacity);
+    ctx->fetch_rowptr[slot].ensure(8 * (n_rows + 1));
+    ctx->fetch_cols[slot].ensure(2 * m + 16);
+    launch_rebase_rowptr(ctx->rowstart.as<uint64_t>() + g.row_begin, n_rows + 1, ctx->fetch_rowptr[slot].as<uint64_t>(),
+                         ctx->stream);
+    if (m) launch_narrow_cols(ctx->cand.as<uint32_t>(), m, ctx->fetch_cols[slot].as<uint16_t>(), ctx->stream);
+    launched("fetch");
+    ck(cudaEventRecord(ctx->ev_fetch_ready, ctx->stream), "event");
+    ck(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_fetch_ready, 0), "wait");
+    ck(cudaMemcpyAsync(rowptr, ctx->fetch_rowptr[slot].p, 8 * (n_rows + 1), cudaMemcpyDeviceToHost, ctx->d2h_stream),
+       "D2H rowptr");
+    if (m) ck(cudaMemcpyAsync(cols, ctx->fetch_cols[slot].p, 2 * m, cudaMemcpyDeviceToHost, ctx->d2h_stream), "D2H cols");
+    ck(cudaEventRecord(ctx->ev_fetched[slot], ctx->d2h_stream), "event");
+    ctx->fetch_pending[slot] = true;
+    *out_count = total;
+    if (total > capacity) {
+      ctx->err = "candidate buffer overflow: " + std::to_string(total) + " pairs > capacity " + std::to_string(capacity);
+      rc2 = REFSIG_E_OVERFLOW;
+    }
+  });
+  return rc != REFSIG_OK ? rc : rc2;
+}
+
+int refsig_gpu_wait_fetch(refsig_gpu_ctx* ctx) {
+  return guard(ctx, [&] {
+    for (int k = 0; k < 2; ++k)
+      if (ctx->fetch_pending[k]) {
+        ck(cudaEventSynchronize(ctx->ev_fetched[k]), "fetch");
+        ctx->fetch_pending[k] = false;
+      }
+  });
 }
 
 int refsig_gpu_device_buffer(refsig_gpu_ctx* ctx, int which, void** ptr, uint64_t* bytes) {

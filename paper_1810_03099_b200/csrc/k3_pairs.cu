@@ -498,6 +498,20 @@ __global__ void __launch_bounds__(256) narrow_cols_kernel(const uint32_t* __rest
 
 }  // namespace
 
+__global__ void rebase_rowptr_kernel(const uint64_t* __restrict__ in, uint64_t n, uint64_t* __restrict__ out) {
+  const uint64_t base = in[0];
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = in[i] - base;
+}
+
+void launch_rebase_rowptr(const uint64_t* in, uint64_t n, uint64_t* out, cudaStream_t s) {
+  if (!n) return;
+  const uint64_t blocks = std::min<uint64_t>(ceil_div(n, 256), 148ull * 8);
+  rebase_rowptr_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(in, n, out);
+  note_launch();
+}
+
 void launch_narrow_cols(const uint32_t* in, uint64_t n, uint16_t* out, cudaStream_t s) {
   if (!n) return;
   const uint64_t blocks = std::min<uint64_t>(ceil_div(n / 2 + 1, 256), 148ull * 16);

@@ -164,6 +164,8 @@ void launch_emit_pairs(const uint32_t* bitmap, const PairGrid& g, const uint32_t
 
 // out[k] = (uint16) in[k] (column ids of a grid with n_cols <= 65536).
 void launch_narrow_cols(const uint32_t* in, uint64_t n, uint16_t* out, cudaStream_t s);
+// out[i] = in[i] - in[0] for i < n (a row range's CSR offsets rebased to 0).
+void launch_rebase_rowptr(const uint64_t* in, uint64_t n, uint64_t* out, cudaStream_t s);
 
 // ---- K4a simhash -------------------------------------------------------------
 struct SimhashArgs {

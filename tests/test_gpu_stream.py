@@ -80,3 +80,34 @@ def test_query_join_cached_database_forms(gpu_ctx_factory):
     ref.count()
     ref.sign(fetch=False)
     assert np.array_equal(ref.mrc_query_pairs(0.99), k_new)
+
+
+def test_async_csr16_fetch_equals_sync(gpu_ctx_factory):
+    """get_pairs_csr16_async (two slots in flight) delivers what get_pairs_csr16 does."""
+    import torch
+    batches = _batches(4, 600)
+    refs = np.arange(10, dtype=np.uint32) * 5
+    ctx = gpu_ctx_factory()
+    host = [(torch.empty(601, dtype=torch.int64).pin_memory().numpy().view(np.uint64),
+             torch.empty(200_000, dtype=torch.int16).pin_memory().numpy().view(np.uint16)) for _ in range(2)]
+    want, got = [], []
+    for k, (tok, off, V) in enumerate(batches):
+        ctx.load_corpus(tok, off, V)
+        ctx.count()
+        ctx.set_reference_docs(refs)
+        ctx.sign(fetch=False)
+        ctx.mrc_pairs_rows(0.9, 0, len(off) - 1, fetch=False)
+        want.append(ctx.pairs_csr16())
+        ctx.wait_fetch()
+        if k >= 2:
+            rp, cs = host[k & 1]
+            got.append((rp.copy(), cs[: int(rp[-1])].copy()))  # slot reused: batch k-2 complete
+        n = ctx.pairs_csr16_async(*host[k & 1])
+        assert n == len(want[-1][1])
+    ctx.wait_fetch()
+    for k in (2, 3):
+        rp, cs = host[k & 1]
+        got.append((rp.copy(), cs[: int(rp[-1])].copy()))
+    # got holds batches 0,1 (read when their slots were reused) then 2,3
+    for (wr, wc), (gr, gc) in zip(want, got):
+        assert np.array_equal(wr, gr) and np.array_equal(wc, gc)
