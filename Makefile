@@ -14,9 +14,9 @@ LIBDIR:= $(PKG)/lib
 BUILD := build
 
 CU_SRCS := $(CSRC)/k0_text.cu $(CSRC)/k1_count.cu $(CSRC)/scan.cu $(CSRC)/k2_sign.cu $(CSRC)/k3_pairs.cu $(CSRC)/k3_tc.cu \
-           $(CSRC)/k4_simhash.cu $(CSRC)/k5_exact.cu $(CSRC)/k6_formats.cu $(CSRC)/capi.cu
+           $(CSRC)/k4_simhash.cu $(CSRC)/k5_exact.cu $(CSRC)/k5_tc.cu $(CSRC)/k6_formats.cu $(CSRC)/capi.cu
 CU_OBJS := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
-HDRS    := $(CSRC)/common.cuh $(CSRC)/kernels.cuh include/refsig_gpu.h
+HDRS    := $(CSRC)/common.cuh $(CSRC)/kernels.cuh $(CSRC)/tc_common.cuh include/refsig_gpu.h
 
 GPU_LIB := $(LIBDIR)/librefsig_gpu.so
 GEN_LIB := $(LIBDIR)/libmrcgen.so

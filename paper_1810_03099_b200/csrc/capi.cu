@@ -410,6 +410,13 @@ void reset_downstream(refsig_gpu_ctx* c) {
   c->have_pairs = false;
 }
 
+int sm_count_host() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
 uint32_t words_per_row(uint32_t n_cols) { return static_cast<uint32_t>(ceil_div(n_cols, kTile) * 4); }
 
 // The 64-bit keys (i<<32|j) of the last pair computation, built on demand
@@ -1420,7 +1427,7 @@ int refsig_gpu_exact_pairs(refsig_gpu_ctx* ctx, float tau_cos, uint64_t* out_pai
                   ctx->posts.as<uint2>(),      ctx->headA.as<float>(),      ctx->head_norm.as<float>(),
                   H,                           N,                           std::min<uint32_t>(N, kExactPanel),
                   tau_cos,                     ctx->bitmap.as<uint32_t>(),  g.words_per_row,
-                  ctx->rowcnt.as<uint32_t>(),  nullptr};
+                  ctx->rowcnt.as<uint32_t>(),  nullptr,                     0};
       launch_exact_tail(a, 0, N, ctx->stream);
       launched("exact");
     }
@@ -1441,15 +1448,30 @@ int refsig_gpu_evaluate(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_hi, r
     const uint32_t ld = ctx->ld;
     ctx->headAT.ensure(sizeof(float) * static_cast<size_t>(H) * ld);
     launch_transpose_head(ctx->headA.as<float>(), N, H, ld, ctx->headAT.as<float>(), ctx->stream);
+    // the head and MRC dots on tcgen05 when the operands fit (every config: H = 64, K <= 128),
+    // else the FP32 tiles; REFSIG_EVAL=fp32 forces the latter
+    static const bool eval_fp32 = [] {
+      const char* m = std::getenv("REFSIG_EVAL");
+      return m && std::strcmp(m, "fp32") == 0;
+    }();
+    const bool tc = !eval_fp32 && eval_tc_supported(H, ctx->K);
+    if (tc) {
+      const size_t fb = eval_tc_form_bytes(H, ctx->K, N);
+      ctx->tc_forms.ensure(2 * fb);
+      launch_eval_tc_forms(ctx->headAT.as<float>(), H, ctx->ST.as<float>(), ctx->K, ld, N, ctx->tc_forms.p,
+                           ctx->tc_forms.as<char>() + fb, ctx->stream);
+      launched("evaluation forms");
+    }
     // row panels (multiples of 128 rows) whose fixed-point tail sums fit ~2 GB
-    uint64_t panel = std::max<uint64_t>(128, ((2ull << 30) / (4ull * N)) / 128 * 128);
-    const uint32_t grid = eval_grid();
+    uint64_t panel = std::max<uint64_t>(128, ((2ull << 30) / (4ull * ld)) / 128 * 128);
+    const uint32_t grid = tc ? static_cast<uint32_t>(sm_count_host()) : eval_grid();
     ctx->eval_part.ensure(sizeof(double) * 8 * grid);
     std::vector<double> part(8 * grid);
     double sum[7] = {0, 0, 0, 0, 0, 0, 0};
     for (uint64_t p0 = row_lo; p0 < row_hi; p0 += panel) {
       const uint32_t p1 = static_cast<uint32_t>(std::min<uint64_t>(row_hi, p0 + panel));
-      ctx->eval_tail.ensure(4ull * (p1 - p0) * N);
+      ctx->eval_tail.ensure(4ull * (p1 - p0) * ld);
+      uint32_t used = grid;
       {
         Phase ph(ctx, REFSIG_PHASE_PAIR_TILES);
         ExactArgs a{ctx->ent.as<uint2>(),        ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(),
@@ -1457,19 +1479,26 @@ int refsig_gpu_evaluate(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_hi, r
                     ctx->posts.as<uint2>(),      ctx->headA.as<float>(),      ctx->head_norm.as<float>(),
                     H,                           N,                           std::min<uint32_t>(N, kExactPanel),
                     0.0f,                        nullptr,                     0,
-                    nullptr,                     ctx->eval_tail.as<uint32_t>()};
+                    nullptr,                     ctx->eval_tail.as<uint32_t>(), ld};
         launch_exact_tail(a, static_cast<uint32_t>(p0), p1, ctx->stream);
-        EvalArgs e{ctx->headAT.as<float>(), H, ctx->ST.as<float>(), ctx->K, ld,
-                   ctx->have_fp ? ctx->fp.as<uint64_t>() : nullptr, ctx->eval_tail.as<uint32_t>(), N,
-                   static_cast<uint32_t>(p0), p1, ctx->eval_part.as<double>()};
-        launch_eval_tiles(e, ctx->stream);
+        const uint64_t* fp = ctx->have_fp ? ctx->fp.as<uint64_t>() : nullptr;
+        if (tc) {
+          const size_t fb = eval_tc_form_bytes(H, ctx->K, N);
+          used = launch_eval_tc(ctx->tc_forms.p, ctx->tc_forms.as<char>() + fb, H, ctx->K, N,
+                                static_cast<uint32_t>(p0), p1, ctx->eval_tail.as<uint32_t>(), ld, fp,
+                                ctx->eval_part.as<double>(), ctx->stream);
+        } else {
+          EvalArgs e{ctx->headAT.as<float>(), H, ctx->ST.as<float>(), ctx->K, ld, fp, ctx->eval_tail.as<uint32_t>(),
+                     N, static_cast<uint32_t>(p0), p1, ctx->eval_part.as<double>(), ld};
+          launch_eval_tiles(e, ctx->stream);
+        }
         launched("evaluate");
       }
-      ck(cudaMemcpyAsync(part.data(), ctx->eval_part.p, sizeof(double) * 8 * grid, cudaMemcpyDeviceToHost,
+      ck(cudaMemcpyAsync(part.data(), ctx->eval_part.p, sizeof(double) * 8 * used, cudaMemcpyDeviceToHost,
                          ctx->stream),
          "D2H eval");
       sync(ctx);
-      for (uint32_t b = 0; b < grid; ++b)  // CTA order: deterministic
+      for (uint32_t b = 0; b < used; ++b)  // CTA order: deterministic
         for (int q = 0; q < 7; ++q) sum[q] += part[8 * b + q];
     }
     const double n = sum[0];

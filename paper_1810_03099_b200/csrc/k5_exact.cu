@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(512) exact_tail_kernel(ExactArgs a, uint32_t r
     }
     __syncthreads();
     if (a.tail_out) {  // evaluation mode: hand the exact tail sums to the tile pass
-      uint32_t* dst = a.tail_out + static_cast<size_t>(blockIdx.x) * a.n_docs;
+      uint32_t* dst = a.tail_out + static_cast<size_t>(blockIdx.x) * a.tail_ld;
       for (uint32_t j = jlo + threadIdx.x; j < c1; j += blockDim.x) dst[j] = acc[j - c0];
       __syncthreads();
       continue;
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(256) eval_tiles_kernel(EvalArgs a, uint32_t nb
     for (int r = 0; r < 4; ++r) {
       const uint32_t i = r0 + ty * 4 + r;
       if (i < a.row_lo || i >= a.row_hi) continue;
-      const uint32_t* trow = a.T + static_cast<size_t>(i - a.row_lo) * a.n_docs;
+      const uint32_t* trow = a.T + static_cast<size_t>(i - a.row_lo) * a.ldT;
       const uint64_t fi = a.fp ? a.fp[i] : 0ull;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {

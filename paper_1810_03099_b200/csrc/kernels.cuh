@@ -204,7 +204,8 @@ struct ExactArgs {
   uint32_t words_per_row;
   uint32_t* rowcnt;
   uint32_t* tail_out;        // evaluation mode: the fixed-point tail sums of rows [row_lo, row_hi) for
-                             // j > i, row-major [row_hi-row_lo][n_docs] (no threshold, no bitmap)
+                             // j > i, row-major [row_hi-row_lo][tail_ld] (no threshold, no bitmap)
+  uint32_t tail_ld;          // row stride of tail_out (>= n_docs; the tensor-core evaluation wants 128-multiples)
 };
 void launch_unit_weights(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const TermInfo* info,
                          const float* inv_norm, uint32_t n_docs, float* x, cudaStream_t s);
@@ -228,12 +229,23 @@ struct EvalArgs {
   uint32_t K;
   uint32_t ld;
   const uint64_t* fp;  // [n_docs] fingerprints (NULL: no Simhash errors)
-  const uint32_t* T;   // tail sums, row-major [row_hi-row_lo][n_docs]
+  const uint32_t* T;   // tail sums, row-major [row_hi-row_lo][ldT]
   uint32_t n_docs, row_lo, row_hi;
   double* out;         // [grid*8]
+  uint32_t ldT;
 };
 uint32_t eval_grid();
 void launch_eval_tiles(const EvalArgs& a, cudaStream_t s);
+// The same evaluation with the head and MRC dots on tcgen05 (k5_tc.cu): split-
+// fp16 operand forms of [head | MRC] per document, then one tile kernel
+// (returns its grid: out holds grid x 8 doubles). T rows have stride ldT.
+bool eval_tc_supported(uint32_t H, uint32_t K);
+size_t eval_tc_form_bytes(uint32_t H, uint32_t K, uint32_t n_docs);
+void launch_eval_tc_forms(const float* AT, uint32_t H, const float* ST, uint32_t K, uint32_t ld, uint32_t n_docs,
+                          void* rowf, void* colf, cudaStream_t s);
+uint32_t launch_eval_tc(const void* rowf, const void* colf, uint32_t H, uint32_t K, uint32_t n_docs, uint32_t row_lo,
+                        uint32_t row_hi, const uint32_t* T, uint32_t ldT, const uint64_t* fp, double* out,
+                        cudaStream_t s);
 // AT[c*ld + d] = A[d*H + c] (ld >= n_docs, pad columns zero).
 void launch_transpose_head(const float* A, uint32_t n_docs, uint32_t H, uint32_t ld, float* AT, cudaStream_t s);
 void launch_pair_cosines(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const float* x,
