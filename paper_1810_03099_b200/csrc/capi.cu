@@ -949,8 +949,16 @@ static void do_count(refsig_gpu_ctx* ctx, int weight_mode) {
   ctx->info.ensure(sizeof(TermInfo) * V);
   if (ctx->flags.ensure(16)) ck(cudaMemsetAsync(ctx->flags.p, 0, 16, ctx->stream), "memset");
   Phase ph(ctx, REFSIG_PHASE_COUNT);
-  // df replicas: ~8 MB budget, 1..16 copies (see k1_count.cu df_add)
-  const uint32_t reps = std::max<uint32_t>(1u, std::min<uint32_t>(16u, (2u << 20) / V));
+  // df replicas (k1_count.cu df_replica): Zipf-head terms are in nearly every document, so one
+  // array would serialise their atomics; R copies divide that contention. REFSIG_DF_REPS overrides
+  // (measurement).
+  static const uint32_t reps_env = [] {
+    const char* m = std::getenv("REFSIG_DF_REPS");
+    return m ? static_cast<uint32_t>(std::atoi(m)) : 0u;
+  }();
+  // ~32 MB of replicas, 1..32 copies: 32 at configs[1] (measured: 1 copy 283 us, 2: 165, 4: 113, 16: 98,
+  // 32: 95.5, 64: 97 us for K1), 16 at configs[3], 8 at configs[4]
+  const uint32_t reps = reps_env ? reps_env : std::max<uint32_t>(1u, std::min<uint32_t>(32u, (8u << 20) / V));
   ctx->df_rep.ensure(sizeof(uint32_t) * static_cast<size_t>(V) * reps);
   ck(cudaMemsetAsync(ctx->df_rep.p, 0, sizeof(uint32_t) * static_cast<size_t>(V) * reps, ctx->stream), "memset df");
   CountArgs a{ctx->tok, ctx->doc_off.as<uint64_t>(), V, ctx->ent.as<uint2>(), ctx->nnz.as<uint32_t>(),

@@ -236,7 +236,9 @@ __device__ __forceinline__ uint32_t rle_regs(const uint32_t (&v)[IPT], uint32_t 
       const uint32_t rest = hmask & ~((2u << q) - 1);  // heads after q in this thread
       const uint32_t end = rest ? base + (__ffs(rest) - 1) : next;
       ent[pos] = make_uint2(v[q], end - (base + q));
+#ifndef REFSIG_K1_NO_DF  // (timing experiment only: df left unset)
       atomicAdd(dfr + v[q], 1u);
+#endif
       ++pos;
     }
   }

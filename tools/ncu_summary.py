@@ -23,7 +23,7 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROF = os.path.join(REPO, "profiles")
 
 # bench.py roofline keys -> kernel name fragments
-ROOF_KERNELS = {"mrc_tiles": ["mrc_tc_kernel", "tc_forms_kernel", "mrc_bitmap_kernel"], "sign": ["sign_kernel"], "pair_emit": ["emit_kernel"],
+ROOF_KERNELS = {"mrc_tiles": ["mrc_tc_kernel", "tc_forms_kernel"], "sign": ["sign_kernel"], "pair_emit": ["emit_kernel"],
                 "count": ["count_warp_kernel", "group_sort_kernel", "count_large_kernel", "idf_kernel"],
                 "reference": ["ref_build_kernel"],
                 "simhash": ["simhash_kernel"], "hamming_tiles": ["hamming_bitmap_kernel"]}
@@ -95,20 +95,24 @@ def to_bytes(v, unit):
     return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
 
 
-def full(path, tag):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+def full(path, tag, title=None, append=False, write_traffic=True):
+    if path.endswith(".csv"):  # `ncu -i rep --page raw --csv` output made on the GPU box
+        raw = open(path).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     hdr, units = rows[0], rows[1]
     idx = {h: i for i, h in enumerate(hdr)}
     stall = [h for h in hdr if "issue_stalled" in h and h.endswith("per_issue_active.ratio")]
-    lines = [f"# ncu --set full ({tag}) — per-kernel metrics", "",
-             "Captured with `--set full --clock-control none --import-source on`; one launch per kernel of "
-             "tools/prof_pipeline.py --steps 1 (configs[1]: the MRC step). DRAM bytes are cold-cache (ncu flushes "
-             "caches between replays).", ""]
+    lines = ([f"## {title}", ""] if append else
+             [f"# ncu --set full ({tag}) — per-kernel metrics", "",
+              "Captured with `--set full --clock-control none --import-source on`; one launch per kernel of "
+              "tools/prof_all.py (see each section). DRAM bytes are cold-cache (ncu flushes caches between "
+              "replays).", ""] + ([f"## {title}", ""] if title else []))
     per_kernel = collections.defaultdict(list)  # kernel name -> [bytes per launch]
     for r in rows[2:]:
         k = short(r[idx["Kernel Name"]])
-        lines.append(f"## `{k}`")
+        lines.append(f"### `{k}`")
         for m, label in WANT:
             if m in idx:
                 lines.append(f"- {label}: {r[idx[m]]} {units[idx[m]]}")
@@ -126,8 +130,9 @@ def full(path, tag):
         for key, frags in ROOF_KERNELS.items():
             if any(f in k for f in frags) and not (key == "simhash" and "text_" in k):
                 traffic[key] = traffic.get(key, 0.0) + sum(v) / len(v)
-    open(os.path.join(PROF, f"ncu_full_{tag}.md"), "w").write("\n".join(lines) + "\n")
-    json.dump({k: v for k, v in traffic.items()}, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
+    open(os.path.join(PROF, f"ncu_full_{tag}.md"), "a" if append else "w").write("\n".join(lines) + "\n")
+    if write_traffic:
+        json.dump({k: v for k, v in traffic.items()}, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
 
 
 def main():
@@ -135,12 +140,15 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--full")
     ap.add_argument("--tag", default="r01")
+    ap.add_argument("--title", default=None)
+    ap.add_argument("--append", action="store_true")
+    ap.add_argument("--no-traffic", action="store_true")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     if a.launches:
         launches(a.launches, a.tag)
     if a.full:
-        full(a.full, a.tag)
+        full(a.full, a.tag, a.title, a.append, not a.no_traffic)
 
 
 if __name__ == "__main__":
