@@ -747,6 +747,7 @@ PairGrid self_grid(const refsig_gpu_ctx* c) {
 // highest-df terms as dense rows + norms, and the tail postings. Returns H.
 uint32_t prepare_exact(refsig_gpu_ctx* ctx) {
   const uint32_t N = ctx->n_docs, V = ctx->vocab;
+  require(ctx->n_tokens < (1ull << 32), "exact verifier: more than 2^32 postings");  // 32-bit posting offsets
   ensure_unit_weights(ctx);
   // head terms: the kExactHead highest df (ties by id), from the device df
   const uint32_t H = std::min<uint32_t>(kExactHead, (V + 3) & ~3u);
