@@ -491,10 +491,11 @@ int run_emit(refsig_gpu_ctx* c, const PairGrid& g, uint64_t* out, uint64_t capac
   return finish_emit(c, out, capacity, out_count);
 }
 
-void prepare_bitmap(refsig_gpu_ctx* c, const PairGrid& g, bool zero) {
+// zero_rowcnt = false: the caller's first kernel zeroes the row counts (run_mrc_tiles)
+void prepare_bitmap(refsig_gpu_ctx* c, const PairGrid& g, bool zero, bool zero_rowcnt = true) {
   c->bitmap.ensure(sizeof(uint32_t) * static_cast<size_t>(g.n_rows) * g.words_per_row);
   c->rowcnt.ensure(sizeof(uint32_t) * (g.n_rows ? g.n_rows : 1));
-  ck(cudaMemsetAsync(c->rowcnt.p, 0, sizeof(uint32_t) * g.n_rows, c->stream), "memset rowcnt");
+  if (zero_rowcnt) ck(cudaMemsetAsync(c->rowcnt.p, 0, sizeof(uint32_t) * g.n_rows, c->stream), "memset rowcnt");
   if (zero)
     ck(cudaMemsetAsync(c->bitmap.p, 0, sizeof(uint32_t) * static_cast<size_t>(g.n_rows) * g.words_per_row,
                        c->stream),
@@ -510,7 +511,7 @@ bool k3_use_tc(const refsig_gpu_ctx* c, uint32_t K, float tau) {
   }();
   if (c->k3_path == REFSIG_K3_FP32) return false;
   if (c->k3_path == REFSIG_K3_TENSOR) {
-    require(mrc_tc_supported(K, tau), "tensor-core K3 needs K <= 128 and |tau| = 0 or >= 2^-14");
+    require(mrc_tc_supported(K, tau), "tensor-core K3 needs K <= 234 and |tau| = 0 or >= 2^-14");
     return true;
   }
   return !off && mrc_tc_supported(K, tau);
@@ -518,7 +519,9 @@ bool k3_use_tc(const refsig_gpu_ctx* c, uint32_t K, float tau) {
 
 void run_mrc_tiles(refsig_gpu_ctx* c, const float* STr, uint32_t ldr, uint32_t nr, const float* STc, uint32_t ldc,
                    uint32_t ncl, bool self, uint32_t K, float tau, const PairGrid& g) {
+  // (prepare_bitmap left the row counts to this function: zeroed by the forms kernel on the tcgen05 path)
   if (!k3_use_tc(c, K, tau)) {
+    ck(cudaMemsetAsync(c->rowcnt.p, 0, sizeof(uint32_t) * g.n_rows, c->stream), "memset rowcnt");
     launch_mrc_bitmap(STr, ldr, STc, ldc, K, tau, g, c->bitmap.as<uint32_t>(), c->rowcnt.as<uint32_t>(), c->stream);
     return;
   }
@@ -529,18 +532,18 @@ void run_mrc_tiles(refsig_gpu_ctx* c, const float* STr, uint32_t ldr, uint32_t n
     c->tc_forms.ensure(rb + cb);
     rowf = c->tc_forms.as<char>();
     colf = rowf + rb;
-    launch_mrc_tc_forms(STr, ldr, nr, K, tau, rowf, colf, c->stream);
+    launch_mrc_tc_forms(STr, ldr, nr, K, tau, rowf, colf, c->rowcnt.as<uint32_t>(), g.n_rows, c->stream);
   } else {
     // query join: the database's column forms do not depend on tau and stay
     // valid until it is signed again, so they are built once per database
     refsig_gpu_ctx* db = c->db;
     c->tc_forms.ensure(rb);
     rowf = c->tc_forms.as<char>();
-    launch_mrc_tc_forms(STr, ldr, nr, K, tau, rowf, nullptr, c->stream);
+    launch_mrc_tc_forms(STr, ldr, nr, K, tau, rowf, nullptr, c->rowcnt.as<uint32_t>(), g.n_rows, c->stream);
     static const bool no_cache = std::getenv("REFSIG_NO_FORM_CACHE") != nullptr;
     if (no_cache || db->tc_colf_gen != db->sign_gen || db->tc_colf.cap < cb) {
       db->tc_colf.ensure(cb);
-      launch_mrc_tc_forms(STc, ldc, ncl, K, tau, nullptr, db->tc_colf.p, c->stream);
+      launch_mrc_tc_forms(STc, ldc, ncl, K, tau, nullptr, db->tc_colf.p, nullptr, 0, c->stream);
       db->tc_colf_gen = db->sign_gen;
     }
     colf = db->tc_colf.as<char>();
@@ -557,7 +560,8 @@ void build_reference(refsig_gpu_ctx* c, const RefArgs& r, uint64_t n_entries) {
   require(u_cap * r.Kp < (1ull << 32), "reference term union too large (|U| * K >= 2^32)");
   const size_t rbytes = sizeof(float) * std::max<uint64_t>(u_cap, 1) * r.Kp;
   c->R.ensure(rbytes);
-  c->ref_count.ensure(sizeof(uint32_t));
+  if (c->ref_count.ensure(3 * sizeof(uint32_t)))  // [row counter, finished CTAs, |U|]; the kernel leaves [0],[1] zero
+    ck(cudaMemsetAsync(c->ref_count.p, 0, 3 * sizeof(uint32_t), c->stream), "memset");
   Phase ph(c, REFSIG_PHASE_REFERENCE);
   // info[].ref_row is -1 right after count(); a replaced reference resets it
   if (c->ref_dirty) launch_ref_reset(c->info.as<TermInfo>(), V, c->stream);
@@ -1093,8 +1097,9 @@ int refsig_gpu_get_inv_norm(refsig_gpu_ctx* ctx, float* inv_norm) {
   });
 }
 
-static void do_set_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_ids, uint32_t K) {
-  require(ctx->counted, "count() not called");
+// Validate the reference doc ids and upload them (returns the |U| bound: their token counts).
+static uint64_t stage_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_ids, uint32_t K) {
+  require(ctx->loaded, "no corpus loaded");
   require(!ctx->db, "query context uses the attached database's reference");
   require(ref_doc_ids != nullptr, "ref_doc_ids is NULL");
   require(K >= 1 && K <= kMaxRefs, "K must be in 1..256");
@@ -1105,9 +1110,19 @@ static void do_set_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_i
   }
   ctx->ref_docs.ensure(4ull * K);
   upload(ctx, ctx->ref_docs.p, ref_doc_ids, 4ull * K);
+  return u_cap;
+}
+
+static void build_reference_docs(refsig_gpu_ctx* ctx, uint32_t K, uint64_t u_cap) {
+  require(ctx->counted, "count() not called");
   RefArgs r{K,     nullptr, nullptr, ctx->ent.as<uint2>(), false, ref_row_stride(K), ctx->ref_docs.as<uint32_t>(),
             ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>()};
   build_reference(ctx, r, u_cap);
+}
+
+static void do_set_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_ids, uint32_t K) {
+  require(ctx->counted, "count() not called");
+  build_reference_docs(ctx, K, stage_reference_docs(ctx, ref_doc_ids, K));
 }
 
 int refsig_gpu_set_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_doc_ids, uint32_t K) {
@@ -1222,7 +1237,7 @@ int refsig_gpu_reference_union(refsig_gpu_ctx* ctx, uint32_t* out_u) {
   return guard(ctx, [&] {
     require(ctx->have_ref, "no reference set");
     require(out_u != nullptr, "NULL output");
-    ck(cudaMemcpyAsync(ctx->h_pin, ctx->ref_count.p, 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    ck(cudaMemcpyAsync(ctx->h_pin, ctx->ref_count.as<uint32_t>() + 2, 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
     sync(ctx);
     *out_u = static_cast<uint32_t>(ctx->h_pin[0] & 0xffffffffu);
   });
@@ -1236,10 +1251,7 @@ static void do_sign(refsig_gpu_ctx* ctx) {
   ctx->S.ensure(sizeof(float) * static_cast<size_t>(N) * K);
   const uint32_t ld = static_cast<uint32_t>(ceil_div(N, kTile) * kTile);
   ctx->ST.ensure(sizeof(float) * static_cast<size_t>(ld) * K);
-  ctx->ld = ld;
-  if (ld > N)  // zero pad columns: the tile kernels read whole 128-column panels
-    ck(cudaMemset2DAsync(ctx->ST.as<float>() + N, sizeof(float) * ld, 0, sizeof(float) * (ld - N), K, ctx->stream),
-       "memset ST pad");
+  ctx->ld = ld;  // (the sign kernel zeroes the pad columns [N, ld) of ST)
   ctx->inv_norm.ensure(sizeof(float) * N);
   if (ctx->db) ck(cudaStreamSynchronize(ctx->db->stream), "sync database");
   SignArgs a{ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->info.as<TermInfo>(),
@@ -1298,7 +1310,7 @@ int refsig_gpu_mrc_pairs(refsig_gpu_ctx* ctx, float tau, uint64_t* out_pairs, ui
     const PairGrid g = self_grid(ctx);
     {
       Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
-      prepare_bitmap(ctx, g, false);
+      prepare_bitmap(ctx, g, false, false);
       run_mrc_tiles(ctx, ctx->ST.as<float>(), ctx->ld, ctx->n_docs, ctx->ST.as<float>(), ctx->ld, ctx->n_docs, true,
                     ctx->K, tau, g);
       launched("mrc bitmap");
@@ -1576,7 +1588,7 @@ int refsig_gpu_mrc_query_pairs(refsig_gpu_ctx* q, float tau, uint64_t* out_pairs
     const PairGrid g{q->n_docs, db->n_docs, words_per_row(db->n_docs), false, 0, q->n_docs, 0};
     {
       Phase ph_tiles(q, REFSIG_PHASE_PAIR_TILES);
-      prepare_bitmap(q, g, false);
+      prepare_bitmap(q, g, false, false);
       run_mrc_tiles(q, q->ST.as<float>(), q->ld, q->n_docs, db->ST.as<float>(), db->ld, db->n_docs, false, q->K, tau,
                     g);
       launched("mrc query bitmap");
@@ -1626,7 +1638,7 @@ int refsig_gpu_mrc_pairs_rows(refsig_gpu_ctx* ctx, float tau, uint32_t row_lo, u
     g.row_end = row_hi;
     {
       Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
-      prepare_bitmap(ctx, g, false);
+      prepare_bitmap(ctx, g, false, false);
       run_mrc_tiles(ctx, ctx->ST.as<float>(), ctx->ld, ctx->n_docs, ctx->ST.as<float>(), ctx->ld, ctx->n_docs, true,
                     ctx->K, tau, g);
       launched("mrc bitmap");
@@ -1640,15 +1652,19 @@ int refsig_gpu_mrc_pairs_rows(refsig_gpu_ctx* ctx, float tau, uint32_t row_lo, u
 // scan -> emit (rows [lo, hi)), no host synchronisation.
 static void enqueue_step(refsig_gpu_ctx* ctx, int weight_mode, const uint32_t* refs, uint32_t K, float tau,
                          uint32_t lo, uint32_t hi) {
+  // the reference ids' H2D goes first, so that count's idf kernel -> reference build -> sign -> operand
+  // forms -> tiles -> scan -> emission is a chain of programmatic-dependent launches with no copy or memset
+  // node in between
+  const uint64_t u_cap = stage_reference_docs(ctx, refs, K);
   do_count(ctx, weight_mode);
-  do_set_reference_docs(ctx, refs, K);
+  build_reference_docs(ctx, K, u_cap);
   do_sign(ctx);
   PairGrid g = self_grid(ctx);
   g.row_begin = lo;
   g.row_end = hi;
   {
     Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
-    prepare_bitmap(ctx, g, false);
+    prepare_bitmap(ctx, g, false, false);
     run_mrc_tiles(ctx, ctx->ST.as<float>(), ctx->ld, ctx->n_docs, ctx->ST.as<float>(), ctx->ld, ctx->n_docs, true,
                   ctx->K, tau, g);
     launched("mrc bitmap");

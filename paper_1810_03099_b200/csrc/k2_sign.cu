@@ -67,8 +67,11 @@ __global__ void ref_reset_kernel(TermInfo* __restrict__ info, uint32_t vocab) {
 constexpr int kRefIpt2 = 4;
 __global__ void __launch_bounds__(256) ref_build_kernel(RefArgs r, TermInfo* __restrict__ info,
                                                         float* __restrict__ R, uint32_t* __restrict__ counter) {
+  // counter[0]: next compact row, counter[1]: finished CTAs — both zero at launch; the last CTA
+  // stores |U| in counter[2] and zeroes [0] and [1] again (no memset node before this PDL launch)
   __shared__ float red[8];
   const uint32_t k = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  pdl_wait();
   const uint2* e;
   uint32_t n;
   ref_range(r, k, e, n);
@@ -141,6 +144,15 @@ __global__ void __launch_bounds__(256) ref_build_kernel(RefArgs r, TermInfo* __r
       while (row[j] < 0) row[j] = ld_acquire(&info[x[j].x].ref_row);  // owner CTA publishes shortly
       const float w = r.explicit_w ? __uint_as_float(x[j].y) : static_cast<float>(x[j].y) * info[x[j].x].idf;
       R[static_cast<size_t>(row[j]) * r.Kp + k] = w * inv;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(counter + 1, 1u) == gridDim.x - 1) {
+      counter[2] = atomicAdd(counter, 0u);
+      counter[0] = 0;
+      counter[1] = 0;
     }
   }
 }
@@ -335,6 +347,16 @@ __device__ __forceinline__ void sign_half_docs(const SignArgs& a, uint32_t q, ui
   __syncwarp();
 }
 
+// The zero pad columns [n_docs, ld) of ST (the tile kernels read whole 128-column
+// panels), written by block 0 of the sign launch instead of a memset node
+// between the reference build and this PDL launch.
+__device__ __forceinline__ void sign_zero_pad(const SignArgs& a) {
+  if (blockIdx.x != 0) return;
+  const uint32_t pad = a.ld - a.n_docs;
+  for (uint32_t idx = threadIdx.x; idx < pad * a.K; idx += blockDim.x)
+    a.ST[static_cast<size_t>(idx / pad) * a.ld + a.n_docs + idx % pad] = 0.0f;
+}
+
 template <int KW>
 __global__ void __launch_bounds__(256, KW <= 24 ? 4 : (KW <= 32 ? 3 : 2)) sign_kernel(SignArgs a) {
   constexpr int CPL = (KW + 31) / 32;  // columns per lane
@@ -345,6 +367,8 @@ __global__ void __launch_bounds__(256, KW <= 24 ? 4 : (KW <= 32 ? 3 : 2)) sign_k
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   float* tw = tsm_dyn + wid * TW;
   int2* qw = reinterpret_cast<int2*>(tw);
+  pdl_wait();
+  sign_zero_pad(a);
   const bool cta = blockIdx.x < a.n_long;  // one long document per CTA
   {
     const uint32_t warp_blocks = static_cast<uint32_t>(ceil_div(a.n_half - a.n_long, kSignWarps));
@@ -491,6 +515,8 @@ __global__ void __launch_bounds__(256) sign_col_kernel(SignArgs a) {
   __shared__ float red[kSignWarps][32 * KS + 1];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int2* qw = queue[wid];
+  pdl_wait();
+  sign_zero_pad(a);
   const bool cta = blockIdx.x < a.n_long;  // one long document per CTA
   uint32_t q;
   if (cta) {
@@ -587,8 +613,7 @@ void launch_ref_build(const RefArgs& r, TermInfo* info, uint32_t vocab, uint32_t
                       uint64_t n_entries_max, cudaStream_t s) {
   (void)vocab;
   (void)n_entries_max;
-  cudaMemsetAsync(counter, 0, sizeof(uint32_t), s);
-  ref_build_kernel<<<r.K, 256, 0, s>>>(r, info, R, counter);
+  launch_pdl(ref_build_kernel, dim3(r.K), dim3(256), 0, s, r, info, R, counter);
   note_launch();
 }
 
@@ -597,7 +622,7 @@ void launch_sign_kw(const SignArgs& a, unsigned g, cudaStream_t s) {
   constexpr int TW = 32 * (KW + 1) > 2 * static_cast<int>(kSignStep) ? 32 * (KW + 1) : 2 * kSignStep;
   constexpr size_t smem = sizeof(float) * kSignWarps * TW;
   ensure_smem(sign_kernel<KW>, smem);
-  sign_kernel<KW><<<g, 32 * kSignWarps, smem, s>>>(a);
+  launch_pdl(sign_kernel<KW>, dim3(g), dim3(32 * kSignWarps), smem, s, a);
 }
 
 void launch_sign(const SignArgs& a, cudaStream_t s) {
@@ -608,13 +633,13 @@ void launch_sign(const SignArgs& a, cudaStream_t s) {
                                                 ceil_div(a.n_docs - a.n_half, 2 * kSignWarps));
   if (a.K > 32) {  // column-owner variant, Kp = roundup(K, 32)
     switch (a.Kp / 32) {
-      case 2: sign_col_kernel<2><<<g, 32 * kSignWarps, 0, s>>>(a); break;
-      case 3: sign_col_kernel<3><<<g, 32 * kSignWarps, 0, s>>>(a); break;
-      case 4: sign_col_kernel<4><<<g, 32 * kSignWarps, 0, s>>>(a); break;
-      case 5: sign_col_kernel<5><<<g, 32 * kSignWarps, 0, s>>>(a); break;
-      case 6: sign_col_kernel<6><<<g, 32 * kSignWarps, 0, s>>>(a); break;
-      case 7: sign_col_kernel<7><<<g, 32 * kSignWarps, 0, s>>>(a); break;
-      default: sign_col_kernel<8><<<g, 32 * kSignWarps, 0, s>>>(a); break;
+      case 2: launch_pdl(sign_col_kernel<2>, dim3(g), dim3(32 * kSignWarps), 0, s, a); break;
+      case 3: launch_pdl(sign_col_kernel<3>, dim3(g), dim3(32 * kSignWarps), 0, s, a); break;
+      case 4: launch_pdl(sign_col_kernel<4>, dim3(g), dim3(32 * kSignWarps), 0, s, a); break;
+      case 5: launch_pdl(sign_col_kernel<5>, dim3(g), dim3(32 * kSignWarps), 0, s, a); break;
+      case 6: launch_pdl(sign_col_kernel<6>, dim3(g), dim3(32 * kSignWarps), 0, s, a); break;
+      case 7: launch_pdl(sign_col_kernel<7>, dim3(g), dim3(32 * kSignWarps), 0, s, a); break;
+      default: launch_pdl(sign_col_kernel<8>, dim3(g), dim3(32 * kSignWarps), 0, s, a); break;
     }
     note_launch();
     return;

@@ -409,8 +409,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
 // write each panel as 16-byte chunks in [chunk][doc] order (coalesced).
 __global__ void __launch_bounds__(256) tc_forms_kernel(const float* __restrict__ ST, uint32_t ld, uint32_t n_docs,
                                                        uint32_t K, uint32_t KP, float tau, __half* __restrict__ rowf,
-                                                       __half* __restrict__ colf) {
+                                                       __half* __restrict__ colf, uint32_t* __restrict__ rowcnt,
+                                                       uint32_t n_rowcnt) {
   extern __shared__ __align__(16) __half fsm[];
+  pdl_wait();
+  // the tile kernel's row counts start at zero: zeroed here, 128 per panel (no memset node before this PDL launch)
+  if (rowcnt && threadIdx.x < 128 && blockIdx.x * 128 + threadIdx.x < n_rowcnt) rowcnt[blockIdx.x * 128 + threadIdx.x] = 0;
   const uint32_t stride = KP + 8;  // halves per doc row (16-byte aligned, staggers banks)
   __half* R = fsm;
   __half* C = fsm + 128 * stride;
@@ -475,8 +479,11 @@ __global__ void __launch_bounds__(256) tc_forms_kernel(const float* __restrict__
 // [kc][dl] (coalesced). Grid: (panels, ceil(K'/8 / 2)), 256 threads.
 __global__ void __launch_bounds__(256) tc_forms_any_kernel(const float* __restrict__ ST, uint32_t ld, uint32_t n_docs,
                                                            uint32_t K, uint32_t KP, float tau,
-                                                           __half* __restrict__ rowf, __half* __restrict__ colf) {
+                                                           __half* __restrict__ rowf, __half* __restrict__ colf,
+                                                           uint32_t* __restrict__ rowcnt, uint32_t n_rowcnt) {
   const uint32_t pan = blockIdx.x, dl = threadIdx.x & 127, kc = blockIdx.y * 2 + (threadIdx.x >> 7);
+  pdl_wait();
+  if (rowcnt && blockIdx.y == 0 && threadIdx.x < 128 && pan * 128 + threadIdx.x < n_rowcnt) rowcnt[pan * 128 + threadIdx.x] = 0;
   if (kc * 8 >= KP) return;
   const uint32_t d = pan * 128 + dl;
   const __half t0 = __float2half_rn(tau);
@@ -563,21 +570,21 @@ size_t mrc_tc_form_bytes(uint32_t K, uint32_t n_docs) {
 }
 
 void launch_mrc_tc_forms(const float* ST, uint32_t ld, uint32_t n_docs, uint32_t K, float tau, void* rowf, void* colf,
-                         cudaStream_t s) {
+                         uint32_t* rowcnt, uint32_t n_rowcnt, cudaStream_t s) {
   const uint32_t KP = mrc_tc_kp(K);
   const uint32_t n_pan = static_cast<uint32_t>(ceil_div(n_docs, 128));
   if (!n_pan) return;
   if (KP > kTcSmallKP) {
     const dim3 grid(n_pan, static_cast<unsigned>(ceil_div(KP / 8, 2)));
-    tc_forms_any_kernel<<<grid, 256, 0, s>>>(ST, ld, n_docs, K, KP, tau, static_cast<__half*>(rowf),
-                                             static_cast<__half*>(colf));
+    launch_pdl(tc_forms_any_kernel, grid, dim3(256), 0, s, ST, ld, n_docs, K, KP, tau, static_cast<__half*>(rowf),
+               static_cast<__half*>(colf), rowcnt, n_rowcnt);
     note_launch();
     return;
   }
   const size_t smem = 2ull * 128 * (KP + 8) * sizeof(__half);  // <= 69.6 KB at K' = 128
   ensure_smem(tc_forms_kernel, 72 * 1024);
-  tc_forms_kernel<<<n_pan, 256, smem, s>>>(ST, ld, n_docs, K, KP, tau, static_cast<__half*>(rowf),
-                                           static_cast<__half*>(colf));
+  launch_pdl(tc_forms_kernel, dim3(n_pan), dim3(256), smem, s, ST, ld, n_docs, K, KP, tau, static_cast<__half*>(rowf),
+             static_cast<__half*>(colf), rowcnt, n_rowcnt);
   note_launch();
 }
 

@@ -147,8 +147,9 @@ void launch_mrc_bitmap(const float* ST_rows, uint32_t ld_rows, const float* ST_c
 uint32_t mrc_tc_kp(uint32_t K);
 bool mrc_tc_supported(uint32_t K, float tau);
 size_t mrc_tc_form_bytes(uint32_t K, uint32_t n_docs);
+// rowcnt != NULL: also zero rowcnt[0 .. n_rowcnt) (the tile kernel's row counts; n_rowcnt <= n_docs panels).
 void launch_mrc_tc_forms(const float* ST, uint32_t ld, uint32_t n_docs, uint32_t K, float tau, void* rowf, void* colf,
-                         cudaStream_t s);
+                         uint32_t* rowcnt, uint32_t n_rowcnt, cudaStream_t s);
 void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
                    uint32_t* rowcnt, cudaStream_t s);
 void launch_hamming_bitmap(const uint64_t* f_rows, const uint64_t* f_cols, int max_dist, const PairGrid& g,
