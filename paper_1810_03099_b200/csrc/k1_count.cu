@@ -66,14 +66,25 @@ __device__ __forceinline__ uint32_t next_pow2(uint32_t x) {
 // previous level's) and every compare-exchange of the level sorts ascending —
 // the register stages then need no direction selects. The last level
 // (K = P) is ascending everywhere, which restores the keys.
-template <int IPT, int T, int K, int J, bool NORM>
+// BAR = 0: the CTA barrier; BAR > 0: named barrier BAR over the T threads of
+// a sub-group (two independent sorts in one CTA, group_split_kernel).
+template <int BAR, int T>
+__device__ __forceinline__ void group_barrier() {
+  if constexpr (BAR == 0) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(BAR), "r"(T) : "memory");
+  }
+}
+
+template <int IPT, int T, int K, int J, bool NORM, int BAR = 0>
 __device__ __forceinline__ void gbitonic_stage(uint32_t (&v)[IPT], uint32_t t, uint32_t* sm) {
   if constexpr (J >= 32 * IPT) {
     constexpr uint32_t tj = J / IPT;
-    __syncthreads();
+    group_barrier<BAR, T>();
 #pragma unroll
     for (int q = 0; q < IPT; ++q) sm[q * T + t] = v[q];
-    __syncthreads();
+    group_barrier<BAR, T>();
     const bool take_min = NORM ? (t & tj) == 0 : ((t & tj) == 0) == (((t * IPT) & K) == 0);
 #pragma unroll
     for (int q = 0; q < IPT; ++q) {
@@ -105,10 +116,10 @@ __device__ __forceinline__ void gbitonic_stage(uint32_t (&v)[IPT], uint32_t t, u
       }
     }
   }
-  if constexpr (J > 1) gbitonic_stage<IPT, T, K, J / 2, NORM>(v, t, sm);
+  if constexpr (J > 1) gbitonic_stage<IPT, T, K, J / 2, NORM, BAR>(v, t, sm);
 }
 
-template <int IPT, int T, int K, int KMAX>
+template <int IPT, int T, int K, int KMAX, int BAR = 0>
 __device__ __forceinline__ void gbitonic_level(uint32_t (&v)[IPT], uint32_t t, uint32_t* sm, uint32_t& cur) {
   if constexpr (K >= IPT) {
     const uint32_t want = ((t * IPT) & K) ? 0xffffffffu : 0u;  // descending block: hold complements
@@ -116,17 +127,17 @@ __device__ __forceinline__ void gbitonic_level(uint32_t (&v)[IPT], uint32_t t, u
 #pragma unroll
     for (int q = 0; q < IPT; ++q) v[q] ^= x;
     cur = want;
-    gbitonic_stage<IPT, T, K, K / 2, true>(v, t, sm);
+    gbitonic_stage<IPT, T, K, K / 2, true, BAR>(v, t, sm);
   } else {
-    gbitonic_stage<IPT, T, K, K / 2, false>(v, t, sm);
+    gbitonic_stage<IPT, T, K, K / 2, false, BAR>(v, t, sm);
   }
-  if constexpr (K < KMAX) gbitonic_level<IPT, T, 2 * K, KMAX>(v, t, sm, cur);
+  if constexpr (K < KMAX) gbitonic_level<IPT, T, 2 * K, KMAX, BAR>(v, t, sm, cur);
 }
 
-template <int IPT, int T>
+template <int IPT, int T, int BAR = 0>
 __device__ __forceinline__ void gbitonic_sort(uint32_t (&v)[IPT], uint32_t t, uint32_t* sm) {
   uint32_t cur = 0;
-  gbitonic_level<IPT, T, 2, T * IPT>(v, t, sm, cur);
+  gbitonic_level<IPT, T, 2, T * IPT, BAR>(v, t, sm, cur);
 }
 
 // Multi-warp sort whose warp-local levels (K <= 32*IPT: registers and
@@ -324,6 +335,114 @@ __global__ void __launch_bounds__(32 * W) group_sort_kernel(CountArgs a, const u
   if (t == 0) a.nnz[d] = n;
 }
 
+// Split pass: documents of (P/2, P] tokens, P = 256 W, without the pow2 padding
+// of the whole document (~30% of the keys at configs[1]): the first M = P/2
+// tokens are sorted by warps [0, W/2) (M keys, no padding), the other r =
+// len - M by the first R/256 warps of [W/2, W) as R = pow2(r) keys (at least
+// 64: IPT 2 / 4 for one warp), each half with its own named barrier; then one
+// merge path over the two sorted runs in shared memory gives every thread its
+// 8 consecutive keys of the document, which are run-length encoded as in
+// group_sort_kernel.
+template <int IPT, int WR, int BAR>
+__device__ __forceinline__ void split_rest_sort(const CountArgs& a, uint64_t b, uint32_t M, uint32_t len,
+                                                uint32_t tr, uint32_t* scratch, uint32_t* B, uint32_t& bad) {
+  constexpr int TR = 32 * WR;
+  if (tr >= static_cast<uint32_t>(TR)) return;
+  uint32_t v[IPT];
+  const uint32_t wbase = (tr & ~31u) * IPT, lane = tr & 31;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const uint32_t i = M + wbase + k * 32 + lane;
+    v[k] = load_key(a, b, i, len, bad);
+  }
+  if constexpr (WR == 1) {
+    bitonic_regs<IPT>(v, lane);
+  } else {
+    gbitonic_sort<IPT, TR, BAR>(v, tr, scratch);
+    group_barrier<BAR, TR>();  // B aliases the scratch the last exchange stage read
+  }
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) B[tr * IPT + q] = v[q];
+}
+
+template <int W>
+__global__ void __launch_bounds__(32 * W) group_split_kernel(CountArgs a, const uint32_t* __restrict__ docs,
+                                                            uint32_t n_docs) {
+  constexpr int T = 32 * W, WM = W / 2, TM = 32 * WM;
+  constexpr uint32_t M = 256u * WM;             // main run: exactly M tokens (len > M)
+  // sort exchanges: main [0, 8 TM), rest [8 TM, 8 T); afterwards the sorted runs A (M = 8 TM words)
+  // and B (<= M) in the same two regions
+  __shared__ uint32_t scratch[8 * T];
+  uint32_t* const A = scratch;
+  uint32_t* const B = scratch + 8 * TM;
+  __shared__ uint32_t rle_sm[3 * W + 2];
+  const uint32_t t = threadIdx.x, lane = t & 31;
+  const uint32_t d = docs[blockIdx.x];
+  const uint64_t b = a.doc_off[d];
+  const uint32_t len = static_cast<uint32_t>(a.doc_off[d + 1] - b);
+  const uint32_t r = len - M;
+  const uint32_t R = max(64u, next_pow2(r));
+  uint32_t bad = 0;
+  if (t < static_cast<uint32_t>(TM)) {  // main: tokens [0, M)
+    uint32_t v[8];
+    const uint32_t wbase = (t & ~31u) * 8;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = load_key(a, b, wbase + k * 32 + lane, len, bad);
+    if constexpr (WM == 1) {
+      bitonic_regs<8>(v, lane);
+    } else {
+      gbitonic_sort<8, TM, 1>(v, t, scratch);
+      group_barrier<1, TM>();  // A aliases the scratch the last exchange stage read
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) A[t * 8 + q] = v[q];
+  } else {  // rest: tokens [M, len) as R keys
+    const uint32_t tr = t - TM;
+    uint32_t* sc = B;
+    if (R == 64) {
+      split_rest_sort<2, 1, 2>(a, b, M, len, tr, sc, B, bad);
+    } else if (R == 128) {
+      split_rest_sort<4, 1, 2>(a, b, M, len, tr, sc, B, bad);
+    } else if (R == 256) {
+      split_rest_sort<8, 1, 2>(a, b, M, len, tr, sc, B, bad);
+    } else if (R == 512) {
+      if constexpr (WM >= 2) split_rest_sort<8, 2, 2>(a, b, M, len, tr, sc, B, bad);
+    } else if (R == 1024) {
+      if constexpr (WM >= 4) split_rest_sort<8, 4, 2>(a, b, M, len, tr, sc, B, bad);
+    } else if (R == 2048) {
+      if constexpr (WM >= 8) split_rest_sort<8, 8, 2>(a, b, M, len, tr, sc, B, bad);
+    } else {
+      if constexpr (WM >= 16) split_rest_sort<8, 16, 2>(a, b, M, len, tr, sc, B, bad);
+    }
+  }
+  flag_bad(a, bad);
+  __syncthreads();
+  // merge path: thread t takes outputs [8t, 8t + 8) of merge(A[0, M), B[0, R)); B's padding is kInf
+  uint32_t v[8];
+  const uint32_t diag = 8 * t;
+  if (diag >= M + R) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = kInf;
+  } else {
+    uint32_t lo = diag > R ? diag - R : 0u, hi = min(diag, M);
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (A[mid] <= B[diag - mid - 1]) lo = mid + 1; else hi = mid;
+    }
+    uint32_t i = lo, j = diag - lo;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t x = i < M ? A[i] : kInf, y = j < R ? B[j] : kInf;
+      const bool ta = x <= y;
+      v[q] = ta ? x : y;
+      i += ta;
+      j += !ta;
+    }
+  }
+  const uint32_t n = rle_regs<8, W>(v, t, len, a.ent + b, a, rle_sm);
+  if (t == 0) a.nnz[d] = n;
+}
+
 // ---------------------------------------------------------------------------
 // Documents longer than 8192 tokens: bitonic sort in a global scratch region
 // (next_pow2(len) keys each), then a chunked block-wide RLE.
@@ -513,6 +632,22 @@ void launch_count_warp(int ipt, const CountArgs& a, const uint32_t* docs, uint32
 
 void launch_count_group(int cls, const CountArgs& a, const uint32_t* docs, uint32_t n, cudaStream_t s) {
   if (n == 0) return;
+  // split pass (group_split_kernel) for the classes in the mask (bit cls + 1); REFSIG_K1_SPLIT overrides
+  static const uint32_t split_mask = [] {
+    const char* m = std::getenv("REFSIG_K1_SPLIT");
+    return m ? static_cast<uint32_t>(std::strtoul(m, nullptr, 0)) : 0x1Cu;  // classes 1-3 (>= 1025 tokens): measured A/B per class
+  }();
+  if ((split_mask >> (cls + 1)) & 1u) {
+    switch (cls) {
+      case -1: group_split_kernel<2><<<n, 64, 0, s>>>(a, docs, n); break;
+      case 0: group_split_kernel<4><<<n, 128, 0, s>>>(a, docs, n); break;
+      case 1: group_split_kernel<8><<<n, 256, 0, s>>>(a, docs, n); break;
+      case 2: group_split_kernel<16><<<n, 512, 0, s>>>(a, docs, n); break;
+      default: group_split_kernel<32><<<n, 1024, 0, s>>>(a, docs, n); break;
+    }
+    note_launch();
+    return;
+  }
   // 8 keys per thread: twice the threads of 16-key groups, half the serial
   // compare-exchange chain per thread (measured faster for every class)
   switch (cls) {
