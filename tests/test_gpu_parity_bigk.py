@@ -108,3 +108,24 @@ def test_mrc_pairs_c3_sampled_panel(gpu_ctx_factory):
     pairs, border = oracle.mrc_pairs(o.S, tau, BAND, 0, 2048)
     nb = assert_pairs_match(keys, pairs, border, "c3 rows [0,2048)")
     print(f"c3 panel: {len(keys)} GPU pairs, {len(pairs)} oracle, {len(border)} in band, {nb} differ")
+
+
+@pytest.mark.parametrize("K", [64, 128])
+def test_evaluate_large_k_vs_oracle(gpu_ctx_factory, K):
+    """SPEC eval with the MRC dot at K = 64 / 128 on tcgen05 (k5_tc.cu: head and
+    MRC chains of one K walk) against the oracle's double-precision evaluation."""
+    cp, cfg = C.config_corpus("c0")
+    cp = cp.slice_docs(900)
+    refs = C.sample_refs(1, cp.n_docs, K)
+    ctx = gpu_ctx_factory()
+    _signed(ctx, cp, refs)
+    ctx.simhash(0)
+    g = ctx.evaluate()
+    o = oracle.mrc_pipeline(cp.tokens, cp.doc_off, cp.vocab, refs)
+    fp = oracle.simhash(o.counts, o.idf, 0)
+    ref = oracle.evaluate(o.x, o.S, fp)
+    assert g["pairs"] == ref["pairs"]
+    for k in ("mrc_mae", "mrc_mean_error", "simhash_mae", "simhash_mean_error"):
+        assert abs(g[k] - ref[k]) <= 2e-6 + 1e-5 * abs(ref[k]), (k, g[k], ref[k])
+    for k in ("mrc_variance", "simhash_variance"):
+        assert abs(g[k] - ref[k]) <= 1e-7 + 1e-4 * abs(ref[k]), (k, g[k], ref[k])

@@ -112,3 +112,19 @@ def test_step_tensor_core_and_cuda_core_k3(gpu_ctx_factory, K):
     for _ in range(3):
         ctx.mrc_step(refs, 0.9)
         assert np.array_equal(ctx.step_result(fetch=True), want)
+
+
+@pytest.mark.parametrize("K", [64, 128])
+def test_step_large_k_graph(gpu_ctx_factory, K):
+    """The captured step with the chunked tcgen05 K3 (K' = 208 / 400) and the
+    PDL chain (reference build, sign, forms) equals the eager calls."""
+    cp, cfg = C.config_corpus("c1")
+    cp = cp.slice_docs(3000)
+    refs = C.sample_refs(3, cp.n_docs, K)
+    ctx = gpu_ctx_factory()
+    ctx.load_corpus(cp.tokens, cp.doc_off, cp.vocab)
+    want = eager(ctx, refs, 0.99)
+    for _ in range(3):
+        ctx.mrc_step(refs, 0.99)
+        assert np.array_equal(ctx.step_result(fetch=True), want)
+    assert ctx.reference_union() > 0
