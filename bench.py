@@ -15,12 +15,16 @@ events on the stream the library launches on, max over ranks.
 
 --impl reference times the reference CPU path (the oracle restatement in
 oracle/; the reference has no MRC sign/compare code) on this host's cores.
-N>1 (torchrun): the pair triangle is split into row panels (shard.py), K1/K2
-are replicated per rank (no data-path collective), scaling "strong".
+N>1 (torchrun): weak scaling — every rank runs the whole path on its own
+batch (a seeded document permutation of configs[1]; batches are independent,
+no data-path collective); value = N batches' pairs / the slowest rank's time.
+The same run also reports strong_variant: ONE triangle in row panels
+(shard.py) with K1/K2 replicated per rank.
 """
 from __future__ import annotations
 
 import argparse
+import collections
 import json
 import os
 import statistics
@@ -105,6 +109,16 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def allreduce(dist, vals, dev, op):
+    """max / sum of a few host numbers over ranks (device tensors under NCCL,
+    host tensors under gloo); float64 keeps int64 counts exact below 2^53."""
+    import torch
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=dev if on_dev else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return t.tolist()
 
 
 def dist_env():
@@ -205,7 +219,9 @@ def workload_config(cfg, cp, tau, world):
             "n_docs": cp.n_docs, "tokens": int(cp.doc_off[-1]), "K": cfg["K"], "tau": tau,
             "pairs_per_step": cp.n_docs * (cp.n_docs - 1) // 2,
             "l2": "flushed before every timed step (512 MB write); inputs < L2 otherwise",
-            "parallelism": f"pair-triangle row panels x{world}" if world > 1 else "single GPU"}
+            "parallelism": (f"dp{world}: one independent batch per GPU (rank r: a seeded document permutation "
+                            f"of configs[1]); row-panel strong scaling in strong_variant") if world > 1
+                           else "single GPU"}
 
 
 # --------------------------------------------------------------------------
@@ -219,19 +235,36 @@ def run_ours(args):
 
     world, rank, local = dist_env()
     dist = None
+    # BENCH_DIST_BACKEND=gloo + BENCH_DEVICE=0: a functional check of the N > 1
+    # plumbing with every rank on one GPU (timings meaningless; never a bench line)
+    gpu = int(os.environ.get("BENCH_DEVICE", local))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        torch.cuda.set_device(gpu)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(backend)
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    local = gpu
 
     cp, cfg, refs, thr = corpus_and_config(args.config)
     tau = args.tau if args.tau is not None else thr["tau_mrc"]
     N, K = cp.n_docs, cfg["K"]
-    lo, hi = shard.row_shards(N, world)[rank]
-    my_pairs = shard.pairs_in_rows(N, lo, hi)
     P = N * (N - 1) // 2
+    cp0, refs0 = cp, refs
+    if world > 1 and rank > 0:
+        # weak scaling: every rank runs the whole hot path on its OWN batch — a
+        # seeded document permutation of configs[1] (same work, its own layout);
+        # batches are independent, so no data-path collective
+        from paper_1810_03099_b200 import corpus as C
+        pin, off, rrefs = permuted_batches(cp, refs, 1, seed=1000 + rank)[0]
+        cp = C.Corpus(np.asarray(pin).copy(), off, cp.vocab, cp.dup_src)
+        refs = rrefs
+    lo, hi = 0, N
+    my_pairs = P
 
     stream = torch.cuda.Stream(dev)
     ctx = R.Context(local)
@@ -285,17 +318,15 @@ def run_ours(args):
         ctx.set_profiling(False)
         n_eager = max(3, args.steps)
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    # N > 1: the same corpus split into row panels of ONE triangle (strong scaling, K1/K2 replicated)
+    strong = measure_strong_panels(cp0, refs0, tau, world, rank, dev, flush, args, dist) if dist else None
     tot_ms = sum(step_ms)
     tot_sign = sum(phases[k][0] for k in ("count", "reference", "sign")) / n_eager * args.steps
     if dist:
-        t = torch.tensor([tot_ms, tot_sign], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms, tot_sign = t.tolist()
-        c = torch.tensor([n_cand], dtype=torch.int64, device=dev)
-        dist.all_reduce(c)
-        n_cand = int(c.item())
+        tot_ms, tot_sign = allreduce(dist, [tot_ms, tot_sign], dev, "max")
+        n_cand = int(allreduce(dist, [n_cand], dev, "sum")[0])
     ms_per_step = tot_ms / args.steps
-    value = P / (ms_per_step / 1e3)
+    value = world * P / (ms_per_step / 1e3)  # all ranks' batches / the slowest rank's time
     sig_per_s = N / (tot_sign / args.steps / 1e3)
 
     # Isolated K2 with a cold L2 (HBM roofline of the signature kernel).
@@ -315,13 +346,11 @@ def run_ours(args):
                  if world == 1 and N <= 65536 else None)
     modes = sorted(e2e_all)
     if dist:
-        t = torch.tensor([e2e_all[m]["_ms"] for m in modes], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        for m, v in zip(modes, t.tolist()):
+        for m, v in zip(modes, allreduce(dist, [e2e_all[m]["_ms"] for m in modes], dev, "max")):
             e2e_all[m]["_ms"] = v
     main_mode = "step16" if "step16" in e2e_all else "step"
     e2e = e2e_fresh if e2e_fresh else e2e_all[main_mode]
-    e2e_value = P / (e2e["_ms"] / 1e3)
+    e2e_value = world * P / (e2e["_ms"] / 1e3)
     # the rank-0 extras at the larger configs (configs[3] compare + sign, configs[4] query stream)
     extras = measure_extras(dev, args) if world == 1 and not args.no_extras else None
 
@@ -354,9 +383,9 @@ def run_ours(args):
         dominant = max(("mrc_tiles", "sign", "count", "pair_emit"), key=lambda k: roof[k]["share_of_step"])
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": data_desc(cfg),
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": data_desc(cfg),
                 "config": workload_config(cfg, cp, tau, world),
-                "signatures_per_sec": sig_per_s, "candidates_per_step": n_cand,
+                "signatures_per_sec": world * sig_per_s, "candidates_per_step": n_cand,
                 "roofline": {**roof[dominant], "kernel": dominant},
                 "rooflines": roof,
                 "phase_ms_per_step": {k: v[0] / n_eager for k, v in phases.items() if v[1]},
@@ -402,6 +431,8 @@ def run_ours(args):
                                          "ms_per_step": e2e_all["keys"]["_ms"],
                                          "d2h_bytes_per_step": e2e_all["keys"]["d2h"],
                                          "note": "same, pairs returned as sorted uint64 (i<<32|j) keys"}}}
+        if strong:
+            line["strong_variant"] = strong
         if extras:
             line["configs_extra"] = extras
         if world == 1 and not args.no_cpu_baseline:
@@ -412,6 +443,51 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def measure_strong_panels(cp, refs, tau, world, rank, dev, flush, args, dist):
+    """N > 1 strong-scaling variant: ONE configs[1] triangle cut into row
+    panels of equal tile counts (shard.row_shards), every rank counting and
+    signing the whole corpus (replicated K1/K2, no data-path collective) and
+    comparing its panel. Device time per step = max over ranks."""
+    import torch
+    import paper_1810_03099_b200 as R
+    from paper_1810_03099_b200 import shard
+    N = cp.n_docs
+    lo, hi = shard.row_shards(N, world)[rank]
+    stream = torch.cuda.Stream(dev)
+    ctx = R.Context(dev.index)
+    ctx.set_stream(stream.cuda_stream)
+    tok = torch.from_numpy(cp.tokens.view(np.int32)).to(dev)
+    try:
+        with torch.cuda.stream(stream):
+            ctx.load_corpus_device(tok.data_ptr(), cp.doc_off, cp.vocab)
+            for _ in range(args.warmup):
+                flush.fill_(1)
+                ctx.mrc_step(refs, tau, R.WEIGHT_TFIDF, lo, hi)
+                ctx.step_result()
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            torch.cuda.synchronize(dev)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(args.steps)]
+            n = 0
+            for s in range(args.steps):
+                flush.fill_(s)
+                ev[s][0].record(stream)
+                ctx.mrc_step(refs, tau, R.WEIGHT_TFIDF, lo, hi)
+                ev[s][1].record(stream)
+                n = ctx.step_result()
+            torch.cuda.synchronize(dev)
+    finally:
+        ctx.close()
+    ms = allreduce(dist, [sum(a.elapsed_time(b) for a, b in ev)], dev, "max")[0] / args.steps
+    n_all = int(allreduce(dist, [n], dev, "sum")[0])
+    P = N * (N - 1) // 2
+    return {"value": P / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "scaling": "strong",
+            "candidates_per_step": n_all,
+            "parallelism": f"one configs[1] triangle in {world} row panels (equal tile counts); K1/K2 replicated",
+            "note": "device time max over ranks; the rank's panel is its share of the pair tiles"}
 
 
 def measure_sign_isolated(ctx, stream, flush, dev, reps):
@@ -751,18 +827,29 @@ def measure_c4(dev, batches=3):
             qc.stage_corpus(*qb[1])
             e0.record(stream)
             w0 = time.perf_counter()
+            evs, host = [], collections.defaultdict(float)
+
+            def call(name, fn):
+                t = time.perf_counter()
+                r = fn()
+                host[name] += (time.perf_counter() - t) * 1e3
+                return r
             for b in range(1, batches + 1):
-                qc.swap_corpus()
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(stream)
+                evs.append(ev)
+                call("swap_corpus", qc.swap_corpus)
                 if b + 1 <= batches:
-                    qc.stage_corpus(*qb[b + 1])
-                qc.count()
-                qc.sign(fetch=False)
-                cands.append(qc.mrc_query_pairs(tau, fetch=False))
-                qc.simhash(0)
-                hams.append(qc.hamming_query_pairs(thr["hamming_max"], fetch=False))
+                    call("stage_corpus", lambda: qc.stage_corpus(*qb[b + 1]))
+                call("count", qc.count)
+                call("sign", lambda: qc.sign(fetch=False))
+                cands.append(call("mrc_query_pairs", lambda: qc.mrc_query_pairs(tau, fetch=False)))
+                call("simhash", lambda: qc.simhash(0))
+                hams.append(call("hamming_query_pairs", lambda: qc.hamming_query_pairs(thr["hamming_max"], fetch=False)))
             e1.record(stream)
             torch.cuda.synchronize(dev)
             wall = time.perf_counter() - w0
+            each = [a.elapsed_time(b) for a, b in zip(evs, evs[1:] + [e1])]
             ph = qc.phase_times()
             qc.set_profiling(False)
             ms_b = e0.elapsed_time(e1) / batches
@@ -786,7 +873,8 @@ def measure_c4(dev, batches=3):
     return {"workload": f"configs[4]: database {D} docs (vocab {db.vocab}, {int(db.doc_off[-1])} tokens) at K={K} "
                         f"resident in HBM; {batches} streamed batches of {Q} queries (10% near-duplicates of "
                         f"database docs); MRC tau={tau} and Hamming <= {thr['hamming_max']} over Q x D",
-            "ms_per_batch": ms_b, "wall_ms_per_batch": wall * 1e3 / batches,
+            "ms_per_batch": ms_b, "wall_ms_per_batch": wall * 1e3 / batches, "ms_each_batch": each,
+            "host_ms_per_call": {k: v / batches for k, v in host.items()},
             "doc_pairs_per_sec": Q * D / (ms_b / 1e3), "pairs_per_batch": Q * D,
             "query_signatures_per_sec": Q / (sig_ms / 1e3), "db_signatures_per_sec": D / (db_sig_ms / 1e3),
             "db_signature_ms": db_sig_ms, "candidates_per_batch": [int(c) for c in cands],

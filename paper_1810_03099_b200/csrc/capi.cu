@@ -96,6 +96,9 @@ struct DevBuf {
     if (p) cudaFree(p);
   }
   // Grow-only; contents are not preserved. Returns true if (re)allocated.
+  // A regrowth takes 1/8 headroom: streamed batches vary in size by a few
+  // percent, and every reallocation's cudaFree waits for the whole device
+  // (it would serialise the batch pipeline).
   bool ensure(size_t bytes) {
     if (bytes == 0) bytes = 16;
     if (bytes <= cap) return false;
@@ -103,6 +106,7 @@ struct DevBuf {
       cudaFree(p);
       p = nullptr;
       cap = 0;
+      bytes += bytes / 8;
     }
     const size_t extra = canary_on() ? kCanaryBytes : 0;
     ck(cudaMalloc(&p, bytes + extra), "cudaMalloc");

@@ -18,6 +18,19 @@ struct __align__(8) TermInfo {
 };
 static_assert(sizeof(TermInfo) == 8, "TermInfo is one 8-byte gather");
 
+// Read-only loads that do not allocate in L1: streamed count entries and the
+// per-nonzero TermInfo gathers, so L1 keeps the reused reference-table rows.
+__device__ __forceinline__ uint2 ld_na(const uint2* p) {
+  uint2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ TermInfo ld_na(const TermInfo* p) {
+  TermInfo v;
+  asm("ld.global.nc.L1::no_allocate.v2.b32 {%0, %1}, [%2];" : "=f"(v.idf), "=r"(v.ref_row) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

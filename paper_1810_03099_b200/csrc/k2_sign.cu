@@ -170,6 +170,25 @@ __global__ void __launch_bounds__(256) ref_build_kernel(RefArgs r, TermInfo* __r
 // interleaved steps; the 8 column vectors are added in warp order), shorter
 // ones a warp. Every sum has a fixed order: signatures do not depend on
 // scheduling.
+// K2_HINT (A/B): 0 plain __ldg / gathers, 1 count entries L1::no_allocate,
+// 2 entries and TermInfo gathers L1::no_allocate.
+#ifndef REFSIG_K2_HINT
+#define REFSIG_K2_HINT 0
+#endif
+__device__ __forceinline__ uint2 sign_ent(const uint2* p) {
+#if REFSIG_K2_HINT >= 1
+  return ld_na(p);
+#else
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ TermInfo sign_info(const TermInfo* p) {
+#if REFSIG_K2_HINT >= 2
+  return ld_na(p);
+#else
+  return *p;
+#endif
+}
 constexpr int kSignWarps = 8;
 constexpr uint32_t kSignStep = 128;
 
@@ -183,11 +202,11 @@ __device__ __forceinline__ void sign_slab_steps(const SignArgs& a, const uint2* 
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const uint32_t i = c + 32u * u + lane;
-      x[u] = i < n ? __ldg(e + i) : make_uint2(0u, 0u);
+      x[u] = i < n ? sign_ent(e + i) : make_uint2(0u, 0u);
     }
     TermInfo ti[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) ti[u] = (c + 32u * u + lane < n) ? a.info[x[u].x] : TermInfo{0.0f, -1};
+    for (int u = 0; u < 4; ++u) ti[u] = (c + 32u * u + lane < n) ? sign_info(a.info + x[u].x) : TermInfo{0.0f, -1};
     uint32_t qn = 0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -274,11 +293,11 @@ __device__ __forceinline__ void sign_half_docs(const SignArgs& a, uint32_t q, ui
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const uint32_t i = c + 16u * u + hl;
-      x[u] = i < n ? __ldg(e + i) : make_uint2(0u, 0u);
+      x[u] = i < n ? sign_ent(e + i) : make_uint2(0u, 0u);
     }
     TermInfo ti[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) ti[u] = (c + 16u * u + hl < n) ? a.info[x[u].x] : TermInfo{0.0f, -1};
+    for (int u = 0; u < 4; ++u) ti[u] = (c + 16u * u + hl < n) ? sign_info(a.info + x[u].x) : TermInfo{0.0f, -1};
     uint32_t qn = 0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -461,11 +480,11 @@ __device__ __forceinline__ void signc_steps(const SignArgs& a, const uint2* __re
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const uint32_t i = c + 32u * u + lane;
-      x[u] = i < n ? __ldg(e + i) : make_uint2(0u, 0u);
+      x[u] = i < n ? sign_ent(e + i) : make_uint2(0u, 0u);
     }
     TermInfo ti[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) ti[u] = (c + 32u * u + lane < n) ? a.info[x[u].x] : TermInfo{0.0f, -1};
+    for (int u = 0; u < 4; ++u) ti[u] = (c + 32u * u + lane < n) ? sign_info(a.info + x[u].x) : TermInfo{0.0f, -1};
     uint32_t qn = 0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {

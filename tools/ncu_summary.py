@@ -24,7 +24,7 @@ PROF = os.path.join(REPO, "profiles")
 
 # bench.py roofline keys -> kernel name fragments
 ROOF_KERNELS = {"mrc_tiles": ["mrc_tc_kernel", "tc_forms_kernel"], "sign": ["sign_kernel"], "pair_emit": ["emit_kernel"],
-                "count": ["count_warp_kernel", "group_sort_kernel", "count_large_kernel", "idf_kernel"],
+                "count": ["count_warp_kernel", "group_sort_kernel", "group_split_kernel", "count_large_kernel", "idf_kernel"],
                 "reference": ["ref_build_kernel"],
                 "simhash": ["simhash_kernel"], "hamming_tiles": ["hamming_bitmap_kernel"]}
 
@@ -75,7 +75,7 @@ def launches(path, tag):
     open(os.path.join(PROF, f"ncu_launches_{tag}.md"), "w").write("\n".join(lines) + "\n")
 
 
-STEP_KERNELS = ["count_warp_kernel", "group_sort_kernel", "count_large_kernel", "idf_kernel", "ref_build_kernel", "sign_kernel", "sign_col_kernel", "tc_forms_kernel",
+STEP_KERNELS = ["count_warp_kernel", "group_sort_kernel", "group_split_kernel", "count_large_kernel", "idf_kernel", "ref_build_kernel", "sign_kernel", "sign_col_kernel", "tc_forms_kernel",
                 "mrc_tc_kernel", "mrc_bitmap_kernel2", "scan_small_kernel", "emit_kernel"]
 
 WANT = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "dram read"),
