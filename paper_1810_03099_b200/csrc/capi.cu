@@ -559,13 +559,15 @@ void run_mrc_tiles(refsig_gpu_ctx* c, const float* STr, uint32_t ldr, uint32_t n
 // A5: union, remap and the compact table from c->ref_{start,n} and `ent`.
 void build_reference(refsig_gpu_ctx* c, const RefArgs& r, uint64_t n_entries) {
   const uint32_t V = c->vocab;
-  const uint64_t u_cap = std::min<uint64_t>(n_entries, V);  // |U| bound
+  // rows: one per reference entry (A5's canonical row of a term is its first entry's)
+  const uint64_t u_cap = std::min<uint64_t>(n_entries, static_cast<uint64_t>(V) * r.K);
   // K2 addresses R rows by 32-bit element offsets (row * Kp)
   require(u_cap * r.Kp < (1ull << 32), "reference term union too large (|U| * K >= 2^32)");
   const size_t rbytes = sizeof(float) * std::max<uint64_t>(u_cap, 1) * r.Kp;
   c->R.ensure(rbytes);
-  if (c->ref_count.ensure(3 * sizeof(uint32_t)))  // [row counter, finished CTAs, |U|]; the kernel leaves [0],[1] zero
-    ck(cudaMemsetAsync(c->ref_count.p, 0, 3 * sizeof(uint32_t), c->stream), "memset");
+  // [barrier arrivals, finished CTAs, |U|, |U| partial sums]; the kernel leaves [0], [1], [3] zero
+  if (c->ref_count.ensure(4 * sizeof(uint32_t)))
+    ck(cudaMemsetAsync(c->ref_count.p, 0, 4 * sizeof(uint32_t), c->stream), "memset");
   Phase ph(c, REFSIG_PHASE_REFERENCE);
   // info[].ref_row is -1 right after count(); a replaced reference resets it
   if (c->ref_dirty) launch_ref_reset(c->info.as<TermInfo>(), V, c->stream);

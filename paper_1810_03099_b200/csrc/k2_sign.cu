@@ -41,9 +41,6 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 __global__ void ref_reset_kernel(TermInfo* __restrict__ info, uint32_t vocab) {
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < vocab; t += gridDim.x * blockDim.x)
@@ -51,27 +48,42 @@ __global__ void ref_reset_kernel(TermInfo* __restrict__ info, uint32_t vocab) {
 }
 
 // A5 in ONE launch: CTA k per reference vector (all K CTAs are co-resident:
-// K <= 256 CTAs of 256 threads).
+// K <= 256 CTAs of 256 threads). Row numbering needs no claims: the j-th
+// entry of reference k owns row base_k + j (base_k = entries of references
+// 0..k-1), and a term's canonical row is the smallest row of any reference
+// holding it — atomicMin on info[t].ref_row as unsigned (-1 = none = max),
+// fire-and-forget, so the result does not depend on scheduling.
 //   pass 1: weights (count * idf, or explicit), the squared norm in a fixed
-//           order (thread-strided partials, block tree), and the claims:
-//           atomicCAS(info[t].ref_row, -1, -2) — the CTA that saw -1 owns
-//           term t: it takes the next compact row (warp-aggregated atomic on
-//           *counter), zeroes that R row, fences, and publishes the row;
-//   pass 2: R[row(t)*Kp + k] = w / ||w_k||, where a term claimed by another
-//           CTA waits (spins) until its owner has published the row — the
-//           owner zeroed the row before publishing, so this write lands after
-//           the zeroing.
-// The row numbering depends on claim order, the values K2 reads through it do
-// not. Needs info[].ref_row == -1 (count() leaves it so; a replaced reference
-// is reset first) and *counter == 0; *counter ends as |U|.
+//           order, the atomicMin of every entry's row, and the zeroing of the
+//           CTA's own rows;
+//   grid barrier (arrival counter; CTAs are co-resident);
+//   pass 2: R[row(t)*Kp + k] = w / ||w_k|| through the canonical row (read
+//           from L2: this CTA's L1 may hold the pre-barrier line), and the
+//           count of canonical rows (|U|).
+// Rows of terms that are not canonical stay zero and are never referenced.
+// Needs info[].ref_row == -1 (count() leaves it so; a replaced reference is
+// reset first) and counter[0,1,3] == 0, which the last CTA restores.
 constexpr int kRefIpt2 = 4;
 __global__ void __launch_bounds__(256) ref_build_kernel(RefArgs r, TermInfo* __restrict__ info,
                                                         float* __restrict__ R, uint32_t* __restrict__ counter) {
-  // counter[0]: next compact row, counter[1]: finished CTAs — both zero at launch; the last CTA
-  // stores |U| in counter[2] and zeroes [0] and [1] again (no memset node before this PDL launch)
+  // counter: [0] barrier arrivals, [1] finished CTAs, [2] |U| (output), [3] |U| accumulator
   __shared__ float red[8];
+  __shared__ uint32_t ured[8];
   const uint32_t k = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   pdl_wait();
+  uint32_t base = 0;  // entries of references 0..k-1
+  for (uint32_t q = threadIdx.x; q < k; q += 256) {
+    const uint2* eq;
+    uint32_t nq;
+    ref_range(r, q, eq, nq);
+    base += nq;
+  }
+  base = warp_sum_u32(base);
+  if (lane == 0) ured[wid] = base;
+  __syncthreads();
+  base = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) base += ured[w];
   const uint2* e;
   uint32_t n;
   ref_range(r, k, e, n);
@@ -83,51 +95,31 @@ __global__ void __launch_bounds__(256) ref_build_kernel(RefArgs r, TermInfo* __r
       const uint32_t i = p0 + j * 256 + threadIdx.x;
       x[j] = i < n ? e[i] : make_uint2(0xFFFFFFFFu, 0u);
     }
-    float w[kRefIpt2];
-#pragma unroll
-    for (int j = 0; j < kRefIpt2; ++j)
-      w[j] = x[j].x == 0xFFFFFFFFu ? 0.0f
-                                   : (r.explicit_w ? __uint_as_float(x[j].y) : static_cast<float>(x[j].y) * info[x[j].x].idf);
-#pragma unroll
-    for (int j = 0; j < kRefIpt2; ++j) sq = fmaf(w[j], w[j], sq);
-    bool own[kRefIpt2];
-#pragma unroll
-    for (int j = 0; j < kRefIpt2; ++j)
-      own[j] = x[j].x != 0xFFFFFFFFu && atomicCAS(reinterpret_cast<int*>(&info[x[j].x].ref_row), -1, -2) == -1;
-    // one counter atomic per warp for all of its claims of this pass
-    uint32_t b[kRefIpt2], tot = 0;
 #pragma unroll
     for (int j = 0; j < kRefIpt2; ++j) {
-      b[j] = __ballot_sync(0xffffffffu, own[j]);
-      tot += __popc(b[j]);
-    }
-    uint32_t base = 0;
-    if (lane == 0 && tot) base = atomicAdd(counter, tot);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    uint32_t row[kRefIpt2];
-#pragma unroll
-    for (int j = 0; j < kRefIpt2; ++j) {
-      row[j] = base + __popc(b[j] & ((1u << lane) - 1u));
-      base += __popc(b[j]);
-      if (own[j]) {
-        float4* rr = reinterpret_cast<float4*>(R + static_cast<size_t>(row[j]) * r.Kp);
-        for (uint32_t q = 0; q < r.Kp / 4; ++q) rr[q] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      }
-    }
-    if (tot) {
-      __threadfence();  // the zeroed rows are visible before any row is published
-#pragma unroll
-      for (int j = 0; j < kRefIpt2; ++j)
-        if (own[j]) st_release(&info[x[j].x].ref_row, static_cast<int>(row[j]));
+      if (x[j].x == 0xFFFFFFFFu) continue;
+      const uint32_t row = base + p0 + j * 256 + threadIdx.x;
+      atomicMin(reinterpret_cast<unsigned int*>(&info[x[j].x].ref_row), row);
+      const float w = r.explicit_w ? __uint_as_float(x[j].y) : static_cast<float>(x[j].y) * info[x[j].x].idf;
+      sq = fmaf(w, w, sq);
+      float4* rr = reinterpret_cast<float4*>(R + static_cast<size_t>(row) * r.Kp);
+      for (uint32_t q = 0; q < r.Kp / 4; ++q) rr[q] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     }
   }
   sq = warp_sum(sq);
   if (lane == 0) red[wid] = sq;
+  __threadfence();  // row minima and zeroed rows visible before the arrival
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(counter, 1u);
+    while (static_cast<uint32_t>(ld_acquire(reinterpret_cast<const int*>(counter))) < gridDim.x) __nanosleep(64);
+  }
   __syncthreads();
   float tot = 0.0f;
 #pragma unroll
   for (int w = 0; w < 8; ++w) tot += red[w];
   const float inv = tot > 0.0f ? 1.0f / sqrtf(tot) : 0.0f;
+  uint32_t canon = 0;
   for (uint32_t p0 = 0; p0 < n; p0 += 256 * kRefIpt2) {
     uint2 x[kRefIpt2];
 #pragma unroll
@@ -135,24 +127,33 @@ __global__ void __launch_bounds__(256) ref_build_kernel(RefArgs r, TermInfo* __r
       const uint32_t i = p0 + j * 256 + threadIdx.x;
       x[j] = i < n ? e[i] : make_uint2(0xFFFFFFFFu, 0u);
     }
-    int row[kRefIpt2];
+    uint32_t row[kRefIpt2];
 #pragma unroll
-    for (int j = 0; j < kRefIpt2; ++j) row[j] = x[j].x == 0xFFFFFFFFu ? 0 : ld_acquire(&info[x[j].x].ref_row);
+    for (int j = 0; j < kRefIpt2; ++j)
+      row[j] = x[j].x == 0xFFFFFFFFu ? 0u : static_cast<uint32_t>(__ldcg(&info[x[j].x].ref_row));
 #pragma unroll
     for (int j = 0; j < kRefIpt2; ++j) {
       if (x[j].x == 0xFFFFFFFFu) continue;
-      while (row[j] < 0) row[j] = ld_acquire(&info[x[j].x].ref_row);  // owner CTA publishes shortly
       const float w = r.explicit_w ? __uint_as_float(x[j].y) : static_cast<float>(x[j].y) * info[x[j].x].idf;
       R[static_cast<size_t>(row[j]) * r.Kp + k] = w * inv;
+      canon += row[j] == base + p0 + j * 256 + threadIdx.x;
     }
   }
+  canon = warp_sum_u32(canon);
+  __syncthreads();  // ured reuse
+  if (lane == 0) ured[wid] = canon;
   __syncthreads();
   if (threadIdx.x == 0) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) c += ured[w];
+    atomicAdd(counter + 3, c);
     __threadfence();
     if (atomicAdd(counter + 1, 1u) == gridDim.x - 1) {
-      counter[2] = atomicAdd(counter, 0u);
+      counter[2] = atomicAdd(counter + 3, 0u);
       counter[0] = 0;
       counter[1] = 0;
+      counter[3] = 0;
     }
   }
 }
