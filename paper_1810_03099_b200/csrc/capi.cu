@@ -202,7 +202,7 @@ struct refsig_gpu_ctx {
 
   // exact
   bool have_x = false;
-  DevBuf x, post_off, post_fill, posts, head_col, headA, head_norm, tail_df;  // K5
+  DevBuf x, post_off, posts, head_col, headA, head_norm, entpos, csc_ka, csc_kb, csc_va, csc_vb, csc_doc, csc_tmp;  // K5
   DevBuf headAT, eval_tail, eval_part;                                         // evaluation
   DevBuf cf_rep, cf;                                                           // corpus frequencies
   DevBuf records;                                                              // MRCS records
@@ -280,8 +280,9 @@ struct refsig_gpu_ctx {
             {"rowcnt", &rowcnt}, {"rowstart", &rowstart}, {"cand", &cand}, {"scan_tmp", &scan_tmp}, {"keys", &keys},
             {"emit_ctr", &emit_ctr}, {"cand16", &cand16}, {"text", &text}, {"text_off", &text_off},
             {"text_cnt", &text_cnt}, {"fp", &fp}, {"term_hash", &term_hash}, {"x", &x}, {"post_off", &post_off},
-            {"post_fill", &post_fill}, {"posts", &posts}, {"head_col", &head_col}, {"headA", &headA},
-            {"head_norm", &head_norm}, {"tail_df", &tail_df}, {"headAT", &headAT}, {"eval_tail", &eval_tail},
+            {"posts", &posts}, {"head_col", &head_col}, {"headA", &headA},
+            {"head_norm", &head_norm}, {"entpos", &entpos}, {"csc_ka", &csc_ka}, {"csc_kb", &csc_kb},
+            {"csc_va", &csc_va}, {"csc_vb", &csc_vb}, {"csc_doc", &csc_doc}, {"csc_tmp", &csc_tmp}, {"headAT", &headAT}, {"eval_tail", &eval_tail},
             {"eval_part", &eval_part}, {"cf_rep", &cf_rep}, {"cf", &cf}, {"records", &records},
             {"tc_forms", &tc_forms}, {"fetch_rowptr0", &fetch_rowptr[0]}, {"fetch_rowptr1", &fetch_rowptr[1]},
             {"fetch_cols0", &fetch_cols[0]}, {"fetch_cols1", &fetch_cols[1]}};
@@ -759,20 +760,19 @@ uint32_t prepare_exact(refsig_gpu_ctx* ctx) {
   const uint32_t N = ctx->n_docs, V = ctx->vocab;
   require(ctx->n_tokens < (1ull << 32), "exact verifier: more than 2^32 postings");  // 32-bit posting offsets
   ensure_unit_weights(ctx);
-  // head terms: the kExactHead highest df (ties by id), from the device df
+  // head terms: the kExactHead highest df (ties by id), selected on the device
   const uint32_t H = std::min<uint32_t>(kExactHead, (V + 3) & ~3u);
-  std::vector<uint32_t> hdf(V);
-  ck(cudaMemcpyAsync(hdf.data(), ctx->df.p, 4ull * V, cudaMemcpyDeviceToHost, ctx->stream), "D2H df");
-  sync(ctx);
-  std::vector<uint32_t> ids(V);
-  for (uint32_t t = 0; t < V; ++t) ids[t] = t;
-  const uint32_t nh = std::min(H, V);
-  std::partial_sort(ids.begin(), ids.begin() + nh, ids.end(),
-                    [&](uint32_t a, uint32_t b) { return hdf[a] != hdf[b] ? hdf[a] > hdf[b] : a < b; });
-  std::vector<int32_t> head_col(V, -1);
-  for (uint32_t k = 0; k < nh; ++k) head_col[ids[k]] = static_cast<int32_t>(k);
+  const uint64_t T = std::max<uint64_t>(ctx->n_tokens, 1);
+  const uint64_t W = std::max<uint64_t>(T, V);  // sort scratch: slots or terms
+  ctx->csc_ka.ensure(4ull * W);
+  ctx->csc_kb.ensure(4ull * W);
+  ctx->csc_va.ensure(4ull * W);
+  ctx->csc_vb.ensure(4ull * W);
+  ctx->csc_tmp.ensure(std::max(csc_sort_temp_bytes(ctx->n_tokens, V), head_select_temp_bytes(V)));
   ctx->head_col.ensure(4ull * V);
-  upload(ctx, ctx->head_col.p, head_col.data(), 4ull * V);
+  launch_head_select(ctx->df.as<uint32_t>(), V, H, ctx->csc_ka.as<uint32_t>(), ctx->csc_kb.as<uint32_t>(),
+                     ctx->csc_va.as<uint32_t>(), ctx->csc_vb.as<uint32_t>(), ctx->csc_tmp.p, ctx->csc_tmp.cap,
+                     ctx->head_col.as<int32_t>(), ctx->stream);
   // dense head rows + their norms
   ctx->headA.ensure(sizeof(float) * static_cast<size_t>(N) * H);
   ctx->head_norm.ensure(sizeof(float) * N);
@@ -780,20 +780,18 @@ uint32_t prepare_exact(refsig_gpu_ctx* ctx) {
   launch_head_rows(ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), ctx->x.as<float>(),
                    ctx->head_col.as<int32_t>(), N, H, ctx->headA.as<float>(), ctx->head_norm.as<float>(),
                    ctx->stream);
-  // tail postings: offsets = exclusive scan of the tail df, then an atomic fill
+  // doc-sorted postings of every term: offsets = exclusive scan of df, lists by a stable radix sort by term
   ctx->post_off.ensure(8ull * (V + 1));
-  ctx->post_fill.ensure(8ull * (V + 1));
-  ctx->tail_df.ensure(4ull * V);
-  ctx->posts.ensure(sizeof(uint2) * std::max<uint64_t>(ctx->n_tokens, 1));
+  ctx->posts.ensure(sizeof(uint2) * T);
+  ctx->entpos.ensure(4ull * T);
+  ctx->csc_doc.ensure(4ull * T);
   ctx->scan_tmp.ensure(scan_tmp_bytes(std::max(N, V)));
-  launch_tail_df(ctx->df.as<uint32_t>(), ctx->head_col.as<int32_t>(), V, ctx->tail_df.as<uint32_t>(), ctx->stream);
-  launch_exclusive_scan_u32_to_u64(ctx->tail_df.as<uint32_t>(), ctx->post_off.as<uint64_t>(), V, ctx->scan_tmp.p,
+  launch_exclusive_scan_u32_to_u64(ctx->df.as<uint32_t>(), ctx->post_off.as<uint64_t>(), V, ctx->scan_tmp.p,
                                    ctx->stream);
-  ck(cudaMemcpyAsync(ctx->post_fill.p, ctx->post_off.p, 8ull * (V + 1), cudaMemcpyDeviceToDevice, ctx->stream),
-     "copy");
-  launch_postings_fill(ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(),
-                       ctx->x.as<float>(), ctx->head_col.as<int32_t>(), N, ctx->post_fill.as<uint64_t>(),
-                       ctx->posts.as<uint2>(), ctx->stream);
+  build_csc_postings(ctx->ent.as<uint2>(), ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(), N, V, ctx->n_tokens,
+                     ctx->x.as<float>(), ctx->csc_ka.as<uint32_t>(), ctx->csc_kb.as<uint32_t>(),
+                     ctx->csc_va.as<uint32_t>(), ctx->csc_vb.as<uint32_t>(), ctx->csc_doc.as<uint32_t>(),
+                     ctx->csc_tmp.p, ctx->csc_tmp.cap, ctx->posts.as<uint2>(), ctx->entpos.as<uint32_t>(), ctx->stream);
   return H;
 }
 
@@ -1451,7 +1449,7 @@ int refsig_gpu_exact_pairs(refsig_gpu_ctx* ctx, float tau_cos, uint64_t* out_pai
       prepare_bitmap(ctx, g, true);
       ExactArgs a{ctx->ent.as<uint2>(),        ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(),
                   ctx->x.as<float>(),          ctx->head_col.as<int32_t>(), ctx->post_off.as<uint64_t>(),
-                  ctx->posts.as<uint2>(),      ctx->headA.as<float>(),      ctx->head_norm.as<float>(),
+                  ctx->posts.as<uint2>(),      ctx->entpos.as<uint32_t>(),  ctx->headA.as<float>(),      ctx->head_norm.as<float>(),
                   H,                           N,                           std::min<uint32_t>(N, kExactPanel),
                   tau_cos,                     ctx->bitmap.as<uint32_t>(),  g.words_per_row,
                   ctx->rowcnt.as<uint32_t>(),  nullptr,                     0};
@@ -1503,7 +1501,7 @@ int refsig_gpu_evaluate(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_hi, r
         Phase ph(ctx, REFSIG_PHASE_PAIR_TILES);
         ExactArgs a{ctx->ent.as<uint2>(),        ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(),
                     ctx->x.as<float>(),          ctx->head_col.as<int32_t>(), ctx->post_off.as<uint64_t>(),
-                    ctx->posts.as<uint2>(),      ctx->headA.as<float>(),      ctx->head_norm.as<float>(),
+                    ctx->posts.as<uint2>(),      ctx->entpos.as<uint32_t>(),  ctx->headA.as<float>(),      ctx->head_norm.as<float>(),
                     H,                           N,                           std::min<uint32_t>(N, kExactPanel),
                     0.0f,                        nullptr,                     0,
                     nullptr,                     ctx->eval_tail.as<uint32_t>(), ld};

@@ -4,22 +4,27 @@
 // vectors, 0 for an empty vector, clamped to 1. Here over the weighted
 // (TF or TF-IDF) corpus vectors, x = w/||w||, in fp32.
 //
-// v2: head / tail split with exact bounds. The H terms of highest df (the
-// Zipf head: at configs[1] the top 64 terms carry 77% of the sum of
-// df*(df-1)/2 multiply-adds but, being frequent, little TF-IDF weight) are
-// kept as dense rows A[d][H] with their norm hn[d]; the other terms (tail) go
-// to postings lists. One CTA per row i (column panels of up to kExactPanel
-// docs in shared memory):
-//   1. tail: for each tail term of doc i, every posting j > i adds
-//      round(x_i * x_j * 2^30) to acc[j] with a shared-memory integer atomic —
-//      fixed-point sums are exact, so the result is independent of the order
-//      the atomics land in (no barrier per term);
+// Head / tail split with exact bounds. The H terms of highest df (the Zipf
+// head: at configs[1] the top 64 terms carry 77% of the sum of df*(df-1)/2
+// multiply-adds but, being frequent, little TF-IDF weight; selected on the
+// device by a stable descending sort of df) are kept as dense rows A[d][H]
+// with their norm hn[d]; every term's postings are doc-sorted (a stable radix
+// sort of the CSR slots by term id) and entpos gives each entry's position in
+// its term's list. One CTA (32 warps) per row i (column panels of up to
+// kExactPanel docs in shared memory):
+//   1. tail: for each tail term of doc i, exactly the postings after doc i
+//      (j > i) add round(x_i * x_j * 2^30) to acc[j] with a shared-memory
+//      integer atomic — fixed-point sums are exact, so the result does not
+//      depend on the order the atomics land in. The kept lists are walked as
+//      one flat index space split evenly over the warps (32 postings per warp
+//      step, two steps at once inside one term), so lanes stay busy whatever
+//      the list lengths;
 //   2. scan j > i: tail = acc[j] * 2^-30; since head_ij <= hn_i * hn_j
 //      (Cauchy-Schwarz), only pairs with tail + hn_i*hn_j >= tau - 1e-5 can
 //      match; for those the head dot A_i . A_j (H fused multiply-adds in a
 //      fixed order) is added and cos = min(tail + head, 1) >= tau sets the
 //      pair's bit (shared pair bitmap, common emitter).
-// Deterministic; the work is the tail's sum of df^2 (23% of the total at
+// Deterministic; the work is the tail's sum of df(df-1)/2 (424 M postings at
 // configs[1]) plus a dense scan of the triangle. Fixed-point error <= 2^-31
 // per product (< 1e-7 per pair for < 200 shared tail terms), far inside the
 // 1e-5 border band of the parity tests.
@@ -28,6 +33,8 @@
 // sorted ids, warp-tree sum.
 
 #include <algorithm>
+
+#include <cub/device/device_radix_sort.cuh>
 
 #include "kernels.cuh"
 
@@ -48,31 +55,6 @@ __global__ void unit_weights_kernel(const uint2* __restrict__ ent, const uint64_
       x[b + i] = static_cast<float>(e.y) * info[e.x].idf * inv;
     }
   }
-}
-
-__global__ void postings_fill_kernel(const uint2* __restrict__ ent, const uint64_t* __restrict__ doc_off,
-                                     const uint32_t* __restrict__ nnz, const float* __restrict__ x,
-                                     const int32_t* __restrict__ head_col, uint32_t n_docs,
-                                     uint64_t* __restrict__ fill, uint2* __restrict__ posts) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t d = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); d < n_docs; d += nw) {
-    const uint64_t b = doc_off[d];
-    const uint32_t n = nnz[d];
-    for (uint32_t i = lane; i < n; i += 32) {
-      const uint32_t t = ent[b + i].x;
-      if (head_col && head_col[t] >= 0) continue;  // head terms live in the dense rows
-      const uint64_t q = atomicAdd(reinterpret_cast<unsigned long long*>(fill + t), 1ull);
-      posts[q] = make_uint2(d, __float_as_uint(x[b + i]));
-    }
-  }
-}
-
-// tdf[t] = df[t] for tail terms, 0 for head terms.
-__global__ void tail_df_kernel(const uint32_t* __restrict__ df, const int32_t* __restrict__ head_col,
-                               uint32_t vocab, uint32_t* __restrict__ tdf) {
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < vocab; t += gridDim.x * blockDim.x)
-    tdf[t] = head_col[t] >= 0 ? 0u : df[t];
 }
 
 // Dense head rows A[d][H] (zeroed by the caller) and hn[d] = ||head part||.
@@ -99,15 +81,58 @@ __global__ void head_rows_kernel(const uint2* __restrict__ ent, const uint64_t* 
 }
 
 constexpr float kFix = 1073741824.0f;  // 2^30
+constexpr uint32_t kTailBatch = 1024;    // doc-i terms per batch (one per thread)
 
-__global__ void __launch_bounds__(512) exact_tail_kernel(ExactArgs a, uint32_t row_lo) {
-  extern __shared__ uint32_t acc[];  // [panel] fixed-point tail sums, then H floats of A_i
-  __shared__ uint32_t red[16];
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint2 lds_u2(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint2 ldg_u2(const uint2* p) {
+  uint2 v;
+  asm("ld.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void reds_add(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// Block-wide exclusive scan of v over the kTailBatch threads (warp scans + warp totals).
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* part, uint32_t& total) {
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t inc = warp_inclusive_scan(v, static_cast<int>(lane));
+  if (lane == 31) part[wid] = inc;
+  __syncthreads();
+  const uint32_t x = part[lane];  // kTailBatch / 32 == 32 warp totals
+  const uint32_t xi = warp_inclusive_scan(x, static_cast<int>(lane));
+  const uint32_t off = __shfl_sync(0xffffffffu, xi - x, wid);
+  total = __shfl_sync(0xffffffffu, xi, 31);
+  __syncthreads();  // part is reused by the next scan
+  return off + inc - v;
+}
+
+// Row i per CTA (32 warps). Tail terms of doc i in batches of 1024: each keeps
+// the part of its doc-sorted posting list after doc i — [entpos(i, t) + 1,
+// end of t) — and the kept lists are walked as ONE flat index space split
+// evenly over the warps: 32 consecutive postings per warp step, lane l's term
+// found from the starts inside the 32-wide window (one OR-reduction +
+// popcount), so every lane does a posting per step whatever the list lengths.
+__global__ void __launch_bounds__(kTailBatch) exact_tail_kernel(ExactArgs a, uint32_t row_lo) {
+  extern __shared__ uint4 acc4[];  // [panel/4] fixed-point tail sums, then H floats of A_i
+  uint32_t* acc = reinterpret_cast<uint32_t*>(acc4);
+  __shared__ uint32_t red[32];
+  __shared__ uint32_t s_start[kTailBatch];  // flat start of kept term k
+  __shared__ uint2 s_rec[kTailBatch];       // (first posting after doc i, x_i bits) of kept term k
   const uint32_t i = row_lo + blockIdx.x;
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const uint64_t b = a.doc_off[i];
   const uint32_t n = a.nnz[i];
-  float* ai = reinterpret_cast<float*>(acc + a.panel);
+  float* ai = reinterpret_cast<float*>(acc + (a.panel + 3) / 4 * 4);
   for (uint32_t k = threadIdx.x; k < a.H; k += blockDim.x) ai[k] = a.A[static_cast<size_t>(i) * a.H + k];
   const float hni = a.hn[i];
   uint32_t cnt = 0;
@@ -115,20 +140,85 @@ __global__ void __launch_bounds__(512) exact_tail_kernel(ExactArgs a, uint32_t r
   for (uint32_t c0 = (i + 1) / a.panel * a.panel; c0 < a.n_docs; c0 += a.panel) {
     const uint32_t c1 = min(a.n_docs, c0 + a.panel);
     const uint32_t jlo = max(c0, i + 1);
-    for (uint32_t k = threadIdx.x; k < c1 - c0; k += blockDim.x) acc[k] = 0u;
-    __syncthreads();
-    // 1. tail terms of doc i: warp per term, lanes over its postings
-    for (uint32_t p = wid; p < n; p += nwarp) {
-      const uint32_t t = a.ent[b + p].x;
-      if (a.head_col[t] >= 0) continue;
-      const float xi = a.x[b + p];
-      const uint64_t q1 = a.post_off[t + 1];
-      for (uint64_t q = a.post_off[t] + lane; q < q1; q += 32) {
-        const uint2 pj = a.posts[q];
-        if (pj.x >= jlo && pj.x < c1) atomicAdd(&acc[pj.x - c0], __float2uint_rn(xi * __uint_as_float(pj.y) * kFix));
+    for (uint32_t k = threadIdx.x; k < (c1 - c0 + 3) / 4; k += blockDim.x) acc4[k] = make_uint4(0u, 0u, 0u, 0u);
+    // 1. tail products x_i * x_j of every shared tail term, j > i, into acc[j - c0]
+    for (uint32_t p0 = 0; p0 < n; p0 += kTailBatch) {
+      const uint32_t p = p0 + threadIdx.x;
+      uint32_t len = 0, q = 0;
+      float xi = 0.0f;
+      if (p < n) {
+        const uint32_t t = a.ent[b + p].x;
+        if (a.head_col[t] < 0) {
+          q = a.entpos[b + p] + 1u;
+          len = static_cast<uint32_t>(a.post_off[t + 1]) - q;
+          xi = a.x[b + p];
+        }
       }
+      uint32_t n_kept, M;
+      const uint32_t k = block_excl_scan(len ? 1u : 0u, red, n_kept);
+      const uint32_t f = block_excl_scan(len, red, M);
+      if (len) {
+        s_start[k] = f;
+        s_rec[k] = make_uint2(q - f, __float_as_uint(xi));  // posting of flat index idx: q - f + idx
+      }
+      __syncthreads();
+      const uint32_t per = (M + nwarp - 1) / nwarp;
+      const uint32_t f0 = min(M, wid * per), f1 = min(M, f0 + per);
+      if (f0 < f1) {
+        // cur = last kept term starting before f0 (-1 if none)
+        int lo = 0, hi = static_cast<int>(n_kept);
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (s_start[mid] < f0) lo = mid + 1; else hi = mid;
+        }
+        int cur = lo - 1;
+        // shared-window addresses computed once (the compiler otherwise rebuilds them every step)
+        uint32_t start_a = static_cast<uint32_t>(__cvta_generic_to_shared(s_start));
+        uint32_t rec_a = static_cast<uint32_t>(__cvta_generic_to_shared(s_rec));
+        uint32_t acc_a = static_cast<uint32_t>(__cvta_generic_to_shared(acc));
+        const uint2* posts = a.posts;
+        asm volatile("" : "+r"(start_a), "+r"(rec_a), "+r"(acc_a), "+l"(posts));  // opaque: kept in registers
+        const uint32_t le = (2u << lane) - 1u, span = c1 - c0;
+        const int nk = static_cast<int>(n_kept);
+        // the term containing the window start and where the next one starts
+        uint2 rec = cur >= 0 ? lds_u2(rec_a + 8u * cur) : make_uint2(0u, 0u);
+        uint32_t next = cur + 1 < nk ? lds_u32(start_a + 4u * (cur + 1)) : 0xFFFFFFFFu;
+        uint32_t base = f0;
+        while (base < f1) {
+          if (next >= base + 64u && base + 32u < f1) {  // two whole windows inside the current term
+            const uint32_t idx = base + lane;
+            const uint2 p0 = ldg_u2(posts + rec.x + idx);
+            const bool in2 = idx + 32u < f1;
+            const uint2 p1 = in2 ? ldg_u2(posts + rec.x + idx + 32u) : make_uint2(0xFFFFFFFFu, 0u);
+            const float xr = __uint_as_float(rec.y) * kFix;
+            const uint32_t j0 = p0.x - c0, j1 = p1.x - c0;
+            if (j0 < span) reds_add(acc_a + 4u * j0, __float2uint_rn(xr * __uint_as_float(p0.y)));
+            if (j1 < span) reds_add(acc_a + 4u * j1, __float2uint_rn(xr * __uint_as_float(p1.y)));
+            base += 64u;
+            continue;
+          }
+          const uint32_t idx = base + lane;
+          uint2 r = rec;
+          if (next < base + 32u) {  // a term starts inside the window: per-lane terms
+            const int m = cur + 1 + static_cast<int>(lane);
+            const uint32_t sm = m < nk ? lds_u32(start_a + 4u * m) : 0xFFFFFFFFu;
+            const uint32_t bits = __reduce_or_sync(0xffffffffu, sm < base + 32u ? 1u << (sm - base) : 0u);
+            const int term = cur + __popc(bits & le);
+            if (term != cur) r = lds_u2(rec_a + 8u * term);
+            cur += __popc(bits);
+            rec = lds_u2(rec_a + 8u * cur);
+            next = cur + 1 < nk ? lds_u32(start_a + 4u * (cur + 1)) : 0xFFFFFFFFu;
+          }
+          if (idx < f1) {
+            const uint2 pj = ldg_u2(posts + r.x + idx);
+            const uint32_t jj = pj.x - c0;
+            if (jj < span) reds_add(acc_a + 4u * jj, __float2uint_rn(__uint_as_float(r.y) * kFix * __uint_as_float(pj.y)));
+          }
+          base += 32u;
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
     if (a.tail_out) {  // evaluation mode: hand the exact tail sums to the tile pass
       uint32_t* dst = a.tail_out + static_cast<size_t>(blockIdx.x) * a.tail_ld;
       for (uint32_t j = jlo + threadIdx.x; j < c1; j += blockDim.x) dst[j] = acc[j - c0];
@@ -164,6 +254,41 @@ __global__ void __launch_bounds__(512) exact_tail_kernel(ExactArgs a, uint32_t r
     uint32_t s = 0;
     for (uint32_t w = 0; w < nwarp; ++w) s += red[w];
     a.rowcnt[i] = s;
+  }
+}
+
+// Doc-sorted postings (CSC) of every term: a STABLE radix sort of the padded
+// CSR slots — already in document order — by term id alone (padding slots get
+// the key V, after every term), so each term's list comes out in document
+// order; posting q = (doc of the slot, x[slot]) and entpos[slot] = q — the
+// position of entry (d, t) inside t's list, so row i's walk starts right
+// after itself.
+__global__ void csc_keys_kernel(const uint2* __restrict__ ent, const uint64_t* __restrict__ doc_off,
+                                const uint32_t* __restrict__ nnz, uint32_t n_docs, uint32_t vocab,
+                                uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                uint32_t* __restrict__ slot_doc) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t d = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); d < n_docs; d += nw) {
+    const uint64_t b = doc_off[d], e = doc_off[d + 1];
+    const uint32_t n = nnz[d];
+    for (uint64_t s = b + lane; s < e; s += 32) {
+      keys[s] = s - b < n ? ent[s].x : vocab;
+      vals[s] = static_cast<uint32_t>(s);
+      slot_doc[s] = d;
+    }
+  }
+}
+
+__global__ void csc_fill_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t n_slots,
+                                uint32_t vocab, const uint32_t* __restrict__ slot_doc, const float* __restrict__ x,
+                                uint2* __restrict__ posts, uint32_t* __restrict__ entpos) {
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < n_slots;
+       q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (keys[q] >= vocab) break;  // padding sorts last
+    const uint32_t s = vals[q];
+    posts[q] = make_uint2(slot_doc[s], __float_as_uint(x[s]));
+    entpos[s] = static_cast<uint32_t>(q);
   }
 }
 
@@ -356,17 +481,68 @@ void launch_unit_weights(const uint2* ent, const uint64_t* doc_off, const uint32
   note_launch();
 }
 
-void launch_postings_fill(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const float* x,
-                          const int32_t* head_col, uint32_t n_docs, uint64_t* fill, uint2* posts, cudaStream_t s) {
-  if (!n_docs) return;
-  unsigned g = static_cast<unsigned>(std::min<uint64_t>(ceil_div(n_docs, 8), sm_count() * 16ull));
-  postings_fill_kernel<<<g, 256, 0, s>>>(ent, doc_off, nnz, x, head_col, n_docs, fill, posts);
+static int bit_length(uint64_t v) { return v ? 64 - __builtin_clzll(v) : 1; }
+
+size_t csc_sort_temp_bytes(uint64_t n_slots, uint32_t vocab) {
+  size_t bytes = 0;
+  cub::DoubleBuffer<uint32_t> k(nullptr, nullptr);
+  cub::DoubleBuffer<uint32_t> v(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, k, v, static_cast<int64_t>(n_slots), 0, bit_length(vocab));
+  return bytes;
+}
+
+void build_csc_postings(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, uint32_t n_docs,
+                        uint32_t vocab, uint64_t n_slots, const float* x, uint32_t* keys_a, uint32_t* keys_b,
+                        uint32_t* vals_a, uint32_t* vals_b, uint32_t* slot_doc, void* tmp, size_t tmp_bytes,
+                        uint2* posts, uint32_t* entpos, cudaStream_t s) {
+  if (!n_slots) return;
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>(ceil_div(n_docs, 8), sm_count() * 16ull));
+  csc_keys_kernel<<<g, 256, 0, s>>>(ent, doc_off, nnz, n_docs, vocab, keys_a, vals_a, slot_doc);
+  note_launch();
+  cub::DoubleBuffer<uint32_t> k(keys_a, keys_b);
+  cub::DoubleBuffer<uint32_t> v(vals_a, vals_b);
+  size_t bytes = tmp_bytes;
+  cub::DeviceRadixSort::SortPairs(tmp, bytes, k, v, static_cast<int64_t>(n_slots), 0, bit_length(vocab), s);  // stable
+  note_launch();
+  const unsigned g2 = static_cast<unsigned>(std::min<uint64_t>(ceil_div(n_slots, 256), sm_count() * 8ull));
+  csc_fill_kernel<<<g2, 256, 0, s>>>(k.Current(), v.Current(), n_slots, vocab, slot_doc, x, posts, entpos);
   note_launch();
 }
 
-void launch_tail_df(const uint32_t* df, const int32_t* head_col, uint32_t vocab, uint32_t* tdf, cudaStream_t s) {
-  unsigned g = static_cast<unsigned>(std::min<uint64_t>(ceil_div(vocab, 256), sm_count() * 8ull));
-  tail_df_kernel<<<g, 256, 0, s>>>(df, head_col, vocab, tdf);
+// Head terms on the device: a stable descending radix sort of (df, id) —
+// equal df keep ascending ids — and head_col[id_k] = k for the first H.
+__global__ void head_keys_kernel(const uint32_t* __restrict__ df, uint32_t vocab, uint32_t* __restrict__ keys,
+                                 uint32_t* __restrict__ ids, int32_t* __restrict__ head_col) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < vocab; t += gridDim.x * blockDim.x) {
+    keys[t] = df[t];
+    ids[t] = t;
+    head_col[t] = -1;
+  }
+}
+__global__ void head_col_kernel(const uint32_t* __restrict__ ids, uint32_t H, int32_t* __restrict__ head_col) {
+  for (uint32_t k = threadIdx.x; k < H; k += blockDim.x) head_col[ids[k]] = static_cast<int32_t>(k);
+}
+
+size_t head_select_temp_bytes(uint32_t vocab) {
+  size_t bytes = 0;
+  cub::DoubleBuffer<uint32_t> k(nullptr, nullptr);
+  cub::DoubleBuffer<uint32_t> v(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, k, v, static_cast<int64_t>(vocab));
+  return bytes;
+}
+
+void launch_head_select(const uint32_t* df, uint32_t vocab, uint32_t H, uint32_t* keys_a, uint32_t* keys_b,
+                        uint32_t* ids_a, uint32_t* ids_b, void* tmp, size_t tmp_bytes, int32_t* head_col,
+                        cudaStream_t s) {
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>(ceil_div(vocab, 256), sm_count() * 8ull));
+  head_keys_kernel<<<g, 256, 0, s>>>(df, vocab, keys_a, ids_a, head_col);
+  note_launch();
+  cub::DoubleBuffer<uint32_t> k(keys_a, keys_b);
+  cub::DoubleBuffer<uint32_t> v(ids_a, ids_b);
+  size_t bytes = tmp_bytes;
+  cub::DeviceRadixSort::SortPairsDescending(tmp, bytes, k, v, static_cast<int64_t>(vocab), 0, 32, s);  // stable
+  note_launch();
+  head_col_kernel<<<1, 256, 0, s>>>(v.Current(), std::min(H, vocab), head_col);
   note_launch();
 }
 
@@ -380,9 +556,9 @@ void launch_head_rows(const uint2* ent, const uint64_t* doc_off, const uint32_t*
 
 void launch_exact_tail(const ExactArgs& a, uint32_t row_lo, uint32_t row_hi, cudaStream_t s) {
   if (row_hi <= row_lo) return;
-  const size_t smem = sizeof(uint32_t) * (a.panel + a.H);
+  const size_t smem = sizeof(uint32_t) * ((a.panel + 3) / 4 * 4 + a.H);
   ensure_smem(exact_tail_kernel, smem);
-  exact_tail_kernel<<<row_hi - row_lo, 512, smem, s>>>(a, row_lo);
+  exact_tail_kernel<<<row_hi - row_lo, kTailBatch, smem, s>>>(a, row_lo);
   note_launch();
 }
 

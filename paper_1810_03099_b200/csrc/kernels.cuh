@@ -193,8 +193,9 @@ struct ExactArgs {
   const uint32_t* nnz;
   const float* x;            // unit weights aligned with ent (padded CSR)
   const int32_t* head_col;   // [vocab] column in A of a head term, -1 for tail terms
-  const uint64_t* post_off;  // [vocab+1] tail postings offsets (exclusive scan of tail df)
-  const uint2* posts;        // (doc, x bits) per tail posting
+  const uint64_t* post_off;  // [vocab+1] postings offsets (exclusive scan of df)
+  const uint2* posts;        // (doc, x bits) per posting, each term's list sorted by doc
+  const uint32_t* entpos;    // [padded CSR slot] position of entry (d, t) in t's postings
   const float* A;            // [n_docs][H] dense head rows
   const float* hn;           // [n_docs] norm of the head part
   uint32_t H;                // multiple of 4
@@ -210,10 +211,18 @@ struct ExactArgs {
 };
 void launch_unit_weights(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const TermInfo* info,
                          const float* inv_norm, uint32_t n_docs, float* x, cudaStream_t s);
-// Tail postings (head_col NULL: all terms).
-void launch_postings_fill(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const float* x,
-                          const int32_t* head_col, uint32_t n_docs, uint64_t* fill, uint2* posts, cudaStream_t s);
-void launch_tail_df(const uint32_t* df, const int32_t* head_col, uint32_t vocab, uint32_t* tdf, cudaStream_t s);
+// The H highest-df terms (ties: lower id first) -> head_col[t] = rank or -1.
+size_t head_select_temp_bytes(uint32_t vocab);
+void launch_head_select(const uint32_t* df, uint32_t vocab, uint32_t H, uint32_t* keys_a, uint32_t* keys_b,
+                        uint32_t* ids_a, uint32_t* ids_b, void* tmp, size_t tmp_bytes, int32_t* head_col,
+                        cudaStream_t s);
+// Doc-sorted postings of every term (stable radix sort of the padded CSR slots
+// by term id); keys/vals/slot_doc hold n_slots words, tmp is csc_sort_temp_bytes().
+size_t csc_sort_temp_bytes(uint64_t n_slots, uint32_t vocab);
+void build_csc_postings(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, uint32_t n_docs,
+                        uint32_t vocab, uint64_t n_slots, const float* x, uint32_t* keys_a, uint32_t* keys_b,
+                        uint32_t* vals_a, uint32_t* vals_b, uint32_t* slot_doc, void* tmp, size_t tmp_bytes,
+                        uint2* posts, uint32_t* entpos, cudaStream_t s);
 void launch_head_rows(const uint2* ent, const uint64_t* doc_off, const uint32_t* nnz, const float* x,
                       const int32_t* head_col, uint32_t n_docs, uint32_t H, float* A, float* hn, cudaStream_t s);
 // Rows [row_lo, row_hi): tail accumulation, bound, head dot, threshold into the bitmap.
