@@ -133,6 +133,20 @@ struct DevBuf {
 
 }  // namespace
 
+constexpr int kPlanListCount = 10;  // refsig_gpu_ctx::kPlanLists
+// Host side of a work plan (the K1/K2/K4a document lists) and where it sits in
+// its pinned staging buffer: doc_off (u64), the u32 lists, then the u64
+// scratch offsets of documents > 8192 tokens.
+struct PlanInfo {
+  uint32_t n_docs = 0, vocab = 0;
+  uint64_t n_tokens = 0;
+  uint32_t plan_off[kPlanListCount] = {}, plan_n[kPlanListCount] = {};
+  uint32_t n_sign_long = 0, n_sign_half = 0;
+  uint32_t n_loff = 0;
+  uint64_t scratch = 0;  // words of K1 long-document scratch
+  size_t off_bytes = 0, list_bytes = 0, loff_at = 0, bytes = 0;
+};
+
 struct refsig_gpu_ctx {
   int device = 0;
   cudaStream_t own_stream = nullptr;
@@ -142,7 +156,8 @@ struct refsig_gpu_ctx {
   cudaStream_t side[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
   std::string err;
-  uint64_t* h_pin = nullptr;  // pinned scratch for small D2H reads
+  uint64_t* h_pin = nullptr;  // mapped pinned scratch for small D2H reads (written by kernels)
+  uint32_t* d_pin = nullptr;  // its device address
 
   // corpus
   bool loaded = false;
@@ -159,6 +174,7 @@ struct refsig_gpu_ctx {
   cudaEvent_t plan_done = nullptr;  // h_plan consumed by its copy
   enum { kPlanTiny, kPlanW4, kPlanW8, kPlanW16, kPlanG0, kPlanG1, kPlanG2, kPlanG3, kPlanLong, kPlanOrder, kPlanLists };
   uint32_t plan_off[kPlanLists] = {}, plan_n[kPlanLists] = {};
+  static_assert(kPlanLists == kPlanListCount, "PlanInfo list count");
   const uint32_t* plan_list(int k) const { return plan.as<uint32_t>() + plan_off[k]; }
   DevBuf long_off, long_scratch;
   uint32_t n_sign_long = 0;  // order[0, n_sign_long): > kSignLongTokens tokens, one CTA each in K2/K4a
@@ -210,12 +226,19 @@ struct refsig_gpu_ctx {
 
   // staged next corpus (refsig_gpu_stage_corpus / swap_corpus): tokens copied on
   // copy_stream into `tokens_next` while the current batch computes
-  DevBuf tokens_next;
+  // and the staged batch's work plan (built on the host at stage time, copied
+  // on copy_stream too: no small copies left for the compute stream at swap)
+  DevBuf tokens_next, doc_off_next, plan_next, long_off_next;
+  uint32_t* h_plan_next[2] = {nullptr, nullptr};  // alternate: the last stage's copy may still run
+  size_t h_plan_next_cap[2] = {0, 0};
+  cudaEvent_t ev_plan_next[2] = {nullptr, nullptr};  // h_plan_next[k] consumed
+  bool plan_next_recorded[2] = {false, false};
+  int plan_slot = 0;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_staged = nullptr, ev_next_free = nullptr;
   bool staged = false, next_free_recorded = false;
   std::vector<uint64_t> staged_off;
-  uint32_t staged_docs = 0, staged_vocab = 0;
+  PlanInfo staged_pi;
 
   // asynchronous result fetch (refsig_gpu_get_pairs_csr16_async): two slots of
   // device staging (rebased rowptr, 16-bit columns) copied to the host on
@@ -273,6 +296,8 @@ struct refsig_gpu_ctx {
   // (name, buffer) of every device buffer, for refsig_gpu_debug_check
   std::vector<std::pair<const char*, const DevBuf*>> buffers() const {
     return {{"tokens", &tokens}, {"doc_off", &doc_off}, {"plan", &plan}, {"long_off", &long_off},
+            {"tokens_next", &tokens_next}, {"doc_off_next", &doc_off_next}, {"plan_next", &plan_next},
+            {"long_off_next", &long_off_next},
             {"long_scratch", &long_scratch}, {"ent", &ent}, {"nnz", &nnz}, {"df", &df}, {"df_rep", &df_rep},
             {"info", &info}, {"flags", &flags}, {"rowptr", &rowptr}, {"c_ids", &c_ids}, {"c_counts", &c_counts},
             {"inv_norm", &inv_norm}, {"ref_docs", &ref_docs}, {"ref_start", &ref_start}, {"ref_n", &ref_n},
@@ -296,6 +321,10 @@ struct refsig_gpu_ctx {
     if (h_stage) cudaFreeHost(h_stage);
     if (stage_done) cudaEventDestroy(stage_done);
     if (h_plan) cudaFreeHost(h_plan);
+    for (int k = 0; k < 2; ++k) {
+      if (h_plan_next[k]) cudaFreeHost(h_plan_next[k]);
+      if (ev_plan_next[k]) cudaEventDestroy(ev_plan_next[k]);
+    }
     if (plan_done) cudaEventDestroy(plan_done);
     if (step_exec) cudaGraphExecDestroy(step_exec);
     if (ev_staged) cudaEventDestroy(ev_staged);
@@ -328,7 +357,7 @@ int guard(refsig_gpu_ctx* ctx, F&& f) {
 // Synchronise the stream and surface errors of enqueued work (CUDA faults,
 // token ids >= vocab flagged by K1).
 void sync(refsig_gpu_ctx* c) {
-  if (c->flags.p) ck(cudaMemcpyAsync(c->h_pin + 7, c->flags.p, 4, cudaMemcpyDeviceToHost, c->stream), "D2H flags");
+  if (c->flags.p) launch_words_to_host(c->flags.as<uint32_t>(), 1, c->d_pin + 14, c->stream);  // -> h_pin[7]
   ck(cudaStreamSynchronize(c->stream), "kernel execution");
   ck(cudaGetLastError(), "kernel launch");
   if (c->flags.p) {
@@ -452,7 +481,8 @@ void enqueue_emit(refsig_gpu_ctx* c, const PairGrid& g) {
                       c->cand.as<uint32_t>(), c->cand.cap / sizeof(uint32_t), c->emit_ctr.as<uint32_t>(), c->stream);
     launched("emit");
   }
-  ck(cudaMemcpyAsync(c->h_pin, c->rowstart.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, c->stream), "D2H count");
+  launch_words_to_host(reinterpret_cast<const uint32_t*>(c->rowstart.as<uint64_t>() + n), 2, c->d_pin,
+                       c->stream);  // -> h_pin[0]
   c->emit_pending = true;
   c->have_pairs = false;
   c->keys_valid = false;
@@ -610,37 +640,30 @@ struct HostProf {  // REFSIG_HOST_PROF=1: host time of load_common's sections (s
   }
 };
 
-void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, uint32_t vocab) {
-  HostProf hp{"load_common"};
+static_assert(kMaxRefs <= kParamWords, "reference ids travel as kernel parameters");
+
+void validate_doc_off(const uint64_t* doc_off, uint32_t n_docs, uint32_t vocab) {
   require(doc_off != nullptr, "doc_off is NULL");
   require(n_docs >= 1, "empty corpus");
   require(vocab >= 1 && vocab < 0x7fffffffu, "vocab out of range");
   require(doc_off[0] == 0, "doc_off[0] must be 0");
+}
+
+// Validate doc_off and build the plan into the pinned buffer *h (grown as
+// needed; the caller guarantees no copy still reads it).
+void plan_build(const uint64_t* doc_off, uint32_t n_docs, uint32_t vocab, PlanInfo& pi, uint32_t*& h, size_t& h_cap,
+                HostProf& hp) {
   uint64_t max_len = 0;
   for (uint32_t d = 0; d < n_docs; ++d) {
     require(doc_off[d + 1] >= doc_off[d], "doc_off must be non-decreasing");
     max_len = std::max<uint64_t>(max_len, doc_off[d + 1] - doc_off[d]);
   }
   require(max_len < (1ull << 31), "document longer than 2^31 tokens");
-  // Same document layout as the loaded corpus (a new batch of the same shape,
-  // or the same batch re-uploaded): the work plan is a function of doc_off
-  // only, so it and the device copy of doc_off stay valid, and so does a
-  // captured step graph (it reads the token buffer, which was just rewritten).
-  if (c->loaded && c->plan_tok == c->tok && n_docs == c->n_docs && vocab == c->vocab &&
-      c->h_off.size() == static_cast<size_t>(n_docs) + 1 &&
-      std::memcmp(c->h_off.data(), doc_off, sizeof(uint64_t) * (n_docs + 1)) == 0) {
-    c->have_text = false;
-    c->counted = false;
-    reset_downstream(c);
-    return;
-  }
   hp.lap("validate");
-  c->h_off.assign(doc_off, doc_off + n_docs + 1);
-  c->have_text = false;  // refsig_gpu_load_text sets it after this
-  c->n_docs = n_docs;
-  c->vocab = vocab;
-  c->n_tokens = doc_off[n_docs];
-  c->doc_off.ensure(sizeof(uint64_t) * (n_docs + 1));
+  pi = PlanInfo{};
+  pi.n_docs = n_docs;
+  pi.vocab = vocab;
+  pi.n_tokens = doc_off[n_docs];
   // Work plan: documents in decreasing length (counting sort on the length
   // for the usual corpora, a key sort otherwise; ties by id), then split by
   // work class, each list keeping that order (longest first = fewest tails).
@@ -678,70 +701,111 @@ void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, ui
     ++n_class[cls[d]];
   }
   n_class[refsig_gpu_ctx::kPlanOrder] = n_docs;
-  // one pinned staging area: doc_off (u64), then the u32 lists
   uint32_t off = 0;
   for (int k = 0; k < refsig_gpu_ctx::kPlanLists; ++k) {
-    c->plan_off[k] = off;
-    c->plan_n[k] = n_class[k];
+    pi.plan_off[k] = off;
+    pi.plan_n[k] = n_class[k];
     off += n_class[k];
   }
-  const size_t off_bytes = sizeof(uint64_t) * (n_docs + 1), list_bytes = sizeof(uint32_t) * std::max(off, 1u);
-  // documents > 8192 tokens: their scratch offsets (u64) follow the lists in the same staging buffer
-  const size_t loff_at = (off_bytes + list_bytes + 7) & ~size_t{7};
-  const size_t bytes = loff_at + sizeof(uint64_t) * n_class[refsig_gpu_ctx::kPlanLong];
-  if (!c->plan_done) ck(cudaEventCreateWithFlags(&c->plan_done, cudaEventDisableTiming), "event");
+  pi.off_bytes = sizeof(uint64_t) * (n_docs + 1);
+  pi.list_bytes = sizeof(uint32_t) * std::max(off, 1u);
+  pi.loff_at = (pi.off_bytes + pi.list_bytes + 7) & ~size_t{7};
+  pi.bytes = pi.loff_at + sizeof(uint64_t) * n_class[refsig_gpu_ctx::kPlanLong];
   hp.lap("classes");
-  ck(cudaEventSynchronize(c->plan_done), "plan staging");  // the previous copy consumed h_plan
-  hp.lap("plan_done sync");
-  if (bytes > c->h_plan_cap) {
-    if (c->h_plan) cudaFreeHost(c->h_plan);
-    c->h_plan = nullptr;
-    c->h_plan_cap = 0;
-    ck(cudaMallocHost(reinterpret_cast<void**>(&c->h_plan), bytes), "cudaMallocHost");
-    c->h_plan_cap = bytes;
+  if (pi.bytes > h_cap) {
+    if (h) cudaFreeHost(h);
+    h = nullptr;
+    h_cap = 0;
+    ck(cudaMallocHost(reinterpret_cast<void**>(&h), pi.bytes), "cudaMallocHost");
+    h_cap = pi.bytes;
   }
-  std::memcpy(c->h_plan, doc_off, off_bytes);
-  uint32_t* lists = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(c->h_plan) + off_bytes);
+  std::memcpy(h, doc_off, pi.off_bytes);
+  uint32_t* lists = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(h) + pi.off_bytes);
   uint32_t fill[refsig_gpu_ctx::kPlanLists];
-  for (int k = 0; k < refsig_gpu_ctx::kPlanLists; ++k) fill[k] = c->plan_off[k];
-  uint64_t* loff = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(c->h_plan) + loff_at);
-  uint32_t n_loff = 0;
-  uint64_t scratch = 0;
+  for (int k = 0; k < refsig_gpu_ctx::kPlanLists; ++k) fill[k] = pi.plan_off[k];
+  uint64_t* loff = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(h) + pi.loff_at);
   for (uint32_t i = 0; i < n_docs; ++i) {
     const uint32_t d = order[i];
     lists[fill[refsig_gpu_ctx::kPlanOrder]++] = d;
     const int k = cls[d];
     lists[fill[k]++] = d;
     if (k == refsig_gpu_ctx::kPlanLong) {
-      loff[n_loff++] = scratch;
+      loff[pi.n_loff++] = pi.scratch;
       uint64_t p = 1;
       while (p < len(d)) p <<= 1;
-      scratch += p;
+      pi.scratch += p;
     }
   }
-  c->n_sign_long = 0;
-  while (c->n_sign_long < n_docs && len(order[c->n_sign_long]) > kSignLongTokens) ++c->n_sign_long;
-  c->n_sign_half = c->n_sign_long;
-  while (c->n_sign_half < n_docs && len(order[c->n_sign_half]) > kSignHalfTokens) ++c->n_sign_half;
+  while (pi.n_sign_long < n_docs && len(order[pi.n_sign_long]) > kSignLongTokens) ++pi.n_sign_long;
+  pi.n_sign_half = pi.n_sign_long;
+  while (pi.n_sign_half < n_docs && len(order[pi.n_sign_half]) > kSignHalfTokens) ++pi.n_sign_half;
   hp.lap("lists");
-  c->plan.ensure(list_bytes);
-  ck(cudaMemcpyAsync(c->doc_off.p, c->h_plan, off_bytes, cudaMemcpyHostToDevice, c->stream), "H2D doc_off");
-  ck(cudaMemcpyAsync(c->plan.p, lists, list_bytes, cudaMemcpyHostToDevice, c->stream), "H2D plan");
-  if (n_loff) {
-    // (a reallocation here frees the old buffers: cudaFree waits for the device)
-    c->long_scratch.ensure(sizeof(uint32_t) * scratch);
-    c->long_off.ensure(8ull * n_loff);
-    // ordered on ctx->stream after earlier work that may still read the previous offsets (K1's
-    // side streams fork from and join back into ctx->stream)
-    ck(cudaMemcpyAsync(c->long_off.p, loff, 8ull * n_loff, cudaMemcpyHostToDevice, c->stream), "H2D long offsets");
+}
+
+// The plan's three device copies on stream s (ordered after earlier work on s
+// that may still read the destinations).
+void plan_copy(const PlanInfo& pi, const uint32_t* h, DevBuf& doc_off_dst, DevBuf& plan_dst, DevBuf& long_off_dst,
+               cudaStream_t s) {
+  doc_off_dst.ensure(pi.off_bytes);
+  plan_dst.ensure(pi.list_bytes);
+  ck(cudaMemcpyAsync(doc_off_dst.p, h, pi.off_bytes, cudaMemcpyHostToDevice, s), "H2D doc_off");
+  ck(cudaMemcpyAsync(plan_dst.p, reinterpret_cast<const char*>(h) + pi.off_bytes, pi.list_bytes,
+                     cudaMemcpyHostToDevice, s),
+     "H2D plan");
+  if (pi.n_loff) {
+    long_off_dst.ensure(8ull * pi.n_loff);
+    ck(cudaMemcpyAsync(long_off_dst.p, reinterpret_cast<const char*>(h) + pi.loff_at, 8ull * pi.n_loff,
+                       cudaMemcpyHostToDevice, s),
+       "H2D long offsets");
   }
-  ck(cudaEventRecord(c->plan_done, c->stream), "event");  // h_plan (offsets, lists, long offsets) consumed
-  hp.lap("copies");
+}
+
+// Make the plan the context's current one (host fields and state).
+void plan_apply(refsig_gpu_ctx* c, const PlanInfo& pi, const uint64_t* doc_off) {
+  c->h_off.assign(doc_off, doc_off + pi.n_docs + 1);
+  c->have_text = false;  // refsig_gpu_load_text sets it after this
+  c->n_docs = pi.n_docs;
+  c->vocab = pi.vocab;
+  c->n_tokens = pi.n_tokens;
+  std::memcpy(c->plan_off, pi.plan_off, sizeof(pi.plan_off));
+  std::memcpy(c->plan_n, pi.plan_n, sizeof(pi.plan_n));
+  c->n_sign_long = pi.n_sign_long;
+  c->n_sign_half = pi.n_sign_half;
+  // (a reallocation here frees the old buffer: cudaFree waits for the device)
+  if (pi.n_loff) c->long_scratch.ensure(sizeof(uint32_t) * pi.scratch);
   c->loaded = true;
   c->counted = false;
   c->plan_tok = c->tok;
   ++c->load_gen;
   reset_downstream(c);
+}
+
+void load_common(refsig_gpu_ctx* c, const uint64_t* doc_off, uint32_t n_docs, uint32_t vocab) {
+  HostProf hp{"load_common"};
+  validate_doc_off(doc_off, n_docs, vocab);
+  // Same document layout as the loaded corpus (a new batch of the same shape,
+  // or the same batch re-uploaded): the work plan is a function of doc_off
+  // only, so it and the device copy of doc_off stay valid, and so does a
+  // captured step graph (it reads the token buffer, which was just rewritten).
+  if (c->loaded && c->plan_tok == c->tok && n_docs == c->n_docs && vocab == c->vocab &&
+      c->h_off.size() == static_cast<size_t>(n_docs) + 1 &&
+      std::memcmp(c->h_off.data(), doc_off, sizeof(uint64_t) * (n_docs + 1)) == 0) {
+    c->have_text = false;
+    c->counted = false;
+    reset_downstream(c);
+    return;
+  }
+  if (!c->plan_done) ck(cudaEventCreateWithFlags(&c->plan_done, cudaEventDisableTiming), "event");
+  ck(cudaEventSynchronize(c->plan_done), "plan staging");  // the previous copy consumed h_plan
+  hp.lap("plan_done sync");
+  PlanInfo pi;
+  plan_build(doc_off, n_docs, vocab, pi, c->h_plan, c->h_plan_cap, hp);
+  // ordered on ctx->stream after earlier work that may still read the previous plan (K1's side
+  // streams fork from and join back into ctx->stream)
+  plan_copy(pi, c->h_plan, c->doc_off, c->plan, c->long_off, c->stream);
+  ck(cudaEventRecord(c->plan_done, c->stream), "event");  // h_plan consumed
+  hp.lap("copies");
+  plan_apply(c, pi, doc_off);
 }
 
 // R row stride: K <= 32 -> roundup(K,4) (float4 rows, lane-per-hit K2);
@@ -813,7 +877,8 @@ int refsig_gpu_create(int device, refsig_gpu_ctx** out) {
   c->device = device;
   bool ok = cudaSetDevice(device) == cudaSuccess &&
             cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) == cudaSuccess &&
-            cudaMallocHost(&c->h_pin, 64) == cudaSuccess &&
+            cudaHostAlloc(&c->h_pin, 64, cudaHostAllocMapped) == cudaSuccess &&
+            cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_pin), c->h_pin, 0) == cudaSuccess &&
             cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess;
   for (int k = 0; ok && k < 3; ++k)
     ok = cudaStreamCreateWithFlags(&c->side[k], cudaStreamNonBlocking) == cudaSuccess &&
@@ -900,9 +965,7 @@ int refsig_gpu_load_corpus_device(refsig_gpu_ctx* ctx, const uint32_t* d_tokens,
 int refsig_gpu_stage_corpus(refsig_gpu_ctx* ctx, const uint32_t* tokens, const uint64_t* doc_off, uint32_t n_docs,
                             uint32_t vocab) {
   return guard(ctx, [&] {
-    require(doc_off != nullptr, "doc_off is NULL");
-    require(n_docs >= 1, "empty corpus");
-    require(doc_off[0] == 0, "doc_off[0] must be 0");
+    validate_doc_off(doc_off, n_docs, vocab);
     const uint64_t T = doc_off[n_docs];
     require(tokens != nullptr || T == 0, "tokens is NULL");
     require(!ctx->staged, "a staged corpus is waiting for refsig_gpu_swap_corpus");
@@ -911,35 +974,53 @@ int refsig_gpu_stage_corpus(refsig_gpu_ctx* ctx, const uint32_t* tokens, const u
       ck(cudaEventCreateWithFlags(&ctx->ev_staged, cudaEventDisableTiming), "event");
       ck(cudaEventCreateWithFlags(&ctx->ev_next_free, cudaEventDisableTiming), "event");
     }
-    // the staging buffer may still be read by work enqueued before the last swap
+    // pinned plan staging alternates between two buffers: the one written now was last read
+    // by the copies of two stages ago (long done in a steady stream)
+    const int ps = ctx->plan_slot;
+    ctx->plan_slot ^= 1;
+    if (!ctx->ev_plan_next[ps]) ck(cudaEventCreateWithFlags(&ctx->ev_plan_next[ps], cudaEventDisableTiming), "event");
+    if (ctx->plan_next_recorded[ps]) ck(cudaEventSynchronize(ctx->ev_plan_next[ps]), "staged plan copies");
+    HostProf hp{"stage_corpus"};
+    plan_build(doc_off, n_docs, vocab, ctx->staged_pi, ctx->h_plan_next[ps], ctx->h_plan_next_cap[ps], hp);
+    // the staging buffers may still be read by work enqueued before the last swap
     if (ctx->next_free_recorded) ck(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_next_free, 0), "wait");
+    // the small plan copies first, so the compute stream never queues behind the tokens
+    plan_copy(ctx->staged_pi, ctx->h_plan_next[ps], ctx->doc_off_next, ctx->plan_next, ctx->long_off_next,
+              ctx->copy_stream);
+    ck(cudaEventRecord(ctx->ev_plan_next[ps], ctx->copy_stream), "event");
+    ctx->plan_next_recorded[ps] = true;
     ctx->tokens_next.ensure(sizeof(uint32_t) * std::max<uint64_t>(T, 1));
     if (T)
       ck(cudaMemcpyAsync(ctx->tokens_next.p, tokens, sizeof(uint32_t) * T, cudaMemcpyHostToDevice, ctx->copy_stream),
          "H2D staged tokens");
     ck(cudaEventRecord(ctx->ev_staged, ctx->copy_stream), "event");
     ctx->staged_off.assign(doc_off, doc_off + n_docs + 1);
-    ctx->staged_docs = n_docs;
-    ctx->staged_vocab = vocab;
     ctx->staged = true;
   });
+}
+
+static void swap_buf(DevBuf& a, DevBuf& b) {
+  std::swap(a.p, b.p);
+  std::swap(a.cap, b.cap);
 }
 
 int refsig_gpu_swap_corpus(refsig_gpu_ctx* ctx) {
   return guard(ctx, [&] {
     require(ctx->staged, "no staged corpus (refsig_gpu_stage_corpus)");
-    // compute waits for the copy on the device, not the host
+    // compute waits for the copies on the device, not the host
     ck(cudaStreamWaitEvent(ctx->stream, ctx->ev_staged, 0), "wait staged");
-    std::swap(ctx->tokens.p, ctx->tokens_next.p);
-    std::swap(ctx->tokens.cap, ctx->tokens_next.cap);
-    // the previous batch's buffer becomes the staging buffer: free once the
-    // work already enqueued on the compute stream is done with it
+    swap_buf(ctx->tokens, ctx->tokens_next);
+    swap_buf(ctx->doc_off, ctx->doc_off_next);
+    swap_buf(ctx->plan, ctx->plan_next);
+    swap_buf(ctx->long_off, ctx->long_off_next);
+    // the previous batch's buffers become the staging buffers: free once the
+    // work already enqueued on the compute stream is done with them
     ck(cudaEventRecord(ctx->ev_next_free, ctx->stream), "event");
     ctx->next_free_recorded = true;
     ctx->staged = false;
     ctx->tok = ctx->tokens.as<uint32_t>();
-    g_alloc_gen.fetch_add(1);  // captured step graphs read the old token buffer
-    load_common(ctx, ctx->staged_off.data(), ctx->staged_docs, ctx->staged_vocab);
+    g_alloc_gen.fetch_add(1);  // captured step graphs read the old buffers
+    plan_apply(ctx, ctx->staged_pi, ctx->staged_off.data());
   });
 }
 
@@ -1113,7 +1194,7 @@ static uint64_t stage_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_do
     u_cap += ctx->h_off[ref_doc_ids[k] + 1] - ctx->h_off[ref_doc_ids[k]];
   }
   ctx->ref_docs.ensure(4ull * K);
-  upload(ctx, ctx->ref_docs.p, ref_doc_ids, 4ull * K);
+  launch_param_words(ref_doc_ids, K, ctx->ref_docs.as<uint32_t>(), ctx->stream);  // K <= kParamWords
   return u_cap;
 }
 
@@ -1698,12 +1779,9 @@ int refsig_gpu_mrc_step(refsig_gpu_ctx* ctx, int weight_mode, const uint32_t* re
     key.alloc_gen = g_alloc_gen.load();
     if (ctx->step_exec && key == ctx->step_key) {
       // replay: every buffer and the candidate capacity are exactly as
-      // captured; the captured H2D copy reads the reference ids from the
-      // pinned staging buffer, which other calls may have reused
-      ck(cudaEventSynchronize(ctx->stage_done), "staging");
-      std::memcpy(ctx->h_stage, ref_doc_ids, 4ull * K);
+      // captured; the reference ids are kernel parameters of the graph (the
+      // key includes them)
       ck(cudaGraphLaunch(ctx->step_exec, ctx->stream), "cudaGraphLaunch");
-      ck(cudaEventRecord(ctx->stage_done, ctx->stream), "event");
       ctx->emit_pending = true;
       ctx->have_pairs = ctx->keys_valid = false;
       ctx->emit_grid = self_grid(ctx);
@@ -1745,7 +1823,7 @@ int refsig_gpu_mrc_step(refsig_gpu_ctx* ctx, int weight_mode, const uint32_t* re
     ctx->capturing = false;
     ctx->prof = prof;
     ck(e, "stream capture");
-    ck(cudaEventRecord(ctx->stage_done, ctx->stream), "event");
+    if (ctx->stage_done) ck(cudaEventRecord(ctx->stage_done, ctx->stream), "event");
     e = cudaGraphInstantiate(&ctx->step_exec, graph, 0);
     cudaGraphDestroy(graph);
     ck(e, "cudaGraphInstantiate");

@@ -505,6 +505,33 @@ __global__ void rebase_rowptr_kernel(const uint64_t* __restrict__ in, uint64_t n
     out[i] = in[i] - base;
 }
 
+// Small host -> device values passed as kernel parameters (no copy engine:
+// a small cudaMemcpyAsync can queue behind a large staged upload on the same
+// engine and stall the compute stream for the length of that upload).
+struct ParamWords {
+  uint32_t v[kParamWords];
+};
+__global__ void param_words_kernel(ParamWords p, uint32_t n, uint32_t* __restrict__ dst) {
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = p.v[i];
+}
+
+void launch_param_words(const uint32_t* host_src, uint32_t n, uint32_t* dst, cudaStream_t s) {
+  ParamWords p;
+  for (uint32_t i = 0; i < n && i < kParamWords; ++i) p.v[i] = host_src[i];
+  param_words_kernel<<<1, 256, 0, s>>>(p, n < kParamWords ? n : kParamWords, dst);
+  note_launch();
+}
+
+// Device words -> mapped pinned host memory by a kernel (again no copy engine).
+__global__ void words_to_host_kernel(const uint32_t* __restrict__ src, uint32_t n, uint32_t* __restrict__ dst) {
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+void launch_words_to_host(const uint32_t* src, uint32_t n, uint32_t* mapped_dst, cudaStream_t s) {
+  words_to_host_kernel<<<1, 32, 0, s>>>(src, n, mapped_dst);
+  note_launch();
+}
+
 void launch_rebase_rowptr(const uint64_t* in, uint64_t n, uint64_t* out, cudaStream_t s) {
   if (!n) return;
   const uint64_t blocks = std::min<uint64_t>(ceil_div(n, 256), 148ull * 8);

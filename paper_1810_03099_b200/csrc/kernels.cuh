@@ -167,6 +167,11 @@ void launch_emit_pairs(const uint32_t* bitmap, const PairGrid& g, const uint32_t
 void launch_narrow_cols(const uint32_t* in, uint64_t n, uint16_t* out, cudaStream_t s);
 // out[i] = in[i] - in[0] for i < n (a row range's CSR offsets rebased to 0).
 void launch_rebase_rowptr(const uint64_t* in, uint64_t n, uint64_t* out, cudaStream_t s);
+// n <= kParamWords host words to the device as kernel parameters (no copy engine).
+constexpr uint32_t kParamWords = 256;
+void launch_param_words(const uint32_t* host_src, uint32_t n, uint32_t* dst, cudaStream_t s);
+// n device words into mapped pinned host memory (device pointer of it) by a kernel.
+void launch_words_to_host(const uint32_t* src, uint32_t n, uint32_t* mapped_dst, cudaStream_t s);
 
 // ---- K4a simhash -------------------------------------------------------------
 struct SimhashArgs {
