@@ -395,9 +395,9 @@ def run_ours(args):
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
                         "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["_ms"],
                         "note": ("a stream of fresh batches (each a different document order of configs[1]: new "
-                                 "layout and work plan every batch) through the public API: stage_corpus (next "
-                                 "batch's pinned tokens, H2D on the copy stream overlapping this batch) + "
-                                 "swap_corpus + count + set_reference_docs + sign + mrc_pairs_rows + "
+                                 "layout and work plan every batch) through the public API: swap_corpus + count + "
+                                 "set_reference_docs + sign + stage_corpus (pinned tokens of the batch two ahead, "
+                                 "H2D on the copy stream overlapping this batch) + mrc_pairs_rows + "
                                  "get_pairs_csr16_async (rowptr + sorted uint16 columns into pinned host memory, "
                                  "D2H overlapping the next batch) + wait_fetch; host wall clock over all batches / "
                                  "batches" if e2e_fresh else
@@ -635,9 +635,9 @@ def permuted_batches(cp, refs, n_batches, seed=1234):
 def measure_e2e_stream(ctx, cp, refs, tau, stream, dev, steps, warmup=2, n_distinct=4):
     """Headline e2e: a stream of FRESH batches (each a different document order,
     so a new layout and work plan every batch) through the public API, host
-    wall clock over all batches: stage_corpus (next batch's pinned tokens: H2D
-    on the copy stream, overlapping this batch) -> swap_corpus -> count ->
-    set_reference_docs -> sign -> mrc_pairs_rows (sorted CSR on the device;
+    wall clock over all batches: swap_corpus -> count -> set_reference_docs ->
+    sign -> stage_corpus (pinned tokens of the batch two ahead: H2D on the copy
+    stream, queued behind the next batch's, overlapping this one) -> mrc_pairs_rows (sorted CSR on the device;
     returns the exact count) -> get_pairs_csr16_async (rowptr + uint16 columns
     into pinned host memory on the D2H stream, overlapping the next batch) ->
     wait_fetch before the host buffers are reused. No CUDA graph: a captured
@@ -657,8 +657,9 @@ def measure_e2e_stream(ctx, cp, refs, tau, stream, dev, steps, warmup=2, n_disti
                  torch.empty(cap, dtype=torch.int16).pin_memory().numpy().view(np.uint16)) for _ in range(2)]
         torch.cuda.synchronize(dev)
         n = 0
-        b = batches[1 % n_distinct]
-        ctx.stage_corpus(b[0], b[1], cp.vocab)
+        for k in (1, 2):  # two batches staged ahead: the copy engine always has the next upload queued
+            b = batches[k % n_distinct]
+            ctx.stage_corpus(b[0], b[1], cp.vocab)
         t0 = None
         for s in range(warmup + steps):
             if s == warmup:
@@ -666,18 +667,19 @@ def measure_e2e_stream(ctx, cp, refs, tau, stream, dev, steps, warmup=2, n_disti
                 t0 = time.perf_counter()
             ctx.swap_corpus()
             cur = batches[(s + 1) % n_distinct]
-            nxt = batches[(s + 2) % n_distinct]
-            ctx.stage_corpus(nxt[0], nxt[1], cp.vocab)  # H2D of the next batch overlaps this one
+            nxt = batches[(s + 3) % n_distinct]
             ctx.count(R.WEIGHT_TFIDF)
             ctx.set_reference_docs(cur[2])
             ctx.sign(fetch=False)
+            ctx.stage_corpus(nxt[0], nxt[1], cp.vocab)  # H2D of a later batch overlaps this one
             n = ctx.mrc_pairs_rows(tau, 0, N, fetch=False)
             rowptr, cols = host[s & 1]
             ctx.pairs_csr16_async(rowptr, cols)  # D2H overlaps the next batch
             # (the buffers of batch s-1 are complete once this returns; the caller consumes them here)
         ctx.wait_fetch()
         t1 = time.perf_counter()
-        ctx.swap_corpus()  # drain the last staged batch
+        ctx.swap_corpus()  # drain the staged batches
+        ctx.swap_corpus()
     h2d = cp.tokens.nbytes + cp.doc_off.nbytes + refs.nbytes
     return {"_ms": 1e3 * (t1 - t0) / steps, "h2d": int(h2d), "d2h": int(n * 2 + (N + 1) * 8),
             "batches": steps, "distinct_layouts": n_distinct}

@@ -212,13 +212,15 @@ int refsig_gpu_set_reference_counts(refsig_gpu_ctx* ctx, uint32_t K, const uint6
 int refsig_gpu_set_signatures(refsig_gpu_ctx* ctx, uint32_t n_docs, uint32_t K, const float* S, int on_device);
 
 /* ---- streaming batches (configs[4] query batches) -----------------------------
- * refsig_gpu_stage_corpus starts the host->device copy of the NEXT batch on
- * the context's copy stream (into a second token buffer) and returns at once;
- * pass pinned host memory for the copy to overlap. refsig_gpu_swap_corpus
- * makes the staged batch the context's corpus, exactly as load_corpus would
- * (the compute stream waits for the copy on the device; the host does not).
- * Typical loop: stage(b0); swap; stage(b1); count/sign/pairs(b0); swap;
- * stage(b2); count/sign/pairs(b1); ... */
+ * refsig_gpu_stage_corpus starts the host->device copy of a LATER batch on
+ * the context's copy stream (into staging buffers; up to two batches may be
+ * staged ahead) and returns at once; pass pinned host memory for the copy to
+ * overlap. refsig_gpu_swap_corpus makes the oldest staged batch the context's
+ * corpus, exactly as load_corpus would (the compute stream waits for the copy
+ * on the device; the host does not).
+ * Typical loop: stage(b0); stage(b1); swap; count/sign/pairs(b0); stage(b2);
+ * swap; count/sign/pairs(b1); ... — with two staged, the copy engine always
+ * has the next upload queued behind the current one. */
 int refsig_gpu_stage_corpus(refsig_gpu_ctx* ctx, const uint32_t* tokens, const uint64_t* doc_off, uint32_t n_docs,
                             uint32_t vocab);
 int refsig_gpu_swap_corpus(refsig_gpu_ctx* ctx);

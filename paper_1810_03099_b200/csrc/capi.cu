@@ -224,21 +224,33 @@ struct refsig_gpu_ctx {
   DevBuf records;                                                              // MRCS records
   DevBuf tc_forms;                                                             // K3 tcgen05 operand forms
 
-  // staged next corpus (refsig_gpu_stage_corpus / swap_corpus): tokens copied on
-  // copy_stream into `tokens_next` while the current batch computes
-  // and the staged batch's work plan (built on the host at stage time, copied
-  // on copy_stream too: no small copies left for the compute stream at swap)
-  DevBuf tokens_next, doc_off_next, plan_next, long_off_next;
-  uint32_t* h_plan_next[2] = {nullptr, nullptr};  // alternate: the last stage's copy may still run
-  size_t h_plan_next_cap[2] = {0, 0};
-  cudaEvent_t ev_plan_next[2] = {nullptr, nullptr};  // h_plan_next[k] consumed
-  bool plan_next_recorded[2] = {false, false};
-  int plan_slot = 0;
-  cudaStream_t copy_stream = nullptr;
-  cudaEvent_t ev_staged = nullptr, ev_next_free = nullptr;
-  bool staged = false, next_free_recorded = false;
-  std::vector<uint64_t> staged_off;
-  PlanInfo staged_pi;
+  // staged batches (refsig_gpu_stage_corpus / swap_corpus), up to kStageDepth
+  // ahead in a ring: tokens and the work plan (built on the host at stage time)
+  // copied on copy_stream into the slot's buffers while earlier batches
+  // compute; a swap exchanges the slot's buffers with the live ones
+  struct Staged {
+    DevBuf tokens, doc_off, plan, long_off;
+    cudaEvent_t ev_ready = nullptr;  // the slot's copies are done (copy stream)
+    cudaEvent_t ev_plan = nullptr;   // its plan copies are done: h_plan reusable (copy stream)
+    cudaEvent_t ev_free = nullptr;   // its buffers are no longer read by compute (compute stream)
+    bool free_recorded = false;
+    PlanInfo pi;
+    std::vector<uint64_t> off;
+  };
+  static constexpr int kStageDepth = 2;
+  Staged stg[kStageDepth];
+  // pinned plan staging, a ring deeper than the slots: the buffer reused now was
+  // read by plan copies issued kPlanRing stages ago (those can queue behind a
+  // token upload on the copy engine, so one ring per slot was not enough)
+  static constexpr int kPlanRing = 4;
+  uint32_t* h_plans[kPlanRing] = {};
+  size_t h_plans_cap[kPlanRing] = {};
+  cudaEvent_t ev_hplan[kPlanRing] = {};
+  bool hplan_recorded[kPlanRing] = {};
+  int hplan_next = 0;
+  int stg_head = 0, stg_count = 0;
+  cudaStream_t copy_stream = nullptr;  // staged tokens, back to back
+  cudaStream_t plan_stream = nullptr;  // staged plans: small copies that must not sit between two token uploads
 
   // asynchronous result fetch (refsig_gpu_get_pairs_csr16_async): two slots of
   // device staging (rebased rowptr, 16-bit columns) copied to the host on
@@ -296,8 +308,9 @@ struct refsig_gpu_ctx {
   // (name, buffer) of every device buffer, for refsig_gpu_debug_check
   std::vector<std::pair<const char*, const DevBuf*>> buffers() const {
     return {{"tokens", &tokens}, {"doc_off", &doc_off}, {"plan", &plan}, {"long_off", &long_off},
-            {"tokens_next", &tokens_next}, {"doc_off_next", &doc_off_next}, {"plan_next", &plan_next},
-            {"long_off_next", &long_off_next},
+            {"stg0.tokens", &stg[0].tokens}, {"stg0.doc_off", &stg[0].doc_off}, {"stg0.plan", &stg[0].plan},
+            {"stg0.long_off", &stg[0].long_off}, {"stg1.tokens", &stg[1].tokens}, {"stg1.doc_off", &stg[1].doc_off},
+            {"stg1.plan", &stg[1].plan}, {"stg1.long_off", &stg[1].long_off},
             {"long_scratch", &long_scratch}, {"ent", &ent}, {"nnz", &nnz}, {"df", &df}, {"df_rep", &df_rep},
             {"info", &info}, {"flags", &flags}, {"rowptr", &rowptr}, {"c_ids", &c_ids}, {"c_counts", &c_counts},
             {"inv_norm", &inv_norm}, {"ref_docs", &ref_docs}, {"ref_start", &ref_start}, {"ref_n", &ref_n},
@@ -321,17 +334,20 @@ struct refsig_gpu_ctx {
     if (h_stage) cudaFreeHost(h_stage);
     if (stage_done) cudaEventDestroy(stage_done);
     if (h_plan) cudaFreeHost(h_plan);
-    for (int k = 0; k < 2; ++k) {
-      if (h_plan_next[k]) cudaFreeHost(h_plan_next[k]);
-      if (ev_plan_next[k]) cudaEventDestroy(ev_plan_next[k]);
+    for (int k = 0; k < kPlanRing; ++k) {
+      if (h_plans[k]) cudaFreeHost(h_plans[k]);
+      if (ev_hplan[k]) cudaEventDestroy(ev_hplan[k]);
+    }
+    for (auto& g : stg) {
+      if (g.ev_ready) cudaEventDestroy(g.ev_ready);
+      if (g.ev_plan) cudaEventDestroy(g.ev_plan);
+      if (g.ev_free) cudaEventDestroy(g.ev_free);
     }
     if (plan_done) cudaEventDestroy(plan_done);
     if (step_exec) cudaGraphExecDestroy(step_exec);
-    if (ev_staged) cudaEventDestroy(ev_staged);
     if (ev_fetch_ready) cudaEventDestroy(ev_fetch_ready);
     for (auto e : ev_fetched)
       if (e) cudaEventDestroy(e);
-    if (ev_next_free) cudaEventDestroy(ev_next_free);
   }
 };
 
@@ -905,6 +921,10 @@ void refsig_gpu_destroy(refsig_gpu_ctx* ctx) {
     if (ctx->ev_join[k]) cudaEventDestroy(ctx->ev_join[k]);
   }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->plan_stream) {
+    cudaStreamSynchronize(ctx->plan_stream);
+    cudaStreamDestroy(ctx->plan_stream);
+  }
   if (ctx->copy_stream) {
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamDestroy(ctx->copy_stream);
@@ -968,34 +988,45 @@ int refsig_gpu_stage_corpus(refsig_gpu_ctx* ctx, const uint32_t* tokens, const u
     validate_doc_off(doc_off, n_docs, vocab);
     const uint64_t T = doc_off[n_docs];
     require(tokens != nullptr || T == 0, "tokens is NULL");
-    require(!ctx->staged, "a staged corpus is waiting for refsig_gpu_swap_corpus");
+    require(ctx->stg_count < refsig_gpu_ctx::kStageDepth,
+            "two staged corpora are waiting for refsig_gpu_swap_corpus");
     if (!ctx->copy_stream) {
       ck(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
-      ck(cudaEventCreateWithFlags(&ctx->ev_staged, cudaEventDisableTiming), "event");
-      ck(cudaEventCreateWithFlags(&ctx->ev_next_free, cudaEventDisableTiming), "event");
+      ck(cudaStreamCreateWithFlags(&ctx->plan_stream, cudaStreamNonBlocking), "plan stream");
     }
-    // pinned plan staging alternates between two buffers: the one written now was last read
-    // by the copies of two stages ago (long done in a steady stream)
-    const int ps = ctx->plan_slot;
-    ctx->plan_slot ^= 1;
-    if (!ctx->ev_plan_next[ps]) ck(cudaEventCreateWithFlags(&ctx->ev_plan_next[ps], cudaEventDisableTiming), "event");
-    if (ctx->plan_next_recorded[ps]) ck(cudaEventSynchronize(ctx->ev_plan_next[ps]), "staged plan copies");
+    auto& g = ctx->stg[(ctx->stg_head + ctx->stg_count) % refsig_gpu_ctx::kStageDepth];
+    if (!g.ev_ready) {
+      ck(cudaEventCreateWithFlags(&g.ev_ready, cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&g.ev_plan, cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&g.ev_free, cudaEventDisableTiming), "event");
+    }
     HostProf hp{"stage_corpus"};
-    plan_build(doc_off, n_docs, vocab, ctx->staged_pi, ctx->h_plan_next[ps], ctx->h_plan_next_cap[ps], hp);
-    // the staging buffers may still be read by work enqueued before the last swap
-    if (ctx->next_free_recorded) ck(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_next_free, 0), "wait");
-    // the small plan copies first, so the compute stream never queues behind the tokens
-    plan_copy(ctx->staged_pi, ctx->h_plan_next[ps], ctx->doc_off_next, ctx->plan_next, ctx->long_off_next,
-              ctx->copy_stream);
-    ck(cudaEventRecord(ctx->ev_plan_next[ps], ctx->copy_stream), "event");
-    ctx->plan_next_recorded[ps] = true;
-    ctx->tokens_next.ensure(sizeof(uint32_t) * std::max<uint64_t>(T, 1));
+    const int hk = ctx->hplan_next;
+    ctx->hplan_next = (hk + 1) % refsig_gpu_ctx::kPlanRing;
+    if (!ctx->ev_hplan[hk]) ck(cudaEventCreateWithFlags(&ctx->ev_hplan[hk], cudaEventDisableTiming), "event");
+    if (ctx->hplan_recorded[hk]) ck(cudaEventSynchronize(ctx->ev_hplan[hk]), "staged plan copies");
+    hp.lap("plan ring sync");
+    plan_build(doc_off, n_docs, vocab, g.pi, ctx->h_plans[hk], ctx->h_plans_cap[hk], hp);
+    // the slot's device buffers may still be read by work enqueued before they were swapped out
+    if (g.free_recorded) {
+      ck(cudaStreamWaitEvent(ctx->copy_stream, g.ev_free, 0), "wait");
+      ck(cudaStreamWaitEvent(ctx->plan_stream, g.ev_free, 0), "wait");
+    }
+    // the small plan copies on their own stream: they run beside the previous batch's token
+    // upload instead of delaying the next one (a small copy next to a large D2H takes ~60 us)
+    plan_copy(g.pi, ctx->h_plans[hk], g.doc_off, g.plan, g.long_off, ctx->plan_stream);
+    ck(cudaEventRecord(g.ev_plan, ctx->plan_stream), "event");
+    ck(cudaEventRecord(ctx->ev_hplan[hk], ctx->plan_stream), "event");
+    ctx->hplan_recorded[hk] = true;
+    hp.lap("plan copies");
+    g.tokens.ensure(sizeof(uint32_t) * std::max<uint64_t>(T, 1));
     if (T)
-      ck(cudaMemcpyAsync(ctx->tokens_next.p, tokens, sizeof(uint32_t) * T, cudaMemcpyHostToDevice, ctx->copy_stream),
+      ck(cudaMemcpyAsync(g.tokens.p, tokens, sizeof(uint32_t) * T, cudaMemcpyHostToDevice, ctx->copy_stream),
          "H2D staged tokens");
-    ck(cudaEventRecord(ctx->ev_staged, ctx->copy_stream), "event");
-    ctx->staged_off.assign(doc_off, doc_off + n_docs + 1);
-    ctx->staged = true;
+    ck(cudaEventRecord(g.ev_ready, ctx->copy_stream), "event");
+    hp.lap("token copy");
+    g.off.assign(doc_off, doc_off + n_docs + 1);
+    ++ctx->stg_count;
   });
 }
 
@@ -1006,21 +1037,24 @@ static void swap_buf(DevBuf& a, DevBuf& b) {
 
 int refsig_gpu_swap_corpus(refsig_gpu_ctx* ctx) {
   return guard(ctx, [&] {
-    require(ctx->staged, "no staged corpus (refsig_gpu_stage_corpus)");
-    // compute waits for the copies on the device, not the host
-    ck(cudaStreamWaitEvent(ctx->stream, ctx->ev_staged, 0), "wait staged");
-    swap_buf(ctx->tokens, ctx->tokens_next);
-    swap_buf(ctx->doc_off, ctx->doc_off_next);
-    swap_buf(ctx->plan, ctx->plan_next);
-    swap_buf(ctx->long_off, ctx->long_off_next);
-    // the previous batch's buffers become the staging buffers: free once the
-    // work already enqueued on the compute stream is done with them
-    ck(cudaEventRecord(ctx->ev_next_free, ctx->stream), "event");
-    ctx->next_free_recorded = true;
-    ctx->staged = false;
+    require(ctx->stg_count > 0, "no staged corpus (refsig_gpu_stage_corpus)");
+    auto& g = ctx->stg[ctx->stg_head];
+    // compute waits for the slot's copies on the device, not the host
+    ck(cudaStreamWaitEvent(ctx->stream, g.ev_plan, 0), "wait staged plan");
+    ck(cudaStreamWaitEvent(ctx->stream, g.ev_ready, 0), "wait staged");
+    swap_buf(ctx->tokens, g.tokens);
+    swap_buf(ctx->doc_off, g.doc_off);
+    swap_buf(ctx->plan, g.plan);
+    swap_buf(ctx->long_off, g.long_off);
+    // the previous batch's buffers now sit in the slot: free once the work
+    // already enqueued on the compute stream is done with them
+    ck(cudaEventRecord(g.ev_free, ctx->stream), "event");
+    g.free_recorded = true;
+    ctx->stg_head = (ctx->stg_head + 1) % refsig_gpu_ctx::kStageDepth;
+    --ctx->stg_count;
     ctx->tok = ctx->tokens.as<uint32_t>();
     g_alloc_gen.fetch_add(1);  // captured step graphs read the old buffers
-    plan_apply(ctx, ctx->staged_pi, ctx->staged_off.data());
+    plan_apply(ctx, g.pi, g.off.data());
   });
 }
 

@@ -44,6 +44,33 @@ def test_stage_swap_equals_load(gpu_ctx_factory):
         assert np.array_equal(Sa, Sb) and np.array_equal(ka, kb), f"batch {k}"
 
 
+def test_stage_two_ahead_equals_load(gpu_ctx_factory):
+    """Two batches staged ahead (the copy engine always has the next upload
+    queued): each batch still gives what load_corpus gives; a third stage
+    before a swap is refused."""
+    batches = _batches(4)
+    refs = np.arange(10, dtype=np.uint32) * 7
+    a, b = gpu_ctx_factory(), gpu_ctx_factory()
+    b.stage_corpus(*batches[0])
+    b.stage_corpus(*batches[1])
+    with pytest.raises((R.ValidationError, R.RefsigRuntimeError)):
+        b.stage_corpus(*batches[2])
+    for k, (tok, off, V) in enumerate(batches):
+        b.swap_corpus()
+        b.count()
+        b.set_reference_docs(refs)
+        Sb = b.sign()
+        if k + 2 < len(batches):
+            b.stage_corpus(*batches[k + 2])
+        kb = b.mrc_pairs(0.95)
+        a.load_corpus(tok, off, V)
+        a.count()
+        a.set_reference_docs(refs)
+        Sa = a.sign()
+        ka = a.mrc_pairs(0.95)
+        assert np.array_equal(Sa, Sb) and np.array_equal(ka, kb), f"batch {k}"
+
+
 def test_query_join_cached_database_forms(gpu_ctx_factory):
     cp, _ = C.config_corpus("c0")
     refs = C.sample_refs(0, cp.n_docs, 64)

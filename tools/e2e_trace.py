@@ -36,15 +36,16 @@ with torch.cuda.stream(stream):
              torch.empty(cap, dtype=torch.int16).pin_memory().numpy().view(np.uint16)) for _ in range(2)]
     torch.cuda.synchronize(dev)
     ctx.stage_corpus(batches[1][0], batches[1][1], cp.vocab)
+    ctx.stage_corpus(batches[2][0], batches[2][1], cp.vocab)
 
     def loop(steps, s0=0):
         for s in range(s0, s0 + steps):
             ctx.swap_corpus()
-            cur, nxt = batches[(s + 1) % 4], batches[(s + 2) % 4]
-            ctx.stage_corpus(nxt[0], nxt[1], cp.vocab)
+            cur, nxt = batches[(s + 1) % 4], batches[(s + 3) % 4]
             ctx.count(R.WEIGHT_TFIDF)
             ctx.set_reference_docs(cur[2])
             ctx.sign(fetch=False)
+            ctx.stage_corpus(nxt[0], nxt[1], cp.vocab)
             ctx.mrc_pairs_rows(tau, 0, N, fetch=False)
             rowptr, cols = host[s & 1]
             ctx.pairs_csr16_async(rowptr, cols)
