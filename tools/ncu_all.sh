@@ -5,11 +5,11 @@
 cd "$(dirname "$0")/.."
 out=gpurun_out
 python tools/step_timing.py --steps 3 > $out/plain_st.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_r02.csv \
+  ncu -f --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_r02.csv \
       python tools/step_timing.py --steps 3 > $out/ncu_l.log 2>&1
-for spec in "c1 57 70" "c3 18 17" "c4 20 18"; do
-  set -- $spec
-  ncu --set full --clock-control none --import-source on -s $2 -c $3 -o /tmp/prof_$1 \
+for c in c1 c3 c4; do
+  set -- $c
+  ncu -f --set full --clock-control none --import-source on --nvtx --nvtx-include "measured/" -o /tmp/prof_$1 \
       python tools/prof_all.py --config $1 > $out/ncu_$1.log 2>&1
   ncu -i /tmp/prof_$1.ncu-rep --page raw --csv > $out/ncu_raw_$1.csv 2>/dev/null
   python tools/sass_mix.py /tmp/prof_$1.ncu-rep --top 12 > $out/ncu_mix_$1.txt 2>/dev/null

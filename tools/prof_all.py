@@ -6,9 +6,10 @@ deterministic command to put under `ncu --set full` for per-kernel evidence.
   python tools/prof_all.py --config c3   # K2 column-owner (K=64), chunked tcgen05 K3, persistent emission
   python tools/prof_all.py --config c4   # database sign (K=128), the rb=1 tcgen05 query join, Hamming scan
 
-A warm-up pass runs first (buffers sized, caches of the host plan built), so
-with `ncu -s <launches of the warm-up>` only the measured pass is captured;
-the script prints the number of launches of each pass."""
+A warm-up pass runs first (buffers sized, caches of the host plan built); the
+measured pass runs inside the NVTX range "measured", so
+`ncu --nvtx --nvtx-include "measured/"` captures only it (CUB's sorts launch
+several kernels per library call, so launch counts cannot be used to skip)."""
 import argparse
 import os
 import sys
@@ -23,6 +24,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c1")
     args = ap.parse_args()
+    import torch
     import paper_1810_03099_b200 as R
     from paper_1810_03099_b200 import corpus as C
 
@@ -42,12 +44,17 @@ def main():
         qc.attach_database(dbc)
         for p in range(2):
             l0 = R.Context.launch_count()
+            if p == 1:
+                torch.cuda.nvtx.range_push("measured")
             qc.load_corpus(q.tokens, q.doc_off, q.vocab)
             qc.count()
             qc.sign(fetch=False)
             qc.mrc_query_pairs(tau, fetch=False)
             qc.simhash(0)
             qc.hamming_query_pairs(thr["hamming_max"], fetch=False)
+            qc.synchronize()
+            if p == 1:
+                torch.cuda.nvtx.range_pop()
             print(f"pass {p}: {R.Context.launch_count() - l0} launches")
         return
     cp, cfg = C.config_corpus(args.config)
@@ -56,6 +63,8 @@ def main():
     ctx.load_corpus(cp.tokens, cp.doc_off, cp.vocab)
     for p in range(2):
         l0 = R.Context.launch_count()
+        if p == 1:
+            torch.cuda.nvtx.range_push("measured")
         ctx.count(R.WEIGHT_TFIDF)
         ctx.set_reference_docs(refs)
         ctx.sign(fetch=False)
@@ -70,10 +79,14 @@ def main():
             ctx.hamming_pairs(thr["hamming_max"], fetch=False)
             ctx.exact_pairs(thr["tau_cos"], fetch=False)
             ctx.evaluate()
+            ctx.exact_pairs(thr["tau_cos"], fetch=False)
             ctx.corpus_freq()
             ctx.signature_records(1)
             ctx.pair_cosines(np.array([1, (2 << 32) | 3], np.uint64))
             ctx.counts()
+        ctx.synchronize()
+        if p == 1:
+            torch.cuda.nvtx.range_pop()
         print(f"pass {p}: {R.Context.launch_count() - l0} launches")
     if args.config == "c1":
         text, off = C.synth_text(cp.tokens[: int(cp.doc_off[4000])], cp.doc_off[:4001], cp.vocab)
