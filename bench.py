@@ -624,7 +624,8 @@ def permuted_batches(cp, refs, n_batches, seed=1234):
         off = np.zeros(cp.n_docs + 1, np.uint64)
         np.cumsum(lens[perm], out=off[1:])
         idx = np.concatenate([np.arange(cp.doc_off[d], cp.doc_off[d + 1], dtype=np.int64) for d in perm])
-        pin = torch.empty(len(idx), dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+        t = torch.empty(len(idx), dtype=torch.int32)
+        pin = (t.pin_memory() if torch.cuda.is_available() else t).numpy().view(np.uint32)
         pin[:] = cp.tokens[idx]
         inv = np.empty(cp.n_docs, np.int64)
         inv[perm] = np.arange(cp.n_docs)

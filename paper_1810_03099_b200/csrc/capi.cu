@@ -69,9 +69,6 @@ void ck(cudaError_t e, const char* what) {
 void require(bool ok, const char* msg) {
   if (!ok) fail(REFSIG_E_VALIDATION, msg);
 }
-void require(bool ok, const std::string& msg) {
-  if (!ok) fail(REFSIG_E_VALIDATION, msg);
-}
 
 // Debug guard (REFSIG_CANARY=1): every device buffer gets kCanaryBytes of
 // 0xA5 past its capacity; refsig_gpu_debug_check verifies them (a kernel that
@@ -190,7 +187,8 @@ struct refsig_gpu_ctx {
   // reference
   bool have_ref = false;
   uint32_t K = 0, Kp = 0;  // Kp: row stride of R
-  DevBuf ref_docs, ref_start, ref_n, ref_ent, ref_count, R;
+  DevBuf ref_start, ref_n, ref_ent, ref_count, R;
+  std::vector<uint32_t> ref_ids;  // reference document ids (kernel parameters)
   bool ref_dirty = false;  // info[].ref_row holds a previous reference's rows
 
   // sign
@@ -291,11 +289,6 @@ struct refsig_gpu_ctx {
   uint64_t load_gen = 0;
   bool capturing = false;
 
-  // pinned staging for small uploads (no hidden stream sync of pageable H2D)
-  void* h_stage = nullptr;
-  size_t stage_cap = 0;
-  cudaEvent_t stage_done = nullptr;
-
   // profiling: event pairs per phase on `stream`, resolved lazily
   bool prof = false;
   struct Mark {
@@ -313,7 +306,7 @@ struct refsig_gpu_ctx {
             {"stg1.plan", &stg[1].plan}, {"stg1.long_off", &stg[1].long_off},
             {"long_scratch", &long_scratch}, {"ent", &ent}, {"nnz", &nnz}, {"df", &df}, {"df_rep", &df_rep},
             {"info", &info}, {"flags", &flags}, {"rowptr", &rowptr}, {"c_ids", &c_ids}, {"c_counts", &c_counts},
-            {"inv_norm", &inv_norm}, {"ref_docs", &ref_docs}, {"ref_start", &ref_start}, {"ref_n", &ref_n},
+            {"inv_norm", &inv_norm}, {"ref_start", &ref_start}, {"ref_n", &ref_n},
             {"ref_ent", &ref_ent}, {"ref_count", &ref_count}, {"R", &R}, {"S", &S}, {"ST", &ST}, {"bitmap", &bitmap},
             {"rowcnt", &rowcnt}, {"rowstart", &rowstart}, {"cand", &cand}, {"scan_tmp", &scan_tmp}, {"keys", &keys},
             {"emit_ctr", &emit_ctr}, {"cand16", &cand16}, {"text", &text}, {"text_off", &text_off},
@@ -331,8 +324,6 @@ struct refsig_gpu_ctx {
       cudaEventDestroy(m.b);
     }
     for (auto e : ev_free) cudaEventDestroy(e);
-    if (h_stage) cudaFreeHost(h_stage);
-    if (stage_done) cudaEventDestroy(stage_done);
     if (h_plan) cudaFreeHost(h_plan);
     for (int k = 0; k < kPlanRing; ++k) {
       if (h_plans[k]) cudaFreeHost(h_plans[k]);
@@ -432,27 +423,6 @@ struct Phase {
   }
 };
 
-// Copy a small host array to the device through the pinned staging buffer:
-// returns without waiting for the stream (the caller's buffer is free to reuse).
-void upload(refsig_gpu_ctx* c, void* dst, const void* src, size_t bytes) {
-  if (!bytes) return;
-  if (!c->stage_done) ck(cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming), "event");
-  if (!c->capturing) ck(cudaEventSynchronize(c->stage_done), "staging");  // previous upload consumed
-  if (bytes > c->stage_cap) {
-    if (c->h_stage) cudaFreeHost(c->h_stage);
-    c->h_stage = nullptr;
-    c->stage_cap = 0;
-    size_t cap = std::max<size_t>(bytes, 1 << 16);
-    ck(cudaMallocHost(&c->h_stage, cap), "cudaMallocHost");
-    c->stage_cap = cap;
-    g_alloc_gen.fetch_add(1);  // captured copies read from h_stage
-  }
-  std::memcpy(c->h_stage, src, bytes);
-  ck(cudaMemcpyAsync(dst, c->h_stage, bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
-  // (while capturing, the record would become a graph node and the event
-  // could no longer be waited on from the host; mrc_step records it itself)
-  if (!c->capturing) ck(cudaEventRecord(c->stage_done, c->stream), "event");
-}
 
 void reset_downstream(refsig_gpu_ctx* c) {
   c->have_ref = c->signed_ = c->have_fp = c->have_x = c->have_inv_norm = false;
@@ -1083,6 +1053,8 @@ static void do_count(refsig_gpu_ctx* ctx, int weight_mode) {
   // ~32 MB of replicas, 1..32 copies: 32 at configs[1] (measured: 1 copy 283 us, 2: 165, 4: 113, 16: 98,
   // 32: 95.5, 64: 97 us for K1), 16 at configs[3], 8 at configs[4]
   const uint32_t reps = reps_env ? reps_env : std::max<uint32_t>(1u, std::min<uint32_t>(32u, (8u << 20) / V));
+  // zeroed right before K1 (measured: zeroing them in the idf kernel of the previous count
+  // instead left the lines cold in L2 — K1's atomics then missed, count 90 -> 125 us)
   ctx->df_rep.ensure(sizeof(uint32_t) * static_cast<size_t>(V) * reps);
   ck(cudaMemsetAsync(ctx->df_rep.p, 0, sizeof(uint32_t) * static_cast<size_t>(V) * reps, ctx->stream), "memset df");
   CountArgs a{ctx->tok, ctx->doc_off.as<uint64_t>(), V, ctx->ent.as<uint2>(), ctx->nnz.as<uint32_t>(),
@@ -1100,9 +1072,15 @@ static void do_count(refsig_gpu_ctx* ctx, int weight_mode) {
   launch_count_group(1, a, ctx->plan_list(P::kPlanG1), ctx->plan_n[P::kPlanG1], m0);
   launch_count_group(0, a, ctx->plan_list(P::kPlanG0), ctx->plan_n[P::kPlanG0], m0);
   launch_count_group(-1, a, ctx->plan_list(P::kPlanW16), ctx->plan_n[P::kPlanW16], ctx->side[1]);
+#ifdef REFSIG_K1_WARP_BIG_FIRST
+  launch_count_warp(8, a, ctx->plan_list(P::kPlanW8), ctx->plan_n[P::kPlanW8], ctx->side[0]);
+  launch_count_warp(4, a, ctx->plan_list(P::kPlanW4), ctx->plan_n[P::kPlanW4], ctx->side[0]);
+  launch_count_warp(2, a, ctx->plan_list(P::kPlanTiny), ctx->plan_n[P::kPlanTiny], ctx->side[0]);
+#else
   launch_count_warp(2, a, ctx->plan_list(P::kPlanTiny), ctx->plan_n[P::kPlanTiny], ctx->side[0]);
   launch_count_warp(4, a, ctx->plan_list(P::kPlanW4), ctx->plan_n[P::kPlanW4], ctx->side[0]);
   launch_count_warp(8, a, ctx->plan_list(P::kPlanW8), ctx->plan_n[P::kPlanW8], ctx->side[0]);
+#endif
   launch_count_large(a, ctx->plan_list(P::kPlanLong), ctx->long_off.as<uint64_t>(), ctx->plan_n[P::kPlanLong],
                      ctx->long_scratch.as<uint32_t>(), ctx->side[0]);
   for (int k = 0; k < 3; ++k) {  // join
@@ -1117,8 +1095,7 @@ static void do_count(refsig_gpu_ctx* ctx, int weight_mode) {
     // Query mode: the database's IDF and reference rows (configs[4]); the
     // query batch keeps its own df.
     ck(cudaStreamSynchronize(db->stream), "sync database");
-    ck(cudaMemcpyAsync(ctx->info.p, db->info.p, sizeof(TermInfo) * V, cudaMemcpyDeviceToDevice, ctx->stream),
-       "copy database idf");
+    launch_copy_words(db->info.as<uint32_t>(), 2ull * V, ctx->info.as<uint32_t>(), ctx->stream);  // TermInfo = 2 words
     ctx->weight_mode = db->weight_mode;
   }
   launched("count");
@@ -1227,15 +1204,15 @@ static uint64_t stage_reference_docs(refsig_gpu_ctx* ctx, const uint32_t* ref_do
     require(ref_doc_ids[k] < ctx->n_docs, "reference doc id >= n_docs");
     u_cap += ctx->h_off[ref_doc_ids[k] + 1] - ctx->h_off[ref_doc_ids[k]];
   }
-  ctx->ref_docs.ensure(4ull * K);
-  launch_param_words(ref_doc_ids, K, ctx->ref_docs.as<uint32_t>(), ctx->stream);  // K <= kParamWords
+  ctx->ref_ids.assign(ref_doc_ids, ref_doc_ids + K);  // kernel parameters of the reference build
   return u_cap;
 }
 
 static void build_reference_docs(refsig_gpu_ctx* ctx, uint32_t K, uint64_t u_cap) {
   require(ctx->counted, "count() not called");
-  RefArgs r{K,     nullptr, nullptr, ctx->ent.as<uint2>(), false, ref_row_stride(K), ctx->ref_docs.as<uint32_t>(),
-            ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>()};
+  RefArgs r{K, nullptr, nullptr, ctx->ent.as<uint2>(), false, ref_row_stride(K), ctx->doc_off.as<uint64_t>(),
+            ctx->nnz.as<uint32_t>(), {}};
+  std::copy(ctx->ref_ids.begin(), ctx->ref_ids.end(), r.ids);
   build_reference(ctx, r, u_cap);
 }
 
@@ -1292,7 +1269,7 @@ static void do_set_reference_table(refsig_gpu_ctx* ctx, uint32_t K, const uint64
   ck(cudaMemcpyAsync(ctx->ref_start.p, start.data(), 8ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D");
   ck(cudaMemcpyAsync(ctx->ref_n.p, cnt.data(), 4ull * K, cudaMemcpyHostToDevice, ctx->stream), "H2D");
   RefArgs r{K, ctx->ref_start.as<uint64_t>(), ctx->ref_n.as<uint32_t>(), ctx->ref_ent.as<uint2>(), !from_counts,
-            ref_row_stride(K), nullptr, nullptr, nullptr};
+            ref_row_stride(K), nullptr, nullptr, {}};
   build_reference(ctx, r, n);
   ck(cudaStreamSynchronize(ctx->stream), "reference");
 }
@@ -1556,7 +1533,7 @@ int refsig_gpu_exact_pairs(refsig_gpu_ctx* ctx, float tau_cos, uint64_t* out_pai
     require(out_count != nullptr, "out_count is NULL");
     require(tau_cos > 0.0f && tau_cos <= 1.0f, "tau_cos must be in (0, 1]");
     require(capacity == 0 || out_pairs != nullptr, "out_pairs is NULL");
-    const uint32_t N = ctx->n_docs, V = ctx->vocab;
+    const uint32_t N = ctx->n_docs;
     const uint32_t H = prepare_exact(ctx);
     const PairGrid g = self_grid(ctx);
     {
@@ -1857,7 +1834,6 @@ int refsig_gpu_mrc_step(refsig_gpu_ctx* ctx, int weight_mode, const uint32_t* re
     ctx->capturing = false;
     ctx->prof = prof;
     ck(e, "stream capture");
-    if (ctx->stage_done) ck(cudaEventRecord(ctx->stage_done, ctx->stream), "event");
     e = cudaGraphInstantiate(&ctx->step_exec, graph, 0);
     cudaGraphDestroy(graph);
     ck(e, "cudaGraphInstantiate");

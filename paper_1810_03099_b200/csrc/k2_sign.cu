@@ -26,13 +26,13 @@ namespace refsig_gpu {
 namespace {
 
 __device__ __forceinline__ void ref_range(const RefArgs& r, uint32_t k, const uint2*& e, uint32_t& n) {
-  if (r.docs) {
-    const uint32_t d = r.docs[k];
-    e = r.ent + r.doc_off[d];
-    n = r.nnz[d];
-  } else {
+  if (r.start) {
     e = r.ent + r.start[k];
     n = r.n[k];
+  } else {
+    const uint32_t d = r.ids[k];
+    e = r.ent + r.doc_off[d];
+    n = r.nnz[d];
   }
 }
 

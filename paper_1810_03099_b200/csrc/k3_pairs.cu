@@ -527,6 +527,25 @@ __global__ void words_to_host_kernel(const uint32_t* __restrict__ src, uint32_t 
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
+// Device-to-device copy on the SMs (a cudaMemcpyAsync D2D would take a copy
+// engine, where it can queue behind a staged host upload).
+__global__ void copy_words_kernel(const uint32_t* __restrict__ src, uint64_t n, uint32_t* __restrict__ dst) {
+  const uint64_t n4 = n / 4;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) d4[i] = s4[i];
+  for (uint64_t i = n4 * 4 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    dst[i] = src[i];
+}
+
+void launch_copy_words(const uint32_t* src, uint64_t n, uint32_t* dst, cudaStream_t s) {
+  if (!n) return;
+  const uint64_t blocks = std::min<uint64_t>(ceil_div(n, 1024), 148ull * 8);
+  copy_words_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(src, n, dst);
+  note_launch();
+}
+
 void launch_words_to_host(const uint32_t* src, uint32_t n, uint32_t* mapped_dst, cudaStream_t s) {
   words_to_host_kernel<<<1, 32, 0, s>>>(src, n, mapped_dst);
   note_launch();

@@ -91,9 +91,9 @@ struct RefArgs {
   const uint2* ent;
   bool explicit_w;
   uint32_t Kp;  // row stride of R: roundup(K,4) for K <= 32, roundup(K,32) above (k2_sign.cu)
-  const uint32_t* docs;
-  const uint64_t* doc_off;
+  const uint64_t* doc_off;  // with nnz and ids: reference k = document ids[k] of the corpus
   const uint32_t* nnz;
+  uint32_t ids[256];  // by value (kernel parameter: no upload before the reference build); K <= 256
 };
 // info[t].ref_row = -1 for all t (only needed when a reference is replaced).
 void launch_ref_reset(TermInfo* info, uint32_t vocab, cudaStream_t s);
@@ -170,6 +170,8 @@ void launch_rebase_rowptr(const uint64_t* in, uint64_t n, uint64_t* out, cudaStr
 // n <= kParamWords host words to the device as kernel parameters (no copy engine).
 constexpr uint32_t kParamWords = 256;
 void launch_param_words(const uint32_t* host_src, uint32_t n, uint32_t* dst, cudaStream_t s);
+// n words device -> device by a kernel (16-byte aligned pointers).
+void launch_copy_words(const uint32_t* src, uint64_t n, uint32_t* dst, cudaStream_t s);
 // n device words into mapped pinned host memory (device pointer of it) by a kernel.
 void launch_words_to_host(const uint32_t* src, uint32_t n, uint32_t* mapped_dst, cudaStream_t s);
 

@@ -144,3 +144,60 @@ def test_doc_shards_cover_and_balance():
         assert sh[0][0] == 0 and sh[-1][1] == cp.n_docs and all(b == c for (_, b), (c, _) in zip(sh, sh[1:]))
         toks = [int(cp.doc_off[hi]) - int(cp.doc_off[lo]) for lo, hi in sh]
         assert max(toks) <= sum(toks) / w * 1.1 + 5000
+
+
+def _weak_worker(rank, world, port, q):
+    """bench.py --gpus N (weak scaling): rank r runs its own batch, a seeded
+    document permutation of the corpus; the helpers reduce over ranks."""
+    import torch.distributed as dist
+
+    import bench
+    import oracle
+    from paper_1810_03099_b200 import corpus as C
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cp, _ = C.config_corpus("c0")
+    cp = cp.slice_docs(500)
+    refs = C.sample_refs(0, cp.n_docs, 10)
+    tok, off, rrefs = bench.permuted_batches(cp, refs, 1, seed=1000 + rank)[0]
+    o = oracle.mrc_pipeline(np.asarray(tok), off, cp.vocab, rrefs)
+    pairs, _ = oracle.mrc_pairs(o.S, 0.95, 1e-5, threads=1)
+    # map the batch's pairs back to original document ids: the same set as the unpermuted corpus
+    lens = np.diff(cp.doc_off).astype(np.int64)
+    perm = np.empty(cp.n_docs, np.int64)
+    # the batch's permutation (bench.permuted_batches draws it from the same seed): document p of
+    # the batch is original document perm[p]
+    rng = np.random.default_rng(1000 + rank)
+    perm[:] = rng.permutation(cp.n_docs)
+    assert np.array_equal(np.diff(off).astype(np.int64), lens[perm])
+    i = perm[(pairs >> np.uint64(32)).astype(np.int64)]
+    j = perm[(pairs & np.uint64(0xFFFFFFFF)).astype(np.int64)]
+    orig = np.sort((np.minimum(i, j).astype(np.uint64) << np.uint64(32)) | np.maximum(i, j).astype(np.uint64))
+    mx = bench.allreduce(dist, [float(rank + 1), 7.0], None, "max")
+    sm = bench.allreduce(dist, [float(len(pairs))], None, "sum")
+    if rank == 0:
+        o0 = oracle.mrc_pipeline(cp.tokens, cp.doc_off, cp.vocab, refs)
+        ref_pairs, _ = oracle.mrc_pairs(o0.S, 0.95, 1e-5, threads=1)
+        q.put((orig.tobytes(), ref_pairs.tobytes(), mx, sm, len(ref_pairs)))
+    else:
+        q.put((orig.tobytes(), None, mx, sm, None))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_weak_scaling_batches():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_weak_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = next(r for r in res if r[1] is not None)
+    for orig, _, mx, sm, _ in res:
+        assert orig == ref[1]  # every rank's batch is the same work (same pair set up to the permutation)
+        assert mx == [2.0, 7.0] and sm == [2.0 * ref[4]]
