@@ -108,6 +108,13 @@ struct TcArgs {
   uint32_t* rowcnt;
   uint32_t two;  // 2, as data (see fma_pipe_shift_in)
   uint32_t dbg;  // timing experiments only (REFSIG_TC_DEBUG): 1 no epilogue math, 2 no B refill, 4 no MMA
+  // rectangle (query x database) only: stripe-major walk. Item i = (column
+  // stripe i / n_groups of `stripe` column blocks, row group i % n_groups);
+  // CTA b takes items b, b + grid, ... so at any time the CTAs work on one or
+  // two stripes and each B panel comes from DRAM about once (with contiguous
+  // tile ranges per CTA every row group re-read the whole database from DRAM).
+  uint32_t stripe;    // column blocks per stripe; 0 = contiguous tile ranges
+  uint32_t n_groups;  // row groups of this call
 };
 
 // Row group p = row blocks rb0 + rb*p (.. + rb - 1): A resident in smem while
@@ -130,8 +137,20 @@ __device__ __forceinline__ bool tc_rvalid(const TcArgs& a, uint32_t p, uint32_t 
 
 template <uint32_t FS>
 struct TileWalk {
-  uint32_t p, c;
+  uint32_t p, c;        // row group, column block relative to tc_cs (absolute for a rectangle)
+  uint32_t item, cend;  // stripe-major walk: current item, end column of its stripe
+  __device__ void set_item(const TcArgs& a) {
+    const uint32_t st = item / a.n_groups;
+    p = item % a.n_groups;
+    c = st * a.stripe;
+    cend = min(c + a.stripe, a.nbc);
+  }
   __device__ void start(const TcArgs& a, uint64_t t) {
+    if (a.stripe) {
+      item = blockIdx.x;
+      set_item(a);
+      return;
+    }
     p = 0;
     while (t >= tc_ct<FS>(a, p)) {
       t -= tc_ct<FS>(a, p);
@@ -139,8 +158,16 @@ struct TileWalk {
     }
     c = static_cast<uint32_t>(t);
   }
-  // returns true when the next tile starts a new row group
+  // returns true when the next tile starts a new row group (stripe-major: a new item)
   __device__ bool next(const TcArgs& a) {
+    if (a.stripe) {
+      if (++c == cend) {
+        item += gridDim.x;
+        set_item(a);
+        return true;
+      }
+      return false;
+    }
     if (++c == tc_ct<FS>(a, p)) {
       c = 0;
       ++p;
@@ -149,6 +176,17 @@ struct TileWalk {
     return false;
   }
 };
+
+// Tiles of this CTA in the stripe-major walk.
+__device__ __forceinline__ uint32_t tc_striped_tiles(const TcArgs& a) {
+  const uint32_t ns = (a.nbc + a.stripe - 1) / a.stripe;
+  uint32_t n = 0;
+  for (uint32_t i = blockIdx.x; i < a.n_groups * ns; i += gridDim.x) {
+    const uint32_t c0 = (i / a.n_groups) * a.stripe;
+    n += min(a.stripe, a.nbc - c0);
+  }
+  return n;
+}
 
 // Tile = rb*128 rows (row group: A panels resident) x 128 columns (one B
 // panel per tile, streamed through S stages in 64-wide K chunks, so
@@ -168,7 +206,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
   // MMA issuers keep descriptors and counters in uniform registers
   const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
   const uint64_t t0 = a.n_tiles * blockIdx.x / gridDim.x, t1 = a.n_tiles * (blockIdx.x + 1) / gridDim.x;
-  const uint32_t n_it = static_cast<uint32_t>(t1 - t0);
+  const uint32_t n_it = a.stripe ? tc_striped_tiles(a) : static_cast<uint32_t>(t1 - t0);
   const uint32_t PB = 256u * a.KP;  // bytes per operand panel
   // B ring(s): every ring has ONE consumer taking its fills in order (with two
   // consumers of a shared ring, one could wait on a stage's fill k while fill
@@ -616,6 +654,19 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
   a.bitmap = bitmap;
   a.rowcnt = rowcnt;
   a.two = 2;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(T, static_cast<uint64_t>(sms)));
+  // rectangle with a database wider than a few column blocks per CTA: stripe-major walk.
+  // REFSIG_TC_STRIPE: 0 never, 1 for every rectangle (tests), unset = when nbc >= 8 * grid
+  static const int stripe_mode = [] {
+    const char* m = std::getenv("REFSIG_TC_STRIPE");
+    return m ? std::atoi(m) : -1;
+  }();
+  a.n_groups = static_cast<uint32_t>(ceil_div(a.rb1 - a.rb0, a.rb));
+  if (!g.triangle && stripe_mode != 0 && (stripe_mode == 1 || (a.n_groups >= 2 && a.nbc >= 8ull * grid)))
+    a.stripe = static_cast<uint32_t>(ceil_div(a.nbc, grid));
   static const uint32_t dbg = [] {
     const char* m = std::getenv("REFSIG_TC_DEBUG");
     return m ? static_cast<uint32_t>(std::atoi(m)) : 0u;
@@ -637,10 +688,6 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
     default: kern = mrc_tc_kernel<0>; break;
   }
   ensure_smem(kern, smem);
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(T, static_cast<uint64_t>(sms)));
 #ifdef REFSIG_TC_TRACE
   if (dbg & 8) {
     static bool dumped = false;
@@ -655,10 +702,10 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
   if (std::getenv("REFSIG_TC_PRINT"))
     std::fprintf(stderr,
                  "mrc_tc: KP %u nch %u last %u CB %u rb %u abufs %u stages %u smem %zu grid %u tiles %llu rows %u cols "
-                 "%u wpr %u tri %d rb0 %u rb1 %u nbc %u Ar %p Bc %p bitmap %p\n",
+                 "%u wpr %u tri %d rb0 %u rb1 %u nbc %u stripe %u groups %u Ar %p Bc %p bitmap %p\n",
                  a.KP, a.nch, a.last_steps, a.CB, a.rb, a.abufs, a.stages, smem, grid,
                  static_cast<unsigned long long>(a.n_tiles), g.n_rows, g.n_cols, g.words_per_row, g.triangle ? 1 : 0,
-                 a.rb0, a.rb1, a.nbc, static_cast<const void*>(a.Ar), static_cast<const void*>(a.Bc),
+                 a.rb0, a.rb1, a.nbc, a.stripe, a.n_groups, static_cast<const void*>(a.Ar), static_cast<const void*>(a.Bc),
                  static_cast<void*>(a.bitmap));
   launch_pdl(kern, dim3(grid), dim3(kTcThreads), smem, s, a);
 #ifdef REFSIG_TC_TRACE

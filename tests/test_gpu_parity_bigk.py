@@ -6,6 +6,10 @@ orc_mrc_query_pairs, fp64).
 
 Bar: candidate sets identical except pairs whose oracle score is within 1e-5
 of tau, which the oracle lists (tests/parity_util.py)."""
+import os
+import subprocess
+import sys
+
 import numpy as np
 import pytest
 
@@ -129,3 +133,42 @@ def test_evaluate_large_k_vs_oracle(gpu_ctx_factory, K):
         assert abs(g[k] - ref[k]) <= 2e-6 + 1e-5 * abs(ref[k]), (k, g[k], ref[k])
     for k in ("mrc_variance", "simhash_variance"):
         assert abs(g[k] - ref[k]) <= 1e-7 + 1e-4 * abs(ref[k]), (k, g[k], ref[k])
+
+
+_STRIPE_SNIPPET = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, {repo!r})
+import paper_1810_03099_b200 as R
+from paper_1810_03099_b200 import corpus as C
+cfg = C.load_configs()["configs"]["c4"]
+db_spec = dict(cfg["corpus"], n_docs=6000, vocab=50000)
+q_spec = dict(cfg["queries"], n_docs=700, vocab=50000)
+db = C.generate(db_spec)
+q = C.generate_queries(q_spec, db_spec, db)
+refs = C.sample_refs(0, db.n_docs, {K})
+with R.Context(0) as dbc, R.Context(0) as qc:
+    dbc.load_corpus(db.tokens, db.doc_off, db.vocab); dbc.count(); dbc.set_reference_docs(refs); dbc.sign(fetch=False)
+    qc.set_k3_path(R.K3_TENSOR)
+    qc.attach_database(dbc)
+    qc.load_corpus(q.tokens, q.doc_off, q.vocab); qc.count(); qc.sign(fetch=False)
+    keys = qc.mrc_query_pairs(0.9)
+print(len(keys), hashlib.sha256(np.ascontiguousarray(keys).tobytes()).hexdigest())
+"""
+
+
+@pytest.mark.parametrize("K", [20, 128])
+def test_query_join_stripe_walk_equals_contiguous(K):
+    """The stripe-major tile walk of the query rectangle (k3_tc.cu TileWalk,
+    forced on with REFSIG_TC_STRIPE=1) gives the same candidate keys as the
+    contiguous walk (REFSIG_TC_STRIPE=0), both paths of the tcgen05 kernel
+    (K' <= 128 with two row blocks, chunked K' = 400)."""
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _STRIPE_SNIPPET.format(repo=repo, K=K)
+    out = {}
+    for mode in ("0", "1"):
+        env = dict(os.environ, REFSIG_TC_STRIPE=mode)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[mode] = r.stdout.strip().splitlines()[-1]
+    assert out["0"] == out["1"] and int(out["0"].split()[0]) > 0, out
