@@ -451,6 +451,78 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
   }
 }
 
+// Few wide rows (a query batch against a large database: 10k rows of 31k
+// words at configs[4]): warp-per-row leaves ~1.2 rows per warp and a 2-row
+// tail. Here a CTA takes a row and its 8 warps take consecutive 128-word
+// batches in rounds (warp w: batch 8r + w); a round's output offsets come
+// from the warps' batch totals through shared memory, then each warp expands
+// its batch exactly as emit_kernel does (direct stores for sparse slices,
+// staged coalesced stores for dense ones).
+__global__ void __launch_bounds__(256) emit_wide_kernel(const uint32_t* __restrict__ bitmap, PairGrid g,
+                                                        const uint32_t* __restrict__ rowcnt,
+                                                        const uint64_t* __restrict__ rowstart,
+                                                        uint32_t* __restrict__ out, uint64_t capacity,
+                                                        uint32_t direct_max) {
+  __shared__ uint32_t stage_all[kEmitWarps][1024];
+  __shared__ uint32_t wtot[2][kEmitWarps];
+  pdl_wait();
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t* stage = stage_all[wid];
+  const uint32_t i = g.row_begin + blockIdx.x;
+  if (i >= g.row_end || rowcnt[i] == 0) return;  // CTA-uniform
+  const uint32_t wpr = g.words_per_row;
+  uint64_t row_base = rowstart[i];
+  const uint32_t* row = bitmap + static_cast<size_t>(i) * wpr;
+  const uint32_t c_first = g.triangle ? (i / kTile) * 4 : 0;
+  uint32_t par = 0;
+  for (uint32_t r0 = c_first; r0 < wpr; r0 += 128 * kEmitWarps, par ^= 1) {
+    const uint32_t c = r0 + 128 * wid;
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = c + 32 * k + lane < wpr ? row[c + 32 * k + lane] : 0u;
+    const uint32_t p01 = warp_inclusive_scan(__popc(w[0]) | (__popc(w[1]) << 16), static_cast<int>(lane));
+    const uint32_t p23 = warp_inclusive_scan(__popc(w[2]) | (__popc(w[3]) << 16), static_cast<int>(lane));
+    const uint32_t t01 = __shfl_sync(0xffffffffu, p01, 31), t23 = __shfl_sync(0xffffffffu, p23, 31);
+    if (lane == 0) wtot[par][wid] = (t01 & 0xffffu) + (t01 >> 16) + (t23 & 0xffffu) + (t23 >> 16);
+    __syncthreads();  // (wtot double-buffered by round parity: one barrier per round)
+    uint64_t base = row_base;
+    uint32_t round_total = 0;
+#pragma unroll
+    for (uint32_t u = 0; u < kEmitWarps; ++u) {
+      const uint32_t x = wtot[par][u];
+      base += u < wid ? x : 0u;
+      round_total += x;
+    }
+    row_base += round_total;
+    if ((t01 | t23) == 0) continue;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t pk = k < 2 ? p01 : p23, tk = k < 2 ? t01 : t23, sh = (k & 1) * 16;
+      const uint32_t inc = (pk >> sh) & 0xffffu, tot = (tk >> sh) & 0xffffu;
+      if (tot == 0) continue;
+      uint32_t word = w[k];
+      const uint32_t ex = inc - __popc(word);
+      const uint32_t col = (c + 32 * k + lane) * 32u;
+      if (base + tot > capacity) {  // overflow: exact positions, writes below capacity only
+        uint64_t pos = base + ex;
+        for (; word; word &= word - 1, ++pos)
+          if (pos < capacity) out[pos] = col + (__ffs(word) - 1);
+      } else if (tot <= direct_max) {
+        uint32_t* o = out + base + ex;
+        for (; word; word &= word - 1) *o++ = col + (__ffs(word) - 1);
+      } else {
+        uint32_t o = ex;
+        for (; word; word &= word - 1) stage[o++] = col + (__ffs(word) - 1);
+        __syncwarp();
+        uint32_t* dst = out + base;
+        for (uint32_t e = lane; e < tot; e += 32) dst[e] = stage[e];
+        __syncwarp();
+      }
+      base += tot;
+    }
+  }
+}
+
 // keys[k] = (i << 32) | cols[k] for the pairs of row i (warp per row).
 __global__ void __launch_bounds__(256) cols_to_keys_kernel(const uint64_t* __restrict__ rowstart, uint32_t row_begin,
                                                            uint32_t row_end, const uint32_t* __restrict__ cols,
@@ -623,7 +695,8 @@ void launch_emit_pairs(const uint32_t* bitmap, const PairGrid& g, const uint32_t
   if (g.row_end <= g.row_begin) return;
   // one row per warp; persistent warps (at most 7 CTAs of 8 warps per SM, 32 KB
   // of stages each) when there are many more rows than resident warps
-  const uint64_t need = ceil_div(g.row_end - g.row_begin, kEmitWarps);
+  const uint64_t rows = g.row_end - g.row_begin;
+  const uint64_t need = ceil_div(rows, kEmitWarps);
   const uint64_t resident = static_cast<uint64_t>(sms()) * 7;
   const int persistent = need > 4 * resident ? 1 : 0;
   const uint64_t blocks = persistent ? resident : need;
@@ -631,6 +704,20 @@ void launch_emit_pairs(const uint32_t* bitmap, const PairGrid& g, const uint32_t
     const char* m = std::getenv("REFSIG_EMIT_DIRECT");
     return m ? static_cast<uint32_t>(std::atoi(m)) : kEmitDirect;
   }();
+  // few rows of many batches each (fewer than ~2 rows per resident warp, >= 8 batches per row):
+  // a CTA per row (REFSIG_EMIT_WIDE=0/1 forces the choice, for measurement and tests)
+  static const int wide_mode = [] {
+    const char* m = std::getenv("REFSIG_EMIT_WIDE");
+    return m ? std::atoi(m) : -1;
+  }();
+  const bool wide = wide_mode == 1 ||
+                    (wide_mode != 0 && rows < 2 * resident * kEmitWarps && g.words_per_row >= 128u * kEmitWarps);
+  if (wide) {
+    launch_pdl(emit_wide_kernel, dim3(static_cast<unsigned>(rows)), dim3(32 * kEmitWarps), 0, s, bitmap, g, rowcnt,
+               rowstart, out, capacity, direct_max);
+    note_launch();
+    return;
+  }
   launch_pdl(emit_kernel, dim3(static_cast<unsigned>(blocks)), dim3(32 * kEmitWarps), 0, s, bitmap, g, rowcnt,
              rowstart, out, capacity, counter, persistent, direct_max);
   note_launch();

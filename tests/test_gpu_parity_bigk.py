@@ -172,3 +172,39 @@ def test_query_join_stripe_walk_equals_contiguous(K):
         assert r.returncode == 0, r.stderr[-2000:]
         out[mode] = r.stdout.strip().splitlines()[-1]
     assert out["0"] == out["1"] and int(out["0"].split()[0]) > 0, out
+
+
+_EMIT_SNIPPET = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, {repo!r})
+import paper_1810_03099_b200 as R
+from paper_1810_03099_b200 import corpus as C
+h = hashlib.sha256()
+cp, cfg = C.config_corpus("c1")
+cp = cp.slice_docs(6000)
+refs = C.sample_refs(cfg["ref_seed"], cp.n_docs, cfg["K"])
+with R.Context(0) as c:
+    c.load_corpus(cp.tokens, cp.doc_off, cp.vocab); c.count(); c.set_reference_docs(refs); c.sign(fetch=False)
+    for tau in (0.9, 0.99):
+        k = c.mrc_pairs(tau); h.update(np.ascontiguousarray(k).tobytes()); print(len(k))
+    c.simhash(0)
+    k = c.hamming_pairs(12); h.update(np.ascontiguousarray(k).tobytes()); print(len(k))
+print(h.hexdigest())
+"""
+
+
+def test_emit_wide_rows_equals_warp_per_row():
+    """The CTA-per-row emitter for few wide rows (k3_pairs.cu emit_wide_kernel,
+    forced with REFSIG_EMIT_WIDE=1) writes the same sorted candidates as the
+    warp-per-row emitter (REFSIG_EMIT_WIDE=0): MRC at two thresholds (sparse
+    and dense rows) and a Hamming join."""
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _EMIT_SNIPPET.format(repo=repo)
+    out = {}
+    for mode in ("0", "1"):
+        env = dict(os.environ, REFSIG_EMIT_WIDE=mode)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[mode] = r.stdout.strip().splitlines()
+    assert out["0"] == out["1"] and int(out["0"][0]) > 0, out
