@@ -1006,12 +1006,23 @@ def rival_rooflines(rv, N, pairs, cp, peaks, peaks_src, n_sm, clock_mhz):
                                "(8 int8 byte-plane MMAs per 32 nonzeros) add L2 and tensor work on top",
                        "fingerprints_per_sec": N / (ts / 1e3) if ts else None}}
     th = rv["hamming_tiles_ms"]
-    # K4b: one 64-bit XOR + popcount (2 POPC) per pair; POPC pipe 16/clk/SM (profiles/alu_peaks)
+    # K4b on the tensor cores (k3_tc.cu kind::i8): s_a . s_b over +-1 int8 operands = 64 - 2 hd, the
+    # threshold folded in, K' = 96 int8 per pair row; executed int8 ops per computed 128x128 block =
+    # 2 * 96 * 128 * 128. Peak: B200 dense int8 = 2x dense bf16 (nominal 4.5 vs 2.25 P), applied to the
+    # measured bf16 figure. The POPC-pipe bound of the CUDA-core kernel (REFSIG_HAMMING=cuda) beside it.
+    nb = (N + 127) // 128
+    blocks = nb * (nb + 1) // 2
+    ops = blocks * 2 * 96 * 128 * 128
+    i8_peak = 2 * peaks.get("bf16_tflops", 2250.0)
+    ach = ops / (th / 1e3) / 1e12 if th else 0.0
     popc_peak = n_sm * 16 * clock_mhz * 1e6 / 2 / 1e12  # 1e12 pairs/s
-    ach = pairs / (th / 1e3) / 1e12 if th else 0.0
-    out["hamming_tiles"] = {"bound": "popc", "achieved": ach, "peak": popc_peak, "unit": "Tpairs/s",
-                            "frac": ach / popc_peak if popc_peak else None, "ms_per_launch": th,
-                            "peak_source": f"{n_sm} SMs x 16 POPC/clk / 2 per 64-bit pair x {clock_mhz:.0f} MHz",
+    out["hamming_tiles"] = {"bound": "tensor", "achieved": ach, "peak": i8_peak, "unit": "TOPS (int8)",
+                            "frac": ach / i8_peak if i8_peak else None, "ms_per_launch": th,
+                            "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (B200 dense int8 = 2x bf16)",
+                            "pairs_per_sec": pairs / (th / 1e3) if th else None,
+                            "popc_bound_pairs_per_sec": popc_peak * 1e12,
+                            "note": "phase = int8 forms kernel + tcgen05 kind::i8 tile kernel; the CUDA-core "
+                                    "XOR/POPC kernel's bound is popc_bound_pairs_per_sec",
                             "emit_ms": rv["hamming_emit_ms"], "candidates": rv["hamming_pairs"],
                             "doc_pairs_per_sec": pairs / ((th + rv["hamming_emit_ms"]) / 1e3)}
     return out

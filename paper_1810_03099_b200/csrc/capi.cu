@@ -221,6 +221,7 @@ struct refsig_gpu_ctx {
   DevBuf cf_rep, cf;                                                           // corpus frequencies
   DevBuf records;                                                              // MRCS records
   DevBuf tc_forms;                                                             // K3 tcgen05 operand forms
+  DevBuf ham_forms;                                                            // Hamming int8 forms (tcgen05 kind::i8)
 
   // staged batches (refsig_gpu_stage_corpus / swap_corpus), up to kStageDepth
   // ahead in a ring: tokens and the work plan (built on the host at stage time)
@@ -313,7 +314,7 @@ struct refsig_gpu_ctx {
             {"text_cnt", &text_cnt}, {"fp", &fp}, {"term_hash", &term_hash}, {"x", &x}, {"post_off", &post_off},
             {"posts", &posts}, {"head_col", &head_col}, {"headA", &headA},
             {"head_norm", &head_norm}, {"entpos", &entpos}, {"csc_ka", &csc_ka}, {"csc_kb", &csc_kb},
-            {"csc_va", &csc_va}, {"csc_vb", &csc_vb}, {"csc_doc", &csc_doc}, {"csc_tmp", &csc_tmp}, {"headAT", &headAT}, {"eval_tail", &eval_tail},
+            {"ham_forms", &ham_forms}, {"csc_va", &csc_va}, {"csc_vb", &csc_vb}, {"csc_doc", &csc_doc}, {"csc_tmp", &csc_tmp}, {"headAT", &headAT}, {"eval_tail", &eval_tail},
             {"eval_part", &eval_part}, {"cf_rep", &cf_rep}, {"cf", &cf}, {"records", &records},
             {"tc_forms", &tc_forms}, {"fetch_rowptr0", &fetch_rowptr[0]}, {"fetch_rowptr1", &fetch_rowptr[1]},
             {"fetch_cols0", &fetch_cols[0]}, {"fetch_cols1", &fetch_cols[1]}};
@@ -1504,6 +1505,31 @@ int refsig_gpu_get_fingerprints(refsig_gpu_ctx* ctx, uint64_t* fp) {
   });
 }
 
+// Hamming tiles into ctx's bitmap / row counts: on the tensor cores (int8 +-1
+// forms, kind::i8) unless REFSIG_HAMMING=cuda selects the POPC kernel.
+static void hamming_tiles(refsig_gpu_ctx* c, const uint64_t* f_rows, uint32_t n_rows, const uint64_t* f_cols,
+                          uint32_t n_cols, int max_dist, const PairGrid& g) {
+  static const bool cuda_cores = [] {
+    const char* m = std::getenv("REFSIG_HAMMING");
+    return m && std::strcmp(m, "cuda") == 0;
+  }();
+  if (cuda_cores) {
+    launch_hamming_bitmap(f_rows, f_cols, max_dist, g, c->bitmap.as<uint32_t>(), c->rowcnt.as<uint32_t>(), c->stream);
+    return;
+  }
+  const size_t rb = ham_tc_form_bytes(n_rows), cb = ham_tc_form_bytes(n_cols);
+  c->ham_forms.ensure(rb + cb);
+  void* rowf = c->ham_forms.p;
+  void* colf = c->ham_forms.as<char>() + rb;
+  if (f_rows == f_cols) {  // self join: both forms in one pass (they differ in the threshold byte)
+    launch_ham_tc_forms(f_rows, n_rows, max_dist, rowf, colf, c->stream);
+  } else {
+    launch_ham_tc_forms(f_rows, n_rows, max_dist, rowf, nullptr, c->stream);
+    launch_ham_tc_forms(f_cols, n_cols, max_dist, nullptr, colf, c->stream);
+  }
+  launch_ham_tc(rowf, colf, g, c->bitmap.as<uint32_t>(), c->rowcnt.as<uint32_t>(), c->stream);
+}
+
 int refsig_gpu_hamming_pairs(refsig_gpu_ctx* ctx, int max_dist, uint64_t* out_pairs, uint64_t capacity,
                              uint64_t* out_count) {
   int rc2 = REFSIG_OK;
@@ -1516,8 +1542,7 @@ int refsig_gpu_hamming_pairs(refsig_gpu_ctx* ctx, int max_dist, uint64_t* out_pa
     {
       Phase ph_tiles(ctx, REFSIG_PHASE_PAIR_TILES);
       prepare_bitmap(ctx, g, false);
-      launch_hamming_bitmap(ctx->fp.as<uint64_t>(), ctx->fp.as<uint64_t>(), max_dist, g, ctx->bitmap.as<uint32_t>(),
-                            ctx->rowcnt.as<uint32_t>(), ctx->stream);
+      hamming_tiles(ctx, ctx->fp.as<uint64_t>(), ctx->n_docs, ctx->fp.as<uint64_t>(), ctx->n_docs, max_dist, g);
       launched("hamming bitmap");
     }
     rc2 = run_emit(ctx, g, out_pairs, capacity, out_count);
@@ -1709,8 +1734,7 @@ int refsig_gpu_hamming_query_pairs(refsig_gpu_ctx* q, int max_dist, uint64_t* ou
     {
       Phase ph_tiles(q, REFSIG_PHASE_PAIR_TILES);
       prepare_bitmap(q, g, false);
-      launch_hamming_bitmap(q->fp.as<uint64_t>(), db->fp.as<uint64_t>(), max_dist, g, q->bitmap.as<uint32_t>(),
-                            q->rowcnt.as<uint32_t>(), q->stream);
+      hamming_tiles(q, q->fp.as<uint64_t>(), q->n_docs, db->fp.as<uint64_t>(), db->n_docs, max_dist, g);
       launched("hamming query bitmap");
     }
     rc2 = run_emit(q, g, out_pairs, capacity, out_count);

@@ -306,7 +306,10 @@ __global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel2(MrcArgs a) {
   }
 }
 
-// Hamming tile: warp w handles rows (w&3)*32+lane and words (w>>2)*2..+1.
+// Hamming tile: warp w handles rows (w&1)*64 + lane and (w&1)*64 + 32 + lane
+// (two rows per thread: every broadcast LDS.128 of two column fingerprints
+// serves four pairs, half the shared-memory traffic of one row per thread —
+// the kernel was MIO-throttled) and word w>>1 (32 columns).
 __global__ void __launch_bounds__(256) hamming_bitmap_kernel(const uint64_t* __restrict__ fr,
                                                              const uint64_t* __restrict__ fc, int max_dist,
                                                              PairGrid g, uint32_t nbr, uint32_t nbc,
@@ -323,32 +326,37 @@ __global__ void __launch_bounds__(256) hamming_bitmap_kernel(const uint64_t* __r
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t i = row0 + (w & 3) * 32 + lane;
-  const uint64_t x64 = i < g.n_rows ? fr[i] : 0ull;
-  const uint32_t xl = static_cast<uint32_t>(x64), xh = static_cast<uint32_t>(x64 >> 32);
+  const uint32_t iA = row0 + (w & 1) * 64 + lane, iB = iA + 32;
+  const uint64_t a64 = iA < g.n_rows ? fr[iA] : 0ull, b64 = iB < g.n_rows ? fr[iB] : 0ull;
+  const uint32_t al = static_cast<uint32_t>(a64), ah = static_cast<uint32_t>(a64 >> 32);
+  const uint32_t bl = static_cast<uint32_t>(b64), bh = static_cast<uint32_t>(b64 >> 32);
   const int thr = max_dist + 1;
-  uint32_t cnt = 0;
+  const int wi = w >> 1;
+  uint32_t bitsA = 0, bitsB = 0;
+  // Columns 31..0 of this word: shift in the sign of (hd - thr) so column b
+  // ends at bit b (one funnel shift per pair).
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int wi = (w >> 2) * 2 + q;
-    uint32_t bits = 0;
-    // Columns 31..0 of this word: shift in the sign of (hd - thr) so column b
-    // ends at bit b (one funnel shift per pair).
-#pragma unroll
-    for (int b = 31; b >= 0; b -= 2) {
-      const uint4 y = *reinterpret_cast<const uint4*>(&Fc[wi * 32 + b - 1]);  // cols b-1, b
-      const int d1 = __popc(xl ^ y.z) + __popc(xh ^ y.w) - thr;
-      bits = __funnelshift_l(static_cast<uint32_t>(d1), bits, 1);
-      const int d0 = __popc(xl ^ y.x) + __popc(xh ^ y.y) - thr;
-      bits = __funnelshift_l(static_cast<uint32_t>(d0), bits, 1);
-    }
-    if (i < g.n_rows) {
-      const uint32_t v = bits & col_mask(col0 + wi * 32, i, g);
-      bitmap[static_cast<size_t>(i) * g.words_per_row + bj * 4 + wi] = v;
-      cnt += __popc(v);
-    }
+  for (int b = 31; b >= 0; b -= 2) {
+    const uint4 y = *reinterpret_cast<const uint4*>(&Fc[wi * 32 + b - 1]);  // cols b-1, b
+    const int a1 = __popc(al ^ y.z) + __popc(ah ^ y.w) - thr;
+    const int b1 = __popc(bl ^ y.z) + __popc(bh ^ y.w) - thr;
+    bitsA = __funnelshift_l(static_cast<uint32_t>(a1), bitsA, 1);
+    bitsB = __funnelshift_l(static_cast<uint32_t>(b1), bitsB, 1);
+    const int a0 = __popc(al ^ y.x) + __popc(ah ^ y.y) - thr;
+    const int b0 = __popc(bl ^ y.x) + __popc(bh ^ y.y) - thr;
+    bitsA = __funnelshift_l(static_cast<uint32_t>(a0), bitsA, 1);
+    bitsB = __funnelshift_l(static_cast<uint32_t>(b0), bitsB, 1);
   }
-  if (cnt) atomicAdd(rowcnt + i, cnt);
+  if (iA < g.n_rows) {
+    const uint32_t v = bitsA & col_mask(col0 + wi * 32, iA, g);
+    bitmap[static_cast<size_t>(iA) * g.words_per_row + bj * 4 + wi] = v;
+    if (v) atomicAdd(rowcnt + iA, __popc(v));
+  }
+  if (iB < g.n_rows) {
+    const uint32_t v = bitsB & col_mask(col0 + wi * 32, iB, g);
+    bitmap[static_cast<size_t>(iB) * g.words_per_row + bj * 4 + wi] = v;
+    if (v) atomicAdd(rowcnt + iB, __popc(v));
+  }
 }
 
 // Warp per row: the row's set bits as ascending column ids at

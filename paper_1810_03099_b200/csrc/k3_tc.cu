@@ -196,7 +196,7 @@ __device__ __forceinline__ uint32_t tc_striped_tiles(const TcArgs& a) {
 // (whole panel per stage), two row blocks and two A buffers, all compile-time
 // (the MMA issue loop fully unrolled: at K = 20 the issuing thread's latency
 // per MMA is on the critical path).
-template <uint32_t FS>
+template <uint32_t FS, bool I8 = false>
 __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t tsm[];
   __shared__ __align__(8) uint64_t full_bar[kTcMaxStages], empty_bar[kTcMaxStages], afull_bar[2], aempty_bar[2], tfull_bar[2],
@@ -327,8 +327,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
 #pragma unroll
               for (uint32_t j = 0; j < kStepsMax; ++j) {
                 if (j < steps) {
-                  mma_f16_e(e, d0, dAc + j * 256, dB + j * 256, (ch | j) != 0);
-                  if (v1) mma_f16_e(e, d0 + 128, dAc + dPB + j * 256, dB + j * 256, (ch | j) != 0);
+                  if constexpr (I8) {  // Hamming: +-1 int8 operands, s32 accumulators (same bytes per step)
+                    mma_i8_e(e, d0, dAc + j * 256, dB + j * 256, (ch | j) != 0);
+                    if (v1) mma_i8_e(e, d0 + 128, dAc + dPB + j * 256, dB + j * 256, (ch | j) != 0);
+                  } else {
+                    mma_f16_e(e, d0, dAc + j * 256, dB + j * 256, (ch | j) != 0);
+                    if (v1) mma_f16_e(e, d0 + 128, dAc + dPB + j * 256, dB + j * 256, (ch | j) != 0);
+                  }
                 }
               }
             }
@@ -437,6 +442,43 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// Hamming on the tensor cores: with s = 2x - 1 in {-1, +1}^64 per
+// fingerprint, s_a . s_b = 64 - 2 hd(a, b), so hd <= max_dist <=> s_a . s_b -
+// (64 - 2 max_dist) >= 0 — an exact int8 MMA with s32 accumulators and the
+// same folded-threshold trick as the MRC compare: row form [s_a | -thr | 0..],
+// column form [s_b | 1 | 0..], K' = 96 bytes (three K=32 int8 steps), stored
+// in the f16 kernel's panel layout (16-byte chunks [6][128 docs]), so the
+// tile kernel and its sign-bit epilogue are reused unchanged.
+constexpr uint32_t kHamKPBytes = 96;
+__global__ void __launch_bounds__(256) ham_forms_kernel(const uint64_t* __restrict__ fp, uint32_t n, int thr,
+                                                        uint8_t* __restrict__ rowf, uint8_t* __restrict__ colf) {
+  // thread (chunk kc, doc dl) of panel blockIdx.x: 16 bytes at [kc][dl]
+  const uint32_t pan = blockIdx.x;
+  for (uint32_t idx = threadIdx.x; idx < 6 * 128; idx += blockDim.x) {
+    const uint32_t kc = idx >> 7, dl = idx & 127, d = pan * 128 + dl;
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    uint32_t wr[4] = {0u, 0u, 0u, 0u};
+    if (d < n) {
+      if (kc < 4) {
+        const uint32_t bits = static_cast<uint32_t>(fp[d] >> (16 * kc)) & 0xffffu;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t nib = (bits >> (4 * q)) & 0xfu;
+          const uint32_t y = (nib * 0x00204081u) & 0x01010101u;  // bit t of the nibble -> byte t = 0 / 1
+          w[q] = y | ((y ^ 0x01010101u) * 0xffu);                 // 1 -> +1 (0x01), 0 -> -1 (0xff)
+          wr[q] = w[q];
+        }
+      } else if (kc == 4) {
+        wr[0] = static_cast<uint32_t>(static_cast<uint8_t>(static_cast<int8_t>(-thr)));
+        w[0] = 1u;
+      }
+    }
+    const size_t off = (static_cast<size_t>(pan) * 6 * 128 + static_cast<size_t>(kc) * 128 + dl) * 16;
+    if (rowf) *reinterpret_cast<uint4*>(rowf + off) = make_uint4(wr[0], wr[1], wr[2], wr[3]);
+    if (colf) *reinterpret_cast<uint4*>(colf + off) = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
@@ -626,12 +668,13 @@ void launch_mrc_tc_forms(const float* ST, uint32_t ld, uint32_t n_docs, uint32_t
   note_launch();
 }
 
-void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
-                   uint32_t* rowcnt, cudaStream_t s) {
+// The tile kernel over operand panels of K' = KP halves (i8: 2*KP int8 values).
+static void launch_tc_tiles(const void* rowf, const void* colf, uint32_t KP, const PairGrid& g, uint32_t* bitmap,
+                            uint32_t* rowcnt, cudaStream_t s, bool i8) {
   TcArgs a{};
   a.Ar = static_cast<const __half*>(rowf);
   a.Bc = static_cast<const __half*>(colf);
-  a.KP = mrc_tc_kp(K);
+  a.KP = KP;
   a.g = g;
   a.nbr = static_cast<uint32_t>(ceil_div(g.n_rows, 128));
   a.nbc = static_cast<uint32_t>(ceil_div(g.n_cols, 128));
@@ -676,7 +719,8 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
   // per launch: the attribute is per device context (a process may drive several GPUs)
   const uint32_t fs = a.KP <= kTcSmallKP ? a.KP / 16 : 0u;
   void (*kern)(TcArgs) = nullptr;
-  switch (fs) {
+  switch (i8 ? 100u : fs) {
+    case 100: kern = mrc_tc_kernel<kHamKPBytes / 32, true>; break;  // KP = 48 halves = 96 bytes
     case 1: kern = mrc_tc_kernel<1>; break;
     case 2: kern = mrc_tc_kernel<2>; break;
     case 3: kern = mrc_tc_kernel<3>; break;
@@ -725,6 +769,26 @@ void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGri
   }
 #endif
   note_launch();
+}
+
+void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
+                   uint32_t* rowcnt, cudaStream_t s) {
+  launch_tc_tiles(rowf, colf, mrc_tc_kp(K), g, bitmap, rowcnt, s, false);
+}
+
+size_t ham_tc_form_bytes(uint32_t n) { return static_cast<size_t>(ceil_div(n, 128)) * 128 * kHamKPBytes; }
+
+void launch_ham_tc_forms(const uint64_t* fp, uint32_t n, int max_dist, void* rowf, void* colf, cudaStream_t s) {
+  if (!n) return;
+  ham_forms_kernel<<<static_cast<unsigned>(ceil_div(n, 128)), 256, 0, s>>>(fp, n, 64 - 2 * max_dist,
+                                                                            static_cast<uint8_t*>(rowf),
+                                                                            static_cast<uint8_t*>(colf));
+  note_launch();
+}
+
+void launch_ham_tc(const void* rowf, const void* colf, const PairGrid& g, uint32_t* bitmap, uint32_t* rowcnt,
+                   cudaStream_t s) {
+  launch_tc_tiles(rowf, colf, kHamKPBytes / 2, g, bitmap, rowcnt, s, true);
 }
 
 }  // namespace refsig_gpu

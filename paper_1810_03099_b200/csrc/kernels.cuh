@@ -152,6 +152,13 @@ void launch_mrc_tc_forms(const float* ST, uint32_t ld, uint32_t n_docs, uint32_t
                          uint32_t* rowcnt, uint32_t n_rowcnt, cudaStream_t s);
 void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
                    uint32_t* rowcnt, cudaStream_t s);
+// Hamming join on the tensor cores (k3_tc.cu): +-1 int8 forms of the 64-bit
+// fingerprints (row forms carry the threshold), then the tcgen05 tile kernel
+// with kind::i8 into the same bitmap / row counts as launch_hamming_bitmap.
+size_t ham_tc_form_bytes(uint32_t n);
+void launch_ham_tc_forms(const uint64_t* fp, uint32_t n, int max_dist, void* rowf, void* colf, cudaStream_t s);
+void launch_ham_tc(const void* rowf, const void* colf, const PairGrid& g, uint32_t* bitmap, uint32_t* rowcnt,
+                   cudaStream_t s);
 void launch_hamming_bitmap(const uint64_t* f_rows, const uint64_t* f_cols, int max_dist, const PairGrid& g,
                            uint32_t* bitmap, uint32_t* rowcnt, cudaStream_t s);
 // keys[k] = (i<<32) | cols[k] for rows [row_begin, row_end) (CSR -> sorted keys).

@@ -79,6 +79,18 @@ __device__ __forceinline__ void mma_f16_e(uint32_t e, uint32_t d_tmem, uint64_t 
       "@q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate), "r"(e));
 }
+// kind::i8 instruction descriptor: D s32, A/B signed 8-bit, K-major both, M=128, N=128
+// (CUTLASS UMMA::InstrDescriptor: c_format 2 = S32, a/b_format 1 = INT8).
+constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+// One K=32 int8 step (32 bytes per row: the same bytes per step as a K=16 f16 step).
+__device__ __forceinline__ void mma_i8_e(uint32_t e, uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(kIdescI8), "r"(accumulate), "r"(e));
+}
 __device__ __forceinline__ void mma_commit_e(uint32_t e, uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
