@@ -805,6 +805,18 @@ PairGrid self_grid(const refsig_gpu_ctx* c) {
 
 }  // namespace
 
+// Column panel of the K5 tail accumulator: kExactPanel docs of shared memory;
+// REFSIG_EXACT_PANEL (a multiple of 4) forces smaller panels (tests: the
+// multi-panel walk on a small corpus).
+static uint32_t exact_panel(uint32_t N) {
+  static const uint32_t env = [] {
+    const char* m = std::getenv("REFSIG_EXACT_PANEL");
+    return m ? static_cast<uint32_t>(std::atoi(m)) : 0u;
+  }();
+  const uint32_t p = env ? std::max<uint32_t>(4u, env & ~3u) : kExactPanel;
+  return std::min<uint32_t>(N, std::min<uint32_t>(p, kExactPanel));
+}
+
 // K5 inputs (exact verifier and evaluation): unit weights, the kExactHead
 // highest-df terms as dense rows + norms, and the tail postings. Returns H.
 uint32_t prepare_exact(refsig_gpu_ctx* ctx) {
@@ -1567,7 +1579,7 @@ int refsig_gpu_exact_pairs(refsig_gpu_ctx* ctx, float tau_cos, uint64_t* out_pai
       ExactArgs a{ctx->ent.as<uint2>(),        ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(),
                   ctx->x.as<float>(),          ctx->head_col.as<int32_t>(), ctx->post_off.as<uint64_t>(),
                   ctx->posts.as<uint2>(),      ctx->entpos.as<uint32_t>(),  ctx->headA.as<float>(),      ctx->head_norm.as<float>(),
-                  H,                           N,                           std::min<uint32_t>(N, kExactPanel),
+                  H,                           N,                           exact_panel(N),
                   tau_cos,                     ctx->bitmap.as<uint32_t>(),  g.words_per_row,
                   ctx->rowcnt.as<uint32_t>(),  nullptr,                     0};
       launch_exact_tail(a, 0, N, ctx->stream);
@@ -1619,7 +1631,7 @@ int refsig_gpu_evaluate(refsig_gpu_ctx* ctx, uint32_t row_lo, uint32_t row_hi, r
         ExactArgs a{ctx->ent.as<uint2>(),        ctx->doc_off.as<uint64_t>(), ctx->nnz.as<uint32_t>(),
                     ctx->x.as<float>(),          ctx->head_col.as<int32_t>(), ctx->post_off.as<uint64_t>(),
                     ctx->posts.as<uint2>(),      ctx->entpos.as<uint32_t>(),  ctx->headA.as<float>(),      ctx->head_norm.as<float>(),
-                    H,                           N,                           std::min<uint32_t>(N, kExactPanel),
+                    H,                           N,                           exact_panel(N),
                     0.0f,                        nullptr,                     0,
                     nullptr,                     ctx->eval_tail.as<uint32_t>(), ld};
         launch_exact_tail(a, static_cast<uint32_t>(p0), p1, ctx->stream);

@@ -208,3 +208,40 @@ def test_emit_wide_rows_equals_warp_per_row():
         assert r.returncode == 0, r.stderr[-2000:]
         out[mode] = r.stdout.strip().splitlines()
     assert out["0"] == out["1"] and int(out["0"][0]) > 0, out
+
+
+_PANEL_SNIPPET = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, {repo!r})
+import paper_1810_03099_b200 as R
+from paper_1810_03099_b200 import corpus as C
+cp, cfg = C.config_corpus("c1")
+cp = cp.slice_docs(5000)
+refs = C.sample_refs(cfg["ref_seed"], cp.n_docs, cfg["K"])
+with R.Context(0) as c:
+    c.load_corpus(cp.tokens, cp.doc_off, cp.vocab); c.count(); c.set_reference_docs(refs); c.sign(fetch=False)
+    c.simhash(0)
+    k = c.exact_pairs(0.8)
+    ev = c.evaluate()
+print(len(k), hashlib.sha256(np.ascontiguousarray(k).tobytes()).hexdigest(), repr(ev["mrc_mae"]), repr(ev["simhash_variance"]))
+"""
+
+
+def test_exact_multi_panel_equals_single_panel():
+    """K5's tail accumulator in several column panels (REFSIG_EXACT_PANEL=1024:
+    five panels over 5,000 documents, the configs[3]-size path) gives the same
+    exact pairs and the same evaluation sums as one panel (fixed-point tail
+    sums: order-free, so bit-identical)."""
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _PANEL_SNIPPET.format(repo=repo)
+    out = {}
+    for panel in ("", "1024"):
+        env = dict(os.environ)
+        env.pop("REFSIG_EXACT_PANEL", None)
+        if panel:
+            env["REFSIG_EXACT_PANEL"] = panel
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[panel] = r.stdout.strip().splitlines()[-1]
+    assert out[""] == out["1024"] and int(out[""].split()[0]) > 0, out
