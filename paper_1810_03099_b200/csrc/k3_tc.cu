@@ -135,19 +135,31 @@ __device__ __forceinline__ bool tc_rvalid(const TcArgs& a, uint32_t p, uint32_t 
   return h < tc_rb<FS>(a) && tc_r0<FS>(a, p) + h < a.rb1;
 }
 
-template <uint32_t FS>
+template <uint32_t FS, bool MC = false>
 struct TileWalk {
   uint32_t p, c;        // row group, column block relative to tc_cs (absolute for a rectangle)
   uint32_t item, cend;  // stripe-major walk: current item, end column of its stripe
+  bool ghost = false;   // MC: this CTA's half of the pair's item has no row group (odd count)
+  // MC (CTA pairs sharing each B chunk by multicast): items are (stripe, pair of
+  // row groups), walked by the cluster; rank r takes row group 2 gp + r
   __device__ void set_item(const TcArgs& a) {
-    const uint32_t st = item / a.n_groups;
-    p = item % a.n_groups;
-    c = st * a.stripe;
+    if constexpr (MC) {
+      const uint32_t ngp = (a.n_groups + 1) / 2;
+      const uint32_t st = item / ngp, gp = item % ngp;
+      p = 2 * gp + (blockIdx.x & 1u);
+      ghost = p >= a.n_groups;
+      if (ghost) p = 2 * gp;  // valid operands, results discarded
+      c = st * a.stripe;
+    } else {
+      const uint32_t st = item / a.n_groups;
+      p = item % a.n_groups;
+      c = st * a.stripe;
+    }
     cend = min(c + a.stripe, a.nbc);
   }
   __device__ void start(const TcArgs& a, uint64_t t) {
     if (a.stripe) {
-      item = blockIdx.x;
+      item = MC ? blockIdx.x >> 1 : blockIdx.x;
       set_item(a);
       return;
     }
@@ -162,7 +174,7 @@ struct TileWalk {
   __device__ bool next(const TcArgs& a) {
     if (a.stripe) {
       if (++c == cend) {
-        item += gridDim.x;
+        item += MC ? gridDim.x >> 1 : gridDim.x;
         set_item(a);
         return true;
       }
@@ -177,12 +189,15 @@ struct TileWalk {
   }
 };
 
-// Tiles of this CTA in the stripe-major walk.
+// Tiles of this CTA in the stripe-major walk (MC: of its pair).
+template <bool MC = false>
 __device__ __forceinline__ uint32_t tc_striped_tiles(const TcArgs& a) {
   const uint32_t ns = (a.nbc + a.stripe - 1) / a.stripe;
+  const uint32_t ng = MC ? (a.n_groups + 1) / 2 : a.n_groups;
+  const uint32_t i0 = MC ? blockIdx.x >> 1 : blockIdx.x, di = MC ? gridDim.x >> 1 : gridDim.x;
   uint32_t n = 0;
-  for (uint32_t i = blockIdx.x; i < a.n_groups * ns; i += gridDim.x) {
-    const uint32_t c0 = (i / a.n_groups) * a.stripe;
+  for (uint32_t i = i0; i < ng * ns; i += di) {
+    const uint32_t c0 = (i / ng) * a.stripe;
     n += min(a.stripe, a.nbc - c0);
   }
   return n;
@@ -196,8 +211,9 @@ __device__ __forceinline__ uint32_t tc_striped_tiles(const TcArgs& a) {
 // (whole panel per stage), two row blocks and two A buffers, all compile-time
 // (the MMA issue loop fully unrolled: at K = 20 the issuing thread's latency
 // per MMA is on the critical path).
-template <uint32_t FS, bool I8 = false>
+template <uint32_t FS, bool I8 = false, bool MC = false>
 __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
+  static_assert(!MC || FS == 0, "B multicast is built for the chunked (K' > 128, single issuer) path");
   extern __shared__ __align__(1024) uint8_t tsm[];
   __shared__ __align__(8) uint64_t full_bar[kTcMaxStages], empty_bar[kTcMaxStages], afull_bar[2], aempty_bar[2], tfull_bar[2],
       tempty_bar[2];
@@ -206,7 +222,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
   // MMA issuers keep descriptors and counters in uniform registers
   const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
   const uint64_t t0 = a.n_tiles * blockIdx.x / gridDim.x, t1 = a.n_tiles * (blockIdx.x + 1) / gridDim.x;
-  const uint32_t n_it = a.stripe ? tc_striped_tiles(a) : static_cast<uint32_t>(t1 - t0);
+  const uint32_t n_it = a.stripe ? tc_striped_tiles<MC>(a) : static_cast<uint32_t>(t1 - t0);
+  const uint32_t crank = MC ? cluster_rank() : 0u;
   const uint32_t PB = 256u * a.KP;  // bytes per operand panel
   // B ring(s): every ring has ONE consumer taking its fills in order (with two
   // consumers of a shared ring, one could wait on a stage's fill k while fill
@@ -227,7 +244,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < S; ++s) {
       mb_init(&full_bar[s], 1);
-      mb_init(&empty_bar[s], 1);
+      mb_init(&empty_bar[s], MC ? 2 : 1);  // MC: both CTAs' MMA commits free a stage
     }
     for (int s = 0; s < 2; ++s) {
       mb_init(&afull_bar[s], 1);
@@ -246,11 +263,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
+  if constexpr (MC) cluster_sync_all();  // the peer's barriers are initialised before any multicast
   pdl_wait();  // setup above overlaps the operand-forms kernel's tail
 
   if (warp == 0) {
     if (lane == 0 && n_it) {  // producer
-      TileWalk<FS> w;
+      TileWalk<FS, MC> w;
       w.start(a, t0);
       uint32_t g = 0;  // row groups started by this CTA
       uint32_t qm[2] = {0, 0};  // B chunks issued into issuer m's ring
@@ -278,7 +296,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
             mb_arrive(&full_bar[st]);
           } else {
             mb_expect_tx(&full_bar[st], bytes);
-            bulk_g2s(sBbase + static_cast<size_t>(st) * CB, src + static_cast<size_t>(ch) * CB, bytes, &full_bar[st]);
+            if constexpr (MC) {  // the leader's one copy fills both CTAs' stage
+              if (crank == 0)
+                bulk_g2s_mc(sBbase + static_cast<size_t>(st) * CB, src + static_cast<size_t>(ch) * CB, bytes,
+                            &full_bar[st], 3);
+            } else {
+              bulk_g2s(sBbase + static_cast<size_t>(st) * CB, src + static_cast<size_t>(ch) * CB, bytes,
+                       &full_bar[st]);
+            }
           }
         }
         new_group = w.next(a);
@@ -292,7 +317,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
     // converged, one elected lane issues
     const uint32_t m = warp - 1;
     if (n_it) {
-      TileWalk<FS> w;
+      TileWalk<FS, MC> w;
       w.start(a, t0);
       const uint64_t dA0 = smem_desc(smem_u32(sAbase)), dB0 = smem_desc(smem_u32(sBbase));
       const uint64_t dPB = PB >> 4, dCB = CB >> 4;
@@ -337,7 +362,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
                 }
               }
             }
-            mma_commit_e(e, &empty_bar[st]);
+            if constexpr (MC)
+              mma_commit_mc_e(e, &empty_bar[st], 3);  // both CTAs' producers wait on this stage
+            else
+              mma_commit_e(e, &empty_bar[st]);
           }
           if (lane == 0 && m == 0) tc_trace(TC_DBG(a), 3, it);
           __syncwarp();
@@ -358,7 +386,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
     const uint32_t q = ew & 3, eg = (ew - 3) >> 3, h = ((ew - 3) >> 2) & 1;
     const uint32_t wpr = a.g.words_per_row;
     const uint32_t two = a.two;
-    TileWalk<FS> w;
+    TileWalk<FS, MC> w;
     if (n_it) w.start(a, t0);
     uint32_t cnt = 0;
     for (uint32_t it = 0; it < n_it; ++it) {
@@ -373,7 +401,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
         mb_wait_warp(&tfull_bar[acc], u & 1u);
         if (warp == 3 && lane == 0) tc_trace(TC_DBG(a), 5, it);
         tc_fence_after();
-        const bool valid = tc_rvalid<FS>(a, p, h) && !(a.g.triangle && bj < r);
+        const bool valid = tc_rvalid<FS>(a, p, h) && !(a.g.triangle && bj < r) && !w.ghost;
         const bool edge = (a.g.triangle && bj == r) || bj + 1 == a.nbc;
         uint32_t mw[4];
 #pragma unroll
@@ -439,6 +467,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync_all();  // no multicast copy or commit still targets this CTA
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
@@ -710,6 +739,17 @@ static void launch_tc_tiles(const void* rowf, const void* colf, uint32_t KP, con
   a.n_groups = static_cast<uint32_t>(ceil_div(a.rb1 - a.rb0, a.rb));
   if (!g.triangle && stripe_mode != 0 && (stripe_mode == 1 || (a.n_groups >= 2 && a.nbc >= 8ull * grid)))
     a.stripe = static_cast<uint32_t>(ceil_div(a.nbc, grid));
+  // CTA pairs sharing every B chunk by cluster multicast (chunked path, stripe walk, even grid):
+  // correct (tests) but measured no faster at configs[4] (7.40 vs 7.29 ms: one L2 read per pair, yet
+  // each SM still ingests the whole 64 B/clk of B — the per-SM share, not L2, is the bound), so off
+  // unless REFSIG_TC_MC=1
+  static const int mc_mode = [] {
+    const char* m = std::getenv("REFSIG_TC_MC");
+    return m ? std::atoi(m) : 0;
+  }();
+  const bool mc = mc_mode == 1 && !i8 && a.KP > kTcSmallKP && a.stripe && grid >= 2 && a.n_groups >= 2;
+  unsigned grid_mc = grid & ~1u;
+  if (mc) a.stripe = static_cast<uint32_t>(ceil_div(a.nbc, grid_mc / 2));
   static const uint32_t dbg = [] {
     const char* m = std::getenv("REFSIG_TC_DEBUG");
     return m ? static_cast<uint32_t>(std::atoi(m)) : 0u;
@@ -729,7 +769,7 @@ static void launch_tc_tiles(const void* rowf, const void* colf, uint32_t KP, con
     case 6: kern = mrc_tc_kernel<6>; break;
     case 7: kern = mrc_tc_kernel<7>; break;
     case 8: kern = mrc_tc_kernel<8>; break;
-    default: kern = mrc_tc_kernel<0>; break;
+    default: kern = mc ? mrc_tc_kernel<0, false, true> : mrc_tc_kernel<0>; break;
   }
   ensure_smem(kern, smem);
 #ifdef REFSIG_TC_TRACE
@@ -746,12 +786,17 @@ static void launch_tc_tiles(const void* rowf, const void* colf, uint32_t KP, con
   if (std::getenv("REFSIG_TC_PRINT"))
     std::fprintf(stderr,
                  "mrc_tc: KP %u nch %u last %u CB %u rb %u abufs %u stages %u smem %zu grid %u tiles %llu rows %u cols "
-                 "%u wpr %u tri %d rb0 %u rb1 %u nbc %u stripe %u groups %u Ar %p Bc %p bitmap %p\n",
+                 "%u wpr %u tri %d rb0 %u rb1 %u nbc %u stripe %u groups %u mc %d Ar %p Bc %p bitmap %p\n",
                  a.KP, a.nch, a.last_steps, a.CB, a.rb, a.abufs, a.stages, smem, grid,
                  static_cast<unsigned long long>(a.n_tiles), g.n_rows, g.n_cols, g.words_per_row, g.triangle ? 1 : 0,
-                 a.rb0, a.rb1, a.nbc, a.stripe, a.n_groups, static_cast<const void*>(a.Ar), static_cast<const void*>(a.Bc),
+                 a.rb0, a.rb1, a.nbc, a.stripe, a.n_groups, mc ? 1 : 0, static_cast<const void*>(a.Ar),
+                 static_cast<const void*>(a.Bc),
                  static_cast<void*>(a.bitmap));
-  launch_pdl(kern, dim3(grid), dim3(kTcThreads), smem, s, a);
+  if (mc) {
+    launch_pdl_cluster2(kern, dim3(grid_mc), dim3(kTcThreads), smem, s, a);
+  } else {
+    launch_pdl(kern, dim3(grid), dim3(kTcThreads), smem, s, a);
+  }
 #ifdef REFSIG_TC_TRACE
   if (dbg & 8) {
     static int calls = 0;

@@ -143,7 +143,7 @@ import paper_1810_03099_b200 as R
 from paper_1810_03099_b200 import corpus as C
 cfg = C.load_configs()["configs"]["c4"]
 db_spec = dict(cfg["corpus"], n_docs=6000, vocab=50000)
-q_spec = dict(cfg["queries"], n_docs=700, vocab=50000)
+q_spec = dict(cfg["queries"], n_docs={NQ}, vocab=50000)
 db = C.generate(db_spec)
 q = C.generate_queries(q_spec, db_spec, db)
 refs = C.sample_refs(0, db.n_docs, {K})
@@ -157,21 +157,24 @@ print(len(keys), hashlib.sha256(np.ascontiguousarray(keys).tobytes()).hexdigest(
 """
 
 
-@pytest.mark.parametrize("K", [20, 128])
-def test_query_join_stripe_walk_equals_contiguous(K):
+@pytest.mark.parametrize("K,NQ", [(20, 700), (128, 700), (128, 600)])
+def test_query_join_stripe_walk_equals_contiguous(K, NQ):
     """The stripe-major tile walk of the query rectangle (k3_tc.cu TileWalk,
     forced on with REFSIG_TC_STRIPE=1) gives the same candidate keys as the
     contiguous walk (REFSIG_TC_STRIPE=0), both paths of the tcgen05 kernel
-    (K' <= 128 with two row blocks, chunked K' = 400)."""
+    (K' <= 128 with two row blocks, chunked K' = 400), and so does the stripe
+    walk in CTA pairs sharing every B chunk by cluster multicast
+    (REFSIG_TC_MC=1, chunked path; 600 queries: an odd number of row groups,
+    so one CTA of a pair runs a ghost half)."""
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = _STRIPE_SNIPPET.format(repo=repo, K=K)
+    code = _STRIPE_SNIPPET.format(repo=repo, K=K, NQ=NQ)
     out = {}
-    for mode in ("0", "1"):
-        env = dict(os.environ, REFSIG_TC_STRIPE=mode)
+    for mode in ("0", "1", "mc"):
+        env = dict(os.environ, REFSIG_TC_STRIPE="1" if mode == "mc" else mode, REFSIG_TC_MC="1" if mode == "mc" else "0")
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         out[mode] = r.stdout.strip().splitlines()[-1]
-    assert out["0"] == out["1"] and int(out["0"].split()[0]) > 0, out
+    assert out["0"] == out["1"] == out["mc"] and int(out["0"].split()[0]) > 0, out
 
 
 _EMIT_SNIPPET = r"""
