@@ -264,6 +264,7 @@ struct refsig_gpu_ctx {
   // query joins (they do not depend on tau); valid while sign_gen is unchanged
   DevBuf tc_colf;
   uint64_t sign_gen = 0, tc_colf_gen = ~0ull;
+  bool tc_colf_col64 = false;  // tc_colf laid out as 64-document panels (CTA-pair kernel)
 
   // query mode
   refsig_gpu_ctx* db = nullptr;
@@ -563,12 +564,19 @@ void run_mrc_tiles(refsig_gpu_ctx* c, const float* STr, uint32_t ldr, uint32_t n
     rowf = c->tc_forms.as<char>();
     launch_mrc_tc_forms(STr, ldr, nr, K, tau, rowf, nullptr, c->rowcnt.as<uint32_t>(), g.n_rows, c->stream);
     static const bool no_cache = std::getenv("REFSIG_NO_FORM_CACHE") != nullptr;
-    if (no_cache || db->tc_colf_gen != db->sign_gen || db->tc_colf.cap < cb) {
+    const bool pair = mrc_tc2_applies(K, g);  // CTA-pair kernel: column forms in 64-document panels
+    if (no_cache || db->tc_colf_gen != db->sign_gen || db->tc_colf.cap < cb || db->tc_colf_col64 != pair) {
       db->tc_colf.ensure(cb);
-      launch_mrc_tc_forms(STc, ldc, ncl, K, tau, nullptr, db->tc_colf.p, nullptr, 0, c->stream);
+      launch_mrc_tc_forms(STc, ldc, ncl, K, tau, nullptr, db->tc_colf.p, nullptr, 0, c->stream, pair);
       db->tc_colf_gen = db->sign_gen;
+      db->tc_colf_col64 = pair;
     }
     colf = db->tc_colf.as<char>();
+    launched("tcgen05 operand forms");
+    if (pair) {
+      launch_mrc_tc2(rowf, colf, K, g, c->bitmap.as<uint32_t>(), c->rowcnt.as<uint32_t>(), c->stream);
+      return;
+    }
   }
   launched("tcgen05 operand forms");
   launch_mrc_tc(rowf, colf, K, g, c->bitmap.as<uint32_t>(), c->rowcnt.as<uint32_t>(), c->stream);

@@ -474,6 +474,264 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
   }
 }
 
+// ---- K3 on CTA pairs (cta_group::2), chunked K' > 128, query rectangle ----
+// The pair (cluster of 2 CTAs on one TPC) computes 256 rows x 128 columns per
+// tile with ONE tcgen05.mma.cta_group::2 per K step (M = 256): each CTA holds
+// its own 128-row A block (resident per item) and HALF of each B chunk — 64
+// columns, from column forms laid out as 64-document panels — and its TMEM
+// receives its 128 rows x all 128 columns (CUTLASS SM100_MMA_F16BF16_2x1SM_SS
+// split). So every SM ingests half the B bytes per flop of the one-CTA rb = 1
+// kernel (whose per-SM share of L2 bandwidth bounded the configs[4] join).
+// The leader (rank 0) issues the MMAs; the peer's copies land in the peer's
+// own barriers, so a forwarder thread of the peer re-arrives each completed
+// fill on the leader's pair barriers (remote mbarrier arrive), and another
+// forwards the peer epilogue's accumulator releases. Commits from the leader
+// multicast to both CTAs (ring stages, A buffers, accumulators).
+// Items: (column stripe, row-group pair) as in the stripe-major walk; rank r
+// takes row block 2 gp + r (a ghost half without stores when the count is odd).
+constexpr uint32_t kTc2ChunkBytes = 64u * kTcChunkK * 2u;  // one K chunk of a 64-doc B half panel: 8 KB
+
+struct Tc2Walk {
+  uint32_t p, c, item, cend;
+  bool ghost;
+  __device__ void set_item(const TcArgs& a) {
+    const uint32_t ngp = (a.n_groups + 1) / 2;
+    const uint32_t st = item / ngp, gp = item % ngp;
+    p = 2 * gp + (blockIdx.x & 1u);
+    ghost = p >= a.n_groups;
+    if (ghost) p = 2 * gp;
+    c = st * a.stripe;
+    cend = min(c + a.stripe, a.nbc);
+  }
+  __device__ void start(const TcArgs& a) {
+    item = blockIdx.x >> 1;
+    set_item(a);
+  }
+  __device__ bool next(const TcArgs& a) {
+    if (++c == cend) {
+      item += gridDim.x >> 1;
+      set_item(a);
+      return true;
+    }
+    return false;
+  }
+};
+
+__global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t tsm[];
+  constexpr uint32_t NACC = 4;  // 4 x 128 TMEM columns: the MMAs run up to three tiles ahead of the epilogues
+  __shared__ __align__(8) uint64_t full_bar[kTcMaxStages], empty_bar[kTcMaxStages], ptile_bar[2], afull_bar[2],
+      pafull_bar[2], aempty_bar[2], tfull_bar[NACC], tempty_bar[NACC], ptempty_bar[NACC];
+  __shared__ uint32_t tmem_base_sh;
+  const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const uint32_t n_it = tc_striped_tiles<true>(a);
+  const uint32_t PB = 256u * a.KP;                    // bytes of one 128-row A panel
+  const uint32_t S = a.stages, NCH = a.nch, ABUFS = a.abufs, LAST = a.last_steps;
+  uint8_t* sAbase = tsm;                               // ABUFS A panels
+  uint8_t* sBbase = tsm + ABUFS * PB;                  // S stages x 8 KB half chunks
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < S; ++s) {
+      mb_init(&full_bar[s], 1);
+      mb_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mb_init(&ptile_bar[s], 1);
+      mb_init(&afull_bar[s], 1);
+      mb_init(&pafull_bar[s], 1);
+      mb_init(&aempty_bar[s], 1);
+    }
+    for (uint32_t s = 0; s < NACC; ++s) {
+      mb_init(&tfull_bar[s], 1);
+      mb_init(&tempty_bar[s], 8);
+      mb_init(&ptempty_bar[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {  // the same warp in both CTAs (cta_group::2 allocation)
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  pdl_wait();
+
+  if (warp == 0) {
+    if (lane == 0 && n_it) {  // producer (both CTAs): own A block, own B halves
+      Tc2Walk w;
+      w.start(a);
+      uint32_t g = 0, q = 0;
+      bool new_group = true;
+      for (uint32_t it = 0; it < n_it; ++it) {
+        if (new_group) {
+          const uint32_t ab = g % ABUFS;
+          if (g >= ABUFS) mb_wait_cluster(&aempty_bar[ab], ((g / ABUFS) - 1) & 1u);
+          mb_expect_tx(&afull_bar[ab], PB);
+          bulk_g2s(sAbase + ab * PB, reinterpret_cast<const uint8_t*>(a.Ar) + static_cast<size_t>(a.rb0 + w.p) * PB,
+                   PB, &afull_bar[ab]);
+          ++g;
+        }
+        // the 64-document half panel 2 bj + rank of the column forms
+        const uint8_t* src =
+            reinterpret_cast<const uint8_t*>(a.Bc) + static_cast<size_t>(2 * w.c + rank) * (PB / 2);
+        for (uint32_t ch = 0; ch < NCH; ++ch, ++q) {
+          const uint32_t st = q % S;
+          if (q >= S) mb_wait_cluster(&empty_bar[st], ((q / S) - 1) & 1u);
+          const uint32_t bytes = ch + 1 < NCH ? kTc2ChunkBytes : LAST * 2048u;
+          mb_expect_tx(&full_bar[st], bytes);
+          bulk_g2s(sBbase + static_cast<size_t>(st) * kTc2ChunkBytes, src + static_cast<size_t>(ch) * kTc2ChunkBytes,
+                   bytes, &full_bar[st]);
+        }
+        new_group = w.next(a);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (n_it && rank == 0) {  // leader: the MMA issuer
+      Tc2Walk w;
+      w.start(a);
+      const uint64_t dA0 = smem_desc(smem_u32(sAbase));
+      const uint64_t dB0 = smem_desc_lbo(smem_u32(sBbase), 1024u);
+      const uint64_t dPB = PB >> 4, dCB = kTc2ChunkBytes >> 4;
+      uint32_t g = 0, q = 0;
+      bool new_group = true;
+      for (uint32_t it = 0; it < n_it; ++it) {
+        if (new_group) {
+          mb_wait(&afull_bar[g % ABUFS], (g / ABUFS) & 1u);
+          mb_wait_cluster(&pafull_bar[g % ABUFS], (g / ABUFS) & 1u);
+          __syncwarp();
+          ++g;
+        }
+        const uint32_t ab = (g - 1) % ABUFS;
+        const uint32_t acc = it % NACC;
+        if (it >= NACC) {
+          mb_wait(&tempty_bar[acc], ((it / NACC) - 1) & 1u);
+          mb_wait_cluster(&ptempty_bar[acc], ((it / NACC) - 1) & 1u);
+          __syncwarp();
+        }
+        // the peer's B halves of this whole tile have landed (forwarded once per tile: a release
+        // remote arrive per 8 KB chunk made the forwarder the bottleneck)
+        mb_wait_cluster(&ptile_bar[it & 1], (it >> 1) & 1u);
+        __syncwarp();
+        const uint64_t dA = dA0 + ab * dPB;
+        const uint32_t d0 = tmem + acc * 128;
+        for (uint32_t ch = 0; ch < NCH; ++ch, ++q) {
+          const uint32_t st = q % S;
+          mb_wait(&full_bar[st], (q / S) & 1u);
+          __syncwarp();
+          const uint32_t e = elect_one();
+          tc_fence_after();
+          const uint32_t steps = ch + 1 < NCH ? kTcChunkK / 16 : LAST;
+          const uint64_t dB = dB0 + st * dCB, dAc = dA + ch * (kTcChunkK / 16) * 256u;
+#pragma unroll
+          for (uint32_t j = 0; j < kTcChunkK / 16; ++j)
+            if (j < steps) mma2_f16_e(e, d0, dAc + j * 256, dB + j * 128, (ch | j) != 0);
+          mma2_commit_mc_e(e, &empty_bar[st], 3);
+        }
+        __syncwarp();
+        mma2_commit_mc_e(elect_one(), &tfull_bar[acc], 3);
+        new_group = w.next(a);
+        __syncwarp();
+        if (new_group || it + 1 == n_it) mma2_commit_mc_e(elect_one(), &aempty_bar[ab], 3);
+        __syncwarp();
+      }
+    } else if (n_it && lane == 0) {  // peer: forward A / B fill completions to the leader
+      Tc2Walk w;
+      w.start(a);
+      uint32_t g = 0, q = 0;
+      bool new_group = true;
+      for (uint32_t it = 0; it < n_it; ++it) {
+        if (new_group) {
+          mb_wait(&afull_bar[g % ABUFS], (g / ABUFS) & 1u);
+          mb_arrive_remote(&pafull_bar[g % ABUFS], 0);
+          ++g;
+        }
+        for (uint32_t ch = 0; ch < NCH; ++ch, ++q) mb_wait(&full_bar[q % S], (q / S) & 1u);
+        mb_arrive_remote(&ptile_bar[it & 1], 0);
+        new_group = w.next(a);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 2) {
+    if (n_it && rank == 1 && lane == 0) {  // peer: forward accumulator releases to the leader
+      for (uint32_t it = 0; it + NACC < n_it; ++it) {  // the leader waits releases of tiles 0 .. n_it - 1 - NACC
+        const uint32_t acc = it % NACC;
+        mb_wait(&tempty_bar[acc], (it / NACC) & 1u);
+        mb_arrive_remote(&ptempty_bar[acc], 0);
+      }
+    }
+    __syncwarp();
+  } else {  // epilogue warps 3..18: group eg (accumulator it % 2), lane quarter q, column half h
+    const uint32_t ew = threadIdx.x >> 5;
+    const uint32_t q = ew & 3, eg = (ew - 3) >> 3, h = ((ew - 3) >> 2) & 1;
+    const uint32_t wpr = a.g.words_per_row;
+    const uint32_t two = a.two;
+    Tc2Walk w;
+    if (n_it) w.start(a);
+    uint32_t cnt = 0;
+    for (uint32_t it = 0; it < n_it; ++it) {
+      const uint32_t acc = it % NACC;
+      const uint32_t r = a.rb0 + w.p;
+      const uint32_t bj = w.c;
+      const uint32_t i = r * 128 + q * 32 + lane;
+      if ((it & 1) == eg) {
+        mb_wait_warp(&tfull_bar[acc], (it / NACC) & 1u);
+        tc_fence_after();
+        const bool valid = !w.ghost && r < a.rb1;
+        uint32_t v0[32], v1[32];
+        const uint32_t ta = tmem + ((q * 32u) << 16) + acc * 128 + h * 64;
+        TC_LD32(ta, v0);
+        TC_LD32(ta + 32, v1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mb_arrive(&tempty_bar[acc]);
+        if (valid) {
+          uint32_t b[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) b[k] = 0;
+#pragma unroll
+          for (int c = 7; c >= 0; --c) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              b[k] = __funnelshift_l(v0[8 * k + c], b[k], 1);
+              b[4 + k] = __funnelshift_l(v1[8 * k + c], b[4 + k], 1);
+            }
+            b[3] = fma_pipe_shift_in(b[3], v0[24 + c], two);
+            b[7] = fma_pipe_shift_in(b[7], v1[24 + c], two);
+          }
+          uint32_t m0 = ~__byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+          uint32_t m1 = ~__byte_perm(__byte_perm(b[4], b[5], 0x0040), __byte_perm(b[6], b[7], 0x0040), 0x5410);
+          if (bj + 1 == a.nbc) {
+            const uint32_t c0 = bj * 128 + h * 64;
+            m0 &= tc_col_mask(c0, i, a.g);
+            m1 &= tc_col_mask(c0 + 32, i, a.g);
+          }
+          if (i < a.g.n_rows) {
+            *reinterpret_cast<uint2*>(a.bitmap + static_cast<size_t>(i) * wpr + bj * 4 + h * 2) = make_uint2(m0, m1);
+            cnt += __popc(m0) + __popc(m1);
+          }
+        }
+      }
+      if (w.next(a) || it + 1 == n_it) {
+        if (cnt && i < a.g.n_rows) atomicAdd(a.rowcnt + i, cnt);
+        cnt = 0;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // no commit or remote arrive still targets this CTA
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
 // Hamming on the tensor cores: with s = 2x - 1 in {-1, +1}^64 per
 // fingerprint, s_a . s_b = 64 - 2 hd(a, b), so hd <= max_dist <=> s_a . s_b -
 // (64 - 2 max_dist) >= 0 — an exact int8 MMA with s32 accumulators and the
@@ -589,7 +847,8 @@ __global__ void __launch_bounds__(256) tc_forms_kernel(const float* __restrict__
 __global__ void __launch_bounds__(256) tc_forms_any_kernel(const float* __restrict__ ST, uint32_t ld, uint32_t n_docs,
                                                            uint32_t K, uint32_t KP, float tau,
                                                            __half* __restrict__ rowf, __half* __restrict__ colf,
-                                                           uint32_t* __restrict__ rowcnt, uint32_t n_rowcnt) {
+                                                           uint32_t* __restrict__ rowcnt, uint32_t n_rowcnt,
+                                                           uint32_t col64) {
   const uint32_t pan = blockIdx.x, dl = threadIdx.x & 127, kc = blockIdx.y * 2 + (threadIdx.x >> 7);
   pdl_wait();
   if (rowcnt && blockIdx.y == 0 && threadIdx.x < 128 && pan * 128 + threadIdx.x < n_rowcnt) rowcnt[pan * 128 + threadIdx.x] = 0;
@@ -622,7 +881,12 @@ __global__ void __launch_bounds__(256) tc_forms_any_kernel(const float* __restri
   }
   const size_t off = (static_cast<size_t>(pan) * (KP / 8) + kc) * 128 * 8 + static_cast<size_t>(dl) * 8;
   if (rowf) *reinterpret_cast<uint4*>(rowf + off) = *reinterpret_cast<const uint4*>(rv);
-  if (colf) *reinterpret_cast<uint4*>(colf + off) = *reinterpret_cast<const uint4*>(cv);
+  if (colf) {  // col64: 64-document panels (the B halves of the CTA-pair kernel)
+    const size_t o = col64 ? (static_cast<size_t>(2 * pan + (dl >> 6)) * (KP / 8) + kc) * 64 * 8 +
+                                 static_cast<size_t>(dl & 63) * 8
+                           : off;
+    *reinterpret_cast<uint4*>(colf + o) = *reinterpret_cast<const uint4*>(cv);
+  }
 }
 
 // Shared-memory plan of mrc_tc_kernel for a K': row blocks per group, A
@@ -679,14 +943,14 @@ size_t mrc_tc_form_bytes(uint32_t K, uint32_t n_docs) {
 }
 
 void launch_mrc_tc_forms(const float* ST, uint32_t ld, uint32_t n_docs, uint32_t K, float tau, void* rowf, void* colf,
-                         uint32_t* rowcnt, uint32_t n_rowcnt, cudaStream_t s) {
+                         uint32_t* rowcnt, uint32_t n_rowcnt, cudaStream_t s, bool col64) {
   const uint32_t KP = mrc_tc_kp(K);
   const uint32_t n_pan = static_cast<uint32_t>(ceil_div(n_docs, 128));
   if (!n_pan) return;
   if (KP > kTcSmallKP) {
     const dim3 grid(n_pan, static_cast<unsigned>(ceil_div(KP / 8, 2)));
     launch_pdl(tc_forms_any_kernel, grid, dim3(256), 0, s, ST, ld, n_docs, K, KP, tau, static_cast<__half*>(rowf),
-               static_cast<__half*>(colf), rowcnt, n_rowcnt);
+               static_cast<__half*>(colf), rowcnt, n_rowcnt, col64 ? 1u : 0u);
     note_launch();
     return;
   }
@@ -819,6 +1083,61 @@ static void launch_tc_tiles(const void* rowf, const void* colf, uint32_t KP, con
 void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
                    uint32_t* rowcnt, cudaStream_t s) {
   launch_tc_tiles(rowf, colf, mrc_tc_kp(K), g, bitmap, rowcnt, s, false);
+}
+
+// CTA-pair kernel: chunked K' (> 128), query rectangle wide enough for the
+// stripe walk; REFSIG_TC2=0 disables it (measurement), 1 forces it where it applies.
+bool mrc_tc2_applies(uint32_t K, const PairGrid& g) {
+  static const int mode = [] {
+    const char* m = std::getenv("REFSIG_TC2");
+    return m ? std::atoi(m) : -1;
+  }();
+  if (mode == 0 || g.triangle) return false;
+  const uint32_t KP = mrc_tc_kp(K);
+  const uint32_t nbc = static_cast<uint32_t>(ceil_div(g.n_cols, 128));
+  const uint32_t rb0 = g.row_begin / 128, rb1 = static_cast<uint32_t>(ceil_div(g.row_end, 128));
+  if (KP <= kTcSmallKP || KP > 512 || rb1 - rb0 < 2) return false;
+  return mode == 1 || nbc >= 8u * 74u;
+}
+
+void launch_mrc_tc2(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
+                    uint32_t* rowcnt, cudaStream_t s) {
+  TcArgs a{};
+  a.Ar = static_cast<const __half*>(rowf);
+  a.Bc = static_cast<const __half*>(colf);
+  a.KP = mrc_tc_kp(K);
+  a.g = g;
+  a.nbr = static_cast<uint32_t>(ceil_div(g.n_rows, 128));
+  a.nbc = static_cast<uint32_t>(ceil_div(g.n_cols, 128));
+  a.rb0 = g.row_begin / 128;
+  a.rb1 = std::min(static_cast<uint32_t>(ceil_div(g.row_end, 128)), a.nbr);
+  if (g.row_end <= g.row_begin || a.rb1 <= a.rb0 || a.nbc == 0) return;
+  const uint32_t PB = 256u * a.KP;
+  a.rb = 1;
+  a.abufs = 2u * PB + 4u * kTc2ChunkBytes <= kTcSmemBudget ? 2u : 1u;
+  a.stages = std::min<uint32_t>(kTcMaxStages, (kTcSmemBudget - a.abufs * PB) / kTc2ChunkBytes);
+  a.CB = kTc2ChunkBytes;
+  a.nch = static_cast<uint32_t>(ceil_div(a.KP, kTcChunkK));
+  a.last_steps = (a.KP - kTcChunkK * (a.nch - 1)) / 16;
+  a.n_groups = a.rb1 - a.rb0;
+  a.bitmap = bitmap;
+  a.rowcnt = rowcnt;
+  a.two = 2;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = static_cast<unsigned>(sms) & ~1u;
+  a.stripe = static_cast<uint32_t>(ceil_div(a.nbc, grid / 2));
+  uint64_t T = 0;
+  a.n_tiles = T;
+  const size_t smem = std::max<size_t>(static_cast<size_t>(a.abufs) * PB + static_cast<size_t>(a.stages) * kTc2ChunkBytes,
+                                       116u * 1024u);
+  ensure_smem(mrc_tc2_kernel, smem);
+  if (std::getenv("REFSIG_TC_PRINT"))
+    std::fprintf(stderr, "mrc_tc2: KP %u nch %u last %u abufs %u stages %u smem %zu grid %u stripe %u groups %u nbc %u\n",
+                 a.KP, a.nch, a.last_steps, a.abufs, a.stages, smem, grid, a.stripe, a.n_groups, a.nbc);
+  launch_pdl_cluster2(mrc_tc2_kernel, dim3(grid), dim3(kTcThreads), smem, s, a);
+  note_launch();
 }
 
 size_t ham_tc_form_bytes(uint32_t n) { return static_cast<size_t>(ceil_div(n, 128)) * 128 * kHamKPBytes; }

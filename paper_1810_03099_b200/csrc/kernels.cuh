@@ -149,7 +149,11 @@ bool mrc_tc_supported(uint32_t K, float tau);
 size_t mrc_tc_form_bytes(uint32_t K, uint32_t n_docs);
 // rowcnt != NULL: also zero rowcnt[0 .. n_rowcnt) (the tile kernel's row counts; n_rowcnt <= n_docs panels).
 void launch_mrc_tc_forms(const float* ST, uint32_t ld, uint32_t n_docs, uint32_t K, float tau, void* rowf, void* colf,
-                         uint32_t* rowcnt, uint32_t n_rowcnt, cudaStream_t s);
+                         uint32_t* rowcnt, uint32_t n_rowcnt, cudaStream_t s, bool col64 = false);
+// CTA-pair (cta_group::2) K3 for the chunked query join; column forms in 64-document panels (col64).
+bool mrc_tc2_applies(uint32_t K, const PairGrid& g);
+void launch_mrc_tc2(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
+                    uint32_t* rowcnt, cudaStream_t s);
 void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
                    uint32_t* rowcnt, cudaStream_t s);
 // Hamming join on the tensor cores (k3_tc.cu): +-1 int8 forms of the 64-bit

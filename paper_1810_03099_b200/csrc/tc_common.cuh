@@ -23,6 +23,15 @@ __device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Wait with cluster-scope acquire (barriers a peer CTA arrives on remotely).
+__device__ __forceinline__ void mb_wait_cluster(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "W: mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
 // Warp-wide wait: every lane spins on the barrier, then the warp reconverges.
 // The lanes of a spin loop can leave it in different iterations; the
 // .sync.aligned tcgen05 instructions (and elect.sync / R2UR around the MMA
@@ -79,6 +88,37 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(2048u >> 4) << 16) |
          (static_cast<uint64_t>(128u >> 4) << 32) | (1ull << 46);
+}
+// Same with a given leading-dimension byte offset (distance between 8-wide K
+// chunks): 1024 for a 64-row operand panel (the B half of a CTA-pair MMA).
+__device__ __forceinline__ uint64_t smem_desc_lbo(uint32_t saddr, uint32_t lbo) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(lbo >> 4) << 16) |
+         (static_cast<uint64_t>(128u >> 4) << 32) | (1ull << 46);
+}
+// CTA pair (cta_group::2): D f32, A/B f16, K-major, M = 256 (128 rows per CTA), N = 128 (64 B
+// columns per CTA) — CUTLASS SM100_MMA_F16BF16_2x1SM_SS operand split.
+constexpr uint32_t kIdesc2 = (1u << 4) | ((128u >> 3) << 17) | ((256u >> 4) << 24);
+__device__ __forceinline__ void mma2_f16_e(uint32_t e, uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(kIdesc2), "r"(accumulate), "r"(e));
+}
+__device__ __forceinline__ void mma2_commit_mc_e(uint32_t e, uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::
+          "r"(smem_u32(bar)),
+      "h"(cta_mask), "r"(e)
+      : "memory");
+}
+// Arrive on the mbarrier at the same offset in CTA `cta` of the cluster.
+__device__ __forceinline__ void mb_arrive_remote(uint64_t* bar, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
 }
 // kind::f16 instruction descriptor: D f32, A/B f16, K-major both, M=128, N=128.
 constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);

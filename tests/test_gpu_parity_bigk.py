@@ -164,17 +164,20 @@ def test_query_join_stripe_walk_equals_contiguous(K, NQ):
     contiguous walk (REFSIG_TC_STRIPE=0), both paths of the tcgen05 kernel
     (K' <= 128 with two row blocks, chunked K' = 400), and so does the stripe
     walk in CTA pairs sharing every B chunk by cluster multicast
-    (REFSIG_TC_MC=1, chunked path; 600 queries: an odd number of row groups,
-    so one CTA of a pair runs a ghost half)."""
+    (REFSIG_TC_MC=1, chunked path), and the cta_group::2 kernel (REFSIG_TC2=1:
+    M = 256 over a CTA pair, each SM holding half of every B chunk; applies
+    at K' > 128). 600 queries: an odd number of row blocks, so one CTA of a
+    pair runs a ghost half."""
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     code = _STRIPE_SNIPPET.format(repo=repo, K=K, NQ=NQ)
     out = {}
-    for mode in ("0", "1", "mc"):
-        env = dict(os.environ, REFSIG_TC_STRIPE="1" if mode == "mc" else mode, REFSIG_TC_MC="1" if mode == "mc" else "0")
+    for mode in ("0", "1", "mc", "pair"):
+        env = dict(os.environ, REFSIG_TC_STRIPE="0" if mode == "0" else "1", REFSIG_TC_MC="1" if mode == "mc" else "0",
+                   REFSIG_TC2="1" if mode == "pair" else "0")
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         out[mode] = r.stdout.strip().splitlines()[-1]
-    assert out["0"] == out["1"] == out["mc"] and int(out["0"].split()[0]) > 0, out
+    assert out["0"] == out["1"] == out["mc"] == out["pair"] and int(out["0"].split()[0]) > 0, out
 
 
 _EMIT_SNIPPET = r"""
