@@ -489,7 +489,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc_kernel(TcArgs a) {
 // multicast to both CTAs (ring stages, A buffers, accumulators).
 // Items: (column stripe, row-group pair) as in the stripe-major walk; rank r
 // takes row block 2 gp + r (a ghost half without stores when the count is odd).
-constexpr uint32_t kTc2ChunkBytes = 64u * kTcChunkK * 2u;  // one K chunk of a 64-doc B half panel: 8 KB
+constexpr uint32_t kTc2ChunkK = 64;  // K halves per B stage: 8 KB of a 64-doc half panel (16 KB stages, 7 of
+                                     // them, measured 7.40 vs 6.92 ms at configs[4])
+constexpr uint32_t kTc2ChunkBytes = 64u * kTc2ChunkK * 2u;
 
 struct Tc2Walk {
   uint32_t p, c, item, cend;
@@ -625,11 +627,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a) {
           __syncwarp();
           const uint32_t e = elect_one();
           tc_fence_after();
-          const uint32_t steps = ch + 1 < NCH ? kTcChunkK / 16 : LAST;
-          const uint64_t dB = dB0 + st * dCB, dAc = dA + ch * (kTcChunkK / 16) * 256u;
+          const uint32_t steps = ch + 1 < NCH ? kTc2ChunkK / 16 : LAST;
+          const uint64_t dB = dB0 + st * dCB, dAc = dA + ch * (kTc2ChunkK / 16) * 256u;
+          if (!(a.dbg & 4)) {
 #pragma unroll
-          for (uint32_t j = 0; j < kTcChunkK / 16; ++j)
-            if (j < steps) mma2_f16_e(e, d0, dAc + j * 256, dB + j * 128, (ch | j) != 0);
+            for (uint32_t j = 0; j < kTc2ChunkK / 16; ++j)
+              if (j < steps) mma2_f16_e(e, d0, dAc + j * 256, dB + j * 128, (ch | j) != 0);
+          }
           mma2_commit_mc_e(e, &empty_bar[st], 3);
         }
         __syncwarp();
@@ -690,7 +694,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mb_arrive(&tempty_bar[acc]);
-        if (valid) {
+        if (valid && !(a.dbg & 1)) {
           uint32_t b[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k) b[k] = 0;
@@ -1117,12 +1121,16 @@ void launch_mrc_tc2(const void* rowf, const void* colf, uint32_t K, const PairGr
   a.abufs = 2u * PB + 4u * kTc2ChunkBytes <= kTcSmemBudget ? 2u : 1u;
   a.stages = std::min<uint32_t>(kTcMaxStages, (kTcSmemBudget - a.abufs * PB) / kTc2ChunkBytes);
   a.CB = kTc2ChunkBytes;
-  a.nch = static_cast<uint32_t>(ceil_div(a.KP, kTcChunkK));
-  a.last_steps = (a.KP - kTcChunkK * (a.nch - 1)) / 16;
+  a.nch = static_cast<uint32_t>(ceil_div(a.KP, kTc2ChunkK));
+  a.last_steps = (a.KP - kTc2ChunkK * (a.nch - 1)) / 16;
   a.n_groups = a.rb1 - a.rb0;
   a.bitmap = bitmap;
   a.rowcnt = rowcnt;
   a.two = 2;
+  {
+    const char* m = std::getenv("REFSIG_TC_DEBUG");  // timing experiments: 1 no epilogue math, 4 no MMA
+    a.dbg = m ? static_cast<uint32_t>(std::atoi(m)) : 0u;
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
