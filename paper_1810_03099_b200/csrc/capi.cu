@@ -574,7 +574,8 @@ void run_mrc_tiles(refsig_gpu_ctx* c, const float* STr, uint32_t ldr, uint32_t n
     colf = db->tc_colf.as<char>();
     launched("tcgen05 operand forms");
     if (pair) {
-      launch_mrc_tc2(rowf, colf, K, g, c->bitmap.as<uint32_t>(), c->rowcnt.as<uint32_t>(), c->stream);
+      if (!launch_mrc_tc2(rowf, colf, K, g, c->bitmap.as<uint32_t>(), c->rowcnt.as<uint32_t>(), c->stream))
+        fail(REFSIG_E_RUNTIME, "CTA-pair K3: TMA descriptor (cuTensorMapEncodeTiled) failed");
       return;
     }
   }

@@ -37,6 +37,8 @@
 // bitmap/rowcnt format as the CUDA-core kernel (k3_pairs.cu), so the scan
 // and emitter are shared.
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 
 #include <cstdio>
@@ -519,10 +521,10 @@ struct Tc2Walk {
   }
 };
 
-__global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a, const __grid_constant__ CUtensorMap bmap) {
   extern __shared__ __align__(1024) uint8_t tsm[];
   constexpr uint32_t NACC = 4;  // 4 x 128 TMEM columns: the MMAs run up to three tiles ahead of the epilogues
-  __shared__ __align__(8) uint64_t full_bar[kTcMaxStages], empty_bar[kTcMaxStages], ptile_bar[2], afull_bar[2],
+  __shared__ __align__(8) uint64_t full_bar[kTcMaxStages], empty_bar[kTcMaxStages], afull_bar[2],
       pafull_bar[2], aempty_bar[2], tfull_bar[NACC], tempty_bar[NACC], ptempty_bar[NACC];
   __shared__ uint32_t tmem_base_sh;
   const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
@@ -538,7 +540,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a) {
       mb_init(&empty_bar[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
-      mb_init(&ptile_bar[s], 1);
       mb_init(&afull_bar[s], 1);
       mb_init(&pafull_bar[s], 1);
       mb_init(&aempty_bar[s], 1);
@@ -577,16 +578,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a) {
                    PB, &afull_bar[ab]);
           ++g;
         }
-        // the 64-document half panel 2 bj + rank of the column forms
-        const uint8_t* src =
-            reinterpret_cast<const uint8_t*>(a.Bc) + static_cast<size_t>(2 * w.c + rank) * (PB / 2);
+        // the 64-document half panel 2 bj + rank of the column forms, one 8 KB box per K chunk by
+        // TMA with .cta_group::2: both CTAs' boxes complete the LEADER's stage barrier (peer bit
+        // cleared), so no forwarding sits in the refill chain
+        const uint32_t c_base = (2 * w.c + rank) * (a.KP / 8);
+        const uint32_t bar_mask = 0xFEFFFFFFu;
         for (uint32_t ch = 0; ch < NCH; ++ch, ++q) {
           const uint32_t st = q % S;
           if (q >= S) mb_wait_cluster(&empty_bar[st], ((q / S) - 1) & 1u);
-          const uint32_t bytes = ch + 1 < NCH ? kTc2ChunkBytes : LAST * 2048u;
-          mb_expect_tx(&full_bar[st], bytes);
-          bulk_g2s(sBbase + static_cast<size_t>(st) * kTc2ChunkBytes, src + static_cast<size_t>(ch) * kTc2ChunkBytes,
-                   bytes, &full_bar[st]);
+          if (rank == 0) mb_expect_tx(&full_bar[st], 2u * kTc2ChunkBytes);
+          asm volatile(
+              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(sBbase + static_cast<size_t>(st) * kTc2ChunkBytes)),
+              "l"(reinterpret_cast<uint64_t>(&bmap)), "r"(smem_u32(&full_bar[st]) & bar_mask), "r"(0),
+              "r"((c_base + ch * (kTc2ChunkK / 8)) * 2u)  // 1 KB chunks = two 512-byte rows
+              : "memory");
         }
         new_group = w.next(a);
       }
@@ -615,15 +621,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a) {
           mb_wait_cluster(&ptempty_bar[acc], ((it / NACC) - 1) & 1u);
           __syncwarp();
         }
-        // the peer's B halves of this whole tile have landed (forwarded once per tile: a release
-        // remote arrive per 8 KB chunk made the forwarder the bottleneck)
-        mb_wait_cluster(&ptile_bar[it & 1], (it >> 1) & 1u);
-        __syncwarp();
         const uint64_t dA = dA0 + ab * dPB;
         const uint32_t d0 = tmem + acc * 128;
         for (uint32_t ch = 0; ch < NCH; ++ch, ++q) {
           const uint32_t st = q % S;
-          mb_wait(&full_bar[st], (q / S) & 1u);
+          mb_wait_cluster(&full_bar[st], (q / S) & 1u);  // both halves (the peer's box completes it too)
           __syncwarp();
           const uint32_t e = elect_one();
           tc_fence_after();
@@ -646,7 +648,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a) {
     } else if (n_it && lane == 0) {  // peer: forward A / B fill completions to the leader
       Tc2Walk w;
       w.start(a);
-      uint32_t g = 0, q = 0;
+      uint32_t g = 0;
       bool new_group = true;
       for (uint32_t it = 0; it < n_it; ++it) {
         if (new_group) {
@@ -654,8 +656,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a) {
           mb_arrive_remote(&pafull_bar[g % ABUFS], 0);
           ++g;
         }
-        for (uint32_t ch = 0; ch < NCH; ++ch, ++q) mb_wait(&full_bar[q % S], (q / S) & 1u);
-        mb_arrive_remote(&ptile_bar[it & 1], 0);
         new_group = w.next(a);
       }
     }
@@ -1104,7 +1104,7 @@ bool mrc_tc2_applies(uint32_t K, const PairGrid& g) {
   return mode == 1 || nbc >= 8u * 74u;
 }
 
-void launch_mrc_tc2(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
+bool launch_mrc_tc2(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
                     uint32_t* rowcnt, cudaStream_t s) {
   TcArgs a{};
   a.Ar = static_cast<const __half*>(rowf);
@@ -1115,7 +1115,7 @@ void launch_mrc_tc2(const void* rowf, const void* colf, uint32_t K, const PairGr
   a.nbc = static_cast<uint32_t>(ceil_div(g.n_cols, 128));
   a.rb0 = g.row_begin / 128;
   a.rb1 = std::min(static_cast<uint32_t>(ceil_div(g.row_end, 128)), a.nbr);
-  if (g.row_end <= g.row_begin || a.rb1 <= a.rb0 || a.nbc == 0) return;
+  if (g.row_end <= g.row_begin || a.rb1 <= a.rb0 || a.nbc == 0) return true;
   const uint32_t PB = 256u * a.KP;
   a.rb = 1;
   a.abufs = 2u * PB + 4u * kTc2ChunkBytes <= kTcSmemBudget ? 2u : 1u;
@@ -1141,11 +1141,31 @@ void launch_mrc_tc2(const void* rowf, const void* colf, uint32_t K, const PairGr
   const size_t smem = std::max<size_t>(static_cast<size_t>(a.abufs) * PB + static_cast<size_t>(a.stages) * kTc2ChunkBytes,
                                        116u * 1024u);
   ensure_smem(mrc_tc2_kernel, smem);
+  // the column forms as 512-byte rows of u16 (a 2-D box of 256 x 16 = one contiguous 8 KB chunk; a
+  // [8 halves][64 docs][chunks] 3-D view with 16-byte inner rows measured 9.25 vs 6.92 ms)
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return false;  // the caller reports it
+  CUtensorMap bmap;
+  const cuuint64_t n64 = 2ull * a.nbc;
+  const cuuint64_t gdim[2] = {256, n64 * (a.KP / 8) * 2};
+  const cuuint64_t gstride[1] = {512};
+  const cuuint32_t box[2] = {256, kTc2ChunkBytes / 512};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult er = encode(&bmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(colf), gdim, gstride, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (er != CUDA_SUCCESS) return false;
   if (std::getenv("REFSIG_TC_PRINT"))
     std::fprintf(stderr, "mrc_tc2: KP %u nch %u last %u abufs %u stages %u smem %zu grid %u stripe %u groups %u nbc %u\n",
                  a.KP, a.nch, a.last_steps, a.abufs, a.stages, smem, grid, a.stripe, a.n_groups, a.nbc);
-  launch_pdl_cluster2(mrc_tc2_kernel, dim3(grid), dim3(kTcThreads), smem, s, a);
+  launch_pdl_cluster2(mrc_tc2_kernel, dim3(grid), dim3(kTcThreads), smem, s, a, bmap);
   note_launch();
+  return true;
 }
 
 size_t ham_tc_form_bytes(uint32_t n) { return static_cast<size_t>(ceil_div(n, 128)) * 128 * kHamKPBytes; }

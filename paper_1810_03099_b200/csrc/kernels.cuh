@@ -152,7 +152,8 @@ void launch_mrc_tc_forms(const float* ST, uint32_t ld, uint32_t n_docs, uint32_t
                          uint32_t* rowcnt, uint32_t n_rowcnt, cudaStream_t s, bool col64 = false);
 // CTA-pair (cta_group::2) K3 for the chunked query join; column forms in 64-document panels (col64).
 bool mrc_tc2_applies(uint32_t K, const PairGrid& g);
-void launch_mrc_tc2(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
+// false: the TMA descriptor could not be built (cuTensorMapEncodeTiled unavailable / failed)
+bool launch_mrc_tc2(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
                     uint32_t* rowcnt, cudaStream_t s);
 void launch_mrc_tc(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
                    uint32_t* rowcnt, cudaStream_t s);
