@@ -555,7 +555,14 @@ void run_mrc_tiles(refsig_gpu_ctx* c, const float* STr, uint32_t ldr, uint32_t n
     c->tc_forms.ensure(rb + cb);
     rowf = c->tc_forms.as<char>();
     colf = rowf + rb;
-    launch_mrc_tc_forms(STr, ldr, nr, K, tau, rowf, colf, c->rowcnt.as<uint32_t>(), g.n_rows, c->stream);
+    const bool pair = mrc_tc2_applies(K, g);  // CTA-pair kernel: column forms in 64-document panels
+    launch_mrc_tc_forms(STr, ldr, nr, K, tau, rowf, colf, c->rowcnt.as<uint32_t>(), g.n_rows, c->stream, pair);
+    if (pair) {
+      launched("tcgen05 operand forms");
+      if (!launch_mrc_tc2(rowf, colf, K, g, c->bitmap.as<uint32_t>(), c->rowcnt.as<uint32_t>(), c->stream))
+        fail(REFSIG_E_RUNTIME, "CTA-pair K3: TMA descriptor (cuTensorMapEncodeTiled) failed");
+      return;
+    }
   } else {
     // query join: the database's column forms do not depend on tau and stay
     // valid until it is signed again, so they are built once per database

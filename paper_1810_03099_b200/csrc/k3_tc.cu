@@ -496,25 +496,50 @@ constexpr uint32_t kTc2ChunkK = 64;  // K halves per B stage: 8 KB of a 64-doc h
 constexpr uint32_t kTc2ChunkBytes = 64u * kTc2ChunkK * 2u;
 
 struct Tc2Walk {
-  uint32_t p, c, item, cend;
+  uint32_t p, c, item, cend, gp;  // p: this CTA's row block (relative to rb0), c: absolute column block
   bool ghost;
+  // rectangle: stripe-major items (stripe, row-block pair gp); triangle: the pair's contiguous range of
+  // pair tiles, pair group gp = row blocks rb0 + 2 gp (+1), columns from rb0 + 2 gp (the lower block;
+  // the upper block's tile on that column lies below the diagonal and is masked)
+  __device__ uint32_t tri_cs(const TcArgs& a, uint32_t g) const { return a.rb0 + 2 * g; }
+  __device__ void set_rows(const TcArgs& a) {
+    p = 2 * gp + (blockIdx.x & 1u);
+    ghost = a.rb0 + p >= a.rb1;
+    if (ghost) p = 2 * gp;  // valid operands, results discarded
+  }
   __device__ void set_item(const TcArgs& a) {
     const uint32_t ngp = (a.n_groups + 1) / 2;
-    const uint32_t st = item / ngp, gp = item % ngp;
-    p = 2 * gp + (blockIdx.x & 1u);
-    ghost = p >= a.n_groups;
-    if (ghost) p = 2 * gp;
+    const uint32_t st = item / ngp;
+    gp = item % ngp;
+    set_rows(a);
     c = st * a.stripe;
     cend = min(c + a.stripe, a.nbc);
   }
-  __device__ void start(const TcArgs& a) {
+  __device__ void start(const TcArgs& a, uint64_t t) {
+    if (a.g.triangle) {
+      gp = 0;
+      while (t >= a.nbc - tri_cs(a, gp)) {
+        t -= a.nbc - tri_cs(a, gp);
+        ++gp;
+      }
+      set_rows(a);
+      c = tri_cs(a, gp) + static_cast<uint32_t>(t);
+      cend = a.nbc;
+      return;
+    }
     item = blockIdx.x >> 1;
     set_item(a);
   }
   __device__ bool next(const TcArgs& a) {
     if (++c == cend) {
-      item += gridDim.x >> 1;
-      set_item(a);
+      if (a.g.triangle) {
+        ++gp;
+        set_rows(a);
+        c = tri_cs(a, gp);
+      } else {
+        item += gridDim.x >> 1;
+        set_item(a);
+      }
       return true;
     }
     return false;
@@ -529,7 +554,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a, const 
   __shared__ uint32_t tmem_base_sh;
   const uint32_t warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0), lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
-  const uint32_t n_it = tc_striped_tiles<true>(a);
+  const uint32_t npairs = gridDim.x >> 1, pair = blockIdx.x >> 1;
+  const uint64_t pt0 = a.n_tiles * pair / npairs, pt1 = a.n_tiles * (pair + 1) / npairs;  // triangle: pair tiles
+  const uint32_t n_it = a.g.triangle ? static_cast<uint32_t>(pt1 - pt0) : tc_striped_tiles<true>(a);
   const uint32_t PB = 256u * a.KP;                    // bytes of one 128-row A panel
   const uint32_t S = a.stages, NCH = a.nch, ABUFS = a.abufs, LAST = a.last_steps;
   uint8_t* sAbase = tsm;                               // ABUFS A panels
@@ -566,7 +593,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a, const 
   if (warp == 0) {
     if (lane == 0 && n_it) {  // producer (both CTAs): own A block, own B halves
       Tc2Walk w;
-      w.start(a);
+      w.start(a, pt0);
       uint32_t g = 0, q = 0;
       bool new_group = true;
       for (uint32_t it = 0; it < n_it; ++it) {
@@ -601,7 +628,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a, const 
   } else if (warp == 1) {
     if (n_it && rank == 0) {  // leader: the MMA issuer
       Tc2Walk w;
-      w.start(a);
+      w.start(a, pt0);
       const uint64_t dA0 = smem_desc(smem_u32(sAbase));
       const uint64_t dB0 = smem_desc_lbo(smem_u32(sBbase), 1024u);
       const uint64_t dPB = PB >> 4, dCB = kTc2ChunkBytes >> 4;
@@ -647,7 +674,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a, const 
       }
     } else if (n_it && lane == 0) {  // peer: forward A / B fill completions to the leader
       Tc2Walk w;
-      w.start(a);
+      w.start(a, pt0);
       uint32_t g = 0;
       bool new_group = true;
       for (uint32_t it = 0; it < n_it; ++it) {
@@ -675,7 +702,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a, const 
     const uint32_t wpr = a.g.words_per_row;
     const uint32_t two = a.two;
     Tc2Walk w;
-    if (n_it) w.start(a);
+    if (n_it) w.start(a, pt0);
     uint32_t cnt = 0;
     for (uint32_t it = 0; it < n_it; ++it) {
       const uint32_t acc = it % NACC;
@@ -685,7 +712,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a, const 
       if ((it & 1) == eg) {
         mb_wait_warp(&tfull_bar[acc], (it / NACC) & 1u);
         tc_fence_after();
-        const bool valid = !w.ghost && r < a.rb1;
+        const bool valid = !w.ghost && r < a.rb1 && !(a.g.triangle && bj < r);
         uint32_t v0[32], v1[32];
         const uint32_t ta = tmem + ((q * 32u) << 16) + acc * 128 + h * 64;
         TC_LD32(ta, v0);
@@ -710,7 +737,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mrc_tc2_kernel(TcArgs a, const 
           }
           uint32_t m0 = ~__byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
           uint32_t m1 = ~__byte_perm(__byte_perm(b[4], b[5], 0x0040), __byte_perm(b[6], b[7], 0x0040), 0x5410);
-          if (bj + 1 == a.nbc) {
+          if ((a.g.triangle && bj == r) || bj + 1 == a.nbc) {
             const uint32_t c0 = bj * 128 + h * 64;
             m0 &= tc_col_mask(c0, i, a.g);
             m1 &= tc_col_mask(c0 + 32, i, a.g);
@@ -781,7 +808,7 @@ __global__ void __launch_bounds__(256) ham_forms_kernel(const uint64_t* __restri
 __global__ void __launch_bounds__(256) tc_forms_kernel(const float* __restrict__ ST, uint32_t ld, uint32_t n_docs,
                                                        uint32_t K, uint32_t KP, float tau, __half* __restrict__ rowf,
                                                        __half* __restrict__ colf, uint32_t* __restrict__ rowcnt,
-                                                       uint32_t n_rowcnt) {
+                                                       uint32_t n_rowcnt, uint32_t col64) {
   extern __shared__ __align__(16) __half fsm[];
   pdl_wait();
   // the tile kernel's row counts start at zero: zeroed here, 128 per panel (no memset node before this PDL launch)
@@ -840,7 +867,12 @@ __global__ void __launch_bounds__(256) tc_forms_kernel(const float* __restrict__
     const uint32_t kc = idx >> 7, dl = idx & 127;
     const size_t off = base + (static_cast<size_t>(kc) * 128 + dl) * 8;
     if (rowf) *reinterpret_cast<uint4*>(rowf + off) = *reinterpret_cast<const uint4*>(R + dl * stride + kc * 8);
-    if (colf) *reinterpret_cast<uint4*>(colf + off) = *reinterpret_cast<const uint4*>(C + dl * stride + kc * 8);
+    if (colf) {  // col64: 64-document panels (the B halves of the CTA-pair kernel)
+      const size_t o = col64 ? (static_cast<size_t>(2 * pan + (dl >> 6)) * chunks + kc) * 64 * 8 +
+                                   static_cast<size_t>(dl & 63) * 8
+                             : off;
+      *reinterpret_cast<uint4*>(colf + o) = *reinterpret_cast<const uint4*>(C + dl * stride + kc * 8);
+    }
   }
 }
 
@@ -961,7 +993,7 @@ void launch_mrc_tc_forms(const float* ST, uint32_t ld, uint32_t n_docs, uint32_t
   const size_t smem = 2ull * 128 * (KP + 8) * sizeof(__half);  // <= 69.6 KB at K' = 128
   ensure_smem(tc_forms_kernel, 72 * 1024);
   launch_pdl(tc_forms_kernel, dim3(n_pan), dim3(256), smem, s, ST, ld, n_docs, K, KP, tau, static_cast<__half*>(rowf),
-             static_cast<__half*>(colf), rowcnt, n_rowcnt);
+             static_cast<__half*>(colf), rowcnt, n_rowcnt, col64 ? 1u : 0u);
   note_launch();
 }
 
@@ -1096,12 +1128,14 @@ bool mrc_tc2_applies(uint32_t K, const PairGrid& g) {
     const char* m = std::getenv("REFSIG_TC2");
     return m ? std::atoi(m) : -1;
   }();
-  if (mode == 0 || g.triangle) return false;
+  if (mode == 0) return false;
   const uint32_t KP = mrc_tc_kp(K);
   const uint32_t nbc = static_cast<uint32_t>(ceil_div(g.n_cols, 128));
   const uint32_t rb0 = g.row_begin / 128, rb1 = static_cast<uint32_t>(ceil_div(g.row_end, 128));
-  if (KP <= kTcSmallKP || KP > 512 || rb1 - rb0 < 2) return false;
-  return mode == 1 || nbc >= 8u * 74u;
+  if (KP > 512 || rb1 - rb0 < 2) return false;
+  if (mode == 1) return true;
+  if (g.triangle) return false;  // (measured below; see DESIGN)
+  return KP > kTcSmallKP && nbc >= 8u * 74u;
 }
 
 bool launch_mrc_tc2(const void* rowf, const void* colf, uint32_t K, const PairGrid& g, uint32_t* bitmap,
@@ -1135,9 +1169,14 @@ bool launch_mrc_tc2(const void* rowf, const void* colf, uint32_t K, const PairGr
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid = static_cast<unsigned>(sms) & ~1u;
-  a.stripe = static_cast<uint32_t>(ceil_div(a.nbc, grid / 2));
-  uint64_t T = 0;
-  a.n_tiles = T;
+  if (g.triangle) {  // pair tiles: row-block pairs x their columns from the lower block
+    uint64_t T = 0;
+    for (uint32_t r0 = a.rb0; r0 < a.rb1; r0 += 2) T += a.nbc - r0;
+    a.n_tiles = T;
+    a.stripe = 0;
+  } else {
+    a.stripe = static_cast<uint32_t>(ceil_div(a.nbc, grid / 2));
+  }
   const size_t smem = std::max<size_t>(static_cast<size_t>(a.abufs) * PB + static_cast<size_t>(a.stages) * kTc2ChunkBytes,
                                        116u * 1024u);
   ensure_smem(mrc_tc2_kernel, smem);

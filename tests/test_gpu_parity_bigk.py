@@ -251,3 +251,20 @@ def test_exact_multi_panel_equals_single_panel():
         assert r.returncode == 0, r.stderr[-2000:]
         out[panel] = r.stdout.strip().splitlines()[-1]
     assert out[""] == out["1024"] and int(out[""].split()[0]) > 0, out
+
+
+@pytest.mark.parametrize("name,n,K", [("c0", 0, 10), ("c1", 4000, 128)])
+def test_self_join_pair_kernel_equals_single_cta(name, n, K):
+    """The cta_group::2 kernel on the triangle (forced with REFSIG_TC2=1: the
+    auto choice keeps it for the wide query join, where it is faster) writes
+    the same candidates as the one-CTA tcgen05 kernel, at K' <= 128 and at
+    K' = 400 (odd row-block counts run a ghost half)."""
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mode in ("0", "1"):
+        env = dict(os.environ, REFSIG_TC2=mode)
+        r = subprocess.run([sys.executable, os.path.join(repo, "tools", "tc2_self_probe.py"), name, str(n), str(K)],
+                           env=env, capture_output=True, text=True, timeout=600, cwd=repo)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[mode] = r.stdout.strip().splitlines()
+    assert out["0"] == out["1"] and int(out["0"][0]) > 0, out

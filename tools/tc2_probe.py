@@ -1,3 +1,5 @@
+"""configs[4]-shaped query join (6,000-doc database, K = 128): candidate count
+and hash, for comparing K3 kernel variants.  python tools/tc2_probe.py [n_queries]"""
 import hashlib, sys, os
 sys.path.insert(0, os.getcwd())
 import numpy as np
