@@ -74,13 +74,15 @@ def main():
     dbc.set_profiling(False)
     db_sig_ms = sum(ph[k][0] for k in ("count", "reference", "sign"))
     qc.attach_database(dbc)
-    # warm-up batch (sizes buffers, builds the database column forms)
-    qc.load_corpus(*batches[0])
-    qc.count()
-    qc.sign(fetch=False)
-    qc.mrc_query_pairs(tau, fetch=False)
-    qc.simhash(0)
-    qc.hamming_query_pairs(thr["hamming_max"], fetch=False)
+    # warm-up: every batch once (sizes the streaming buffers for the largest batch, builds the
+    # database column forms)
+    for wb in batches:
+        qc.load_corpus(*wb)
+        qc.count()
+        qc.sign(fetch=False)
+        qc.mrc_query_pairs(tau, fetch=False)
+        qc.simhash(0)
+        qc.hamming_query_pairs(thr["hamming_max"], fetch=False)
     torch.cuda.synchronize(dev)
     # streamed batches
     qc.set_profiling(True)
@@ -88,14 +90,16 @@ def main():
     with torch.cuda.stream(stream):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         qc.stage_corpus(*batches[1])
+        if args.batches >= 2:
+            qc.stage_corpus(*batches[2])  # two batches staged ahead
         e0.record(stream)
         w0 = time.time()
         for b in range(1, args.batches + 1):
             qc.swap_corpus()
-            if b + 1 <= args.batches:
-                qc.stage_corpus(*batches[b + 1])  # upload of the next batch overlaps this one
             qc.count()
             qc.sign(fetch=False)
+            if b + 2 <= args.batches:
+                qc.stage_corpus(*batches[b + 2])  # host plan + upload of a later batch overlap this one
             cands.append(qc.mrc_query_pairs(tau, fetch=False))
             qc.simhash(0)
             hams.append(qc.hamming_query_pairs(thr["hamming_max"], fetch=False))

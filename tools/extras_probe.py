@@ -18,4 +18,5 @@ if mode == "c3c4":
     r = bench.measure_c3(dev)
     print("c3", json.dumps({k: r[k] for k in ("candidates",)}), flush=True)
 r = bench.measure_c4(dev)
-print(mode, json.dumps({k: r.get(k) for k in ("ms_per_batch", "wall_ms_per_batch", "phase_ms_per_batch")}), flush=True)
+print(mode, json.dumps({k: r.get(k) for k in ("ms_per_batch", "ms_each_batch", "wall_ms_per_batch", "host_ms_per_call",
+                                               "phase_ms_per_batch")}), flush=True)
