@@ -1056,9 +1056,11 @@ def rooflines(phases, sign_iso_ms, N, K, pairs, cp, peaks, peaks_src, n_sm, cloc
                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; fp16 kind::f16 has the same rate)",
                         "mma_flops_per_launch": mma_flops, "k_prime": kp, "blocks_128x128": blocks,
                         "fp32_equiv_tflops": 2.0 * K * pairs / (t3 / 1e3) / 1e12 if t3 else 0.0,
-                        "note": "phase = operand-form kernel + tcgen05 tile kernel; per tile the epilogue's "
-                                "sign-bit packing (1 ALU op per pair, ALU pipe 2 cyc/warp-instr) matches the "
-                                "MMA time, see DESIGN.md K3",
+                        "tmem_read_bytes_per_launch": blocks * 128 * 128 * 4,
+                        "tmem_read_gbps": blocks * 128 * 128 * 4 / (t3 / 1e3) / 1e9 if t3 else 0.0,
+                        "note": "phase = operand-form kernel + tcgen05 tile kernel. At K' = 64 the MMAs are a "
+                                "third of the per-tile time: every pair's fp32 accumulator is read out of TMEM "
+                                "(4 B per pair for one sign bit; tmem_read_gbps), see DESIGN.md K3 / section 10",
                         "share_of_step": t3 / ms_per_step}
     # K2: HBM bound; survey §8d per-signature bytes 8*nnz + 4*K + 4.
     nnz = nnz_total(cp)
