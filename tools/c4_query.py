@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--db-docs", type=int, default=0)
     ap.add_argument("--tau", type=float, default=None)
     ap.add_argument("--path", choices=["auto", "tensor", "fp32"], default="auto")
+    ap.add_argument("--K", type=int, default=0, help="override configs[4]'s K (measurement)")
     args = ap.parse_args()
     import torch
     import paper_1810_03099_b200 as R
@@ -52,7 +53,7 @@ def main():
         pin[:] = qb.tokens
         batches.append((pin, qb.doc_off, qb.vocab))
     gen_s = time.time() - t
-    K = cfg["K"]
+    K = args.K or cfg["K"]
     refs = C.sample_refs(cfg["ref_seed"], db.n_docs, K)
     dev = torch.device("cuda", 0)
     dbc = R.Context(0)
