@@ -359,6 +359,31 @@ __global__ void __launch_bounds__(256) hamming_bitmap_kernel(const uint64_t* __r
   }
 }
 
+// The set bits of `word` as ascending column ids col + b at dst[0..): the
+// word is bit-reversed once, then each bit is one FLO + one XOR; two bits per
+// loop step (the loop runs max-over-lanes times, so its overhead counts).
+#ifndef REFSIG_EMIT_PAIRLOOP
+#define REFSIG_EMIT_PAIRLOOP 1
+#endif
+template <class T>
+__device__ __forceinline__ void expand_word(uint32_t word, uint32_t col, T* dst) {
+#if REFSIG_EMIT_PAIRLOOP
+  uint32_t rw = __brev(word);
+  while (rw) {
+    const uint32_t b0 = __clz(rw);
+    rw ^= 0x80000000u >> b0;
+    dst[0] = col + b0;
+    if (!rw) break;
+    const uint32_t b1 = __clz(rw);
+    rw ^= 0x80000000u >> b1;
+    dst[1] = col + b1;
+    dst += 2;
+  }
+#else
+  for (; word; word &= word - 1) *dst++ = col + (__ffs(word) - 1);
+#endif
+}
+
 // Warp per row: the row's set bits as ascending column ids at
 // out[rowstart[i] ..). A row is read in batches of 128 words (4096 columns),
 // lane l loading words c + 32k + l (k = 0..3: four coalesced 128-byte loads;
@@ -432,11 +457,9 @@ __global__ void __launch_bounds__(256) emit_kernel(const uint32_t* __restrict__ 
           for (; word; word &= word - 1, ++pos)
             if (pos < capacity) out[pos] = col + (__ffs(word) - 1);
         } else if (tot <= direct_max) {
-          uint32_t* o = out + base + ex;
-          for (; word; word &= word - 1) *o++ = col + (__ffs(word) - 1);
+          expand_word(word, col, out + base + ex);
         } else {
-          uint32_t o = ex;
-          for (; word; word &= word - 1) stage[o++] = col + (__ffs(word) - 1);
+          expand_word(word, col, stage + ex);
           __syncwarp();
           uint32_t* dst = out + base;
           for (uint32_t e = lane; e < tot; e += 32) dst[e] = stage[e];
@@ -516,11 +539,9 @@ __global__ void __launch_bounds__(256) emit_wide_kernel(const uint32_t* __restri
         for (; word; word &= word - 1, ++pos)
           if (pos < capacity) out[pos] = col + (__ffs(word) - 1);
       } else if (tot <= direct_max) {
-        uint32_t* o = out + base + ex;
-        for (; word; word &= word - 1) *o++ = col + (__ffs(word) - 1);
+        expand_word(word, col, out + base + ex);
       } else {
-        uint32_t o = ex;
-        for (; word; word &= word - 1) stage[o++] = col + (__ffs(word) - 1);
+        expand_word(word, col, stage + ex);
         __syncwarp();
         uint32_t* dst = out + base;
         for (uint32_t e = lane; e < tot; e += 32) dst[e] = stage[e];
