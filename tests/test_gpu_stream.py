@@ -138,3 +138,41 @@ def test_async_csr16_fetch_equals_sync(gpu_ctx_factory):
     # got holds batches 0,1 (read when their slots were reused) then 2,3
     for (wr, wc), (gr, gc) in zip(want, got):
         assert np.array_equal(wr, gr) and np.array_equal(wc, gc)
+
+
+def _ragged(V, n_docs=300, seed=1):
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, 900, n_docs)  # ragged: empty documents, T not a multiple of 32
+    off = np.zeros(n_docs + 1, np.uint64)
+    off[1:] = np.cumsum(lens)
+    tok = (rng.zipf(1.3, int(off[-1])) * 2654435761 % V).astype(np.uint32)
+    tok[: min(len(tok), 50)] = V - 1  # the widest id of the vocabulary
+    return tok, off
+
+
+@pytest.mark.parametrize("V", [30000, 65537, 130000, 1 << 20, (1 << 24) + 1])
+def test_stage_equals_load_vocab_widths(gpu_ctx_factory, V):
+    """A staged batch counts exactly like load_corpus at every id width."""
+    tok, off = _ragged(V)
+    a, b = gpu_ctx_factory(), gpu_ctx_factory()
+    b.stage_corpus(tok, off, V)
+    b.swap_corpus()
+    b.count()
+    a.load_corpus(tok, off, V)
+    a.count()
+    for x, y in zip(a.counts(), b.counts()):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("bad", [130001, 1 << 31])
+def test_stage_out_of_vocab(gpu_ctx_factory, bad):
+    """An id >= vocab in a staged batch is reported like in a loaded one."""
+    V = 130000
+    tok, off = _ragged(V)
+    tok[len(tok) // 2] = bad
+    b = gpu_ctx_factory()
+    b.stage_corpus(tok, off, V)
+    b.swap_corpus()
+    b.count()
+    with pytest.raises(R.ValidationError, match="vocab"):
+        b.synchronize()
