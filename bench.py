@@ -721,12 +721,19 @@ def measure_c3(dev, reps=3):
     with R.Context(torch.cuda.current_device()) as ctx, torch.cuda.stream(stream):
         ctx.set_stream(stream.cuda_stream)
         ctx.load_corpus(cp.tokens, cp.doc_off, cp.vocab)
-        ctx.set_profiling(True)
-        ctx.count(R.WEIGHT_TFIDF)
+        ctx.count(R.WEIGHT_TFIDF)  # first call: buffer allocation and first touch (~4 ms), not timed
         ctx.set_reference_docs(refs)
-        torch.cuda.synchronize(dev)
-        cnt_ph = ctx.phase_times()
-        ctx.set_profiling(False)
+        cnt_ph = None
+        for r in range(reps):  # best of reps, each after an L2 flush
+            flush.fill_(r + 10)
+            ctx.set_profiling(True)
+            ctx.count(R.WEIGHT_TFIDF)
+            ctx.set_reference_docs(refs)
+            torch.cuda.synchronize(dev)
+            ph = ctx.phase_times()
+            ctx.set_profiling(False)
+            if cnt_ph is None or ph["count"][0] < cnt_ph["count"][0]:
+                cnt_ph = ph
         rowptr, _, _ = ctx.counts()
         nnz = int(rowptr[-1])
         ctx.sign(fetch=False)
