@@ -193,10 +193,34 @@ __device__ __forceinline__ TermInfo sign_info(const TermInfo* p) {
 constexpr int kSignWarps = 8;
 constexpr uint32_t kSignStep = 128;
 
+// Hit walk by column groups (REFSIG_K2_CG, default): CG_L = KW/4 lanes per
+// hit, one float4 of its R row each, CG_H = 32/CG_L hits per pass. A warp load
+// then touches CG_H rows (~1.6 L1 wavefronts per 80-byte row) instead of 32
+// (one wavefront per lane: 5 per hit at KW = 20) — K2 is bound by L1
+// wavefronts (TermInfo gathers + R rows), not by bytes. Lane (g, j) keeps
+// the 4 column sums of group j over the hits g, g + CG_H, ... of the
+// document; sign_cg_columns adds them over g in a fixed order.
+#ifndef REFSIG_K2_CG
+#define REFSIG_K2_CG 1
+#endif
+template <int KW>
+struct SignCG {
+  static constexpr int L = KW / 4;   // lanes per hit
+  static constexpr int H = 32 / L;   // hits per pass (warp)
+  static constexpr int H2 = 16 / L;  // hits per pass (16-lane half)
+};
+#if REFSIG_K2_CG
+template <int KW>
+using SignAcc = float[4];
+#else
+template <int KW>
+using SignAcc = float[KW];
+#endif
+
 template <int KW>
 __device__ __forceinline__ void sign_slab_steps(const SignArgs& a, const uint2* __restrict__ e, uint32_t n,
                                                 uint32_t s0, uint32_t stride, uint32_t c0, uint32_t lane, int2* qw,
-                                                float (&acc)[KW], float& sq, bool do_sq) {
+                                                SignAcc<KW>& acc, float& sq, bool do_sq) {
   const uint32_t lt = (1u << lane) - 1u;
   for (uint32_t c = s0 * kSignStep; c < n; c += stride * kSignStep) {
     uint2 x[4];
@@ -220,6 +244,39 @@ __device__ __forceinline__ void sign_slab_steps(const SignArgs& a, const uint2* 
       qn += __popc(hits);
     }
     __syncwarp();
+#if REFSIG_K2_CG
+    {
+      constexpr uint32_t L = SignCG<KW>::L, H = SignCG<KW>::H;
+      const uint32_t g = lane / L, j = lane - g * L;
+      if (g < H) {
+        const float* __restrict__ Rj = a.R + c0 + 4 * j;
+        uint32_t h = g;
+        for (; h + H < qn; h += 2 * H) {  // two rows in flight per lane
+          const int2 h0 = qw[h], h1 = qw[h + H];
+          const float4 r0 = __ldg(reinterpret_cast<const float4*>(Rj + static_cast<uint32_t>(h0.x)));
+          const float4 r1 = __ldg(reinterpret_cast<const float4*>(Rj + static_cast<uint32_t>(h1.x)));
+          const float w0 = __int_as_float(h0.y), w1 = __int_as_float(h1.y);
+          acc[0] = fmaf(w0, r0.x, acc[0]);
+          acc[1] = fmaf(w0, r0.y, acc[1]);
+          acc[2] = fmaf(w0, r0.z, acc[2]);
+          acc[3] = fmaf(w0, r0.w, acc[3]);
+          acc[0] = fmaf(w1, r1.x, acc[0]);
+          acc[1] = fmaf(w1, r1.y, acc[1]);
+          acc[2] = fmaf(w1, r1.z, acc[2]);
+          acc[3] = fmaf(w1, r1.w, acc[3]);
+        }
+        if (h < qn) {
+          const int2 h0 = qw[h];
+          const float4 r0 = __ldg(reinterpret_cast<const float4*>(Rj + static_cast<uint32_t>(h0.x)));
+          const float w0 = __int_as_float(h0.y);
+          acc[0] = fmaf(w0, r0.x, acc[0]);
+          acc[1] = fmaf(w0, r0.y, acc[1]);
+          acc[2] = fmaf(w0, r0.z, acc[2]);
+          acc[3] = fmaf(w0, r0.w, acc[3]);
+        }
+      }
+    }
+#else
     for (uint32_t h = lane; h < qn; h += 32) {
       const int2 hv = qw[h];
       const float w = __int_as_float(hv.y);
@@ -240,8 +297,26 @@ __device__ __forceinline__ void sign_slab_steps(const SignArgs& a, const uint2* 
         }
       }
     }
+#endif
     __syncwarp();
   }
+}
+
+// Column sums of the column-group accumulators: col[0] = column `lane` (0
+// past KW) = sum over the hit slots g = 0 .. CG_H-1 of lane (g, lane/4)'s
+// component lane%4. tw: >= 128 floats of this warp.
+template <int KW>
+__device__ __forceinline__ float sign_cg_columns(const float (&acc)[4], uint32_t lane, float* tw) {
+  constexpr uint32_t L = SignCG<KW>::L, H = SignCG<KW>::H;
+  reinterpret_cast<float4*>(tw)[lane] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  __syncwarp();
+  float x = 0.0f;
+  if (lane < static_cast<uint32_t>(KW)) {
+#pragma unroll
+    for (uint32_t g = 0; g < H; ++g) x += tw[g * L * 4 + lane];
+  }
+  __syncwarp();
+  return x;
 }
 
 // Lane-order column sums of the warp's KW-vectors: col[t] = column
@@ -285,9 +360,13 @@ __device__ __forceinline__ void sign_half_docs(const SignArgs& a, uint32_t q, ui
   const uint32_t nmax = max(n, __shfl_xor_sync(0xffffffffu, n, 16));
   int2* qw = reinterpret_cast<int2*>(tw) + h * 64;
   const uint32_t lt = (1u << hl) - 1u;
+#if REFSIG_K2_CG
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#else
   float acc[KW];
 #pragma unroll
   for (int k = 0; k < KW; ++k) acc[k] = 0.0f;
+#endif
   float sq = 0.0f;
   for (uint32_t c = 0; c < nmax; c += 64) {
     uint2 x[4];
@@ -311,6 +390,24 @@ __device__ __forceinline__ void sign_half_docs(const SignArgs& a, uint32_t q, ui
       qn += __popc(mine);
     }
     __syncwarp();
+#if REFSIG_K2_CG
+    {
+      constexpr uint32_t L = SignCG<KW>::L, H2 = SignCG<KW>::H2;
+      const uint32_t g = hl / L, j = hl - g * L;
+      if (g < H2) {
+        const float* __restrict__ Rj = a.R + 4 * j;
+        for (uint32_t hh = g; hh < qn; hh += H2) {
+          const int2 hv = qw[hh];
+          const float4 r = __ldg(reinterpret_cast<const float4*>(Rj + static_cast<uint32_t>(hv.x)));
+          const float w = __int_as_float(hv.y);
+          acc[0] = fmaf(w, r.x, acc[0]);
+          acc[1] = fmaf(w, r.y, acc[1]);
+          acc[2] = fmaf(w, r.z, acc[2]);
+          acc[3] = fmaf(w, r.w, acc[3]);
+        }
+      }
+    }
+#else
     const uint32_t qmax = max(qn, __shfl_xor_sync(0xffffffffu, qn, 16));
     for (uint32_t hh = hl; hh < qmax; hh += 16) {
       if (hh < qn) {
@@ -327,8 +424,28 @@ __device__ __forceinline__ void sign_half_docs(const SignArgs& a, uint32_t q, ui
         }
       }
     }
+#endif
     __syncwarp();
   }
+#if REFSIG_K2_CG
+  // half h's column-group sums at tw[h][16][4]; lane hl adds columns hl and
+  // hl+16 over the half's hit slots in order
+  float* th = tw + h * 64;
+  reinterpret_cast<float4*>(th)[hl] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  __syncwarp();
+  float col0 = 0.0f, col1 = 0.0f;
+  {
+    constexpr uint32_t L = SignCG<KW>::L, H2 = SignCG<KW>::H2;
+    if (hl < static_cast<uint32_t>(KW)) {
+#pragma unroll
+      for (uint32_t g = 0; g < H2; ++g) col0 += th[g * L * 4 + hl];
+    }
+    if (hl + 16 < static_cast<uint32_t>(KW)) {
+#pragma unroll
+      for (uint32_t g = 0; g < H2; ++g) col1 += th[g * L * 4 + hl + 16];
+    }
+  }
+#else
   // transpose-sum: half h's 16 KW-vectors at tw[h][16][KW+1]; lane hl sums
   // columns hl and hl+16 over the half's 16 rows in lane order
   float* th = tw + h * 16 * (KW + 1);
@@ -344,6 +461,7 @@ __device__ __forceinline__ void sign_half_docs(const SignArgs& a, uint32_t q, ui
 #pragma unroll 8
     for (int l = 0; l < 16; ++l) col1 += th[l * (KW + 1) + hl + 16];
   }
+#endif
 #pragma unroll
   for (int o = 8; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
   const float inv = sq > 0.0f ? 1.0f / sqrtf(sq) : 0.0f;
@@ -411,12 +529,19 @@ __global__ void __launch_bounds__(256, KW <= 24 ? 4 : (KW <= 32 ? 3 : 2)) sign_k
   const uint32_t s0 = cta ? wid : 0u, stride = cta ? kSignWarps : 1u;
   float sq = 0.0f, inv = 0.0f, ss = 0.0f;
   for (uint32_t c0 = 0; c0 < a.K; c0 += KW) {
+    float col[CPL];
+#if REFSIG_K2_CG
+    static_assert(CPL == 1, "column groups: KW <= 32");
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    sign_slab_steps<KW>(a, e, n, s0, stride, c0, lane, qw, acc, sq, c0 == 0);
+    col[0] = sign_cg_columns<KW>(acc, lane, tw);
+#else
     float acc[KW];
 #pragma unroll
     for (int k = 0; k < KW; ++k) acc[k] = 0.0f;
     sign_slab_steps<KW>(a, e, n, s0, stride, c0, lane, qw, acc, sq, c0 == 0);
-    float col[CPL];
     sign_transpose_sum<KW, CPL>(acc, lane, tw, col);
+#endif
     if (c0 == 0) sq = warp_sum(sq);
     if (cta) {  // add the 8 warps' columns (and norms) in warp order
 #pragma unroll
