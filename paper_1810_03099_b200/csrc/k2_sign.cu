@@ -191,7 +191,12 @@ __device__ __forceinline__ TermInfo sign_info(const TermInfo* p) {
 #endif
 }
 constexpr int kSignWarps = 8;
-constexpr uint32_t kSignStep = 128;
+#ifndef REFSIG_K2_U
+#define REFSIG_K2_U 4
+#endif
+constexpr int kSignU = REFSIG_K2_U;                  // count entries per lane per step (K <= 32 warp path)
+constexpr uint32_t kSignStep = 32 * kSignU;
+constexpr uint32_t kSignStepC = 128;                 // K > 32 (sign_col_kernel)
 
 // Hit walk by column groups (REFSIG_K2_CG, default): CG_L = KW/4 lanes per
 // hit, one float4 of its R row each, CG_H = 32/CG_L hits per pass. A warp load
@@ -223,18 +228,18 @@ __device__ __forceinline__ void sign_slab_steps(const SignArgs& a, const uint2* 
                                                 SignAcc<KW>& acc, float& sq, bool do_sq) {
   const uint32_t lt = (1u << lane) - 1u;
   for (uint32_t c = s0 * kSignStep; c < n; c += stride * kSignStep) {
-    uint2 x[4];
+    uint2 x[kSignU];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kSignU; ++u) {
       const uint32_t i = c + 32u * u + lane;
       x[u] = i < n ? sign_ent(e + i) : make_uint2(0u, 0u);
     }
-    TermInfo ti[4];
+    TermInfo ti[kSignU];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) ti[u] = (c + 32u * u + lane < n) ? sign_info(a.info + x[u].x) : TermInfo{0.0f, -1};
+    for (int u = 0; u < kSignU; ++u) ti[u] = (c + 32u * u + lane < n) ? sign_info(a.info + x[u].x) : TermInfo{0.0f, -1};
     uint32_t qn = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kSignU; ++u) {
       const float w = static_cast<float>(x[u].y) * ti[u].idf;
       if (do_sq) sq = fmaf(w, w, sq);
       const uint32_t hits = __ballot_sync(0xffffffffu, ti[u].ref_row >= 0);
@@ -496,7 +501,10 @@ __device__ __forceinline__ void sign_zero_pad(const SignArgs& a) {
 }
 
 template <int KW>
-__global__ void __launch_bounds__(256, KW <= 24 ? 4 : (KW <= 32 ? 3 : 2)) sign_kernel(SignArgs a) {
+#ifndef REFSIG_K2_MINB
+#define REFSIG_K2_MINB 4
+#endif
+__global__ void __launch_bounds__(256, KW <= 24 ? REFSIG_K2_MINB : (KW <= 32 ? 3 : 2)) sign_kernel(SignArgs a) {
   constexpr int CPL = (KW + 31) / 32;  // columns per lane
   // per-warp area: the 128-entry hit queue, then the 32 x (KW+1) transpose
   constexpr int TW = 32 * (KW + 1) > 2 * static_cast<int>(kSignStep) ? 32 * (KW + 1) : 2 * kSignStep;
@@ -601,7 +609,7 @@ __device__ __forceinline__ void signc_steps(const SignArgs& a, const uint2* __re
                                             uint32_t stride, uint32_t lane, int2* qw, float (&acc)[KS], float& sq) {
   const uint32_t lt = (1u << lane) - 1u;
   const float* __restrict__ Rl = a.R + lane;  // this lane's column within each 32-column slab
-  for (uint32_t c = s0 * kSignStep; c < n; c += stride * kSignStep) {
+  for (uint32_t c = s0 * kSignStepC; c < n; c += stride * kSignStepC) {
     uint2 x[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -656,7 +664,7 @@ __device__ __forceinline__ void signc_steps(const SignArgs& a, const uint2* __re
 
 template <int KS>
 __global__ void __launch_bounds__(256) sign_col_kernel(SignArgs a) {
-  __shared__ __align__(16) int2 queue[kSignWarps][kSignStep];
+  __shared__ __align__(16) int2 queue[kSignWarps][kSignStepC];
   __shared__ float red[kSignWarps][32 * KS + 1];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int2* qw = queue[wid];
