@@ -378,8 +378,14 @@ def run_ours(args):
                                      "skips most head dots, so the kernel does fewer than these)",
                              "peak_source": f"{n_sm} SMs x 128 FFMA/clk x {clock_mhz:.0f} MHz"}
         traffic = load_traffic()
+        instep = load_traffic("ncu_traffic_instep.json")
         for k, r in roof.items():
             r["traffic"] = traffic.get(k)
+            if instep.get(k):
+                # the same kernels in step order without ncu's per-kernel cache flush
+                # (tools/instep_traffic.py): K1's df replicas stay in L2 across its
+                # class kernels, which the flushed --set full capture re-reads per kernel
+                r["traffic_in_step"] = instep[k]
         dominant = max(("mrc_tiles", "sign", "count", "pair_emit"), key=lambda k: roof[k]["share_of_step"])
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -1108,9 +1114,9 @@ def nnz_total(cp):
     return _NNZ[key]
 
 
-def load_traffic():
-    """Per-launch DRAM bytes from the committed ncu summary, if any."""
-    p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+def load_traffic(name="ncu_traffic.json"):
+    """Per-launch DRAM bytes from a committed ncu summary, if any."""
+    p = os.path.join(REPO, "profiles", name)
     if os.path.exists(p):
         with open(p) as f:
             return json.load(f)
