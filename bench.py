@@ -342,8 +342,13 @@ def run_ours(args):
     # full pipeline, candidate keys D2H into pinned memory.
     e2e_all = measure_e2e(ctx, cp, refs, tau, lo, hi, stream, dev, steps=args.steps, warmup=2)
     e2e_pipe = measure_e2e_pipelined(cp, refs, tau, lo, hi, dev, steps=max(args.steps, 5)) if world == 1 else None
-    e2e_fresh = (measure_e2e_stream(ctx, cp, refs, tau, stream, dev, steps=max(args.steps, 8))
-                 if world == 1 and N <= 65536 else None)
+    e2e_fresh = None
+    if world == 1 and N <= 65536:
+        # three runs of >= 20 fresh batches, the median run reported (host wall clock
+        # varies by ~20% between runs on a shared host), all three listed
+        runs = [measure_e2e_stream(ctx, cp, refs, tau, stream, dev, steps=max(args.steps, 20)) for _ in range(3)]
+        runs.sort(key=lambda r: r["_ms"])
+        e2e_fresh = dict(runs[1], runs_ms=[r["_ms"] for r in runs])
     modes = sorted(e2e_all)
     if dist:
         for m, v in zip(modes, allreduce(dist, [e2e_all[m]["_ms"] for m in modes], dev, "max")):
@@ -409,7 +414,8 @@ def run_ours(args):
                                  "batches" if e2e_fresh else
                                  "load_corpus(pinned host tokens) + mrc_step (one CUDA-graph replay) + step_result + "
                                  "get_pairs_csr into pinned host memory; host wall clock, synchronised"),
-                        **({"batches": e2e_fresh["batches"], "distinct_layouts": e2e_fresh["distinct_layouts"]}
+                        **({"batches": e2e_fresh["batches"], "distinct_layouts": e2e_fresh["distinct_layouts"],
+                            "runs_ms": e2e_fresh["runs_ms"], "reported": "median of the three runs"}
                            if e2e_fresh else {}),
                         "same_layout_graph_variant": {
                             "value": P / (e2e_all[main_mode]["_ms"] / 1e3), "ms_per_step": e2e_all[main_mode]["_ms"],
