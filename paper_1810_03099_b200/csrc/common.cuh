@@ -31,6 +31,18 @@ __device__ __forceinline__ TermInfo ld_na(const TermInfo* p) {
   return v;
 }
 
+// L1 eviction-priority variants (K2 cache-policy A/B, REFSIG_K2_HINT 3/4).
+__device__ __forceinline__ uint2 ld_ef(const uint2* p) {
+  uint2 v;
+  asm("ld.global.nc.L1::evict_first.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ TermInfo ld_el(const TermInfo* p) {
+  TermInfo v;
+  asm("ld.global.nc.L1::evict_last.v2.b32 {%0, %1}, [%2];" : "=f"(v.idf), "=r"(v.ref_row) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

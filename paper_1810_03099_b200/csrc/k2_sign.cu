@@ -172,19 +172,24 @@ __global__ void __launch_bounds__(256) ref_build_kernel(RefArgs r, TermInfo* __r
 // ones a warp. Every sum has a fixed order: signatures do not depend on
 // scheduling.
 // K2_HINT (A/B): 0 plain __ldg / gathers, 1 count entries L1::no_allocate,
-// 2 entries and TermInfo gathers L1::no_allocate.
+// 2 entries and TermInfo gathers L1::no_allocate, 3 entries L1::evict_first
+// and TermInfo gathers L1::evict_last.
 #ifndef REFSIG_K2_HINT
 #define REFSIG_K2_HINT 0
 #endif
 __device__ __forceinline__ uint2 sign_ent(const uint2* p) {
-#if REFSIG_K2_HINT >= 1
+#if REFSIG_K2_HINT >= 3
+  return ld_ef(p);
+#elif REFSIG_K2_HINT >= 1
   return ld_na(p);
 #else
   return __ldg(p);
 #endif
 }
 __device__ __forceinline__ TermInfo sign_info(const TermInfo* p) {
-#if REFSIG_K2_HINT >= 2
+#if REFSIG_K2_HINT >= 3
+  return ld_el(p);
+#elif REFSIG_K2_HINT >= 2
   return ld_na(p);
 #else
   return *p;
