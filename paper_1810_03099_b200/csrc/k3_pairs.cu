@@ -86,7 +86,6 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
@@ -150,7 +149,7 @@ __global__ void __launch_bounds__(256, 2) mrc_bitmap_kernel2(MrcArgs a) {
   const uint32_t panel = kcm * kTile;
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
-  const uint32_t lane = tid & 31, wid = tid >> 5;
+  const uint32_t lane = tid & 31;
   const uint32_t t_begin = static_cast<uint32_t>(a.n_tiles * blockIdx.x / gridDim.x);
   const uint32_t t_end = static_cast<uint32_t>(a.n_tiles * (blockIdx.x + 1) / gridDim.x);
   if (t_begin >= t_end) return;
