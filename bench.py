@@ -384,6 +384,17 @@ def run_ours(args):
                              "peak_source": f"{n_sm} SMs x 128 FFMA/clk x {clock_mhz:.0f} MHz"}
         traffic = load_traffic()
         instep = load_traffic("ncu_traffic_instep.json")
+        inst = load_traffic("ncu_inst.json")
+        for k in ("count", "sign"):
+            if inst.get(k) and roof[k].get("ms_per_launch"):
+                # instruction-issue roofline beside the HBM one: warp instructions per step
+                # (ncu smsp__inst_executed.sum of the phase's kernels) over the phase's device
+                # time, against 4 issue slots per SM per clock
+                ach = inst[k] / (roof[k]["ms_per_launch"] * 1e-3) / 1e9
+                pk = n_sm * 4 * clock_mhz * 1e6 / 1e9
+                roof[k]["issue"] = {"achieved": ach, "peak": pk, "unit": "G warp-inst/s", "frac": ach / pk,
+                                    "warp_inst_per_launch": inst[k],
+                                    "peak_source": f"{n_sm} SMs x 4 issue/clk x {clock_mhz:.0f} MHz"}
         for k, r in roof.items():
             r["traffic"] = traffic.get(k)
             if instep.get(k):

@@ -110,6 +110,7 @@ def full(path, tag, title=None, append=False, write_traffic=True):
               "tools/prof_all.py (see each section). DRAM bytes are cold-cache (ncu flushes caches between "
               "replays).", ""] + ([f"## {title}", ""] if title else []))
     per_kernel = collections.defaultdict(list)  # kernel name -> [bytes per launch]
+    per_inst = collections.defaultdict(list)  # kernel name -> [warp instructions per launch]
     for r in rows[2:]:
         k = short(r[idx["Kernel Name"]])
         lines.append(f"### `{k}`")
@@ -124,6 +125,8 @@ def full(path, tag, title=None, append=False, write_traffic=True):
         rd = to_bytes(r[idx["dram__bytes_read.sum"]], units[idx["dram__bytes_read.sum"]])
         wr = to_bytes(r[idx["dram__bytes_write.sum"]], units[idx["dram__bytes_write.sum"]])
         per_kernel[k].append(rd + wr)
+        if "smsp__inst_executed.sum" in idx:
+            per_inst[k].append(float(r[idx["smsp__inst_executed.sum"]].replace(",", "")))
     # per step: each distinct kernel of a group once (mean over its captured launches)
     traffic = {}
     for k, v in per_kernel.items():
@@ -133,6 +136,12 @@ def full(path, tag, title=None, append=False, write_traffic=True):
     open(os.path.join(PROF, f"ncu_full_{tag}.md"), "a" if append else "w").write("\n".join(lines) + "\n")
     if write_traffic:
         json.dump({k: v for k, v in traffic.items()}, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
+        inst = {}
+        for k, v in per_inst.items():
+            for key, frags in ROOF_KERNELS.items():
+                if any(f in k for f in frags) and not (key == "simhash" and "text_" in k):
+                    inst[key] = inst.get(key, 0.0) + sum(v) / len(v)
+        json.dump(inst, open(os.path.join(PROF, "ncu_inst.json"), "w"), indent=1)
 
 
 def main():
