@@ -463,14 +463,14 @@ void enqueue_emit(refsig_gpu_ctx* c, const PairGrid& g) {
     ck(cudaMemsetAsync(c->emit_ctr.p, 0, 2 * sizeof(uint32_t), c->stream), "memset");
   {
     Phase ph(c, REFSIG_PHASE_PAIR_EMIT);
+    // the total also goes straight to h_pin[0] (mapped) from the scan: no readback node after the
+    // emission (the host reads it only after synchronising the stream, i.e. after the emission too)
     launch_exclusive_scan_u32_to_u64(c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(), n, c->scan_tmp.p,
-                                     c->stream);
+                                     c->stream, reinterpret_cast<uint64_t*>(c->d_pin));
     launch_emit_pairs(c->bitmap.as<uint32_t>(), g, c->rowcnt.as<uint32_t>(), c->rowstart.as<uint64_t>(),
                       c->cand.as<uint32_t>(), c->cand.cap / sizeof(uint32_t), c->emit_ctr.as<uint32_t>(), c->stream);
     launched("emit");
   }
-  launch_words_to_host(reinterpret_cast<const uint32_t*>(c->rowstart.as<uint64_t>() + n), 2, c->d_pin,
-                       c->stream);  // -> h_pin[0]
   c->emit_pending = true;
   c->have_pairs = false;
   c->keys_valid = false;

@@ -76,7 +76,9 @@ void launch_inv_norm(const uint2* ent, const uint64_t* doc_off, const uint32_t* 
 // ---- scans ----------------------------------------------------------------
 // out[0..n] = exclusive prefix of in[0..n) (out[n] = total). tmp >= scan_tmp_bytes(n).
 size_t scan_tmp_bytes(uint64_t n);
-void launch_exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp, cudaStream_t s);
+// total_out (optional, e.g. mapped pinned memory): also receives out[n].
+void launch_exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp, cudaStream_t s,
+                                      uint64_t* total_out = nullptr);
 
 // ---- A5 reference table ----------------------------------------------------
 // K reference vectors. Docs mode (docs != NULL): vector k is corpus doc

@@ -74,7 +74,8 @@ __global__ void __launch_bounds__(kScanThreads) scan_partials_kernel(uint64_t* p
 
 __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t* __restrict__ in, uint64_t n,
                                                                   const uint64_t* __restrict__ partial,
-                                                                  uint64_t nb, uint64_t* __restrict__ out) {
+                                                                  uint64_t nb, uint64_t* __restrict__ out,
+                                                                  uint64_t* total_out) {
   __shared__ uint64_t sh[33];
   const uint64_t base = blockIdx.x * kScanBlock + threadIdx.x * kScanIpt;
   uint32_t v[kScanIpt];
@@ -91,7 +92,10 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t
     if (base + q < n) out[base + q] = off;
     off += v[q];
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = partial[nb];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out[n] = partial[nb];
+    if (total_out) *total_out = partial[nb];
+  }
 }
 
 // n <= kSmallScan: one 256-thread CTA per tile of 1024 values (thread t owns
@@ -112,7 +116,7 @@ __device__ __forceinline__ uint4 load4(const uint32_t* __restrict__ in, uint32_t
 }
 
 __global__ void __launch_bounds__(kSmallThreads) scan_small_kernel(const uint32_t* __restrict__ in, uint64_t n,
-                                                                   uint64_t* __restrict__ out) {
+                                                                   uint64_t* __restrict__ out, uint64_t* total_out) {
   pdl_wait();
   __shared__ uint64_t sh[33];
   const uint32_t nn = static_cast<uint32_t>(n);
@@ -145,22 +149,27 @@ __global__ void __launch_bounds__(kSmallThreads) scan_small_kernel(const uint32_
     if (i + 1 < nn) out[i + 1] = o1;
     if (i + 2 < nn) out[i + 2] = o2;
   }
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = pre_tot + tot;
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    out[n] = pre_tot + tot;
+    if (total_out) *total_out = pre_tot + tot;  // e.g. mapped pinned memory: the host reads it after a sync
+  }
 }
 
 }  // namespace
 
 size_t scan_tmp_bytes(uint64_t n) { return sizeof(uint64_t) * (ceil_div(n, kScanBlock) + 2); }
 
-void launch_exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp, cudaStream_t s) {
+void launch_exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp, cudaStream_t s,
+                                      uint64_t* total_out) {
   uint64_t nb = ceil_div(n, kScanBlock);
   if (nb == 0) {
     cudaMemsetAsync(out, 0, sizeof(uint64_t), s);
+    if (total_out) launch_words_to_host(reinterpret_cast<const uint32_t*>(out), 2, reinterpret_cast<uint32_t*>(total_out), s);
     return;
   }
   if (n <= kSmallScan) {
     launch_pdl(scan_small_kernel, dim3(static_cast<unsigned>(ceil_div(n, kSmallTile))), dim3(kSmallThreads), 0, s, in,
-               n, out);
+               n, out, total_out);
     note_launch();
     return;
   }
@@ -169,7 +178,7 @@ void launch_exclusive_scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_
   note_launch();
   scan_partials_kernel<<<1, kScanThreads, 0, s>>>(partial, nb);
   note_launch();
-  scan_apply_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, n, partial, nb, out);
+  scan_apply_kernel<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, n, partial, nb, out, total_out);
   note_launch();
 }
 
