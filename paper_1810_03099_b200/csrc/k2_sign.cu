@@ -206,8 +206,9 @@ constexpr uint32_t kSignStepC = 128;                 // K > 32 (sign_col_kernel)
 // Hit walk by column groups (REFSIG_K2_CG, default): CG_L = KW/4 lanes per
 // hit, one float4 of its R row each, CG_H = 32/CG_L hits per pass. A warp load
 // then touches CG_H rows (~1.6 L1 wavefronts per 80-byte row) instead of 32
-// (one wavefront per lane: 5 per hit at KW = 20) — K2 is bound by L1
-// wavefronts (TermInfo gathers + R rows), not by bytes. Lane (g, j) keeps
+// (one wavefront per lane: 5 per hit at KW = 20): configs[1] sign 40.9 ->
+// 35.3 us. (The rest of K2 there is about half per-document latency, half
+// TermInfo gathers + R rows; K2.) Lane (g, j) keeps
 // the 4 column sums of group j over the hits g, g + CG_H, ... of the
 // document; sign_cg_columns adds them over g in a fixed order.
 #ifndef REFSIG_K2_CG
